@@ -1,0 +1,364 @@
+#!/usr/bin/env python
+"""Benchmark of the fused stencil-chain path (BASELINE.json metric:
+fused-chain cell-updates/s, % of HBM roofline, vs host CPU).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl loomfuse|reference]
+                    [--config heat3d|biharm|box|hydro|hydro_large]
+
+A bench "step" is one full run of the configured chain over its grid (e.g.
+configs[1]: 50 time steps of the 3D heat chain on 512^3).  N=1 is the default;
+for N>1 launch under torchrun (one rank per GPU, NCCL): the outer dimension is
+split into slabs and faces are exchanged every time step (strong scaling, the
+grid is fixed).  Rank 0 prints one JSON line.
+
+--impl reference times the reference's CPU path -- the HFAV-style fused CPU
+schedule restated in oracle/ (the reference's own executor is absent from the
+snapshot) -- on all host threads, on a bounded sample.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+FALLBACK_HBM_GBS = 6650.0
+
+
+# --------------------------------------------------------------------- workloads
+def _heat3d_inputs(sizes, seed=0):
+    from paper_1710_08774_b200 import inputs
+    return [inputs.heat3d_input(*sizes, seed=seed)]
+
+
+def _biharm_inputs(sizes, seed=0):
+    from paper_1710_08774_b200 import inputs
+    return [inputs.biharm_input(*sizes, seed=seed)]
+
+
+def _box_inputs(sizes, seed=0):
+    from paper_1710_08774_b200 import inputs
+    return [inputs.box_input(*sizes, seed=seed)]
+
+
+def _hydro_inputs(sizes, seed=0):
+    from paper_1710_08774_b200 import inputs
+    st, dtdx = inputs.hydro_input(*sizes, seed=seed)
+    return st + [np.array([dtdx], dtype=np.float64)]
+
+
+WORKLOADS = {
+    # BASELINE.json configs[1] -- the default bench line
+    "heat3d": dict(config_index=1, spec="heat3d", sizes=(512, 512, 512), chain_steps=50,
+                   gen=_heat3d_inputs, dtype="f64", halo=(1, 1, True)),
+    "biharm": dict(config_index=0, spec="biharmonic2d", sizes=(4096, 4096), chain_steps=100,
+                   gen=_biharm_inputs, dtype="f64", halo=(2, 2, False)),
+    "box": dict(config_index=3, spec="box2x", sizes=(16384, 16384), chain_steps=1,
+                gen=_box_inputs, dtype="f32", halo=None),
+    "hydro": dict(config_index=2, spec="hydro2d", sizes=(4096, 4096), chain_steps=20,
+                  gen=_hydro_inputs, dtype="f64", halo=(2, 2, False)),
+    "hydro_large": dict(config_index=4, spec="hydro2d", sizes=(32768, 32768), chain_steps=10,
+                        gen=_hydro_inputs, dtype="f64", halo=(2, 2, False)),
+}
+
+
+def measured_peak():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
+
+
+def ncu_traffic(workload):
+    """DRAM bytes per launch from the committed ncu summary, if any."""
+    p = ROOT / "profiles" / "traffic.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        v = d.get(workload)
+        if isinstance(v, dict):
+            return v.get("dram_bytes_per_launch")
+    return None
+
+
+# --------------------------------------------------------------------- clocks
+class ClockSampler:
+    """Samples SM clock + throttle reasons through NVML during the timed region."""
+
+    def __init__(self, index=0, period=0.02):
+        self.samples, self.reasons = [], set()
+        self.period, self.index = period, index
+        self._stop = threading.Event()
+        self.max_mhz = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nv = None
+
+    def _run(self):
+        nv = self.nv
+        names = {
+            "hw_slowdown": getattr(nv, "nvmlClocksThrottleReasonHwSlowdown", 0x8),
+            "hw_thermal_slowdown": getattr(nv, "nvmlClocksThrottleReasonHwThermalSlowdown", 0x40),
+            "sw_thermal_slowdown": getattr(nv, "nvmlClocksThrottleReasonSwThermalSlowdown", 0x20),
+            "sw_power_cap": getattr(nv, "nvmlClocksThrottleReasonSwPowerCap", 0x4),
+            "hw_power_brake_slowdown": getattr(nv, "nvmlClocksThrottleReasonHwPowerBrakeSlowdown", 0x80),
+        }
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                r = nv.nvmlDeviceGetCurrentClocksThrottleReasons(self.h)
+                for k, bit in names.items():
+                    if r & bit:
+                        self.reasons.add(k)
+            except Exception:
+                pass
+            time.sleep(self.period)
+
+    def __enter__(self):
+        if self.nv is not None:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.nv is not None:
+            self._stop.set()
+            self.t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                    "samples": 0}
+        return {"sm_mhz": float(np.median(self.samples)), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+# --------------------------------------------------------------------- CPU legs
+def cpu_runner(name, w):
+    """The HFAV-style fused CPU schedule (oracle/) on one bounded unit of the
+    workload with all host threads: returns (run, cell-updates per run, text)."""
+    import oracle
+    threads = oracle.max_threads()
+    sizes = w["sizes"]
+    if name == "heat3d":
+        u = w["gen"](sizes)[0]
+        o = np.empty_like(u)
+        return (lambda: oracle.heat3d_step(u, o, threads=threads)), int(np.prod(sizes)), threads, \
+            f"1 time step of {'x'.join(map(str, sizes))}"
+    if name == "biharm":
+        u = w["gen"](sizes)[0]
+        o = np.zeros_like(u)
+        return (lambda: oracle.biharm_step(u, o, threads=threads)), int(np.prod(sizes)), threads, \
+            f"1 iteration of {'x'.join(map(str, sizes))}"
+    if name == "box":
+        img = w["gen"](sizes)[0]
+        return (lambda: oracle.box(img, fused=True, threads=threads)), int(np.prod(sizes)), threads, \
+            f"1 pass of {'x'.join(map(str, sizes))}"
+    nj = max(64, min(sizes[0], 256))  # hydro: a full-width row band, 1 step
+    st = w["gen"]((nj, sizes[1]))
+    return (lambda: oracle.hydro(st[:4], float(st[4][0]), 1, fused=True, threads=threads)), nj * sizes[1], \
+        threads, f"1 step of a {nj}x{sizes[1]} row band"
+
+
+def cpu_sample(name, w, budget_s=10.0):
+    """Repeat the CPU unit for ~budget_s; returns (cell-updates/s, threads, text)."""
+    run, cells, threads, unit = cpu_runner(name, w)
+    run()  # warm
+    t0 = time.perf_counter()
+    reps = 0
+    while True:
+        run()
+        reps += 1
+        if time.perf_counter() - t0 >= budget_s:
+            break
+    dt = time.perf_counter() - t0
+    return cells * reps / dt, threads, f"{reps} x {unit} (fused CPU schedule, {threads} threads, {dt:.1f} s)"
+
+
+def cpu_model():
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+# --------------------------------------------------------------------- main
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="loomfuse", choices=["loomfuse", "reference"])
+    ap.add_argument("--config", default="heat3d", choices=sorted(WORKLOADS))
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--no-e2e", action="store_true", help="skip the end-to-end leg")
+    ap.add_argument("--cpu-budget", type=float, default=10.0)
+    args = ap.parse_args()
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    w = WORKLOADS[args.config]
+    cells = int(np.prod(w["sizes"]))
+    metric = "fused-chain cell-updates/s"
+    workload = f"BASELINE configs[{w['config_index']}] {w['spec']} " + "x".join(map(str, w["sizes"])) + \
+        f", {w['chain_steps']} steps"
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        run, unit_cells, threads, unit = cpu_runner(args.config, w)
+        for _ in range(args.warmup):
+            run()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            run()
+        dt = (time.perf_counter() - t0) / args.steps
+        value = unit_cells / dt
+        sample = f"{args.steps} x {unit} (fused CPU schedule, {threads} threads)"
+        line = {
+            "impl": "reference", "metric": metric, "value": value, "unit": "cell-updates/s",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": dt * 1e3,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": w["dtype"], "data": "synthetic (seeded splitmix64, BASELINE.json shapes)",
+            "config": {"workload": workload, "cpu": cpu_model(), "threads": threads},
+            "cpu_baseline": {"value": value, "unit": "cell-updates/s", "cores": threads, "kind": "port",
+                             "sample": sample},
+            "e2e": {"value": value, "unit": "cell-updates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        }
+        print(json.dumps(line), flush=True)
+        return
+
+    import torch
+    import paper_1710_08774_b200 as lf
+    from paper_1710_08774_b200 import slabs
+
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    else:
+        torch.cuda.set_device(0)
+    dev = torch.device("cuda", torch.cuda.current_device())
+
+    plan = lf.Plan.with_ranges(w["spec"], w["sizes"])
+    if not plan.executor:
+        raise SystemExit(f"no fused executor for {w['spec']}: run lf_run to see why")
+    host = w["gen"](w["sizes"])
+    nax = len(plan.axioms)
+    stream = torch.cuda.current_stream()
+
+    # ---------------- device-resident timing ----------------
+    if world == 1:
+        d_ax = [torch.from_numpy(h).to(dev) for h in host[:nax]]
+        d_goal = [torch.empty(t.extent, dtype=getattr(torch, str(t.dtype)), device=dev) for t in plan.goals]
+        bufs = d_ax + d_goal
+
+        def one_step():
+            plan.run(bufs, steps=w["chain_steps"], stream=stream)
+        launches = plan.launches_per_step * w["chain_steps"]
+    else:
+        lo_h, hi_h, periodic = w["halo"]
+        n0 = w["sizes"][0]
+        lo, hi = slabs.slab_range(n0, rank, world)
+        halo = slabs.Halo(lo_h, hi_h, periodic)
+        d_ax = [torch.from_numpy(np.ascontiguousarray(h[lo:hi + lo_h + hi_h])).to(dev) for h in host[:nax]]
+        d_sc = [torch.empty_like(a) for a in d_ax]
+        slab_plan = plan
+
+        def step(src, dst):
+            slab_plan.run_slab(list(src) + list(dst), lo, hi, n0, stream=stream)
+
+        def one_step():
+            slabs.run_slabs(step, d_ax, d_sc, w["chain_steps"], halo, rank, world)
+        launches = plan.launches_per_step * w["chain_steps"]
+
+    def barrier():
+        if world > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        one_step()
+    barrier()
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(torch.cuda.current_device()) as clk:
+        barrier()
+        start.record(stream)
+        for _ in range(args.steps):
+            one_step()
+        end.record(stream)
+        barrier()
+    ms = start.elapsed_time(end) / args.steps
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms = float(t.item())
+    value = cells * w["chain_steps"] / (ms / 1e3)
+
+    # roofline of the dominant (only) kernel: algorithmic bytes per launch /
+    # average launch duration over the timed region
+    peak, peak_src = measured_peak()
+    bpc = plan.compulsory_bytes_per_cell
+    cells_per_launch = cells / max(1, plan.launches_per_step) / (world if world > 1 else 1)
+    launch_s = (ms / 1e3) / (launches if launches else 1)
+    achieved = bpc * cells_per_launch / launch_s / 1e9
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                "traffic": ncu_traffic(args.config), "peak_source": peak_src,
+                "algorithmic_bytes_per_cell": bpc}
+
+    line = {
+        "metric": metric, "value": value, "unit": "cell-updates/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": w["dtype"], "data": "synthetic (seeded splitmix64, BASELINE.json shapes)",
+        "config": {"workload": workload, "executor": plan.executor, "l2": "inputs larger than L2 (126 MB)",
+                   "parallelism": f"slab{world}" if world > 1 else "single-gpu"},
+        "roofline": roofline, "gpu_launches": launches * args.steps, "clocks": clk.summary(),
+    }
+
+    # ---------------- end-to-end through the host-buffer ABI call ----------------
+    if not args.no_e2e and world == 1:
+        pinned = [torch.from_numpy(h).pin_memory() for h in host[:nax]]
+        outs = [torch.empty(t.extent, dtype=getattr(torch, str(t.dtype))).pin_memory() for t in plan.goals]
+        hb = [p.numpy() for p in pinned] + [o.numpy() for o in outs]
+        for _ in range(max(1, args.warmup)):
+            plan.run_host(hb, steps=w["chain_steps"])
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            plan.run_host(hb, steps=w["chain_steps"])
+        e2e_s = (time.perf_counter() - t0) / args.steps
+        line["e2e"] = {"value": cells * w["chain_steps"] / e2e_s, "unit": "cell-updates/s",
+                       "h2d_bytes_per_step": int(sum(t.bytes for t in plan.axioms)),
+                       "d2h_bytes_per_step": int(sum(t.bytes for t in plan.goals)),
+                       "ms_per_step": e2e_s * 1e3, "api": "lf_run_host"}
+    # ---------------- CPU baseline (rank 0, N=1 only) ----------------
+    if rank == 0 and world == 1 and not args.no_cpu:
+        rate, threads, sample = cpu_sample(args.config, w, budget_s=args.cpu_budget)
+        line["cpu_baseline"] = {"value": rate, "unit": "cell-updates/s", "cores": threads, "kind": "port",
+                                "sample": sample, "cpu": cpu_model()}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,146 @@
+/*
+ * loomfuse-b200 -- C ABI of the B200-native fused stencil-chain executor.
+ *
+ * Drop-in boundary for the reference's fused path.  In the reference the user
+ * writes a rule file (`.lf`: kernels / globals / config, R/SPEC.md:88,
+ * R/PAPER.md:358-375) and the code generator emits "one function per goal
+ * set, taking terminal buffers as parameters" (R/SPEC.md:500), with the
+ * prototype in `<name>.h` (R/SPEC.md:507) and buffers ordered axioms then
+ * goals.  That emitted function is the hot path this library replaces:
+ *
+ *   reference (emitted, host)            loomfuse-b200
+ *   ----------------------------------   ---------------------------------------
+ *   parse_spec + analysis pipeline        lf_plan_create        (rulespec.cpp:550,
+ *     (rulespec/inference/nests/fusion/                          inference.cpp:404,
+ *      shifts/storage)                                           storage.cpp:526)
+ *   buffer_extents / storage report       lf_plan_terminal, lf_plan_report
+ *                                                               (storage.cpp:403-427,
+ *                                                                R/SPEC.md:440)
+ *   void <name>(axioms..., goals...)      lf_run_host  (host buffers, same order)
+ *                                         lf_run       (device buffers + stream)
+ *   outer-level parallelism (external,    lf_run_slab  (one row/plane slab of a
+ *     R/PAPER.md:499)                                   domain split across GPUs)
+ *   DiagList / internal_error /           int status codes below + lf_last_error()
+ *     CLI exit codes (diag.hpp:37-70,     (thread-local message, `file:line:col`
+ *     R/SPEC.md:596)                       prefixes as SourceLoc::str)
+ *
+ * No exceptions cross this boundary; every entry point returns a status.
+ * Plans are immutable after creation and may be shared between threads;
+ * execution is stream-ordered.
+ */
+#ifndef LOOMFUSE_B200_H
+#define LOOMFUSE_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* status codes (R/SPEC.md:596: 0 ok / 1 user error / 2 verify mismatch) */
+#define LF_OK 0
+#define LF_ERR_SPEC 1        /* rule-file or argument error (diagnostics in lf_last_error) */
+#define LF_ERR_MISMATCH 2    /* reserved: verification mismatch */
+#define LF_ERR_INTERNAL 3    /* contract violation inside the planner/executor */
+#define LF_ERR_CUDA 4        /* CUDA runtime / driver failure */
+#define LF_ERR_UNSUPPORTED 5 /* valid chain, but no fused sm_100a executor for it */
+
+#define LF_MAX_DIMS 4
+
+typedef struct lf_plan lf_plan;
+
+/* One terminal buffer (axiom or goal) as the reference's storage analysis
+ * sizes it: extent = trips + offset spread, base = logical coordinate of
+ * index 0 (storage.cpp:403-427).  Dims are outermost first; buffers are dense
+ * and row-major.  For iterated chains (config `iterate:`) the goal buffer
+ * takes its paired axiom's layout so the two can ping-pong. */
+typedef struct {
+  char name[64];
+  char type[32];      /* element type text from the declaration, e.g. "double" */
+  int32_t is_goal;
+  int32_t elem_bytes;
+  int32_t ndim;
+  int32_t loop_dim[LF_MAX_DIMS]; /* index into loop-order; -1 for none */
+  int64_t extent[LF_MAX_DIMS];
+  int64_t base[LF_MAX_DIMS];
+  int64_t bytes;      /* elem_bytes * prod(extent) */
+} lf_terminal;
+
+/* A slab of the outermost loop dimension owned by one rank (lf_run_slab):
+ * rows [lo, hi) of the global range [0, global).  Terminal buffers of a slab
+ * are sized for that slab (the planner's extents with `hi-lo` trips along the
+ * outermost dim).  Ghost rows on an internal face are filled by the caller's
+ * halo exchange before each step; ghost rows on a global face are refilled by
+ * the executor from the chain's boundary mode. */
+typedef struct {
+  int64_t lo;
+  int64_t hi;
+  int64_t global;
+} lf_slab;
+
+/* Parse, validate, infer and analyse a rule file.  `filename` is only used in
+ * diagnostics.  On LF_ERR_SPEC the diagnostics are in lf_last_error(). */
+int lf_plan_create(const char* spec_text, size_t len, const char* filename, lf_plan** out);
+
+/* Canonical text of a rule file (print_spec, rulespec.cpp:668-705): parsing
+ * the output again yields a structurally equal rule set.  Same buffer
+ * convention as lf_plan_report. */
+int lf_spec_print(const char* spec_text, size_t len, const char* filename, char* buf, size_t cap,
+                  size_t* needed);
+
+/* Release a plan and the device scratch it owns. */
+void lf_plan_destroy(lf_plan* plan);
+
+/* Number of terminals (axioms in declaration order, then goals). */
+int lf_plan_num_terminals(const lf_plan* plan);
+
+/* Describe terminal `idx`. */
+int lf_plan_terminal(const lf_plan* plan, int idx, lf_terminal* out);
+
+/* Analysis report as JSON (groups + shifts, variables + storage schemes and
+ * windows, terminals, nests/splits, footprint polynomial, chain signature).
+ * Writes at most `cap` bytes including the NUL; returns the full length via
+ * *needed when non-NULL. */
+int lf_plan_report(const lf_plan* plan, char* buf, size_t cap, size_t* needed);
+
+/* Name of the fused executor the plan dispatches to, or "" if none. */
+const char* lf_plan_executor(const lf_plan* plan);
+
+/* Run the chain `steps` times on DEVICE buffers (axioms then goals, sized per
+ * lf_plan_terminal), stream-ordered on `cuda_stream` (a cudaStream_t, NULL =
+ * legacy default stream).  steps == 1 is exactly the reference's emitted
+ * function.  steps > 1 requires `iterate:` pairs: the goal of step s is the
+ * axiom of step s+1, ghost cells are refilled from `boundary:` after every
+ * step, and the final state is left in the goal buffers.  Intermediate states
+ * ping-pong between the goal buffer and a plan-owned scratch buffer, so the
+ * axiom buffers are never written.  One multi-step run per plan at a time. */
+int lf_run(const lf_plan* plan, void* const* terminals, int nterm, int steps, void* cuda_stream);
+
+/* Same on HOST buffers: copies axioms host->device, runs, copies goals
+ * device->host, synchronises.  This is the drop-in for the emitted host
+ * function <name>(terminals...) of R/SPEC.md:500.  Device buffers are owned
+ * and cached by the plan.  Pinned host memory gives full copy bandwidth. */
+int lf_run_host(const lf_plan* plan, void* const* terminals, int nterm, int steps);
+
+/* One step on a slab of the outermost loop dimension (multi-GPU row/plane
+ * slabs).  Buffers are device buffers sized for the slab. */
+int lf_run_slab(const lf_plan* plan, void* const* terminals, int nterm, const lf_slab* slab,
+                void* cuda_stream);
+
+/* Number of fused-executor kernel launches one step issues (for bench
+ * accounting), and the algorithmic (compulsory) HBM bytes per cell-update. */
+int lf_plan_launches_per_step(const lf_plan* plan);
+double lf_plan_compulsory_bytes_per_cell(const lf_plan* plan);
+
+/* Thread-local message of the last failing call on this thread ("" if none). */
+const char* lf_last_error(void);
+
+/* Library version string. */
+const char* lf_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* LOOMFUSE_B200_H */

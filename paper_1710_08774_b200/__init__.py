@@ -1,0 +1,294 @@
+"""loomfuse-b200: B200-native fused stencil-chain executor.
+
+Python mirror of the C ABI in ``include/loomfuse_b200.h``.  The interface is
+the reference's: a `.lf` rule file (kernels / globals / config, R/SPEC.md:88)
+planned once (``Plan``), then the emitted per-goal-set function
+(R/SPEC.md:500) -- here ``Plan.run`` on device buffers or ``Plan.run_host``
+on host arrays, terminals ordered axioms then goals.
+
+The compute path is the sm_100a library ``libloomfuse_b200.so`` built in-tree
+by ``paper_1710_08774_b200.build``; there is no CPU fallback -- importing the
+package without the library raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import json
+from dataclasses import dataclass
+from pathlib import Path
+from typing import Any, Sequence
+
+import numpy as np
+
+PKG_DIR = Path(__file__).resolve().parent
+LIB_PATH = PKG_DIR / "libloomfuse_b200.so"
+SPEC_DIR = PKG_DIR / "specs"
+
+LF_OK = 0
+LF_ERR_SPEC = 1
+LF_ERR_MISMATCH = 2
+LF_ERR_INTERNAL = 3
+LF_ERR_CUDA = 4
+LF_ERR_UNSUPPORTED = 5
+LF_MAX_DIMS = 4
+
+#: every symbol the header declares (checked by tests/test_abi.py)
+ABI_SYMBOLS = (
+    "lf_plan_create", "lf_plan_destroy", "lf_plan_num_terminals", "lf_plan_terminal",
+    "lf_plan_report", "lf_plan_executor", "lf_run", "lf_run_host", "lf_run_slab",
+    "lf_plan_launches_per_step", "lf_plan_compulsory_bytes_per_cell", "lf_last_error",
+    "lf_version", "lf_spec_print",
+)
+
+
+class LoomfuseError(RuntimeError):
+    """A non-zero status from the C ABI; ``code`` is the LF_* status."""
+
+    def __init__(self, code: int, message: str):
+        super().__init__(f"[{code}] {message}")
+        self.code = code
+
+
+class _Terminal(ctypes.Structure):
+    _fields_ = [
+        ("name", ctypes.c_char * 64),
+        ("type", ctypes.c_char * 32),
+        ("is_goal", ctypes.c_int32),
+        ("elem_bytes", ctypes.c_int32),
+        ("ndim", ctypes.c_int32),
+        ("loop_dim", ctypes.c_int32 * LF_MAX_DIMS),
+        ("extent", ctypes.c_int64 * LF_MAX_DIMS),
+        ("base", ctypes.c_int64 * LF_MAX_DIMS),
+        ("bytes", ctypes.c_int64),
+    ]
+
+
+class _Slab(ctypes.Structure):
+    _fields_ = [("lo", ctypes.c_int64), ("hi", ctypes.c_int64), ("global_", ctypes.c_int64)]
+
+
+_lib: ctypes.CDLL | None = None
+
+
+def lib() -> ctypes.CDLL:
+    """Load the in-tree sm_100a library (fails loudly if it was not built)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not LIB_PATH.exists():
+        raise ImportError(
+            f"{LIB_PATH} is missing: run `python -m paper_1710_08774_b200.build` "
+            "(there is no CPU fallback for the fused executor)")
+    L = ctypes.CDLL(str(LIB_PATH))
+    P = ctypes.c_void_p
+    L.lf_plan_create.argtypes = [ctypes.c_char_p, ctypes.c_size_t, ctypes.c_char_p, ctypes.POINTER(P)]
+    L.lf_spec_print.argtypes = [ctypes.c_char_p, ctypes.c_size_t, ctypes.c_char_p, ctypes.c_char_p,
+                                ctypes.c_size_t, ctypes.POINTER(ctypes.c_size_t)]
+    L.lf_plan_destroy.argtypes = [P]
+    L.lf_plan_destroy.restype = None
+    L.lf_plan_num_terminals.argtypes = [P]
+    L.lf_plan_terminal.argtypes = [P, ctypes.c_int, ctypes.POINTER(_Terminal)]
+    L.lf_plan_report.argtypes = [P, ctypes.c_char_p, ctypes.c_size_t, ctypes.POINTER(ctypes.c_size_t)]
+    L.lf_plan_executor.argtypes = [P]
+    L.lf_plan_executor.restype = ctypes.c_char_p
+    L.lf_run.argtypes = [P, ctypes.POINTER(P), ctypes.c_int, ctypes.c_int, P]
+    L.lf_run_host.argtypes = [P, ctypes.POINTER(P), ctypes.c_int, ctypes.c_int]
+    L.lf_run_slab.argtypes = [P, ctypes.POINTER(P), ctypes.c_int, ctypes.POINTER(_Slab), P]
+    L.lf_plan_launches_per_step.argtypes = [P]
+    L.lf_plan_compulsory_bytes_per_cell.argtypes = [P]
+    L.lf_plan_compulsory_bytes_per_cell.restype = ctypes.c_double
+    L.lf_last_error.restype = ctypes.c_char_p
+    L.lf_version.restype = ctypes.c_char_p
+    _lib = L
+    return L
+
+
+def _check(code: int) -> None:
+    if code != LF_OK:
+        raise LoomfuseError(code, lib().lf_last_error().decode(errors="replace"))
+
+
+_NP_DTYPES = {("double", 8): np.float64, ("float", 4): np.float32}
+
+
+@dataclass(frozen=True)
+class Terminal:
+    """One terminal buffer as sized by the reference's buffer_extents."""
+    name: str
+    type: str
+    is_goal: bool
+    elem_bytes: int
+    loop_dims: tuple[int, ...]
+    extent: tuple[int, ...]
+    base: tuple[int, ...]
+    bytes: int
+
+    @property
+    def dtype(self) -> np.dtype:
+        for (t, b), dt in _NP_DTYPES.items():
+            if t in self.type and b == self.elem_bytes:
+                return np.dtype(dt)
+        raise TypeError(f"no numpy dtype for terminal type {self.type!r}")
+
+
+def _ptr(x: Any) -> int:
+    if isinstance(x, int):
+        return x
+    if hasattr(x, "data_ptr"):
+        return int(x.data_ptr())
+    if isinstance(x, np.ndarray):
+        if not x.flags.c_contiguous:
+            raise ValueError("host arrays must be C-contiguous")
+        return int(x.ctypes.data)
+    raise TypeError(f"cannot take a buffer pointer from {type(x).__name__}")
+
+
+def spec_path(name: str) -> Path:
+    """Path of a bundled rule file (``heat3d``, ``biharmonic2d``, ...)."""
+    p = SPEC_DIR / (name if name.endswith(".lf") else name + ".lf")
+    if not p.exists():
+        raise FileNotFoundError(p)
+    return p
+
+
+class Plan:
+    """A planned rule file (lf_plan_create) -- immutable, reusable."""
+
+    def __init__(self, text: str, filename: str = "<input>"):
+        L = lib()
+        h = ctypes.c_void_p()
+        raw = text.encode()
+        _check(L.lf_plan_create(raw, len(raw), filename.encode(), ctypes.byref(h)))
+        self._h = h
+        self.filename = filename
+        self.terminals: list[Terminal] = []
+        for i in range(L.lf_plan_num_terminals(h)):
+            t = _Terminal()
+            _check(L.lf_plan_terminal(h, i, ctypes.byref(t)))
+            n = t.ndim
+            self.terminals.append(Terminal(
+                t.name.decode(), t.type.decode(), bool(t.is_goal), t.elem_bytes,
+                tuple(t.loop_dim[:n]), tuple(t.extent[:n]), tuple(t.base[:n]), t.bytes))
+
+    @classmethod
+    def from_file(cls, path: str | Path) -> "Plan":
+        p = Path(path)
+        return cls(p.read_text(), str(p))
+
+    @classmethod
+    def bundled(cls, name: str) -> "Plan":
+        return cls.from_file(spec_path(name))
+
+    @classmethod
+    def with_ranges(cls, name: str, sizes: Sequence[int]) -> "Plan":
+        """A bundled spec with its `ranges:` replaced by [0, n) per loop dim."""
+        return cls(set_ranges(spec_path(name).read_text(), sizes), str(spec_path(name)))
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value and _lib is not None:
+            _lib.lf_plan_destroy(h)
+            self._h = None
+
+    # ---- introspection ---------------------------------------------------
+    def report(self) -> dict:
+        L = lib()
+        need = ctypes.c_size_t()
+        _check(L.lf_plan_report(self._h, None, 0, ctypes.byref(need)))
+        buf = ctypes.create_string_buffer(need.value)
+        _check(L.lf_plan_report(self._h, buf, need.value, None))
+        return json.loads(buf.value.decode())
+
+    @property
+    def executor(self) -> str:
+        return lib().lf_plan_executor(self._h).decode()
+
+    @property
+    def launches_per_step(self) -> int:
+        return lib().lf_plan_launches_per_step(self._h)
+
+    @property
+    def compulsory_bytes_per_cell(self) -> float:
+        return lib().lf_plan_compulsory_bytes_per_cell(self._h)
+
+    @property
+    def axioms(self) -> list[Terminal]:
+        return [t for t in self.terminals if not t.is_goal]
+
+    @property
+    def goals(self) -> list[Terminal]:
+        return [t for t in self.terminals if t.is_goal]
+
+    # ---- execution -----------------------------------------------------------
+    def _ptrs(self, bufs: Sequence[Any]):
+        if len(bufs) != len(self.terminals):
+            raise ValueError(f"expected {len(self.terminals)} buffers (axioms then goals), got {len(bufs)}")
+        arr = (ctypes.c_void_p * len(bufs))(*[_ptr(b) for b in bufs])
+        return arr
+
+    def run(self, bufs: Sequence[Any], steps: int = 1, stream: Any = None) -> None:
+        """Device buffers (torch tensors or raw pointers), stream-ordered."""
+        s = _stream_handle(stream)
+        _check(lib().lf_run(self._h, self._ptrs(bufs), len(bufs), steps, s))
+
+    def run_host(self, arrays: Sequence[np.ndarray], steps: int = 1) -> None:
+        """Host arrays in, goals written back (the emitted function's contract)."""
+        for a, t in zip(arrays, self.terminals):
+            if isinstance(a, np.ndarray) and a.nbytes != t.bytes:
+                raise ValueError(f"{t.name}: expected {t.bytes} bytes, got {a.nbytes}")
+        _check(lib().lf_run_host(self._h, self._ptrs(arrays), len(arrays), steps))
+
+    def run_slab(self, bufs: Sequence[Any], lo: int, hi: int, global_: int, stream: Any = None) -> None:
+        slab = _Slab(lo, hi, global_)
+        _check(lib().lf_run_slab(self._h, self._ptrs(bufs), len(bufs), ctypes.byref(slab),
+                                 _stream_handle(stream)))
+
+
+def print_spec(text: str, filename: str = "<input>") -> str:
+    """Canonical text of a rule file (lf_spec_print; round-trips through parse)."""
+    L = lib()
+    raw = text.encode()
+    need = ctypes.c_size_t()
+    _check(L.lf_spec_print(raw, len(raw), filename.encode(), None, 0, ctypes.byref(need)))
+    buf = ctypes.create_string_buffer(need.value)
+    _check(L.lf_spec_print(raw, len(raw), filename.encode(), buf, need.value, None))
+    return buf.value.decode()
+
+
+def _stream_handle(stream: Any):
+    if stream is None:
+        return None
+    if isinstance(stream, int):
+        return stream
+    if hasattr(stream, "cuda_stream"):
+        return int(stream.cuda_stream)
+    raise TypeError("stream must be a torch.cuda.Stream, an int handle or None")
+
+
+def set_ranges(text: str, sizes: Sequence[int]) -> str:
+    """Rewrite the `ranges:` block of a rule file to [0, n) per loop-order dim."""
+    lines = text.splitlines()
+    out, i = [], 0
+    order = None
+    for ln in lines:
+        s = ln.strip()
+        if s.startswith("loop-order:"):
+            order = [v.strip() for v in s.split(":", 1)[1].strip().strip("[]").split(",")]
+    if order is None or len(order) != len(sizes):
+        raise ValueError("sizes must match the spec's loop-order")
+    while i < len(lines):
+        ln = lines[i]
+        out.append(ln)
+        if ln.strip() == "ranges:":
+            ind = len(ln) - len(ln.lstrip()) + 2
+            i += 1
+            while i < len(lines) and (len(lines[i]) - len(lines[i].lstrip())) >= ind and lines[i].strip():
+                i += 1
+            for v, n in zip(order, sizes):
+                out.append(" " * ind + f"{v}: [0, {int(n)}]")
+            continue
+        i += 1
+    return "\n".join(out) + "\n"
+
+
+__all__ = ["Plan", "Terminal", "LoomfuseError", "lib", "spec_path", "set_ranges", "print_spec", "ABI_SYMBOLS"]

@@ -1,0 +1,337 @@
+// extern "C" boundary of loomfuse-b200 (include/loomfuse_b200.h).
+// Maps the reference's pipeline entry (parse_spec -> analysis, rulespec.cpp:550,
+// storage.cpp:526) and its emitted per-goal-set function (R/SPEC.md:500) onto
+// plan objects and fused sm_100a executors.  No exception crosses this file.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/loomfuse_b200.h"
+#include "exec/exec.hpp"
+#include "planner/planner.hpp"
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, std::string msg) {
+  g_err = std::move(msg);
+  return code;
+}
+
+struct Signed {
+  const lfx::Executor* exec;
+  std::string signature;
+  std::string error;  // embedded spec failed to plan (build bug)
+};
+
+const std::vector<Signed>& signed_executors() {
+  static std::vector<Signed> v;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    for (const auto& e : lfx::executors()) {
+      Signed s{&e, "", ""};
+      const char* text = lfx::embedded_spec(e.spec_file);
+      lf::DiagList d;
+      auto rs = lf::parse_spec(text ? text : "", e.spec_file, d);
+      std::optional<lf::Plan> p;
+      if (rs) p = lf::make_plan(*rs, d);
+      if (p)
+        s.signature = p->signature;
+      else
+        s.error = d.str();
+      v.push_back(std::move(s));
+    }
+  });
+  return v;
+}
+
+}  // namespace
+
+struct lf_plan {
+  lf::Plan plan;
+  const lfx::Executor* exec = nullptr;
+  std::string unsupported;  // why no executor applies
+  std::string report;
+  std::mutex mu;            // guards the device caches below
+  std::vector<void*> dev;   // lf_run_host device terminals
+  std::vector<void*> scratch;  // per goal; iterated goals only
+  cudaStream_t stream = nullptr;
+  ~lf_plan() {
+    for (void* p : dev)
+      if (p) cudaFree(p);
+    for (void* p : scratch)
+      if (p) cudaFree(p);
+    if (stream) cudaStreamDestroy(stream);
+  }
+};
+
+namespace {
+
+int64_t terminal_bytes(const lf::Terminal& t) {
+  int64_t n = t.elem_bytes;
+  for (long e : t.extent) n *= e;
+  return n;
+}
+
+int ensure_scratch(lf_plan* p, std::string& err) {
+  const auto& T = p->plan.terminals;
+  if (p->scratch.size() == T.size()) return LF_OK;
+  p->scratch.assign(T.size(), nullptr);
+  for (size_t i = 0; i < T.size(); ++i) {
+    if (!T[i].is_goal) continue;
+    bool iterated = false;
+    for (const auto& [g, a] : p->plan.rs.iterate) iterated |= g == T[i].name;
+    if (!iterated) continue;
+    cudaError_t e = cudaMalloc(&p->scratch[i], terminal_bytes(T[i]));
+    if (e != cudaSuccess) return lfx::cuda_status(e, "cudaMalloc(scratch)", err);
+  }
+  return LF_OK;
+}
+
+// scratch pointers ordered like the executors expect: one per iterated goal,
+// in goal order
+std::vector<void*> scratch_list(lf_plan* p) {
+  std::vector<void*> s;
+  for (size_t i = 0; i < p->plan.terminals.size(); ++i)
+    if (p->scratch[i]) s.push_back(p->scratch[i]);
+  return s;
+}
+
+int check_run_args(const lf_plan* plan, void* const* terms, int nterm, int steps) {
+  if (!plan) return fail(LF_ERR_SPEC, "plan is NULL");
+  if (!plan->exec)
+    return fail(LF_ERR_UNSUPPORTED, "no fused sm_100a executor for chain '" + plan->plan.rs.name +
+                                        "' (signature " + plan->plan.signature + "): " + plan->unsupported);
+  if (nterm != static_cast<int>(plan->plan.terminals.size()))
+    return fail(LF_ERR_SPEC, "expected " + std::to_string(plan->plan.terminals.size()) + " terminal buffers, got " +
+                                 std::to_string(nterm));
+  if (!terms) return fail(LF_ERR_SPEC, "terminal array is NULL");
+  for (int i = 0; i < nterm; ++i)
+    if (!terms[i]) return fail(LF_ERR_SPEC, "terminal " + plan->plan.terminals[i].name + " is NULL");
+  if (steps < 1) return fail(LF_ERR_SPEC, "steps must be >= 1");
+  if (steps > 1 && plan->plan.rs.iterate.empty())
+    return fail(LF_ERR_SPEC, "steps > 1 needs `iterate:` pairs in the rule file's config");
+  return LF_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* lf_last_error(void) { return g_err.c_str(); }
+
+const char* lf_version(void) { return "loomfuse-b200 0.1 (sm_100a)"; }
+
+int lf_plan_create(const char* spec_text, size_t len, const char* filename, lf_plan** out) {
+  try {
+    g_err.clear();
+    if (!out) return fail(LF_ERR_SPEC, "out is NULL");
+    *out = nullptr;
+    if (!spec_text) return fail(LF_ERR_SPEC, "spec_text is NULL");
+    std::string text(spec_text, len);
+    std::string file = filename ? filename : "<input>";
+    lf::DiagList d;
+    auto rs = lf::parse_spec(text, file, d);
+    if (!rs) return fail(LF_ERR_SPEC, d.str());
+    auto plan = lf::make_plan(*rs, d);
+    if (!plan) return fail(LF_ERR_SPEC, d.str());
+    auto* p = new lf_plan;
+    p->plan = std::move(*plan);
+    p->report = p->plan.report_json();
+    std::string why = "no built-in executor implements this chain";
+    for (const auto& s : signed_executors()) {
+      if (!s.error.empty()) {
+        why = std::string("embedded spec ") + s.exec->spec_file + " failed to plan: " + s.error;
+        continue;
+      }
+      if (s.signature != p->plan.signature) continue;
+      std::string w;
+      if (s.exec->supports(p->plan, w)) {
+        p->exec = s.exec;
+        break;
+      }
+      why = std::string(s.exec->name) + ": " + w;
+    }
+    if (!p->exec) p->unsupported = why;
+    *out = p;
+    return LF_OK;
+  } catch (const std::exception& e) {
+    return fail(LF_ERR_INTERNAL, std::string("internal error: ") + e.what());
+  }
+}
+
+int lf_spec_print(const char* spec_text, size_t len, const char* filename, char* buf, size_t cap,
+                  size_t* needed) {
+  try {
+    g_err.clear();
+    if (!spec_text) return fail(LF_ERR_SPEC, "spec_text is NULL");
+    lf::DiagList d;
+    auto rs = lf::parse_spec(std::string(spec_text, len), filename ? filename : "<input>", d);
+    if (!rs) return fail(LF_ERR_SPEC, d.str());
+    std::string text = lf::print_spec(*rs);
+    if (needed) *needed = text.size() + 1;
+    if (buf && cap) {
+      size_t n = std::min(cap - 1, text.size());
+      std::memcpy(buf, text.data(), n);
+      buf[n] = '\0';
+    }
+    return LF_OK;
+  } catch (const std::exception& e) {
+    return fail(LF_ERR_INTERNAL, std::string("internal error: ") + e.what());
+  }
+}
+
+void lf_plan_destroy(lf_plan* plan) { delete plan; }
+
+int lf_plan_num_terminals(const lf_plan* plan) {
+  return plan ? static_cast<int>(plan->plan.terminals.size()) : 0;
+}
+
+int lf_plan_terminal(const lf_plan* plan, int idx, lf_terminal* out) {
+  if (!plan || !out) return fail(LF_ERR_SPEC, "NULL argument");
+  if (idx < 0 || idx >= static_cast<int>(plan->plan.terminals.size()))
+    return fail(LF_ERR_SPEC, "terminal index out of range");
+  const auto& t = plan->plan.terminals[idx];
+  if (t.dims.size() > LF_MAX_DIMS) return fail(LF_ERR_SPEC, "terminal rank exceeds LF_MAX_DIMS");
+  std::memset(out, 0, sizeof *out);
+  std::strncpy(out->name, t.name.c_str(), sizeof out->name - 1);
+  std::strncpy(out->type, t.type.c_str(), sizeof out->type - 1);
+  out->is_goal = t.is_goal;
+  out->elem_bytes = t.elem_bytes;
+  out->ndim = static_cast<int32_t>(t.dims.size());
+  for (size_t k = 0; k < t.dims.size(); ++k) {
+    out->loop_dim[k] = t.dims[k];
+    out->extent[k] = t.extent.size() > k ? t.extent[k] : 1;
+    out->base[k] = t.base.size() > k ? t.base[k] : 0;
+  }
+  out->bytes = terminal_bytes(t);
+  return LF_OK;
+}
+
+int lf_plan_report(const lf_plan* plan, char* buf, size_t cap, size_t* needed) {
+  if (!plan) return fail(LF_ERR_SPEC, "plan is NULL");
+  if (needed) *needed = plan->report.size() + 1;
+  if (buf && cap) {
+    size_t n = std::min(cap - 1, plan->report.size());
+    std::memcpy(buf, plan->report.data(), n);
+    buf[n] = '\0';
+  }
+  return LF_OK;
+}
+
+const char* lf_plan_executor(const lf_plan* plan) { return plan && plan->exec ? plan->exec->name : ""; }
+
+int lf_plan_launches_per_step(const lf_plan* plan) { return plan && plan->exec ? plan->exec->launches_per_step : 0; }
+
+double lf_plan_compulsory_bytes_per_cell(const lf_plan* plan) {
+  return plan && plan->exec ? plan->exec->bytes_per_cell : 0.0;
+}
+
+int lf_run(const lf_plan* cplan, void* const* terms, int nterm, int steps, void* cuda_stream) {
+  try {
+    g_err.clear();
+    int st = check_run_args(cplan, terms, nterm, steps);
+    if (st != LF_OK) return st;
+    lf_plan* plan = const_cast<lf_plan*>(cplan);
+    std::lock_guard<std::mutex> lk(plan->mu);
+    std::string err;
+    std::vector<void*> scratch;
+    if (steps > 1) {
+      if ((st = ensure_scratch(plan, err)) != LF_OK) return fail(st, err);
+      scratch = scratch_list(plan);
+    }
+    lfx::ExecArgs a;
+    a.plan = &plan->plan;
+    a.terms = terms;
+    a.steps = steps;
+    a.stream = static_cast<cudaStream_t>(cuda_stream);
+    a.scratch = scratch.data();
+    st = plan->exec->run(a, err);
+    if (st != LF_OK) return fail(st, err);
+    return LF_OK;
+  } catch (const std::exception& e) {
+    return fail(LF_ERR_INTERNAL, std::string("internal error: ") + e.what());
+  }
+}
+
+int lf_run_host(const lf_plan* cplan, void* const* terms, int nterm, int steps) {
+  try {
+    g_err.clear();
+    int st = check_run_args(cplan, terms, nterm, steps);
+    if (st != LF_OK) return st;
+    lf_plan* plan = const_cast<lf_plan*>(cplan);
+    std::lock_guard<std::mutex> lk(plan->mu);
+    std::string err;
+    const auto& T = plan->plan.terminals;
+    if (!plan->stream) {
+      cudaError_t e = cudaStreamCreateWithFlags(&plan->stream, cudaStreamNonBlocking);
+      if (e != cudaSuccess) return fail(lfx::cuda_status(e, "cudaStreamCreate", err), err);
+    }
+    if (plan->dev.size() != T.size()) {
+      plan->dev.assign(T.size(), nullptr);
+      for (size_t i = 0; i < T.size(); ++i) {
+        cudaError_t e = cudaMalloc(&plan->dev[i], terminal_bytes(T[i]));
+        if (e != cudaSuccess) return fail(lfx::cuda_status(e, "cudaMalloc(terminal)", err), err);
+      }
+    }
+    std::vector<void*> scratch;
+    if (steps > 1) {
+      if ((st = ensure_scratch(plan, err)) != LF_OK) return fail(st, err);
+      scratch = scratch_list(plan);
+    }
+    for (size_t i = 0; i < T.size(); ++i) {
+      if (T[i].is_goal) continue;
+      cudaError_t e = cudaMemcpyAsync(plan->dev[i], terms[i], terminal_bytes(T[i]), cudaMemcpyHostToDevice,
+                                      plan->stream);
+      if (e != cudaSuccess) return fail(lfx::cuda_status(e, "cudaMemcpyAsync(H2D)", err), err);
+    }
+    lfx::ExecArgs a;
+    a.plan = &plan->plan;
+    a.terms = plan->dev.data();
+    a.steps = steps;
+    a.stream = plan->stream;
+    a.scratch = scratch.data();
+    st = plan->exec->run(a, err);
+    if (st != LF_OK) return fail(st, err);
+    for (size_t i = 0; i < T.size(); ++i) {
+      if (!T[i].is_goal) continue;
+      cudaError_t e = cudaMemcpyAsync(terms[i], plan->dev[i], terminal_bytes(T[i]), cudaMemcpyDeviceToHost,
+                                      plan->stream);
+      if (e != cudaSuccess) return fail(lfx::cuda_status(e, "cudaMemcpyAsync(D2H)", err), err);
+    }
+    cudaError_t e = cudaStreamSynchronize(plan->stream);
+    if (e != cudaSuccess) return fail(lfx::cuda_status(e, "cudaStreamSynchronize", err), err);
+    return LF_OK;
+  } catch (const std::exception& e) {
+    return fail(LF_ERR_INTERNAL, std::string("internal error: ") + e.what());
+  }
+}
+
+int lf_run_slab(const lf_plan* cplan, void* const* terms, int nterm, const lf_slab* slab, void* cuda_stream) {
+  try {
+    g_err.clear();
+    int st = check_run_args(cplan, terms, nterm, 1);
+    if (st != LF_OK) return st;
+    if (!slab || slab->lo < 0 || slab->hi <= slab->lo || slab->hi > slab->global)
+      return fail(LF_ERR_SPEC, "invalid slab");
+    lfx::ExecArgs a;
+    a.plan = &cplan->plan;
+    a.terms = terms;
+    a.steps = 1;
+    a.stream = static_cast<cudaStream_t>(cuda_stream);
+    a.slab = slab;
+    std::string err;
+    st = cplan->exec->run(a, err);
+    if (st != LF_OK) return fail(st, err);
+    return LF_OK;
+  } catch (const std::exception& e) {
+    return fail(LF_ERR_INTERNAL, std::string("internal error: ") + e.what());
+  }
+}
+
+}  // extern "C"

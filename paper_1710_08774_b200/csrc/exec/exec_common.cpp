@@ -1,0 +1,57 @@
+// Host helpers shared by the executors: TMA descriptor encoding through the
+// runtime's driver entry point, CUDA error mapping.
+#include <mutex>
+
+#include "common.cuh"
+#include "exec.hpp"
+
+namespace lfx {
+
+int cuda_status(cudaError_t e, const char* what, std::string& err) {
+  if (e == cudaSuccess) return LF_OK;
+  err = std::string(what) + ": " + cudaGetErrorName(e) + " (" + cudaGetErrorString(e) + ")";
+  return LF_ERR_CUDA;
+}
+
+static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+
+bool make_tensor_map(CUtensorMap* map, const void* base, CUtensorMapDataType dtype, int elem_bytes, int rank,
+                     const uint64_t* dims, const uint32_t* box, std::string& err) {
+  auto fn = encode_fn();
+  if (!fn) {
+    err = "cuTensorMapEncodeTiled unavailable from the CUDA driver";
+    return false;
+  }
+  cuuint64_t gdim[5];
+  cuuint64_t gstride[4];
+  cuuint32_t bdim[5], estride[5];
+  uint64_t acc = static_cast<uint64_t>(elem_bytes);
+  for (int d = 0; d < rank; ++d) {
+    gdim[d] = dims[d];
+    bdim[d] = box[d];
+    estride[d] = 1;
+    if (d > 0) gstride[d - 1] = acc;
+    acc *= dims[d];
+  }
+  CUresult r = fn(map, dtype, rank, const_cast<void*>(base), gdim, gstride, bdim, estride,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    err = "cuTensorMapEncodeTiled failed with CUresult " + std::to_string(static_cast<int>(r));
+    return false;
+  }
+  return true;
+}
+
+}  // namespace lfx

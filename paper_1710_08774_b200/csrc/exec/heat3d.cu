@@ -1,0 +1,265 @@
+// Fused sm_100a executor for the 3D heat chain (BASELINE.json configs[1];
+// specs/heat3d.lf): fluxx, fluxy, fluxz -> divupd, fp64, periodic.
+//
+// HFAV contracts fx to a scalar carry, fy to 2 rows and fz to 2 planes
+// (SURVEY.md App. A).  On B200 the same elision is done as 2.5-D streaming:
+// one CTA owns a 64 x 16 (i, j) column of the grid and marches along k.
+//   * a producer warp streams u planes (tile + 1-cell halo, 66 x 18 doubles)
+//     into an S-stage shared-memory ring with TMA (cp.async.bulk.tensor.3d),
+//     completion signalled on mbarriers; consumers free slots on a second
+//     mbarrier set, so loads run S-2 planes ahead of the math;
+//   * 8 consumer warps compute two rows x two cells each; fx/fy live only in
+//     registers (recomputed per cell from the staged plane), fz(k-1) is the
+//     register carry of the previous plane -- no intermediate touches HBM;
+//   * the output is written once, and the periodic ghost layer of the goal
+//     buffer is refilled by the CTAs that own the wrapped cells, so the next
+//     step can stream the buffer straight back in (iterate: pairs).
+// Compulsory traffic: 8 B read + 8 B written per cell-update.
+#include <cstdio>
+
+#include "../../userkernels/stencil_kernels.h"
+#include "common.cuh"
+#include "exec.hpp"
+
+namespace lfx {
+namespace {
+
+constexpr int TX = 64;                 // cells along i per CTA (32 lanes x 2)
+constexpr int TY = 16;                 // rows along j per CTA (8 warps x 2)
+constexpr int CWARPS = TY / 2;         // consumer warps
+constexpr int THREADS = (CWARPS + 1) * 32;
+constexpr int LD = TX + 2;             // staged row length (halo 1 each side)
+constexpr int ROWS = TY + 2;
+constexpr int STAGE_TX = LD * ROWS * 8;                     // bytes TMA delivers
+constexpr int STAGE_BYTES = (STAGE_TX + 127) / 128 * 128;   // 128-B aligned slots
+constexpr int S = 6;                                        // ring depth
+constexpr int SMEM = S * STAGE_BYTES + 2 * S * 8 + 128;
+
+struct Params {
+  int ni, nj, nk;       // interior sizes of this launch
+  long long pj, pk;     // element strides of the (nk+2, nj+2, ni+2) layout
+  int tiles_x;          // ni / TX
+  int kchunks;          // CTAs along k per column
+  int wrap_i, wrap_j, wrap_k;  // refill periodic ghosts along this dim
+};
+
+__global__ void __launch_bounds__(THREADS, 2)
+    heat3d_fused(const __grid_constant__ CUtensorMap tin, double* __restrict__ out, const Params p) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  double* ring = reinterpret_cast<double*>(smem);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + S * STAGE_BYTES);
+  uint64_t* empty = full + S;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int tile = blockIdx.x;
+  const int i0 = (tile % p.tiles_x) * TX;
+  const int j0 = (tile / p.tiles_x) * TY;
+  const int k0 = static_cast<int>((long long)blockIdx.y * p.nk / p.kchunks);
+  const int k1 = static_cast<int>((long long)(blockIdx.y + 1) * p.nk / p.kchunks);
+  const int kc = k1 - k0;
+  const int nplanes = kc + 2;  // logical planes k0-1 .. k1
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], CWARPS);
+    }
+    fence_barrier_init();
+  }
+  __syncthreads();
+
+  if (warp == CWARPS) {
+    // ---------------- producer: one elected lane streams planes ----------------
+    if (lane == 0) {
+      tma_prefetch_desc(&tin);
+      for (int q = 0; q < nplanes; ++q) {
+        const int slot = q % S;
+        if (q >= S) mbar_wait(&empty[slot], ((q / S) & 1) ^ 1);
+        mbar_arrive_expect_tx(&full[slot], STAGE_TX);
+        // storage coordinates: logical + 1 (terminal base is -1 in every dim)
+        tma_load_3d(reinterpret_cast<unsigned char*>(ring) + slot * STAGE_BYTES, &tin, &full[slot], i0, j0,
+                    k0 + q);
+      }
+    }
+    return;
+  }
+
+  // ---------------- consumers ----------------
+  const int r0 = 2 * warp;  // first tile row of this warp
+  const int c0 = 2 * lane;  // first tile column of this lane
+  auto stage = [&](int q) { return reinterpret_cast<const double*>(reinterpret_cast<unsigned char*>(ring) +
+                                                                   (q % S) * STAGE_BYTES); };
+  auto center = [&](const double* sp, int r, int c) { return sp[(r0 + r + 1) * LD + (c0 + c + 1)]; };
+
+  double uprev[2][2], ucur[2][2], unext[2][2];
+  mbar_wait(&full[0], 0);
+  {
+    const double* sp = stage(0);
+#pragma unroll
+    for (int r = 0; r < 2; ++r)
+#pragma unroll
+      for (int c = 0; c < 2; ++c) uprev[r][c] = center(sp, r, c);
+  }
+  __syncwarp();
+  if (lane == 0) mbar_arrive(&empty[0]);
+  mbar_wait(&full[1 % S], (1 / S) & 1);
+  {
+    const double* sp = stage(1);
+#pragma unroll
+    for (int r = 0; r < 2; ++r)
+#pragma unroll
+      for (int c = 0; c < 2; ++c) ucur[r][c] = center(sp, r, c);
+  }
+
+  const int gi = i0 + c0;  // logical i of this lane's first cell
+  for (int kk = 0; kk < kc; ++kk) {
+    const int q = kk + 1, qn = kk + 2;
+    mbar_wait(&full[qn % S], (qn / S) & 1);
+    const double* sn = stage(qn);
+#pragma unroll
+    for (int r = 0; r < 2; ++r)
+#pragma unroll
+      for (int c = 0; c < 2; ++c) unext[r][c] = center(sn, r, c);
+    const double* sp = stage(q);
+    const int k = k0 + kk;
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+      const int row = r0 + r + 1;
+      // i-1 .. i+2 of this row, and the two cells of the rows above/below
+      const double w = sp[row * LD + c0];
+      const double e = sp[row * LD + c0 + 3];
+      double o[2];
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        const double uc = ucur[r][c];
+        const double ue = c == 0 ? ucur[r][1] : e;
+        const double uw = c == 0 ? w : ucur[r][0];
+        const double un = sp[(row + 1) * LD + c0 + c + 1];
+        const double us = sp[(row - 1) * LD + c0 + c + 1];
+        double fxp, fxm, fyp, fym, fzp, fzm;
+        face_flux(ue, uc, &fxp);
+        face_flux(uc, uw, &fxm);
+        face_flux(un, uc, &fyp);
+        face_flux(uc, us, &fym);
+        face_flux(unext[r][c], uc, &fzp);
+        face_flux(uc, uprev[r][c], &fzm);
+        heat_divupd(uc, fxp, fxm, fyp, fym, fzp, fzm, &o[c]);
+      }
+      const int j = j0 + r0 + r;
+      double* rowp = out + (long long)(k + 1) * p.pk + (long long)(j + 1) * p.pj;
+      st_stream(rowp + gi + 1, o[0]);
+      st_stream(rowp + gi + 2, o[1]);
+      // periodic ghost refill by the owners of the wrapped cells
+      if (p.wrap_i) {
+        if (gi == 0) st_stream(rowp + p.ni + 1, o[0]);
+        if (gi + 1 == p.ni - 1) st_stream(rowp, o[1]);
+      }
+      if (p.wrap_j && (j == 0 || j == p.nj - 1)) {
+        double* g = out + (long long)(k + 1) * p.pk + (long long)(j == 0 ? p.nj + 1 : 0) * p.pj;
+        st_stream(g + gi + 1, o[0]);
+        st_stream(g + gi + 2, o[1]);
+      }
+      if (p.wrap_k && (k == 0 || k == p.nk - 1)) {
+        double* g = out + (long long)(k == 0 ? p.nk + 1 : 0) * p.pk + (long long)(j + 1) * p.pj;
+        st_stream(g + gi + 1, o[0]);
+        st_stream(g + gi + 2, o[1]);
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[q % S]);
+#pragma unroll
+    for (int r = 0; r < 2; ++r)
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        uprev[r][c] = ucur[r][c];
+        ucur[r][c] = unext[r][c];
+      }
+  }
+}
+
+bool supports(const lf::Plan& plan, std::string& why) {
+  const auto& r = plan.rs.ranges;
+  long nk = r[0].trips(), nj = r[1].trips(), ni = r[2].trips();
+  for (const auto& rg : r)
+    if (rg.stride != 1) {
+      why = "heat3d executor needs unit strides";
+      return false;
+    }
+  if (ni % TX || nj % TY || nk < 1) {
+    why = "heat3d executor needs N_i % 64 == 0 and N_j % 16 == 0 (got " + std::to_string(ni) + "x" +
+          std::to_string(nj) + ")";
+    return false;
+  }
+  if ((ni + 2) * 8 % 16) {
+    why = "row pitch must be a multiple of 16 bytes";
+    return false;
+  }
+  return true;
+}
+
+int launch_step(const double* in, double* out, int ni, int nj, int nk, bool wrap_k, cudaStream_t st,
+                std::string& err) {
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(heat3d_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
+    if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(heat3d)", err);
+    attr = true;
+  }
+  CUtensorMap map;
+  uint64_t dims[3] = {(uint64_t)ni + 2, (uint64_t)nj + 2, (uint64_t)nk + 2};
+  uint32_t box[3] = {LD, ROWS, 1};
+  if (!make_tensor_map(&map, in, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 8, 3, dims, box, err)) return LF_ERR_CUDA;
+  Params p;
+  p.ni = ni;
+  p.nj = nj;
+  p.nk = nk;
+  p.pj = ni + 2;
+  p.pk = (long long)(ni + 2) * (nj + 2);
+  p.tiles_x = ni / TX;
+  const int tiles = (ni / TX) * (nj / TY);
+  // one resident wave: split k so that tiles * kchunks fills the SMs once
+  int dev = 0, sms = 148, per_sm = 1;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, heat3d_fused, THREADS, SMEM);
+  if (per_sm < 1) per_sm = 1;
+  int kchunks = (sms * per_sm) / tiles;
+  if (kchunks < 1) kchunks = 1;
+  if (kchunks > nk) kchunks = nk;
+  p.kchunks = kchunks;
+  p.wrap_i = 1;
+  p.wrap_j = 1;
+  p.wrap_k = wrap_k ? 1 : 0;
+  dim3 grid(tiles, kchunks);
+  heat3d_fused<<<grid, THREADS, SMEM, st>>>(map, out, p);
+  return cuda_status(cudaGetLastError(), "heat3d_fused launch", err);
+}
+
+int run(const ExecArgs& a, std::string& err) {
+  const auto& r = a.plan->rs.ranges;
+  int nk = (int)r[0].trips(), nj = (int)r[1].trips(), ni = (int)r[2].trips();
+  bool wrap_k = true;
+  if (a.slab) {
+    nk = (int)(a.slab->hi - a.slab->lo);
+    wrap_k = false;  // k ghosts of a slab come from the caller's halo exchange
+  }
+  const double* src = static_cast<const double*>(a.terms[0]);
+  double* goal = static_cast<double*>(a.terms[1]);
+  double* scratch = a.steps > 1 ? static_cast<double*>(a.scratch[0]) : nullptr;
+  // steps alternate goal/scratch so that the last one lands in the goal and
+  // the axiom buffer is never written
+  for (int s = 0; s < a.steps; ++s) {
+    bool to_goal = ((a.steps - 1 - s) % 2) == 0;
+    double* dst = to_goal ? goal : scratch;
+    int st = launch_step(src, dst, ni, nj, nk, wrap_k, a.stream, err);
+    if (st != LF_OK) return st;
+    src = dst;
+  }
+  return LF_OK;
+}
+
+}  // namespace
+
+extern const Executor heat3d_executor = {"heat3d_fused_tma", "heat3d.lf", 1, 16.0, supports, run};
+
+}  // namespace lfx

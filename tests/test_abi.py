@@ -1,0 +1,64 @@
+"""The C-ABI library loads on a CPU-only host and exports every symbol the
+header declares; argument errors come back as status codes, never crashes."""
+import ctypes
+import re
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+import paper_1710_08774_b200 as lf
+from paper_1710_08774_b200 import inputs
+
+HEADER = Path(lf.PKG_DIR).parent / "include" / "loomfuse_b200.h"
+
+
+def declared_symbols():
+    text = HEADER.read_text()
+    return sorted(set(re.findall(r"^\s*(?:const\s+)?[\w\s\*]*?\b(lf_\w+)\s*\(", text, re.M)))
+
+
+def test_header_symbols_all_exported():
+    syms = declared_symbols()
+    assert len(syms) >= 13
+    L = lf.lib()
+    for s in syms:
+        assert hasattr(L, s), s
+    assert set(syms) == set(lf.ABI_SYMBOLS)
+
+
+def test_version_and_last_error():
+    L = lf.lib()
+    assert b"sm_100a" in L.lf_version()
+    with pytest.raises(lf.LoomfuseError):
+        lf.Plan("not: [a valid", "x.lf")
+    assert L.lf_last_error().decode()
+
+
+def test_run_argument_errors_are_status_codes():
+    p = lf.Plan.with_ranges("heat3d", (4, 16, 64))
+    with pytest.raises(ValueError):
+        p.run([0])
+    L = lf.lib()
+    one = (ctypes.c_void_p * 1)(1)
+    assert L.lf_run(p._h, one, 1, 1, None) == lf.LF_ERR_SPEC  # wrong terminal count
+    arr = (ctypes.c_void_p * 2)(0, 0)
+    assert L.lf_run(p._h, arr, 2, 1, None) == lf.LF_ERR_SPEC  # NULL buffers
+    arr = (ctypes.c_void_p * 2)(1, 1)
+    assert L.lf_run(p._h, arr, 2, 0, None) == lf.LF_ERR_SPEC  # steps < 1
+    box = lf.Plan.with_ranges("box2x", (16, 16))
+    a = np.zeros(box.terminals[0].bytes // 4, np.float32)
+    b = np.zeros(box.terminals[1].bytes // 4, np.float32)
+    with pytest.raises(lf.LoomfuseError):
+        box.run_host([a, b], steps=2)  # no iterate: pairs
+
+
+def test_terminal_layout_matches_inputs():
+    p = lf.Plan.with_ranges("heat3d", (4, 16, 64))
+    u = inputs.heat3d_input(4, 16, 64)
+    assert u.shape == p.terminals[0].extent and u.nbytes == p.terminals[0].bytes
+    q = lf.Plan.with_ranges("biharmonic2d", (32, 32))
+    assert inputs.biharm_input(32, 32).shape == q.terminals[0].extent == q.terminals[1].extent
+    r = lf.Plan.with_ranges("box2x", (8, 12))
+    assert inputs.box_input(8, 12).shape == r.terminals[0].extent
+    assert r.terminals[0].dtype == np.float32

@@ -1,0 +1,98 @@
+"""sm_100a fused heat3d executor vs the CPU oracle, bit-exact (config 2).
+
+Small grids are compared against run_naive; the full 512^3 grid against the
+HFAV fused CPU schedule (itself pinned to run_naive in test_oracle.py) plus
+size-independent properties (mass conservation under periodic diffusion, the
+maximum principle)."""
+import numpy as np
+import pytest
+
+import oracle
+import paper_1710_08774_b200 as lf
+from paper_1710_08774_b200 import inputs
+
+pytestmark = pytest.mark.gpu
+
+
+def _torch():
+    import torch
+    return torch
+
+
+def interior(a):
+    return a[1:-1, 1:-1, 1:-1]
+
+
+def bits(a):
+    return np.ascontiguousarray(a).view(np.uint64)
+
+
+@pytest.mark.parametrize("shape,steps", [((4, 16, 64), 1), ((8, 16, 64), 3), ((20, 32, 128), 2),
+                                         ((64, 64, 64), 4), ((3, 48, 192), 5)])
+def test_device_path_matches_naive(shape, steps):
+    torch = _torch()
+    plan = lf.Plan.with_ranges("heat3d", shape)
+    assert plan.executor == "heat3d_fused_tma"
+    u = inputs.heat3d_input(*shape, seed=11, sigma=4.0)
+    ref = oracle.heat3d(u, steps)
+    du = torch.from_numpy(u).cuda()
+    keep = du.clone()
+    out = torch.full_like(du, float("nan"))
+    plan.run([du, out], steps=steps)
+    torch.cuda.synchronize()
+    got = out.cpu().numpy()
+    assert np.array_equal(bits(interior(got)), bits(interior(ref)))
+    assert torch.equal(du, keep), "axiom buffer must not be written"
+    # the periodic ghost faces the next step reads are refilled
+    g = got.copy()
+    for ax in range(3):
+        sl_g = [slice(1, -1)] * 3
+        sl_s = [slice(1, -1)] * 3
+        sl_g[ax], sl_s[ax] = 0, -2
+        assert np.array_equal(bits(g[tuple(sl_g)]), bits(g[tuple(sl_s)]))
+
+
+def test_host_path_matches_oracle():
+    shape, steps = (16, 32, 128), 3
+    plan = lf.Plan.with_ranges("heat3d", shape)
+    u = inputs.heat3d_input(*shape, seed=5, sigma=5.0)
+    out = np.zeros_like(u)
+    plan.run_host([u, out], steps=steps)
+    ref = oracle.heat3d(u, steps, fused=True)
+    assert np.array_equal(bits(interior(out)), bits(interior(ref)))
+    # a second call reuses the cached device buffers
+    out2 = np.zeros_like(u)
+    plan.run_host([u, out2], steps=1)
+    assert np.array_equal(bits(interior(out2)), bits(interior(oracle.heat3d(u, 1))))
+
+
+def test_full_size_512_matches_fused_cpu_and_conserves_mass():
+    torch = _torch()
+    shape, steps = (512, 512, 512), 2
+    plan = lf.Plan.bundled("heat3d")
+    u = inputs.heat3d_input(*shape, seed=0)
+    du = torch.from_numpy(u).cuda()
+    out = torch.empty_like(du)
+    plan.run([du, out], steps=steps)
+    torch.cuda.synchronize()
+    got = out.cpu().numpy()
+    ref = oracle.heat3d(u, steps, fused=True)
+    assert np.array_equal(bits(interior(got)), bits(interior(ref)))
+    s0 = interior(u).sum(dtype=np.float64)
+    assert interior(got).sum(dtype=np.float64) == pytest.approx(s0, rel=1e-12)
+    assert interior(got).max() <= interior(u).max() and interior(got).min() >= interior(u).min()
+
+
+def test_slab_mode_skips_k_wrap():
+    torch = _torch()
+    shape = (8, 16, 64)
+    plan = lf.Plan.with_ranges("heat3d", shape)
+    u = inputs.heat3d_input(*shape, seed=3, sigma=3.0)
+    du = torch.from_numpy(u).cuda()
+    out = torch.zeros_like(du)
+    plan.run_slab([du, out], 0, 8, 8)
+    torch.cuda.synchronize()
+    got = out.cpu().numpy()
+    ref = oracle.heat3d(u, 1)
+    assert np.array_equal(bits(interior(got)), bits(interior(ref)))
+    assert not got[0].any() and not got[-1].any()

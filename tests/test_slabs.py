@@ -1,0 +1,61 @@
+"""Slab decomposition + halo exchange (the multi-GPU host logic) on CPU with
+gloo, world_size 2: slabs advanced independently and stitched by the exchange
+must reproduce the single-domain oracle bit for bit."""
+import os
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import oracle
+from paper_1710_08774_b200 import inputs, slabs
+
+
+def _worker(rank, world, port, shape, steps, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        nk, nj, ni = shape
+        u = inputs.heat3d_input(nk, nj, ni, seed=21, sigma=2.0)
+        lo, hi = slabs.slab_range(nk, rank, world)
+        local = torch.from_numpy(u[lo:hi + 2].copy())  # ghost planes lo-1 .. hi
+        scratch = torch.empty_like(local)
+
+        def step(src, dst):
+            dst[0].copy_(torch.from_numpy(oracle.heat3d(src[0].numpy(), 1)))
+
+        halo = slabs.Halo(1, 1, periodic=True)
+        res = slabs.run_slabs(step, [local], [scratch], steps, halo, rank, world)
+        q.put((rank, lo, hi, res[0][1:-1].numpy().copy()))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,shape,steps", [(2, (8, 6, 10), 3), (3, (9, 4, 6), 2)])
+def test_heat3d_slabs_match_single_domain(world, shape, steps):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = 29500 + np.random.randint(0, 2000)
+    procs = [ctx.Process(target=_worker, args=(r, world, port, shape, steps, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    parts = [q.get(timeout=120) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    nk, nj, ni = shape
+    ref = oracle.heat3d(inputs.heat3d_input(nk, nj, ni, seed=21, sigma=2.0), steps)
+    for rank, lo, hi, part in parts:
+        got = part[:, 1:-1, 1:-1]
+        want = ref[1 + lo:1 + hi, 1:-1, 1:-1]
+        assert np.array_equal(got.view(np.uint64), want.view(np.uint64)), rank
+
+
+def test_slab_ranges_cover():
+    for n, w in [(512, 8), (7, 3), (4096, 6)]:
+        rs = [slabs.slab_range(n, r, w) for r in range(w)]
+        assert rs[0][0] == 0 and rs[-1][1] == n
+        assert all(a[1] == b[0] for a, b in zip(rs, rs[1:]))
