@@ -73,6 +73,31 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, u
       : "memory");
 }
 
+// L2 eviction policy for streaming outputs: written once, read next launch
+// from the far end of the grid, so they should not displace input rows that
+// neighbouring CTAs are about to read as halo.
+__device__ __forceinline__ uint64_t l2_evict_first_policy() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ void st_hint(double* ptr, double v, uint64_t pol) {
+  asm volatile("st.global.L1::no_allocate.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(ptr), "d"(v), "l"(pol) : "memory");
+}
+__device__ __forceinline__ void st_hint(float* ptr, float v, uint64_t pol) {
+  asm volatile("st.global.L1::no_allocate.L2::cache_hint.f32 [%0], %1, %2;" ::"l"(ptr), "f"(v), "l"(pol) : "memory");
+}
+__device__ __forceinline__ void st_hint2(double* ptr, double a, double b, uint64_t pol) {
+  asm volatile("st.global.L1::no_allocate.L2::cache_hint.v2.f64 [%0], {%1, %2}, %3;" ::"l"(ptr), "d"(a), "d"(b),
+               "l"(pol)
+               : "memory");
+}
+__device__ __forceinline__ void st_hint4(float* ptr, float a, float b, float c, float d, uint64_t pol) {
+  asm volatile("st.global.L1::no_allocate.L2::cache_hint.v4.f32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(ptr), "f"(a),
+               "f"(b), "f"(c), "f"(d), "l"(pol)
+               : "memory");
+}
+
 // streaming stores: evict-first so output does not displace halo rows in L2
 __device__ __forceinline__ void st_stream(double* p, double v) {
   asm volatile("st.global.L1::no_allocate.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");

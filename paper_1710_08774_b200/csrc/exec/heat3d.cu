@@ -15,6 +15,7 @@
 //     buffer is refilled by the CTAs that own the wrapped cells, so the next
 //     step can stream the buffer straight back in (iterate: pairs).
 // Compulsory traffic: 8 B read + 8 B written per cell-update.
+#include <algorithm>
 #include <cstdio>
 
 #include "../../userkernels/stencil_kernels.h"
@@ -34,30 +35,41 @@ constexpr int STAGE_TX = LD * ROWS * 8;                     // bytes TMA deliver
 constexpr int STAGE_BYTES = (STAGE_TX + 127) / 128 * 128;   // 128-B aligned slots
 constexpr int S = 6;                                        // ring depth
 constexpr int SMEM = S * STAGE_BYTES + 2 * S * 8 + 128;
+constexpr int KCH = 32;                // planes per work unit
 
 struct Params {
   int ni, nj, nk;       // interior sizes of this launch
   long long pj, pk;     // element strides of the (nk+2, nj+2, ni+2) layout
-  int tiles_x;          // ni / TX
-  int kchunks;          // CTAs along k per column
+  int tiles_x, tiles;   // column tiles
+  int kchunks;          // work units along k per column
+  int units;            // tiles * kchunks
   int wrap_i, wrap_j, wrap_k;  // refill periodic ghosts along this dim
 };
+
+// Work unit u = (k chunk, column tile), k-chunk major: at any moment all
+// persistent CTAs are inside the same one or two k chunks, so the halo rows a
+// CTA stages were staged moments earlier by its neighbours and hit in L2.
+struct Unit {
+  int i0, j0, k0, kc;
+};
+__device__ __forceinline__ Unit unit_of(const Params& p, int u) {
+  const int kb = u / p.tiles, t = u - kb * p.tiles;
+  Unit r;
+  r.i0 = (t % p.tiles_x) * TX;
+  r.j0 = (t / p.tiles_x) * TY;
+  r.k0 = static_cast<int>((long long)kb * p.nk / p.kchunks);
+  r.kc = static_cast<int>((long long)(kb + 1) * p.nk / p.kchunks) - r.k0;
+  return r;
+}
 
 __global__ void __launch_bounds__(THREADS, 2)
     heat3d_fused(const __grid_constant__ CUtensorMap tin, double* __restrict__ out, const Params p) {
   extern __shared__ __align__(128) unsigned char smem[];
-  double* ring = reinterpret_cast<double*>(smem);
+  unsigned char* ring = smem;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + S * STAGE_BYTES);
   uint64_t* empty = full + S;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int tile = blockIdx.x;
-  const int i0 = (tile % p.tiles_x) * TX;
-  const int j0 = (tile / p.tiles_x) * TY;
-  const int k0 = static_cast<int>((long long)blockIdx.y * p.nk / p.kchunks);
-  const int k1 = static_cast<int>((long long)(blockIdx.y + 1) * p.nk / p.kchunks);
-  const int kc = k1 - k0;
-  const int nplanes = kc + 2;  // logical planes k0-1 .. k1
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) {
@@ -72,108 +84,121 @@ __global__ void __launch_bounds__(THREADS, 2)
     // ---------------- producer: one elected lane streams planes ----------------
     if (lane == 0) {
       tma_prefetch_desc(&tin);
-      for (int q = 0; q < nplanes; ++q) {
-        const int slot = q % S;
-        if (q >= S) mbar_wait(&empty[slot], ((q / S) & 1) ^ 1);
-        mbar_arrive_expect_tx(&full[slot], STAGE_TX);
-        // storage coordinates: logical + 1 (terminal base is -1 in every dim)
-        tma_load_3d(reinterpret_cast<unsigned char*>(ring) + slot * STAGE_BYTES, &tin, &full[slot], i0, j0,
-                    k0 + q);
+      int g = 0;  // running plane counter across this CTA's units
+      for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
+        const Unit w = unit_of(p, u);
+        for (int q = 0; q < w.kc + 2; ++q, ++g) {
+          const int slot = g % S;
+          if (g >= S) mbar_wait(&empty[slot], ((g / S) & 1) ^ 1);
+          mbar_arrive_expect_tx(&full[slot], STAGE_TX);
+          // storage coordinates = logical + 1 (terminal base is -1 in every dim):
+          // box origin at logical (i0-1, j0-1, k0-1+q)
+          tma_load_3d(ring + slot * STAGE_BYTES, &tin, &full[slot], w.i0, w.j0, w.k0 + q);
+        }
       }
     }
     return;
   }
 
-  // ---------------- consumers ----------------
-  const int r0 = 2 * warp;  // first tile row of this warp
-  const int c0 = 2 * lane;  // first tile column of this lane
-  auto stage = [&](int q) { return reinterpret_cast<const double*>(reinterpret_cast<unsigned char*>(ring) +
-                                                                   (q % S) * STAGE_BYTES); };
-  auto center = [&](const double* sp, int r, int c) { return sp[(r0 + r + 1) * LD + (c0 + c + 1)]; };
-
-  double uprev[2][2], ucur[2][2], unext[2][2];
-  mbar_wait(&full[0], 0);
-  {
-    const double* sp = stage(0);
+  // ---------------- consumers: warp w owns rows 2w, 2w+1; lane owns cells lane, lane+32
+  const uint64_t pol = l2_evict_first_policy();
+  const int r0 = 2 * warp;
+  auto stage = [&](int g) { return reinterpret_cast<const double*>(ring + (g % S) * STAGE_BYTES); };
+  auto at = [&](const double* sp, int row, int col) { return sp[row * LD + col]; };
+  int g = 0;
+  for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
+    const Unit w = unit_of(p, u);
+    double uprev[2][2], ucur[2][2], unext[2][2];
+    mbar_wait(&full[g % S], (g / S) & 1);
+    {
+      const double* sp = stage(g);
 #pragma unroll
-    for (int r = 0; r < 2; ++r)
+      for (int r = 0; r < 2; ++r)
 #pragma unroll
-      for (int c = 0; c < 2; ++c) uprev[r][c] = center(sp, r, c);
-  }
-  __syncwarp();
-  if (lane == 0) mbar_arrive(&empty[0]);
-  mbar_wait(&full[1 % S], (1 / S) & 1);
-  {
-    const double* sp = stage(1);
-#pragma unroll
-    for (int r = 0; r < 2; ++r)
-#pragma unroll
-      for (int c = 0; c < 2; ++c) ucur[r][c] = center(sp, r, c);
-  }
-
-  const int gi = i0 + c0;  // logical i of this lane's first cell
-  for (int kk = 0; kk < kc; ++kk) {
-    const int q = kk + 1, qn = kk + 2;
-    mbar_wait(&full[qn % S], (qn / S) & 1);
-    const double* sn = stage(qn);
-#pragma unroll
-    for (int r = 0; r < 2; ++r)
-#pragma unroll
-      for (int c = 0; c < 2; ++c) unext[r][c] = center(sn, r, c);
-    const double* sp = stage(q);
-    const int k = k0 + kk;
-#pragma unroll
-    for (int r = 0; r < 2; ++r) {
-      const int row = r0 + r + 1;
-      // i-1 .. i+2 of this row, and the two cells of the rows above/below
-      const double w = sp[row * LD + c0];
-      const double e = sp[row * LD + c0 + 3];
-      double o[2];
-#pragma unroll
-      for (int c = 0; c < 2; ++c) {
-        const double uc = ucur[r][c];
-        const double ue = c == 0 ? ucur[r][1] : e;
-        const double uw = c == 0 ? w : ucur[r][0];
-        const double un = sp[(row + 1) * LD + c0 + c + 1];
-        const double us = sp[(row - 1) * LD + c0 + c + 1];
-        double fxp, fxm, fyp, fym, fzp, fzm;
-        face_flux(ue, uc, &fxp);
-        face_flux(uc, uw, &fxm);
-        face_flux(un, uc, &fyp);
-        face_flux(uc, us, &fym);
-        face_flux(unext[r][c], uc, &fzp);
-        face_flux(uc, uprev[r][c], &fzm);
-        heat_divupd(uc, fxp, fxm, fyp, fym, fzp, fzm, &o[c]);
-      }
-      const int j = j0 + r0 + r;
-      double* rowp = out + (long long)(k + 1) * p.pk + (long long)(j + 1) * p.pj;
-      st_stream(rowp + gi + 1, o[0]);
-      st_stream(rowp + gi + 2, o[1]);
-      // periodic ghost refill by the owners of the wrapped cells
-      if (p.wrap_i) {
-        if (gi == 0) st_stream(rowp + p.ni + 1, o[0]);
-        if (gi + 1 == p.ni - 1) st_stream(rowp, o[1]);
-      }
-      if (p.wrap_j && (j == 0 || j == p.nj - 1)) {
-        double* g = out + (long long)(k + 1) * p.pk + (long long)(j == 0 ? p.nj + 1 : 0) * p.pj;
-        st_stream(g + gi + 1, o[0]);
-        st_stream(g + gi + 2, o[1]);
-      }
-      if (p.wrap_k && (k == 0 || k == p.nk - 1)) {
-        double* g = out + (long long)(k == 0 ? p.nk + 1 : 0) * p.pk + (long long)(j + 1) * p.pj;
-        st_stream(g + gi + 1, o[0]);
-        st_stream(g + gi + 2, o[1]);
-      }
+        for (int c = 0; c < 2; ++c) uprev[r][c] = at(sp, r0 + r + 1, lane + 32 * c + 1);
     }
     __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[q % S]);
+    if (lane == 0) mbar_arrive(&empty[g % S]);
+    ++g;
+    mbar_wait(&full[g % S], (g / S) & 1);
+    {
+      const double* sp = stage(g);
 #pragma unroll
-    for (int r = 0; r < 2; ++r)
+      for (int r = 0; r < 2; ++r)
 #pragma unroll
-      for (int c = 0; c < 2; ++c) {
-        uprev[r][c] = ucur[r][c];
-        ucur[r][c] = unext[r][c];
+        for (int c = 0; c < 2; ++c) ucur[r][c] = at(sp, r0 + r + 1, lane + 32 * c + 1);
+    }
+    const int gi0 = w.i0 + lane;  // logical i of cell c=0 (c=1 is gi0+32)
+    const bool wrap_lo_i = p.wrap_i && gi0 == 0;               // owns cell 0
+    const bool wrap_hi_i = p.wrap_i && gi0 + 32 == p.ni - 1;   // owns cell ni-1
+    for (int kk = 0; kk < w.kc; ++kk, ++g) {
+      const int gn = g + 1;
+      mbar_wait(&full[gn % S], (gn / S) & 1);
+      const double* sn = stage(gn);
+#pragma unroll
+      for (int r = 0; r < 2; ++r)
+#pragma unroll
+        for (int c = 0; c < 2; ++c) unext[r][c] = at(sn, r0 + r + 1, lane + 32 * c + 1);
+      const double* sp = stage(g);
+      const int k = w.k0 + kk;
+      double o[2][2];
+#pragma unroll
+      for (int r = 0; r < 2; ++r) {
+        const int row = r0 + r + 1;
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          const int col = lane + 32 * c + 1;
+          const double uc = ucur[r][c];
+          const double uw = at(sp, row, col - 1);
+          const double ue = at(sp, row, col + 1);
+          const double un = r == 0 ? ucur[1][c] : at(sp, row + 1, col);
+          const double us = r == 1 ? ucur[0][c] : at(sp, row - 1, col);
+          double fxp, fxm, fyp, fym, fzp, fzm;
+          face_flux(ue, uc, &fxp);
+          face_flux(uc, uw, &fxm);
+          face_flux(un, uc, &fyp);
+          face_flux(uc, us, &fym);
+          face_flux(unext[r][c], uc, &fzp);
+          face_flux(uc, uprev[r][c], &fzm);
+          heat_divupd(uc, fxp, fxm, fyp, fym, fzp, fzm, &o[r][c]);
+        }
       }
+      // plane k fully consumed: hand the slot back to the producer before the stores
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[g % S]);
+      double* plane = out + (long long)(k + 1) * p.pk;
+#pragma unroll
+      for (int r = 0; r < 2; ++r) {
+        const int j = w.j0 + r0 + r;
+        double* rowp = plane + (long long)(j + 1) * p.pj + 1;  // logical i = 0
+        st_hint(rowp + gi0, o[r][0], pol);
+        st_hint(rowp + gi0 + 32, o[r][1], pol);
+        // periodic ghost refill by the owners of the wrapped cells
+        if (wrap_lo_i) st_hint(rowp + p.ni, o[r][0], pol);
+        if (wrap_hi_i) st_hint(rowp - 1, o[r][1], pol);
+        if (p.wrap_j && (j == 0 || j == p.nj - 1)) {
+          double* gr = plane + (long long)(j == 0 ? p.nj + 1 : 0) * p.pj + 1;
+          st_hint(gr + gi0, o[r][0], pol);
+          st_hint(gr + gi0 + 32, o[r][1], pol);
+        }
+        if (p.wrap_k && (k == 0 || k == p.nk - 1)) {
+          double* gr = out + (long long)(k == 0 ? p.nk + 1 : 0) * p.pk + (long long)(j + 1) * p.pj + 1;
+          st_hint(gr + gi0, o[r][0], pol);
+          st_hint(gr + gi0 + 32, o[r][1], pol);
+        }
+      }
+#pragma unroll
+      for (int r = 0; r < 2; ++r)
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          uprev[r][c] = ucur[r][c];
+          ucur[r][c] = unext[r][c];
+        }
+    }
+    // the unit's last staged plane (k0+kc) was only read for centres
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[g % S]);
+    ++g;
   }
 }
 
@@ -216,22 +241,23 @@ int launch_step(const double* in, double* out, int ni, int nj, int nk, bool wrap
   p.pj = ni + 2;
   p.pk = (long long)(ni + 2) * (nj + 2);
   p.tiles_x = ni / TX;
-  const int tiles = (ni / TX) * (nj / TY);
-  // one resident wave: split k so that tiles * kchunks fills the SMs once
-  int dev = 0, sms = 148, per_sm = 1;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, heat3d_fused, THREADS, SMEM);
-  if (per_sm < 1) per_sm = 1;
-  int kchunks = (sms * per_sm) / tiles;
-  if (kchunks < 1) kchunks = 1;
-  if (kchunks > nk) kchunks = nk;
-  p.kchunks = kchunks;
+  p.tiles = (ni / TX) * (nj / TY);
+  p.kchunks = (nk + KCH - 1) / KCH;
+  p.units = p.tiles * p.kchunks;
   p.wrap_i = 1;
   p.wrap_j = 1;
   p.wrap_k = wrap_k ? 1 : 0;
-  dim3 grid(tiles, kchunks);
-  heat3d_fused<<<grid, THREADS, SMEM, st>>>(map, out, p);
+  // persistent grid: every resident CTA slot on the chip, never more than units
+  static int slots = 0;
+  if (!slots) {
+    int dev = 0, sms = 148, per_sm = 1;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, heat3d_fused, THREADS, SMEM);
+    slots = sms * std::max(per_sm, 1);
+  }
+  const int ctas = std::min(p.units, slots);
+  heat3d_fused<<<ctas, THREADS, SMEM, st>>>(map, out, p);
   return cuda_status(cudaGetLastError(), "heat3d_fused launch", err);
 }
 
