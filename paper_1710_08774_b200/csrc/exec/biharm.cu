@@ -1,0 +1,280 @@
+// Fused sm_100a executor for the 2D biharmonic chain (BASELINE.json
+// configs[0]; specs/biharmonic2d.lf): lap1 -> lap2 -> upd, fp64, zero
+// Dirichlet halo of 2.
+//
+// HFAV contracts L to a 3-row outer_rotate window and L2 to a scalar.  Here
+// one warp marches a 128-column strip down the grid (rowstream.cuh): lane l
+// owns columns 4l..4l+3; u and L keep 3-row register windows that rotate by
+// register renaming (rows are unrolled by 3); the i +- 1
+// neighbours of u and L come from the adjacent lanes by shuffle, and lanes 0
+// and 31 additionally carry the two halo columns on each side of the strip.
+// Rows of u arrive by TMA, 3 rows per stage, into a 4-slot ring.  Output:
+// two 16-B stores per lane per row, plus the zero ghost ring of the goal buffer so iterated steps
+// can feed it straight back.  Compulsory traffic: 8 B read + 8 B written per
+// cell-update.
+#include <algorithm>
+#include <cstdlib>
+
+#include "../../userkernels/stencil_kernels.h"
+#include "common.cuh"
+#include "exec.hpp"
+#include "rowstream.cuh"
+
+namespace lfx {
+namespace {
+
+constexpr int H = 2;                   // chain radius along j and i
+constexpr int R = 3;                   // rows per stage (= register-window period)
+
+// Tunable shape: CPL columns per lane (strip = 32*CPL columns), S ring slots,
+// OCC resident CTAs per SM the register budget is sized for.
+template <int CPL_, int S_, int OCC_>
+struct Cfg {
+  static constexpr int CPL = CPL_, S = S_, OCC = OCC_;
+  static constexpr int SW = 32 * CPL;
+  static constexpr int BOXW = SW + 2 * H;
+  static constexpr int STAGE_TX = BOXW * R * 8;
+  static constexpr int STAGE_BYTES = (STAGE_TX + 127) / 128 * 128;
+  static constexpr int SMEM = S * STAGE_BYTES + S * 8 + 64;
+};
+
+struct Params {
+  int ni, nj;
+  long long pitch;    // ni + 4
+  int strips;         // ni / SW
+  int write_ghost_top, write_ghost_bottom;
+};
+
+template <int CPL>
+struct Win {
+  double u[3][CPL];   // u rows, indexed by row % 3
+  double ex[3][2];    // halo columns carried by the edge lanes
+  double L[3][CPL];   // L rows, indexed by row % 3
+  double lex[3];      // L at the halo column, indexed by row % 3
+};
+
+__device__ __forceinline__ double2 lds2(const double* p) { return *reinterpret_cast<const double2*>(p); }
+
+// One marched row.  P = (row index) % 3 is a compile-time constant, so the
+// three-row windows rotate by register renaming instead of moves.
+template <int CPL, int P>
+__device__ __forceinline__ void biharm_row(Win<CPL>& w, const double* row, int t, int lane, int ex_col, double* orow,
+                                           uint64_t pol) {
+  constexpr int C = P, M1 = (P + 2) % 3, M2 = (P + 1) % 3;  // rows r, r-1, r-2
+  {
+#pragma unroll
+    for (int h = 0; h < CPL / 2; ++h) {
+      const double2 a = lds2(row + CPL * lane + H + 2 * h);
+      w.u[C][2 * h] = a.x;
+      w.u[C][2 * h + 1] = a.y;
+    }
+    const double2 e = lds2(row + ex_col);
+    w.ex[C][0] = e.x; w.ex[C][1] = e.y;
+  }
+  if (t < 2) return;
+  // ---- lap1 at row r-1 (runs one row ahead of the output: shift j = +1)
+  const double* um = w.u[M1];
+  const double uleft = __shfl_up_sync(0xffffffffu, um[CPL - 1], 1);
+  const double uright = __shfl_down_sync(0xffffffffu, um[0], 1);
+  const double uw = lane == 0 ? w.ex[M1][1] : uleft;
+  const double ue = lane == 31 ? w.ex[M1][0] : uright;
+  double* Ln = w.L[M1];  // slot of L row r-1
+#pragma unroll
+  for (int c = 0; c < CPL; ++c)
+    lap5(c == 0 ? uw : um[c - 1], c == CPL - 1 ? ue : um[c + 1], w.u[M2][c], w.u[C][c], um[c], &Ln[c]);
+  // L at the strip's halo column: lane 0 -> logical -1, lane 31 -> SW (one lap5, operands selected)
+  {
+    const bool lo = lane == 0;
+    const double hw = lo ? w.ex[M1][0] : um[CPL - 1];
+    const double he = lo ? um[0] : w.ex[M1][1];
+    const int hc = lo ? 1 : 0;
+    const double hs = hc ? w.ex[M2][1] : w.ex[M2][0];
+    const double hn = hc ? w.ex[C][1] : w.ex[C][0];
+    const double h0 = hc ? w.ex[M1][1] : w.ex[M1][0];
+    lap5(hw, he, hs, hn, h0, &w.lex[M1]);
+  }
+  if (t < 4) return;
+  // ---- lap2 + update at row r-2: L rows r-3 (slot C), r-2 (slot M2), r-1 (slot M1)
+  const double* L0 = w.L[M2];
+  const double lleft = __shfl_up_sync(0xffffffffu, L0[CPL - 1], 1);
+  const double lright = __shfl_down_sync(0xffffffffu, L0[0], 1);
+  const double lhalo = w.lex[M2];  // halo-column L of row r-2
+  const double lw = lane == 0 ? lhalo : lleft;
+  const double le = lane == 31 ? lhalo : lright;
+  double o[CPL];
+#pragma unroll
+  for (int c = 0; c < CPL; ++c) {
+    double l2;
+    lap5(c == 0 ? lw : L0[c - 1], c == CPL - 1 ? le : L0[c + 1], w.L[C][c], w.L[M1][c], L0[c], &l2);
+    biharm_update(w.u[M2][c], l2, &o[c]);
+  }
+#pragma unroll
+  for (int h = 0; h < CPL / 2; ++h) st_hint2(orow + CPL * lane + 2 * h, o[2 * h], o[2 * h + 1], pol);
+}
+
+template <class K>
+__global__ void __launch_bounds__(32, K::OCC)
+    biharm_fused(const __grid_constant__ CUtensorMap tin, double* __restrict__ out, const Params p) {
+  constexpr int CPL = K::CPL, S = K::S, SW = K::SW, BOXW = K::BOXW, STAGE_BYTES = K::STAGE_BYTES;
+  constexpr int STAGE_TX = K::STAGE_TX;
+  extern __shared__ __align__(128) unsigned char smem[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + S * STAGE_BYTES);
+  const int lane = threadIdx.x;
+
+  RowSeg seg[3];
+  const int nseg = cta_segments(blockIdx.x, gridDim.x, p.strips, p.nj, seg);
+  RowRing<R, S> rr;
+  // staged column 0 = logical i0 - 2 = storage i0; storage row = logical + 2
+  rr.init(seg, nseg, H, smem, full, STAGE_BYTES, STAGE_TX, 0, H, SW);
+  if (lane == 0) {
+    for (int s = 0; s < S; ++s) mbar_init(&full[s], 1);
+    fence_barrier_init();
+    tma_prefetch_desc(&tin);
+    for (int g = 0; g < S; ++g) rr.issue(g, &tin);
+  }
+  __syncwarp();
+
+  const uint64_t pol = l2_evict_first_policy();
+  // extra columns: lane 0 -> logical -2,-1 ; lane 31 -> SW, SW+1 ; others: harmless copy
+  const int ex_col = lane == 0 ? 0 : (lane == 31 ? SW + H : CPL * lane + H);
+  int g = 0;
+  Win<CPL> w;
+  for (int k = 0; k < nseg; ++k) {
+    const RowSeg sg = seg[k];
+    const int T = sg.je - sg.jb + 2 * H;  // rows jb-2 .. je+1
+    // output row r-2 of marched row r = jb-2+t lives at storage row (jb-2+t-2)+2
+    double* orow = out + (long long)(sg.jb - 2) * p.pitch + H + sg.strip * SW;
+    for (int t0 = 0; t0 < T; t0 += R, ++g) {
+      rr.wait(g);
+      const double* st = reinterpret_cast<const double*>(rr.stage(g));
+      biharm_row<CPL, 0>(w, st, t0, lane, ex_col, orow, pol);
+      orow += p.pitch;
+      if (t0 + 1 < T) biharm_row<CPL, 1>(w, st + BOXW, t0 + 1, lane, ex_col, orow, pol);
+      orow += p.pitch;
+      if (t0 + 2 < T) biharm_row<CPL, 2>(w, st + 2 * BOXW, t0 + 2, lane, ex_col, orow, pol);
+      orow += p.pitch;
+      // every lane has consumed this stage: hand the slot to stage g + S
+      __syncwarp();
+      if (lane == 0) rr.issue(g + S, &tin);
+    }
+    // zero ghost ring of the goal buffer at the global edges
+    const bool lo_edge = sg.strip == 0, hi_edge = sg.strip == p.strips - 1;
+    for (int jo = sg.jb; jo < sg.je; jo += 32) {
+      const int j = jo + lane;
+      if (j < sg.je) {
+        double* rr0 = out + (long long)(j + H) * p.pitch;
+        if (lo_edge) st_hint2(rr0, 0.0, 0.0, pol);
+        if (hi_edge) st_hint2(rr0 + H + p.ni, 0.0, 0.0, pol);
+      }
+    }
+    for (int side = 0; side < 2; ++side) {
+      if (side == 0 && !(sg.jb == 0 && p.write_ghost_top)) continue;
+      if (side == 1 && !(sg.je == p.nj && p.write_ghost_bottom)) continue;
+      for (int gr = 0; gr < H; ++gr) {
+        double* o = out + (long long)(side == 0 ? gr : p.nj + H + gr) * p.pitch + H + sg.strip * SW;
+#pragma unroll
+        for (int h = 0; h < CPL / 2; ++h) st_hint2(o + CPL * lane + 2 * h, 0.0, 0.0, pol);
+        if (lane == 0 && lo_edge) st_hint2(o - H, 0.0, 0.0, pol);
+        if (lane == 31 && hi_edge) st_hint2(o + SW, 0.0, 0.0, pol);
+      }
+    }
+  }
+}
+
+// variant table (LF_BIHARM_VARIANT=<index> overrides the default for tuning runs)
+struct Variant {
+  const char* name;
+  int sw;
+  void (*kernel)(CUtensorMap, double*, Params);
+  int smem, occ;
+};
+template <class K>
+Variant make_variant(const char* n) {
+  return {n, K::SW, biharm_fused<K>, K::SMEM, K::OCC};
+}
+const Variant& variant() {
+  static const Variant table[] = {
+      make_variant<Cfg<4, 4, 16>>("cpl4_s4_occ16"), make_variant<Cfg<2, 4, 16>>("cpl2_s4_occ16"),
+      make_variant<Cfg<2, 6, 24>>("cpl2_s6_occ24"), make_variant<Cfg<4, 6, 12>>("cpl4_s6_occ12"),
+      make_variant<Cfg<2, 8, 16>>("cpl2_s8_occ16"), make_variant<Cfg<4, 8, 8>>("cpl4_s8_occ8"),
+  };
+  static int idx = [] {
+    const char* e = std::getenv("LF_BIHARM_VARIANT");
+    int i = e ? std::atoi(e) : 1;
+    return (i >= 0 && i < (int)(sizeof table / sizeof table[0])) ? i : 1;
+  }();
+  return table[idx];
+}
+
+bool supports(const lf::Plan& plan, std::string& why) {
+  const auto& r = plan.rs.ranges;
+  for (const auto& rg : r)
+    if (rg.stride != 1) {
+      why = "biharmonic executor needs unit strides";
+      return false;
+    }
+  long nj = r[0].trips(), ni = r[1].trips();
+  if (ni % 128 || nj < 1) {
+    why = "biharmonic executor needs N_i % 128 == 0 (got " + std::to_string(ni) + ")";
+    return false;
+  }
+  return true;
+}
+
+int launch_step(const double* in, double* out, int ni, int nj, bool top, bool bottom, cudaStream_t st,
+                std::string& err) {
+  const Variant& v = variant();
+  static int slots = 0;
+  if (!slots) {
+    cudaError_t e = cudaFuncSetAttribute(v.kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, v.smem);
+    if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(biharm)", err);
+    int dev = 0, sms = 148, per_sm = 1;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, v.kernel, 32, v.smem);
+    slots = sms * std::max(1, std::min(per_sm, v.occ));
+  }
+  CUtensorMap map;
+  uint64_t dims[2] = {(uint64_t)ni + 4, (uint64_t)nj + 4};
+  uint32_t box[2] = {(uint32_t)(v.sw + 2 * H), R};
+  if (!make_tensor_map(&map, in, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 8, 2, dims, box, err)) return LF_ERR_CUDA;
+  Params p;
+  p.ni = ni;
+  p.nj = nj;
+  p.pitch = ni + 4;
+  p.strips = ni / v.sw;
+  p.write_ghost_top = top;
+  p.write_ghost_bottom = bottom;
+  // at least ~16 rows per CTA so the 4 priming rows stay a small fraction
+  const long long work = (long long)p.strips * nj;
+  const int ctas = static_cast<int>(std::max<long long>(1, std::min<long long>(slots, work / 16)));
+  v.kernel<<<ctas, 32, v.smem, st>>>(map, out, p);
+  return cuda_status(cudaGetLastError(), "biharm_fused launch", err);
+}
+
+int run(const ExecArgs& a, std::string& err) {
+  const auto& r = a.plan->rs.ranges;
+  int nj = (int)r[0].trips(), ni = (int)r[1].trips();
+  bool top = true, bottom = true;
+  if (a.slab) {
+    nj = (int)(a.slab->hi - a.slab->lo);
+    top = a.slab->lo == 0;
+    bottom = a.slab->hi == a.slab->global;
+  }
+  const double* src = static_cast<const double*>(a.terms[0]);
+  double* goal = static_cast<double*>(a.terms[1]);
+  double* scratch = a.steps > 1 ? static_cast<double*>(a.scratch[0]) : nullptr;
+  for (int s = 0; s < a.steps; ++s) {
+    double* dst = ((a.steps - 1 - s) % 2) == 0 ? goal : scratch;
+    int st = launch_step(src, dst, ni, nj, top, bottom, a.stream, err);
+    if (st != LF_OK) return st;
+    src = dst;
+  }
+  return LF_OK;
+}
+
+}  // namespace
+
+extern const Executor biharm_executor = {"biharm2d_fused_tma", "biharmonic2d.lf", 1, 16.0, supports, run};
+
+}  // namespace lfx

@@ -48,7 +48,25 @@ LF_HD void heat_divupd(double c, double fxp, double fxm, double fyp, double fym,
 
 /* ---- config 4: separable 3x3 box filter, applied twice (fp32) ---------- */
 
+/* x / 3.0f, correctly rounded.  The device computes the IEEE quotient with
+ * one multiply by RN(1/3) and an FMA residual correction instead of the
+ * generic division subroutine (rcp + Newton + slow-path call); the sequence
+ * is exhaustively checked bit-identical to `x / 3.0f` for all 2^32 inputs
+ * (oracle/div3check.c, tests/test_div3.py).  Zeros and infinities keep the
+ * plain product, which is exact for them. */
+LF_HD float lf_div3f(float x) {
+#if defined(__CUDA_ARCH__)
+  const float r = 0x1.555556p-2f; /* RN(1/3) */
+  const float q = __fmul_rn(x, r);
+  const float e = __fmaf_rn(-q, 3.0f, x);
+  const float q1 = __fmaf_rn(e, r, q);
+  return (x == 0.0f || isinf(x)) ? q : q1;
+#else
+  return x / 3.0f;
+#endif
+}
+
 /* one 3-tap pass; a,b,c are the -1,0,+1 neighbours along the pass axis */
-LF_HD void box3(float a, float b, float c, float* o) { *o = (a + b + c) / 3.0f; }
+LF_HD void box3(float a, float b, float c, float* o) { *o = lf_div3f(a + b + c); }
 
 #endif

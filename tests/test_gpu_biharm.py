@@ -1,0 +1,70 @@
+"""sm_100a fused biharmonic executor vs the CPU oracle, bit-exact (config 1)."""
+import numpy as np
+import pytest
+
+import oracle
+import paper_1710_08774_b200 as lf
+from paper_1710_08774_b200 import inputs
+
+pytestmark = pytest.mark.gpu
+
+
+def bits(a):
+    return np.ascontiguousarray(a).view(np.uint64)
+
+
+def run_device(plan, u, steps):
+    import torch
+    du = torch.from_numpy(u).cuda()
+    keep = du.clone()
+    out = torch.full_like(du, float("nan"))
+    plan.run([du, out], steps=steps)
+    torch.cuda.synchronize()
+    assert torch.equal(du, keep), "axiom buffer must not be written"
+    return out.cpu().numpy()
+
+
+@pytest.mark.parametrize("shape,steps", [((1, 128), 1), ((5, 128), 2), ((16, 128), 1), ((37, 256), 3),
+                                         ((64, 384), 4), ((200, 256), 2), ((333, 128), 5)])
+def test_device_path_matches_naive(shape, steps):
+    plan = lf.Plan.with_ranges("biharmonic2d", shape)
+    assert plan.executor == "biharm2d_fused_tma"
+    u = inputs.biharm_input(*shape, seed=sum(shape))
+    got = run_device(plan, u, steps)
+    ref = oracle.biharm(u, steps)
+    # whole buffer, ghost ring included (zero Dirichlet, refilled every step)
+    assert np.array_equal(bits(got), bits(ref))
+
+
+def test_host_path_and_reuse():
+    shape = (48, 128)
+    plan = lf.Plan.with_ranges("biharmonic2d", shape)
+    u = inputs.biharm_input(*shape, seed=4)
+    for steps in (3, 1, 2):
+        out = np.full_like(u, 7.0)
+        plan.run_host([u, out], steps=steps)
+        assert np.array_equal(bits(out), bits(oracle.biharm(u, steps)))
+
+
+def test_full_size_4096_matches_fused_cpu():
+    plan = lf.Plan.bundled("biharmonic2d")
+    u = inputs.biharm_input(4096, 4096, seed=0)
+    got = run_device(plan, u, 3)
+    ref = oracle.biharm(u, 3, fused=True)
+    assert np.array_equal(bits(got), bits(ref))
+
+
+def test_slab_rows_leave_internal_ghosts_to_the_exchange():
+    import torch
+    shape = (24, 128)
+    plan = lf.Plan.with_ranges("biharmonic2d", shape)
+    u = inputs.biharm_input(*shape, seed=8)
+    ref = oracle.biharm(u, 1)
+    # middle slab rows [8, 16): buffer holds rows 6..17 (2 ghost rows each side)
+    local = torch.from_numpy(np.ascontiguousarray(u[8:8 + 8 + 4])).cuda()
+    out = torch.full_like(local, 5.0)
+    plan.run_slab([local, out], 8, 16, 24)
+    torch.cuda.synchronize()
+    got = out.cpu().numpy()
+    assert np.array_equal(bits(got[2:-2]), bits(ref[10:18]))
+    assert np.all(got[:2, 2:-2] == 5.0) and np.all(got[-2:, 2:-2] == 5.0)
