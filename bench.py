@@ -168,9 +168,10 @@ def cpu_runner(name, w):
         img = w["gen"](sizes)[0]
         return (lambda: oracle.box(img, fused=True, threads=threads)), int(np.prod(sizes)), threads, \
             f"1 pass of {'x'.join(map(str, sizes))}"
-    nj = max(64, min(sizes[0], 256))  # hydro: a full-width row band, 1 step
+    nj = max(16, min(sizes[0], 64))  # hydro: a full-width row band, 1 step
     st = w["gen"]((nj, sizes[1]))
-    return (lambda: oracle.hydro(st[:4], float(st[4][0]), 1, fused=True, threads=threads)), nj * sizes[1], \
+    outs = [np.empty_like(a) for a in st[:4]]
+    return (lambda: oracle.hydro_step(st[:4], outs, float(st[4][0]), threads=threads)), nj * sizes[1], \
         threads, f"1 step of a {nj}x{sizes[1]} row band"
 
 

@@ -48,6 +48,7 @@ def lib() -> ctypes.CDLL:
             PP = ctypes.POINTER(ctypes.c_void_p)
             L.lfo_hydro_naive.argtypes = [PP, PP, Lg, Lg, ctypes.c_double, I]
             L.lfo_hydro_fused.argtypes = [PP, PP, Lg, Lg, ctypes.c_double, I, I]
+            L.lfo_hydro_fused_step.argtypes = [PP, PP, Lg, Lg, ctypes.c_double, I]
             L.lfo_hydro_flops_per_cell.restype = ctypes.c_long
         _lib = L
     return _lib
@@ -126,6 +127,14 @@ def hydro(state, dtdx: float, steps: int, fused: bool = False, threads: int = 0)
     else:
         _ok(lib().lfo_hydro_naive(pin, pout, nj, ni, dtdx, steps))
     return outs
+
+
+def hydro_step(state, outs, dtdx: float, threads: int = 0) -> None:
+    """One fused CPU step in -> out with no copies (the CPU-baseline unit)."""
+    nj, ni = state[0].shape[0] - 4, state[0].shape[1] - 4
+    PA = ctypes.c_void_p * 4
+    _ok(lib().lfo_hydro_fused_step(PA(*[_p(a) for a in state]), PA(*[_p(a) for a in outs]), nj, ni, dtdx,
+                                   threads))
 
 
 def hydro_flops_per_cell() -> int:

@@ -60,6 +60,8 @@ int lfo_hydro_naive(const double* const in[4], double* const out[4], long nj, lo
                     double dtdx, int steps);
 int lfo_hydro_fused(const double* const in[4], double* const out[4], long nj, long ni,
                     double dtdx, int steps, int threads);
+int lfo_hydro_fused_step(const double* const in[4], double* const out[4], long nj, long ni,
+                         double dtdx, int threads);
 /* counts double-precision operations of one cell-step of the hydro chain */
 long lfo_hydro_flops_per_cell(void);
 

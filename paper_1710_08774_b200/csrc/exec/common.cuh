@@ -55,7 +55,9 @@ __device__ __forceinline__ void tma_prefetch_desc(const CUtensorMap* map) {
 }
 
 // 2D / 3D tiled TMA loads into CTA shared memory, completing on `bar`.
-// Coordinates are element indices, innermost first.
+// Coordinates are element indices, innermost first.  The box origin along the
+// contiguous dimension must be 16-B aligned (an odd fp64 column faults with
+// "illegal instruction" on sm_100a); destinations are 128-B aligned slots.
 __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
   asm volatile(
       "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(

@@ -1,0 +1,314 @@
+// Fused sm_100a executor for the Hydro2D step (BASELINE.json configs[2] and
+// configs[4]; specs/hydro2d.lf): x-sweep chain then y-sweep chain, fused into
+// ONE pass over the grid, fp64 SoA state (rho, rho*u, rho*v, E), reflective
+// walls.
+//
+// The planner fuses all 12 kernel rules into one (j, i) nest: the x-swept
+// state rho1..en1 is an intermediate with a 5-row window and every x/y
+// intermediate is contracted.  The executor realises exactly that:
+//   * a CTA of 128 threads owns a strip of 127 cells and marches its rows;
+//     rows of the four state arrays arrive by TMA (4 tensor maps, 2 rows per
+//     stage, 4-slot mbarrier ring);
+//   * x-sweep of a row through shared memory: prims (131 columns), slope +
+//     trace (129), Riemann + flux on exactly 128 faces -- one face per thread,
+//     so the expensive solver never runs a partial warp -- then the update;
+//   * thread t keeps column i0+t's y-sweep in registers: the x-swept state,
+//     prims, the plus-face trace state and the previous face flux are rolling
+//     windows along j, one y-face Riemann solve per row per thread;
+//   * the new state leaves once (64 B per cell-step of HBM traffic), with the
+//     reflective ghost ring written by the owners of the mirrored cells.
+#include <algorithm>
+
+#include "../../userkernels/hydro_kernels.h"
+#include "common.cuh"
+#include "exec.hpp"
+#include "rowstream.cuh"
+
+namespace lfx {
+namespace {
+
+constexpr int NT = 128;                // threads per CTA = x-faces per row
+constexpr int W = NT - 1;              // cells per strip
+constexpr int H = 2;                   // radius of each sweep
+constexpr int BOXW = 132;              // staged columns from the even storage column <= i0 (131 used)
+constexpr int R = 2;                   // rows per stage
+constexpr int S = 4;                   // ring slots
+constexpr int ARR_TX = BOXW * R * 8;   // bytes TMA delivers per array per stage
+constexpr int ARR_BYTES = (ARR_TX + 127) / 128 * 128;  // 128-B aligned array slots
+constexpr int STAGE_TX = 4 * ARR_TX;
+constexpr int STAGE_BYTES = 4 * ARR_BYTES;
+constexpr int NPRIM = W + 4;           // 131 prim columns
+constexpr int NQ = W + 2;              // 129 trace columns
+constexpr int XBUF = 4 * NPRIM + 8 * NQ + 4 * NT;  // doubles per x-sweep buffer
+constexpr int SMEM = S * STAGE_BYTES + 2 * XBUF * 8 + S * 8 + 128;
+
+struct Params {
+  int ni, nj;            // interior of this launch (slab rows for multi-GPU)
+  long long pitch;       // ni + 4
+  int strips;
+  int ghost_top, ghost_bottom;  // refill reflective ghost rows at these faces
+  const double* dtdx;    // rank-0 terminal g_dtdx
+  double* out[4];
+};
+
+struct Maps {
+  CUtensorMap m[4];
+};
+
+__device__ __forceinline__ void store_cell(const Params& p, int j, int i, const double v[4]) {
+  // interior value plus its reflective images in the ghost ring
+  const long long P = p.pitch;
+  const long long base = (long long)(j + H) * P + (i + H);
+#pragma unroll
+  for (int a = 0; a < 4; ++a) p.out[a][base] = v[a];
+  int im = -100, jm = -100;
+  if (i < H) im = -1 - i;
+  if (i >= p.ni - H) im = 2 * p.ni - 1 - i;
+  if (p.ghost_top && j < H) jm = -1 - j;
+  if (p.ghost_bottom && j >= p.nj - H) jm = 2 * p.nj - 1 - j;
+  if (im != -100) {
+    const long long g = (long long)(j + H) * P + (im + H);
+    p.out[0][g] = v[0];
+    p.out[1][g] = -v[1];  // rho*u odd across i-faces
+    p.out[2][g] = v[2];
+    p.out[3][g] = v[3];
+  }
+  if (jm != -100) {
+    const long long g = (long long)(jm + H) * P + (i + H);
+    p.out[0][g] = v[0];
+    p.out[1][g] = v[1];
+    p.out[2][g] = -v[2];  // rho*v odd across j-faces
+    p.out[3][g] = v[3];
+    if (im != -100) {
+      const long long c = (long long)(jm + H) * P + (im + H);
+      p.out[0][c] = v[0];
+      p.out[1][c] = -v[1];
+      p.out[2][c] = -v[2];
+      p.out[3][c] = v[3];
+    }
+  }
+}
+
+__global__ void __launch_bounds__(NT, 2) hydro_fused(const __grid_constant__ Maps maps, const Params p) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  unsigned char* ring = smem;
+  double* xb0 = reinterpret_cast<double*>(smem + S * STAGE_BYTES);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + S * STAGE_BYTES + 2 * XBUF * 8);
+  const int t = threadIdx.x;
+  const double dtdx = *p.dtdx;
+
+  // ---- segment list (strip-major row ranges) and stage bookkeeping
+  RowSeg seg[3];
+  const int nseg = cta_segments(blockIdx.x, gridDim.x, p.strips, p.nj, seg);
+  int nst[3], total = 0;
+  for (int k = 0; k < nseg; ++k) {
+    nst[k] = (seg[k].je - seg[k].jb + 2 * H + R - 1) / R;
+    total += nst[k];
+  }
+  auto issue = [&](int g) {
+    if (g >= total) return;
+    int k = 0, gg = g;
+    while (gg >= nst[k]) gg -= nst[k++];
+    const int slot = g % S;
+    unsigned char* dst = ring + slot * STAGE_BYTES;
+    fence_proxy_async();
+    mbar_arrive_expect_tx(&full[slot], STAGE_TX);
+    // storage col of logical i0-2, rounded down to an even column: TMA box
+    // origins must be 16-B aligned along the contiguous dimension
+    const int c0 = (seg[k].strip * W) & ~1;
+    const int r0 = seg[k].jb - H + gg * R + H; // storage row of the stage's first row
+#pragma unroll
+    for (int a = 0; a < 4; ++a) tma_load_2d(dst + a * ARR_BYTES, &maps.m[a], &full[slot], c0, r0);
+  };
+  if (t == 0) {
+    for (int s = 0; s < S; ++s) mbar_init(&full[s], 1);
+    fence_barrier_init();
+    for (int a = 0; a < 4; ++a) tma_prefetch_desc(&maps.m[a]);
+    for (int g = 0; g < S; ++g) issue(g);
+  }
+  __syncthreads();
+
+  int g = 0, pending = -1;
+  for (int k = 0; k < nseg; ++k) {
+    const RowSeg sg = seg[k];
+    const int i0 = sg.strip * W;
+    const int off = i0 & 1;                  // staged column of logical i0-2 (see issue())
+    const int ncell = min(W, p.ni - i0);     // cells of this strip
+    const bool owns = t < ncell;
+    const int T = sg.je - sg.jb + 2 * H;     // marched rows jb-2 .. je+1
+    // y-sweep windows of column i0 + t
+    double yq1[4], yq2[4];  // prims of rows r-1, r-2
+    double ypp[4];          // plus-face trace state of row r-2
+    double yfp[4];          // flux of face (r-3)+1/2
+    double u1a[4], u1b[4];  // x-swept state rows r-1, r-2
+    for (int tt = 0; tt < T; ++tt) {
+      const int tr = tt % R;
+      if (tr == 0) mbar_wait(&full[g % S], (g / S) & 1);
+      const double* st = reinterpret_cast<const double*>(ring + (g % S) * STAGE_BYTES);
+      const double* row[4];
+#pragma unroll
+      for (int a = 0; a < 4; ++a) row[a] = st + a * (ARR_BYTES / 8) + tr * BOXW + off;
+      double* xb = xb0 + (tt & 1) * XBUF;
+      double* xq = xb;                  // [4][NPRIM]  prims, column c <-> logical i0-2+c
+      double* xm = xq + 4 * NPRIM;      // [4][NQ]     minus-face states, c <-> i0-1+c
+      double* xp = xm + 4 * NQ;         // [4][NQ]     plus-face states
+      double* xf = xp + 4 * NQ;         // [4][NT]     face fluxes, face c <-> (i0-1+c)+1/2
+
+      // ---- x: conservative -> primitive on 131 columns
+      for (int c = t; c < NPRIM; c += NT)
+        hy_constoprim(row[0][c], row[1][c], row[2][c], row[3][c], &xq[c], &xq[NPRIM + c], &xq[2 * NPRIM + c],
+                      &xq[3 * NPRIM + c]);
+      __syncthreads();
+      if (pending >= 0) {  // every thread is past the last read of stage `pending`
+        if (t == 0) issue(pending + S);
+        pending = -1;
+      }
+      // ---- x: slope + trace on 129 columns
+      for (int c = t; c < NQ; c += NT) {
+        double d[4];
+        hy_slope(xq[c], xq[NPRIM + c], xq[2 * NPRIM + c], xq[3 * NPRIM + c], xq[c + 1], xq[NPRIM + c + 1],
+                 xq[2 * NPRIM + c + 1], xq[3 * NPRIM + c + 1], xq[c + 2], xq[NPRIM + c + 2],
+                 xq[2 * NPRIM + c + 2], xq[3 * NPRIM + c + 2], &d[0], &d[1], &d[2], &d[3]);
+        hy_trace(xq[c + 1], xq[NPRIM + c + 1], xq[2 * NPRIM + c + 1], xq[3 * NPRIM + c + 1], d[0], d[1], d[2], d[3],
+                 dtdx, &xm[c], &xm[NQ + c], &xm[2 * NQ + c], &xm[3 * NQ + c], &xp[c], &xp[NQ + c],
+                 &xp[2 * NQ + c], &xp[3 * NQ + c]);
+      }
+      __syncthreads();
+      // ---- x: one Riemann solve + flux per thread (face t between cells i0-1+t and i0+t)
+      {
+        double gs[4];
+        hy_riemann(xp[t], xp[NQ + t], xp[2 * NQ + t], xp[3 * NQ + t], xm[t + 1], xm[NQ + t + 1],
+                   xm[2 * NQ + t + 1], xm[3 * NQ + t + 1], &gs[0], &gs[1], &gs[2], &gs[3]);
+        hy_flux(gs[0], gs[1], gs[2], gs[3], &xf[t], &xf[NT + t], &xf[2 * NT + t], &xf[3 * NT + t]);
+      }
+      __syncthreads();
+      if (tr == R - 1 || tt == T - 1) {
+        pending = g;
+        ++g;
+      }
+      if (!owns) continue;  // whole-warp uniform except in the strip's last warp
+      // ---- x: update of cell i0+t -> x-swept state of row r (rho1, mx1, my1, en1)
+      double u1[4];
+      hy_update(row[0][t + 2], row[1][t + 2], row[2][t + 2], row[3][t + 2], xf[t], xf[NT + t], xf[2 * NT + t],
+                xf[3 * NT + t], xf[t + 1], xf[NT + t + 1], xf[2 * NT + t + 1], xf[3 * NT + t + 1], dtdx, &u1[0],
+                &u1[1], &u1[2], &u1[3]);
+      // ---- y: prims of row r (normal momentum rho*v)
+      double yq[4];
+      hy_constoprim(u1[0], u1[2], u1[1], u1[3], &yq[0], &yq[1], &yq[2], &yq[3]);
+      if (tt >= 2) {
+        double d[4], ym[4], yp[4];
+        hy_slope(yq2[0], yq2[1], yq2[2], yq2[3], yq1[0], yq1[1], yq1[2], yq1[3], yq[0], yq[1], yq[2], yq[3], &d[0],
+                 &d[1], &d[2], &d[3]);
+        hy_trace(yq1[0], yq1[1], yq1[2], yq1[3], d[0], d[1], d[2], d[3], dtdx, &ym[0], &ym[1], &ym[2], &ym[3],
+                 &yp[0], &yp[1], &yp[2], &yp[3]);
+        if (tt >= 3) {
+          // face (r-2)+1/2 between rows r-2 (plus side) and r-1 (minus side)
+          double gs[4], f[4];
+          hy_riemann(ypp[0], ypp[1], ypp[2], ypp[3], ym[0], ym[1], ym[2], ym[3], &gs[0], &gs[1], &gs[2], &gs[3]);
+          hy_flux(gs[0], gs[1], gs[2], gs[3], &f[0], &f[1], &f[2], &f[3]);
+          if (tt >= 4) {
+            // update of row r-2 from faces (r-3)+1/2 and (r-2)+1/2
+            double o[4];
+            hy_update(u1b[0], u1b[2], u1b[1], u1b[3], yfp[0], yfp[1], yfp[2], yfp[3], f[0], f[1], f[2], f[3],
+                      dtdx, &o[0], &o[2], &o[1], &o[3]);
+            store_cell(p, sg.jb - 2 + tt - 2, i0 + t, o);
+          }
+#pragma unroll
+          for (int a = 0; a < 4; ++a) yfp[a] = f[a];
+        }
+#pragma unroll
+        for (int a = 0; a < 4; ++a) ypp[a] = yp[a];
+      }
+#pragma unroll
+      for (int a = 0; a < 4; ++a) {
+        yq2[a] = yq1[a];
+        yq1[a] = yq[a];
+        u1b[a] = u1a[a];
+        u1a[a] = u1[a];
+      }
+    }
+  }
+}
+
+bool supports(const lf::Plan& plan, std::string& why) {
+  const auto& r = plan.rs.ranges;
+  for (const auto& rg : r)
+    if (rg.stride != 1) {
+      why = "hydro executor needs unit strides";
+      return false;
+    }
+  long nj = r[0].trips(), ni = r[1].trips();
+  if (ni < 4 || nj < 4 || (ni + 4) * 8 % 16) {
+    why = "hydro executor needs N_i, N_j >= 4 and an even N_i (got " + std::to_string(nj) + "x" +
+          std::to_string(ni) + ")";
+    return false;
+  }
+  return true;
+}
+
+int launch_step(const double* const in[4], double* const out[4], const double* dtdx, int ni, int nj, bool top,
+                bool bottom, cudaStream_t st, std::string& err) {
+  static int slots = 0;
+  if (!slots) {
+    cudaError_t e = cudaFuncSetAttribute(hydro_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
+    if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(hydro)", err);
+    int dev = 0, sms = 148, per_sm = 1;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, hydro_fused, NT, SMEM);
+    slots = sms * std::max(1, per_sm);
+  }
+  Maps maps;
+  uint64_t dims[2] = {(uint64_t)ni + 4, (uint64_t)nj + 4};
+  uint32_t box[2] = {BOXW, R};
+  for (int a = 0; a < 4; ++a)
+    if (!make_tensor_map(&maps.m[a], in[a], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 8, 2, dims, box, err))
+      return LF_ERR_CUDA;
+  Params p;
+  p.ni = ni;
+  p.nj = nj;
+  p.pitch = ni + 4;
+  p.strips = (ni + W - 1) / W;
+  p.ghost_top = top;
+  p.ghost_bottom = bottom;
+  p.dtdx = dtdx;
+  for (int a = 0; a < 4; ++a) p.out[a] = out[a];
+  const long long work = (long long)p.strips * nj;
+  const int ctas = static_cast<int>(std::max<long long>(1, std::min<long long>(slots, work / 8)));
+  hydro_fused<<<ctas, NT, SMEM, st>>>(maps, p);
+  return cuda_status(cudaGetLastError(), "hydro_fused launch", err);
+}
+
+int run(const ExecArgs& a, std::string& err) {
+  const auto& r = a.plan->rs.ranges;
+  int nj = (int)r[0].trips(), ni = (int)r[1].trips();
+  bool top = true, bottom = true;
+  if (a.slab) {
+    nj = (int)(a.slab->hi - a.slab->lo);
+    top = a.slab->lo == 0;
+    bottom = a.slab->hi == a.slab->global;
+  }
+  // terminals: g_rho g_mx g_my g_E g_dtdx | g_rho_n g_mx_n g_my_n g_E_n
+  const double* src[4];
+  double* goal[4];
+  double* scr[4] = {nullptr, nullptr, nullptr, nullptr};
+  for (int v = 0; v < 4; ++v) {
+    src[v] = static_cast<const double*>(a.terms[v]);
+    goal[v] = static_cast<double*>(a.terms[5 + v]);
+    if (a.steps > 1) scr[v] = static_cast<double*>(a.scratch[v]);
+  }
+  const double* dtdx = static_cast<const double*>(a.terms[4]);
+  for (int s = 0; s < a.steps; ++s) {
+    double* const* dst = ((a.steps - 1 - s) % 2) == 0 ? goal : scr;
+    int stt = launch_step(src, dst, dtdx, ni, nj, top, bottom, a.stream, err);
+    if (stt != LF_OK) return stt;
+    for (int v = 0; v < 4; ++v) src[v] = dst[v];
+  }
+  return LF_OK;
+}
+
+}  // namespace
+
+extern const Executor hydro_executor = {"hydro2d_fused_tma", "hydro2d.lf", 1, 64.0, supports, run};
+
+}  // namespace lfx

@@ -1,0 +1,168 @@
+/*
+ * User kernels of the Hydro2D chain (BASELINE.json configs[2] / configs[4]):
+ * compressible Euler, MUSCL-Hancock Godunov scheme, directionally split,
+ * gamma = 1.4, fp64.  Authored from textbook numerics for this framework (the
+ * CEA Hydro2D sources are not part of the reference snapshot).
+ *
+ * Each sweep is the six-kernel chain the paper describes (R/PAPER.md:468-486):
+ *   constoprim -> slope (minmod) -> trace (half-step predictor) ->
+ *   riemann (two-shock iterative solver, fixed 10 Newton steps) ->
+ *   flux -> update (conservative)
+ * written for a generic "normal" direction: (r, mn, mt, e) = density, normal
+ * momentum, transverse momentum, total energy.  The x-sweep passes
+ * (rho, rho*u, rho*v, E) and the y-sweep (rho, rho*v, rho*u, E).
+ *
+ * As with stencil_kernels.h, the same source runs in the CPU oracle and is
+ * inlined into the sm_100a executor.  Only + - * / sqrt fabs and comparisons
+ * are used (all correctly rounded on both sides), fixed iteration counts, no
+ * early exits -- so the two schedules agree bit for bit.
+ */
+#ifndef LF_USERKERNELS_HYDRO_H
+#define LF_USERKERNELS_HYDRO_H
+
+#if defined(__CUDACC__)
+#define LF_HD __host__ __device__ __forceinline__
+#else
+#include <math.h>
+#define LF_HD static inline
+#endif
+
+#define HY_GAMMA 1.4
+#define HY_SMALLR 1e-10
+#define HY_SMALLP 1e-12
+#define HY_SMALLC 1e-10
+#define HY_NITER 10
+
+LF_HD double hy_max(double a, double b) { return a > b ? a : b; }
+LF_HD double hy_min(double a, double b) { return a < b ? a : b; }
+
+/* conservative -> primitive (density, normal & transverse velocity, pressure) */
+LF_HD void hy_constoprim(double r, double mn, double mt, double e, double* qr, double* qn, double* qt,
+                         double* qp) {
+  const double rr = hy_max(r, HY_SMALLR);
+  const double inv = 1.0 / rr;
+  const double un = mn * inv;
+  const double ut = mt * inv;
+  const double ek = 0.5 * rr * (un * un + ut * ut);
+  *qr = rr;
+  *qn = un;
+  *qt = ut;
+  *qp = hy_max((HY_GAMMA - 1.0) * (e - ek), HY_SMALLP);
+}
+
+/* minmod-limited slope from the left and right differences */
+LF_HD double hy_minmod(double dl, double dr) {
+  if (dl * dr <= 0.0) return 0.0;
+  return fabs(dl) < fabs(dr) ? dl : dr;
+}
+
+LF_HD void hy_slope(double rm, double nm, double tm, double pm, double r0, double n0, double t0, double p0,
+                    double rp, double np, double tp, double pp, double* dr, double* dn, double* dt, double* dp) {
+  *dr = hy_minmod(r0 - rm, rp - r0);
+  *dn = hy_minmod(n0 - nm, np - n0);
+  *dt = hy_minmod(t0 - tm, tp - t0);
+  *dp = hy_minmod(p0 - pm, pp - p0);
+}
+
+/* MUSCL-Hancock predictor: evolve the cell's primitive state by half a time
+ * step with the primitive Euler equations, then extrapolate to the left
+ * (minus) and right (plus) faces. */
+LF_HD void hy_trace(double r, double n, double t, double p, double dr, double dn, double dt, double dp,
+                    double dtdx, double* mr, double* mn, double* mt, double* mp, double* pr, double* pn,
+                    double* pt, double* pp) {
+  const double h = -0.5 * dtdx;
+  const double sr = h * (n * dr + r * dn);
+  const double sn = h * (n * dn + dp / r);
+  const double st = h * (n * dt);
+  const double sp = h * (n * dp + HY_GAMMA * p * dn);
+  *mr = hy_max(r - 0.5 * dr + sr, HY_SMALLR);
+  *mn = n - 0.5 * dn + sn;
+  *mt = t - 0.5 * dt + st;
+  *mp = hy_max(p - 0.5 * dp + sp, HY_SMALLP);
+  *pr = hy_max(r + 0.5 * dr + sr, HY_SMALLR);
+  *pn = n + 0.5 * dn + sn;
+  *pt = t + 0.5 * dt + st;
+  *pp = hy_max(p + 0.5 * dp + sp, HY_SMALLP);
+}
+
+/* Godunov state at a face from left/right primitive states: two-shock
+ * approximation of the exact Riemann problem, p* by HY_NITER Newton steps on
+ * the Lagrangian wave speeds, then sampling at x/t = 0 with a linear fan. */
+LF_HD void hy_riemann(double rl, double nl, double tl, double pl, double rr, double nr, double tr, double pr,
+                      double* gr, double* gn, double* gt, double* gp) {
+  const double k = (HY_GAMMA + 1.0) / (2.0 * HY_GAMMA);
+  const double cl = sqrt(HY_GAMMA * pl * rl); /* Lagrangian sound speeds rho*c */
+  const double cr = sqrt(HY_GAMMA * pr * rr);
+  const double ipl = 1.0 / pl, ipr = 1.0 / pr;
+  double ps = hy_max((cr * pl + cl * pr + cl * cr * (nl - nr)) / (cl + cr), HY_SMALLP);
+  for (int it = 0; it < HY_NITER; ++it) {
+    const double wl = cl * sqrt(1.0 + k * (ps - pl) * ipl);
+    const double wr = cr * sqrt(1.0 + k * (ps - pr) * ipr);
+    const double zl = 2.0 * wl * wl * wl / (wl * wl + cl * cl);
+    const double zr = 2.0 * wr * wr * wr / (wr * wr + cr * cr);
+    const double usl = nl - (ps - pl) / wl;
+    const double usr = nr + (ps - pr) / wr;
+    ps = hy_max(ps + zl * zr / (zl + zr) * (usl - usr), HY_SMALLP);
+  }
+  const double wl = cl * sqrt(1.0 + k * (ps - pl) * ipl);
+  const double wr = cr * sqrt(1.0 + k * (ps - pr) * ipr);
+  const double us = (wl * nl + wr * nr + pl - pr) / (wl + wr);
+  const int left = us > 0.0;
+  const double ro = left ? rl : rr;
+  const double uo = left ? nl : -nr; /* velocity along the sampled wave direction */
+  const double po = left ? pl : pr;
+  const double wo = left ? wl : wr;
+  const double to = left ? tl : tr;
+  const double uss = left ? us : -us;
+  const double co = sqrt(HY_GAMMA * po / ro);
+  const double rstar = hy_max(ro / (1.0 + ro * (po - ps) / (wo * wo)), HY_SMALLR);
+  const double cstar = sqrt(HY_GAMMA * ps / rstar);
+  double spout = co - uo;
+  double spin = cstar - uss;
+  if (ps >= po) {
+    const double ushock = wo / ro - uo;
+    spout = ushock;
+    spin = ushock;
+  }
+  const double scr = hy_max(spout - spin, HY_SMALLC + fabs(spout + spin));
+  const double frac = hy_min(hy_max(0.5 * (1.0 + (spout + spin) / scr), 0.0), 1.0);
+  double r = frac * rstar + (1.0 - frac) * ro;
+  double u = frac * uss + (1.0 - frac) * uo;
+  double p = frac * ps + (1.0 - frac) * po;
+  if (spout < 0.0) {
+    r = ro;
+    u = uo;
+    p = po;
+  }
+  if (spin > 0.0) {
+    r = rstar;
+    u = uss;
+    p = ps;
+  }
+  *gr = r;
+  *gn = left ? u : -u;
+  *gt = to;
+  *gp = p;
+}
+
+/* conservative flux through the face from the Godunov state */
+LF_HD void hy_flux(double r, double n, double t, double p, double* fr, double* fn, double* ft, double* fe) {
+  const double m = r * n;
+  const double et = p * (1.0 / (HY_GAMMA - 1.0)) + 0.5 * r * (n * n + t * t);
+  *fr = m;
+  *fn = m * n + p;
+  *ft = m * t;
+  *fe = n * (et + p);
+}
+
+/* conservative update of one cell from its two face fluxes */
+LF_HD void hy_update(double r, double mn, double mt, double e, double frm, double fnm, double ftm, double fem,
+                     double frp, double fnp, double ftp, double fep, double dtdx, double* ro, double* no,
+                     double* to, double* eo) {
+  *ro = r + dtdx * (frm - frp);
+  *no = mn + dtdx * (fnm - fnp);
+  *to = mt + dtdx * (ftm - ftp);
+  *eo = e + dtdx * (fem - fep);
+}
+
+#endif
