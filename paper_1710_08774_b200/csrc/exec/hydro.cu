@@ -18,6 +18,7 @@
 //   * the new state leaves once (64 B per cell-step of HBM traffic), with the
 //     reflective ghost ring written by the owners of the mirrored cells.
 #include <algorithm>
+#include <cstdlib>
 
 #include "../../userkernels/hydro_kernels.h"
 #include "common.cuh"
@@ -32,7 +33,7 @@ constexpr int W = NT - 1;              // cells per strip
 constexpr int H = 2;                   // radius of each sweep
 constexpr int BOXW = 132;              // staged columns from the even storage column <= i0 (131 used)
 constexpr int R = 2;                   // rows per stage
-constexpr int S = 4;                   // ring slots
+constexpr int S = 3;                   // ring slots (compute per row >> load latency)
 constexpr int ARR_TX = BOXW * R * 8;   // bytes TMA delivers per array per stage
 constexpr int ARR_BYTES = (ARR_TX + 127) / 128 * 128;  // 128-B aligned array slots
 constexpr int STAGE_TX = 4 * ARR_TX;
@@ -40,7 +41,7 @@ constexpr int STAGE_BYTES = 4 * ARR_BYTES;
 constexpr int NPRIM = W + 4;           // 131 prim columns
 constexpr int NQ = W + 2;              // 129 trace columns
 constexpr int XBUF = 4 * NPRIM + 8 * NQ + 4 * NT;  // doubles per x-sweep buffer
-constexpr int SMEM = S * STAGE_BYTES + 2 * XBUF * 8 + S * 8 + 128;
+constexpr int SMEM = S * STAGE_BYTES + XBUF * 8 + S * 8 + 128;
 
 struct Params {
   int ni, nj;            // interior of this launch (slab rows for multi-GPU)
@@ -89,11 +90,12 @@ __device__ __forceinline__ void store_cell(const Params& p, int j, int i, const 
   }
 }
 
-__global__ void __launch_bounds__(NT, 2) hydro_fused(const __grid_constant__ Maps maps, const Params p) {
+template <int MINB>
+__global__ void __launch_bounds__(NT, MINB) hydro_fused(const __grid_constant__ Maps maps, const Params p) {
   extern __shared__ __align__(128) unsigned char smem[];
   unsigned char* ring = smem;
   double* xb0 = reinterpret_cast<double*>(smem + S * STAGE_BYTES);
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + S * STAGE_BYTES + 2 * XBUF * 8);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + S * STAGE_BYTES + XBUF * 8);
   const int t = threadIdx.x;
   const double dtdx = *p.dtdx;
 
@@ -102,7 +104,7 @@ __global__ void __launch_bounds__(NT, 2) hydro_fused(const __grid_constant__ Map
   const int nseg = cta_segments(blockIdx.x, gridDim.x, p.strips, p.nj, seg);
   int nst[3], total = 0;
   for (int k = 0; k < nseg; ++k) {
-    nst[k] = (seg[k].je - seg[k].jb + 2 * H + R - 1) / R;
+    nst[k] = (seg[k].je - seg[k].jb + 2 * H + 1 + R - 1) / R;  // marched rows jb-2 .. je+2
     total += nst[k];
   }
   auto issue = [&](int g) {
@@ -135,12 +137,21 @@ __global__ void __launch_bounds__(NT, 2) hydro_fused(const __grid_constant__ Map
     const int off = i0 & 1;                  // staged column of logical i0-2 (see issue())
     const int ncell = min(W, p.ni - i0);     // cells of this strip
     const bool owns = t < ncell;
-    const int T = sg.je - sg.jb + 2 * H;     // marched rows jb-2 .. je+1
-    // y-sweep windows of column i0 + t
-    double yq1[4], yq2[4];  // prims of rows r-1, r-2
-    double ypp[4];          // plus-face trace state of row r-2
-    double yfp[4];          // flux of face (r-3)+1/2
-    double u1a[4], u1b[4];  // x-swept state rows r-1, r-2
+    // marched rows r = jb-2 .. je+2: the y-sweep lags the x-sweep by three rows
+    // so that the y-face Riemann solve of a column can run next to the x-face
+    // solve of the same thread (two independent dependency chains per thread)
+    const int T = sg.je - sg.jb + 2 * H + 1;
+    // y-sweep windows of column i0 + t (indices relative to the marched row r)
+    double yq1[4], yq2[4];    // prims of rows r-1, r-2
+    double yqm[4];            // minus-face trace state of row r-2 (read at C of row r+... see below)
+    double ypo[4], ypn[4];    // plus-face trace states of rows r-3 and r-2
+    double yfp[4];            // flux of face (r-4)+1/2
+    double u1a[4], u1b[4], u1c[4];  // x-swept state rows r-1, r-2, r-3
+    // benign states for the dummy y-problems before the pipeline fills
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+      ypo[a] = ypn[a] = yqm[a] = (a == 0 || a == 3) ? 1.0 : 0.0;
+    }
     for (int tt = 0; tt < T; ++tt) {
       const int tr = tt % R;
       if (tr == 0) mbar_wait(&full[g % S], (g / S) & 1);
@@ -148,13 +159,16 @@ __global__ void __launch_bounds__(NT, 2) hydro_fused(const __grid_constant__ Map
       const double* row[4];
 #pragma unroll
       for (int a = 0; a < 4; ++a) row[a] = st + a * (ARR_BYTES / 8) + tr * BOXW + off;
-      double* xb = xb0 + (tt & 1) * XBUF;
+      // one x-buffer suffices: A writes prims (last read in B of the previous row),
+      // B writes face states (read in C), C writes fluxes (read in D) -- each
+      // write is separated from the previous row's reads by a __syncthreads
+      double* xb = xb0;
       double* xq = xb;                  // [4][NPRIM]  prims, column c <-> logical i0-2+c
       double* xm = xq + 4 * NPRIM;      // [4][NQ]     minus-face states, c <-> i0-1+c
       double* xp = xm + 4 * NQ;         // [4][NQ]     plus-face states
       double* xf = xp + 4 * NQ;         // [4][NT]     face fluxes, face c <-> (i0-1+c)+1/2
 
-      // ---- x: conservative -> primitive on 131 columns
+      // ---- A. x: conservative -> primitive on 131 columns
       for (int c = t; c < NPRIM; c += NT)
         hy_constoprim(row[0][c], row[1][c], row[2][c], row[3][c], &xq[c], &xq[NPRIM + c], &xq[2 * NPRIM + c],
                       &xq[3 * NPRIM + c]);
@@ -163,7 +177,7 @@ __global__ void __launch_bounds__(NT, 2) hydro_fused(const __grid_constant__ Map
         if (t == 0) issue(pending + S);
         pending = -1;
       }
-      // ---- x: slope + trace on 129 columns
+      // ---- B. x: slope + trace on 129 columns
       for (int c = t; c < NQ; c += NT) {
         double d[4];
         hy_slope(xq[c], xq[NPRIM + c], xq[2 * NPRIM + c], xq[3 * NPRIM + c], xq[c + 1], xq[NPRIM + c + 1],
@@ -174,12 +188,41 @@ __global__ void __launch_bounds__(NT, 2) hydro_fused(const __grid_constant__ Map
                  &xp[2 * NQ + c], &xp[3 * NQ + c]);
       }
       __syncthreads();
-      // ---- x: one Riemann solve + flux per thread (face t between cells i0-1+t and i0+t)
+      // ---- C. two independent Riemann solves per thread:
+      //   x-face t of row r (between cells i0-1+t and i0+t), and
+      //   y-face (r-3)+1/2 of column i0+t (plus state of row r-3, minus state of row r-2)
       {
-        double gs[4];
-        hy_riemann(xp[t], xp[NQ + t], xp[2 * NQ + t], xp[3 * NQ + t], xm[t + 1], xm[NQ + t + 1],
-                   xm[2 * NQ + t + 1], xm[3 * NQ + t + 1], &gs[0], &gs[1], &gs[2], &gs[3]);
-        hy_flux(gs[0], gs[1], gs[2], gs[3], &xf[t], &xf[NT + t], &xf[2 * NT + t], &xf[3 * NT + t]);
+        // both problems advance in one loop: two independent dependency chains
+        // per thread (the y-problem of a non-owning thread or of the pipeline's
+        // first rows is a benign dummy whose result is dropped)
+        const bool yface = owns && tt >= 4;
+        hy_rp cx, cy;
+        double psx = hy_riemann_init(xp[t], xp[NQ + t], xp[3 * NQ + t], xm[t + 1], xm[NQ + t + 1],
+                                     xm[3 * NQ + t + 1], &cx);
+        double psy = hy_riemann_init(ypo[0], ypo[1], ypo[3], yqm[0], yqm[1], yqm[3], &cy);
+#pragma unroll 2
+        for (int it = 0; it < HY_NITER; ++it) {
+          psx = hy_riemann_newton(&cx, psx);
+          psy = hy_riemann_newton(&cy, psy);
+        }
+        double gx[4], gy[4];
+        hy_riemann_sample(&cx, psx, xp[t], xp[2 * NQ + t], xm[t + 1], xm[2 * NQ + t + 1], &gx[0], &gx[1], &gx[2],
+                          &gx[3]);
+        hy_riemann_sample(&cy, psy, ypo[0], ypo[2], yqm[0], yqm[2], &gy[0], &gy[1], &gy[2], &gy[3]);
+        hy_flux(gx[0], gx[1], gx[2], gx[3], &xf[t], &xf[NT + t], &xf[2 * NT + t], &xf[3 * NT + t]);
+        if (yface) {
+          double f[4];
+          hy_flux(gy[0], gy[1], gy[2], gy[3], &f[0], &f[1], &f[2], &f[3]);
+          if (tt >= 5) {
+            // update of row r-3 from faces (r-4)+1/2 and (r-3)+1/2
+            double o[4];
+            hy_update(u1c[0], u1c[2], u1c[1], u1c[3], yfp[0], yfp[1], yfp[2], yfp[3], f[0], f[1], f[2], f[3],
+                      dtdx, &o[0], &o[2], &o[1], &o[3]);
+            store_cell(p, sg.jb - 2 + tt - 3, i0 + t, o);
+          }
+#pragma unroll
+          for (int a = 0; a < 4; ++a) yfp[a] = f[a];
+        }
       }
       __syncthreads();
       if (tr == R - 1 || tt == T - 1) {
@@ -187,42 +230,32 @@ __global__ void __launch_bounds__(NT, 2) hydro_fused(const __grid_constant__ Map
         ++g;
       }
       if (!owns) continue;  // whole-warp uniform except in the strip's last warp
-      // ---- x: update of cell i0+t -> x-swept state of row r (rho1, mx1, my1, en1)
+      // ---- D. x: update of cell i0+t -> x-swept state of row r; y: prims of row r,
+      //      slope + trace of row r-1
       double u1[4];
       hy_update(row[0][t + 2], row[1][t + 2], row[2][t + 2], row[3][t + 2], xf[t], xf[NT + t], xf[2 * NT + t],
                 xf[3 * NT + t], xf[t + 1], xf[NT + t + 1], xf[2 * NT + t + 1], xf[3 * NT + t + 1], dtdx, &u1[0],
                 &u1[1], &u1[2], &u1[3]);
-      // ---- y: prims of row r (normal momentum rho*v)
       double yq[4];
       hy_constoprim(u1[0], u1[2], u1[1], u1[3], &yq[0], &yq[1], &yq[2], &yq[3]);
       if (tt >= 2) {
-        double d[4], ym[4], yp[4];
+        double d[4], yp[4];
         hy_slope(yq2[0], yq2[1], yq2[2], yq2[3], yq1[0], yq1[1], yq1[2], yq1[3], yq[0], yq[1], yq[2], yq[3], &d[0],
                  &d[1], &d[2], &d[3]);
-        hy_trace(yq1[0], yq1[1], yq1[2], yq1[3], d[0], d[1], d[2], d[3], dtdx, &ym[0], &ym[1], &ym[2], &ym[3],
+        // minus state of row r-1 is read by the y-face (r-2)+1/2 at C of the next row
+        hy_trace(yq1[0], yq1[1], yq1[2], yq1[3], d[0], d[1], d[2], d[3], dtdx, &yqm[0], &yqm[1], &yqm[2], &yqm[3],
                  &yp[0], &yp[1], &yp[2], &yp[3]);
-        if (tt >= 3) {
-          // face (r-2)+1/2 between rows r-2 (plus side) and r-1 (minus side)
-          double gs[4], f[4];
-          hy_riemann(ypp[0], ypp[1], ypp[2], ypp[3], ym[0], ym[1], ym[2], ym[3], &gs[0], &gs[1], &gs[2], &gs[3]);
-          hy_flux(gs[0], gs[1], gs[2], gs[3], &f[0], &f[1], &f[2], &f[3]);
-          if (tt >= 4) {
-            // update of row r-2 from faces (r-3)+1/2 and (r-2)+1/2
-            double o[4];
-            hy_update(u1b[0], u1b[2], u1b[1], u1b[3], yfp[0], yfp[1], yfp[2], yfp[3], f[0], f[1], f[2], f[3],
-                      dtdx, &o[0], &o[2], &o[1], &o[3]);
-            store_cell(p, sg.jb - 2 + tt - 2, i0 + t, o);
-          }
 #pragma unroll
-          for (int a = 0; a < 4; ++a) yfp[a] = f[a];
+        for (int a = 0; a < 4; ++a) {
+          ypo[a] = ypn[a];  // plus state of row r-2 (for the face (r-2)+1/2 at the next row)
+          ypn[a] = yp[a];   // plus state of row r-1
         }
-#pragma unroll
-        for (int a = 0; a < 4; ++a) ypp[a] = yp[a];
       }
 #pragma unroll
       for (int a = 0; a < 4; ++a) {
         yq2[a] = yq1[a];
         yq1[a] = yq[a];
+        u1c[a] = u1b[a];
         u1b[a] = u1a[a];
         u1a[a] = u1[a];
       }
@@ -248,14 +281,20 @@ bool supports(const lf::Plan& plan, std::string& why) {
 
 int launch_step(const double* const in[4], double* const out[4], const double* dtdx, int ni, int nj, bool top,
                 bool bottom, cudaStream_t st, std::string& err) {
+  // LF_HYDRO_VARIANT: register budget for 2 / 3 / 4 (default) CTAs per SM: on
+  // this latency-bound fp64 code 4 resident CTAs beat the spill-free budget
+  static void (*kern)(Maps, Params) = nullptr;
   static int slots = 0;
   if (!slots) {
-    cudaError_t e = cudaFuncSetAttribute(hydro_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
+    const char* v = std::getenv("LF_HYDRO_VARIANT");
+    const int var = v ? std::atoi(v) : 2;
+    kern = var == 0 ? hydro_fused<2> : (var == 2 ? hydro_fused<4> : hydro_fused<3>);
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
     if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(hydro)", err);
     int dev = 0, sms = 148, per_sm = 1;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, hydro_fused, NT, SMEM);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NT, SMEM);
     slots = sms * std::max(1, per_sm);
   }
   Maps maps;
@@ -275,7 +314,7 @@ int launch_step(const double* const in[4], double* const out[4], const double* d
   for (int a = 0; a < 4; ++a) p.out[a] = out[a];
   const long long work = (long long)p.strips * nj;
   const int ctas = static_cast<int>(std::max<long long>(1, std::min<long long>(slots, work / 8)));
-  hydro_fused<<<ctas, NT, SMEM, st>>>(maps, p);
+  kern<<<ctas, NT, SMEM, st>>>(maps, p);
   return cuda_status(cudaGetLastError(), "hydro_fused launch", err);
 }
 

@@ -87,40 +87,66 @@ LF_HD void hy_trace(double r, double n, double t, double p, double dr, double dn
 
 /* Godunov state at a face from left/right primitive states: two-shock
  * approximation of the exact Riemann problem, p* by HY_NITER Newton steps on
- * the Lagrangian wave speeds, then sampling at x/t = 0 with a linear fan. */
-LF_HD void hy_riemann(double rl, double nl, double tl, double pl, double rr, double nr, double tr, double pr,
-                      double* gr, double* gn, double* gt, double* gp) {
+ * the Lagrangian wave speeds w = c*sqrt(1 + k (p*-p)/p), then sampling at
+ * x/t = 0 with a linear fan.  Written with reciprocals so that a Newton step
+ * costs 2 sqrt + 3 divisions: z = 2w^3/(w^2+c^2) enters only through
+ * z_l z_r / (z_l + z_r) = 1 / (1/z_l + 1/z_r).
+ *
+ * The solver is split into init / newton / sample so an executor can advance
+ * two independent problems in one loop (hy_riemann is exactly
+ * init + HY_NITER x newton + sample, so results are identical). */
+typedef struct {
+  double nl, pl, nr, pr;       /* normal velocities and pressures */
+  double cl, cr, cl2, cr2;     /* Lagrangian sound speeds rho*c and squares */
+  double kpl, kpr;             /* (gamma+1)/(2 gamma) / p */
+} hy_rp;
+
+LF_HD double hy_riemann_init(double rl, double nl, double pl, double rr, double nr, double pr, hy_rp* c) {
   const double k = (HY_GAMMA + 1.0) / (2.0 * HY_GAMMA);
-  const double cl = sqrt(HY_GAMMA * pl * rl); /* Lagrangian sound speeds rho*c */
-  const double cr = sqrt(HY_GAMMA * pr * rr);
-  const double ipl = 1.0 / pl, ipr = 1.0 / pr;
-  double ps = hy_max((cr * pl + cl * pr + cl * cr * (nl - nr)) / (cl + cr), HY_SMALLP);
-  for (int it = 0; it < HY_NITER; ++it) {
-    const double wl = cl * sqrt(1.0 + k * (ps - pl) * ipl);
-    const double wr = cr * sqrt(1.0 + k * (ps - pr) * ipr);
-    const double zl = 2.0 * wl * wl * wl / (wl * wl + cl * cl);
-    const double zr = 2.0 * wr * wr * wr / (wr * wr + cr * cr);
-    const double usl = nl - (ps - pl) / wl;
-    const double usr = nr + (ps - pr) / wr;
-    ps = hy_max(ps + zl * zr / (zl + zr) * (usl - usr), HY_SMALLP);
-  }
-  const double wl = cl * sqrt(1.0 + k * (ps - pl) * ipl);
-  const double wr = cr * sqrt(1.0 + k * (ps - pr) * ipr);
-  const double us = (wl * nl + wr * nr + pl - pr) / (wl + wr);
+  c->nl = nl;
+  c->pl = pl;
+  c->nr = nr;
+  c->pr = pr;
+  c->cl = sqrt(HY_GAMMA * pl * rl);
+  c->cr = sqrt(HY_GAMMA * pr * rr);
+  c->cl2 = c->cl * c->cl;
+  c->cr2 = c->cr * c->cr;
+  c->kpl = k / pl;
+  c->kpr = k / pr;
+  return hy_max((c->cr * pl + c->cl * pr + c->cl * c->cr * (nl - nr)) / (c->cl + c->cr), HY_SMALLP);
+}
+
+LF_HD double hy_riemann_newton(const hy_rp* c, double ps) {
+  const double wl = c->cl * sqrt(1.0 + c->kpl * (ps - c->pl));
+  const double wr = c->cr * sqrt(1.0 + c->kpr * (ps - c->pr));
+  const double iwl = 1.0 / wl, iwr = 1.0 / wr;
+  const double izl = 0.5 * (wl * wl + c->cl2) * (iwl * iwl * iwl); /* 1/z_l */
+  const double izr = 0.5 * (wr * wr + c->cr2) * (iwr * iwr * iwr);
+  const double usl = c->nl - (ps - c->pl) * iwl;
+  const double usr = c->nr + (ps - c->pr) * iwr;
+  return hy_max(ps + (usl - usr) / (izl + izr), HY_SMALLP);
+}
+
+LF_HD void hy_riemann_sample(const hy_rp* c, double ps, double rl, double tl, double rr, double tr, double* gr,
+                             double* gn, double* gt, double* gp) {
+  const double wl = c->cl * sqrt(1.0 + c->kpl * (ps - c->pl));
+  const double wr = c->cr * sqrt(1.0 + c->kpr * (ps - c->pr));
+  const double us = (wl * c->nl + wr * c->nr + c->pl - c->pr) / (wl + wr);
   const int left = us > 0.0;
   const double ro = left ? rl : rr;
-  const double uo = left ? nl : -nr; /* velocity along the sampled wave direction */
-  const double po = left ? pl : pr;
+  const double uo = left ? c->nl : -c->nr; /* velocity along the sampled wave direction */
+  const double po = left ? c->pl : c->pr;
   const double wo = left ? wl : wr;
   const double to = left ? tl : tr;
   const double uss = left ? us : -us;
-  const double co = sqrt(HY_GAMMA * po / ro);
+  const double iro = 1.0 / ro;
+  const double co = sqrt(HY_GAMMA * po * iro);
   const double rstar = hy_max(ro / (1.0 + ro * (po - ps) / (wo * wo)), HY_SMALLR);
   const double cstar = sqrt(HY_GAMMA * ps / rstar);
   double spout = co - uo;
   double spin = cstar - uss;
   if (ps >= po) {
-    const double ushock = wo / ro - uo;
+    const double ushock = wo * iro - uo;
     spout = ushock;
     spin = ushock;
   }
@@ -143,6 +169,14 @@ LF_HD void hy_riemann(double rl, double nl, double tl, double pl, double rr, dou
   *gn = left ? u : -u;
   *gt = to;
   *gp = p;
+}
+
+LF_HD void hy_riemann(double rl, double nl, double tl, double pl, double rr, double nr, double tr, double pr,
+                      double* gr, double* gn, double* gt, double* gp) {
+  hy_rp c;
+  double ps = hy_riemann_init(rl, nl, pl, rr, nr, pr, &c);
+  for (int it = 0; it < HY_NITER; ++it) ps = hy_riemann_newton(&c, ps);
+  hy_riemann_sample(&c, ps, rl, tl, rr, tr, gr, gn, gt, gp);
 }
 
 /* conservative flux through the face from the Godunov state */
