@@ -130,8 +130,11 @@ __global__ void __launch_bounds__(32, K::OCC)
     for (int s = 0; s < S; ++s) mbar_init(&full[s], 1);
     fence_barrier_init();
     tma_prefetch_desc(&tin);
-    for (int g = 0; g < S; ++g) rr.issue(g, &tin);
+    pdl_trigger();
   }
+  pdl_wait();  // previous step's output (our input) complete, our output buffer free
+  if (lane == 0)
+    for (int g = 0; g < S; ++g) rr.issue(g, &tin);
   __syncwarp();
 
   const uint64_t pol = l2_evict_first_policy();
@@ -248,8 +251,8 @@ int launch_step(const double* in, double* out, int ni, int nj, bool top, bool bo
   // at least ~16 rows per CTA so the 4 priming rows stay a small fraction
   const long long work = (long long)p.strips * nj;
   const int ctas = static_cast<int>(std::max<long long>(1, std::min<long long>(slots, work / 16)));
-  v.kernel<<<ctas, 32, v.smem, st>>>(map, out, p);
-  return cuda_status(cudaGetLastError(), "biharm_fused launch", err);
+  return cuda_status(launch_pdl(v.kernel, dim3(ctas), dim3(32), v.smem, st, map, out, p), "biharm_fused launch",
+                     err);
 }
 
 int run(const ExecArgs& a, std::string& err) {

@@ -8,7 +8,9 @@
 #include <cudaTypedefs.h>
 #include <stdint.h>
 
+#include <cstdlib>
 #include <string>
+#include <utility>
 
 namespace lfx {
 
@@ -116,9 +118,36 @@ __device__ __forceinline__ void st_stream4(float* p, float a, float b, float c, 
                : "memory");
 }
 
+// Programmatic dependent launch: let the next kernel in the stream be
+// scheduled while this one drains, and make every thread of the dependent
+// kernel wait for the previous grid (inputs written, buffers free) before its
+// first global access.
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 #endif  // __CUDACC__
 
 // ------------------------------------------------------------------ host
+#if defined(__CUDACC__)
+// launch with programmatic stream serialization (pairs with pdl_wait/trigger)
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                       Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  static const bool off = std::getenv("LF_NO_PDL") != nullptr;  // A/B switch for tuning runs
+  cfg.attrs = attr;
+  cfg.numAttrs = off ? 0 : 1;
+  return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
+#endif
+
 // Encode a row-major tensor map: dims[0] is the innermost (contiguous) one.
 bool make_tensor_map(CUtensorMap* map, const void* base, CUtensorMapDataType dtype, int elem_bytes, int rank,
                      const uint64_t* dims, const uint32_t* box, std::string& err);

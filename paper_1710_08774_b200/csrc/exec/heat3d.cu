@@ -77,8 +77,10 @@ __global__ void __launch_bounds__(THREADS, 2)
       mbar_init(&empty[s], CWARPS);
     }
     fence_barrier_init();
+    pdl_trigger();
   }
   __syncthreads();
+  pdl_wait();  // previous step's output (our input) complete, our output buffer free
 
   if (warp == CWARPS) {
     // ---------------- producer: one elected lane streams planes ----------------
@@ -257,6 +259,8 @@ int launch_step(const double* in, double* out, int ni, int nj, int nk, bool wrap
     slots = sms * std::max(per_sm, 1);
   }
   const int ctas = std::min(p.units, slots);
+  // plain stream-ordered launch: measured A/B, programmatic dependent launch
+  // costs heat3d ~8% (its one-wave 380-us kernels have no launch gap to hide)
   heat3d_fused<<<ctas, THREADS, SMEM, st>>>(map, out, p);
   return cuda_status(cudaGetLastError(), "heat3d_fused launch", err);
 }

@@ -97,6 +97,8 @@ __global__ void __launch_bounds__(NT, MINB) hydro_fused(const __grid_constant__ 
   double* xb0 = reinterpret_cast<double*>(smem + S * STAGE_BYTES);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + S * STAGE_BYTES + XBUF * 8);
   const int t = threadIdx.x;
+  if (t == 0) pdl_trigger();
+  pdl_wait();  // previous step's output (our input) complete, our output buffer free
   const double dtdx = *p.dtdx;
 
   // ---- segment list (strip-major row ranges) and stage bookkeeping
@@ -314,8 +316,7 @@ int launch_step(const double* const in[4], double* const out[4], const double* d
   for (int a = 0; a < 4; ++a) p.out[a] = out[a];
   const long long work = (long long)p.strips * nj;
   const int ctas = static_cast<int>(std::max<long long>(1, std::min<long long>(slots, work / 8)));
-  kern<<<ctas, NT, SMEM, st>>>(maps, p);
-  return cuda_status(cudaGetLastError(), "hydro_fused launch", err);
+  return cuda_status(launch_pdl(kern, dim3(ctas), dim3(NT), SMEM, st, maps, p), "hydro_fused launch", err);
 }
 
 int run(const ExecArgs& a, std::string& err) {
