@@ -56,18 +56,40 @@ def _hydro_inputs(sizes, seed=0):
     return st + [np.array([dtdx], dtype=np.float64)]
 
 
+# slab generators: the axioms of one rank's slab [lo, hi) of the outer
+# dimension (storage rows incl. halo), built without the whole grid where it
+# is large; `reduce_max` combines per-rank maxima (global dt of hydro)
+def _heat3d_slab(sizes, lo, hi, reduce_max):
+    from paper_1710_08774_b200 import inputs
+    return [inputs.heat3d_planes(*sizes, lo, hi + 2)]
+
+
+def _biharm_slab(sizes, lo, hi, reduce_max):
+    return [np.ascontiguousarray(_biharm_inputs(sizes)[0][lo:hi + 4])]
+
+
+def _box_slab(sizes, lo, hi, reduce_max):
+    return [np.ascontiguousarray(_box_inputs(sizes)[0][lo:hi + 4])]
+
+
+def _hydro_slab(sizes, lo, hi, reduce_max):
+    from paper_1710_08774_b200 import inputs
+    st, smax = inputs.hydro_rows(sizes[0], sizes[1], lo - 2, hi + 2)
+    return st + [np.array([0.5 / reduce_max(smax)], dtype=np.float64)]
+
+
 WORKLOADS = {
     # BASELINE.json configs[1] -- the default bench line
     "heat3d": dict(config_index=1, spec="heat3d", sizes=(512, 512, 512), chain_steps=50,
-                   gen=_heat3d_inputs, dtype="f64", halo=(1, 1, True)),
+                   gen=_heat3d_inputs, slab=_heat3d_slab, dtype="f64", halo=(1, 1, True)),
     "biharm": dict(config_index=0, spec="biharmonic2d", sizes=(4096, 4096), chain_steps=100,
-                   gen=_biharm_inputs, dtype="f64", halo=(2, 2, False)),
+                   gen=_biharm_inputs, slab=_biharm_slab, dtype="f64", halo=(2, 2, False)),
     "box": dict(config_index=3, spec="box2x", sizes=(16384, 16384), chain_steps=1,
-                gen=_box_inputs, dtype="f32", halo=None),
+                gen=_box_inputs, slab=_box_slab, dtype="f32", halo=None),
     "hydro": dict(config_index=2, spec="hydro2d", sizes=(4096, 4096), chain_steps=20,
-                  gen=_hydro_inputs, dtype="f64", halo=(2, 2, False)),
+                  gen=_hydro_inputs, slab=_hydro_slab, dtype="f64", halo=(2, 2, False)),
     "hydro_large": dict(config_index=4, spec="hydro2d", sizes=(32768, 32768), chain_steps=10,
-                        gen=_hydro_inputs, dtype="f64", halo=(2, 2, False)),
+                        gen=_hydro_inputs, slab=_hydro_slab, dtype="f64", halo=(2, 2, False)),
 }
 
 
@@ -263,34 +285,55 @@ def main():
     plan = lf.Plan.with_ranges(w["spec"], w["sizes"])
     if not plan.executor:
         raise SystemExit(f"no fused executor for {w['spec']}: run lf_run to see why")
-    host = w["gen"](w["sizes"])
     nax = len(plan.axioms)
     stream = torch.cuda.current_stream()
+    tdt = lambda t: getattr(torch, str(t.dtype))
 
     # ---------------- device-resident timing ----------------
     if world == 1:
+        host = w["gen"](w["sizes"])
         d_ax = [torch.from_numpy(h).to(dev) for h in host[:nax]]
-        d_goal = [torch.empty(t.extent, dtype=getattr(torch, str(t.dtype)), device=dev) for t in plan.goals]
+        d_goal = [torch.empty(t.extent, dtype=tdt(t), device=dev) for t in plan.goals]
         bufs = d_ax + d_goal
 
         def one_step():
             plan.run(bufs, steps=w["chain_steps"], stream=stream)
-        launches = plan.launches_per_step * w["chain_steps"]
     else:
-        lo_h, hi_h, periodic = w["halo"]
+        # outer-dimension slabs, faces exchanged by NCCL every time step
         n0 = w["sizes"][0]
         lo, hi = slabs.slab_range(n0, rank, world)
-        halo = slabs.Halo(lo_h, hi_h, periodic)
-        d_ax = [torch.from_numpy(np.ascontiguousarray(h[lo:hi + lo_h + hi_h])).to(dev) for h in host[:nax]]
-        d_sc = [torch.empty_like(a) for a in d_ax]
-        slab_plan = plan
 
-        def step(src, dst):
-            slab_plan.run_slab(list(src) + list(dst), lo, hi, n0, stream=stream)
+        def reduce_max(x):
+            t = torch.tensor([x], dtype=torch.float64, device=dev)
+            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+            return float(t.item())
+        host = None
+        local = w["slab"](w["sizes"], lo, hi, reduce_max)
+        d_ax = [torch.from_numpy(np.ascontiguousarray(h)).to(dev) for h in local]
+        state = [i for i, t in enumerate(plan.axioms) if len(t.extent) > 0]
+        d_goal = []
+        for t in plan.goals:
+            ext = list(t.extent)
+            ext[0] = ext[0] - n0 + (hi - lo)  # same halo, local rows
+            d_goal.append(torch.empty(ext, dtype=tdt(t), device=dev))
+        if w["halo"] is None:  # no iterate pairs: independent slabs, halo rows replicated in the input
+            def one_step():
+                for _ in range(w["chain_steps"]):
+                    plan.run_slab(d_ax + d_goal, lo, hi, n0, stream=stream)
+        else:
+            halo = slabs.Halo(*w["halo"])
+            cur = [d_ax[i] for i in state]
+            nxt = [torch.empty_like(d_ax[i]) for i in state]
 
-        def one_step():
-            slabs.run_slabs(step, d_ax, d_sc, w["chain_steps"], halo, rank, world)
-        launches = plan.launches_per_step * w["chain_steps"]
+            def step(src, dst):
+                bufs = list(d_ax)
+                for k, i in enumerate(state):
+                    bufs[i] = src[k]
+                plan.run_slab(bufs + list(dst), lo, hi, n0, stream=stream)
+
+            def one_step():
+                slabs.run_slabs(step, cur, nxt, w["chain_steps"], halo, rank, world)
+    launches = plan.launches_per_step * w["chain_steps"]
 
     def barrier():
         if world > 1:
@@ -336,9 +379,15 @@ def main():
     }
 
     # ---------------- end-to-end through the host-buffer ABI call ----------------
-    if not args.no_e2e and world == 1:
+    e2e_bytes = sum(t.bytes for t in plan.terminals)
+    if not args.no_e2e and world == 1 and e2e_bytes > 40e9:
+        line["e2e"] = None
+        line["e2e_skipped"] = f"{e2e_bytes / 1e9:.0f} GB of terminals: pinned host copies would not fit beside the device run"
+    elif not args.no_e2e and world == 1:
+        del d_ax, d_goal, bufs  # lf_run_host owns its own device buffers
+        torch.cuda.empty_cache()
         pinned = [torch.from_numpy(h).pin_memory() for h in host[:nax]]
-        outs = [torch.empty(t.extent, dtype=getattr(torch, str(t.dtype))).pin_memory() for t in plan.goals]
+        outs = [torch.empty(t.extent, dtype=tdt(t)).pin_memory() for t in plan.goals]
         hb = [p.numpy() for p in pinned] + [o.numpy() for o in outs]
         for _ in range(max(1, args.warmup)):
             plan.run_host(hb, steps=w["chain_steps"])

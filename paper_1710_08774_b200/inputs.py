@@ -148,3 +148,49 @@ def hydro_input(nj: int, ni: int, seed: int = 0):
     smax = float(np.max(c))  # |u| = 0 initially
     dtdx = 0.5 / smax
     return st, dtdx
+
+
+# ---------------------------------------------------------------- slabs
+def heat3d_planes(nk: int, nj: int, ni: int, k0: int, k1: int, seed: int = 0, sigma: float = 32.0) -> np.ndarray:
+    """Storage planes [k0, k1) of heat3d_input(nk, nj, ni) (logical k0-1 .. k1-2),
+    generated without building the whole grid: what one slab rank needs."""
+    out = np.empty((k1 - k0, nj + 2, ni + 2), dtype=np.float64)
+    ck, cj, ci = nk // 2, nj // 2, ni // 2
+    di2 = (np.arange(ni, dtype=np.float64) - ci) ** 2
+    dj2 = (np.arange(nj, dtype=np.float64) - cj) ** 2
+    inv = 1.0 / (2.0 * sigma * sigma)
+    for s in range(k0, k1):
+        k = (s - 1) % nk  # periodic: storage plane s holds logical plane s-1
+        u = uniform(nj * ni, seed, offset=k * nj * ni).reshape(nj, ni)
+        r2 = (float(k - ck) ** 2 + dj2)[:, None] + di2[None, :]
+        plane = out[s - k0]
+        plane[1:-1, 1:-1] = u + np.exp(-r2 * inv)
+        fill_periodic(plane, 1)
+    return out
+
+
+def hydro_rows(nj: int, ni: int, r0: int, r1: int, seed: int = 0):
+    """Logical rows [r0, r1) (-2 <= r0 < r1 <= nj+2) of hydro_input's four
+    state arrays, each (r1-r0, ni+4), without building the whole grid, plus
+    this block's max(|u| + c) for the global dt (combine with a MAX reduce)."""
+    lo, hi = max(0, r0), min(nj, r1)
+    x_left = (np.arange(ni) + 0.5) / ni < 0.5
+    delta = (2.0 * uniform((hi - lo) * ni, seed, offset=lo * ni) - 1.0).reshape(hi - lo, ni) * 1e-3
+    rho0 = np.where(x_left, 1.0, 0.125)[None, :] + delta
+    p0 = np.broadcast_to(np.where(x_left, 1.0, 0.1)[None, :], (hi - lo, ni))
+    smax = float(np.max(np.sqrt(GAMMA * p0 / rho0))) if hi > lo else 0.0
+    inner = [np.zeros((hi - lo, ni + 4)) for _ in range(4)]
+    inner[0][:, 2:-2] = rho0
+    inner[3][:, 2:-2] = p0 / (GAMMA - 1.0)
+    for a, odd_i in zip(inner, (False, True, False, False)):
+        for g in range(2):  # reflective ghost columns
+            s = -1.0 if odd_i else 1.0
+            a[:, 1 - g] = s * a[:, 2 + g]
+            a[:, ni + 2 + g] = s * a[:, ni + 1 - g]
+    out = [np.empty((r1 - r0, ni + 4)) for _ in range(4)]
+    for v, odd_j in enumerate((False, False, True, False)):
+        for r in range(r0, r1):
+            src = r if 0 <= r < nj else (-1 - r if r < 0 else 2 * nj - 1 - r)  # mirrored row
+            row = inner[v][src - lo]
+            out[v][r - r0] = -row if (odd_j and src != r) else row
+    return out, smax

@@ -1,5 +1,5 @@
 #!/bin/bash
-# A/B: CFG=heat3d ./tools_ab.sh  -> alternating runs with and without PDL
+# A/B: CFG=heat3d tools/ab.sh  -> alternating runs with and without PDL
 mkdir -p gpurun_out; : > gpurun_out/ab_${CFG}.txt
 for rep in 1 2; do
   for mode in pdl nopdl; do

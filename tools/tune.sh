@@ -1,5 +1,5 @@
 #!/bin/bash
-# variant sweep: VAR_ENV=LF_BIHARM_VARIANT NVAR=6 CFG=biharm ./tools_tune.sh
+# variant sweep: VAR_ENV=LF_BIHARM_VARIANT NVAR=6 CFG=biharm tools/tune.sh
 mkdir -p gpurun_out
 : > gpurun_out/tune_${CFG}.txt
 for v in $(seq 0 $((NVAR-1))); do
