@@ -380,7 +380,7 @@ def main():
 
     # ---------------- end-to-end through the host-buffer ABI call ----------------
     e2e_bytes = sum(t.bytes for t in plan.terminals)
-    if not args.no_e2e and world == 1 and e2e_bytes > 40e9:
+    if not args.no_e2e and world == 1 and e2e_bytes > 100e9:
         line["e2e"] = None
         line["e2e_skipped"] = f"{e2e_bytes / 1e9:.0f} GB of terminals: pinned host copies would not fit beside the device run"
     elif not args.no_e2e and world == 1:

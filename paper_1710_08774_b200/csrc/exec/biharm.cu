@@ -200,11 +200,14 @@ const Variant& variant() {
       make_variant<Cfg<4, 4, 16>>("cpl4_s4_occ16"), make_variant<Cfg<2, 4, 16>>("cpl2_s4_occ16"),
       make_variant<Cfg<2, 6, 24>>("cpl2_s6_occ24"), make_variant<Cfg<4, 6, 12>>("cpl4_s6_occ12"),
       make_variant<Cfg<2, 8, 16>>("cpl2_s8_occ16"), make_variant<Cfg<4, 8, 8>>("cpl4_s8_occ8"),
+      make_variant<Cfg<2, 16, 8>>("cpl2_s16_occ8"), make_variant<Cfg<2, 12, 10>>("cpl2_s12_occ10"),
+      make_variant<Cfg<4, 6, 10>>("cpl4_s6_occ10"),
   };
   static int idx = [] {
     const char* e = std::getenv("LF_BIHARM_VARIANT");
-    int i = e ? std::atoi(e) : 1;
-    return (i >= 0 && i < (int)(sizeof table / sizeof table[0])) ? i : 1;
+    // default cpl4_s8_occ8: best of the measured sweep (profiles/r01_biharm_variants.txt)
+    int i = e ? std::atoi(e) : 5;
+    return (i >= 0 && i < (int)(sizeof table / sizeof table[0])) ? i : 5;
   }();
   return table[idx];
 }

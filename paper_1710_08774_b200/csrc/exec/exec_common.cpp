@@ -1,5 +1,6 @@
 // Host helpers shared by the executors: TMA descriptor encoding through the
 // runtime's driver entry point, CUDA error mapping.
+#include <cstdlib>
 #include <mutex>
 
 #include "common.cuh"
@@ -44,9 +45,17 @@ bool make_tensor_map(CUtensorMap* map, const void* base, CUtensorMapDataType dty
     if (d > 0) gstride[d - 1] = acc;
     acc *= dims[d];
   }
+  // L2 sector promotion of TMA fetches; LF_TMA_PROMOTION=0/64/128/256 overrides
+  // the default for tuning runs
+  static const CUtensorMapL2promotion promo = [] {
+    const char* e = std::getenv("LF_TMA_PROMOTION");
+    const int v = e ? std::atoi(e) : 256;
+    return v == 0 ? CU_TENSOR_MAP_L2_PROMOTION_NONE
+                  : v == 64 ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
+                            : v == 128 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B : CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
+  }();
   CUresult r = fn(map, dtype, rank, const_cast<void*>(base), gdim, gstride, bdim, estride,
-                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, promo, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) {
     err = "cuTensorMapEncodeTiled failed with CUresult " + std::to_string(static_cast<int>(r));
     return false;

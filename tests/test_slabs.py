@@ -59,3 +59,55 @@ def test_slab_ranges_cover():
         rs = [slabs.slab_range(n, r, w) for r in range(w)]
         assert rs[0][0] == 0 and rs[-1][1] == n
         assert all(a[1] == b[0] for a, b in zip(rs, rs[1:]))
+
+
+def _hydro_worker(rank, world, port, shape, steps, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        nj, ni = shape
+        lo, hi = slabs.slab_range(nj, rank, world)
+
+        def reduce_max(x):
+            t = torch.tensor([x], dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            return float(t.item())
+        local, smax = inputs.hydro_rows(nj, ni, lo - 2, hi + 2, seed=4)
+        dtdx = 0.5 / reduce_max(smax)
+        cur = [torch.from_numpy(a) for a in local]
+        nxt = [torch.empty_like(a) for a in cur]
+        top, bottom = lo == 0, hi == nj
+
+        def step(src, dst):
+            # the oracle advances the slab as a full domain; rows it reflects at
+            # an internal face are overwritten by the exchange that follows
+            out = oracle.hydro([s.numpy() for s in src], dtdx, 1)
+            for d, o in zip(dst, out):
+                d.copy_(torch.from_numpy(o))
+
+        res = slabs.run_slabs(step, cur, nxt, steps, slabs.Halo(2, 2, periodic=False), rank, world)
+        q.put((rank, lo, hi, [r[2:-2].numpy().copy() for r in res]))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,shape,steps", [(2, (12, 10), 3), (3, (15, 8), 2)])
+def test_hydro_row_slabs_match_single_domain(world, shape, steps):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = 31500 + np.random.randint(0, 2000)
+    procs = [ctx.Process(target=_hydro_worker, args=(r, world, port, shape, steps, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    parts = [q.get(timeout=120) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    st, dtdx = inputs.hydro_input(*shape, seed=4)
+    ref = oracle.hydro(st, dtdx, steps)
+    for rank, lo, hi, part in parts:
+        for v in range(4):
+            got = part[v][:, 2:-2]
+            want = ref[v][2 + lo:2 + hi, 2:-2]
+            assert np.array_equal(got.view(np.uint64), want.view(np.uint64)), (rank, v)
