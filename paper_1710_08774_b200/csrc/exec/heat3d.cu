@@ -17,6 +17,7 @@
 // Compulsory traffic: 8 B read + 8 B written per cell-update.
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 
 #include "../../userkernels/stencil_kernels.h"
 #include "common.cuh"
@@ -26,16 +27,21 @@ namespace lfx {
 namespace {
 
 constexpr int TX = 64;                 // cells along i per CTA (32 lanes x 2)
-constexpr int TY = 16;                 // rows along j per CTA (8 warps x 2)
-constexpr int CWARPS = TY / 2;         // consumer warps
+constexpr int CWARPS = 8;              // consumer warps
 constexpr int THREADS = (CWARPS + 1) * 32;
 constexpr int LD = TX + 2;             // staged row length (halo 1 each side)
-constexpr int ROWS = TY + 2;
-constexpr int STAGE_TX = LD * ROWS * 8;                     // bytes TMA delivers
-constexpr int STAGE_BYTES = (STAGE_TX + 127) / 128 * 128;   // 128-B aligned slots
-constexpr int S = 6;                                        // ring depth
-constexpr int SMEM = S * STAGE_BYTES + 2 * S * 8 + 128;
-constexpr int KCH = 32;                // planes per work unit
+
+// Tunable shape: RPW rows per consumer warp (tile height TY = 8*RPW), S ring
+// slots, KCH planes per work unit.
+template <int RPW_, int S_, int KCH_>
+struct Cfg {
+  static constexpr int RPW = RPW_, S = S_, KCH = KCH_;
+  static constexpr int TY = CWARPS * RPW;
+  static constexpr int ROWS = TY + 2;
+  static constexpr int STAGE_TX = LD * ROWS * 8;                    // bytes TMA delivers
+  static constexpr int STAGE_BYTES = (STAGE_TX + 127) / 128 * 128;  // 128-B aligned slots
+  static constexpr int SMEM = S * STAGE_BYTES + 2 * S * 8 + 128;
+};
 
 struct Params {
   int ni, nj, nk;       // interior sizes of this launch
@@ -52,6 +58,7 @@ struct Params {
 struct Unit {
   int i0, j0, k0, kc;
 };
+template <int TY>
 __device__ __forceinline__ Unit unit_of(const Params& p, int u) {
   const int kb = u / p.tiles, t = u - kb * p.tiles;
   Unit r;
@@ -62,8 +69,10 @@ __device__ __forceinline__ Unit unit_of(const Params& p, int u) {
   return r;
 }
 
+template <class K>
 __global__ void __launch_bounds__(THREADS, 2)
     heat3d_fused(const __grid_constant__ CUtensorMap tin, double* __restrict__ out, const Params p) {
+  constexpr int RPW = K::RPW, S = K::S, TY = K::TY, STAGE_BYTES = K::STAGE_BYTES, STAGE_TX = K::STAGE_TX;
   extern __shared__ __align__(128) unsigned char smem[];
   unsigned char* ring = smem;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + S * STAGE_BYTES);
@@ -77,10 +86,8 @@ __global__ void __launch_bounds__(THREADS, 2)
       mbar_init(&empty[s], CWARPS);
     }
     fence_barrier_init();
-    pdl_trigger();
   }
   __syncthreads();
-  pdl_wait();  // previous step's output (our input) complete, our output buffer free
 
   if (warp == CWARPS) {
     // ---------------- producer: one elected lane streams planes ----------------
@@ -88,7 +95,7 @@ __global__ void __launch_bounds__(THREADS, 2)
       tma_prefetch_desc(&tin);
       int g = 0;  // running plane counter across this CTA's units
       for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
-        const Unit w = unit_of(p, u);
+        const Unit w = unit_of<TY>(p, u);
         for (int q = 0; q < w.kc + 2; ++q, ++g) {
           const int slot = g % S;
           if (g >= S) mbar_wait(&empty[slot], ((g / S) & 1) ^ 1);
@@ -102,20 +109,20 @@ __global__ void __launch_bounds__(THREADS, 2)
     return;
   }
 
-  // ---------------- consumers: warp w owns rows 2w, 2w+1; lane owns cells lane, lane+32
+  // ---------------- consumers: warp w owns rows RPW*w .. RPW*w+RPW-1; lane owns cells lane, lane+32
   const uint64_t pol = l2_evict_first_policy();
-  const int r0 = 2 * warp;
+  const int r0 = RPW * warp;
   auto stage = [&](int g) { return reinterpret_cast<const double*>(ring + (g % S) * STAGE_BYTES); };
   auto at = [&](const double* sp, int row, int col) { return sp[row * LD + col]; };
   int g = 0;
   for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
-    const Unit w = unit_of(p, u);
-    double uprev[2][2], ucur[2][2], unext[2][2];
+    const Unit w = unit_of<TY>(p, u);
+    double uprev[RPW][2], ucur[RPW][2], unext[RPW][2];
     mbar_wait(&full[g % S], (g / S) & 1);
     {
       const double* sp = stage(g);
 #pragma unroll
-      for (int r = 0; r < 2; ++r)
+      for (int r = 0; r < RPW; ++r)
 #pragma unroll
         for (int c = 0; c < 2; ++c) uprev[r][c] = at(sp, r0 + r + 1, lane + 32 * c + 1);
     }
@@ -126,7 +133,7 @@ __global__ void __launch_bounds__(THREADS, 2)
     {
       const double* sp = stage(g);
 #pragma unroll
-      for (int r = 0; r < 2; ++r)
+      for (int r = 0; r < RPW; ++r)
 #pragma unroll
         for (int c = 0; c < 2; ++c) ucur[r][c] = at(sp, r0 + r + 1, lane + 32 * c + 1);
     }
@@ -138,14 +145,14 @@ __global__ void __launch_bounds__(THREADS, 2)
       mbar_wait(&full[gn % S], (gn / S) & 1);
       const double* sn = stage(gn);
 #pragma unroll
-      for (int r = 0; r < 2; ++r)
+      for (int r = 0; r < RPW; ++r)
 #pragma unroll
         for (int c = 0; c < 2; ++c) unext[r][c] = at(sn, r0 + r + 1, lane + 32 * c + 1);
       const double* sp = stage(g);
       const int k = w.k0 + kk;
-      double o[2][2];
+      double o[RPW][2];
 #pragma unroll
-      for (int r = 0; r < 2; ++r) {
+      for (int r = 0; r < RPW; ++r) {
         const int row = r0 + r + 1;
 #pragma unroll
         for (int c = 0; c < 2; ++c) {
@@ -153,8 +160,8 @@ __global__ void __launch_bounds__(THREADS, 2)
           const double uc = ucur[r][c];
           const double uw = at(sp, row, col - 1);
           const double ue = at(sp, row, col + 1);
-          const double un = r == 0 ? ucur[1][c] : at(sp, row + 1, col);
-          const double us = r == 1 ? ucur[0][c] : at(sp, row - 1, col);
+          const double un = r + 1 < RPW ? ucur[r + 1 < RPW ? r + 1 : r][c] : at(sp, row + 1, col);
+          const double us = r > 0 ? ucur[r > 0 ? r - 1 : r][c] : at(sp, row - 1, col);
           double fxp, fxm, fyp, fym, fzp, fzm;
           face_flux(ue, uc, &fxp);
           face_flux(uc, uw, &fxm);
@@ -170,7 +177,7 @@ __global__ void __launch_bounds__(THREADS, 2)
       if (lane == 0) mbar_arrive(&empty[g % S]);
       double* plane = out + (long long)(k + 1) * p.pk;
 #pragma unroll
-      for (int r = 0; r < 2; ++r) {
+      for (int r = 0; r < RPW; ++r) {
         const int j = w.j0 + r0 + r;
         double* rowp = plane + (long long)(j + 1) * p.pj + 1;  // logical i = 0
         st_hint(rowp + gi0, o[r][0], pol);
@@ -190,7 +197,7 @@ __global__ void __launch_bounds__(THREADS, 2)
         }
       }
 #pragma unroll
-      for (int r = 0; r < 2; ++r)
+      for (int r = 0; r < RPW; ++r)
 #pragma unroll
         for (int c = 0; c < 2; ++c) {
           uprev[r][c] = ucur[r][c];
@@ -204,6 +211,34 @@ __global__ void __launch_bounds__(THREADS, 2)
   }
 }
 
+struct Variant {
+  const char* name;
+  int ty, kch, smem;
+  void (*kernel)(CUtensorMap, double*, Params);
+};
+template <class K>
+Variant make_variant(const char* n) {
+  return {n, K::TY, K::KCH, K::SMEM, heat3d_fused<K>};
+}
+// LF_HEAT3D_VARIANT=<index> overrides the default for tuning runs
+const Variant& variant() {
+  static const Variant table[] = {
+      make_variant<Cfg<2, 6, 32>>("rpw2_s6_k32"), make_variant<Cfg<2, 8, 32>>("rpw2_s8_k32"),
+      make_variant<Cfg<2, 6, 64>>("rpw2_s6_k64"), make_variant<Cfg<2, 6, 16>>("rpw2_s6_k16"),
+      make_variant<Cfg<4, 5, 32>>("rpw4_s5_k32"), make_variant<Cfg<4, 6, 64>>("rpw4_s6_k64"),
+      make_variant<Cfg<4, 4, 32>>("rpw4_s4_k32"), make_variant<Cfg<2, 6, 8>>("rpw2_s6_k8"),
+      make_variant<Cfg<2, 5, 16>>("rpw2_s5_k16"), make_variant<Cfg<2, 7, 16>>("rpw2_s7_k16"),
+      make_variant<Cfg<2, 4, 16>>("rpw2_s4_k16"), make_variant<Cfg<2, 6, 12>>("rpw2_s6_k12"),
+  };
+  static int idx = [] {
+    const char* e = std::getenv("LF_HEAT3D_VARIANT");
+    // default rpw2_s6_k16: best of the measured sweep (profiles/r01_heat3d_variants.txt)
+    int i = e ? std::atoi(e) : 3;
+    return (i >= 0 && i < (int)(sizeof table / sizeof table[0])) ? i : 3;
+  }();
+  return table[idx];
+}
+
 bool supports(const lf::Plan& plan, std::string& why) {
   const auto& r = plan.rs.ranges;
   long nk = r[0].trips(), nj = r[1].trips(), ni = r[2].trips();
@@ -212,9 +247,10 @@ bool supports(const lf::Plan& plan, std::string& why) {
       why = "heat3d executor needs unit strides";
       return false;
     }
+  const int TY = variant().ty;
   if (ni % TX || nj % TY || nk < 1) {
-    why = "heat3d executor needs N_i % 64 == 0 and N_j % 16 == 0 (got " + std::to_string(ni) + "x" +
-          std::to_string(nj) + ")";
+    why = "heat3d executor needs N_i % 64 == 0 and N_j % " + std::to_string(TY) + " == 0 (got " +
+          std::to_string(ni) + "x" + std::to_string(nj) + ")";
     return false;
   }
   if ((ni + 2) * 8 % 16) {
@@ -226,15 +262,20 @@ bool supports(const lf::Plan& plan, std::string& why) {
 
 int launch_step(const double* in, double* out, int ni, int nj, int nk, bool wrap_k, cudaStream_t st,
                 std::string& err) {
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(heat3d_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
+  const Variant& v = variant();
+  static int slots = 0;
+  if (!slots) {
+    cudaError_t e = cudaFuncSetAttribute(v.kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, v.smem);
     if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(heat3d)", err);
-    attr = true;
+    int dev = 0, sms = 148, per_sm = 1;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, v.kernel, THREADS, v.smem);
+    slots = sms * std::max(per_sm, 1);
   }
   CUtensorMap map;
   uint64_t dims[3] = {(uint64_t)ni + 2, (uint64_t)nj + 2, (uint64_t)nk + 2};
-  uint32_t box[3] = {LD, ROWS, 1};
+  uint32_t box[3] = {LD, (uint32_t)(v.ty + 2), 1};
   if (!make_tensor_map(&map, in, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 8, 3, dims, box, err)) return LF_ERR_CUDA;
   Params p;
   p.ni = ni;
@@ -243,25 +284,17 @@ int launch_step(const double* in, double* out, int ni, int nj, int nk, bool wrap
   p.pj = ni + 2;
   p.pk = (long long)(ni + 2) * (nj + 2);
   p.tiles_x = ni / TX;
-  p.tiles = (ni / TX) * (nj / TY);
-  p.kchunks = (nk + KCH - 1) / KCH;
+  p.tiles = (ni / TX) * (nj / v.ty);
+  p.kchunks = (nk + v.kch - 1) / v.kch;
   p.units = p.tiles * p.kchunks;
   p.wrap_i = 1;
   p.wrap_j = 1;
   p.wrap_k = wrap_k ? 1 : 0;
   // persistent grid: every resident CTA slot on the chip, never more than units
-  static int slots = 0;
-  if (!slots) {
-    int dev = 0, sms = 148, per_sm = 1;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, heat3d_fused, THREADS, SMEM);
-    slots = sms * std::max(per_sm, 1);
-  }
   const int ctas = std::min(p.units, slots);
   // plain stream-ordered launch: measured A/B, programmatic dependent launch
   // costs heat3d ~8% (its one-wave 380-us kernels have no launch gap to hide)
-  heat3d_fused<<<ctas, THREADS, SMEM, st>>>(map, out, p);
+  v.kernel<<<ctas, THREADS, v.smem, st>>>(map, out, p);
   return cuda_status(cudaGetLastError(), "heat3d_fused launch", err);
 }
 
