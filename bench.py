@@ -325,14 +325,18 @@ def main():
             cur = [d_ax[i] for i in state]
             nxt = [torch.empty_like(d_ax[i]) for i in state]
 
-            def step(src, dst):
+            def launch(src, dst, part):
                 bufs = list(d_ax)
                 for k, i in enumerate(state):
                     bufs[i] = src[k]
-                plan.run_slab(bufs + list(dst), lo, hi, n0, stream=stream)
+                plan.run_slab(bufs + list(dst), lo, hi, n0, stream=torch.cuda.current_stream(), part=part)
+
+            comm = torch.cuda.Stream(device=dev, priority=-1)
 
             def one_step():
-                slabs.run_slabs(step, cur, nxt, w["chain_steps"], halo, rank, world)
+                # face rows first, their NCCL exchange overlapped with the interior rows
+                slabs.run_slabs_overlapped(launch, cur, nxt, w["chain_steps"], halo, rank, world, hi - lo,
+                                           comm_stream=comm)
     launches = plan.launches_per_step * w["chain_steps"]
 
     def barrier():

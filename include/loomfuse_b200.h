@@ -72,11 +72,16 @@ typedef struct {
  * are sized for that slab (the planner's extents with `hi-lo` trips along the
  * outermost dim).  Ghost rows on an internal face are filled by the caller's
  * halo exchange before each step; ghost rows on a global face are refilled by
- * the executor from the chain's boundary mode. */
+ * the executor from the chain's boundary mode.  [part_lo, part_hi) (slab-local
+ * rows; 0,0 = all) restricts one call to part of the slab, so a caller can
+ * compute the face rows first, start their exchange, and overlap it with the
+ * interior rows. */
 typedef struct {
   int64_t lo;
   int64_t hi;
   int64_t global;
+  int64_t part_lo;
+  int64_t part_hi;
 } lf_slab;
 
 /* Parse, validate, infer and analyse a rule file.  `filename` is only used in

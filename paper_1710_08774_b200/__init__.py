@@ -64,7 +64,8 @@ class _Terminal(ctypes.Structure):
 
 
 class _Slab(ctypes.Structure):
-    _fields_ = [("lo", ctypes.c_int64), ("hi", ctypes.c_int64), ("global_", ctypes.c_int64)]
+    _fields_ = [("lo", ctypes.c_int64), ("hi", ctypes.c_int64), ("global_", ctypes.c_int64),
+                ("part_lo", ctypes.c_int64), ("part_hi", ctypes.c_int64)]
 
 
 _lib: ctypes.CDLL | None = None
@@ -238,8 +239,12 @@ class Plan:
                 raise ValueError(f"{t.name}: expected {t.bytes} bytes, got {a.nbytes}")
         _check(lib().lf_run_host(self._h, self._ptrs(arrays), len(arrays), steps))
 
-    def run_slab(self, bufs: Sequence[Any], lo: int, hi: int, global_: int, stream: Any = None) -> None:
-        slab = _Slab(lo, hi, global_)
+    def run_slab(self, bufs: Sequence[Any], lo: int, hi: int, global_: int, stream: Any = None,
+                 part: tuple[int, int] | None = None) -> None:
+        """One step on rows [lo, hi) of the outer dimension (slab-local buffers);
+        `part` = slab-local rows to compute (default: all)."""
+        p0, p1 = part if part is not None else (0, 0)
+        slab = _Slab(lo, hi, global_, p0, p1)
         _check(lib().lf_run_slab(self._h, self._ptrs(bufs), len(bufs), ctypes.byref(slab),
                                  _stream_handle(stream)))
 

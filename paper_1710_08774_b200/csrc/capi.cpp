@@ -319,6 +319,9 @@ int lf_run_slab(const lf_plan* cplan, void* const* terms, int nterm, const lf_sl
     if (st != LF_OK) return st;
     if (!slab || slab->lo < 0 || slab->hi <= slab->lo || slab->hi > slab->global)
       return fail(LF_ERR_SPEC, "invalid slab");
+    if (slab->part_lo < 0 || slab->part_hi < slab->part_lo || slab->part_hi > slab->hi - slab->lo)
+      return fail(LF_ERR_SPEC, "invalid slab part");
+    if (slab->part_hi == slab->part_lo && slab->part_lo != 0) return LF_OK;  // empty part
     lfx::ExecArgs a;
     a.plan = &cplan->plan;
     a.terms = terms;

@@ -39,7 +39,8 @@ struct Cfg {
 };
 
 struct Params {
-  int ni, nj;
+  int ni, nj;         // nj: rows of the launch's domain (slab or grid)
+  int row_lo, row_hi; // rows this launch computes
   long long pitch;    // ni + 4
   int strips;         // ni / SW
   int write_ghost_top, write_ghost_bottom;
@@ -122,7 +123,7 @@ __global__ void __launch_bounds__(32, K::OCC)
   const int lane = threadIdx.x;
 
   RowSeg seg[3];
-  const int nseg = cta_segments(blockIdx.x, gridDim.x, p.strips, p.nj, seg);
+  const int nseg = cta_segments(blockIdx.x, gridDim.x, p.strips, p.row_lo, p.row_hi, seg);
   RowRing<R, S> rr;
   // staged column 0 = logical i0 - 2 = storage i0; storage row = logical + 2
   rr.init(seg, nseg, H, smem, full, STAGE_BYTES, STAGE_TX, 0, H, SW);
@@ -227,8 +228,8 @@ bool supports(const lf::Plan& plan, std::string& why) {
   return true;
 }
 
-int launch_step(const double* in, double* out, int ni, int nj, bool top, bool bottom, cudaStream_t st,
-                std::string& err) {
+int launch_step(const double* in, double* out, int ni, const RowPart& rp, cudaStream_t st, std::string& err) {
+  const int nj = rp.rows;
   const Variant& v = variant();
   static int slots = 0;
   if (!slots) {
@@ -249,30 +250,34 @@ int launch_step(const double* in, double* out, int ni, int nj, bool top, bool bo
   p.nj = nj;
   p.pitch = ni + 4;
   p.strips = ni / v.sw;
-  p.write_ghost_top = top;
-  p.write_ghost_bottom = bottom;
+  p.row_lo = rp.lo;
+  p.row_hi = rp.hi;
+  p.write_ghost_top = rp.top;
+  p.write_ghost_bottom = rp.bottom;
   // at least ~16 rows per CTA so the 4 priming rows stay a small fraction
-  const long long work = (long long)p.strips * nj;
-  const int ctas = static_cast<int>(std::max<long long>(1, std::min<long long>(slots, work / 16)));
+  const long long work = (long long)p.strips * (rp.hi - rp.lo);
+  // each CTA must get at most 3 row segments (rowstream.cuh): at least
+  // ceil(strips/2) CTAs when the row range is short
+  const long long want = std::max<long long>(work / 16, (p.strips + 1) / 2);
+  const int ctas = static_cast<int>(std::max<long long>(1, std::min<long long>(slots, want)));
+  if ((long long)ctas * 2 < p.strips) {
+    err = "row range too short for the resident grid";
+    return LF_ERR_UNSUPPORTED;
+  }
   return cuda_status(launch_pdl(v.kernel, dim3(ctas), dim3(32), v.smem, st, map, out, p), "biharm_fused launch",
                      err);
 }
 
 int run(const ExecArgs& a, std::string& err) {
   const auto& r = a.plan->rs.ranges;
-  int nj = (int)r[0].trips(), ni = (int)r[1].trips();
-  bool top = true, bottom = true;
-  if (a.slab) {
-    nj = (int)(a.slab->hi - a.slab->lo);
-    top = a.slab->lo == 0;
-    bottom = a.slab->hi == a.slab->global;
-  }
+  const int ni = (int)r[1].trips();
+  const RowPart rp = row_part(a, (int)r[0].trips());
   const double* src = static_cast<const double*>(a.terms[0]);
   double* goal = static_cast<double*>(a.terms[1]);
   double* scratch = a.steps > 1 ? static_cast<double*>(a.scratch[0]) : nullptr;
   for (int s = 0; s < a.steps; ++s) {
     double* dst = ((a.steps - 1 - s) % 2) == 0 ? goal : scratch;
-    int st = launch_step(src, dst, ni, nj, top, bottom, a.stream, err);
+    int st = launch_step(src, dst, ni, rp, a.stream, err);
     if (st != LF_OK) return st;
     src = dst;
   }

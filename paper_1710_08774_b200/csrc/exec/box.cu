@@ -33,6 +33,7 @@ constexpr int OCC = 16;
 
 struct Params {
   int ni, nj;
+  int row_lo, row_hi;   // rows this launch computes
   long long out_pitch;  // ni
   int strips;
 };
@@ -98,7 +99,7 @@ __global__ void __launch_bounds__(32, OCC)
   const int lane = threadIdx.x;
 
   RowSeg seg[3];
-  const int nseg = cta_segments(blockIdx.x, gridDim.x, p.strips, p.nj, seg);
+  const int nseg = cta_segments(blockIdx.x, gridDim.x, p.strips, p.row_lo, p.row_hi, seg);
   RowRing<R, S> rr;
   // staged column 0 = logical i0 - 2 = storage i0; storage row = logical + 2
   rr.init(seg, nseg, H, smem, full, STAGE_BYTES, STAGE_TX, 0, H, SW);
@@ -161,8 +162,9 @@ int run(const ExecArgs& a, std::string& err) {
     slots = sms * std::max(1, std::min(per_sm, OCC));
   }
   const auto& r = a.plan->rs.ranges;
-  int nj = (int)r[0].trips(), ni = (int)r[1].trips();
-  if (a.slab) nj = (int)(a.slab->hi - a.slab->lo);  // rows of this slab, halo rows supplied by the caller
+  const int ni = (int)r[1].trips();
+  const RowPart rp = row_part(a, (int)r[0].trips());  // slab rows: halo rows supplied by the caller
+  const int nj = rp.rows;
   CUtensorMap map;
   uint64_t dims[2] = {(uint64_t)ni + 4, (uint64_t)nj + 4};
   uint32_t box[2] = {BOXW, R};
@@ -171,10 +173,19 @@ int run(const ExecArgs& a, std::string& err) {
   Params p;
   p.ni = ni;
   p.nj = nj;
+  p.row_lo = rp.lo;
+  p.row_hi = rp.hi;
   p.out_pitch = ni;
   p.strips = ni / SW;
-  const long long work = (long long)p.strips * nj;
-  const int ctas = static_cast<int>(std::max<long long>(1, std::min<long long>(slots, work / 16)));
+  const long long work = (long long)p.strips * (rp.hi - rp.lo);
+  // each CTA must get at most 3 row segments (rowstream.cuh): at least
+  // ceil(strips/2) CTAs when the row range is short
+  const long long want = std::max<long long>(work / 16, (p.strips + 1) / 2);
+  const int ctas = static_cast<int>(std::max<long long>(1, std::min<long long>(slots, want)));
+  if ((long long)ctas * 2 < p.strips) {
+    err = "row range too short for the resident grid";
+    return LF_ERR_UNSUPPORTED;
+  }
   // a single pass; `steps` re-applies the same pass (no iterate pairs)
   for (int s = 0; s < a.steps; ++s) {
     box_fused<<<ctas, 32, SMEM, a.stream>>>(map, static_cast<float*>(a.terms[1]), p);

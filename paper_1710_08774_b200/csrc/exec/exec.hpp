@@ -44,4 +44,27 @@ const char* embedded_spec(const char* file);
 // helpers shared by the executors
 int cuda_status(cudaError_t e, const char* what, std::string& err);
 
+// rows of the outer dimension one launch computes (slab-local; whole slab when
+// no part is given) and the slab's row count
+struct RowPart {
+  int rows;      // rows of this launch's domain (slab or whole grid)
+  int lo, hi;    // rows to compute
+  bool top, bottom;  // domain edge is a global boundary
+};
+inline RowPart row_part(const ExecArgs& a, int global_rows) {
+  RowPart r{global_rows, 0, global_rows, true, true};
+  if (a.slab) {
+    r.rows = (int)(a.slab->hi - a.slab->lo);
+    r.top = a.slab->lo == 0;
+    r.bottom = a.slab->hi == a.slab->global;
+    r.lo = 0;
+    r.hi = r.rows;
+    if (a.slab->part_hi > a.slab->part_lo) {
+      r.lo = (int)a.slab->part_lo;
+      r.hi = (int)a.slab->part_hi;
+    }
+  }
+  return r;
+}
+
 }  // namespace lfx

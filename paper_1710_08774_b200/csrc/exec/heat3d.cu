@@ -44,7 +44,8 @@ struct Cfg {
 };
 
 struct Params {
-  int ni, nj, nk;       // interior sizes of this launch
+  int ni, nj, nk;       // interior sizes of this launch's domain (slab planes for multi-GPU)
+  int k_lo, k_hi;       // planes this launch computes
   long long pj, pk;     // element strides of the (nk+2, nj+2, ni+2) layout
   int tiles_x, tiles;   // column tiles
   int kchunks;          // work units along k per column
@@ -64,8 +65,9 @@ __device__ __forceinline__ Unit unit_of(const Params& p, int u) {
   Unit r;
   r.i0 = (t % p.tiles_x) * TX;
   r.j0 = (t / p.tiles_x) * TY;
-  r.k0 = static_cast<int>((long long)kb * p.nk / p.kchunks);
-  r.kc = static_cast<int>((long long)(kb + 1) * p.nk / p.kchunks) - r.k0;
+  const int nk = p.k_hi - p.k_lo;
+  r.k0 = p.k_lo + static_cast<int>((long long)kb * nk / p.kchunks);
+  r.kc = p.k_lo + static_cast<int>((long long)(kb + 1) * nk / p.kchunks) - r.k0;
   return r;
 }
 
@@ -260,8 +262,8 @@ bool supports(const lf::Plan& plan, std::string& why) {
   return true;
 }
 
-int launch_step(const double* in, double* out, int ni, int nj, int nk, bool wrap_k, cudaStream_t st,
-                std::string& err) {
+int launch_step(const double* in, double* out, int ni, int nj, int nk, int k_lo, int k_hi, bool wrap_k,
+                cudaStream_t st, std::string& err) {
   const Variant& v = variant();
   static int slots = 0;
   if (!slots) {
@@ -285,7 +287,9 @@ int launch_step(const double* in, double* out, int ni, int nj, int nk, bool wrap
   p.pk = (long long)(ni + 2) * (nj + 2);
   p.tiles_x = ni / TX;
   p.tiles = (ni / TX) * (nj / v.ty);
-  p.kchunks = (nk + v.kch - 1) / v.kch;
+  p.k_lo = k_lo;
+  p.k_hi = k_hi;
+  p.kchunks = std::max(1, (k_hi - k_lo + v.kch - 1) / v.kch);
   p.units = p.tiles * p.kchunks;
   p.wrap_i = 1;
   p.wrap_j = 1;
@@ -300,12 +304,10 @@ int launch_step(const double* in, double* out, int ni, int nj, int nk, bool wrap
 
 int run(const ExecArgs& a, std::string& err) {
   const auto& r = a.plan->rs.ranges;
-  int nk = (int)r[0].trips(), nj = (int)r[1].trips(), ni = (int)r[2].trips();
-  bool wrap_k = true;
-  if (a.slab) {
-    nk = (int)(a.slab->hi - a.slab->lo);
-    wrap_k = false;  // k ghosts of a slab come from the caller's halo exchange
-  }
+  const int nj = (int)r[1].trips(), ni = (int)r[2].trips();
+  const RowPart rp = row_part(a, (int)r[0].trips());
+  const int nk = rp.rows;
+  const bool wrap_k = a.slab == nullptr;  // k ghosts of a slab come from the caller's halo exchange
   const double* src = static_cast<const double*>(a.terms[0]);
   double* goal = static_cast<double*>(a.terms[1]);
   double* scratch = a.steps > 1 ? static_cast<double*>(a.scratch[0]) : nullptr;
@@ -314,7 +316,7 @@ int run(const ExecArgs& a, std::string& err) {
   for (int s = 0; s < a.steps; ++s) {
     bool to_goal = ((a.steps - 1 - s) % 2) == 0;
     double* dst = to_goal ? goal : scratch;
-    int st = launch_step(src, dst, ni, nj, nk, wrap_k, a.stream, err);
+    int st = launch_step(src, dst, ni, nj, nk, rp.lo, rp.hi, wrap_k, a.stream, err);
     if (st != LF_OK) return st;
     src = dst;
   }

@@ -44,7 +44,8 @@ constexpr int XBUF = 4 * NPRIM + 8 * NQ + 4 * NT;  // doubles per x-sweep buffer
 constexpr int SMEM = S * STAGE_BYTES + XBUF * 8 + S * 8 + 128;
 
 struct Params {
-  int ni, nj;            // interior of this launch (slab rows for multi-GPU)
+  int ni, nj;            // interior of this launch's domain (slab rows for multi-GPU)
+  int row_lo, row_hi;    // rows this launch computes
   long long pitch;       // ni + 4
   int strips;
   int ghost_top, ghost_bottom;  // refill reflective ghost rows at these faces
@@ -103,7 +104,7 @@ __global__ void __launch_bounds__(NT, MINB) hydro_fused(const __grid_constant__ 
 
   // ---- segment list (strip-major row ranges) and stage bookkeeping
   RowSeg seg[3];
-  const int nseg = cta_segments(blockIdx.x, gridDim.x, p.strips, p.nj, seg);
+  const int nseg = cta_segments(blockIdx.x, gridDim.x, p.strips, p.row_lo, p.row_hi, seg);
   int nst[3], total = 0;
   for (int k = 0; k < nseg; ++k) {
     nst[k] = (seg[k].je - seg[k].jb + 2 * H + 1 + R - 1) / R;  // marched rows jb-2 .. je+2
@@ -281,8 +282,9 @@ bool supports(const lf::Plan& plan, std::string& why) {
   return true;
 }
 
-int launch_step(const double* const in[4], double* const out[4], const double* dtdx, int ni, int nj, bool top,
-                bool bottom, cudaStream_t st, std::string& err) {
+int launch_step(const double* const in[4], double* const out[4], const double* dtdx, int ni, const RowPart& rp,
+                cudaStream_t st, std::string& err) {
+  const int nj = rp.rows;
   // LF_HYDRO_VARIANT: register budget for 2 / 3 / 4 (default) CTAs per SM: on
   // this latency-bound fp64 code 4 resident CTAs beat the spill-free budget
   static void (*kern)(Maps, Params) = nullptr;
@@ -310,24 +312,28 @@ int launch_step(const double* const in[4], double* const out[4], const double* d
   p.nj = nj;
   p.pitch = ni + 4;
   p.strips = (ni + W - 1) / W;
-  p.ghost_top = top;
-  p.ghost_bottom = bottom;
+  p.row_lo = rp.lo;
+  p.row_hi = rp.hi;
+  p.ghost_top = rp.top;
+  p.ghost_bottom = rp.bottom;
   p.dtdx = dtdx;
   for (int a = 0; a < 4; ++a) p.out[a] = out[a];
-  const long long work = (long long)p.strips * nj;
-  const int ctas = static_cast<int>(std::max<long long>(1, std::min<long long>(slots, work / 8)));
+  const long long work = (long long)p.strips * (rp.hi - rp.lo);
+  // each CTA must get at most 3 row segments (rowstream.cuh): at least
+  // ceil(strips/2) CTAs when the row range is short
+  const long long want = std::max<long long>(work / 8, (p.strips + 1) / 2);
+  const int ctas = static_cast<int>(std::max<long long>(1, std::min<long long>(slots, want)));
+  if ((long long)ctas * 2 < p.strips) {
+    err = "row range too short for the resident grid";
+    return LF_ERR_UNSUPPORTED;
+  }
   return cuda_status(launch_pdl(kern, dim3(ctas), dim3(NT), SMEM, st, maps, p), "hydro_fused launch", err);
 }
 
 int run(const ExecArgs& a, std::string& err) {
   const auto& r = a.plan->rs.ranges;
-  int nj = (int)r[0].trips(), ni = (int)r[1].trips();
-  bool top = true, bottom = true;
-  if (a.slab) {
-    nj = (int)(a.slab->hi - a.slab->lo);
-    top = a.slab->lo == 0;
-    bottom = a.slab->hi == a.slab->global;
-  }
+  const int ni = (int)r[1].trips();
+  const RowPart rp = row_part(a, (int)r[0].trips());
   // terminals: g_rho g_mx g_my g_E g_dtdx | g_rho_n g_mx_n g_my_n g_E_n
   const double* src[4];
   double* goal[4];
@@ -340,7 +346,7 @@ int run(const ExecArgs& a, std::string& err) {
   const double* dtdx = static_cast<const double*>(a.terms[4]);
   for (int s = 0; s < a.steps; ++s) {
     double* const* dst = ((a.steps - 1 - s) % 2) == 0 ? goal : scr;
-    int stt = launch_step(src, dst, dtdx, ni, nj, top, bottom, a.stream, err);
+    int stt = launch_step(src, dst, dtdx, ni, rp, a.stream, err);
     if (stt != LF_OK) return stt;
     for (int v = 0; v < 4; ++v) src[v] = dst[v];
   }

@@ -27,8 +27,9 @@ struct RowSeg {
   int strip, jb, je;  // output rows [jb, je) of column strip `strip`
 };
 
-// Segments of CTA `cta` of `ctas` over `strips` strips of `nj` rows each.
-__device__ __forceinline__ int cta_segments(int cta, int ctas, int strips, int nj, RowSeg* seg) {
+// Segments of CTA `cta` of `ctas` over `strips` strips of rows [r0, r1).
+__device__ __forceinline__ int cta_segments(int cta, int ctas, int strips, int r0, int r1, RowSeg* seg) {
+  const int nj = r1 - r0;
   const long long total = (long long)strips * nj;
   long long a = total * cta / ctas, b = total * (cta + 1) / ctas;
   int n = 0;
@@ -36,8 +37,8 @@ __device__ __forceinline__ int cta_segments(int cta, int ctas, int strips, int n
     const int s = static_cast<int>(a / nj);
     const long long end = std::min<long long>(b, (long long)(s + 1) * nj);
     seg[n].strip = s;
-    seg[n].jb = static_cast<int>(a - (long long)s * nj);
-    seg[n].je = static_cast<int>(end - (long long)s * nj);
+    seg[n].jb = r0 + static_cast<int>(a - (long long)s * nj);
+    seg[n].je = r0 + static_cast<int>(end - (long long)s * nj);
     ++n;
     a = end;
   }

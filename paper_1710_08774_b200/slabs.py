@@ -49,29 +49,24 @@ def exchange(bufs: Sequence[torch.Tensor], halo: Halo, rank: int, world: int, gr
         return
     up = rank + 1 if rank + 1 < world else (0 if halo.periodic else None)
     down = rank - 1 if rank > 0 else (world - 1 if halo.periodic else None)
+    # dim-0 row blocks of a contiguous buffer are contiguous: send from and
+    # receive into the buffers directly (no staging copies)
     ops = []
-    recvs = []
     for b in bufs:
         n = b.shape[0] - halo.lo - halo.hi
         if up is not None and halo.lo:
-            ops.append(dist.P2POp(dist.isend, b[n:n + halo.lo].contiguous(), up, group))
+            ops.append(dist.P2POp(dist.isend, b[n:n + halo.lo], up, group))
         if down is not None and halo.hi:
-            ops.append(dist.P2POp(dist.isend, b[halo.lo:halo.lo + halo.hi].contiguous(), down, group))
+            ops.append(dist.P2POp(dist.isend, b[halo.lo:halo.lo + halo.hi], down, group))
     for b in bufs:
         n = b.shape[0] - halo.lo - halo.hi
         if down is not None and halo.lo:
-            t = torch.empty_like(b[:halo.lo])
-            ops.append(dist.P2POp(dist.irecv, t, down, group))
-            recvs.append((b[:halo.lo], t))
+            ops.append(dist.P2POp(dist.irecv, b[:halo.lo], down, group))
         if up is not None and halo.hi:
-            t = torch.empty_like(b[halo.lo + n:])
-            ops.append(dist.P2POp(dist.irecv, t, up, group))
-            recvs.append((b[halo.lo + n:], t))
+            ops.append(dist.P2POp(dist.irecv, b[halo.lo + n:], up, group))
     if ops:
         for r in dist.batch_isend_irecv(ops):
             r.wait()
-    for dst, t in recvs:
-        dst.copy_(t)
 
 
 def run_slabs(step: Callable[[Sequence[torch.Tensor], Sequence[torch.Tensor]], None],
@@ -83,5 +78,38 @@ def run_slabs(step: Callable[[Sequence[torch.Tensor], Sequence[torch.Tensor]], N
     for _ in range(steps):
         step(src, dst)
         exchange(dst, halo, rank, world, group)
+        src, dst = dst, src
+    return src
+
+
+def run_slabs_overlapped(launch: Callable[[Sequence[torch.Tensor], Sequence[torch.Tensor], tuple[int, int]], None],
+                         state: Sequence[torch.Tensor], scratch: Sequence[torch.Tensor], steps: int, halo: Halo,
+                         rank: int, world: int, rows: int, group=None,
+                         comm_stream: "torch.cuda.Stream | None" = None) -> Sequence[torch.Tensor]:
+    """Like run_slabs, with the face exchange overlapped with the interior.
+
+    Each step: launch(src, dst, part) computes the slab-local output rows the
+    neighbours need first -- [0, halo.hi) and [rows-halo.lo, rows) -- then the
+    exchange of those rows runs on `comm_stream` while the interior rows
+    [halo.hi, rows-halo.lo) are computed on the current stream; the next step
+    starts once both are done.  Falls back to the sequential schedule on CPU
+    tensors or when the slab is too thin to have an interior."""
+    src, dst = list(state), list(scratch)
+    cuda = src[0].is_cuda
+    inner_lo, inner_hi = halo.hi, rows - halo.lo
+    if not cuda or inner_hi - inner_lo < 1:
+        return run_slabs(lambda s, d: launch(s, d, (0, rows)), state, scratch, steps, halo, rank, world, group)
+    main = torch.cuda.current_stream()
+    comm = comm_stream or torch.cuda.Stream(device=src[0].device, priority=-1)
+    for _ in range(steps):
+        if halo.hi:
+            launch(src, dst, (0, halo.hi))
+        if halo.lo:
+            launch(src, dst, (rows - halo.lo, rows))
+        comm.wait_stream(main)
+        with torch.cuda.stream(comm):
+            exchange(dst, halo, rank, world, group)
+        launch(src, dst, (inner_lo, inner_hi))
+        main.wait_stream(comm)
         src, dst = dst, src
     return src

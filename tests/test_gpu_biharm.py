@@ -68,3 +68,22 @@ def test_slab_rows_leave_internal_ghosts_to_the_exchange():
     got = out.cpu().numpy()
     assert np.array_equal(bits(got[2:-2]), bits(ref[10:18]))
     assert np.all(got[:2, 2:-2] == 5.0) and np.all(got[-2:, 2:-2] == 5.0)
+
+
+@pytest.mark.parametrize("name,gen,shape", [
+    ("biharmonic2d", lambda s: [inputs.biharm_input(*s, seed=2)], (40, 256)),
+    ("box2x", lambda s: [inputs.box_input(*s, seed=2)], (40, 256)),
+])
+def test_row_parts_compose_to_the_whole_slab(name, gen, shape):
+    import torch
+    plan = lf.Plan.with_ranges(name, shape)
+    ax = [torch.from_numpy(a).cuda() for a in gen(shape)]
+    g = plan.goals[0]
+    dt = torch.float64 if g.elem_bytes == 8 else torch.float32
+    whole = torch.zeros(g.extent, dtype=dt, device="cuda")
+    parts = torch.zeros(g.extent, dtype=dt, device="cuda")
+    plan.run_slab(ax + [whole], 0, shape[0], shape[0])
+    for part in [(0, 2), (shape[0] - 2, shape[0]), (2, shape[0] - 2)]:
+        plan.run_slab(ax + [parts], 0, shape[0], shape[0], part=part)
+    torch.cuda.synchronize()
+    assert torch.equal(whole, parts)

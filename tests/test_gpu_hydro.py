@@ -59,3 +59,19 @@ def test_full_size_4096_matches_fused_cpu_and_conserves():
     # reflective walls conserve mass and energy to rounding
     for v in (0, 3):
         assert got[v][2:-2, 2:-2].sum() == pytest.approx(st[v][2:-2, 2:-2].sum(), rel=1e-12)
+
+
+def test_row_parts_compose_to_the_whole_slab():
+    import torch
+    shape = (40, 300)
+    plan = lf.Plan.with_ranges("hydro2d", shape)
+    st, dtdx = inputs.hydro_input(*shape, seed=9)
+    ax = [torch.from_numpy(a).cuda() for a in st] + [torch.tensor([dtdx], dtype=torch.float64, device="cuda")]
+    whole = [torch.zeros_like(ax[0]) for _ in range(4)]
+    parts = [torch.zeros_like(ax[0]) for _ in range(4)]
+    plan.run_slab(ax + whole, 0, 40, 40)
+    for part in [(0, 2), (38, 40), (2, 38)]:
+        plan.run_slab(ax + parts, 0, 40, 40, part=part)
+    torch.cuda.synchronize()
+    for a, b in zip(whole, parts):
+        assert torch.equal(a, b)
