@@ -8,6 +8,7 @@
 #include <functional>
 #include <sstream>
 
+#include "fusion.hpp"
 #include "planner.hpp"
 
 namespace lf {
@@ -214,35 +215,13 @@ std::optional<Plan> make_plan(const RuleSet& rs_in, DiagList& diags) {
   }
   const size_t ng = P.groups.size();
 
-  // ---- single-nest check ------------------------------------------------------
-  // Every BASELINE chain fuses into one nest with no split:
-  // all computing groups span the full loop order over the declared ranges
-  // and no kernel changes rank (no reduction/broadcast, fusion.cpp:8-21).
-  {
-    bool ok = true;
-    int computing = 0;
-    for (const auto& cg : P.groups) {
-      if (cg.kind == RapKind::load) continue;
-      ++computing;
-      if (cg.kind == RapKind::kernel && rs.kernels[cg.kernel].associative) ok = false;
-      if (cg.space.size() != nd) ok = false;
-    }
-    for (const auto& r : g.raps) {
-      if (r.kind != RapKind::kernel) continue;
-      size_t out_rank = 0, in_max = 0, in_min = SIZE_MAX;
-      for (int t : r.out_terms) out_rank = std::max(out_rank, g.terms[t].dims.size());
-      for (int t : r.in_terms) {
-        size_t k = g.terms[t].dims.size();
-        if (k == 0) continue;  // rank-0 parameters (scalars) broadcast trivially
-        in_max = std::max(in_max, k);
-        in_min = std::min(in_min, k);
-      }
-      if (in_max > out_rank || (in_min != SIZE_MAX && in_min < out_rank)) ok = false;
-    }
-    P.one_nest = ok;
-    P.nests = ok ? 1 : computing;
-    P.splits = 0;
-  }
+  // ---- nest fusion (nests.cpp:294-315, fusion.cpp:8-372) --------------------
+  const FusionResult fr = fuse_groups(rs, g, P.groups, P.group_of);
+  P.nests = fr.nests;
+  P.splits = fr.splits;
+  P.one_nest = fr.nests == 1 && fr.splits == 0;
+  P.vertex_of_group = fr.vertex_of_group;
+  auto vertex_of_rap = [&](int rap) { return fr.vertex_of_group[P.group_of[rap]]; };
 
   // ---- pipeline shifts (shifts.cpp:8-79) --------------------------------------
   P.shifts.assign(ng, std::vector<int>(nd, 0));
@@ -262,6 +241,7 @@ std::optional<Plan> make_plan(const RuleSet& rs_in, DiagList& diags) {
     for (const auto& e : g.edges) {
       int gp = P.group_of[e.from], gc = P.group_of[e.to];
       if (gp == gc || g.raps[e.from].kind == RapKind::load) continue;
+      if (vertex_of_rap(e.from) != vertex_of_rap(e.to)) continue;  // only intra-nest edges constrain
       gadj[gp].insert(gc);
     }
     std::vector<int> indeg(ng, 0);
@@ -286,6 +266,7 @@ std::optional<Plan> make_plan(const RuleSet& rs_in, DiagList& diags) {
         if (P.group_of[e.from] != gi) continue;
         int gc = P.group_of[e.to];
         if (gc == gi) continue;
+        if (vertex_of_rap(e.from) != vertex_of_rap(e.to)) continue;
         auto delta = member_delta(e.to);
         for (const auto& o : g.terms[e.term].dims) {
           int r = o.offset - delta[o.dim];
@@ -346,9 +327,27 @@ std::optional<Plan> make_plan(const RuleSet& rs_in, DiagList& diags) {
       }
     }
   }
+  // associative carry: the carry input and the output share one buffer
+  // (storage.cpp:93-105)
+  for (const auto& r : g.raps) {
+    if (r.kind != RapKind::kernel || !rs.kernels[r.kernel].associative) continue;
+    const ConcreteTerm& out = g.terms[r.out_terms[0]];
+    const int vo = var_of.at({out.tag, out.ident});
+    for (int t : r.in_terms) {
+      const ConcreteTerm& ti = g.terms[t];
+      if (ti.ident == out.ident && ti.dims == out.dims && !(ti == out)) {
+        int vi = var_of.at({ti.tag, ti.ident});
+        while (P.vars[vi].alias_of >= 0) vi = P.vars[vi].alias_of;
+        int vc = vo;
+        while (P.vars[vc].alias_of >= 0) vc = P.vars[vc].alias_of;
+        if (vi != vc) P.vars[vi].alias_of = vc;
+      }
+    }
+  }
   for (auto& v : P.vars) {
     std::vector<long> mn(nd, LONG_MAX), mx(nd, LONG_MIN), rmn(nd, LONG_MAX), rmx(nd, LONG_MIN);
     bool writes = false;
+    std::set<int> vertices;  // fused nests touching the variable
     for (const auto& t : g.terms) {
       if (var_of.at({t.tag, t.ident}) != v.id) continue;
       for (const auto& o : t.dims) {
@@ -367,12 +366,40 @@ std::optional<Plan> make_plan(const RuleSet& rs_in, DiagList& diags) {
           rmx[o.dim] = std::max(rmx[o.dim], rel);
         }
       };
+      for (int t : r.out_terms)
+        if (var_of.at({g.terms[t].tag, g.terms[t].ident}) == v.id) vertices.insert(vertex_of_rap(r.id));
+      for (int t : r.in_terms)
+        if (var_of.at({g.terms[t].tag, g.terms[t].ident}) == v.id) vertices.insert(vertex_of_rap(r.id));
       if (r.kind == RapKind::load) continue;
       for (int t : r.in_terms) touch(t);
       for (int t : r.out_terms) {
         if (var_of.at({g.terms[t].tag, g.terms[t].ident}) == v.id) writes = true;
         touch(t);
       }
+    }
+    {
+      // a is visited before b iff offset(a) >lex offset(b): the path is the
+      // distinct read offsets in descending lexicographic order
+      std::set<std::vector<int>> reads;
+      for (const auto& r : g.raps)
+        for (int t : r.in_terms) {
+          const auto& ct = g.terms[t];
+          if (var_of.at({ct.tag, ct.ident}) != v.id) continue;
+          std::vector<int> off(nd, 0);
+          for (const auto& o : ct.dims) off[o.dim] = o.offset;
+          reads.insert(off);
+        }
+      std::string path;
+      for (auto it = reads.rbegin(); it != reads.rend(); ++it) {
+        if (!path.empty()) path += " -> ";
+        path += "(";
+        for (size_t k = it->size(); k-- > 0;) {
+          path += ((*it)[k] > 0 ? "+" : "") + std::to_string((*it)[k]);
+          if (k) path += ",";
+        }
+        path += ")";
+      }
+      v.reuse_path = path;
     }
     v.extents.clear();
     v.spans.clear();
@@ -385,8 +412,8 @@ std::optional<Plan> make_plan(const RuleSet& rs_in, DiagList& diags) {
     }
     if (!v.external.empty()) {
       v.scheme = Scheme::terminal;
-    } else if (!writes || !P.one_nest) {
-      v.scheme = Scheme::full;
+    } else if (!writes || vertices.size() > 1) {
+      v.scheme = Scheme::full;  // crosses a split: lives across nests (storage.cpp:325-329)
     } else {
       v.rotating_dim = -1;
       for (size_t k = 0; k < v.dims.size(); ++k)
@@ -480,6 +507,7 @@ std::optional<Plan> make_plan(const RuleSet& rs_in, DiagList& diags) {
     std::map<std::vector<int>, long> terms;
     std::set<std::string> counted;
     for (const auto& v : P.vars) {
+      if (v.alias_of >= 0) continue;
       std::vector<int> mono;
       long coeff = 1;
       if (v.scheme == Scheme::terminal) {
@@ -625,7 +653,9 @@ std::string Plan::report_json() const {
     const auto& v = vars[i];
     os << (i ? "," : "") << "{\"name\":" << json_str(v.name) << ",\"type\":" << json_str(v.type)
        << ",\"scheme\":" << json_str(scheme_name(v.scheme)) << ",\"span\":" << v.span << ",\"rotating_dim\":"
-       << v.rotating_dim << ",\"external\":" << json_str(v.external) << ",\"extents\":[";
+       << v.rotating_dim << ",\"alias_of\":" << v.alias_of << ",\"reuse_path\":" << json_str(v.reuse_path)
+       << ",\"external\":" << json_str(v.external)
+       << ",\"extents\":[";
     for (size_t k = 0; k < v.extents.size(); ++k)
       os << (k ? "," : "") << "[" << v.extents[k].first << "," << v.extents[k].second << "]";
     os << "],\"spans\":[";

@@ -247,6 +247,7 @@ struct Variable {
   std::string tag, ident, name, type;
   std::vector<int> dims;
   int producer_group = -1;
+  int alias_of = -1;     // associative carry unified with the output (storage.cpp:93-105)
   std::string external;  // backing terminal ("" for intermediates)
   bool axiom_backed = false;
   // buffer_extents (storage.cpp:403-427): per variable dim {extent, base}
@@ -256,6 +257,9 @@ struct Variable {
   int rotating_dim = -1;
   long span = 1;
   std::vector<long> spans;  // per variable dim
+  // reuse Hamiltonian path (storage.cpp:124-141, R/SPEC.md:387-395): distinct
+  // read offsets, first visit first, rendered innermost dim first
+  std::string reuse_path;
 };
 
 struct Terminal {
@@ -274,6 +278,7 @@ struct Plan {
   DataflowDAG dag;
   std::vector<CallsiteGroup> groups;
   std::vector<int> group_of;
+  std::vector<int> vertex_of_group;      // group -> fused nest (fusion.cpp:171-372)
   std::vector<std::vector<int>> shifts;  // group -> per dim (shifts.cpp:8-79)
   std::vector<Variable> vars;
   std::vector<Terminal> terminals;  // axioms (declaration order) then goals

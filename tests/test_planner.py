@@ -204,3 +204,50 @@ def test_ranges_rewrite_and_size_constraints():
     assert p.executor == "heat3d_fused_tma"
     q = lf.Plan.with_ranges("heat3d", (8, 30, 64))  # N_j not a multiple of 16
     assert q.executor == ""
+
+
+FIXTURES = ["normalization", "cosmo", "laplace3"]
+FIXDIR = lf.PKG_DIR.parent / "tests" / "specs"
+
+
+@pytest.mark.parametrize("name", FIXTURES)
+def test_fixture_bookkeeping_matches_reference(name):
+    path = FIXDIR / f"{name}.lf"
+    ref = ref_or_skip(path)
+    mine = lf.Plan.from_file(path).report()
+    assert (mine["terms"], mine["raps"], mine["edges"]) == (ref["terms"], ref["raps"], ref["edges"])
+    assert (mine["nests"], mine["splits"]) == (ref["nests"], ref["splits"])
+    assert mine["footprint"] == ref["footprint"]
+    rv = {v["name"]: v for v in ref["variables"]}
+    for v in mine["variables"]:
+        if v["alias_of"] >= 0:
+            continue  # associative carry folded into its output (storage.cpp:93-105)
+        r = rv[v["name"]]
+        assert v["extents"] == r["extents"], v["name"]
+        if v["scheme"] not in ("terminal", "scalar"):
+            assert (v["scheme"], v["span"]) == (r["scheme"], r["span"]), v["name"]
+
+
+def test_spec_acceptance_criteria():
+    # R/SPEC.md:633 -- normalization: 2 nests, 1 concave split
+    n = lf.Plan.from_file(FIXDIR / "normalization.lf").report()
+    assert (n["nests"], n["splits"]) == (2, 1)
+    assert n["footprint"] == "3*N_j*N_i + 2*N_j + 1"
+    # R/SPEC.md:634 -- COSMO: one nest, buffers 2 (fluxes) and 3 (Laplacian), O(2 NkNjNi + 5 Ni + 2)
+    c = lf.Plan.from_file(FIXDIR / "cosmo.lf").report()
+    v = {x["name"]: x for x in c["variables"]}
+    assert c["nests"] == 1 and c["footprint"] == "2*N_k*N_j*N_i + 5*N_i + 2"
+    assert (v["lap"]["scheme"], v["lap"]["span"]) == ("outer_rotate", 3)
+    assert v["fx"]["span"] == 2 and v["fy"]["span"] == 2
+    # R/SPEC.md:635 -- 1-D 3-point on an intermediate: inner_circular(3)
+    l3 = lf.Plan.from_file(FIXDIR / "laplace3.lf").report()
+    y = next(x for x in l3["variables"] if x["name"] == "y")
+    assert (y["scheme"], y["span"]) == ("inner_circular", 3)
+    # R/SPEC.md:636 -- reuse Hamiltonian path of the 5-point stencil
+    l5 = lf.Plan(LAPLACE5, "laplace5.lf").report()
+    cell = next(x for x in l5["variables"] if x["name"] == "cell")
+    assert cell["reuse_path"] == "(0,+1) -> (+1,0) -> (0,0) -> (-1,0) -> (0,-1)"
+    # Hydro2D: both sweeps fuse into one nest, 5-row window of the x-swept state
+    h = lf.Plan.bundled("hydro2d").report()
+    assert h["nests"] == 1 and h["splits"] == 0
+    assert next(x for x in h["variables"] if x["name"] == "rho1")["span"] == 5
