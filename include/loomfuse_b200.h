@@ -109,8 +109,14 @@ int lf_plan_terminal(const lf_plan* plan, int idx, lf_terminal* out);
  * *needed when non-NULL. */
 int lf_plan_report(const lf_plan* plan, char* buf, size_t cap, size_t* needed);
 
-/* Name of the fused executor the plan dispatches to, or "" if none. */
+/* Name of the fused executor the plan dispatches to, or "" if none: a
+ * hand-written sm_100a executor whose chain signature matches, else the
+ * generic "jit_tiled_fused" executor (kernels with `body:` expressions,
+ * lowered to CUDA and compiled for sm_100a by NVRTC at plan creation). */
 const char* lf_plan_executor(const lf_plan* plan);
+
+/* CUDA source the generic executor generated for this plan ("" otherwise). */
+const char* lf_plan_source(const lf_plan* plan);
 
 /* Run the chain `steps` times on DEVICE buffers (axioms then goals, sized per
  * lf_plan_terminal), stream-ordered on `cuda_stream` (a cudaStream_t, NULL =

@@ -121,11 +121,97 @@ std::string q(const std::string& s) { return "\"" + s + "\""; }
 
 }  // namespace
 
+std::string jstr(const std::string& s) {
+  std::string o = "\"";
+  for (char c : s) {
+    if (c == '"' || c == '\\') o += '\\';
+    if (c == '\n') {
+      o += "\\n";
+      continue;
+    }
+    o += c;
+  }
+  return o + "\"";
+}
+
+// --dag: the reference's inference DAG plus the rule bodies, for the generic
+// run_naive in oracle/generic.py
+void dump_dag(const lf::RuleSet& mine, const loomfuse::RuleSet& rs, const loomfuse::DataflowDAG& dag,
+              const loomfuse::StoragePlan& sp) {
+  std::ostringstream os;
+  os << "{\"loop_order\":[";
+  for (size_t d = 0; d < rs.loop_order.size(); ++d) os << (d ? "," : "") << jstr(rs.loop_order[d]);
+  os << "],\"ranges\":[";
+  for (size_t d = 0; d < rs.ranges.size(); ++d) os << (d ? "," : "") << "[" << rs.ranges[d].lo << "," << rs.ranges[d].hi << "]";
+  os << "],\"terms\":[";
+  for (size_t t = 0; t < dag.terms.size(); ++t) {
+    const auto& ct = dag.terms[t];
+    os << (t ? "," : "") << "{\"tag\":" << jstr(ct.tag) << ",\"ident\":" << jstr(ct.ident) << ",\"dims\":[";
+    for (size_t k = 0; k < ct.dims.size(); ++k) os << (k ? "," : "") << "[" << ct.dims[k].dim << "," << ct.dims[k].offset << "]";
+    os << "]}";
+  }
+  os << "],\"raps\":[";
+  for (size_t r = 0; r < dag.raps.size(); ++r) {
+    const auto& rp = dag.raps[r];
+    const char* kind = rp.kind == loomfuse::RapKind::kernel ? "kernel" : rp.kind == loomfuse::RapKind::load ? "load" : "store";
+    os << (r ? "," : "") << "{\"kind\":\"" << kind << "\",\"kernel\":" << jstr(rp.kind == loomfuse::RapKind::kernel ? rs.kernels[rp.kernel].name : "")
+       << ",\"external\":" << jstr(rp.external) << ",\"in\":[";
+    for (size_t k = 0; k < rp.in_terms.size(); ++k) os << (k ? "," : "") << rp.in_terms[k];
+    os << "],\"out\":[";
+    for (size_t k = 0; k < rp.out_terms.size(); ++k) os << (k ? "," : "") << rp.out_terms[k];
+    os << "],\"slots\":[";
+    for (size_t k = 0; k < rp.ext_slots.size(); ++k) os << (k ? "," : "") << "[" << rp.ext_slots[k].dim << "," << rp.ext_slots[k].shift << "]";
+    os << "]}";
+  }
+  os << "],\"topo\":[";
+  auto order = dag.topo_order();
+  for (size_t k = 0; k < order.size(); ++k) os << (k ? "," : "") << order[k];
+  os << "],\"kernels\":{";
+  for (size_t k = 0; k < mine.kernels.size(); ++k) {
+    const auto& kr = mine.kernels[k];
+    os << (k ? "," : "") << jstr(kr.name) << ":{\"declaration\":" << jstr(kr.declaration) << ",\"inputs\":[";
+    for (size_t i = 0; i < kr.inputs.size(); ++i) os << (i ? "," : "") << jstr(kr.inputs[i].first);
+    os << "],\"outputs\":[";
+    for (size_t i = 0; i < kr.outputs.size(); ++i) os << (i ? "," : "") << jstr(kr.outputs[i].first);
+    os << "],\"bodies\":{";
+    size_t b = 0;
+    for (const auto& [pn, e] : kr.bodies) os << (b++ ? "," : "") << jstr(pn) << ":" << jstr(e);
+    os << "}}";
+  }
+  os << "},\"externals\":{";
+  size_t e = 0;
+  for (const auto& v : sp.vars.vars) {
+    if (v.alias_of >= 0 || !v.terminal()) continue;
+    auto ext = loomfuse::buffer_extents(v.id, sp.vars, dag, rs);
+    os << (e++ ? "," : "") << jstr(v.backing->external) << ":{\"type\":" << jstr(v.type) << ",\"axiom\":" << (v.axiom_backed ? "true" : "false")
+       << ",\"extents\":[";
+    for (size_t k = 0; k < ext.size(); ++k) os << (k ? "," : "") << "[" << ext[k].first << "," << ext[k].second << "]";
+    os << "]}";
+  }
+  os << "},\"axioms\":[";
+  for (size_t a = 0; a < mine.axioms.size(); ++a) os << (a ? "," : "") << jstr(mine.axioms[a].external.name);
+  os << "],\"goals\":[";
+  for (size_t a = 0; a < mine.goals.size(); ++a) os << (a ? "," : "") << jstr(mine.goals[a].external.name);
+  os << "],\"iterate\":[";
+  for (size_t a = 0; a < mine.iterate.size(); ++a) os << (a ? "," : "") << "[" << jstr(mine.iterate[a].first) << "," << jstr(mine.iterate[a].second) << "]";
+  os << "],\"boundary\":{";
+  size_t bcount = 0;
+  for (const auto& [ext, modes] : mine.boundary) {
+    os << (bcount++ ? "," : "") << jstr(ext) << ":[";
+    for (size_t k = 0; k < modes.size(); ++k) os << (k ? "," : "") << jstr(lf::boundary_name(modes[k]));
+    os << "]";
+  }
+  os << "}}";
+  std::cout << os.str() << "\n";
+}
+
 int main(int argc, char** argv) {
-  if (argc != 2) {
-    std::cerr << "usage: refplan <spec.lf>\n";
+  bool want_dag = argc == 3 && std::string(argv[1]) == "--dag";
+  if (argc != 2 && !want_dag) {
+    std::cerr << "usage: refplan [--dag] <spec.lf>\n";
     return 2;
   }
+  if (want_dag) argv[1] = argv[2];
   std::ifstream f(argv[1]);
   std::stringstream ss;
   ss << f.rdbuf();
@@ -148,6 +234,10 @@ int main(int argc, char** argv) {
     loomfuse::InestDAG inest = loomfuse::build_inest_dag(dag, grouping, rs);
     loomfuse::FusionResult fusion = loomfuse::fuse_inest_dag(inest, dag, grouping, rs);
     loomfuse::StoragePlan sp = loomfuse::analyze_storage(rs, dag, grouping, fusion, rs.vector_length);
+    if (want_dag) {
+      dump_dag(*mine, rs, dag, sp);
+      return 0;
+    }
 
     std::ostringstream os;
     os << "{\"terms\":" << dag.terms.size() << ",\"raps\":" << dag.raps.size() << ",\"edges\":" << dag.edges.size()

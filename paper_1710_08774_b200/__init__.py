@@ -37,7 +37,7 @@ ABI_SYMBOLS = (
     "lf_plan_create", "lf_plan_destroy", "lf_plan_num_terminals", "lf_plan_terminal",
     "lf_plan_report", "lf_plan_executor", "lf_run", "lf_run_host", "lf_run_slab",
     "lf_plan_launches_per_step", "lf_plan_compulsory_bytes_per_cell", "lf_last_error",
-    "lf_version", "lf_spec_print",
+    "lf_version", "lf_spec_print", "lf_plan_source",
 )
 
 
@@ -92,6 +92,8 @@ def lib() -> ctypes.CDLL:
     L.lf_plan_report.argtypes = [P, ctypes.c_char_p, ctypes.c_size_t, ctypes.POINTER(ctypes.c_size_t)]
     L.lf_plan_executor.argtypes = [P]
     L.lf_plan_executor.restype = ctypes.c_char_p
+    L.lf_plan_source.argtypes = [P]
+    L.lf_plan_source.restype = ctypes.c_char_p
     L.lf_run.argtypes = [P, ctypes.POINTER(P), ctypes.c_int, ctypes.c_int, P]
     L.lf_run_host.argtypes = [P, ctypes.POINTER(P), ctypes.c_int, ctypes.c_int]
     L.lf_run_slab.argtypes = [P, ctypes.POINTER(P), ctypes.c_int, ctypes.POINTER(_Slab), P]
@@ -203,6 +205,11 @@ class Plan:
     @property
     def executor(self) -> str:
         return lib().lf_plan_executor(self._h).decode()
+
+    @property
+    def source(self) -> str:
+        """CUDA source of the generic executor ("" for hand-written executors)."""
+        return lib().lf_plan_source(self._h).decode()
 
     @property
     def launches_per_step(self) -> int:

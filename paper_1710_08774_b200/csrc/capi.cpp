@@ -6,12 +6,14 @@
 
 #include <algorithm>
 #include <cstring>
+#include <memory>
 #include <mutex>
 #include <string>
 #include <vector>
 
 #include "../../include/loomfuse_b200.h"
 #include "exec/exec.hpp"
+#include "jit/jit.hpp"
 #include "planner/planner.hpp"
 
 namespace {
@@ -55,6 +57,7 @@ const std::vector<Signed>& signed_executors() {
 struct lf_plan {
   lf::Plan plan;
   const lfx::Executor* exec = nullptr;
+  std::shared_ptr<lfx::JitKernel> jit;  // generic executor when no built-in matches
   std::string unsupported;  // why no executor applies
   std::string report;
   std::mutex mu;            // guards the device caches below
@@ -104,7 +107,7 @@ std::vector<void*> scratch_list(lf_plan* p) {
 
 int check_run_args(const lf_plan* plan, void* const* terms, int nterm, int steps) {
   if (!plan) return fail(LF_ERR_SPEC, "plan is NULL");
-  if (!plan->exec)
+  if (!plan->exec && !plan->jit)
     return fail(LF_ERR_UNSUPPORTED, "no fused sm_100a executor for chain '" + plan->plan.rs.name +
                                         "' (signature " + plan->plan.signature + "): " + plan->unsupported);
   if (nterm != static_cast<int>(plan->plan.terminals.size()))
@@ -157,7 +160,12 @@ int lf_plan_create(const char* spec_text, size_t len, const char* filename, lf_p
       }
       why = std::string(s.exec->name) + ": " + w;
     }
-    if (!p->exec) p->unsupported = why;
+    if (!p->exec) {
+      // generic path: `body:` chains compiled for sm_100a with NVRTC
+      std::string jwhy;
+      p->jit = lfx::JitKernel::build(p->plan, jwhy);
+      if (!p->jit) p->unsupported = why + "; generic executor: " + jwhy;
+    }
     *out = p;
     return LF_OK;
   } catch (const std::exception& e) {
@@ -224,12 +232,30 @@ int lf_plan_report(const lf_plan* plan, char* buf, size_t cap, size_t* needed) {
   return LF_OK;
 }
 
-const char* lf_plan_executor(const lf_plan* plan) { return plan && plan->exec ? plan->exec->name : ""; }
+const char* lf_plan_executor(const lf_plan* plan) {
+  if (!plan) return "";
+  if (plan->exec) return plan->exec->name;
+  return plan->jit ? "jit_tiled_fused" : "";
+}
 
-int lf_plan_launches_per_step(const lf_plan* plan) { return plan && plan->exec ? plan->exec->launches_per_step : 0; }
+int lf_plan_launches_per_step(const lf_plan* plan) {
+  if (!plan) return 0;
+  if (plan->exec) return plan->exec->launches_per_step;
+  return plan->jit ? (plan->jit->program().has_fill ? 2 : 1) : 0;
+}
 
 double lf_plan_compulsory_bytes_per_cell(const lf_plan* plan) {
-  return plan && plan->exec ? plan->exec->bytes_per_cell : 0.0;
+  if (!plan) return 0.0;
+  if (plan->exec) return plan->exec->bytes_per_cell;
+  if (!plan->jit) return 0.0;
+  double b = 0;  // every non-scalar terminal read or written once per cell
+  for (const auto& t : plan->plan.terminals)
+    if (!t.dims.empty()) b += t.elem_bytes;
+  return b;
+}
+
+const char* lf_plan_source(const lf_plan* plan) {
+  return plan && plan->jit ? plan->jit->program().source.c_str() : "";
 }
 
 int lf_run(const lf_plan* cplan, void* const* terms, int nterm, int steps, void* cuda_stream) {
@@ -251,7 +277,7 @@ int lf_run(const lf_plan* cplan, void* const* terms, int nterm, int steps, void*
     a.steps = steps;
     a.stream = static_cast<cudaStream_t>(cuda_stream);
     a.scratch = scratch.data();
-    st = plan->exec->run(a, err);
+    st = plan->exec ? plan->exec->run(a, err) : plan->jit->run(a, err);
     if (st != LF_OK) return fail(st, err);
     return LF_OK;
   } catch (const std::exception& e) {
@@ -296,7 +322,7 @@ int lf_run_host(const lf_plan* cplan, void* const* terms, int nterm, int steps) 
     a.steps = steps;
     a.stream = plan->stream;
     a.scratch = scratch.data();
-    st = plan->exec->run(a, err);
+    st = plan->exec ? plan->exec->run(a, err) : plan->jit->run(a, err);
     if (st != LF_OK) return fail(st, err);
     for (size_t i = 0; i < T.size(); ++i) {
       if (!T[i].is_goal) continue;
@@ -329,7 +355,7 @@ int lf_run_slab(const lf_plan* cplan, void* const* terms, int nterm, const lf_sl
     a.stream = static_cast<cudaStream_t>(cuda_stream);
     a.slab = slab;
     std::string err;
-    st = cplan->exec->run(a, err);
+    st = cplan->exec ? cplan->exec->run(a, err) : cplan->jit->run(a, err);
     if (st != LF_OK) return fail(st, err);
     return LF_OK;
   } catch (const std::exception& e) {

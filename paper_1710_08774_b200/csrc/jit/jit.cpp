@@ -1,0 +1,230 @@
+// Generic fused executor, part 2: NVRTC compilation for sm_100a (libnvrtc is
+// opened at first use, so the library still loads where NVRTC is absent) and
+// module loading / launching through the driver entry points the runtime
+// exposes (no -lcuda).  Same numerics contract as the hand-written
+// executors: -fmad=false, IEEE division and square root.
+#include "jit.hpp"
+
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <dlfcn.h>
+
+#include <algorithm>
+#include <cstring>
+#include <mutex>
+
+namespace lfx {
+
+namespace {
+
+// ---- NVRTC through dlopen ----------------------------------------------------
+typedef int nvrtcResult_t;
+struct Nvrtc {
+  void* h = nullptr;
+  int (*create)(void**, const char*, const char*, int, const char* const*, const char* const*) = nullptr;
+  int (*compile)(void*, int, const char* const*) = nullptr;
+  int (*log_size)(void*, size_t*) = nullptr;
+  int (*log)(void*, char*) = nullptr;
+  int (*cubin_size)(void*, size_t*) = nullptr;
+  int (*cubin)(void*, char*) = nullptr;
+  int (*destroy)(void**) = nullptr;
+  std::string error;
+};
+
+const Nvrtc& nvrtc() {
+  static Nvrtc n;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    const char* names[] = {"libnvrtc.so.12", "/usr/local/cuda/lib64/libnvrtc.so.12", "libnvrtc.so"};
+    for (const char* nm : names)
+      if ((n.h = dlopen(nm, RTLD_NOW | RTLD_LOCAL))) break;
+    if (!n.h) {
+      n.error = "libnvrtc.so.12 not found";
+      return;
+    }
+    auto sym = [&](const char* s) { return dlsym(n.h, s); };
+    n.create = reinterpret_cast<decltype(n.create)>(sym("nvrtcCreateProgram"));
+    n.compile = reinterpret_cast<decltype(n.compile)>(sym("nvrtcCompileProgram"));
+    n.log_size = reinterpret_cast<decltype(n.log_size)>(sym("nvrtcGetProgramLogSize"));
+    n.log = reinterpret_cast<decltype(n.log)>(sym("nvrtcGetProgramLog"));
+    n.cubin_size = reinterpret_cast<decltype(n.cubin_size)>(sym("nvrtcGetCUBINSize"));
+    n.cubin = reinterpret_cast<decltype(n.cubin)>(sym("nvrtcGetCUBIN"));
+    n.destroy = reinterpret_cast<decltype(n.destroy)>(sym("nvrtcDestroyProgram"));
+    if (!n.create || !n.compile || !n.cubin || !n.destroy) n.error = "libnvrtc symbols missing";
+  });
+  return n;
+}
+
+// ---- driver entry points -------------------------------------------------------
+struct Drv {
+  PFN_cuModuleLoadData_v2000 load = nullptr;
+  PFN_cuModuleGetFunction_v2000 get = nullptr;
+  PFN_cuLaunchKernel_v4000 launch = nullptr;
+  PFN_cuFuncSetAttribute_v9000 attr = nullptr;
+  PFN_cuModuleUnload_v2000 unload = nullptr;
+  bool ok = false;
+};
+
+const Drv& drv() {
+  static Drv d;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    auto get = [](const char* name, void** p) {
+      cudaDriverEntryPointQueryResult q;
+      return cudaGetDriverEntryPoint(name, p, cudaEnableDefault, &q) == cudaSuccess && q == cudaDriverEntryPointSuccess;
+    };
+    d.ok = get("cuModuleLoadData", reinterpret_cast<void**>(&d.load)) &&
+           get("cuModuleGetFunction", reinterpret_cast<void**>(&d.get)) &&
+           get("cuLaunchKernel", reinterpret_cast<void**>(&d.launch)) &&
+           get("cuFuncSetAttribute", reinterpret_cast<void**>(&d.attr)) &&
+           get("cuModuleUnload", reinterpret_cast<void**>(&d.unload));
+  });
+  return d;
+}
+
+struct Args {
+  void* t[32];
+  long long n0;
+  int row_lo, row_hi, top, bottom;
+};
+
+}  // namespace
+
+std::shared_ptr<JitKernel> JitKernel::build(const lf::Plan& plan, std::string& why) {
+  auto k = std::shared_ptr<JitKernel>(new JitKernel);
+  if (plan.terminals.size() > 32) {
+    why = "more than 32 terminals";
+    return nullptr;
+  }
+  if (!jit_generate(plan, k->prog_)) {
+    why = k->prog_.error;
+    return nullptr;
+  }
+  // compile now (plan creation) so errors surface early; loading waits for a device
+  const Nvrtc& n = nvrtc();
+  if (!n.error.empty()) {
+    why = "generic executor unavailable: " + n.error;
+    return nullptr;
+  }
+  void* prog = nullptr;
+  if (n.create(&prog, k->prog_.source.c_str(), "lf_chain.cu", 0, nullptr, nullptr) != 0) {
+    why = "nvrtcCreateProgram failed";
+    return nullptr;
+  }
+  const char* opts[] = {"--gpu-architecture=sm_100a", "-fmad=false", "-prec-div=true", "-prec-sqrt=true",
+                        "-std=c++17", "-lineinfo"};
+  const int rc = n.compile(prog, 6, opts);
+  if (rc != 0) {
+    size_t ls = 0;
+    n.log_size(prog, &ls);
+    std::string log(ls, '\0');
+    if (ls) n.log(prog, log.data());
+    n.destroy(&prog);
+    why = "NVRTC failed to compile the generated chain:\n" + log;
+    return nullptr;
+  }
+  size_t cs = 0;
+  n.cubin_size(prog, &cs);
+  k->cubin_.resize(cs);
+  n.cubin(prog, k->cubin_.data());
+  n.destroy(&prog);
+  return k;
+}
+
+JitKernel::~JitKernel() {
+  if (module_ && drv().ok) drv().unload(static_cast<CUmodule>(module_));
+}
+
+int JitKernel::launch(void* fn, dim3 grid, dim3 block, size_t smem, cudaStream_t st, void* args, std::string& err) {
+  void* params[] = {args};
+  CUresult r = drv().launch(static_cast<CUfunction>(fn), grid.x, grid.y, grid.z, block.x, block.y, block.z,
+                            static_cast<unsigned>(smem), reinterpret_cast<CUstream>(st), params, nullptr);
+  if (r != CUDA_SUCCESS) {
+    err = "cuLaunchKernel failed with CUresult " + std::to_string(static_cast<int>(r));
+    return LF_ERR_CUDA;
+  }
+  return LF_OK;
+}
+
+int JitKernel::run(const ExecArgs& a, std::string& err) {
+  const Drv& d = drv();
+  if (!d.ok) {
+    err = "CUDA driver entry points unavailable";
+    return LF_ERR_CUDA;
+  }
+  if (!module_) {
+    cudaFree(nullptr);  // make sure the primary context exists
+    CUmodule m;
+    CUresult r = d.load(&m, cubin_.data());
+    if (r != CUDA_SUCCESS) {
+      err = "cuModuleLoadData failed with CUresult " + std::to_string(static_cast<int>(r));
+      return LF_ERR_CUDA;
+    }
+    module_ = m;
+    CUfunction f;
+    if (d.get(&f, m, "lf_jit_step") != CUDA_SUCCESS) {
+      err = "generated kernel missing";
+      return LF_ERR_INTERNAL;
+    }
+    step_ = f;
+    if (d.get(&f, m, "lf_jit_fill") == CUDA_SUCCESS) fill_ = f;
+    d.attr(static_cast<CUfunction>(step_), CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES,
+           static_cast<int>(prog_.smem_bytes));
+  }
+  const auto& rs = a.plan->rs;
+  const auto& T = a.plan->terminals;
+  const int nd = prog_.nd;
+  const RowPart rp = row_part(a, (int)rs.ranges[0].trips());
+  Args args;
+  std::memset(&args, 0, sizeof args);
+  args.n0 = rp.rows;
+  args.row_lo = rp.lo;
+  args.row_hi = rp.hi;
+  args.top = rp.top;
+  args.bottom = rp.bottom;
+  dim3 grid(1, 1, 1);
+  const std::vector<int>& tile = prog_.tile;
+  auto tiles = [&](long n, int t) { return static_cast<unsigned>((n + t - 1) / t); };
+  for (int dd = 0; dd < nd; ++dd) {
+    const long n = dd == 0 ? (rp.hi - rp.lo) : rs.ranges[dd].trips();
+    const unsigned c = tiles(n, tile[dd]);
+    const int axis = nd - 1 - dd;
+    (axis == 0 ? grid.x : axis == 1 ? grid.y : grid.z) = c;
+  }
+  // ping-pong as the built-in executors: goals of the last step land in the
+  // goal buffers, intermediate states in plan-owned scratch, axioms untouched
+  std::vector<void*> src(a.terms, a.terms + T.size());
+  std::vector<int> iter_axiom(T.size(), -1);  // goal terminal -> paired axiom terminal
+  for (const auto& [gname, aname] : rs.iterate) {
+    int gi = -1, ai = -1;
+    for (size_t i = 0; i < T.size(); ++i) {
+      if (T[i].is_goal && T[i].name == gname) gi = static_cast<int>(i);
+      if (!T[i].is_goal && T[i].name == aname) ai = static_cast<int>(i);
+    }
+    if (gi >= 0 && ai >= 0) iter_axiom[gi] = ai;
+  }
+  int scratch_idx = 0;
+  std::vector<void*> scratch(T.size(), nullptr);
+  for (size_t i = 0; i < T.size(); ++i)
+    if (iter_axiom[i] >= 0 && a.steps > 1) scratch[i] = a.scratch[scratch_idx++];
+  std::vector<void*> cur = src;
+  for (int s = 0; s < a.steps; ++s) {
+    const bool to_goal = ((a.steps - 1 - s) % 2) == 0;
+    std::vector<void*> bufs = cur;
+    for (size_t i = 0; i < T.size(); ++i)
+      if (T[i].is_goal) bufs[i] = (to_goal || iter_axiom[i] < 0) ? a.terms[i] : scratch[i];
+    for (size_t i = 0; i < T.size(); ++i) args.t[i] = bufs[i];
+    int st = launch(step_, grid, dim3(prog_.threads), prog_.smem_bytes, a.stream, &args, err);
+    if (st != LF_OK) return st;
+    if (fill_ && prog_.has_fill) {
+      st = launch(fill_, dim3(592), dim3(256), 0, a.stream, &args, err);
+      if (st != LF_OK) return st;
+    }
+    // the goals just written feed the paired axioms of the next step
+    for (size_t i = 0; i < T.size(); ++i)
+      if (iter_axiom[i] >= 0) cur[iter_axiom[i]] = bufs[i];
+  }
+  return LF_OK;
+}
+
+}  // namespace lfx

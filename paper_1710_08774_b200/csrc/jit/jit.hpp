@@ -1,0 +1,47 @@
+// Generic fused executor: `body:` chains lowered to CUDA (codegen.cpp) and
+// compiled for sm_100a at plan creation with NVRTC (jit.cpp).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "../exec/exec.hpp"
+#include "../planner/planner.hpp"
+
+namespace lfx {
+
+struct JitProgram {
+  std::string source;
+  std::string type;  // "double" / "float"
+  int elem_bytes = 8;
+  int nd = 0;
+  std::vector<int> tile;  // per loop dim, outermost first
+  size_t smem_bytes = 0;
+  int threads = 256;
+  bool has_fill = false;
+  std::string error;  // why the chain is not supported
+};
+
+bool jit_generate(const lf::Plan& plan, JitProgram& out);
+
+// A compiled chain; owned by one plan.
+class JitKernel {
+ public:
+  static std::shared_ptr<JitKernel> build(const lf::Plan& plan, std::string& why);
+  int run(const ExecArgs& a, std::string& err);
+  const JitProgram& program() const { return prog_; }
+  ~JitKernel();
+
+ private:
+  JitProgram prog_;
+  void* module_ = nullptr;  // CUmodule
+  void* step_ = nullptr;    // CUfunction
+  void* fill_ = nullptr;
+  std::vector<char> cubin_;
+  int launch(void* fn, dim3 grid, dim3 block, size_t smem, cudaStream_t st, void* args, std::string& err);
+};
+
+}  // namespace lfx

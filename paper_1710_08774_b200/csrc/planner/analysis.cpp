@@ -299,7 +299,7 @@ std::optional<Plan> make_plan(const RuleSet& rs_in, DiagList& diags) {
     P.vars.push_back(v);
     return v.id;
   };
-  for (const auto& t : g.terms) get_var(t);
+  for (const auto& t : g.terms) P.var_of_term.push_back(get_var(t));
   for (const auto& r : g.raps) {
     if (r.kind == RapKind::load) {
       Variable& v = P.vars[get_var(g.terms[r.out_terms[0]])];

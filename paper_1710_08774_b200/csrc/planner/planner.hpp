@@ -281,6 +281,7 @@ struct Plan {
   std::vector<int> vertex_of_group;      // group -> fused nest (fusion.cpp:171-372)
   std::vector<std::vector<int>> shifts;  // group -> per dim (shifts.cpp:8-79)
   std::vector<Variable> vars;
+  std::vector<int> var_of_term;     // term -> variable
   std::vector<Terminal> terminals;  // axioms (declaration order) then goals
   int nests = 0;
   int splits = 0;
