@@ -90,6 +90,13 @@ WORKLOADS = {
                   gen=_hydro_inputs, slab=_hydro_slab, dtype="f64", halo=(2, 2, False)),
     "hydro_large": dict(config_index=4, spec="hydro2d", sizes=(32768, 32768), chain_steps=10,
                         gen=_hydro_inputs, slab=_hydro_slab, dtype="f64", halo=(2, 2, False)),
+    # the same chains written with `body:` expressions: the generic NVRTC path
+    "heat3d_jit": dict(config_index=1, spec="examples/heat3d_body", sizes=(512, 512, 512), chain_steps=50,
+                       gen=_heat3d_inputs, slab=_heat3d_slab, dtype="f64", halo=(1, 1, True)),
+    "biharm_jit": dict(config_index=0, spec="examples/biharm_body", sizes=(4096, 4096), chain_steps=100,
+                       gen=_biharm_inputs, slab=_biharm_slab, dtype="f64", halo=(2, 2, False)),
+    "box_jit": dict(config_index=3, spec="examples/box_body", sizes=(16384, 16384), chain_steps=1,
+                    gen=_box_inputs, slab=_box_slab, dtype="f32", halo=None),
 }
 
 
@@ -174,6 +181,7 @@ def cpu_runner(name, w):
     """The HFAV-style fused CPU schedule (oracle/) on one bounded unit of the
     workload with all host threads: returns (run, cell-updates per run, text)."""
     import oracle
+    name = name.replace("_jit", "")
     threads = oracle.max_threads()
     sizes = w["sizes"]
     if name == "heat3d":

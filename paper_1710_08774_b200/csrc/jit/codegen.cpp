@@ -247,7 +247,8 @@ bool jit_generate(const lf::Plan& P, JitProgram& out) {
   src << "typedef " << T << " T;\n";
   src << "__device__ __forceinline__ T lf_min(T a, T b) { return a < b ? a : b; }\n";
   src << "__device__ __forceinline__ T lf_max(T a, T b) { return a > b ? a : b; }\n";
-  src << "struct LfArgs { void* t[" << std::max<size_t>(1, terms.size()) << "]; long long n0; int row_lo, row_hi, top, bottom; };\n";
+  // must match lfx::Args in jit.cpp (passed by value)
+  src << "struct LfArgs { void* t[32]; long long n0; int row_lo, row_hi, top, bottom; };\n";
   src << "extern \"C\" __global__ void __launch_bounds__(" << out.threads << ") lf_jit_step(const LfArgs a) {\n";
   src << "  extern __shared__ __align__(16) unsigned char lf_smem[];\n";
   // tile origin: innermost dim on blockIdx.x, next on y, outermost on z (or y for 2D)
