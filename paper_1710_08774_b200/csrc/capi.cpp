@@ -235,7 +235,7 @@ int lf_plan_report(const lf_plan* plan, char* buf, size_t cap, size_t* needed) {
 const char* lf_plan_executor(const lf_plan* plan) {
   if (!plan) return "";
   if (plan->exec) return plan->exec->name;
-  return plan->jit ? "jit_tiled_fused" : "";
+  return plan->jit ? (plan->jit->program().march ? "jit_window_fused" : "jit_tiled_fused") : "";
 }
 
 int lf_plan_launches_per_step(const lf_plan* plan) {

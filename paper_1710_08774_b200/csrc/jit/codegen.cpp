@@ -1,12 +1,26 @@
 // Generic fused executor, part 1: lowering a planned single-nest chain whose
 // kernels carry `body:` expressions (R/SPEC.md:82) to sm_100a CUDA source --
-// the role of the reference's missing codegen (R/SPEC.md:449-514), retargeted:
-// instead of one serial loop nest with rolling buffers, one CTA per output
-// tile evaluates every callsite group in dataflow order over the tile plus the
-// halo the planner derived for it, keeping each intermediate in shared memory
-// (contraction to a tile-sized window); only terminals touch HBM.
+// the role of the reference's missing codegen (R/SPEC.md:449-514), retargeted
+// to the GPU:
+//
+//  * 2D/3D chains (`emit_march`): the HFAV schedule itself.  A CTA owns a tile
+//    of the inner loop dimensions and marches the outermost one; at trip t
+//    callsite group g computes row t + s_g, s_g being the pipeline shift
+//    (the recurrence of shifts.cpp:8-79: a producer runs at least as far ahead
+//    as its furthest-reading consumer).  Every intermediate lives in a
+//    shared-memory rolling window of W_v rows (the contraction of
+//    storage.cpp:319-399: W_v = lead of the producer - oldest row any consumer
+//    still reads + 1); axioms are streamed into their own windows by cp.async
+//    one trip ahead.  Only terminals touch HBM.
+//  * 1D chains (`emit_tiled`): one CTA per tile, each group evaluated over the
+//    tile plus the halo the planner derived for it.
+//
+// Ghost refill of iterated goals (`config: boundary:`) is a second kernel that
+// visits ghost cells only.
 #include <algorithm>
 #include <climits>
+#include <cstdio>
+#include <cstdlib>
 #include <deque>
 #include <map>
 #include <sstream>
@@ -24,19 +38,92 @@ std::string elem_type(const std::string& t) {
   return "";
 }
 
-}  // namespace
+std::string plus(long off) {
+  if (!off) return "";
+  return (off > 0 ? " + " : " - ") + std::to_string(std::labs(off));
+}
 
-bool jit_generate(const lf::Plan& P, JitProgram& out) {
+struct GIn {
+  std::string param;
+  int var;
+  std::vector<int> rel;
+};
+struct GOut {
+  std::string param;
+  int var;
+  std::vector<int> rel;
+};
+struct Grp {
+  int kernel;
+  std::vector<int> gmin, gmax;
+  std::vector<GIn> in;
+  std::vector<GOut> out;
+  int shift = 0;  // lead along the outermost dimension (march schedule)
+  int level = 1;  // dependency level (groups of one level share a barrier)
+};
+
+// everything the emitters share
+struct Ctx {
+  const lf::Plan& P;
+  int nd = 0;
+  std::string T;
+  std::vector<long> N;
+  std::vector<std::vector<int>> vmin, vmax;  // per var, per dim: term offset range
+  std::map<int, std::vector<int>> axiom_extra;
+  std::vector<char> smem_var;  // kernel outputs read by some kernel
+  std::vector<Grp> groups;     // kernel groups, dataflow order
+  std::string error;
+
+  explicit Ctx(const lf::Plan& p) : P(p) {}
+
+  int terminal_of(int v, bool goal) const {
+    for (size_t i = 0; i < P.terminals.size(); ++i)
+      if (P.terminals[i].var == v && P.terminals[i].is_goal == goal) return static_cast<int>(i);
+    return -1;
+  }
+  long pitch(const lf::Terminal& t, size_t slot) const {
+    long p = 1;
+    for (size_t k = slot + 1; k < t.extent.size(); ++k) p *= t.extent[k];
+    return p;
+  }
+  // flat index of terminal `ti` at term-frame position pos[d] (+ extra[d])
+  std::string tidx(int ti, const std::vector<std::string>& pos, const std::vector<int>& extra) const {
+    const auto& t = P.terminals[ti];
+    std::string e;
+    for (size_t s = 0; s < t.dims.size(); ++s) {
+      const int d = t.dims[s];
+      const long off = extra[d] - t.base[s];
+      const std::string c = "(long long)(" + pos[d] + plus(off) + ")";
+      const long p = pitch(t, s);
+      e += (e.empty() ? "" : " + ") + c + (p != 1 ? " * " + std::to_string(p) + "LL" : "");
+    }
+    return e.empty() ? std::string("0") : e;
+  }
+  std::vector<int> extra_of(int v) const {
+    auto it = axiom_extra.find(v);
+    return it == axiom_extra.end() ? std::vector<int>(nd, 0) : it->second;
+  }
+  // full-rank axiom terminal backing variable v (or -1)
+  int staged_axiom(int v) const {
+    const int ti = terminal_of(v, false);
+    if (ti < 0 || (int)P.terminals[ti].dims.size() != nd) return -1;
+    return ti;
+  }
+};
+
+bool analyse(Ctx& C) {
+  const lf::Plan& P = C.P;
   const auto& rs = P.rs;
   const auto& g = P.dag;
   const int nd = static_cast<int>(rs.loop_order.size());
   auto fail = [&](const std::string& m) {
-    out.error = m;
+    C.error = m;
     return false;
   };
   if (nd < 1 || nd > 3) return fail("generic executor handles 1-3 loop dimensions");
-  if (!P.one_nest) return fail("chain does not fuse into a single nest (" + std::to_string(P.nests) + " nests, " +
-                               std::to_string(P.splits) + " splits)");
+  if (!P.one_nest)
+    return fail("chain does not fuse into a single nest (" + std::to_string(P.nests) + " nests, " +
+                std::to_string(P.splits) + " splits)");
   for (const auto& r : rs.ranges)
     if (r.stride != 1) return fail("generic executor needs unit strides");
   // ---- element type: one type for the whole chain
@@ -53,39 +140,35 @@ bool jit_generate(const lf::Plan& P, JitProgram& out) {
     if (e.empty() || e != T) return fail("intermediate '" + v.name + "' has type '" + v.type + "'");
     if ((int)v.dims.size() != nd) return fail("intermediate '" + v.name + "' does not span every loop dimension");
   }
-  out.type = T;
-  out.elem_bytes = T == "double" ? 8 : 4;
-  out.nd = nd;
-  std::vector<long> N(nd);
-  for (int d = 0; d < nd; ++d) N[d] = rs.ranges[d].trips();
+  C.T = T;
+  C.nd = nd;
+  C.N.resize(nd);
+  for (int d = 0; d < nd; ++d) C.N[d] = rs.ranges[d].trips();
 
   // ---- per-variable term offset ranges (relative to the canonical cell)
   const size_t nv = P.vars.size();
-  std::vector<std::vector<int>> vmin(nv, std::vector<int>(nd, INT_MAX)), vmax(nv, std::vector<int>(nd, INT_MIN));
+  C.vmin.assign(nv, std::vector<int>(nd, INT_MAX));
+  C.vmax.assign(nv, std::vector<int>(nd, INT_MIN));
   for (size_t t = 0; t < g.terms.size(); ++t) {
     int v = P.var_of_term[t];
     for (const auto& o : g.terms[t].dims) {
-      vmin[v][o.dim] = std::min(vmin[v][o.dim], o.offset);
-      vmax[v][o.dim] = std::max(vmax[v][o.dim], o.offset);
+      C.vmin[v][o.dim] = std::min(C.vmin[v][o.dim], o.offset);
+      C.vmax[v][o.dim] = std::max(C.vmax[v][o.dim], o.offset);
     }
   }
+  for (size_t v = 0; v < nv; ++v)
+    for (int d = 0; d < nd; ++d)
+      if (C.vmin[v][d] == INT_MAX) C.vmin[v][d] = C.vmax[v][d] = 0;
   auto canon = [&](int v) {
     while (P.vars[v].alias_of >= 0) v = P.vars[v].alias_of;
     return v;
   };
-  // terminal index of a variable (axiom or goal buffer)
-  auto terminal_of = [&](int v, bool goal) {
-    for (size_t i = 0; i < P.terminals.size(); ++i)
-      if (P.terminals[i].var == v && P.terminals[i].is_goal == goal) return static_cast<int>(i);
-    return -1;
-  };
   // axiom variables: storage displacement extra[d] = ext shift - term offset
-  std::map<int, std::vector<int>> axiom_extra;
   for (const auto& r : g.raps) {
     if (r.kind != lf::RapKind::load) continue;
     const auto& term = g.terms[r.out_terms[0]];
     const int v = P.var_of_term[r.out_terms[0]];
-    if (axiom_extra.count(v)) continue;
+    if (C.axiom_extra.count(v)) continue;
     std::vector<int> ex(nd, 0);
     for (const auto& s : r.ext_slots) {
       if (s.dim < 0) return fail("axioms with constant subscripts are not supported by the generic executor");
@@ -94,172 +177,135 @@ bool jit_generate(const lf::Plan& P, JitProgram& out) {
         if (o.dim == s.dim) off = o.offset;
       ex[s.dim] = s.shift - off;
     }
-    axiom_extra[v] = ex;
+    C.axiom_extra[v] = ex;
   }
-  // which variables live in shared memory: kernel outputs that some kernel reads
-  std::vector<char> read_by_kernel(nv, 0), smem_var(nv, 0);
+  // which variables live on chip: kernel outputs that some kernel reads
+  std::vector<char> read_by_kernel(nv, 0);
+  C.smem_var.assign(nv, 0);
   for (const auto& r : g.raps)
     if (r.kind == lf::RapKind::kernel)
       for (int t : r.in_terms) read_by_kernel[canon(P.var_of_term[t])] = 1;
   for (size_t v = 0; v < nv; ++v)
     if (read_by_kernel[v] && !P.vars[v].axiom_backed && P.vars[v].alias_of < 0 && !P.vars[v].dims.empty())
-      smem_var[v] = 1;
+      C.smem_var[v] = 1;
 
   // ---- kernel groups in dataflow order
-  struct GIn {
-    std::string param;
-    int var;
-    std::vector<int> rel;
-  };
-  struct GOut {
-    std::string param;
-    int var;
-    std::vector<int> rel;
-  };
-  struct Grp {
-    int kernel;
-    std::vector<int> gmin, gmax;
-    std::vector<GIn> in;
-    std::vector<GOut> out;
-  };
-  std::vector<Grp> groups;
-  {
-    const int ng = static_cast<int>(P.groups.size());
-    std::vector<std::set<int>> adj(ng);
-    std::vector<int> indeg(ng, 0);
-    for (const auto& e : g.edges) {
-      int a = P.group_of[e.from], b = P.group_of[e.to];
-      if (a != b && adj[a].insert(b).second) ++indeg[b];
-    }
-    std::deque<int> q;
-    for (int i = 0; i < ng; ++i)
-      if (!indeg[i]) q.push_back(i);
-    std::vector<int> order;
-    while (!q.empty()) {
-      int v = q.front();
-      q.pop_front();
-      order.push_back(v);
-      for (int w : adj[v])
-        if (--indeg[w] == 0) q.push_back(w);
-    }
-    for (int gi : order) {
-      const auto& cg = P.groups[gi];
-      if (cg.kind != lf::RapKind::kernel) continue;
-      const auto& k = rs.kernels[cg.kernel];
-      if (k.associative) return fail("associative kernels need the reduction path (not in the generic executor)");
-      for (const auto& [op, pat] : k.outputs)
-        if (!k.bodies.count(op))
-          return fail("kernel '" + k.name + "' has no body for output '" + op +
-                      "' (the generic executor compiles `body:` expressions)");
-      const lf::Rap& rep = g.raps[cg.members[0]];
-      std::vector<int> anchor(nd, 0);
-      for (const auto& o : g.terms[rep.out_terms[0]].dims) anchor[o.dim] = o.offset;
-      Grp G;
-      G.kernel = cg.kernel;
-      G.gmin = cg.min_disp(nd);
-      G.gmax = cg.max_disp(nd);
-      for (size_t i = 0; i < k.inputs.size(); ++i) {
-        GIn in{k.inputs[i].first, canon(P.var_of_term[rep.in_terms[i]]), std::vector<int>(nd, 0)};
-        const auto& term = g.terms[rep.in_terms[i]];
-        if (!term.dims.empty() && (int)term.dims.size() != nd)
-          return fail("kernel '" + k.name + "' reads a partial-rank term");
-        for (const auto& o : term.dims) in.rel[o.dim] = o.offset - anchor[o.dim];
-        G.in.push_back(in);
-      }
-      for (size_t i = 0; i < k.outputs.size(); ++i) {
-        GOut o{k.outputs[i].first, canon(P.var_of_term[rep.out_terms[i]]), std::vector<int>(nd, 0)};
-        for (const auto& od : g.terms[rep.out_terms[i]].dims) o.rel[od.dim] = od.offset - anchor[od.dim];
-        G.out.push_back(o);
-      }
-      groups.push_back(std::move(G));
-    }
+  const int ng = static_cast<int>(P.groups.size());
+  std::vector<std::set<int>> adj(ng);
+  std::vector<int> indeg(ng, 0);
+  for (const auto& e : g.edges) {
+    int a = P.group_of[e.from], b = P.group_of[e.to];
+    if (a != b && adj[a].insert(b).second) ++indeg[b];
   }
-
-  // ---- tile shape and shared-memory layout (shrink the tile until it fits)
-  std::vector<int> tile(nd);
-  if (nd == 1) tile = {256};
-  if (nd == 2) tile = {8, 32};
-  if (nd == 3) tile = {4, 4, 32};
-  std::vector<size_t> soff(nv, 0);
-  size_t smem = 0;
-  auto layout = [&] {
-    smem = 0;
-    for (size_t v = 0; v < nv; ++v) {
-      if (!smem_var[v]) continue;
-      size_t n = 1;
-      for (int d = 0; d < nd; ++d) n *= tile[d] + (vmax[v][d] - vmin[v][d]);
-      soff[v] = smem;
-      smem += (n * out.elem_bytes + 15) / 16 * 16;
-    }
-  };
-  layout();
-  while (smem > 96 * 1024) {
-    int d = 0;  // halve the largest outer tile dimension, keep the innermost >= 32
-    for (int k = 0; k < nd; ++k)
-      if ((k < nd - 1 ? tile[k] : tile[k] / 4) > (d < nd - 1 ? tile[d] : tile[d] / 4)) d = k;
-    if (tile[d] <= 1 || (d == nd - 1 && tile[d] <= 32)) break;
-    tile[d] /= 2;
-    layout();
+  std::deque<int> q;
+  for (int i = 0; i < ng; ++i)
+    if (!indeg[i]) q.push_back(i);
+  std::vector<int> order;
+  while (!q.empty()) {
+    int v = q.front();
+    q.pop_front();
+    order.push_back(v);
+    for (int w : adj[v])
+      if (--indeg[w] == 0) q.push_back(w);
   }
-  if (smem > 200 * 1024) return fail("chain needs too much on-chip storage for one tile");
-  out.tile = tile;
-  out.smem_bytes = smem;
-  out.threads = 256;
-
-  // ---- terminal addressing
-  const auto& terms = P.terminals;
-  std::ostringstream src;
-  auto pitch = [&](const lf::Terminal& t, int slot) {
-    long p = 1;
-    for (size_t k = slot + 1; k < t.extent.size(); ++k) p *= t.extent[k];
-    return p;
-  };
-  // index expression of terminal `ti` at logical cell x[d] + rel[d] (+ axiom extra)
-  auto tindex = [&](int ti, const std::vector<int>& rel, const std::vector<int>& extra) {
-    const auto& t = terms[ti];
-    std::string e;
-    for (size_t s = 0; s < t.dims.size(); ++s) {
-      const int d = t.dims[s];
-      long off = rel[d] + extra[d] - t.base[s];
-      std::string c = "(x" + std::to_string(d) + (off ? (off > 0 ? " + " : " - ") + std::to_string(std::labs(off)) : "") + ")";
-      long p = pitch(t, static_cast<int>(s));
-      e += (e.empty() ? "" : " + ") + c + (p != 1 ? " * " + std::to_string(p) + "LL" : "");
+  for (int gi : order) {
+    const auto& cg = P.groups[gi];
+    if (cg.kind != lf::RapKind::kernel) continue;
+    const auto& k = rs.kernels[cg.kernel];
+    if (k.associative) return fail("associative kernels need the reduction path (not in the generic executor)");
+    for (const auto& [op, pat] : k.outputs)
+      if (!k.bodies.count(op))
+        return fail("kernel '" + k.name + "' has no body for output '" + op +
+                    "' (the generic executor compiles `body:` expressions)");
+    const lf::Rap& rep = g.raps[cg.members[0]];
+    std::vector<int> anchor(nd, 0);
+    for (const auto& o : g.terms[rep.out_terms[0]].dims) anchor[o.dim] = o.offset;
+    Grp G;
+    G.kernel = cg.kernel;
+    G.gmin = cg.min_disp(nd);
+    G.gmax = cg.max_disp(nd);
+    for (size_t i = 0; i < k.inputs.size(); ++i) {
+      GIn in{k.inputs[i].first, canon(P.var_of_term[rep.in_terms[i]]), std::vector<int>(nd, 0)};
+      const auto& term = g.terms[rep.in_terms[i]];
+      if (!term.dims.empty() && (int)term.dims.size() != nd)
+        return fail("kernel '" + k.name + "' reads a partial-rank term");
+      for (const auto& o : term.dims) in.rel[o.dim] = o.offset - anchor[o.dim];
+      if (!C.smem_var[in.var] && C.terminal_of(in.var, false) < 0)
+        return fail("kernel '" + k.name + "' reads '" + in.param + "' from an unsupported source");
+      G.in.push_back(in);
     }
-    return e.empty() ? std::string("0") : e;
-  };
-  auto sidx = [&](int v, const std::string& rel_expr_prefix, const std::vector<int>& rel) {
-    // shared-memory index of variable v at tile-relative cell c + rel
-    std::string e;
-    for (int d = 0; d < nd; ++d) {
-      long width = tile[d] + (vmax[v][d] - vmin[v][d]);
-      long off = rel[d] - vmin[v][d];
-      std::string c = "(c" + std::to_string(d) + (off ? (off > 0 ? " + " : " - ") + std::to_string(std::labs(off)) : "") + ")";
-      if (d == 0)
-        e = c;
-      else
-        e = "(" + e + ") * " + std::to_string(width) + " + " + c;
+    for (size_t i = 0; i < k.outputs.size(); ++i) {
+      GOut o{k.outputs[i].first, canon(P.var_of_term[rep.out_terms[i]]), std::vector<int>(nd, 0)};
+      for (const auto& od : g.terms[rep.out_terms[i]].dims) o.rel[od.dim] = od.offset - anchor[od.dim];
+      G.out.push_back(o);
     }
-    (void)rel_expr_prefix;
-    return e;
-  };
+    C.groups.push_back(std::move(G));
+  }
+  // ---- pipeline shifts along dim 0 (reverse dataflow order) and levels
+  const int nG = static_cast<int>(C.groups.size());
+  for (int gi = nG - 1; gi >= 0; --gi) {
+    Grp& G = C.groups[gi];
+    bool any = false;
+    int s = INT_MIN;
+    for (const auto& o : G.out)
+      for (int ci = gi + 1; ci < nG; ++ci)
+        for (const auto& in : C.groups[ci].in)
+          if (in.var == o.var) {
+            s = std::max(s, C.groups[ci].shift + in.rel[0] - o.rel[0]);
+            any = true;
+          }
+    G.shift = any ? s : 0;
+  }
+  for (int gi = 0; gi < nG; ++gi) {
+    Grp& G = C.groups[gi];
+    G.level = 1;
+    for (const auto& in : G.in)
+      for (int pi = 0; pi < gi; ++pi)
+        for (const auto& o : C.groups[pi].out)
+          if (o.var == in.var) G.level = std::max(G.level, C.groups[pi].level + 1);
+  }
+  // one barrier per level: groups of a level are independent of each other
+  std::stable_sort(C.groups.begin(), C.groups.end(), [](const Grp& a, const Grp& b) { return a.level < b.level; });
+  return true;
+}
 
-  src << "// generated by loomfuse-b200 (csrc/jit/codegen.cpp) for chain '" << rs.name << "'\n";
-  src << "typedef " << T << " T;\n";
+// body expressions of group G's outputs, p_<param> bound to its inputs
+bool emit_bodies(Ctx& C, const Grp& G, std::ostream& src, const char* ind) {
+  const auto& k = C.P.rs.kernels[G.kernel];
+  std::map<std::string, std::string> pv;
+  for (const auto& in : G.in) pv[in.param] = "p_" + in.param;
+  for (const auto& o : G.out) {
+    std::string err;
+    auto e = lf::parse_expr(k.bodies.at(o.param), err);
+    if (!e) {
+      C.error = "kernel '" + k.name + "' body of '" + o.param + "': " + err;
+      return false;
+    }
+    std::set<std::string> used;
+    lf::expr_vars(*e, used);
+    for (const auto& u : used)
+      if (!pv.count(u)) {
+        C.error = "kernel '" + k.name + "' body of '" + o.param + "' uses unknown name '" + u + "'";
+        return false;
+      }
+    src << ind << "const T q_" << o.param << " = "
+        << lf::emit_c(*e, C.T, [&](const std::string& n) { return pv.at(n); }) << ";\n";
+  }
+  return true;
+}
+
+void emit_prelude(Ctx& C, std::ostream& src, int threads, int min_blocks = 1) {
+  const auto& terms = C.P.terminals;
+  src << "// generated by loomfuse-b200 (csrc/jit/codegen.cpp) for chain '" << C.P.rs.name << "'\n";
+  src << "typedef " << C.T << " T;\n";
   src << "__device__ __forceinline__ T lf_min(T a, T b) { return a < b ? a : b; }\n";
   src << "__device__ __forceinline__ T lf_max(T a, T b) { return a > b ? a : b; }\n";
   // must match lfx::Args in jit.cpp (passed by value)
-  src << "struct LfArgs { void* t[32]; long long n0; int row_lo, row_hi, top, bottom; };\n";
-  src << "extern \"C\" __global__ void __launch_bounds__(" << out.threads << ") lf_jit_step(const LfArgs a) {\n";
+  src << "struct LfArgs { void* t[32]; long long n0; int row_lo, row_hi, top, bottom, chunk, pad; };\n";
+  src << "extern \"C\" __global__ void __launch_bounds__(" << threads << ", " << min_blocks << ") lf_jit_step(const LfArgs a) {\n";
   src << "  extern __shared__ __align__(16) unsigned char lf_smem[];\n";
-  // tile origin: innermost dim on blockIdx.x, next on y, outermost on z (or y for 2D)
-  const char* bid[3] = {"blockIdx.x", "blockIdx.y", "blockIdx.z"};
-  for (int d = 0; d < nd; ++d) {
-    const int axis = nd - 1 - d;
-    src << "  const long long o" << d << " = " << (d == 0 ? "(long long)a.row_lo + " : "") << "(long long)" << bid[axis]
-        << " * " << tile[d] << ";\n";
-  }
   src << "  const long long N0 = a.n0;\n";
-  for (int d = 1; d < nd; ++d) src << "  const long long N" << d << " = " << N[d] << ";\n";
+  for (int d = 1; d < C.nd; ++d) src << "  const long long N" << d << " = " << C.N[d] << ";\n";
   for (size_t i = 0; i < terms.size(); ++i) {
     if (terms[i].dims.empty())
       src << "  const T s" << i << " = *reinterpret_cast<const T*>(a.t[" << i << "]);\n";
@@ -267,81 +313,392 @@ bool jit_generate(const lf::Plan& P, JitProgram& out) {
       src << "  " << (terms[i].is_goal ? "T" : "const T") << "* __restrict__ t" << i << " = reinterpret_cast<"
           << (terms[i].is_goal ? "T" : "const T") << "*>(a.t[" << i << "]);\n";
   }
+}
+
+// ---------------------------------------------------------------------------
+// 2D / 3D: march the outermost dimension with rolling windows
+// ---------------------------------------------------------------------------
+bool emit_march(Ctx& C, JitProgram& out, std::ostream& src) {
+  const int nd = C.nd;
+  const int NT = 256;
+  const int eb = out.elem_bytes;
+  const size_t nv = C.P.vars.size();
+  auto& G = C.groups;
+  // window bookkeeping along dim 0: lead (newest row written at trip t is
+  // t + lead) and oldest row read at trip t (t + old)
+  std::vector<int> lead(nv, INT_MIN), old(nv, INT_MAX), win(nv, 0), staged(nv, -1);
+  // axiom rows are requested PD trips before they are read
+  int PD = nd == 2 ? 3 : 2;
+  if (const char* e = std::getenv("LF_JIT_PD")) PD = std::max(1, std::atoi(e));
+  for (const auto& g : G)
+    for (const auto& in : g.in) {
+      lead[in.var] = std::max(lead[in.var], C.smem_var[in.var] ? INT_MIN : g.shift + in.rel[0]);
+      old[in.var] = std::min(old[in.var], g.shift + in.rel[0]);
+    }
+  for (const auto& g : G)
+    for (const auto& o : g.out)
+      if (C.smem_var[o.var]) lead[o.var] = g.shift + o.rel[0];
+  for (size_t v = 0; v < nv; ++v) {
+    if (C.smem_var[v]) {
+      win[v] = lead[v] - old[v] + 1;
+    } else if (old[v] != INT_MAX && C.staged_axiom(static_cast<int>(v)) >= 0) {
+      staged[v] = C.staged_axiom(static_cast<int>(v));
+      win[v] = lead[v] - old[v] + 1 + PD;  // + the rows in flight
+    }
+    if (win[v] > 0 && (win[v] > 64 || old[v] < -60 || lead[v] > 60))
+      return (C.error = "pipeline window deeper than 64 rows", false);
+  }
+  // inner tile: cells per plane of the widest window a multiple of the block
+  int span_in[3] = {0, 0, 0};
   for (size_t v = 0; v < nv; ++v)
-    if (smem_var[v]) src << "  T* __restrict__ v" << v << " = reinterpret_cast<T*>(lf_smem + " << soff[v] << ");\n";
-  auto var_read = [&](int v, const std::vector<int>& rel) -> std::string {
-    if (smem_var[v]) return "v" + std::to_string(v) + "[" + sidx(v, "", rel) + "]";
-    // terminal: axiom buffer (or a rank-0 scalar)
-    int ti = terminal_of(v, false);
-    if (ti < 0) return "";
-    if (terms[ti].dims.empty()) return "s" + std::to_string(ti);
-    return "t" + std::to_string(ti) + "[" + tindex(ti, rel, axiom_extra.count(v) ? axiom_extra[v] : std::vector<int>(nd, 0)) + "]";
+    if (win[v] > 0)
+      for (int d = 1; d < nd; ++d) span_in[d] = std::max(span_in[d], C.vmax[v][d] - C.vmin[v][d]);
+  for (const auto& g : G)
+    for (int d = 1; d < nd; ++d) span_in[d] = std::max(span_in[d], g.gmax[d] - g.gmin[d]);
+  std::vector<int> tile(nd, 1);
+  std::vector<size_t> soff(nv, 0);
+  size_t smem = 0;
+  auto plane = [&](size_t v) {
+    size_t n = 1;
+    for (int d = 1; d < nd; ++d) n *= tile[d] + (C.vmax[v][d] - C.vmin[v][d]);
+    return n;
   };
-  for (size_t gi = 0; gi < groups.size(); ++gi) {
-    const Grp& G = groups[gi];
-    const auto& k = rs.kernels[G.kernel];
-    std::vector<int> ext(nd);
-    long cells = 1;
-    for (int d = 0; d < nd; ++d) {
-      ext[d] = tile[d] + (G.gmax[d] - G.gmin[d]);
-      cells *= ext[d];
+  auto layout = [&] {
+    smem = 0;
+    for (size_t v = 0; v < nv; ++v) {
+      if (win[v] <= 0) continue;
+      soff[v] = smem;
+      smem += (win[v] * plane(v) * eb + 15) / 16 * 16;
     }
-    src << "  // group " << gi << ": kernel '" << k.name << "' over the tile + [" ;
-    for (int d = 0; d < nd; ++d) src << (d ? ", " : "") << G.gmin[d] << ".." << G.gmax[d];
-    src << "]\n";
-    src << "  for (int idx = threadIdx.x; idx < " << cells << "; idx += blockDim.x) {\n";
-    src << "    int rem = idx;\n";
-    for (int d = nd - 1; d >= 0; --d) {
-      src << "    const int c" << d << " = rem % " << ext[d] << " + (" << G.gmin[d] << ");";
-      src << " rem /= " << ext[d] << ";\n";
+  };
+  // widths: the outermost inner dimension first; defaults sized for >= 2 CTAs/SM
+  int wide = eb == 8 ? 512 : 1024;
+  int rows_in = 16;
+  if (const char* e = std::getenv("LF_JIT_TILE")) {  // experiments: "<rows>x<width>"
+    int r = 0, w = 0;
+    if (std::sscanf(e, "%dx%d", &r, &w) == 2 && r > 0 && w > 0) rows_in = r, wide = w;
+  }
+  for (;;) {
+    if (nd == 2) {
+      tile[1] = std::max(32, wide - span_in[1]);
+    } else {
+      tile[2] = std::max(16, std::min<int>(64, wide) - span_in[2]);
+      tile[1] = std::max(1, rows_in - span_in[1]);
     }
-    for (int d = 0; d < nd; ++d) src << "    const long long x" << d << " = o" << d << " + c" << d << ";\n";
-    // the group is needed at cells [gmin, N-1+gmax] of the domain
-    src << "    if (";
-    for (int d = 0; d < nd; ++d)
-      src << (d ? " || " : "") << "x" << d << " < " << G.gmin[d] << " || x" << d << " > N" << d << " - 1 + (" << G.gmax[d]
-          << ")";
-    src << ") continue;\n";
-    std::map<std::string, std::string> pv;
-    for (const auto& in : G.in) {
-      std::string r = var_read(in.var, in.rel);
-      if (r.empty()) return fail("kernel '" + k.name + "' reads '" + in.param + "' from an unsupported source");
-      src << "    const T p_" << in.param << " = " << r << ";\n";
-      pv[in.param] = "p_" + in.param;
+    layout();
+    if (smem <= 100 * 1024) break;
+    if (nd == 3 && rows_in > 2) {
+      rows_in /= 2;
+    } else if (wide > 64) {
+      wide /= 2;
+    } else {
+      break;
     }
-    for (const auto& o : G.out) {
-      std::string err;
-      auto e = lf::parse_expr(k.bodies.at(o.param), err);
-      if (!e) return fail("kernel '" + k.name + "' body of '" + o.param + "': " + err);
-      std::set<std::string> used;
-      lf::expr_vars(*e, used);
-      for (const auto& u : used)
-        if (!pv.count(u)) return fail("kernel '" + k.name + "' body of '" + o.param + "' uses unknown name '" + u + "'");
-      src << "    const T q_" << o.param << " = "
-          << lf::emit_c(*e, T, [&](const std::string& n) { return pv.at(n); }) << ";\n";
+  }
+  if (smem > 200 * 1024) return (C.error = "chain needs too much on-chip storage for one tile", false);
+  out.tile = tile;
+  out.tile[0] = 1;
+  out.smem_bytes = smem;
+  out.threads = NT;
+  out.march = true;
+  // trip range relative to the chunk [r0, r1): t in [r0 + TS, r1 - 1 + TE]
+  int TS = INT_MAX, TE = INT_MIN;
+  for (const auto& g : G) {
+    TS = std::min(TS, g.gmin[0] - g.shift);
+    TE = std::max(TE, g.gmax[0] - g.shift);
+  }
+  for (size_t v = 0; v < nv; ++v)
+    if (staged[v] >= 0) TS = std::min(TS, C.vmin[v][0] - lead[v]);
+  out.prologue = TE - TS;
+  {
+    long inner = 1;
+    for (int d = 1; d < nd; ++d) inner *= (C.N[d] + tile[d] - 1) / tile[d];
+    out.inner_tiles = inner;
+  }
+  out.ctas_per_sm = std::max<int>(1, std::min<int>(2048 / NT, static_cast<int>((227 * 1024) / (smem + 1024))));
+  out.chunk = nd == 3 ? 64 : 1 << 30;  // rows per chunk of the work order (2D: whole tiles)
+
+  int minb = std::min(out.ctas_per_sm, 2);  // register cap; 2 measured best
+  if (const char* e = std::getenv("LF_JIT_MINB")) minb = std::max(1, std::atoi(e));
+  emit_prelude(C, src, NT, minb);
+  if (nd == 3)
+    src << "  const int tx = threadIdx.x & 63, ty = threadIdx.x >> 6;\n";
+  else
+    src << "  const int tx = threadIdx.x;\n";
+  for (size_t v = 0; v < nv; ++v)
+    if (win[v] > 0)
+      src << "  T* __restrict__ v" << v << " = reinterpret_cast<T*>(lf_smem + " << soff[v] << ");  // '"
+          << C.P.vars[v].name << "': " << win[v] << " rows x " << plane(v) << "\n";
+  auto width = [&](size_t v, int d) { return tile[d] + (C.vmax[v][d] - C.vmin[v][d]); };
+  // in-plane offset of var v at tile-relative cell (c_d + rel_d)
+  auto inplane = [&](size_t v, const std::vector<int>& rel) {
+    std::string e;
+    for (int d = 1; d < nd; ++d) {
+      const std::string c = "(c" + std::to_string(d) + plus(rel[d] - C.vmin[v][d]) + ")";
+      e = e.empty() ? c : "(" + e + ") * " + std::to_string(width(v, d)) + " + " + c;
     }
-    for (const auto& o : G.out) {
-      if (smem_var[o.var]) src << "    v" << o.var << "[" << sidx(o.var, "", o.rel) << "] = q_" << o.param << ";\n";
-      const int ti = terminal_of(o.var, true);
-      if (ti >= 0) {
-        // goal: own-tile cells of the computed rows, inside the domain
-        src << "    if (";
-        for (int d = 0; d < nd; ++d) {
-          src << (d ? " && " : "") << "c" << d << " + (" << o.rel[d] << ") >= 0 && c" << d << " + (" << o.rel[d] << ") < "
-              << tile[d] << " && x" << d << " + (" << o.rel[d] << ") < N" << d;
-          if (d == 0) src << " && x0 + (" << o.rel[0] << ") < a.row_hi";
+    return e;
+  };
+  // rolling-window slots: b<v> = slot of row t, advanced once per trip; the
+  // slot of row t + off is b<v> + (off mod W) with one conditional wrap
+  auto wrap = [&](size_t v, int off) { return ((off % win[v]) + win[v]) % win[v]; };
+  auto rowbase = [&](size_t v, int off) -> std::string {
+    if (win[v] == 1) return "0";
+    const int o = wrap(v, off);
+    const std::string b = "b" + std::to_string(v);
+    const std::string sum = o ? "(" + b + " + " + std::to_string(o) + ")" : b;
+    const std::string sl = o ? "(" + sum + " >= " + std::to_string(win[v]) + " ? " + sum + " - " + std::to_string(win[v]) +
+                                   " : " + sum + ")"
+                             : b;
+    return sl + " * " + std::to_string(plane(v));
+  };
+  // 3D: a 64-wide column per thread x 4 row lanes; 2D: 256 columns per pass
+  const int STEP = nd == 3 ? NT / 64 : NT;
+  int ILP = 1;  // cells whose operands are loaded before any is evaluated (1 measured best)
+  if (const char* e = std::getenv("LF_JIT_ILP")) ILP = std::max(1, std::atoi(e));
+  const char* LANE = nd == 3 ? "ty" : "tx";
+  // ---- persistent CTAs: each takes an equal share of the (row chunk, inner
+  // tile, row) space in that order and marches it as one or more segments,
+  // so neighbouring tiles run at the same time and share halos in L2
+  for (size_t v = 0; v < nv; ++v)
+    if (staged[v] >= 0) src << "  const unsigned sb" << v << " = (unsigned)__cvta_generic_to_shared(v" << v << ");\n";
+  src << "  const int rows = a.row_hi - a.row_lo;\n";
+  src << "  const long long total = (long long)rows * " << out.inner_tiles << ";\n";
+  src << "  const long long per = (total + gridDim.x - 1) / gridDim.x;\n";
+  src << "  long long s = (long long)blockIdx.x * per;\n";
+  src << "  const long long s_end = min(total, s + per);\n";
+  src << "  while (s < s_end) {\n";
+  src << "  const long long cs = (long long)a.chunk * " << out.inner_tiles << ";\n";
+  src << "  const int ci = (int)(s / cs);\n";
+  src << "  const int rc = min(a.chunk, rows - ci * a.chunk);\n";
+  src << "  const long long off = s - ci * cs;\n";
+  src << "  int bt = (int)(off / rc);\n";
+  src << "  const int r0 = a.row_lo + ci * a.chunk + (int)(off % rc);\n";
+  src << "  const int r1 = (int)min((long long)(a.row_lo + ci * a.chunk + rc), r0 + (s_end - s));\n";
+  src << "  s += r1 - r0;\n";
+  for (int d = nd - 1; d >= 1; --d) {
+    const long nt = (C.N[d] + tile[d] - 1) / tile[d];
+    src << "  const int o" << d << " = (bt % " << nt << ") * " << tile[d] << "; bt /= " << nt << ";\n";
+  }
+  for (size_t v = 0; v < nv; ++v)
+    if (win[v] > 1) src << "  int b" << v << " = " << wrap(v, TS) << ";\n";
+  // ---- axiom streaming: row `row` of staged var v into slot `slotexpr`
+  auto emit_load = [&](size_t v, const std::string& row, const std::string& slotexpr, const char* ind) {
+    std::vector<int> ext(nd), lo(nd);
+    for (int d = 1; d < nd; ++d) {
+      ext[d] = width(v, d);
+      lo[d] = C.vmin[v][d];
+    }
+    const int K = (ext[1] + STEP - 1) / STEP;
+    std::string I(ind);
+    src << I << "{ const int y = " << row << ";\n";
+    src << I << "  if (y >= r0" << plus(C.vmin[v][0]) << " && y <= r1 - 1" << plus(C.vmax[v][0]) << ") {\n";
+    src << I << "    const unsigned dst = sb" << v << " + (" << slotexpr << ") * " << eb << ";\n";
+    if (nd == 3) {
+      src << I << "    const int c2 = tx" << plus(lo[2]) << ";\n";
+      src << I << "    const int x2 = o2 + c2;\n";
+      src << I << "    if (tx < " << ext[2] << " && x2 <= " << (C.N[2] - 1 + C.vmax[v][2]) << ") {\n";
+    } else {
+      src << I << "    {\n";
+    }
+    src << I << "      const int c1hi = min(" << (lo[1] + ext[1] - 1) << ", " << (C.N[1] - 1 + C.vmax[v][1]) << " - o1);\n";
+    src << I << "      #pragma unroll\n";
+    src << I << "      for (int k = 0; k < " << K << "; ++k) {\n";
+    src << I << "        const int c1 = " << LANE << plus(lo[1]) << " + k * " << STEP << ";\n";
+    src << I << "        if (c1 <= c1hi) {\n";
+    src << I << "          const int x1 = o1 + c1;\n";
+    std::vector<std::string> pos = {"y"};
+    for (int d = 1; d < nd; ++d) pos.push_back("x" + std::to_string(d));
+    src << I << "          asm volatile(\"cp.async.ca.shared.global [%0], [%1], " << eb << ";\" :: \"r\"(dst + ("
+        << inplane(v, std::vector<int>(nd, 0)) << ") * " << eb << "), \"l\"(t" << staged[v] << " + "
+        << C.tidx(staged[v], pos, C.extra_of(static_cast<int>(v))) << ") : \"memory\");\n";
+    src << I << "        }\n" << I << "      }\n" << I << "    }\n" << I << "  }\n" << I << "}\n";
+  };
+  for (int p = 0; p < PD; ++p) {
+    for (size_t v = 0; v < nv; ++v)
+      if (staged[v] >= 0)
+        emit_load(v, "r0" + plus(TS + p + lead[v]), std::to_string(wrap(v, TS + p + lead[v]) * plane(v)), "  ");
+    src << "  asm volatile(\"cp.async.commit_group;\" ::: \"memory\");\n";
+  }
+  src << "  for (int t = r0 + (" << TS << "); t <= r1 - 1 + (" << TE << "); ++t) {\n";
+  src << "    asm volatile(\"cp.async.wait_group " << (PD - 1) << ";\" ::: \"memory\");\n";
+  src << "    __syncthreads();\n";
+  for (size_t v = 0; v < nv; ++v)
+    if (staged[v] >= 0) emit_load(v, "t" + plus(PD + lead[v]), rowbase(v, PD + lead[v]), "    ");
+  src << "    asm volatile(\"cp.async.commit_group;\" ::: \"memory\");\n";
+  int level = 1;
+  for (size_t gi = 0; gi < G.size(); ++gi) {
+    const Grp& g = G[gi];
+    const auto& k = C.P.rs.kernels[g.kernel];
+    if (g.level != level) {
+      src << "    __syncthreads();\n";
+      level = g.level;
+    }
+    std::vector<int> ext(nd), lo(nd);
+    for (int d = 1; d < nd; ++d) {
+      ext[d] = tile[d] + (g.gmax[d] - g.gmin[d]);
+      lo[d] = g.gmin[d];
+    }
+    const int K = (ext[1] + STEP - 1) / STEP;
+    src << "    { // group " << gi << ": kernel '" << k.name << "', lead " << g.shift << ", level " << g.level << "\n";
+    src << "      const int y = t" << plus(g.shift) << ";\n";
+    src << "      if (y >= r0" << plus(g.gmin[0]) << " && y <= r1 - 1" << plus(g.gmax[0]) << ") {\n";
+    std::map<std::pair<int, int>, std::string> rbs;
+    auto rb = [&](int v, int r) {
+      auto key = std::make_pair(v, r);
+      auto it = rbs.find(key);
+      if (it != rbs.end()) return it->second;
+      std::string nm = "rb" + std::to_string(v) + "_" + (r < 0 ? "m" + std::to_string(-r) : std::to_string(r));
+      src << "        const int " << nm << " = " << rowbase(v, g.shift + r) << ";\n";
+      rbs[key] = nm;
+      return nm;
+    };
+    for (const auto& in : g.in)
+      if (win[in.var] > 0) rb(in.var, in.rel[0]);
+    for (const auto& o : g.out)
+      if (C.smem_var[o.var]) rb(o.var, o.rel[0]);
+    if (nd == 3) {
+      src << "        const int c2 = tx" << plus(lo[2]) << ";\n";
+      src << "        const int x2 = o2 + c2;\n";
+      src << "        const bool act = tx < " << ext[2] << " && x2 <= " << (C.N[2] - 1 + g.gmax[2]) << ";\n";
+    } else {
+      src << "        const bool act = true;\n";
+    }
+    src << "        const int c1hi = min(" << (lo[1] + ext[1] - 1) << ", " << (C.N[1] - 1 + g.gmax[1]) << " - o1);\n";
+    // phase 1: every operand of the K cells this thread owns (independent loads)
+    // in batches of ILP cells (bounded register footprint)
+    const int B = std::min(K, ILP);
+    src << "        #pragma unroll\n";
+    src << "        for (int kb = 0; kb < " << K << "; kb += " << B << ") {\n";
+    for (const auto& in : g.in) src << "        T a_" << in.param << "[" << B << "];\n";
+    src << "        #pragma unroll\n";
+    src << "        for (int kk = 0; kk < " << B << "; ++kk) {\n";
+    src << "          const int k = kb + kk;\n";
+    src << "          const int c1 = " << LANE << plus(lo[1]) << " + k * " << STEP << ";\n";
+    src << "          const int x1 = o1 + c1;\n";
+    src << "          if (act && c1 <= c1hi) {\n";
+    for (const auto& in : g.in) {
+      std::string r;
+      if (win[in.var] > 0) {
+        r = "v" + std::to_string(in.var) + "[" + rb(in.var, in.rel[0]) + " + " + inplane(in.var, in.rel) + "]";
+      } else {
+        const int ti = C.terminal_of(in.var, false);
+        if (C.P.terminals[ti].dims.empty()) {
+          r = "s" + std::to_string(ti);
+        } else {
+          std::vector<std::string> pos;
+          for (int d = 0; d < nd; ++d) pos.push_back((d == 0 ? std::string("y") : "x" + std::to_string(d)) + plus(in.rel[d]));
+          r = "__ldg(t" + std::to_string(ti) + " + " + C.tidx(ti, pos, C.extra_of(in.var)) + ")";
         }
-        src << ") t" << ti << "[" << tindex(ti, o.rel, std::vector<int>(nd, 0)) << "] = q_" << o.param << ";\n";
       }
+      src << "            a_" << in.param << "[kk] = " << r << ";\n";
+    }
+    src << "          }\n        }\n";
+    // phase 2: evaluate and store
+    src << "        #pragma unroll\n";
+    src << "        for (int kk = 0; kk < " << B << "; ++kk) {\n";
+    src << "          const int k = kb + kk;\n";
+    src << "          const int c1 = " << LANE << plus(lo[1]) << " + k * " << STEP << ";\n";
+    src << "          const int x1 = o1 + c1;\n";
+    src << "          if (act && c1 <= c1hi) {\n";
+    for (const auto& in : g.in) src << "            const T p_" << in.param << " = a_" << in.param << "[kk];\n";
+    if (!emit_bodies(C, g, src, "            ")) return false;
+    for (const auto& o : g.out) {
+      if (C.smem_var[o.var])
+        src << "            v" << o.var << "[" << rb(o.var, o.rel[0]) << " + " << inplane(o.var, o.rel) << "] = q_"
+            << o.param << ";\n";
+      const int ti = C.terminal_of(o.var, true);
+      if (ti < 0) continue;
+      // goal: own chunk rows, own tile cells, inside the domain
+      src << "            if (y" << plus(o.rel[0]) << " >= r0 && y" << plus(o.rel[0]) << " < r1";
+      for (int d = 1; d < nd; ++d)
+        src << " && c" << d << plus(o.rel[d]) << " >= 0 && c" << d << plus(o.rel[d]) << " < " << tile[d] << " && x" << d
+            << plus(o.rel[d]) << " < N" << d;
+      std::vector<std::string> pos;
+      for (int d = 0; d < nd; ++d) pos.push_back((d == 0 ? std::string("y") : "x" + std::to_string(d)) + plus(o.rel[d]));
+      src << ") t" << ti << "[" << C.tidx(ti, pos, std::vector<int>(nd, 0)) << "] = q_" << o.param << ";\n";
+    }
+    src << "          }\n        }\n        }\n      }\n    }\n";
+  }
+  for (size_t v = 0; v < nv; ++v)
+    if (win[v] > 1) src << "    b" << v << " = b" << v << " == " << (win[v] - 1) << " ? 0 : b" << v << " + 1;\n";
+  src << "  }\n";
+  src << "  asm volatile(\"cp.async.wait_group 0;\" ::: \"memory\");\n";
+  src << "  __syncthreads();\n";
+  src << "  }\n";
+  src << "}\n";
+  return true;
+}
+
+// ---------------------------------------------------------------------------
+// 1D: one CTA per tile, every group over tile + halo in shared memory
+// ---------------------------------------------------------------------------
+bool emit_tiled(Ctx& C, JitProgram& out, std::ostream& src) {
+  const int NT = 256;
+  const int eb = out.elem_bytes;
+  const size_t nv = C.P.vars.size();
+  const int tile = 1024;
+  std::vector<size_t> soff(nv, 0);
+  size_t smem = 0;
+  for (size_t v = 0; v < nv; ++v) {
+    if (!C.smem_var[v]) continue;
+    soff[v] = smem;
+    smem += ((tile + C.vmax[v][0] - C.vmin[v][0]) * eb + 15) / 16 * 16;
+  }
+  if (smem > 200 * 1024) return (C.error = "chain needs too much on-chip storage for one tile", false);
+  out.tile = {tile};
+  out.smem_bytes = smem;
+  out.threads = NT;
+  out.march = false;
+  emit_prelude(C, src, NT);
+  src << "  const long long o0 = (long long)a.row_lo + (long long)blockIdx.x * " << tile << ";\n";
+  for (size_t v = 0; v < nv; ++v)
+    if (C.smem_var[v]) src << "  T* __restrict__ v" << v << " = reinterpret_cast<T*>(lf_smem + " << soff[v] << ");\n";
+  for (size_t gi = 0; gi < C.groups.size(); ++gi) {
+    const Grp& g = C.groups[gi];
+    const long cells = tile + g.gmax[0] - g.gmin[0];
+    src << "  for (int idx = threadIdx.x; idx < " << cells << "; idx += " << NT << ") {\n";
+    src << "    const int c0 = idx" << plus(g.gmin[0]) << ";\n";
+    src << "    const long long x0 = o0 + c0;\n";
+    src << "    if (x0 < " << g.gmin[0] << " || x0 > N0 - 1" << plus(g.gmax[0]) << ") continue;\n";
+    for (const auto& in : g.in) {
+      std::string r;
+      if (C.smem_var[in.var]) {
+        r = "v" + std::to_string(in.var) + "[c0" + plus(in.rel[0] - C.vmin[in.var][0]) + "]";
+      } else {
+        const int ti = C.terminal_of(in.var, false);
+        r = C.P.terminals[ti].dims.empty()
+                ? "s" + std::to_string(ti)
+                : "t" + std::to_string(ti) + "[" + C.tidx(ti, {"x0" + plus(in.rel[0])}, C.extra_of(in.var)) + "]";
+      }
+      src << "    const T p_" << in.param << " = " << r << ";\n";
+    }
+    if (!emit_bodies(C, g, src, "    ")) return false;
+    for (const auto& o : g.out) {
+      if (C.smem_var[o.var])
+        src << "    v" << o.var << "[c0" << plus(o.rel[0] - C.vmin[o.var][0]) << "] = q_" << o.param << ";\n";
+      const int ti = C.terminal_of(o.var, true);
+      if (ti >= 0)
+        src << "    if (c0" << plus(o.rel[0]) << " >= 0 && c0" << plus(o.rel[0]) << " < " << tile << " && x0"
+            << plus(o.rel[0]) << " < a.row_hi) t" << ti << "[" << C.tidx(ti, {"x0" + plus(o.rel[0])}, {0}) << "] = q_"
+            << o.param << ";\n";
     }
     src << "  }\n";
-    if (gi + 1 < groups.size()) src << "  __syncthreads();\n";
+    if (gi + 1 < C.groups.size()) src << "  __syncthreads();\n";
   }
   src << "}\n";
+  return true;
+}
 
-  // ---- ghost refill of iterated goals (boundary modes, between steps)
+// ---------------------------------------------------------------------------
+// ghost refill of iterated goals (boundary modes), ghost cells only: region d
+// holds the cells whose outermost ghost dimension is d (dims < d interior)
+// ---------------------------------------------------------------------------
+bool emit_fill(Ctx& C, JitProgram& out, std::ostream& fill) {
+  const auto& rs = C.P.rs;
+  const auto& terms = C.P.terminals;
+  const int nd = C.nd;
   out.has_fill = false;
-  std::ostringstream fill;
   fill << "extern \"C\" __global__ void lf_jit_fill(const LfArgs a) {\n";
   fill << "  const long long N0 = a.n0;\n";
   for (const auto& [gname, aname] : rs.iterate) {
@@ -350,59 +707,108 @@ bool jit_generate(const lf::Plan& P, JitProgram& out) {
       if (terms[i].is_goal && terms[i].name == gname) ti = static_cast<int>(i);
     if (ti < 0 || terms[ti].dims.empty()) continue;
     const auto& t = terms[ti];
-    if ((int)t.dims.size() != nd) return fail("iterated terminal '" + gname + "' must span every loop dimension");
+    if ((int)t.dims.size() != nd)
+      return (C.error = "iterated terminal '" + gname + "' must span every loop dimension", false);
     auto it = rs.boundary.find(t.name);
     if (it == rs.boundary.end()) it = rs.boundary.find("*");
     std::vector<lf::Boundary> modes(nd, lf::Boundary::none);
     if (it != rs.boundary.end())
-      for (int d = 0; d < nd; ++d) modes[d] = it->second.size() == 1 ? it->second[0] : it->second[std::min<size_t>(d, it->second.size() - 1)];
+      for (int d = 0; d < nd; ++d) modes[d] = it->second[std::min<size_t>(d, it->second.size() - 1)];
+    bool any = false;
+    for (auto m : modes) any |= m != lf::Boundary::none;
+    if (!any) continue;
     out.has_fill = true;
-    fill << "  {\n    T* b = reinterpret_cast<T*>(a.t[" << ti << "]);\n";
-    long cells_inner = 1;
-    for (int s = 1; s < nd; ++s) cells_inner *= t.extent[s];
-    const long h0 = -t.base[0];
-    fill << "    const long long total = (N0 + " << (t.extent[0] - N[0]) << ") * " << cells_inner << "LL;\n";
-    fill << "    for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total; idx += (long long)gridDim.x * blockDim.x) {\n";
-    fill << "      long long rem = idx;\n";
-    for (int s = nd - 1; s >= 0; --s) {
-      fill << "      const long long y" << s << " = rem % " << (s == 0 ? std::string("(N0 + ") + std::to_string(t.extent[0] - N[0]) + ")" : std::to_string(t.extent[s])) << " + (" << t.base[s] << ");";
-      fill << " rem /= " << (s == 0 ? std::string("(N0 + ") + std::to_string(t.extent[0] - N[0]) + ")" : std::to_string(t.extent[s])) << ";\n";
-    }
-    (void)h0;
-    fill << "      bool ghost = false, zero = false; T sign = static_cast<T>(1);\n";
+    std::vector<long> lo(nd), hi(nd), E(nd);  // ghost widths below / above the interior, extents
     for (int d = 0; d < nd; ++d) {
-      const std::string y = "y" + std::to_string(d), n = "N" + std::string(d == 0 ? "0" : std::to_string(N[d]));
-      const std::string nn = d == 0 ? "N0" : std::to_string(N[d]);
+      lo[d] = -t.base[d];
+      E[d] = t.extent[d];
+      hi[d] = E[d] - C.N[d] - lo[d];
+    }
+    auto nn = [&](int d) { return d == 0 ? std::string("N0") : std::to_string(C.N[d]); };
+    fill << "  {\n    T* b = reinterpret_cast<T*>(a.t[" << ti << "]);\n";
+    // region sizes
+    fill << "    long long rs[" << nd << "];\n";
+    for (int d = 0; d < nd; ++d) {
+      fill << "    rs[" << d << "] = ";
+      if (d == 0)
+        fill << "(long long)((a.top ? " << lo[0] << " : 0) + (a.bottom ? " << hi[0] << " : 0))";
+      else
+        fill << "(long long)(a.row_hi - a.row_lo)";
+      for (int k = 1; k < d; ++k) fill << " * " << C.N[k];
+      if (d > 0) fill << " * " << (lo[d] + hi[d]);
+      for (int k = d + 1; k < nd; ++k) fill << " * " << E[k];
+      fill << ";\n";
+    }
+    fill << "    long long total = 0; for (int r = 0; r < " << nd << "; ++r) total += rs[r];\n";
+    fill << "    for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total; idx += (long long)gridDim.x * blockDim.x) {\n";
+    fill << "      long long rem = idx; int reg = 0;\n";
+    fill << "      while (rem >= rs[reg]) rem -= rs[reg++];\n";
+    for (int d = 0; d < nd; ++d) fill << "      long long y" << d << ";\n";
+    for (int d = 0; d < nd; ++d) {
+      fill << "      " << (d ? "else " : "") << "if (reg == " << d << ") {\n";
+      // dims > d: anything in the extent (innermost fastest)
+      for (int k = nd - 1; k > d; --k)
+        fill << "        y" << k << " = rem % " << E[k] << " - " << lo[k] << "; rem /= " << E[k] << ";\n";
+      if (d == 0) {
+        fill << "        { const long long g = rem; const long long nt = a.top ? " << lo[0] << " : 0;\n";
+        fill << "          y0 = g < nt ? g - " << lo[0] << " : N0 + (g - nt); }\n";
+      } else {
+        fill << "        { const long long g = rem % " << (lo[d] + hi[d]) << "; rem /= " << (lo[d] + hi[d]) << ";\n";
+        fill << "          y" << d << " = g < " << lo[d] << " ? g - " << lo[d] << " : " << C.N[d] << " + (g - " << lo[d] << "); }\n";
+        for (int k = d - 1; k >= 1; --k) fill << "        y" << k << " = rem % " << C.N[k] << "; rem /= " << C.N[k] << ";\n";
+        fill << "        y0 = a.row_lo + rem;\n";
+      }
+      fill << "      }\n";
+    }
+    fill << "      bool zero = false; T sign = static_cast<T>(1);\n";
+    for (int d = 0; d < nd; ++d) {
+      const std::string y = "y" + std::to_string(d), n = nn(d);
       fill << "      long long z" << d << " = " << y << ";\n";
-      fill << "      if (" << y << " < 0 || " << y << " >= " << nn << ") {\n";
-      if (d == 0) fill << "        if ((" << y << " < 0 && !a.top) || (" << y << " >= " << nn << " && !a.bottom)) continue;\n";
-      fill << "        ghost = true;\n";
+      fill << "      if (" << y << " < 0 || " << y << " >= " << n << ") {\n";
       switch (modes[d]) {
         case lf::Boundary::zero: fill << "        zero = true;\n"; break;
-        case lf::Boundary::periodic: fill << "        z" << d << " = ((" << y << " % " << nn << ") + " << nn << ") % " << nn << ";\n"; break;
-        case lf::Boundary::clamp: fill << "        z" << d << " = " << y << " < 0 ? 0 : " << nn << " - 1;\n"; break;
+        case lf::Boundary::periodic: fill << "        z" << d << " = ((" << y << " % " << n << ") + " << n << ") % " << n << ";\n"; break;
+        case lf::Boundary::clamp: fill << "        z" << d << " = " << y << " < 0 ? 0 : " << n << " - 1;\n"; break;
         case lf::Boundary::even:
         case lf::Boundary::odd:
-          fill << "        z" << d << " = " << y << " < 0 ? -1 - " << y << " : 2 * " << nn << " - 1 - " << y << ";\n";
+          fill << "        z" << d << " = " << y << " < 0 ? -1 - " << y << " : 2 * " << n << " - 1 - " << y << ";\n";
           if (modes[d] == lf::Boundary::odd) fill << "        sign = -sign;\n";
           break;
         case lf::Boundary::none: fill << "        continue;\n"; break;
       }
       fill << "      }\n";
     }
-    fill << "      if (!ghost) continue;\n";
     std::string dst, srci;
     for (int s = 0; s < nd; ++s) {
-      long p = pitch(t, s);
-      std::string ps = p != 1 ? " * " + std::to_string(p) + "LL" : "";
-      dst += (s ? " + " : "") + std::string("(y") + std::to_string(s) + " - (" + std::to_string(t.base[s]) + "))" + ps;
-      srci += (s ? " + " : "") + std::string("(z") + std::to_string(s) + " - (" + std::to_string(t.base[s]) + "))" + ps;
+      const long p = C.pitch(t, s);
+      const std::string ps = p != 1 ? " * " + std::to_string(p) + "LL" : "";
+      dst += (s ? " + " : "") + std::string("(y") + std::to_string(s) + plus(-t.base[s]) + ")" + ps;
+      srci += (s ? " + " : "") + std::string("(z") + std::to_string(s) + plus(-t.base[s]) + ")" + ps;
     }
     fill << "      b[" << dst << "] = zero ? static_cast<T>(0) : sign * b[" << srci << "];\n";
     fill << "    }\n  }\n";
   }
   fill << "}\n";
-  src << fill.str();
+  return true;
+}
+
+}  // namespace
+
+bool jit_generate(const lf::Plan& P, JitProgram& out) {
+  Ctx C(P);
+  if (!analyse(C)) {
+    out.error = C.error;
+    return false;
+  }
+  out.type = C.T;
+  out.elem_bytes = C.T == "double" ? 8 : 4;
+  out.nd = C.nd;
+  std::ostringstream src;
+  const bool ok = C.nd >= 2 ? emit_march(C, out, src) : emit_tiled(C, out, src);
+  if (!ok || !emit_fill(C, out, src)) {
+    out.error = C.error;
+    return false;
+  }
   out.source = src.str();
   return true;
 }

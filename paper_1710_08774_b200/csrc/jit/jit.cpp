@@ -10,6 +10,7 @@
 #include <dlfcn.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 
@@ -62,6 +63,7 @@ struct Drv {
   PFN_cuLaunchKernel_v4000 launch = nullptr;
   PFN_cuFuncSetAttribute_v9000 attr = nullptr;
   PFN_cuModuleUnload_v2000 unload = nullptr;
+  PFN_cuOccupancyMaxActiveBlocksPerMultiprocessor_v6050 occupancy = nullptr;
   bool ok = false;
 };
 
@@ -77,7 +79,8 @@ const Drv& drv() {
            get("cuModuleGetFunction", reinterpret_cast<void**>(&d.get)) &&
            get("cuLaunchKernel", reinterpret_cast<void**>(&d.launch)) &&
            get("cuFuncSetAttribute", reinterpret_cast<void**>(&d.attr)) &&
-           get("cuModuleUnload", reinterpret_cast<void**>(&d.unload));
+           get("cuModuleUnload", reinterpret_cast<void**>(&d.unload)) &&
+           get("cuOccupancyMaxActiveBlocksPerMultiprocessor", reinterpret_cast<void**>(&d.occupancy));
   });
   return d;
 }
@@ -85,7 +88,7 @@ const Drv& drv() {
 struct Args {
   void* t[32];
   long long n0;
-  int row_lo, row_hi, top, bottom;
+  int row_lo, row_hi, top, bottom, chunk, pad;
 };
 
 }  // namespace
@@ -173,7 +176,6 @@ int JitKernel::run(const ExecArgs& a, std::string& err) {
   }
   const auto& rs = a.plan->rs;
   const auto& T = a.plan->terminals;
-  const int nd = prog_.nd;
   const RowPart rp = row_part(a, (int)rs.ranges[0].trips());
   Args args;
   std::memset(&args, 0, sizeof args);
@@ -183,13 +185,26 @@ int JitKernel::run(const ExecArgs& a, std::string& err) {
   args.top = rp.top;
   args.bottom = rp.bottom;
   dim3 grid(1, 1, 1);
-  const std::vector<int>& tile = prog_.tile;
-  auto tiles = [&](long n, int t) { return static_cast<unsigned>((n + t - 1) / t); };
-  for (int dd = 0; dd < nd; ++dd) {
-    const long n = dd == 0 ? (rp.hi - rp.lo) : rs.ranges[dd].trips();
-    const unsigned c = tiles(n, tile[dd]);
-    const int axis = nd - 1 - dd;
-    (axis == 0 ? grid.x : axis == 1 ? grid.y : grid.z) = c;
+  const long rows = rp.hi - rp.lo;
+  if (rows <= 0) return LF_OK;
+  if (prog_.march) {
+    // persistent: one wave of resident CTAs, each an equal share of the
+    // (chunk, tile, row) space; tiny grids keep >= 16 rows per CTA
+    if (!resident_) {
+      int dev = 0, sms = 0, occ = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      if (d.occupancy(&occ, static_cast<CUfunction>(step_), prog_.threads, prog_.smem_bytes) != CUDA_SUCCESS || occ < 1)
+        occ = prog_.ctas_per_sm;
+      resident_ = std::max(1, sms) * std::max(1, occ);
+    }
+    long chunk = std::min<long>(prog_.chunk, rows);
+    if (const char* e = std::getenv("LF_JIT_CHUNK")) chunk = std::max(1L, std::min<long>(rows, std::atol(e)));
+    const long total = rows * prog_.inner_tiles;
+    args.chunk = static_cast<int>(chunk);
+    grid.x = static_cast<unsigned>(std::max<long>(1, std::min<long>(resident_, total / 16)));
+  } else {
+    grid.x = static_cast<unsigned>((rows + prog_.tile[0] - 1) / prog_.tile[0]);
   }
   // ping-pong as the built-in executors: goals of the last step land in the
   // goal buffers, intermediate states in plan-owned scratch, axioms untouched

@@ -22,6 +22,11 @@ struct JitProgram {
   size_t smem_bytes = 0;
   int threads = 256;
   bool has_fill = false;
+  bool march = false;       // 2D/3D rolling-window schedule (outer dim chunked over blockIdx.y)
+  int prologue = 0;         // extra trips per chunk (pipeline fill)
+  long inner_tiles = 1;     // CTAs across the inner dimensions
+  int ctas_per_sm = 1;      // resident CTAs per SM the shared-memory footprint allows
+  int chunk = 64;           // rows per chunk of the persistent work order
   std::string error;  // why the chain is not supported
 };
 
@@ -40,6 +45,7 @@ class JitKernel {
   void* module_ = nullptr;  // CUmodule
   void* step_ = nullptr;    // CUfunction
   void* fill_ = nullptr;
+  int resident_ = 0;  // CTAs resident at once (occupancy x SMs)
   std::vector<char> cubin_;
   int launch(void* fn, dim3 grid, dim3 block, size_t smem, cudaStream_t st, void* args, std::string& err);
 };

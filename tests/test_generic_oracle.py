@@ -64,7 +64,7 @@ def test_generic_multi_output_scalar_and_asymmetric_halo():
 def test_jit_plans_for_body_chains_and_reports_source():
     for s in ["biharm_body", "heat3d_body", "box_body", "multi_body", "laplace3_body"]:
         p = lf.Plan.from_file(SPECS / f"{s}.lf")
-        assert p.executor == "jit_tiled_fused", s
+        assert p.executor.startswith("jit_"), s
         assert "lf_jit_step" in p.source
     # a chain without bodies and without a matching built-in stays unsupported
     q = lf.Plan.from_file(SPECS / "cosmo.lf")

@@ -40,7 +40,7 @@ CASES = {
 @pytest.mark.parametrize("steps", [1, 3])
 def test_jit_matches_generic_oracle(name, steps):
     plan = lf.Plan.from_file(SPECS / f"{name}.lf")
-    assert plan.executor == "jit_tiled_fused"
+    assert plan.executor.startswith("jit_")
     if steps > 1 and name not in ("biharm_body", "heat3d_body"):
         pytest.skip("chain has no iterate pairs")
     ax = CASES[name]()
