@@ -255,11 +255,7 @@ int launch_step(const double* in, double* out, int ni, const RowPart& rp, cudaSt
   p.write_ghost_top = rp.top;
   p.write_ghost_bottom = rp.bottom;
   // at least ~16 rows per CTA so the 4 priming rows stay a small fraction
-  const long long work = (long long)p.strips * (rp.hi - rp.lo);
-  // each CTA must get at most 3 row segments (rowstream.cuh): at least
-  // ceil(strips/2) CTAs when the row range is short
-  const long long want = std::max<long long>(work / 16, (p.strips + 1) / 2);
-  const int ctas = static_cast<int>(std::max<long long>(1, std::min<long long>(slots, want)));
+  const int ctas = rowstream_ctas(slots, p.strips, rp.hi - rp.lo);
   if ((long long)ctas * 2 < p.strips) {
     err = "row range too short for the resident grid";
     return LF_ERR_UNSUPPORTED;

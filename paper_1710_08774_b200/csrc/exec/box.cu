@@ -39,57 +39,119 @@ struct Params {
 };
 
 struct Win {
-  float r1[3][CPL];  // row pass 1, rows by index % 3
-  float r1h[3];      // ... at the strip's halo column
-  float r2[3][CPL];  // row pass 2
+  float2 r1[3][2];  // row pass 1, rows by index % 3, columns (0,1) (2,3)
+  float r1h[3];     // ... at the strip's halo column
+  float2 r2[3][2];  // row pass 2
 };
 
-template <int P>
+// ---- fast path ------------------------------------------------------------
+// x / 3.0f for +0 <= x < 2^128: q = x*RN(1/3), one residual correction.
+// oracle/div3check.c proves it equals IEEE division for every finite nonzero
+// float, and it returns +0 for +0; lf_div3f only adds the select that -0 and
+// infinities need.  The precondition is checked per staged row (see
+// box_fused): every input value is a non-negative float below 2^126, so each
+// 3-term sum of the chain (and every quotient) is +0 or positive and finite.
+constexpr float RN3 = 0x1.555556p-2f;
+__device__ __forceinline__ float div3_nn(float x) {
+  const float q = __fmul_rn(x, RN3);
+  return __fmaf_rn(__fmaf_rn(-q, 3.0f, x), RN3, q);
+}
+__device__ __forceinline__ float2 div3_nn2(float2 x) {  // lanewise, packed FFMA2/FMUL2
+  const float2 r = make_float2(RN3, RN3);
+  const float2 q = __fmul2_rn(x, r);
+  return __ffma2_rn(__ffma2_rn(q, make_float2(-3.0f, -3.0f), x), r, q);
+}
+// (a+b+c)/3 for the column pairs of one lane: left-to-right sums as the user kernel
+__device__ __forceinline__ float2 box3x2(float2 a, float2 b, float2 c) {
+  return div3_nn2(__fadd2_rn(__fadd2_rn(a, b), c));
+}
+// one 3-tap pass along i over a lane's 4 columns v (pairs p0 = (v0,v1), p1 = (v2,v3))
+// with left / right neighbours l, r
+__device__ __forceinline__ void row_pass_nn(float l, float2 p0, float2 p1, float r, float2* out) {
+  out[0] = box3x2(make_float2(l, p0.x), p0, make_float2(p0.y, p1.x));
+  out[1] = box3x2(make_float2(p0.y, p1.x), p1, make_float2(p1.y, r));
+}
+// exact for every input (the user kernel as written)
+__device__ __forceinline__ void row_pass_any(float l, float2 p0, float2 p1, float r, float2* out) {
+  float o0, o1, o2, o3;
+  box3(l, p0.x, p0.y, &o0);
+  box3(p0.x, p0.y, p1.x, &o1);
+  box3(p0.y, p1.x, p1.y, &o2);
+  box3(p1.x, p1.y, r, &o3);
+  out[0] = make_float2(o0, o1);
+  out[1] = make_float2(o2, o3);
+}
+__device__ __forceinline__ float2 col_pass_any(float2 a, float2 b, float2 c) {
+  float x, y;
+  box3(a.x, b.x, c.x, &x);
+  box3(a.y, b.y, c.y, &y);
+  return make_float2(x, y);
+}
+
+template <int P, bool FAST>
 __device__ __forceinline__ void box_row(Win& w, const float* row, int t, int lane, int ex_col, float* orow,
                                         uint64_t pol) {
   constexpr int C = P, M1 = (P + 2) % 3, M2 = (P + 1) % 3;  // rows r, r-1, r-2
   // 8-B aligned halves: the staged row starts at logical i0-2
-  const float2 v01 = *reinterpret_cast<const float2*>(row + LPAD + CPL * lane);
-  const float2 v23 = *reinterpret_cast<const float2*>(row + LPAD + CPL * lane + 2);
-  const float4 v = make_float4(v01.x, v01.y, v23.x, v23.y);
+  const float2 p0 = *reinterpret_cast<const float2*>(row + LPAD + CPL * lane);
+  const float2 p1 = *reinterpret_cast<const float2*>(row + LPAD + CPL * lane + 2);
   const float2 ex = *reinterpret_cast<const float2*>(row + ex_col);
+  auto bx = [](float a, float b, float c) {
+    float o;
+    if (FAST)
+      o = div3_nn(__fadd_rn(__fadd_rn(a, b), c));
+    else
+      box3(a, b, c, &o);
+    return o;
+  };
   // ---- row1 at row r
   {
-    const float left = __shfl_up_sync(0xffffffffu, v.w, 1);
-    const float right = __shfl_down_sync(0xffffffffu, v.x, 1);
-    const float a = lane == 0 ? ex.y : left;       // logical -1 for lane 0
-    const float b = lane == 31 ? ex.x : right;     // logical SW for lane 31
-    box3(a, v.x, v.y, &w.r1[C][0]);
-    box3(v.x, v.y, v.z, &w.r1[C][1]);
-    box3(v.y, v.z, v.w, &w.r1[C][2]);
-    box3(v.z, v.w, b, &w.r1[C][3]);
+    const float left = __shfl_up_sync(0xffffffffu, p1.y, 1);
+    const float right = __shfl_down_sync(0xffffffffu, p0.x, 1);
+    const float a = lane == 0 ? ex.y : left;    // logical -1 for lane 0
+    const float b = lane == 31 ? ex.x : right;  // logical SW for lane 31
+    if (FAST)
+      row_pass_nn(a, p0, p1, b, w.r1[C]);
+    else
+      row_pass_any(a, p0, p1, b, w.r1[C]);
     // halo column: lane 0 -> logical -1 = box3(img[-2], img[-1], img[0]);
     //              lane 31 -> logical SW = box3(img[SW-1], img[SW], img[SW+1])
     const bool lo = lane == 0;
-    box3(lo ? ex.x : v.w, lo ? ex.y : ex.x, lo ? v.x : ex.y, &w.r1h[C]);
+    w.r1h[C] = bx(lo ? ex.x : p1.y, lo ? ex.y : ex.x, lo ? p0.x : ex.y);
   }
   if (t < 2) return;
   // ---- col1 at row r-1 (own columns and the halo column), then row2 at row r-1
-  float c1[CPL], c1h;
+  float2 c1[2];
 #pragma unroll
-  for (int c = 0; c < CPL; ++c) box3(w.r1[M2][c], w.r1[M1][c], w.r1[C][c], &c1[c]);
-  box3(w.r1h[M2], w.r1h[M1], w.r1h[C], &c1h);
+  for (int c = 0; c < 2; ++c)
+    c1[c] = FAST ? box3x2(w.r1[M2][c], w.r1[M1][c], w.r1[C][c]) : col_pass_any(w.r1[M2][c], w.r1[M1][c], w.r1[C][c]);
+  const float c1h = bx(w.r1h[M2], w.r1h[M1], w.r1h[C]);
   {
-    const float left = __shfl_up_sync(0xffffffffu, c1[CPL - 1], 1);
-    const float right = __shfl_down_sync(0xffffffffu, c1[0], 1);
+    const float left = __shfl_up_sync(0xffffffffu, c1[1].y, 1);
+    const float right = __shfl_down_sync(0xffffffffu, c1[0].x, 1);
     const float a = lane == 0 ? c1h : left;
     const float b = lane == 31 ? c1h : right;
-    box3(a, c1[0], c1[1], &w.r2[M1][0]);
-    box3(c1[0], c1[1], c1[2], &w.r2[M1][1]);
-    box3(c1[1], c1[2], c1[3], &w.r2[M1][2]);
-    box3(c1[2], c1[3], b, &w.r2[M1][3]);
+    if (FAST)
+      row_pass_nn(a, c1[0], c1[1], b, w.r2[M1]);
+    else
+      row_pass_any(a, c1[0], c1[1], b, w.r2[M1]);
   }
   if (t < 4) return;
   // ---- col2 at row r-2: r2 rows r-3 (slot C), r-2 (M2), r-1 (M1)
-  float o[CPL];
+  float2 o[2];
 #pragma unroll
-  for (int c = 0; c < CPL; ++c) box3(w.r2[C][c], w.r2[M2][c], w.r2[M1][c], &o[c]);
-  st_hint4(orow + CPL * lane, o[0], o[1], o[2], o[3], pol);
+  for (int c = 0; c < 2; ++c)
+    o[c] = FAST ? box3x2(w.r2[C][c], w.r2[M2][c], w.r2[M1][c]) : col_pass_any(w.r2[C][c], w.r2[M2][c], w.r2[M1][c]);
+  st_hint4(orow + CPL * lane, o[0].x, o[0].y, o[1].x, o[1].y, pol);
+}
+
+// 1 if this lane's staged values of the row are non-negative floats < 2^126
+__device__ __forceinline__ bool row_nn(const float* row, int lane, int ex_col) {
+  const uint2 v0 = *reinterpret_cast<const uint2*>(row + LPAD + CPL * lane);
+  const uint2 v1 = *reinterpret_cast<const uint2*>(row + LPAD + CPL * lane + 2);
+  const uint2 e = *reinterpret_cast<const uint2*>(row + ex_col);
+  const unsigned m = max(max(max(v0.x, v0.y), max(v1.x, v1.y)), max(e.x, e.y));
+  return m <= 0x7EFFFFFFu;
 }
 
 __global__ void __launch_bounds__(32, OCC)
@@ -120,14 +182,26 @@ __global__ void __launch_bounds__(32, OCC)
     const RowSeg sg = seg[k];
     const int T = sg.je - sg.jb + 2 * H;
     float* orow = out + (long long)(sg.jb - 4) * p.out_pitch + sg.strip * SW;  // output row of t = 0
+    int ok_run = 0;  // consecutive staged rows meeting the fast-path precondition
     for (int t0 = 0; t0 < T; t0 += R, ++g) {
       rr.wait(g);
       const float* st = reinterpret_cast<const float*>(rr.stage(g));
-      box_row<0>(w, st, t0, lane, ex_col, orow, pol);
+      // a row step touches staged rows r-4..r: fast when all five qualify
+#define LF_BOX_ROW(P_, t_)                                                                        \
+  {                                                                                               \
+    const float* rw = st + (P_)*BOXW;                                                             \
+    ok_run = __all_sync(0xffffffffu, row_nn(rw, lane, ex_col)) ? ok_run + 1 : 0;                  \
+    if (ok_run >= 5)                                                                              \
+      box_row<P_, true>(w, rw, t_, lane, ex_col, orow, pol);                                      \
+    else                                                                                          \
+      box_row<P_, false>(w, rw, t_, lane, ex_col, orow, pol);                                     \
+  }
+      LF_BOX_ROW(0, t0)
       orow += p.out_pitch;
-      if (t0 + 1 < T) box_row<1>(w, st + BOXW, t0 + 1, lane, ex_col, orow, pol);
+      if (t0 + 1 < T) LF_BOX_ROW(1, t0 + 1)
       orow += p.out_pitch;
-      if (t0 + 2 < T) box_row<2>(w, st + 2 * BOXW, t0 + 2, lane, ex_col, orow, pol);
+      if (t0 + 2 < T) LF_BOX_ROW(2, t0 + 2)
+#undef LF_BOX_ROW
       orow += p.out_pitch;
       __syncwarp();
       if (lane == 0) rr.issue(g + S, &tin);
@@ -177,11 +251,7 @@ int run(const ExecArgs& a, std::string& err) {
   p.row_hi = rp.hi;
   p.out_pitch = ni;
   p.strips = ni / SW;
-  const long long work = (long long)p.strips * (rp.hi - rp.lo);
-  // each CTA must get at most 3 row segments (rowstream.cuh): at least
-  // ceil(strips/2) CTAs when the row range is short
-  const long long want = std::max<long long>(work / 16, (p.strips + 1) / 2);
-  const int ctas = static_cast<int>(std::max<long long>(1, std::min<long long>(slots, want)));
+  const int ctas = rowstream_ctas(slots, p.strips, rp.hi - rp.lo);
   if ((long long)ctas * 2 < p.strips) {
     err = "row range too short for the resident grid";
     return LF_ERR_UNSUPPORTED;

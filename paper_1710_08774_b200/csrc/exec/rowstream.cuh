@@ -45,6 +45,18 @@ __device__ __forceinline__ int cta_segments(int cta, int ctas, int strips, int r
   return n;
 }
 
+// Persistent grid for `strips` strips of `rows` rows on `slots` resident CTAs.
+// A whole multiple of `strips` CTAs makes CTA c + ctas/strips start strip s+1
+// at exactly the row where CTA c starts strip s, so the halo columns two
+// neighbours share are fetched within moments of each other (one DRAM read,
+// one L2 hit).  At least ceil(strips/2) CTAs: a CTA takes at most 3 segments.
+inline int rowstream_ctas(long long slots, int strips, long long rows) {
+  const long long work = (long long)strips * rows;
+  long long ctas = std::max<long long>(1, std::min<long long>(slots, std::max<long long>(work / 16, (strips + 1) / 2)));
+  if (ctas >= strips) ctas = ctas / strips * strips;
+  return static_cast<int>(ctas);
+}
+
 // One-warp TMA row ring.  Stage g covers rows [jb-H + gg*R, +R) of its
 // segment (gg = stage index within the segment).
 template <int R, int S>

@@ -5,7 +5,7 @@
 set -u
 mkdir -p gpurun_out
 nvidia-smi > gpurun_out/smi.txt 2>&1
-CFGS=${CFGS:-heat3d}
+CFGS=${CFGS-heat3d}
 NCU_CFG=${NCU_CFG:-heat3d}
 KREGEX=${KREGEX:-$NCU_CFG}
 if [ "${TESTS:-1}" = "1" ]; then
@@ -20,7 +20,7 @@ if [ "${NCU:-1}" = "1" ]; then
   timeout 600 python bench.py --config $C --steps 1 --warmup 1 --no-cpu --no-e2e > gpurun_out/plain.log 2>&1 && \
   timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_$C.csv \
       python bench.py --config $C --steps 1 --warmup 1 --no-cpu --no-e2e > gpurun_out/ncu_launches.log 2>&1 && \
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:$KREGEX -s 3 -c 1 -o gpurun_out/prof_$C \
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:$KREGEX -s ${SKIP:-3} -c 1 -o gpurun_out/prof_$C \
       python bench.py --config $C --steps 1 --warmup 1 --no-cpu --no-e2e > gpurun_out/ncu_full.log 2>&1
   echo "ncu exit=$?" >> gpurun_out/ncu_full.log
 fi
