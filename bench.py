@@ -108,6 +108,22 @@ def measured_peak():
     return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
 
 
+# Hydro2D: algorithmic flops per cell-step of the user kernels as written
+# (oracle/flopcount.cpp, pinned by tests/test_flopcount.py; + - * / sqrt = 1)
+HYDRO_FLOPS_PER_CELL_STEP = 995.3264
+
+
+def measured_fp64_peak():
+    """fp64 FMA-pipe TFLOP/s measured live by tools/libfp64probe.so (8 DFMA
+    chains per thread, 8 CTAs of 256 per SM, best of 5)."""
+    import ctypes
+    lib = ctypes.CDLL(str(ROOT / "tools" / "libfp64probe.so"))
+    out = ctypes.c_double(0.0)
+    if lib.lf_probe_fp64_tflops(5, ctypes.byref(out)) != 0:
+        raise RuntimeError("fp64 probe failed")
+    return out.value
+
+
 def ncu_traffic(workload):
     """DRAM bytes per launch from the committed ncu summary, if any."""
     p = ROOT / "profiles" / "traffic.json"
@@ -380,6 +396,16 @@ def main():
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                 "traffic": ncu_traffic(args.config), "peak_source": peak_src,
                 "algorithmic_bytes_per_cell": bpc}
+    if w["spec"] == "hydro2d":
+        # compute-bound chain: the fp64 roofline is the binding one; HBM kept beside it
+        fpk = measured_fp64_peak()
+        tf = HYDRO_FLOPS_PER_CELL_STEP * cells_per_launch / launch_s / 1e12
+        roofline = {"bound": "fp64", "achieved": tf, "peak": fpk, "unit": "TFLOP/s", "frac": tf / fpk,
+                    "traffic": ncu_traffic(args.config),
+                    "peak_source": "measured live (tools/fp64_probe.cu: DFMA chains)",
+                    "algorithmic_flops_per_cell_step": HYDRO_FLOPS_PER_CELL_STEP,
+                    "hbm": {"achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                            "algorithmic_bytes_per_cell": bpc, "peak_source": peak_src}}
 
     line = {
         "metric": metric, "value": value, "unit": "cell-updates/s", "n_gpus": world, "steps": args.steps,
