@@ -88,9 +88,9 @@ LF_HD void hy_trace(double r, double n, double t, double p, double dr, double dn
 /* Godunov state at a face from left/right primitive states: two-shock
  * approximation of the exact Riemann problem, p* by HY_NITER Newton steps on
  * the Lagrangian wave speeds w = c*sqrt(1 + k (p*-p)/p), then sampling at
- * x/t = 0 with a linear fan.  Written with reciprocals so that a Newton step
- * costs 2 sqrt + 3 divisions: z = 2w^3/(w^2+c^2) enters only through
- * z_l z_r / (z_l + z_r) = 1 / (1/z_l + 1/z_r).
+ * x/t = 0 with a linear fan.  z = 2w^3/(w^2+c^2) enters only through
+ * z_l z_r / (z_l + z_r) = 1 / (1/z_l + 1/z_r), and the step is written over
+ * one common denominator, so a Newton step costs 2 sqrt + 1 division.
  *
  * The solver is split into init / newton / sample so an executor can advance
  * two independent problems in one loop (hy_riemann is exactly
@@ -119,12 +119,14 @@ LF_HD double hy_riemann_init(double rl, double nl, double pl, double rr, double 
 LF_HD double hy_riemann_newton(const hy_rp* c, double ps) {
   const double wl = c->cl * sqrt(1.0 + c->kpl * (ps - c->pl));
   const double wr = c->cr * sqrt(1.0 + c->kpr * (ps - c->pr));
-  const double iwl = 1.0 / wl, iwr = 1.0 / wr;
-  const double izl = 0.5 * (wl * wl + c->cl2) * (iwl * iwl * iwl); /* 1/z_l */
-  const double izr = 0.5 * (wr * wr + c->cr2) * (iwr * iwr * iwr);
-  const double usl = c->nl - (ps - c->pl) * iwl;
-  const double usr = c->nr + (ps - c->pr) * iwr;
-  return hy_max(ps + (usl - usr) / (izl + izr), HY_SMALLP);
+  /* (u*_l - u*_r) / (1/z_l + 1/z_r) over one common denominator:
+   *   u*_l - u*_r = ((nl - nr) wl wr - (ps - pl) wr - (ps - pr) wl) / (wl wr)
+   *   1/z_l + 1/z_r = ((wl^2 + cl^2) wr^3 + (wr^2 + cr^2) wl^3) / (2 wl^3 wr^3)
+   * so a Newton step costs 2 sqrt + 1 division. */
+  const double wl2 = wl * wl, wr2 = wr * wr;
+  const double num = 2.0 * wl2 * wr2 * ((c->nl - c->nr) * wl * wr - (ps - c->pl) * wr - (ps - c->pr) * wl);
+  const double den = (wl2 + c->cl2) * (wr2 * wr) + (wr2 + c->cr2) * (wl2 * wl);
+  return hy_max(ps + num / den, HY_SMALLP);
 }
 
 LF_HD void hy_riemann_sample(const hy_rp* c, double ps, double rl, double tl, double rr, double tr, double* gr,
