@@ -166,9 +166,21 @@ def _fill(a, modes, n, base):
                 a[tuple(dst)] = -a[tuple(src)] if m == "odd" else a[tuple(src)]
 
 
+def _term_axes(term, nd):
+    """loop dims a term spans (others are broadcast axes of length 1)"""
+    return {dim for dim, _ in term["dims"]}
+
+
 def run_naive(spec_path, axioms: dict, steps: int = 1) -> dict:
     """Goal buffers after `steps` applications of the chain (axioms untouched).
-    Iterated goals take their paired axiom's layout and ghost refill."""
+    Iterated goals take their paired axiom's layout and ghost refill.
+
+    Every term value is an array over all loop dims (length 1 along the dims
+    the term does not span).  An associative kernel (a reduction: its element
+    inputs span loop dims its output does not) runs sequentially over those
+    dims in loop order, starting from its carry input -- the order in which
+    run_naive's sweep of the group over its space visits them
+    (R/SPEC.md:532-540)."""
     d = ref_dag(spec_path)
     n = [hi - lo for lo, hi in d["ranges"]]
     nd = len(n)
@@ -177,6 +189,10 @@ def run_naive(spec_path, axioms: dict, steps: int = 1) -> dict:
     bodies = {k: {o: parse_body(b) for o, b in v["bodies"].items()} for k, v in kern.items()}
     cur = {k: np.array(v) for k, v in axioms.items()}
     goals = {}
+
+    def shape_of(axes):
+        return [n[k] if k in axes else 1 for k in range(nd)]
+
     for _ in range(steps):
         vals = {}
         goals = {}
@@ -193,25 +209,65 @@ def run_naive(spec_path, axioms: dict, steps: int = 1) -> dict:
                     vals[rap["out"][0]] = a.reshape(-1)[0]
                     continue
                 ext = d["externals"][rap["external"]]["extents"]
-                sl = []
+                sl, axes = [], []
                 for k, (dim, shift) in enumerate(rap["slots"]):
                     start = shift - ext[k][1]
-                    sl.append(slice(start, start + n[dim]))
-                vals[rap["out"][0]] = a[tuple(sl)]
+                    if dim < 0:
+                        sl.append(start)  # constant subscript
+                    else:
+                        sl.append(slice(start, start + n[dim]))
+                        axes.append(dim)
+                v = a[tuple(sl)]
+                # slot order follows the loop order: place the sliced axes, pad the rest
+                vals[rap["out"][0]] = v.reshape(shape_of(set(axes)))
             elif rap["kind"] == "kernel":
                 k = kern[rap["kernel"]]
-                env = dict(zip(k["inputs"], (vals[t] for t in rap["in"])))
+                ins = [vals[t] for t in rap["in"]]
                 dt = None
-                for v in env.values():
+                for v in ins:
                     dt = np.asarray(v).dtype.type
+                if k.get("associative"):
+                    (o_name,) = k["outputs"]
+                    out_t = terms[rap["out"][0]]
+                    out_axes = _term_axes(out_t, nd)
+                    space = set(out_axes)
+                    carry = None
+                    for i, t in enumerate(rap["in"]):
+                        tt = terms[t]
+                        space |= _term_axes(tt, nd)
+                        if tt["ident"] == out_t["ident"] and tt["dims"] == out_t["dims"] and tt["tag"] != out_t["tag"]:
+                            carry = i
+                    red = sorted(space - out_axes)
+                    acc = np.broadcast_to(np.asarray(ins[carry], dtype=dt), shape_of(out_axes)).copy()
+                    for pos in np.ndindex(*[n[a] for a in red]):
+                        env = {}
+                        for i, (pname, v) in enumerate(zip(k["inputs"], ins)):
+                            if i == carry:
+                                env[pname] = acc
+                                continue
+                            v = np.asarray(v)
+                            ix = [slice(None)] * nd
+                            for a, p in zip(red, pos):
+                                if v.ndim == nd and v.shape[a] > 1:
+                                    ix[a] = slice(p, p + 1)
+                            env[pname] = v[tuple(ix)] if v.ndim == nd else v
+                        acc = np.asarray(eval_body(bodies[rap["kernel"]][o_name], env, dt), dtype=dt)
+                    vals[rap["out"][0]] = acc
+                    continue
+                env = dict(zip(k["inputs"], ins))
                 for o, t in zip(k["outputs"], rap["out"]):
                     vals[t] = np.asarray(eval_body(bodies[rap["kernel"]][o], env, dt), dtype=dt)
             else:
                 g = rap["external"]
                 a = goals[g]
-                base = [b for _, b in (d["externals"][pair[g]] if g in pair else d["externals"][g])["extents"]]
-                sl = tuple(slice(-base[k], -base[k] + n[k]) for k in range(nd))
-                a[sl] = np.broadcast_to(vals[rap["in"][0]], [n[k] for k in range(nd)])
+                ext = (d["externals"][pair[g]] if g in pair else d["externals"][g])["extents"]
+                sl, axes = [], []
+                for k, (dim, shift) in enumerate(rap["slots"]):
+                    start = shift - ext[k][1]
+                    sl.append(slice(start, start + n[dim]))
+                    axes.append(dim)
+                v = np.broadcast_to(vals[rap["in"][0]], shape_of(set(axes)))
+                a[tuple(sl)] = v.reshape([n[dim] for dim in axes])
         for g, a_name in pair.items():
             modes = d["boundary"].get(g) or d["boundary"].get("*") or ["none"]
             base = [b for _, b in d["externals"][a_name]["extents"]]

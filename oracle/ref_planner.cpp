@@ -169,7 +169,8 @@ void dump_dag(const lf::RuleSet& mine, const loomfuse::RuleSet& rs, const loomfu
   os << "],\"kernels\":{";
   for (size_t k = 0; k < mine.kernels.size(); ++k) {
     const auto& kr = mine.kernels[k];
-    os << (k ? "," : "") << jstr(kr.name) << ":{\"declaration\":" << jstr(kr.declaration) << ",\"inputs\":[";
+    os << (k ? "," : "") << jstr(kr.name) << ":{\"declaration\":" << jstr(kr.declaration)
+       << ",\"associative\":" << (kr.associative ? "true" : "false") << ",\"inputs\":[";
     for (size_t i = 0; i < kr.inputs.size(); ++i) os << (i ? "," : "") << jstr(kr.inputs[i].first);
     os << "],\"outputs\":[";
     for (size_t i = 0; i < kr.outputs.size(); ++i) os << (i ? "," : "") << jstr(kr.outputs[i].first);

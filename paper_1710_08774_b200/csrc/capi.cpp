@@ -235,13 +235,17 @@ int lf_plan_report(const lf_plan* plan, char* buf, size_t cap, size_t* needed) {
 const char* lf_plan_executor(const lf_plan* plan) {
   if (!plan) return "";
   if (plan->exec) return plan->exec->name;
-  return plan->jit ? (plan->jit->program().march ? "jit_window_fused" : "jit_tiled_fused") : "";
+  if (!plan->jit) return "";
+  const auto& pg = plan->jit->program();
+  return !pg.nest_kernels.empty() ? "jit_nests_fused" : (pg.march ? "jit_window_fused" : "jit_tiled_fused");
 }
 
 int lf_plan_launches_per_step(const lf_plan* plan) {
   if (!plan) return 0;
   if (plan->exec) return plan->exec->launches_per_step;
-  return plan->jit ? (plan->jit->program().has_fill ? 2 : 1) : 0;
+  if (!plan->jit) return 0;
+  const auto& pg = plan->jit->program();
+  return static_cast<int>(std::max<size_t>(1, pg.nest_kernels.size())) + (pg.has_fill ? 1 : 0);
 }
 
 double lf_plan_compulsory_bytes_per_cell(const lf_plan* plan) {

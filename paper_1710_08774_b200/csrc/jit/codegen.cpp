@@ -23,6 +23,7 @@
 #include <cstdlib>
 #include <deque>
 #include <map>
+#include <set>
 #include <sstream>
 
 #include "../planner/dsl.hpp"
@@ -792,9 +793,466 @@ bool emit_fill(Ctx& C, JitProgram& out, std::ostream& fill) {
   return true;
 }
 
+// ---------------------------------------------------------------------------
+// Multi-nest plans (reductions / broadcast splits, fusion.cpp:8-95; the
+// paper's section 3.4): one kernel per fused nest, in nest dataflow order.
+// Terms produced in one nest and read in another are materialised in
+// plan-owned buffers with the variable's buffer extents (storage.cpp:403-427);
+// everything else is recomputed per cell from the reference DAG's rule
+// applications.  A nest holding associative kernels is a reduction nest:
+// one warp per cell of its parallel dims, the reduced dims marched in loop
+// order 32 elements at a time -- lanes evaluate the elements, then the
+// accumulation runs in element order, so the result equals run_naive's
+// sequential sweep bit for bit (no reassociation needed).
+// ---------------------------------------------------------------------------
+bool emit_nests(const lf::Plan& P, JitProgram& out, std::ostream& src, std::string& err) {
+  const auto& rs = P.rs;
+  const auto& g = P.dag;
+  const int nd = static_cast<int>(rs.loop_order.size());
+  auto fail = [&](const std::string& m) {
+    err = m;
+    return false;
+  };
+  if (nd < 1 || nd > 3) return fail("generic executor handles 1-3 loop dimensions");
+  for (const auto& r : rs.ranges)
+    if (r.stride != 1) return fail("generic executor needs unit strides");
+  std::string T;
+  for (const auto& t : P.terminals) {
+    std::string e = elem_type(t.type);
+    if (e.empty()) return fail("unsupported terminal type '" + t.type + "'");
+    if (!T.empty() && e != T) return fail("mixed element types in one chain");
+    T = e;
+  }
+  for (const auto& v : P.vars) {
+    if (!v.external.empty() || v.alias_of >= 0) continue;
+    std::string e = elem_type(v.type);
+    if (e.empty() || e != T) return fail("intermediate '" + v.name + "' has type '" + v.type + "'");
+  }
+  out.type = T;
+  out.elem_bytes = T == "double" ? 8 : 4;
+  out.nd = nd;
+  std::vector<long> N(nd), LO(nd);
+  for (int d = 0; d < nd; ++d) {
+    N[d] = rs.ranges[d].trips();
+    LO[d] = rs.ranges[d].lo;
+  }
+  const int nr = static_cast<int>(g.raps.size());
+  auto nest_of = [&](int r) { return P.vertex_of_group[P.group_of[r]]; };
+  auto term_axes = [&](int t) {
+    std::set<int> a;
+    for (const auto& o : g.terms[t].dims) a.insert(o.dim);
+    return a;
+  };
+  auto term_off = [&](int t, int d) {
+    for (const auto& o : g.terms[t].dims)
+      if (o.dim == d) return o.offset;
+    return 0;
+  };
+  for (int r = 0; r < nr; ++r)
+    if (g.raps[r].kind == lf::RapKind::kernel) {
+      const auto& k = rs.kernels[g.raps[r].kernel];
+      for (const auto& [op, pat] : k.outputs)
+        if (!k.bodies.count(op))
+          return fail("kernel '" + k.name + "' has no body for output '" + op +
+                      "' (the generic executor compiles `body:` expressions)");
+    }
+  // ---- nests in dataflow order (kernel and store raps; loads go where read)
+  std::set<int> nest_ids;
+  for (int r = 0; r < nr; ++r)
+    if (g.raps[r].kind != lf::RapKind::load) nest_ids.insert(nest_of(r));
+  std::map<int, std::set<int>> nadj;
+  std::map<int, int> nindeg;
+  for (int v : nest_ids) nindeg[v] = 0;
+  for (const auto& e : g.edges) {
+    if (g.raps[e.from].kind == lf::RapKind::load) continue;
+    const int a = nest_of(e.from), b = nest_of(e.to);
+    if (a != b && nadj[a].insert(b).second) ++nindeg[b];
+  }
+  std::vector<int> norder;
+  {
+    std::deque<int> q;
+    for (int v : nest_ids)
+      if (!nindeg[v]) q.push_back(v);
+    while (!q.empty()) {
+      int v = q.front();
+      q.pop_front();
+      norder.push_back(v);
+      for (int w : nadj[v])
+        if (--nindeg[w] == 0) q.push_back(w);
+    }
+    if (norder.size() != nest_ids.size()) return fail("cyclic nest dataflow");
+  }
+  const std::vector<int> topo = g.topo_order();
+  // ---- materialised terms: kernel outputs read by a rap of another nest
+  std::map<int, int> mat_of_var;  // var -> materialised buffer index
+  std::vector<int> mat_vars;
+  std::vector<char> term_mat(g.terms.size(), 0);
+  for (const auto& e : g.edges) {
+    const auto& from = g.raps[e.from];
+    if (from.kind != lf::RapKind::kernel) continue;
+    if (nest_of(e.from) == nest_of(e.to)) continue;
+    term_mat[e.term] = 1;
+    const int v = P.var_of_term[e.term];
+    if (!mat_of_var.count(v)) {
+      mat_of_var[v] = static_cast<int>(mat_vars.size());
+      mat_vars.push_back(v);
+    }
+  }
+  const int nterm = static_cast<int>(P.terminals.size());
+  if (nterm + (int)mat_vars.size() > 32) return fail("more than 32 terminal and materialised buffers");
+  out.mat_bytes.clear();
+  for (int v : mat_vars) {
+    size_t n = out.elem_bytes;
+    for (const auto& [ext, base] : P.vars[v].extents) n *= static_cast<size_t>(ext);
+    out.mat_bytes.push_back(n);
+  }
+  auto terminal_of = [&](const std::string& name, bool goal) {
+    for (size_t i = 0; i < P.terminals.size(); ++i)
+      if (P.terminals[i].name == name && P.terminals[i].is_goal == goal) return static_cast<int>(i);
+    return -1;
+  };
+  auto pitch = [&](const std::vector<long>& ext, size_t slot) {
+    long p = 1;
+    for (size_t k = slot + 1; k < ext.size(); ++k) p *= ext[k];
+    return p;
+  };
+  // index of terminal `ti` for a load / store rap (slot coordinate = x + shift - base)
+  auto slot_index = [&](int ti, const std::vector<lf::ExtSlot>& slots) {
+    const auto& t = P.terminals[ti];
+    std::string e;
+    for (size_t s = 0; s < slots.size(); ++s) {
+      const long c0 = slots[s].shift - t.base[s] + (slots[s].dim >= 0 ? LO[slots[s].dim] : 0);
+      std::string c = slots[s].dim >= 0 ? "(long long)(x" + std::to_string(slots[s].dim) + plus(c0) + ")"
+                                        : std::to_string(c0) + "LL";
+      const long p = pitch(t.extent, s);
+      e += (e.empty() ? "" : " + ") + c + (p != 1 ? " * " + std::to_string(p) + "LL" : "");
+    }
+    return e.empty() ? std::string("0") : e;
+  };
+  // index of materialised var buffer for term t at the current cell
+  auto mat_index = [&](int t) {
+    const int v = P.var_of_term[t];
+    const auto& var = P.vars[v];
+    std::vector<long> ext;
+    for (const auto& [e, b] : var.extents) ext.push_back(e);
+    std::string e;
+    for (size_t s = 0; s < var.dims.size(); ++s) {
+      const int d = var.dims[s];
+      const long c0 = term_off(t, d) + LO[d] - var.extents[s].second;
+      const std::string c = "(long long)(x" + std::to_string(d) + plus(c0) + ")";
+      const long p = pitch(ext, s);
+      e += (e.empty() ? "" : " + ") + c + (p != 1 ? " * " + std::to_string(p) + "LL" : "");
+    }
+    return "m" + std::to_string(mat_of_var.at(v)) + "[" + (e.empty() ? std::string("0") : e) + "]";
+  };
+
+  src << "// generated by loomfuse-b200 (csrc/jit/codegen.cpp, multi-nest) for chain '" << rs.name << "'\n";
+  src << "typedef " << T << " T;\n";
+  src << "__device__ __forceinline__ T lf_min(T a, T b) { return a < b ? a : b; }\n";
+  src << "__device__ __forceinline__ T lf_max(T a, T b) { return a > b ? a : b; }\n";
+  src << "struct LfArgs { void* t[32]; long long n0; int row_lo, row_hi, top, bottom, chunk, pad; };\n";
+  auto pointers = [&](std::ostream& o) {
+    for (int i = 0; i < nterm; ++i) {
+      const auto& t = P.terminals[i];
+      if (t.dims.empty())
+        o << "  const T s" << i << " = *reinterpret_cast<const T*>(a.t[" << i << "]);\n";
+      else
+        o << "  " << (t.is_goal ? "T" : "const T") << "* __restrict__ t" << i << " = reinterpret_cast<"
+          << (t.is_goal ? "T" : "const T") << "*>(a.t[" << i << "]);\n";
+    }
+    for (size_t m = 0; m < mat_vars.size(); ++m)
+      o << "  T* __restrict__ m" << m << " = reinterpret_cast<T*>(a.t[" << (nterm + m) << "]);  // '"
+        << P.vars[mat_vars[m]].name << "'\n";
+  };
+  // value expression of an input term of a rap in nest `nv` (computed locally or loaded)
+  std::vector<char> done;  // per term: already defined in the current scope
+  // `guard`: condition on the stores (terminal and materialised) of this rap
+  auto emit_rap = [&](int r, int nv, std::ostream& o, const std::string& ind, bool& okk, const std::string& guard) {
+    const std::string G = guard.empty() ? std::string() : "if (" + guard + ") ";
+    const auto& rap = g.raps[r];
+    auto need = [&](int t) {
+      if (done[t]) return;
+      const int pr = g.producer[t];
+      if (pr >= 0 && g.raps[pr].kind == lf::RapKind::kernel && nest_of(pr) != nv) {
+        o << ind << "const T v" << t << " = " << mat_index(t) << ";\n";
+        done[t] = 1;
+      }
+    };
+    if (rap.kind == lf::RapKind::load) {
+      const int ti = terminal_of(rap.external, false);
+      if (ti < 0) {
+        okk = false;
+        err = "axiom '" + rap.external + "' not found";
+        return;
+      }
+      const int t = rap.out_terms[0];
+      if (P.terminals[ti].dims.empty() && rap.ext_slots.empty())
+        o << ind << "const T v" << t << " = s" << ti << ";\n";
+      else
+        o << ind << "const T v" << t << " = t" << ti << "[" << slot_index(ti, rap.ext_slots) << "];\n";
+      done[t] = 1;
+    } else if (rap.kind == lf::RapKind::store) {
+      const int ti = terminal_of(rap.external, true);
+      if (ti < 0) {
+        okk = false;
+        err = "goal '" + rap.external + "' not found";
+        return;
+      }
+      need(rap.in_terms[0]);
+      o << ind << G << "t" << ti << "[" << slot_index(ti, rap.ext_slots) << "] = v" << rap.in_terms[0] << ";\n";
+    } else {
+      const auto& k = rs.kernels[rap.kernel];
+      for (int t : rap.in_terms) need(t);
+      for (size_t i = 0; i < k.outputs.size(); ++i) {
+        std::string e2;
+        auto e = lf::parse_expr(k.bodies.at(k.outputs[i].first), e2);
+        if (!e) {
+          okk = false;
+          err = "kernel '" + k.name + "': " + e2;
+          return;
+        }
+        std::map<std::string, std::string> pv;
+        for (size_t j = 0; j < k.inputs.size(); ++j) pv[k.inputs[j].first] = "v" + std::to_string(rap.in_terms[j]);
+        std::set<std::string> used;
+        lf::expr_vars(*e, used);
+        for (const auto& u : used)
+          if (!pv.count(u)) {
+            okk = false;
+            err = "kernel '" + k.name + "' body uses unknown name '" + u + "'";
+            return;
+          }
+        const int t = rap.out_terms[i];
+        o << ind << "const T v" << t << " = " << lf::emit_c(*e, T, [&](const std::string& n) { return pv.at(n); })
+          << ";\n";
+        done[t] = 1;
+        if (term_mat[t]) o << ind << G << mat_index(t) << " = v" << t << ";\n";
+      }
+    }
+  };
+  out.nest_kernels.clear();
+  int kid = 0;
+  for (int nv : norder) {
+    // raps of this nest (kernels, stores) plus the loads they read
+    std::vector<char> in_nest(nr, 0);
+    for (int r = 0; r < nr; ++r)
+      if (g.raps[r].kind != lf::RapKind::load && nest_of(r) == nv) in_nest[r] = 1;
+    for (int r = 0; r < nr; ++r)
+      if (in_nest[r])
+        for (int t : g.raps[r].in_terms) {
+          const int pr = g.producer[t];
+          if (pr >= 0 && g.raps[pr].kind == lf::RapKind::load) in_nest[pr] = 1;
+        }
+    std::set<int> space;
+    for (int r = 0; r < nr; ++r)
+      if (in_nest[r] && g.raps[r].kind != lf::RapKind::load)
+        for (int d : P.groups[P.group_of[r]].space) space.insert(d);
+    // reductions
+    std::vector<int> reds;
+    std::set<int> R;
+    for (int r = 0; r < nr; ++r)
+      if (in_nest[r] && g.raps[r].kind == lf::RapKind::kernel && rs.kernels[g.raps[r].kernel].associative) {
+        std::set<int> rd;
+        const auto oax = term_axes(g.raps[r].out_terms[0]);
+        for (int d : P.groups[P.group_of[r]].space)
+          if (!oax.count(d)) rd.insert(d);
+        if (rd.empty()) return fail("associative kernel '" + rs.kernels[g.raps[r].kernel].name + "' reduces nothing");
+        if (!reds.empty() && rd != R) return fail("reductions over different dimensions in one nest");
+        R = rd;
+        reds.push_back(r);
+      }
+    const std::string fn = "lf_nest" + std::to_string(kid++);
+    done.assign(g.terms.size(), 0);
+    bool okk = true;
+    std::ostringstream body;
+    NestLaunch nl;
+    nl.fn = fn;
+    if (reds.empty()) {
+      // ---- cell-parallel nest
+      long long cells = 1;
+      for (int d : space) cells *= N[d];
+      nl.reduction = false;
+      nl.units = cells;
+      src << "extern \"C\" __global__ void __launch_bounds__(256) " << fn << "(const LfArgs a) {\n";
+      pointers(src);
+      src << "  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < " << cells
+          << "LL; idx += (long long)gridDim.x * blockDim.x) {\n";
+      src << "    long long rem = idx;\n";
+      for (int d = nd - 1; d >= 0; --d) {
+        if (space.count(d))
+          src << "    const int x" << d << " = (int)(rem % " << N[d] << "); rem /= " << N[d] << ";\n";
+        else
+          src << "    const int x" << d << " = 0;\n";
+      }
+      for (int r : topo)
+        if (in_nest[r]) emit_rap(r, nv, src, "    ", okk, "");
+      src << "  }\n}\n";
+    } else {
+      // ---- reduction nest: warp per parallel cell, reduced dims in order
+      std::set<int> Pd;
+      for (int d : space)
+        if (!R.count(d)) Pd.insert(d);
+      long long pcells = 1, rcount = 1;
+      for (int d : Pd) pcells *= N[d];
+      for (int d : R) rcount *= N[d];
+      nl.reduction = true;
+      nl.units = pcells;
+      // classify raps: element (depends on the reduced dims), post (after a reduction), pre
+      std::vector<int> cls(nr, 0);  // 0 pre, 1 element, 2 reduction, 3 post
+      for (int r : topo) {
+        if (!in_nest[r]) continue;
+        const auto& rap = g.raps[r];
+        if (std::find(reds.begin(), reds.end(), r) != reds.end()) {
+          cls[r] = 2;
+          continue;
+        }
+        int c = 0;
+        for (int t : rap.in_terms) {
+          const int pr = g.producer[t];
+          if (pr >= 0 && in_nest[pr]) c = std::max(c, cls[pr] == 2 ? 3 : cls[pr]);
+        }
+        if (rap.kind == lf::RapKind::load) {
+          const auto ax = term_axes(rap.out_terms[0]);
+          for (int d : R)
+            if (ax.count(d)) c = std::max(c, 1);
+        } else if (rap.kind == lf::RapKind::store) {
+          const auto ax = term_axes(rap.in_terms[0]);
+          for (int d : R)
+            if (ax.count(d)) c = std::max(c, 1);
+        } else {
+          for (int d : P.groups[P.group_of[r]].space)
+            if (R.count(d)) c = std::max(c, 1);
+        }
+        if (c == 3 && rap.kind != lf::RapKind::store) {
+          for (int d : P.groups[P.group_of[r]].space)
+            if (R.count(d)) return fail("broadcast of a reduction inside its own nest (needs a split)");
+        }
+        cls[r] = c;
+      }
+      src << "extern \"C\" __global__ void __launch_bounds__(256) " << fn << "(const LfArgs a) {\n";
+      pointers(src);
+      src << "  __shared__ T lf_red[8][" << reds.size() << "][32];\n";
+      src << "  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;\n";
+      src << "  for (long long pc = blockIdx.x * 8LL + warp; pc < " << pcells << "LL; pc += gridDim.x * 8LL) {\n";
+      src << "    long long rem = pc;\n";
+      for (int d = nd - 1; d >= 0; --d)
+        if (Pd.count(d)) src << "    const int x" << d << " = (int)(rem % " << N[d] << "); rem /= " << N[d] << ";\n";
+      for (int d = 0; d < nd; ++d)
+        if (!Pd.count(d) && !R.count(d)) src << "    const int x" << d << " = 0;\n";
+      // pre raps (every lane)
+      for (int r : topo)
+        if (in_nest[r] && cls[r] == 0) emit_rap(r, nv, src, "    ", okk, "lane == 0");
+      // carries
+      for (size_t m = 0; m < reds.size(); ++m) {
+        const auto& rap = g.raps[reds[m]];
+        const auto& k = rs.kernels[rap.kernel];
+        const int ot = rap.out_terms[0];
+        int carry = -1;
+        for (size_t i = 0; i < rap.in_terms.size(); ++i) {
+          const auto& ti = g.terms[rap.in_terms[i]];
+          const auto& to = g.terms[ot];
+          if (ti.ident == to.ident && ti.dims == to.dims && !(ti == to)) carry = static_cast<int>(i);
+        }
+        if (carry < 0) return fail("associative kernel '" + k.name + "' has no carry input");
+        const int ct = rap.in_terms[carry];
+        const int pr = g.producer[ct];
+        if (pr >= 0 && g.raps[pr].kind == lf::RapKind::kernel && nest_of(pr) != nv && !done[ct]) {
+          src << "    const T v" << ct << " = " << mat_index(ct) << ";\n";
+          done[ct] = 1;
+        }
+        src << "    T acc" << m << " = v" << ct << ";\n";
+      }
+      // element loop
+      src << "    for (long long rb = 0; rb < " << rcount << "LL; rb += 32) {\n";
+      src << "      const bool ok = rb + lane < " << rcount << "LL;\n";
+      src << "      long long rr = ok ? rb + lane : " << (rcount - 1) << "LL;\n";
+      for (int d = nd - 1; d >= 0; --d)
+        if (R.count(d)) src << "      const int x" << d << " = (int)(rr % " << N[d] << "); rr /= " << N[d] << ";\n";
+      std::ostringstream el;
+      for (int r : topo)
+        if (in_nest[r] && cls[r] == 1) emit_rap(r, nv, el, "      ", okk, "ok");
+      src << el.str();
+      // element operands of each reduction into shared memory, then the ordered accumulation
+      std::vector<std::vector<int>> elem_in(reds.size());
+      for (size_t m = 0; m < reds.size(); ++m) {
+        const auto& rap = g.raps[reds[m]];
+        const auto& k = rs.kernels[rap.kernel];
+        if (k.inputs.size() > 2) return fail("associative kernel '" + k.name + "' with more than one element input");
+        for (size_t i = 0; i < rap.in_terms.size(); ++i) {
+          const int t = rap.in_terms[i];
+          const auto& to = g.terms[rap.out_terms[0]];
+          const auto& ti = g.terms[t];
+          if (ti.ident == to.ident && ti.dims == to.dims && !(ti == to)) continue;
+          const int pr = g.producer[t];
+          if (pr >= 0 && g.raps[pr].kind == lf::RapKind::kernel && nest_of(pr) != nv && !done[t]) {
+            src << "      const T v" << t << " = " << mat_index(t) << ";\n";
+            done[t] = 1;
+          }
+          src << "      lf_red[warp][" << m << "][lane] = v" << t << ";\n";
+          elem_in[m].push_back(static_cast<int>(i));
+        }
+      }
+      src << "      __syncwarp();\n";
+      src << "      const int cnt = (int)min(32LL, " << rcount << "LL - rb);\n";
+      src << "      for (int e = 0; e < cnt; ++e) {\n";
+      for (size_t m = 0; m < reds.size(); ++m) {
+        const auto& rap = g.raps[reds[m]];
+        const auto& k = rs.kernels[rap.kernel];
+        std::string e2;
+        auto e = lf::parse_expr(k.bodies.at(k.outputs[0].first), e2);
+        if (!e) return fail("kernel '" + k.name + "': " + e2);
+        std::map<std::string, std::string> pv;
+        for (size_t i = 0; i < k.inputs.size(); ++i) {
+          const bool is_elem = std::find(elem_in[m].begin(), elem_in[m].end(), (int)i) != elem_in[m].end();
+          pv[k.inputs[i].first] = is_elem ? "lf_red[warp][" + std::to_string(m) + "][e]" : "acc" + std::to_string(m);
+        }
+        src << "        acc" << m << " = " << lf::emit_c(*e, T, [&](const std::string& n) { return pv.at(n); }) << ";\n";
+      }
+      src << "      }\n";
+      src << "      __syncwarp();\n";
+      src << "    }\n";
+      // reduction outputs, post raps, P-level stores (lane 0 writes)
+      for (size_t m = 0; m < reds.size(); ++m) {
+        const int ot = g.raps[reds[m]].out_terms[0];
+        src << "    const T v" << ot << " = acc" << m << ";\n";
+        done[ot] = 1;
+        if (term_mat[ot]) src << "    if (lane == 0) " << mat_index(ot) << " = v" << ot << ";\n";
+      }
+      for (int r : topo)
+        if (in_nest[r] && cls[r] == 3) emit_rap(r, nv, src, "    ", okk, "lane == 0");
+      src << "  }\n}\n";
+    }
+    if (!okk) return false;
+    out.nest_kernels.push_back(nl);
+  }
+  return true;
+}
+
 }  // namespace
 
 bool jit_generate(const lf::Plan& P, JitProgram& out) {
+  bool multi = !P.one_nest;
+  for (const auto& k : P.rs.kernels) multi |= k.associative;
+  if (multi) {
+    std::ostringstream src;
+    std::string err;
+    if (!emit_nests(P, out, src, err)) {
+      out.error = err;
+      return false;
+    }
+    // ghost refill of iterated goals: the same kernel as the single-nest path
+    Ctx C(P);
+    C.nd = out.nd;
+    C.T = out.type;
+    C.N.resize(C.nd);
+    for (int d = 0; d < C.nd; ++d) C.N[d] = P.rs.ranges[d].trips();
+    if (!emit_fill(C, out, src)) {
+      out.error = C.error;
+      return false;
+    }
+    out.source = src.str();
+    out.march = false;
+    return true;
+  }
   Ctx C(P);
   if (!analyse(C)) {
     out.error = C.error;

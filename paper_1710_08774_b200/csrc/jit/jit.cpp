@@ -135,7 +135,75 @@ std::shared_ptr<JitKernel> JitKernel::build(const lf::Plan& plan, std::string& w
 }
 
 JitKernel::~JitKernel() {
+  for (void* p : mats_) cudaFree(p);
   if (module_ && drv().ok) drv().unload(static_cast<CUmodule>(module_));
+}
+
+// multi-nest plans: the nests in dataflow order each step; whole domain only
+int JitKernel::run_nests(const ExecArgs& a, std::string& err) {
+  const auto& rs = a.plan->rs;
+  const auto& T = a.plan->terminals;
+  if (a.slab && (a.slab->lo != 0 || a.slab->hi != a.slab->global || a.slab->part_hi > a.slab->part_lo)) {
+    err = "multi-nest plans (reductions) run on the whole domain only, not on slabs";
+    return LF_ERR_UNSUPPORTED;
+  }
+  if (mats_.empty())
+    for (size_t b : prog_.mat_bytes) {
+      void* p = nullptr;
+      cudaError_t e = cudaMalloc(&p, std::max<size_t>(b, 16));
+      if (e != cudaSuccess) {
+        err = std::string("cudaMalloc(materialised variable): ") + cudaGetErrorString(e);
+        return LF_ERR_CUDA;
+      }
+      mats_.push_back(p);
+    }
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  Args args;
+  std::memset(&args, 0, sizeof args);
+  const long rows = rs.ranges[0].trips();
+  args.n0 = rows;
+  args.row_lo = 0;
+  args.row_hi = static_cast<int>(rows);
+  args.top = args.bottom = 1;
+  std::vector<int> iter_axiom(T.size(), -1);
+  for (const auto& [gname, aname] : rs.iterate) {
+    int gi = -1, ai = -1;
+    for (size_t i = 0; i < T.size(); ++i) {
+      if (T[i].is_goal && T[i].name == gname) gi = static_cast<int>(i);
+      if (!T[i].is_goal && T[i].name == aname) ai = static_cast<int>(i);
+    }
+    if (gi >= 0 && ai >= 0) iter_axiom[gi] = ai;
+  }
+  int scratch_idx = 0;
+  std::vector<void*> scratch(T.size(), nullptr);
+  for (size_t i = 0; i < T.size(); ++i)
+    if (iter_axiom[i] >= 0 && a.steps > 1) scratch[i] = a.scratch[scratch_idx++];
+  std::vector<void*> cur(a.terms, a.terms + T.size());
+  for (int s = 0; s < a.steps; ++s) {
+    const bool to_goal = ((a.steps - 1 - s) % 2) == 0;
+    std::vector<void*> bufs = cur;
+    for (size_t i = 0; i < T.size(); ++i)
+      if (T[i].is_goal) bufs[i] = (to_goal || iter_axiom[i] < 0) ? a.terms[i] : scratch[i];
+    for (size_t i = 0; i < T.size(); ++i) args.t[i] = bufs[i];
+    for (size_t m = 0; m < mats_.size(); ++m) args.t[T.size() + m] = mats_[m];
+    for (size_t k = 0; k < prog_.nest_kernels.size(); ++k) {
+      const auto& nk = prog_.nest_kernels[k];
+      const long long per_cta = nk.reduction ? 8 : 256;
+      const long long want = (nk.units + per_cta - 1) / per_cta;
+      const unsigned ctas = static_cast<unsigned>(std::max<long long>(1, std::min<long long>(want, 32LL * sms)));
+      int st = launch(nest_fns_[k], dim3(ctas), dim3(256), 0, a.stream, &args, err);
+      if (st != LF_OK) return st;
+    }
+    if (fill_ && prog_.has_fill) {
+      int st = launch(fill_, dim3(592), dim3(256), 0, a.stream, &args, err);
+      if (st != LF_OK) return st;
+    }
+    for (size_t i = 0; i < T.size(); ++i)
+      if (iter_axiom[i] >= 0) cur[iter_axiom[i]] = bufs[i];
+  }
+  return LF_OK;
 }
 
 int JitKernel::launch(void* fn, dim3 grid, dim3 block, size_t smem, cudaStream_t st, void* args, std::string& err) {
@@ -165,15 +233,26 @@ int JitKernel::run(const ExecArgs& a, std::string& err) {
     }
     module_ = m;
     CUfunction f;
-    if (d.get(&f, m, "lf_jit_step") != CUDA_SUCCESS) {
-      err = "generated kernel missing";
-      return LF_ERR_INTERNAL;
-    }
-    step_ = f;
     if (d.get(&f, m, "lf_jit_fill") == CUDA_SUCCESS) fill_ = f;
-    d.attr(static_cast<CUfunction>(step_), CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES,
-           static_cast<int>(prog_.smem_bytes));
+    if (!prog_.nest_kernels.empty()) {
+      for (const auto& nk : prog_.nest_kernels) {
+        if (d.get(&f, m, nk.fn.c_str()) != CUDA_SUCCESS) {
+          err = "generated kernel " + nk.fn + " missing";
+          return LF_ERR_INTERNAL;
+        }
+        nest_fns_.push_back(f);
+      }
+    } else {
+      if (d.get(&f, m, "lf_jit_step") != CUDA_SUCCESS) {
+        err = "generated kernel missing";
+        return LF_ERR_INTERNAL;
+      }
+      step_ = f;
+      d.attr(static_cast<CUfunction>(step_), CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES,
+             static_cast<int>(prog_.smem_bytes));
+    }
   }
+  if (!prog_.nest_kernels.empty()) return run_nests(a, err);
   const auto& rs = a.plan->rs;
   const auto& T = a.plan->terminals;
   const RowPart rp = row_part(a, (int)rs.ranges[0].trips());

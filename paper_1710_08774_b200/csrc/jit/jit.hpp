@@ -13,6 +13,12 @@
 
 namespace lfx {
 
+struct NestLaunch {
+  std::string fn;          // kernel name
+  bool reduction = false;  // warp per parallel cell (true) or thread per cell
+  long long units = 0;     // parallel cells
+};
+
 struct JitProgram {
   std::string source;
   std::string type;  // "double" / "float"
@@ -27,6 +33,9 @@ struct JitProgram {
   long inner_tiles = 1;     // CTAs across the inner dimensions
   int ctas_per_sm = 1;      // resident CTAs per SM the shared-memory footprint allows
   int chunk = 64;           // rows per chunk of the persistent work order
+  // multi-nest plans: one kernel per nest, materialised cross-nest variables
+  std::vector<NestLaunch> nest_kernels;
+  std::vector<size_t> mat_bytes;
   std::string error;  // why the chain is not supported
 };
 
@@ -46,8 +55,11 @@ class JitKernel {
   void* step_ = nullptr;    // CUfunction
   void* fill_ = nullptr;
   int resident_ = 0;  // CTAs resident at once (occupancy x SMs)
+  std::vector<void*> nest_fns_;
+  std::vector<void*> mats_;  // device buffers of materialised variables
   std::vector<char> cubin_;
   int launch(void* fn, dim3 grid, dim3 block, size_t smem, cudaStream_t st, void* args, std::string& err);
+  int run_nests(const ExecArgs& a, std::string& err);
 };
 
 }  // namespace lfx

@@ -643,7 +643,10 @@ std::string Plan::report_json() const {
     const auto& cg = groups[gi];
     std::string nm = cg.kind == RapKind::kernel ? rs.kernels[cg.kernel].name
                                                 : (cg.kind == RapKind::load ? "load " : "store ") + cg.external;
-    os << (gi ? "," : "") << "{\"name\":" << json_str(nm) << ",\"members\":" << cg.members.size() << ",\"shift\":[";
+    os << (gi ? "," : "") << "{\"name\":" << json_str(nm) << ",\"members\":" << cg.members.size()
+       << ",\"nest\":" << (gi < vertex_of_group.size() ? vertex_of_group[gi] : -1) << ",\"space\":[";
+    for (size_t k = 0; k < cg.space.size(); ++k) os << (k ? "," : "") << cg.space[k];
+    os << "],\"shift\":[";
     for (size_t d = 0; d < nd; ++d) os << (d ? "," : "") << shifts[gi][d];
     os << "]}";
   }

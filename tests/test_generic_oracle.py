@@ -69,3 +69,42 @@ def test_jit_plans_for_body_chains_and_reports_source():
     # a chain without bodies and without a matching built-in stays unsupported
     q = lf.Plan.from_file(SPECS / "cosmo.lf")
     assert q.executor == ""
+
+
+def normalization_reference(q, z):
+    fl = (q[:, 1:] - q[:, :-1]) * (q[:, 1:] - q[:, :-1])
+    acc = z.copy()
+    for i in range(fl.shape[1]):  # run_naive's sequential sweep of the associative group
+        acc = acc + fl[:, i]
+    return fl / np.sqrt(acc)[:, None]
+
+
+def colsum_reference(u, z, k):
+    L = u[1:-1, :-2] + u[1:-1, 2:] + u[:-2, 1:-1] + u[2:, 1:-1] - 4.0 * u[1:-1, 1:-1]
+    acc = z.copy()
+    for j in range(L.shape[0]):
+        acc = np.where(acc > np.abs(L[j]), acc, np.abs(L[j]))
+    cs = acc + 1.0
+    return u[1:-1, 1:-1] + k * L / cs[None, :], cs
+
+
+def test_generic_reductions_match_numpy():
+    """Associative kernels reduce sequentially in loop order (inner dim and
+    outer dim), then broadcast across a split."""
+    need_ref()
+    rng = np.random.default_rng(3)
+    q, z = rng.random((37, 151)), rng.random(37) * 0.1
+    got = generic.run_naive(SPECS / "normalization_body.lf", {"g_q": q, "g_zero": z})["g_out"]
+    assert np.array_equal(got, normalization_reference(q, z))
+    u = rng.random((47, 72))
+    got = generic.run_naive(SPECS / "colsum_body.lf", {"g_u": u, "g_z": np.zeros(70), "g_k": np.array([0.3])})
+    out, cs = colsum_reference(u, np.zeros(70), np.float64(0.3))
+    assert np.array_equal(got["g_out"], out) and np.array_equal(got["g_cs"], cs)
+
+
+def test_multi_nest_body_chains_plan_to_the_nest_executor():
+    for s, nests in [("normalization_body", 2), ("colsum_body", 3)]:
+        p = lf.Plan.from_file(SPECS / f"{s}.lf")
+        assert p.report()["nests"] == nests and p.report()["splits"] == 1
+        assert p.executor == "jit_nests_fused", s
+        assert "lf_nest0" in p.source and "lf_red" in p.source

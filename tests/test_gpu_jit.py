@@ -33,6 +33,11 @@ CASES = {
     "box_body": lambda: {"g_img": inputs.box_input(33, 70, seed=7)},
     "multi_body": lambda: {"g_x": np.random.default_rng(1).random((21, 52)), "g_scale": np.array([0.75])},
     "laplace3_body": lambda: {"g_x": np.random.default_rng(2).random(1002)},
+    # multi-nest plans: reductions (inner and outer dim) and broadcast splits
+    "normalization_body": lambda: {"g_q": np.random.default_rng(3).random((37, 151)),
+                                   "g_zero": np.random.default_rng(4).random(37) * 0.1},
+    "colsum_body": lambda: {"g_u": np.random.default_rng(5).random((47, 72)), "g_z": np.zeros(70),
+                            "g_k": np.array([0.3])},
 }
 
 
