@@ -97,6 +97,13 @@ WORKLOADS = {
                        gen=_biharm_inputs, slab=_biharm_slab, dtype="f64", halo=(2, 2, False)),
     "box_jit": dict(config_index=3, spec="examples/box_body", sizes=(16384, 16384), chain_steps=1,
                     gen=_box_inputs, slab=_box_slab, dtype="f32", halo=None),
+    # in place (config.aliases, one buffer for u and unew): half the footprint
+    "heat3d_jit_inplace": dict(config_index=1, spec="examples/heat3d_inplace", sizes=(512, 512, 512),
+                               chain_steps=50, gen=_heat3d_inputs, slab=None, dtype="f64", halo=(1, 1, True),
+                               inplace=True),
+    "biharm_jit_inplace": dict(config_index=0, spec="examples/biharm_inplace", sizes=(4096, 4096),
+                               chain_steps=100, gen=_biharm_inputs, slab=None, dtype="f64", halo=(2, 2, False),
+                               inplace=True),
 }
 
 
@@ -197,7 +204,7 @@ def cpu_runner(name, w):
     """The HFAV-style fused CPU schedule (oracle/) on one bounded unit of the
     workload with all host threads: returns (run, cell-updates per run, text)."""
     import oracle
-    name = name.replace("_jit", "")
+    name = name.replace("_jit", "").replace("_inplace", "")
     threads = oracle.max_threads()
     sizes = w["sizes"]
     if name == "heat3d":
@@ -317,12 +324,17 @@ def main():
     if world == 1:
         host = w["gen"](w["sizes"])
         d_ax = [torch.from_numpy(h).to(dev) for h in host[:nax]]
-        d_goal = [torch.empty(t.extent, dtype=tdt(t), device=dev) for t in plan.goals]
+        if w.get("inplace"):  # goal k shares axiom k's buffer
+            d_goal = [d_ax[k] for k in range(len(plan.goals))]
+        else:
+            d_goal = [torch.empty(t.extent, dtype=tdt(t), device=dev) for t in plan.goals]
         bufs = d_ax + d_goal
 
         def one_step():
             plan.run(bufs, steps=w["chain_steps"], stream=stream)
     else:
+        if w.get("inplace"):
+            raise SystemExit("in-place workloads run on one GPU (slab runs need distinct buffers)")
         # outer-dimension slabs, faces exchanged by NCCL every time step
         n0 = w["sizes"][0]
         lo, hi = slabs.slab_range(n0, rank, world)
@@ -412,6 +424,7 @@ def main():
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": w["dtype"], "data": "synthetic (seeded splitmix64, BASELINE.json shapes)",
         "config": {"workload": workload, "executor": plan.executor, "l2": "inputs larger than L2 (126 MB)",
+                   "in_place": bool(w.get("inplace")),
                    "parallelism": f"slab{world}" if world > 1 else "single-gpu"},
         "roofline": roofline, "gpu_launches": launches * args.steps, "clocks": clk.summary(),
     }
@@ -425,7 +438,10 @@ def main():
         del d_ax, d_goal, bufs  # lf_run_host owns its own device buffers
         torch.cuda.empty_cache()
         pinned = [torch.from_numpy(h).pin_memory() for h in host[:nax]]
-        outs = [torch.empty(t.extent, dtype=tdt(t)).pin_memory() for t in plan.goals]
+        if w.get("inplace"):
+            outs = [pinned[k] for k in range(len(plan.goals))]
+        else:
+            outs = [torch.empty(t.extent, dtype=tdt(t)).pin_memory() for t in plan.goals]
         hb = [p.numpy() for p in pinned] + [o.numpy() for o in outs]
         for _ in range(max(1, args.warmup)):
             plan.run_host(hb, steps=w["chain_steps"])

@@ -267,6 +267,27 @@ int main(int argc, char** argv) {
       os << "]}";
       first = false;
     }
+    os << "],\"alias\":[";
+    for (size_t k = 0; k < sp.alias.entries.size(); ++k) {
+      const auto& e = sp.alias.entries[k];
+      const auto& wg = grouping.groups[e.writer_group];
+      std::string wn = wg.kind == loomfuse::RapKind::kernel ? rs.kernels[wg.kernel].name
+                       : wg.kind == loomfuse::RapKind::load ? "load " + wg.external
+                                                            : "store " + wg.external;
+      os << (k ? "," : "") << "{\"input\":" << q(e.input_external) << ",\"output\":" << q(e.output_external)
+         << ",\"var\":" << q(sp.vars.vars[e.var].name) << ",\"writer\":" << q(wn) << ",\"writer_shift\":[";
+      for (size_t d = 0; d < e.writer_shift.size(); ++d) os << (d ? "," : "") << e.writer_shift[d];
+      os << "],\"offsets\":[";
+      for (size_t o = 0; o < e.offsets.size(); ++o) {
+        os << (o ? "," : "") << "[";
+        for (size_t d = 0; d < e.offsets[o].size(); ++d) os << (d ? "," : "") << e.offsets[o][d];
+        os << "]";
+      }
+      const auto& sh = sp.shadows[k];
+      os << "],\"shadow\":{\"scheme\":" << q(scheme(sh.scheme)) << ",\"spans\":[";
+      for (size_t d = 0; d < sh.dims.size(); ++d) os << (d ? "," : "") << sh.dims[d].span;
+      os << "]}}";
+    }
     os << "]}";
     std::cout << os.str() << "\n";
   } catch (const std::exception& e) {

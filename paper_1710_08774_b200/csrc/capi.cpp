@@ -262,6 +262,15 @@ const char* lf_plan_source(const lf_plan* plan) {
   return plan && plan->jit ? plan->jit->program().source.c_str() : "";
 }
 
+// an axiom buffer passed again as a goal (in-place run)
+static bool shares_buffer(const lf_plan* plan, void* const* terms) {
+  const auto& T = plan->plan.terminals;
+  for (size_t i = 0; i < T.size(); ++i)
+    for (size_t j = 0; j < T.size(); ++j)
+      if (!T[i].is_goal && T[j].is_goal && terms[i] && terms[i] == terms[j]) return true;
+  return false;
+}
+
 int lf_run(const lf_plan* cplan, void* const* terms, int nterm, int steps, void* cuda_stream) {
   try {
     g_err.clear();
@@ -270,8 +279,13 @@ int lf_run(const lf_plan* cplan, void* const* terms, int nterm, int steps, void*
     lf_plan* plan = const_cast<lf_plan*>(cplan);
     std::lock_guard<std::mutex> lk(plan->mu);
     std::string err;
+    const bool inplace = shares_buffer(plan, terms);
+    if (inplace && plan->exec)
+      return fail(LF_ERR_UNSUPPORTED, std::string(plan->exec->name) +
+                                          " ping-pongs between distinct buffers; in-place runs (config.aliases) "
+                                          "use the generic executor");
     std::vector<void*> scratch;
-    if (steps > 1) {
+    if (steps > 1 && !inplace) {
       if ((st = ensure_scratch(plan, err)) != LF_OK) return fail(st, err);
       scratch = scratch_list(plan);
     }
@@ -302,15 +316,25 @@ int lf_run_host(const lf_plan* cplan, void* const* terms, int nterm, int steps) 
       cudaError_t e = cudaStreamCreateWithFlags(&plan->stream, cudaStreamNonBlocking);
       if (e != cudaSuccess) return fail(lfx::cuda_status(e, "cudaStreamCreate", err), err);
     }
-    if (plan->dev.size() != T.size()) {
-      plan->dev.assign(T.size(), nullptr);
-      for (size_t i = 0; i < T.size(); ++i) {
-        cudaError_t e = cudaMalloc(&plan->dev[i], terminal_bytes(T[i]));
-        if (e != cudaSuccess) return fail(lfx::cuda_status(e, "cudaMalloc(terminal)", err), err);
-      }
+    // a host buffer passed as an aliased axiom and goal stays one device buffer
+    // when the executor can run the pair in place (half the device footprint)
+    std::vector<int> share(T.size(), -1);
+    if (plan->jit)
+      for (const auto& q : plan->jit->program().inplace)
+        if (terms[q.ai] && terms[q.ai] == terms[q.gi]) share[q.gi] = q.ai;
+    bool inplace = false;
+    for (int s2 : share) inplace |= s2 >= 0;
+    if (plan->dev.size() != T.size()) plan->dev.assign(T.size(), nullptr);
+    for (size_t i = 0; i < T.size(); ++i) {
+      if (share[i] >= 0 || plan->dev[i]) continue;
+      cudaError_t e = cudaMalloc(&plan->dev[i], terminal_bytes(T[i]));
+      if (e != cudaSuccess) return fail(lfx::cuda_status(e, "cudaMalloc(terminal)", err), err);
     }
+    std::vector<void*> dterms(plan->dev);
+    for (size_t i = 0; i < T.size(); ++i)
+      if (share[i] >= 0) dterms[i] = plan->dev[share[i]];
     std::vector<void*> scratch;
-    if (steps > 1) {
+    if (steps > 1 && !inplace) {
       if ((st = ensure_scratch(plan, err)) != LF_OK) return fail(st, err);
       scratch = scratch_list(plan);
     }
@@ -322,7 +346,7 @@ int lf_run_host(const lf_plan* cplan, void* const* terms, int nterm, int steps) 
     }
     lfx::ExecArgs a;
     a.plan = &plan->plan;
-    a.terms = plan->dev.data();
+    a.terms = dterms.data();
     a.steps = steps;
     a.stream = plan->stream;
     a.scratch = scratch.data();
@@ -330,7 +354,7 @@ int lf_run_host(const lf_plan* cplan, void* const* terms, int nterm, int steps) 
     if (st != LF_OK) return fail(st, err);
     for (size_t i = 0; i < T.size(); ++i) {
       if (!T[i].is_goal) continue;
-      cudaError_t e = cudaMemcpyAsync(terms[i], plan->dev[i], terminal_bytes(T[i]), cudaMemcpyDeviceToHost,
+      cudaError_t e = cudaMemcpyAsync(terms[i], dterms[i], terminal_bytes(T[i]), cudaMemcpyDeviceToHost,
                                       plan->stream);
       if (e != cudaSuccess) return fail(lfx::cuda_status(e, "cudaMemcpyAsync(D2H)", err), err);
     }
@@ -352,6 +376,8 @@ int lf_run_slab(const lf_plan* cplan, void* const* terms, int nterm, const lf_sl
     if (slab->part_lo < 0 || slab->part_hi < slab->part_lo || slab->part_hi > slab->hi - slab->lo)
       return fail(LF_ERR_SPEC, "invalid slab part");
     if (slab->part_hi == slab->part_lo && slab->part_lo != 0) return LF_OK;  // empty part
+    if (shares_buffer(cplan, terms))
+      return fail(LF_ERR_UNSUPPORTED, "slab runs need distinct axiom and goal buffers (in-place runs cover the whole domain)");
     lfx::ExecArgs a;
     a.plan = &cplan->plan;
     a.terms = terms;

@@ -302,7 +302,7 @@ void emit_prelude(Ctx& C, std::ostream& src, int threads, int min_blocks = 1) {
   src << "__device__ __forceinline__ T lf_min(T a, T b) { return a < b ? a : b; }\n";
   src << "__device__ __forceinline__ T lf_max(T a, T b) { return a > b ? a : b; }\n";
   // must match lfx::Args in jit.cpp (passed by value)
-  src << "struct LfArgs { void* t[32]; long long n0; int row_lo, row_hi, top, bottom, chunk, pad; };\n";
+  src << "struct LfArgs { void* t[32]; long long n0; int row_lo, row_hi, top, bottom, chunk, inplace; };\n";
   src << "extern \"C\" __global__ void __launch_bounds__(" << threads << ", " << min_blocks << ") lf_jit_step(const LfArgs a) {\n";
   src << "  extern __shared__ __align__(16) unsigned char lf_smem[];\n";
   src << "  const long long N0 = a.n0;\n";
@@ -463,20 +463,93 @@ bool emit_march(Ctx& C, JitProgram& out, std::ostream& src) {
   // so neighbouring tiles run at the same time and share halos in L2
   for (size_t v = 0; v < nv; ++v)
     if (staged[v] >= 0) src << "  const unsigned sb" << v << " = (unsigned)__cvta_generic_to_shared(v" << v << ");\n";
+  // in-place (config.aliases, caller passes one buffer): whole (chunk, tile)
+  // units so that every cross-unit read hits a band captured before the step
+  struct IP {
+    size_t v;
+    int ai, gi, slot;
+  };
+  std::vector<IP> ips;
+  out.inplace.clear();
+  out.inplace_error.clear();
+  const int nterm = static_cast<int>(C.P.terminals.size());
+  for (const auto& [in_ext, out_ext] : C.P.rs.aliases) {
+    int ai = -1, gi = -1;
+    for (int i = 0; i < nterm; ++i) {
+      if (!C.P.terminals[i].is_goal && C.P.terminals[i].name == in_ext) ai = i;
+      if (C.P.terminals[i].is_goal && C.P.terminals[i].name == out_ext) gi = i;
+    }
+    if (ai < 0 || gi < 0) continue;
+    const int v = C.P.terminals[ai].var;
+    if (v < 0 || staged[v] < 0) {
+      out.inplace_error = "aliased input '" + in_ext + "' is not a streamed full-rank axiom";
+      continue;
+    }
+    if (C.P.terminals[ai].extent != C.P.terminals[gi].extent || C.P.terminals[ai].base != C.P.terminals[gi].base) {
+      out.inplace_error = "aliased buffers '" + in_ext + "' and '" + out_ext + "' have different extents";
+      continue;
+    }
+    IP ip{static_cast<size_t>(v), ai, gi, nterm + 3 * static_cast<int>(ips.size())};
+    if (ip.slot + 3 > 32) {
+      out.inplace_error = "too many aliased buffers";
+      continue;
+    }
+    ips.push_back(ip);
+    const auto& t = C.P.terminals[ai];
+    JitProgram::Inplace q;
+    q.ai = ai;
+    q.gi = gi;
+    q.bh = C.vmax[v][0] - C.vmin[v][0];
+    q.bw1 = nd > 1 ? C.vmax[v][1] - C.vmin[v][1] : 0;
+    q.bw2 = nd > 2 ? C.vmax[v][2] - C.vmin[v][2] : 0;
+    q.e0 = t.extent[0];
+    q.e1 = nd > 1 ? t.extent[1] : 1;
+    q.e2 = nd > 2 ? t.extent[2] : 1;
+    q.t1 = nd > 1 ? tile[1] : 1;
+    q.t2 = nd > 2 ? tile[2] : 1;
+    q.n1 = nd > 1 ? C.N[1] : 1;
+    q.n2 = nd > 2 ? C.N[2] : 1;
+    out.inplace.push_back(q);
+  }
+  auto ip_of = [&](size_t v) -> const IP* {
+    for (const auto& ip : ips)
+      if (ip.v == v) return &ip;
+    return nullptr;
+  };
+  for (const auto& ip : ips)
+    src << "  const T* __restrict__ rb" << ip.slot << " = reinterpret_cast<const T*>(a.t[" << ip.slot
+        << "]);  // in-place bands of '" << C.P.vars[ip.v].name << "'\n"
+        << "  const T* __restrict__ cb" << ip.slot << "_1 = reinterpret_cast<const T*>(a.t[" << ip.slot + 1 << "]);\n"
+        << "  const T* __restrict__ cb" << ip.slot << "_2 = reinterpret_cast<const T*>(a.t[" << ip.slot + 2 << "]);\n";
   src << "  const int rows = a.row_hi - a.row_lo;\n";
   src << "  const long long total = (long long)rows * " << out.inner_tiles << ";\n";
   src << "  const long long per = (total + gridDim.x - 1) / gridDim.x;\n";
   src << "  long long s = (long long)blockIdx.x * per;\n";
   src << "  const long long s_end = min(total, s + per);\n";
-  src << "  while (s < s_end) {\n";
-  src << "  const long long cs = (long long)a.chunk * " << out.inner_tiles << ";\n";
-  src << "  const int ci = (int)(s / cs);\n";
-  src << "  const int rc = min(a.chunk, rows - ci * a.chunk);\n";
-  src << "  const long long off = s - ci * cs;\n";
-  src << "  int bt = (int)(off / rc);\n";
-  src << "  const int r0 = a.row_lo + ci * a.chunk + (int)(off % rc);\n";
-  src << "  const int r1 = (int)min((long long)(a.row_lo + ci * a.chunk + rc), r0 + (s_end - s));\n";
-  src << "  s += r1 - r0;\n";
+  src << "  const long long units = a.inplace ? (long long)((rows + a.chunk - 1) / a.chunk) * " << out.inner_tiles
+      << " : 0;\n";
+  src << "  long long u = blockIdx.x;\n";
+  src << "  for (;;) {\n";
+  src << "  int bt, r0_, r1_;\n";
+  src << "  if (a.inplace) {\n";
+  src << "    if (u >= units) break;\n";
+  src << "    const int ci = (int)(u / " << out.inner_tiles << ");\n";
+  src << "    bt = (int)(u % " << out.inner_tiles << ");\n";
+  src << "    r0_ = a.row_lo + ci * a.chunk;\n";
+  src << "    r1_ = min(r0_ + a.chunk, a.row_hi);\n";
+  src << "    u += gridDim.x;\n";
+  src << "  } else {\n";
+  src << "    if (s >= s_end) break;\n";
+  src << "    const long long cs = (long long)a.chunk * " << out.inner_tiles << ";\n";
+  src << "    const int ci = (int)(s / cs);\n";
+  src << "    const int rc = min(a.chunk, rows - ci * a.chunk);\n";
+  src << "    const long long off = s - ci * cs;\n";
+  src << "    bt = (int)(off / rc);\n";
+  src << "    r0_ = a.row_lo + ci * a.chunk + (int)(off % rc);\n";
+  src << "    r1_ = (int)min((long long)(a.row_lo + ci * a.chunk + rc), r0_ + (s_end - s));\n";
+  src << "    s += r1_ - r0_;\n";
+  src << "  }\n";
+  src << "  const int r0 = r0_, r1 = r1_;\n";
   for (int d = nd - 1; d >= 1; --d) {
     const long nt = (C.N[d] + tile[d] - 1) / tile[d];
     src << "  const int o" << d << " = (bt % " << nt << ") * " << tile[d] << "; bt /= " << nt << ";\n";
@@ -510,9 +583,47 @@ bool emit_march(Ctx& C, JitProgram& out, std::ostream& src) {
     src << I << "          const int x1 = o1 + c1;\n";
     std::vector<std::string> pos = {"y"};
     for (int d = 1; d < nd; ++d) pos.push_back("x" + std::to_string(d));
+    src << I << "          const T* sp = t" << staged[v] << " + " << C.tidx(staged[v], pos, C.extra_of(static_cast<int>(v)))
+        << ";\n";
+    if (const IP* ip = ip_of(v)) {
+      // in-place: a cell another unit writes during this step comes from its band
+      const auto& t = C.P.terminals[ip->ai];
+      const auto ex = C.extra_of(static_cast<int>(v));
+      std::vector<long> so(nd);  // storage coordinate = logical + so
+      for (int d = 0; d < nd; ++d) so[d] = ex[d] - t.base[d];
+      const long E0 = t.extent[0], E1 = nd > 1 ? t.extent[1] : 1, E2 = nd > 2 ? t.extent[2] : 1;
+      const long BH = C.vmax[v][0] - C.vmin[v][0];
+      const std::string sy = "(long long)(y" + plus(so[0]) + ")", sx1 = "(long long)(x1" + plus(so[1]) + ")",
+                        sx2 = nd > 2 ? "(long long)(x2" + plus(so[2]) + ")" : "0LL";
+      const std::string sl = std::to_string(ip->slot);
+      src << I << "          if (a.inplace) {\n";
+      src << I << "            if (y < r0 || y >= r1) {\n";
+      src << I << "              if (y >= 0 && y < N0) {\n";
+      src << I << "                const int b = y < r0 ? r0 : r1;\n";
+      src << I << "                sp = rb" << sl << " + ((long long)(b / a.chunk - 1) * " << BH << " + (y - b" << plus(-C.vmin[v][0])
+          << ")) * " << (E1 * E2) << "LL + " << sx1 << " * " << E2 << "LL + " << sx2 << ";\n";
+      src << I << "              }\n";
+      src << I << "            } else if (x1 < o1 || x1 >= o1 + " << tile[1] << ") {\n";
+      src << I << "              if (x1 >= 0 && x1 < N1) {\n";
+      src << I << "                const int e = x1 < o1 ? o1 : o1 + " << tile[1] << ";\n";
+      src << I << "                sp = cb" << sl << "_1 + (((long long)(e / " << tile[1] << " - 1) * "
+          << (C.vmax[v][1] - C.vmin[v][1]) << " + (x1 - e" << plus(-C.vmin[v][1]) << ")) * " << E0 << "LL + " << sy
+          << ") * " << E2 << "LL + " << sx2 << ";\n";
+      src << I << "              }\n";
+      if (nd == 3) {
+        src << I << "            } else if (x2 < o2 || x2 >= o2 + " << tile[2] << ") {\n";
+        src << I << "              if (x2 >= 0 && x2 < N2) {\n";
+        src << I << "                const int e = x2 < o2 ? o2 : o2 + " << tile[2] << ";\n";
+        src << I << "                sp = cb" << sl << "_2 + (((long long)(e / " << tile[2] << " - 1) * "
+            << (C.vmax[v][2] - C.vmin[v][2]) << " + (x2 - e" << plus(-C.vmin[v][2]) << ")) * " << E0 << "LL + " << sy
+            << ") * " << E1 << "LL + " << sx1 << ";\n";
+        src << I << "              }\n";
+      }
+      src << I << "            }\n";
+      src << I << "          }\n";
+    }
     src << I << "          asm volatile(\"cp.async.ca.shared.global [%0], [%1], " << eb << ";\" :: \"r\"(dst + ("
-        << inplane(v, std::vector<int>(nd, 0)) << ") * " << eb << "), \"l\"(t" << staged[v] << " + "
-        << C.tidx(staged[v], pos, C.extra_of(static_cast<int>(v))) << ") : \"memory\");\n";
+        << inplane(v, std::vector<int>(nd, 0)) << ") * " << eb << "), \"l\"(sp) : \"memory\");\n";
     src << I << "        }\n" << I << "      }\n" << I << "    }\n" << I << "  }\n" << I << "}\n";
   };
   for (int p = 0; p < PD; ++p) {
@@ -628,6 +739,54 @@ bool emit_march(Ctx& C, JitProgram& out, std::ostream& src) {
   src << "  __syncthreads();\n";
   src << "  }\n";
   src << "}\n";
+  // ---- in-place: capture the bands other units read before this step writes
+  if (!ips.empty()) {
+    src << "extern \"C\" __global__ void lf_jit_capture(const LfArgs a) {\n";
+    src << "  const long long N0 = a.n0;\n";
+    src << "  const int nch = (int)((N0 + a.chunk - 1) / a.chunk);\n";
+    for (const auto& ip : ips) {
+      const size_t v = ip.v;
+      const auto& t = C.P.terminals[ip.ai];
+      const auto ex = C.extra_of(static_cast<int>(v));
+      std::vector<long> so(nd);
+      for (int d = 0; d < nd; ++d) so[d] = ex[d] - t.base[d];
+      const long E0 = t.extent[0], E1 = nd > 1 ? t.extent[1] : 1, E2 = nd > 2 ? t.extent[2] : 1, PL = E1 * E2;
+      const long BH = C.vmax[v][0] - C.vmin[v][0];
+      const long BW1 = C.vmax[v][1] - C.vmin[v][1], BW2 = nd > 2 ? C.vmax[v][2] - C.vmin[v][2] : 0;
+      const long NT1 = (C.N[1] + tile[1] - 1) / tile[1], NT2 = nd > 2 ? (C.N[2] + tile[2] - 1) / tile[2] : 1;
+      const long nc1 = (NT1 - 1) * BW1 * E0 * E2, nc2 = nd > 2 ? (NT2 - 1) * BW2 * E0 * E1 : 0;
+      src << "  {\n";
+      src << "    const T* m = reinterpret_cast<const T*>(a.t[" << ip.ai << "]);\n";
+      src << "    T* rb = reinterpret_cast<T*>(a.t[" << ip.slot << "]);\n";
+      src << "    T* c1 = reinterpret_cast<T*>(a.t[" << ip.slot + 1 << "]);\n";
+      src << "    T* c2 = reinterpret_cast<T*>(a.t[" << ip.slot + 2 << "]);\n";
+      src << "    const long long nrb = (long long)max(0, nch - 1) * " << BH * PL << "LL;\n";
+      src << "    const long long tot = nrb + " << (nc1 + nc2) << "LL;\n";
+      src << "    for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < tot; idx += (long long)gridDim.x * blockDim.x) {\n";
+      src << "      if (idx < nrb) {\n";
+      src << "        const long long p = idx % " << PL << "LL, r = idx / " << PL << "LL;\n";
+      src << "        const long long y = (r / " << BH << " + 1) * (long long)a.chunk" << plus(C.vmin[v][0]) << " + r % " << BH << ";\n";
+      src << "        rb[idx] = m[(y" << plus(so[0]) << ") * " << PL << "LL + p];\n";
+      src << "      } else if (idx < nrb + " << nc1 << "LL) {\n";
+      src << "        long long j = idx - nrb;\n";
+      src << "        const long long z2 = j % " << E2 << "LL; j /= " << E2 << "LL;\n";
+      src << "        const long long zy = j % " << E0 << "LL; j /= " << E0 << "LL;\n";
+      src << "        const long long x1 = (j / " << std::max(1L, BW1) << " + 1) * " << tile[1] << plus(C.vmin[v][1]) << " + j % "
+          << std::max(1L, BW1) << ";\n";
+      src << "        c1[idx - nrb] = m[zy * " << PL << "LL + (x1" << plus(so[1]) << ") * " << E2 << "LL + z2];\n";
+      if (nd == 3) {
+        src << "      } else {\n";
+        src << "        long long j = idx - nrb - " << nc1 << "LL;\n";
+        src << "        const long long z1 = j % " << E1 << "LL; j /= " << E1 << "LL;\n";
+        src << "        const long long zy = j % " << E0 << "LL; j /= " << E0 << "LL;\n";
+        src << "        const long long x2 = (j / " << std::max(1L, BW2) << " + 1) * " << tile[2] << plus(C.vmin[v][2]) << " + j % "
+            << std::max(1L, BW2) << ";\n";
+        src << "        c2[idx - nrb - " << nc1 << "LL] = m[zy * " << PL << "LL + z1 * " << E2 << "LL + (x2" << plus(so[2]) << ")];\n";
+      }
+      src << "      }\n    }\n  }\n";
+    }
+    src << "}\n";
+  }
   return true;
 }
 
@@ -651,6 +810,8 @@ bool emit_tiled(Ctx& C, JitProgram& out, std::ostream& src) {
   out.smem_bytes = smem;
   out.threads = NT;
   out.march = false;
+  out.inplace.clear();
+  out.inplace_error = C.P.rs.aliases.empty() ? "" : "in-place runs need a 2D/3D chain (the 1D path reads axioms in place)";
   emit_prelude(C, src, NT);
   src << "  const long long o0 = (long long)a.row_lo + (long long)blockIdx.x * " << tile << ";\n";
   for (size_t v = 0; v < nv; ++v)
@@ -950,7 +1111,7 @@ bool emit_nests(const lf::Plan& P, JitProgram& out, std::ostream& src, std::stri
   src << "typedef " << T << " T;\n";
   src << "__device__ __forceinline__ T lf_min(T a, T b) { return a < b ? a : b; }\n";
   src << "__device__ __forceinline__ T lf_max(T a, T b) { return a > b ? a : b; }\n";
-  src << "struct LfArgs { void* t[32]; long long n0; int row_lo, row_hi, top, bottom, chunk, pad; };\n";
+  src << "struct LfArgs { void* t[32]; long long n0; int row_lo, row_hi, top, bottom, chunk, inplace; };\n";
   auto pointers = [&](std::ostream& o) {
     for (int i = 0; i < nterm; ++i) {
       const auto& t = P.terminals[i];

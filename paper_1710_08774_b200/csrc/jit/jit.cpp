@@ -85,12 +85,6 @@ const Drv& drv() {
   return d;
 }
 
-struct Args {
-  void* t[32];
-  long long n0;
-  int row_lo, row_hi, top, bottom, chunk, pad;
-};
-
 }  // namespace
 
 std::shared_ptr<JitKernel> JitKernel::build(const lf::Plan& plan, std::string& why) {
@@ -136,7 +130,74 @@ std::shared_ptr<JitKernel> JitKernel::build(const lf::Plan& plan, std::string& w
 
 JitKernel::~JitKernel() {
   for (void* p : mats_) cudaFree(p);
+  for (void* p : bands_) cudaFree(p);
   if (module_ && drv().ok) drv().unload(static_cast<CUmodule>(module_));
+}
+
+// In place (config.aliases with one buffer for the axiom and its goal): whole
+// (chunk, tile) units; before each step lf_jit_capture copies the rows at
+// chunk boundaries and the columns at tile boundaries that a unit reads but
+// another unit writes, and the step reads those cells from the copies.  The
+// copies are O(surface) -- the grid itself is never duplicated.
+int JitKernel::run_inplace(const ExecArgs& a, JitArgs& args, std::string& err) {
+  const auto& rs = a.plan->rs;
+  const auto& T = a.plan->terminals;
+  if (a.slab && (a.slab->lo != 0 || a.slab->hi != a.slab->global || a.slab->part_hi > a.slab->part_lo)) {
+    err = "in-place runs cover the whole domain (no slabs)";
+    return LF_ERR_UNSUPPORTED;
+  }
+  if (!capture_) {
+    err = "in-place capture kernel missing";
+    return LF_ERR_INTERNAL;
+  }
+  const long rows = rs.ranges[0].trips();
+  // chunk: about two units per resident CTA, at least 8 pipeline depths
+  long chunk = (rows * prog_.inner_tiles + 2L * resident_ - 1) / (2L * resident_);
+  chunk = std::min(rows, std::max(chunk, 8L * std::max(1, prog_.prologue)));
+  if (const char* e = std::getenv("LF_JIT_CHUNK")) chunk = std::max(1L, std::min<long>(rows, std::atol(e)));
+  const long nch = (rows + chunk - 1) / chunk;
+  const size_t eb = static_cast<size_t>(prog_.elem_bytes);
+  std::vector<size_t> need;
+  for (const auto& q : prog_.inplace) {
+    const long nt1 = (q.n1 + q.t1 - 1) / q.t1, nt2 = (q.n2 + q.t2 - 1) / q.t2;
+    need.push_back(std::max<long>(0, nch - 1) * q.bh * q.e1 * q.e2 * eb);
+    need.push_back(std::max<long>(0, nt1 - 1) * q.bw1 * q.e0 * q.e2 * eb);
+    need.push_back(prog_.nd == 3 ? std::max<long>(0, nt2 - 1) * q.bw2 * q.e0 * q.e1 * eb : 0);
+  }
+  if (band_bytes_ != need) {
+    for (void* p : bands_) cudaFree(p);
+    bands_.assign(need.size(), nullptr);
+    for (size_t k = 0; k < need.size(); ++k) {
+      cudaError_t e = cudaMalloc(&bands_[k], std::max<size_t>(need[k], 16));
+      if (e != cudaSuccess) {
+        err = std::string("cudaMalloc(in-place bands): ") + cudaGetErrorString(e);
+        band_bytes_.clear();
+        return LF_ERR_CUDA;
+      }
+    }
+    band_bytes_ = need;
+  }
+  args.n0 = rows;
+  args.row_lo = 0;
+  args.row_hi = static_cast<int>(rows);
+  args.top = args.bottom = 1;
+  args.chunk = static_cast<int>(chunk);
+  args.inplace = 1;
+  for (size_t i = 0; i < T.size(); ++i) args.t[i] = a.terms[i];
+  for (size_t k = 0; k < bands_.size(); ++k) args.t[T.size() + k] = bands_[k];
+  const long units = nch * prog_.inner_tiles;
+  const dim3 grid(static_cast<unsigned>(std::max<long>(1, std::min<long>(resident_, units))));
+  for (int s = 0; s < a.steps; ++s) {
+    int st = launch(capture_, dim3(592), dim3(256), 0, a.stream, &args, err);
+    if (st != LF_OK) return st;
+    st = launch(step_, grid, dim3(prog_.threads), prog_.smem_bytes, a.stream, &args, err);
+    if (st != LF_OK) return st;
+    if (fill_ && prog_.has_fill) {
+      st = launch(fill_, dim3(592), dim3(256), 0, a.stream, &args, err);
+      if (st != LF_OK) return st;
+    }
+  }
+  return LF_OK;
 }
 
 // multi-nest plans: the nests in dataflow order each step; whole domain only
@@ -160,7 +221,7 @@ int JitKernel::run_nests(const ExecArgs& a, std::string& err) {
   int dev = 0, sms = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  Args args;
+  JitArgs args;
   std::memset(&args, 0, sizeof args);
   const long rows = rs.ranges[0].trips();
   args.n0 = rows;
@@ -234,6 +295,7 @@ int JitKernel::run(const ExecArgs& a, std::string& err) {
     module_ = m;
     CUfunction f;
     if (d.get(&f, m, "lf_jit_fill") == CUDA_SUCCESS) fill_ = f;
+    if (d.get(&f, m, "lf_jit_capture") == CUDA_SUCCESS) capture_ = f;
     if (!prog_.nest_kernels.empty()) {
       for (const auto& nk : prog_.nest_kernels) {
         if (d.get(&f, m, nk.fn.c_str()) != CUDA_SUCCESS) {
@@ -256,7 +318,7 @@ int JitKernel::run(const ExecArgs& a, std::string& err) {
   const auto& rs = a.plan->rs;
   const auto& T = a.plan->terminals;
   const RowPart rp = row_part(a, (int)rs.ranges[0].trips());
-  Args args;
+  JitArgs args;
   std::memset(&args, 0, sizeof args);
   args.n0 = rp.rows;
   args.row_lo = rp.lo;
@@ -285,6 +347,17 @@ int JitKernel::run(const ExecArgs& a, std::string& err) {
   } else {
     grid.x = static_cast<unsigned>((rows + prog_.tile[0] - 1) / prog_.tile[0]);
   }
+  // one buffer passed as an aliased axiom and goal: run in place
+  for (size_t i = 0; i < T.size(); ++i)
+    for (size_t j = 0; j < T.size(); ++j)
+      if (!T[i].is_goal && T[j].is_goal && a.terms[i] && a.terms[i] == a.terms[j] && !T[i].dims.empty()) {
+        for (const auto& q : prog_.inplace)
+          if (q.ai == (int)i && q.gi == (int)j) return run_inplace(a, args, err);
+        err = "axiom '" + T[i].name + "' and goal '" + T[j].name + "' share one buffer but " +
+              (prog_.inplace_error.empty() ? std::string("config.aliases does not declare them")
+                                           : prog_.inplace_error);
+        return LF_ERR_UNSUPPORTED;
+      }
   // ping-pong as the built-in executors: goals of the last step land in the
   // goal buffers, intermediate states in plan-owned scratch, axioms untouched
   std::vector<void*> src(a.terms, a.terms + T.size());

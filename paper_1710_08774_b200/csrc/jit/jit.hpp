@@ -20,6 +20,17 @@ struct NestLaunch {
 };
 
 struct JitProgram {
+  // config.aliases pairs the executor can run in place (one buffer):
+  // row bands at chunk boundaries and column bands at tile boundaries
+  struct Inplace {
+    int ai = -1, gi = -1;      // axiom / goal terminal indices
+    int bh = 0, bw1 = 0, bw2 = 0;  // band widths (dim 0, 1, 2)
+    long e0 = 1, e1 = 1, e2 = 1;   // storage extents
+    int t1 = 1, t2 = 1;        // inner tile sizes
+    long n1 = 1, n2 = 1;       // inner trip counts
+  };
+  std::vector<Inplace> inplace;
+  std::string inplace_error;   // why declared aliases cannot run in place
   std::string source;
   std::string type;  // "double" / "float"
   int elem_bytes = 8;
@@ -41,6 +52,14 @@ struct JitProgram {
 
 bool jit_generate(const lf::Plan& plan, JitProgram& out);
 
+// kernel argument block, passed by value; must match `struct LfArgs` in the
+// generated source (codegen.cpp)
+struct JitArgs {
+  void* t[32];  // terminals, then materialised variables / in-place bands
+  long long n0;
+  int row_lo, row_hi, top, bottom, chunk, inplace;
+};
+
 // A compiled chain; owned by one plan.
 class JitKernel {
  public:
@@ -54,12 +73,16 @@ class JitKernel {
   void* module_ = nullptr;  // CUmodule
   void* step_ = nullptr;    // CUfunction
   void* fill_ = nullptr;
+  void* capture_ = nullptr;
+  std::vector<void*> bands_;        // in-place band copies
+  std::vector<size_t> band_bytes_;
   int resident_ = 0;  // CTAs resident at once (occupancy x SMs)
   std::vector<void*> nest_fns_;
   std::vector<void*> mats_;  // device buffers of materialised variables
   std::vector<char> cubin_;
   int launch(void* fn, dim3 grid, dim3 block, size_t smem, cudaStream_t st, void* args, std::string& err);
   int run_nests(const ExecArgs& a, std::string& err);
+  int run_inplace(const ExecArgs& a, JitArgs& args, std::string& err);
 };
 
 }  // namespace lfx

@@ -543,6 +543,87 @@ std::optional<Plan> make_plan(const RuleSet& rs_in, DiagList& diags) {
     P.footprint = s.empty() ? "0" : s;
   }
 
+  // ---- alias chain and shadow windows (storage.cpp:453-524, 544-594) ----------
+  for (const auto& [in_ext, out_ext] : rs.aliases) {
+    std::set<int> start, target;
+    for (const auto& r : g.raps) {
+      if (r.kind == RapKind::load && r.external == in_ext) start.insert(r.id);
+      if (r.kind == RapKind::store && r.external == out_ext) target.insert(r.id);
+    }
+    if (start.empty() || target.empty()) continue;
+    std::set<int> reach;
+    std::vector<int> stack(start.begin(), start.end());
+    while (!stack.empty()) {
+      const int r = stack.back();
+      stack.pop_back();
+      if (!reach.insert(r).second) continue;
+      for (int w : g.out_adj[r]) stack.push_back(w);
+    }
+    bool interdependent = false;
+    for (int t : target) interdependent |= reach.count(t) > 0;
+    if (!interdependent) continue;
+    for (int t : target) {
+      const Rap& st = g.raps[t];
+      const auto& sterm = g.terms[st.in_terms[0]];
+      const int sv = var_of.at({sterm.tag, sterm.ident});
+      // write-through producer, or the store itself when it materialises a copy
+      const int writer = (P.vars[sv].external == out_ext && !P.vars[sv].axiom_backed && P.vars[sv].producer_group >= 0)
+                             ? P.vars[sv].producer_group
+                             : P.group_of[t];
+      const auto& sw = P.shifts[writer];
+      AliasEntry e;
+      e.input = in_ext;
+      e.output = out_ext;
+      e.writer_group = writer;
+      e.writer_shift = sw;
+      std::set<std::vector<int>> offs;
+      for (const auto& r : g.raps) {
+        if (r.kind == RapKind::load) continue;
+        for (int in : r.in_terms) {
+          const auto& ct = g.terms[in];
+          const int rv = var_of.at({ct.tag, ct.ident});
+          if (!P.vars[rv].axiom_backed || P.vars[rv].external != in_ext) continue;
+          e.var = rv;
+          const auto delta = member_delta(r.id);
+          const auto& sc = P.shifts[P.group_of[r.id]];
+          std::vector<int> eff(nd, 0);
+          for (const auto& o : ct.dims) eff[o.dim] = sc[o.dim] + (o.offset - delta[o.dim]) - sw[o.dim];
+          if (eff <= std::vector<int>(nd, 0)) offs.insert(eff);  // read at or after the write trip
+        }
+      }
+      if (e.var < 0 || offs.empty()) continue;
+      e.offsets.assign(offs.rbegin(), offs.rend());
+      // shadow covering the clobbered window
+      Shadow sh;
+      sh.var = e.var;
+      const auto& vd = P.vars[e.var].dims;
+      std::map<int, std::pair<int, int>> win;
+      for (int d : vd) win[d] = {0, 0};
+      for (const auto& o : e.offsets)
+        for (int d : vd) {
+          win[d].first = std::min(win[d].first, o[d]);
+          win[d].second = std::max(win[d].second, o[d]);
+        }
+      int rot = -1;
+      for (int d : vd)
+        if (win[d].second - win[d].first + 1 > 1) {
+          rot = d;
+          break;
+        }
+      for (int d : vd) sh.spans.push_back(win[d].second - win[d].first + 1);
+      if (rot < 0) {
+        sh.scheme = vd.empty() ? Scheme::full : Scheme::inner_circular;
+        if (!vd.empty()) sh.spans.back() = 1;
+      } else {
+        bool inner_full = false;
+        for (int d : vd) inner_full |= d > rot;
+        sh.scheme = inner_full ? Scheme::outer_rotate : Scheme::inner_circular;
+      }
+      P.alias.push_back(std::move(e));
+      P.shadows.push_back(std::move(sh));
+    }
+  }
+
   // ---- canonical chain signature ---------------------------------------------
   // Hash of the computation independent of rule/variable/terminal names: each
   // intermediate is named by its producing function, output slot and the
@@ -681,6 +762,25 @@ std::string Plan::report_json() const {
   for (size_t d = 0; d < nd; ++d) os << (d ? "," : "") << halo_lo[d];
   os << "],\"halo_hi\":[";
   for (size_t d = 0; d < nd; ++d) os << (d ? "," : "") << halo_hi[d];
+  os << "],\"alias\":[";
+  for (size_t k = 0; k < alias.size(); ++k) {
+    const auto& e = alias[k];
+    const auto& wg = groups[e.writer_group];
+    std::string wn = wg.kind == RapKind::kernel ? rs.kernels[wg.kernel].name
+                                                : (wg.kind == RapKind::load ? "load " : "store ") + wg.external;
+    os << (k ? "," : "") << "{\"input\":" << json_str(e.input) << ",\"output\":" << json_str(e.output)
+       << ",\"var\":" << json_str(vars[e.var].name) << ",\"writer\":" << json_str(wn) << ",\"writer_shift\":[";
+    for (size_t d = 0; d < e.writer_shift.size(); ++d) os << (d ? "," : "") << e.writer_shift[d];
+    os << "],\"offsets\":[";
+    for (size_t o = 0; o < e.offsets.size(); ++o) {
+      os << (o ? "," : "") << "[";
+      for (size_t d = 0; d < e.offsets[o].size(); ++d) os << (d ? "," : "") << e.offsets[o][d];
+      os << "]";
+    }
+    os << "],\"shadow\":{\"scheme\":" << json_str(scheme_name(shadows[k].scheme)) << ",\"spans\":[";
+    for (size_t d = 0; d < shadows[k].spans.size(); ++d) os << (d ? "," : "") << shadows[k].spans[d];
+    os << "]}}";
+  }
   os << "],\"footprint\":" << json_str(footprint) << ",\"signature\":" << json_str(signature) << "}";
   return os.str();
 }

@@ -273,6 +273,22 @@ struct Terminal {
   int elem_bytes = 8;
 };
 
+// alias_chain (storage.cpp:453-524): reads of an aliased input that happen at
+// or after the trip that overwrites them, relative to the writer's shift
+struct AliasEntry {
+  std::string input, output;            // [input buffer, output buffer] from config.aliases
+  int var = -1;                         // the axiom-backed variable read
+  int writer_group = -1;                // group writing the output (write-through producer)
+  std::vector<int> writer_shift;
+  std::vector<std::vector<int>> offsets;  // clobbered read offsets, descending lexicographic
+};
+// shadow window of an alias entry (storage.cpp:544-594)
+struct Shadow {
+  int var = -1;
+  Scheme scheme = Scheme::full;
+  std::vector<long> spans;  // per variable dim
+};
+
 struct Plan {
   RuleSet rs;
   DataflowDAG dag;
@@ -289,6 +305,8 @@ struct Plan {
   std::string footprint;
   std::vector<int> halo_lo, halo_hi;  // per loop dim: max terminal read reach
   std::string signature;             // canonical chain signature for dispatch
+  std::vector<AliasEntry> alias;     // in-place safety plan (empty without config.aliases)
+  std::vector<Shadow> shadows;       // one per alias entry
   std::string report_json() const;
 };
 

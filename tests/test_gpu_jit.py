@@ -74,3 +74,62 @@ def test_jit_slab_parts_compose():
         plan.run_slab([u, parts], 0, 9, 9, part=part)
     torch.cuda.synchronize()
     assert torch.equal(whole[1:-1], parts[1:-1])
+
+
+@pytest.mark.parametrize("name,shape,steps,chunk", [
+    ("biharm_inplace", (300, 1000), 3, None),
+    ("biharm_inplace", (300, 1000), 2, "24"),
+    ("heat3d_inplace", (20, 40, 130), 3, None),
+    ("heat3d_inplace", (20, 40, 130), 2, "5"),
+])
+def test_inplace_matches_out_of_place_oracle(name, shape, steps, chunk, monkeypatch):
+    """config.aliases + one buffer for axiom and goal: the generic executor
+    runs in place (bands captured at unit boundaries) and must equal the
+    out-of-place run_naive bit for bit, ghost ring included."""
+    import torch
+    if chunk:
+        monkeypatch.setenv("LF_JIT_CHUNK", chunk)  # many row chunks -> many row bands
+    spec = lf.set_ranges((SPECS / f"{name}.lf").read_text(), shape)
+    plan = lf.Plan(spec, f"{name}.lf")
+    assert plan.executor == "jit_window_fused"
+    if len(shape) == 2:
+        u0 = inputs.biharm_input(*shape, seed=8)
+    else:
+        u0 = inputs.heat3d_input(*shape, seed=8, sigma=4.0)
+    u = torch.from_numpy(u0.copy()).cuda()
+    plan.run([u, u], steps=steps)
+    torch.cuda.synchronize()
+    path = SPECS / f"_tmp_{name}_{'x'.join(map(str, shape))}.lf"
+    path.write_text(spec)
+    try:
+        ref = generic.run_naive(path, {"g_u": u0}, steps=steps)["g_unew"]
+    finally:
+        path.unlink()
+    assert np.array_equal(bits(u.cpu().numpy()), bits(ref))
+
+
+def test_shared_buffers_need_declared_aliases_and_the_generic_executor():
+    import torch
+    # generic executor, aliases not declared
+    p = lf.Plan.from_file(SPECS / "biharm_body.lf")
+    u = torch.from_numpy(inputs.biharm_input(40, 72, seed=1)).cuda()
+    with pytest.raises(lf.LoomfuseError) as e:
+        p.run([u, u])
+    assert e.value.code == lf.LF_ERR_UNSUPPORTED and "aliases" in str(e.value)
+    # built-in executor: ping-pong only
+    b = lf.Plan.with_ranges("biharmonic2d", (64, 128))
+    v = torch.from_numpy(inputs.biharm_input(64, 128, seed=1)).cuda()
+    with pytest.raises(lf.LoomfuseError) as e:
+        b.run([v, v])
+    assert e.value.code == lf.LF_ERR_UNSUPPORTED
+
+
+def test_inplace_host_path():
+    """lf_run_host with one host buffer for the aliased axiom and goal keeps
+    one device buffer and runs in place."""
+    spec = lf.set_ranges((SPECS / "biharm_inplace.lf").read_text(), (200, 600))
+    plan = lf.Plan(spec, "b.lf")
+    u0 = inputs.biharm_input(200, 600, seed=12)
+    u = u0.copy()
+    plan.run_host([u, u], steps=3)
+    assert np.array_equal(bits(u), bits(oracle.biharm(u0, 3)))
