@@ -52,6 +52,11 @@ struct Win {
   double ex[3][2];    // halo columns carried by the edge lanes
   double L[3][CPL];   // L rows, indexed by row % 3
   double lex[3];      // L at the halo column, indexed by row % 3
+  // i-1 / i+1 neighbours of the lane's first / last column, per row slot:
+  // exchanged by shuffle one marched row BEFORE they are consumed, so the
+  // shuffle latency never sits on the lap1 -> lap2 dependency chain
+  double uw[3], ue[3];  // of u
+  double lw[3], le[3];  // of L
 };
 
 __device__ __forceinline__ double2 lds2(const double* p) { return *reinterpret_cast<const double2*>(p); }
@@ -71,18 +76,19 @@ __device__ __forceinline__ void biharm_row(Win<CPL>& w, const double* row, int t
     }
     const double2 e = lds2(row + ex_col);
     w.ex[C][0] = e.x; w.ex[C][1] = e.y;
+    // neighbours of u row r, consumed by lap1 when this row is r-1 (next row)
+    const double left = __shfl_up_sync(0xffffffffu, w.u[C][CPL - 1], 1);
+    const double right = __shfl_down_sync(0xffffffffu, w.u[C][0], 1);
+    w.uw[C] = lane == 0 ? e.y : left;
+    w.ue[C] = lane == 31 ? e.x : right;
   }
   if (t < 2) return;
   // ---- lap1 at row r-1 (runs one row ahead of the output: shift j = +1)
   const double* um = w.u[M1];
-  const double uleft = __shfl_up_sync(0xffffffffu, um[CPL - 1], 1);
-  const double uright = __shfl_down_sync(0xffffffffu, um[0], 1);
-  const double uw = lane == 0 ? w.ex[M1][1] : uleft;
-  const double ue = lane == 31 ? w.ex[M1][0] : uright;
   double* Ln = w.L[M1];  // slot of L row r-1
 #pragma unroll
   for (int c = 0; c < CPL; ++c)
-    lap5(c == 0 ? uw : um[c - 1], c == CPL - 1 ? ue : um[c + 1], w.u[M2][c], w.u[C][c], um[c], &Ln[c]);
+    lap5(c == 0 ? w.uw[M1] : um[c - 1], c == CPL - 1 ? w.ue[M1] : um[c + 1], w.u[M2][c], w.u[C][c], um[c], &Ln[c]);
   // L at the strip's halo column: lane 0 -> logical -1, lane 31 -> SW (one lap5, operands selected)
   {
     const bool lo = lane == 0;
@@ -94,19 +100,21 @@ __device__ __forceinline__ void biharm_row(Win<CPL>& w, const double* row, int t
     const double h0 = hc ? w.ex[M1][1] : w.ex[M1][0];
     lap5(hw, he, hs, hn, h0, &w.lex[M1]);
   }
+  // neighbours of L row r-1, consumed by lap2 when this row is r-2 (next row)
+  {
+    const double left = __shfl_up_sync(0xffffffffu, Ln[CPL - 1], 1);
+    const double right = __shfl_down_sync(0xffffffffu, Ln[0], 1);
+    w.lw[M1] = lane == 0 ? w.lex[M1] : left;
+    w.le[M1] = lane == 31 ? w.lex[M1] : right;
+  }
   if (t < 4) return;
   // ---- lap2 + update at row r-2: L rows r-3 (slot C), r-2 (slot M2), r-1 (slot M1)
   const double* L0 = w.L[M2];
-  const double lleft = __shfl_up_sync(0xffffffffu, L0[CPL - 1], 1);
-  const double lright = __shfl_down_sync(0xffffffffu, L0[0], 1);
-  const double lhalo = w.lex[M2];  // halo-column L of row r-2
-  const double lw = lane == 0 ? lhalo : lleft;
-  const double le = lane == 31 ? lhalo : lright;
   double o[CPL];
 #pragma unroll
   for (int c = 0; c < CPL; ++c) {
     double l2;
-    lap5(c == 0 ? lw : L0[c - 1], c == CPL - 1 ? le : L0[c + 1], w.L[C][c], w.L[M1][c], L0[c], &l2);
+    lap5(c == 0 ? w.lw[M2] : L0[c - 1], c == CPL - 1 ? w.le[M2] : L0[c + 1], w.L[C][c], w.L[M1][c], L0[c], &l2);
     biharm_update(w.u[M2][c], l2, &o[c]);
   }
 #pragma unroll
@@ -202,13 +210,15 @@ const Variant& variant() {
       make_variant<Cfg<2, 6, 24>>("cpl2_s6_occ24"), make_variant<Cfg<4, 6, 12>>("cpl4_s6_occ12"),
       make_variant<Cfg<2, 8, 16>>("cpl2_s8_occ16"), make_variant<Cfg<4, 8, 8>>("cpl4_s8_occ8"),
       make_variant<Cfg<2, 16, 8>>("cpl2_s16_occ8"), make_variant<Cfg<2, 12, 10>>("cpl2_s12_occ10"),
-      make_variant<Cfg<4, 6, 10>>("cpl4_s6_occ10"),
+      make_variant<Cfg<4, 6, 10>>("cpl4_s6_occ10"), make_variant<Cfg<2, 10, 12>>("cpl2_s10_occ12"),
+      make_variant<Cfg<2, 8, 12>>("cpl2_s8_occ12"), make_variant<Cfg<2, 12, 12>>("cpl2_s12_occ12"),
+      make_variant<Cfg<2, 16, 10>>("cpl2_s16_occ10"), make_variant<Cfg<2, 6, 16>>("cpl2_s6_occ16"),
   };
   static int idx = [] {
     const char* e = std::getenv("LF_BIHARM_VARIANT");
-    // default cpl4_s8_occ8: best of the measured sweep (profiles/r01_biharm_variants.txt)
-    int i = e ? std::atoi(e) : 5;
-    return (i >= 0 && i < (int)(sizeof table / sizeof table[0])) ? i : 5;
+    // default cpl2_s12_occ10: best of the measured sweep (profiles/r01_biharm_variants.txt)
+    int i = e ? std::atoi(e) : 7;
+    return (i >= 0 && i < (int)(sizeof table / sizeof table[0])) ? i : 7;
   }();
   return table[idx];
 }
