@@ -36,6 +36,7 @@ static inline bool operator<(Fd a, Fd b) { ++g.cmp; return a.v < b.v; }
 static inline bool operator>(Fd a, Fd b) { ++g.cmp; return a.v > b.v; }
 static inline bool operator<=(Fd a, Fd b) { ++g.cmp; return a.v <= b.v; }
 static inline bool operator>=(Fd a, Fd b) { ++g.cmp; return a.v >= b.v; }
+static inline bool operator==(Fd a, Fd b) { ++g.cmp; return a.v == b.v; }
 static inline Fd sqrt(Fd a) { ++g.sqrt; return Fd(std::sqrt(a.v)); }
 static inline Fd fabs(Fd a) { return Fd(std::fabs(a.v)); }
 

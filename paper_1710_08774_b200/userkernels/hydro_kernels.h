@@ -34,6 +34,14 @@
 #define HY_NITER 10
 
 LF_HD double hy_max(double a, double b) { return a > b ? a : b; }
+/* a / b for a denominator that is finite and nonzero (every division of this
+ * chain): a zero numerator returns a * b, which is the same signed zero as the
+ * quotient.  Keeps the exactly-zero differences of states at rest (velocities,
+ * pressure jumps, slopes) off the device's division slow path. */
+LF_HD double hy_div(double a, double b) {
+  if (a == 0.0) return a * b;
+  return a / b;
+}
 LF_HD double hy_min(double a, double b) { return a < b ? a : b; }
 
 /* conservative -> primitive (density, normal & transverse velocity, pressure) */
@@ -72,7 +80,7 @@ LF_HD void hy_trace(double r, double n, double t, double p, double dr, double dn
                     double* pt, double* pp) {
   const double h = -0.5 * dtdx;
   const double sr = h * (n * dr + r * dn);
-  const double sn = h * (n * dn + dp / r);
+  const double sn = h * (n * dn + hy_div(dp, r));
   const double st = h * (n * dt);
   const double sp = h * (n * dp + HY_GAMMA * p * dn);
   *mr = hy_max(r - 0.5 * dr + sr, HY_SMALLR);
@@ -126,14 +134,14 @@ LF_HD double hy_riemann_newton(const hy_rp* c, double ps) {
   const double wl2 = wl * wl, wr2 = wr * wr;
   const double num = 2.0 * wl2 * wr2 * ((c->nl - c->nr) * wl * wr - (ps - c->pl) * wr - (ps - c->pr) * wl);
   const double den = (wl2 + c->cl2) * (wr2 * wr) + (wr2 + c->cr2) * (wl2 * wl);
-  return hy_max(ps + num / den, HY_SMALLP);
+  return hy_max(ps + hy_div(num, den), HY_SMALLP);
 }
 
 LF_HD void hy_riemann_sample(const hy_rp* c, double ps, double rl, double tl, double rr, double tr, double* gr,
                              double* gn, double* gt, double* gp) {
   const double wl = c->cl * sqrt(1.0 + c->kpl * (ps - c->pl));
   const double wr = c->cr * sqrt(1.0 + c->kpr * (ps - c->pr));
-  const double us = (wl * c->nl + wr * c->nr + c->pl - c->pr) / (wl + wr);
+  const double us = hy_div(wl * c->nl + wr * c->nr + c->pl - c->pr, wl + wr);
   const int left = us > 0.0;
   const double ro = left ? rl : rr;
   const double uo = left ? c->nl : -c->nr; /* velocity along the sampled wave direction */
@@ -143,7 +151,7 @@ LF_HD void hy_riemann_sample(const hy_rp* c, double ps, double rl, double tl, do
   const double uss = left ? us : -us;
   const double iro = 1.0 / ro;
   const double co = sqrt(HY_GAMMA * po * iro);
-  const double rstar = hy_max(ro / (1.0 + ro * (po - ps) / (wo * wo)), HY_SMALLR);
+  const double rstar = hy_max(ro / (1.0 + hy_div(ro * (po - ps), wo * wo)), HY_SMALLR);
   const double cstar = sqrt(HY_GAMMA * ps / rstar);
   double spout = co - uo;
   double spin = cstar - uss;
@@ -153,7 +161,7 @@ LF_HD void hy_riemann_sample(const hy_rp* c, double ps, double rl, double tl, do
     spin = ushock;
   }
   const double scr = hy_max(spout - spin, HY_SMALLC + fabs(spout + spin));
-  const double frac = hy_min(hy_max(0.5 * (1.0 + (spout + spin) / scr), 0.0), 1.0);
+  const double frac = hy_min(hy_max(0.5 * (1.0 + hy_div(spout + spin, scr)), 0.0), 1.0);
   double r = frac * rstar + (1.0 - frac) * ro;
   double u = frac * uss + (1.0 - frac) * uo;
   double p = frac * ps + (1.0 - frac) * po;
