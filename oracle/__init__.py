@@ -49,7 +49,6 @@ def lib() -> ctypes.CDLL:
             L.lfo_hydro_naive.argtypes = [PP, PP, Lg, Lg, ctypes.c_double, I]
             L.lfo_hydro_fused.argtypes = [PP, PP, Lg, Lg, ctypes.c_double, I, I]
             L.lfo_hydro_fused_step.argtypes = [PP, PP, Lg, Lg, ctypes.c_double, I]
-            L.lfo_hydro_flops_per_cell.restype = ctypes.c_long
         _lib = L
     return _lib
 
@@ -136,9 +135,6 @@ def hydro_step(state, outs, dtdx: float, threads: int = 0) -> None:
     _ok(lib().lfo_hydro_fused_step(PA(*[_p(a) for a in state]), PA(*[_p(a) for a in outs]), nj, ni, dtdx,
                                    threads))
 
-
-def hydro_flops_per_cell() -> int:
-    return int(lib().lfo_hydro_flops_per_cell())
 
 
 # ---- reference planner (bookkeeping oracle) -------------------------------------

@@ -280,9 +280,3 @@ int lfo_hydro_fused(const double* const in[4], double* const out[4], long nj, lo
   return 0;
 }
 #undef AT
-
-/* Arithmetic operations (+ - * / sqrt; comparisons, min/max and fabs not
- * counted) of one cell-step as written in hydro_kernels.h, per sweep:
- * constoprim 10, slope 12, trace 40, riemann 412 (10 Newton steps x 34 + 72),
- * flux 13, update 12 = 499; a step is an x-sweep plus a y-sweep. */
-long lfo_hydro_flops_per_cell(void) { return 2 * (10 + 12 + 40 + 412 + 13 + 12); }

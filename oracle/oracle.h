@@ -20,7 +20,10 @@
  * golden vectors for this path, so the numerical oracle is
  * "parity unpinned" against the reference itself; the terminal extents/bases
  * that both schedules rely on are pinned against the reference's own planner
- * compiled from /root/reference (oracle/ref_planner.cpp -> oracle/_ref/).
+ * compiled from /root/reference (oracle/ref_planner.cpp -> oracle/_ref/), and
+ * the chains' numerics are cross-checked bit for bit against a second,
+ * independent run_naive (oracle/generic.py) that evaluates the same kernels
+ * over the dataflow DAG the reference's own inference derives.
  *
  * Buffer conventions (identical to the GPU executors):
  *   terminals are dense row-major arrays of the reference's buffer_extents
@@ -62,8 +65,6 @@ int lfo_hydro_fused(const double* const in[4], double* const out[4], long nj, lo
                     double dtdx, int steps, int threads);
 int lfo_hydro_fused_step(const double* const in[4], double* const out[4], long nj, long ni,
                          double dtdx, int threads);
-/* counts double-precision operations of one cell-step of the hydro chain */
-long lfo_hydro_flops_per_cell(void);
 
 int lfo_max_threads(void);
 
