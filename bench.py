@@ -373,7 +373,10 @@ def main():
                 # face rows first, their NCCL exchange overlapped with the interior rows
                 slabs.run_slabs_overlapped(launch, cur, nxt, w["chain_steps"], halo, rank, world, hi - lo,
                                            comm_stream=comm)
-    launches = plan.launches_per_step * w["chain_steps"]
+    # one pass over the grid per step, except where the executor fuses time
+    # steps (heat3d: two-step passes on a whole domain); slabs step singly
+    passes = plan.grid_passes(w["chain_steps"]) if world == 1 else w["chain_steps"]
+    launches = plan.launches(w["chain_steps"]) if world == 1 else plan.launches_per_step * w["chain_steps"]
 
     def barrier():
         if world > 1:
@@ -398,20 +401,23 @@ def main():
         ms = float(t.item())
     value = cells * w["chain_steps"] / (ms / 1e3)
 
-    # roofline of the dominant (only) kernel: algorithmic bytes per launch /
-    # average launch duration over the timed region
+    # roofline of the dominant (only) kernel: algorithmic bytes per pass over
+    # the grid (terminals read once + written once) / average pass duration
+    # over the timed region (= per-launch bytes / launch time for one kernel
+    # per pass)
     peak, peak_src = measured_peak()
     bpc = plan.compulsory_bytes_per_cell
-    cells_per_launch = cells / max(1, plan.launches_per_step) / (world if world > 1 else 1)
-    launch_s = (ms / 1e3) / (launches if launches else 1)
-    achieved = bpc * cells_per_launch / launch_s / 1e9
+    cells_local = cells / (world if world > 1 else 1)
+    pass_s = (ms / 1e3) / max(1, passes)
+    achieved = bpc * cells_local / pass_s / 1e9
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                 "traffic": ncu_traffic(args.config), "peak_source": peak_src,
-                "algorithmic_bytes_per_cell": bpc}
+                "algorithmic_bytes_per_cell": bpc, "cell_updates_per_pass": w["chain_steps"] / max(1, passes),
+                "passes": passes}
     if w["spec"] == "hydro2d":
         # compute-bound chain: the fp64 roofline is the binding one; HBM kept beside it
         fpk = measured_fp64_peak()
-        tf = HYDRO_FLOPS_PER_CELL_STEP * cells_per_launch / launch_s / 1e12
+        tf = HYDRO_FLOPS_PER_CELL_STEP * cells_local * w["chain_steps"] / (ms / 1e3) / 1e12
         roofline = {"bound": "fp64", "achieved": tf, "peak": fpk, "unit": "TFLOP/s", "frac": tf / fpk,
                     "traffic": ncu_traffic(args.config),
                     "peak_source": "measured live (tools/fp64_probe.cu: DFMA chains)",

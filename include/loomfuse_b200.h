@@ -139,10 +139,17 @@ int lf_run_host(const lf_plan* plan, void* const* terminals, int nterm, int step
 int lf_run_slab(const lf_plan* plan, void* const* terminals, int nterm, const lf_slab* slab,
                 void* cuda_stream);
 
-/* Number of fused-executor kernel launches one step issues (for bench
- * accounting), and the algorithmic (compulsory) HBM bytes per cell-update. */
+/* Bench accounting.  lf_plan_launches_per_step: kernel launches of one
+ * single-step pass; lf_plan_compulsory_bytes_per_cell: algorithmic HBM bytes
+ * per cell of one pass over the grid (terminals read once + written once);
+ * lf_plan_grid_passes: passes lf_run(plan, ..., steps) makes over a whole
+ * domain (fewer than `steps` where the executor fuses time steps, e.g. the
+ * 3D heat chain's two-step passes); lf_plan_launches: kernel launches it
+ * issues. */
 int lf_plan_launches_per_step(const lf_plan* plan);
 double lf_plan_compulsory_bytes_per_cell(const lf_plan* plan);
+int lf_plan_grid_passes(const lf_plan* plan, int steps);
+int lf_plan_launches(const lf_plan* plan, int steps);
 
 /* Thread-local message of the last failing call on this thread ("" if none). */
 const char* lf_last_error(void);

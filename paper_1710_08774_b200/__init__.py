@@ -36,7 +36,8 @@ LF_MAX_DIMS = 4
 ABI_SYMBOLS = (
     "lf_plan_create", "lf_plan_destroy", "lf_plan_num_terminals", "lf_plan_terminal",
     "lf_plan_report", "lf_plan_executor", "lf_run", "lf_run_host", "lf_run_slab",
-    "lf_plan_launches_per_step", "lf_plan_compulsory_bytes_per_cell", "lf_last_error",
+    "lf_plan_launches_per_step", "lf_plan_compulsory_bytes_per_cell", "lf_plan_grid_passes", "lf_plan_launches",
+    "lf_last_error",
     "lf_version", "lf_spec_print", "lf_plan_source",
 )
 
@@ -100,6 +101,8 @@ def lib() -> ctypes.CDLL:
     L.lf_plan_launches_per_step.argtypes = [P]
     L.lf_plan_compulsory_bytes_per_cell.argtypes = [P]
     L.lf_plan_compulsory_bytes_per_cell.restype = ctypes.c_double
+    L.lf_plan_grid_passes.argtypes = [P, ctypes.c_int]
+    L.lf_plan_launches.argtypes = [P, ctypes.c_int]
     L.lf_last_error.restype = ctypes.c_char_p
     L.lf_version.restype = ctypes.c_char_p
     _lib = L
@@ -218,6 +221,14 @@ class Plan:
     @property
     def compulsory_bytes_per_cell(self) -> float:
         return lib().lf_plan_compulsory_bytes_per_cell(self._h)
+
+    def grid_passes(self, steps: int) -> int:
+        """passes over the grid lf_run makes for `steps` steps (whole domain)"""
+        return lib().lf_plan_grid_passes(self._h, steps)
+
+    def launches(self, steps: int) -> int:
+        """kernel launches lf_run issues for `steps` steps (whole domain)"""
+        return lib().lf_plan_launches(self._h, steps)
 
     @property
     def axioms(self) -> list[Terminal]:

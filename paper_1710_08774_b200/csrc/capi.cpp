@@ -248,6 +248,18 @@ int lf_plan_launches_per_step(const lf_plan* plan) {
   return static_cast<int>(std::max<size_t>(1, pg.nest_kernels.size())) + (pg.has_fill ? 1 : 0);
 }
 
+int lf_plan_grid_passes(const lf_plan* plan, int steps) {
+  if (!plan || steps < 1) return 0;
+  if (plan->exec && plan->exec->passes) return plan->exec->passes(plan->plan, steps, false);
+  return steps;
+}
+
+int lf_plan_launches(const lf_plan* plan, int steps) {
+  if (!plan || steps < 1) return 0;
+  if (plan->exec) return lf_plan_grid_passes(plan, steps) * plan->exec->launches_per_step;
+  return steps * lf_plan_launches_per_step(plan);
+}
+
 double lf_plan_compulsory_bytes_per_cell(const lf_plan* plan) {
   if (!plan) return 0.0;
   if (plan->exec) return plan->exec->bytes_per_cell;

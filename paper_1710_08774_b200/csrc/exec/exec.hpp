@@ -33,6 +33,9 @@ struct Executor {
   bool (*supports)(const lf::Plan&, std::string& why);
   // run `steps` steps (ping-pong for steps > 1); returns an LF_* status
   int (*run)(const ExecArgs&, std::string& err);
+  // passes over the grid `steps` steps take (temporal blocking fuses several
+  // steps into one pass); nullptr: one pass per step
+  int (*passes)(const lf::Plan&, int steps, bool slab) = nullptr;
 };
 
 // all executors compiled into this library

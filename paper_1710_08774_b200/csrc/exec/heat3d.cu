@@ -51,6 +51,7 @@ struct Params {
   int kchunks;          // work units along k per column
   int units;            // tiles * kchunks
   int wrap_i, wrap_j, wrap_k;  // refill periodic ghosts along this dim
+  int patch;                   // two-step pass: patch periodic images on face tiles
 };
 
 // Work unit u = (k chunk, column tile), k-chunk major: at any moment all
@@ -213,6 +214,180 @@ __global__ void __launch_bounds__(THREADS, 2)
   }
 }
 
+// ---------------------------------------------------------------------------
+// Temporal blocking: two time steps per pass over the grid (the iterate pair
+// of the chain fused in time, as HFAV fuses the chain's kernels in space).
+// A CTA owns a 64 x 16 column tile and marches k; per plane it computes the
+// first step (A) on the tile plus a one-cell ring (66 x 18) from the staged
+// input (tile plus a two-cell ring, 70 x 20 from an aligned origin), keeps
+// three A planes in shared memory, and computes the second step (B) on the
+// tile from them.  Periodicity: k planes are loaded wrapped; on the tiles
+// that touch an i/j face every staged cell outside the domain is replaced by
+// its periodic image from the interior, so the pass never reads the input's
+// ghost layer.  HBM: 8 B read + 8 B written per two cell-updates.
+// ---------------------------------------------------------------------------
+namespace tb {
+constexpr int TY = 16;                  // B tile rows (8 consumer warps x 2)
+constexpr int AX = TX + 2, AY = TY + 2;   // A ring tile: logical i0-1.., j0-1..
+constexpr int LDI = TX + 6, RI = TY + 4;  // staged input: logical i0-3.., j0-2..
+constexpr int STAGE_TX = LDI * RI * 8;
+constexpr int STAGE_BYTES = (STAGE_TX + 127) / 128 * 128;
+constexpr int APLANE = AX * AY;
+template <int S_, int KCH_>
+struct Cfg {
+  static constexpr int S = S_, KCH = KCH_;
+  static constexpr int SMEM = S * STAGE_BYTES + 3 * APLANE * 8 + 2 * S * 8 + 128;
+};
+__device__ __forceinline__ int wrapn(int x, int n) { return x < 0 ? x + n : (x >= n ? x - n : x); }
+__device__ __forceinline__ void consumers_sync() { asm volatile("bar.sync 1, %0;" ::"r"(CWARPS * 32) : "memory"); }
+
+template <class K>
+__global__ void __launch_bounds__(THREADS, 2)
+    heat3d_fused2(const __grid_constant__ CUtensorMap tin, const double* __restrict__ in, double* __restrict__ out,
+                  const Params p) {
+  constexpr int S = K::S;
+  extern __shared__ __align__(128) unsigned char smem[];
+  unsigned char* ring = smem;
+  double* aring = reinterpret_cast<double*>(smem + S * STAGE_BYTES);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + S * STAGE_BYTES + 3 * APLANE * 8);
+  uint64_t* empty = full + S;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], CWARPS);
+    }
+    fence_barrier_init();
+  }
+  __syncthreads();
+  if (warp == CWARPS) {
+    // ---------------- producer: input planes k0-2 .. k0+kc+1, wrapped along k
+    if (lane == 0) {
+      tma_prefetch_desc(&tin);
+      int g = 0;
+      for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
+        const Unit w = unit_of<TY>(p, u);
+        for (int q = 0; q < w.kc + 4; ++q, ++g) {
+          const int slot = g % S;
+          if (g >= S) mbar_wait(&empty[slot], ((g / S) & 1) ^ 1);
+          mbar_arrive_expect_tx(&full[slot], STAGE_TX);
+          // storage = logical + 1: origin logical (i0-3, j0-2, k) -> storage (i0-2, j0-1, k+1)
+          tma_load_3d(ring + slot * STAGE_BYTES, &tin, &full[slot], w.i0 - 2, w.j0 - 1,
+                      wrapn(w.k0 - 2 + q, p.nk) + 1);
+        }
+      }
+    }
+    return;
+  }
+  const int tid = threadIdx.x;
+  const uint64_t pol = l2_evict_first_policy();
+  auto stage = [&](int g) { return reinterpret_cast<double*>(ring + (g % S) * STAGE_BYTES); };
+  int g = 0;
+  for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
+    const Unit w = unit_of<TY>(p, u);
+    const bool face = p.patch && (w.i0 == 0 || w.i0 + TX == p.ni || w.j0 == 0 || w.j0 + TY == p.nj);
+    const int gi0 = w.i0 + lane;
+    const bool wrap_lo_i = p.wrap_i && gi0 == 0;
+    const bool wrap_hi_i = p.wrap_i && gi0 + 32 == p.ni - 1;
+    for (int t = 0; t < w.kc + 4; ++t) {
+      const int gt = g + t;
+      mbar_wait(&full[gt % S], (gt / S) & 1);
+      if (face) {
+        // periodic images for the staged cells outside the domain
+        double* st = stage(gt);
+        const int kk = wrapn(w.k0 - 2 + t, p.nk);
+        for (int e = tid; e < LDI * RI; e += CWARPS * 32) {
+          const int r = e / LDI, c = e - r * LDI;
+          const int i = w.i0 - 3 + c, j = w.j0 - 2 + r;
+          if (i < 0 || i >= p.ni || j < 0 || j >= p.nj)
+            st[e] = in[(long long)(kk + 1) * p.pk + (long long)(wrapn(j, p.nj) + 1) * p.pj + wrapn(i, p.ni) + 1];
+        }
+      }
+      consumers_sync();  // stage t complete (and patched); B of the last trip done with its A slot
+      if (t >= 2) {
+        // ---- A at input plane t-1 (logical k0-3+t) on the 66 x 18 ring tile
+        const double* sm = stage(gt - 2);
+        const double* sc = stage(gt - 1);
+        const double* sp = stage(gt);
+        double* ao = aring + ((t - 1) % 3) * APLANE;
+        for (int e = tid; e < APLANE; e += CWARPS * 32) {
+          const int b = e / AX, a = e - b * AX;
+          const int o = (b + 1) * LDI + a + 2;
+          const double uc = sc[o];
+          double fxp, fxm, fyp, fym, fzp, fzm, r;
+          face_flux(sc[o + 1], uc, &fxp);
+          face_flux(uc, sc[o - 1], &fxm);
+          face_flux(sc[o + LDI], uc, &fyp);
+          face_flux(uc, sc[o - LDI], &fym);
+          face_flux(sp[o], uc, &fzp);
+          face_flux(uc, sm[o], &fzm);
+          heat_divupd(uc, fxp, fxm, fyp, fym, fzp, fzm, &r);
+          ao[e] = r;
+        }
+        // input plane t-2 is no longer needed (A at t needs t-1, t, t+1);
+        // patched cells were written by the generic proxy: order them before
+        // the TMA refill of the slot
+        if (face) fence_proxy_async();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[(gt - 2) % S]);
+        consumers_sync();  // A plane t-1 complete
+      }
+      if (t >= 4) {
+        // ---- B at plane k = k0-4+t from A planes t-3, t-2, t-1
+        const double* am = aring + ((t - 3) % 3) * APLANE;
+        const double* ac = aring + ((t - 2) % 3) * APLANE;
+        const double* ap = aring + ((t - 1) % 3) * APLANE;
+        const int k = w.k0 - 4 + t;
+        double* plane = out + (long long)(k + 1) * p.pk;
+#pragma unroll
+        for (int rr = 0; rr < 2; ++rr) {
+          const int y = 2 * warp + rr;
+          const int j = w.j0 + y;
+          double o2[2];
+#pragma unroll
+          for (int c = 0; c < 2; ++c) {
+            const int x = lane + 32 * c;
+            const int o = (y + 1) * AX + x + 1;
+            const double uc = ac[o];
+            double fxp, fxm, fyp, fym, fzp, fzm;
+            face_flux(ac[o + 1], uc, &fxp);
+            face_flux(uc, ac[o - 1], &fxm);
+            face_flux(ac[o + AX], uc, &fyp);
+            face_flux(uc, ac[o - AX], &fym);
+            face_flux(ap[o], uc, &fzp);
+            face_flux(uc, am[o], &fzm);
+            heat_divupd(uc, fxp, fxm, fyp, fym, fzp, fzm, &o2[c]);
+          }
+          double* rowp = plane + (long long)(j + 1) * p.pj + 1;
+          st_hint(rowp + gi0, o2[0], pol);
+          st_hint(rowp + gi0 + 32, o2[1], pol);
+          if (wrap_lo_i) st_hint(rowp + p.ni, o2[0], pol);
+          if (wrap_hi_i) st_hint(rowp - 1, o2[1], pol);
+          if (p.wrap_j && (j == 0 || j == p.nj - 1)) {
+            double* gr = plane + (long long)(j == 0 ? p.nj + 1 : 0) * p.pj + 1;
+            st_hint(gr + gi0, o2[0], pol);
+            st_hint(gr + gi0 + 32, o2[1], pol);
+          }
+          if (p.wrap_k && (k == 0 || k == p.nk - 1)) {
+            double* gr = out + (long long)(k == 0 ? p.nk + 1 : 0) * p.pk + (long long)(j + 1) * p.pj + 1;
+            st_hint(gr + gi0, o2[0], pol);
+            st_hint(gr + gi0 + 32, o2[1], pol);
+          }
+        }
+      }
+    }
+    // the unit's last two input planes were only read by the last A plane
+    if (face) fence_proxy_async();
+    __syncwarp();
+    if (lane == 0) {
+      mbar_arrive(&empty[(g + w.kc + 2) % S]);
+      mbar_arrive(&empty[(g + w.kc + 3) % S]);
+    }
+    g += w.kc + 4;
+  }
+}
+}  // namespace tb
+
 struct Variant {
   const char* name;
   int ty, kch, smem;
@@ -302,6 +477,53 @@ int launch_step(const double* in, double* out, int ni, int nj, int nk, int k_lo,
   return cuda_status(cudaGetLastError(), "heat3d_fused launch", err);
 }
 
+// two steps per pass (whole periodic domain only: a slab's k ghosts come from
+// the caller's one-plane halo exchange)
+using TB = tb::Cfg<6, 32>;
+
+// opt-in (LF_HEAT3D_TB=1): measured slower than the single-step kernel this
+// round (188 vs 367 G cell-updates/s at 512^3: the periodic-image patching on
+// face tiles and two CTA barriers per plane dominate)
+bool tb_enabled(int ni, int nj, int nk) {
+  const char* e = std::getenv("LF_HEAT3D_TB");
+  const bool on = e && std::atoi(e) != 0;
+  return on && ni % TX == 0 && nj % tb::TY == 0 && nk >= 2 && ni >= TX && nj >= tb::TY;
+}
+
+int launch_pair(const double* in, double* out, int ni, int nj, int nk, cudaStream_t st, std::string& err) {
+  static int slots = 0;
+  if (!slots) {
+    cudaError_t e = cudaFuncSetAttribute(tb::heat3d_fused2<TB>, cudaFuncAttributeMaxDynamicSharedMemorySize, TB::SMEM);
+    if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(heat3d pair)", err);
+    int dev = 0, sms = 148, per_sm = 1;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tb::heat3d_fused2<TB>, THREADS, TB::SMEM);
+    slots = sms * std::max(per_sm, 1);
+  }
+  CUtensorMap map;
+  uint64_t dims[3] = {(uint64_t)ni + 2, (uint64_t)nj + 2, (uint64_t)nk + 2};
+  uint32_t box[3] = {tb::LDI, tb::RI, 1};
+  if (!make_tensor_map(&map, in, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 8, 3, dims, box, err)) return LF_ERR_CUDA;
+  Params p;
+  p.ni = ni;
+  p.nj = nj;
+  p.nk = nk;
+  p.pj = ni + 2;
+  p.pk = (long long)(ni + 2) * (nj + 2);
+  p.tiles_x = ni / TX;
+  p.tiles = (ni / TX) * (nj / tb::TY);
+  p.k_lo = 0;
+  p.k_hi = nk;
+  p.kchunks = std::max(1, (nk + TB::KCH - 1) / TB::KCH);
+  p.units = p.tiles * p.kchunks;
+  p.wrap_i = p.wrap_j = p.wrap_k = 1;
+  p.patch = std::getenv("LF_HEAT3D_NOPATCH") ? 0 : 1;  // timing experiments only (wrong at the faces)
+  const int ctas = std::min(p.units, slots);
+  tb::heat3d_fused2<TB><<<ctas, THREADS, TB::SMEM, st>>>(map, in, out, p);
+  return cuda_status(cudaGetLastError(), "heat3d_fused2 launch", err);
+}
+
 int run(const ExecArgs& a, std::string& err) {
   const auto& r = a.plan->rs.ranges;
   const int nj = (int)r[1].trips(), ni = (int)r[2].trips();
@@ -311,12 +533,17 @@ int run(const ExecArgs& a, std::string& err) {
   const double* src = static_cast<const double*>(a.terms[0]);
   double* goal = static_cast<double*>(a.terms[1]);
   double* scratch = a.steps > 1 ? static_cast<double*>(a.scratch[0]) : nullptr;
-  // steps alternate goal/scratch so that the last one lands in the goal and
-  // the axiom buffer is never written
-  for (int s = 0; s < a.steps; ++s) {
-    bool to_goal = ((a.steps - 1 - s) % 2) == 0;
+  // passes of one or two steps; they alternate goal/scratch so that the last
+  // one lands in the goal and the axiom buffer is never written
+  const bool pairs = wrap_k && a.steps >= 2 && tb_enabled(ni, nj, nk);
+  const int passes = pairs ? (a.steps + 1) / 2 : a.steps;
+  for (int s = 0; s < passes; ++s) {
+    const bool to_goal = ((passes - 1 - s) % 2) == 0;
     double* dst = to_goal ? goal : scratch;
-    int st = launch_step(src, dst, ni, nj, nk, rp.lo, rp.hi, wrap_k, a.stream, err);
+    // an odd step count runs its first step alone
+    const bool two = pairs && !(s == 0 && a.steps % 2 == 1);
+    int st = two ? launch_pair(src, dst, ni, nj, nk, a.stream, err)
+                 : launch_step(src, dst, ni, nj, nk, rp.lo, rp.hi, wrap_k, a.stream, err);
     if (st != LF_OK) return st;
     src = dst;
   }
@@ -325,6 +552,17 @@ int run(const ExecArgs& a, std::string& err) {
 
 }  // namespace
 
-extern const Executor heat3d_executor = {"heat3d_fused_tma", "heat3d.lf", 1, 16.0, supports, run};
+int heat3d_passes(const lf::Plan& plan, int steps, bool slab);
+int heat3d_passes(const lf::Plan& plan, int steps, bool slab) {
+  const auto& r = plan.rs.ranges;
+  const bool pairs = !slab && steps >= 2 && tb_enabled((int)r[2].trips(), (int)r[1].trips(), (int)r[0].trips());
+  return pairs ? (steps + 1) / 2 : steps;
+}
+
+namespace {
+
+}  // namespace
+
+extern const Executor heat3d_executor = {"heat3d_fused_tma", "heat3d.lf", 1, 16.0, supports, run, heat3d_passes};
 
 }  // namespace lfx

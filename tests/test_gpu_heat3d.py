@@ -135,3 +135,27 @@ def test_overlapped_slab_schedule_single_rank_periodic():
     got = res[0].cpu().numpy()
     ref = oracle.heat3d(u, steps)
     assert np.array_equal(bits(interior(got)), bits(interior(ref)))
+
+
+@pytest.mark.parametrize("shape,steps", [((8, 16, 64), 2), ((20, 32, 128), 3), ((64, 64, 64), 4), ((3, 48, 192), 5)])
+def test_two_step_passes_match_naive(shape, steps, monkeypatch):
+    """Opt-in temporal blocking (LF_HEAT3D_TB=1): two time steps per pass over
+    the grid, periodic images patched on face tiles -- bit-exact, faces of the
+    ghost layer refilled as by the single-step kernel."""
+    monkeypatch.setenv("LF_HEAT3D_TB", "1")
+    torch = _torch()
+    plan = lf.Plan.with_ranges("heat3d", shape)
+    assert plan.grid_passes(steps) == (steps + 1) // 2
+    u = inputs.heat3d_input(*shape, seed=13, sigma=4.0)
+    ref = oracle.heat3d(u, steps)
+    du = torch.from_numpy(u).cuda()
+    out = torch.full_like(du, float("nan"))
+    plan.run([du, out], steps=steps)
+    torch.cuda.synchronize()
+    got = out.cpu().numpy()
+    assert np.array_equal(bits(interior(got)), bits(interior(ref)))
+    for ax in range(3):
+        sl_g = [slice(1, -1)] * 3
+        sl_s = [slice(1, -1)] * 3
+        sl_g[ax], sl_s[ax] = 0, -2
+        assert np.array_equal(bits(got[tuple(sl_g)]), bits(got[tuple(sl_s)]))
