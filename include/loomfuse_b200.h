@@ -88,6 +88,16 @@ typedef struct {
  * diagnostics.  On LF_ERR_SPEC the diagnostics are in lf_last_error(). */
 int lf_plan_create(const char* spec_text, size_t len, const char* filename, lf_plan** out);
 
+/* As lf_plan_create, plus CUDA C source defining the user kernels the rule
+ * file names in `declaration:` (R/PAPER.md:58-62: value inputs, outputs by
+ * pointer or reference), as `__device__` (or __host__ __device__) functions.
+ * A chain that no built-in executor implements is lowered by the generic
+ * executor and compiled for sm_100a together with this source and the shipped
+ * user-kernel headers (userkernels/*.h), so kernels need no `body:`.
+ * kernel_source may be NULL. */
+int lf_plan_create_ex(const char* spec_text, size_t len, const char* filename, const char* kernel_source,
+                      size_t kernel_len, lf_plan** out);
+
 /* Canonical text of a rule file (print_spec, rulespec.cpp:668-705): parsing
  * the output again yields a structurally equal rule set.  Same buffer
  * convention as lf_plan_report. */

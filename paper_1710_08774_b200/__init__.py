@@ -34,7 +34,7 @@ LF_MAX_DIMS = 4
 
 #: every symbol the header declares (checked by tests/test_abi.py)
 ABI_SYMBOLS = (
-    "lf_plan_create", "lf_plan_destroy", "lf_plan_num_terminals", "lf_plan_terminal",
+    "lf_plan_create", "lf_plan_create_ex", "lf_plan_destroy", "lf_plan_num_terminals", "lf_plan_terminal",
     "lf_plan_report", "lf_plan_executor", "lf_run", "lf_run_host", "lf_run_slab",
     "lf_plan_launches_per_step", "lf_plan_compulsory_bytes_per_cell", "lf_plan_grid_passes", "lf_plan_launches",
     "lf_last_error",
@@ -84,6 +84,8 @@ def lib() -> ctypes.CDLL:
     L = ctypes.CDLL(str(LIB_PATH))
     P = ctypes.c_void_p
     L.lf_plan_create.argtypes = [ctypes.c_char_p, ctypes.c_size_t, ctypes.c_char_p, ctypes.POINTER(P)]
+    L.lf_plan_create_ex.argtypes = [ctypes.c_char_p, ctypes.c_size_t, ctypes.c_char_p, ctypes.c_char_p,
+                                    ctypes.c_size_t, ctypes.POINTER(P)]
     L.lf_spec_print.argtypes = [ctypes.c_char_p, ctypes.c_size_t, ctypes.c_char_p, ctypes.c_char_p,
                                 ctypes.c_size_t, ctypes.POINTER(ctypes.c_size_t)]
     L.lf_plan_destroy.argtypes = [P]
@@ -160,11 +162,14 @@ def spec_path(name: str) -> Path:
 class Plan:
     """A planned rule file (lf_plan_create) -- immutable, reusable."""
 
-    def __init__(self, text: str, filename: str = "<input>"):
+    def __init__(self, text: str, filename: str = "<input>", kernel_source: str | None = None):
+        """`kernel_source`: CUDA C defining the `declaration:` functions of a
+        chain that has no built-in executor (lf_plan_create_ex)."""
         L = lib()
         h = ctypes.c_void_p()
         raw = text.encode()
-        _check(L.lf_plan_create(raw, len(raw), filename.encode(), ctypes.byref(h)))
+        ks = kernel_source.encode() if kernel_source else None
+        _check(L.lf_plan_create_ex(raw, len(raw), filename.encode(), ks, len(ks) if ks else 0, ctypes.byref(h)))
         self._h = h
         self.filename = filename
         self.terminals: list[Terminal] = []
@@ -177,9 +182,9 @@ class Plan:
                 tuple(t.loop_dim[:n]), tuple(t.extent[:n]), tuple(t.base[:n]), t.bytes))
 
     @classmethod
-    def from_file(cls, path: str | Path) -> "Plan":
+    def from_file(cls, path: str | Path, kernel_source: str | None = None) -> "Plan":
         p = Path(path)
-        return cls(p.read_text(), str(p))
+        return cls(p.read_text(), str(p), kernel_source)
 
     @classmethod
     def bundled(cls, name: str) -> "Plan":

@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <mutex>
@@ -131,6 +132,11 @@ const char* lf_last_error(void) { return g_err.c_str(); }
 const char* lf_version(void) { return "loomfuse-b200 0.1 (sm_100a)"; }
 
 int lf_plan_create(const char* spec_text, size_t len, const char* filename, lf_plan** out) {
+  return lf_plan_create_ex(spec_text, len, filename, nullptr, 0, out);
+}
+
+int lf_plan_create_ex(const char* spec_text, size_t len, const char* filename, const char* kernel_source,
+                      size_t kernel_len, lf_plan** out) {
   try {
     g_err.clear();
     if (!out) return fail(LF_ERR_SPEC, "out is NULL");
@@ -147,7 +153,10 @@ int lf_plan_create(const char* spec_text, size_t len, const char* filename, lf_p
     p->plan = std::move(*plan);
     p->report = p->plan.report_json();
     std::string why = "no built-in executor implements this chain";
+    // LF_NO_BUILTIN=1: skip the hand-written executors (A/B runs of the generic one)
+    static const bool no_builtin = std::getenv("LF_NO_BUILTIN") && std::atoi(std::getenv("LF_NO_BUILTIN")) != 0;
     for (const auto& s : signed_executors()) {
+      if (no_builtin) break;
       if (!s.error.empty()) {
         why = std::string("embedded spec ") + s.exec->spec_file + " failed to plan: " + s.error;
         continue;
@@ -163,7 +172,8 @@ int lf_plan_create(const char* spec_text, size_t len, const char* filename, lf_p
     if (!p->exec) {
       // generic path: `body:` chains compiled for sm_100a with NVRTC
       std::string jwhy;
-      p->jit = lfx::JitKernel::build(p->plan, jwhy);
+      p->jit = lfx::JitKernel::build(p->plan, jwhy,
+                                     kernel_source ? std::string(kernel_source, kernel_len) : std::string());
       if (!p->jit) p->unsupported = why + "; generic executor: " + jwhy;
     }
     *out = p;

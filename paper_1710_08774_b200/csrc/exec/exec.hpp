@@ -43,6 +43,8 @@ const std::vector<Executor>& executors();
 
 // embedded spec text by file name ("" if unknown); generated at build time
 const char* embedded_spec(const char* file);
+// the shipped user-kernel headers (userkernels/*.h), concatenated
+const std::string& embedded_userkernels();
 
 // helpers shared by the executors
 int cuda_status(cudaError_t e, const char* what, std::string& err);

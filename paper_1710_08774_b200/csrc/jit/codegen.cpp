@@ -18,7 +18,9 @@
 // Ghost refill of iterated goals (`config: boundary:`) is a second kernel that
 // visits ghost cells only.
 #include <algorithm>
+#include <cctype>
 #include <climits>
+#include <functional>
 #include <cstdio>
 #include <cstdlib>
 #include <deque>
@@ -66,6 +68,7 @@ struct Grp {
 // everything the emitters share
 struct Ctx {
   const lf::Plan& P;
+  std::string sources;  // user-kernel sources the generated code is compiled with
   int nd = 0;
   std::string T;
   std::vector<long> N;
@@ -111,6 +114,91 @@ struct Ctx {
     return ti;
   }
 };
+
+// Kernel evaluation: a `body:` expression per output (R/SPEC.md:82), or a
+// call of the function the declaration names (R/PAPER.md:58-62: value
+// inputs, outputs by pointer or reference), found in the shipped user-kernel
+// headers or in the caller's kernel source.  in(param) is the C expression of
+// an input; out(param) the variable an output lands in -- declared here when
+// `declare`, assigned otherwise.
+bool has_function(const std::string& sources, const std::string& fn) {
+  if (fn.empty()) return false;
+  size_t pos = 0;
+  while ((pos = sources.find(fn, pos)) != std::string::npos) {
+    const bool left_ok = pos == 0 || !(std::isalnum(static_cast<unsigned char>(sources[pos - 1])) || sources[pos - 1] == '_');
+    size_t e = pos + fn.size();
+    while (e < sources.size() && std::isspace(static_cast<unsigned char>(sources[e]))) ++e;
+    if (left_ok && e < sources.size() && sources[e] == '(') return true;
+    pos += fn.size();
+  }
+  return false;
+}
+
+bool kernel_evaluable(const lf::KernelRule& k, const std::string& sources, std::string& why) {
+  bool bodies = true;
+  for (const auto& [op, pat] : k.outputs) bodies &= k.bodies.count(op) > 0;
+  if (bodies) return true;
+  const lf::DeclInfo di = lf::parse_declaration(k.declaration);
+  if (has_function(sources, di.function)) return true;
+  why = "kernel '" + k.name + "' has no `body:` and its function '" + di.function +
+        "' is neither a shipped user kernel nor in the kernel source given to the plan";
+  return false;
+}
+
+bool emit_kernel(const lf::KernelRule& k, const std::string& T, const std::function<std::string(const std::string&)>& in,
+                 const std::function<std::string(const std::string&)>& out, bool declare, std::ostream& src,
+                 const std::string& ind, std::string& err) {
+  bool bodies = true;
+  for (const auto& [op, pat] : k.outputs) bodies &= k.bodies.count(op) > 0;
+  std::set<std::string> inputs;
+  for (const auto& [ip, pat] : k.inputs) inputs.insert(ip);
+  if (bodies) {
+    for (const auto& [op, pat] : k.outputs) {
+      std::string e2;
+      auto e = lf::parse_expr(k.bodies.at(op), e2);
+      if (!e) {
+        err = "kernel '" + k.name + "' body of '" + op + "': " + e2;
+        return false;
+      }
+      std::set<std::string> used;
+      lf::expr_vars(*e, used);
+      for (const auto& u : used)
+        if (!inputs.count(u)) {
+          err = "kernel '" + k.name + "' body of '" + op + "' uses unknown name '" + u + "'";
+          return false;
+        }
+      src << ind << (declare ? "const T " : "") << out(op) << " = " << lf::emit_c(*e, T, in) << ";\n";
+    }
+    return true;
+  }
+  const lf::DeclInfo di = lf::parse_declaration(k.declaration);
+  std::set<std::string> outputs;
+  for (const auto& [op, pat] : k.outputs) outputs.insert(op);
+  std::string args;
+  std::vector<std::pair<std::string, std::string>> tmps;  // (temp, destination)
+  for (const auto& prm : di.params) {
+    std::string a;
+    if (outputs.count(prm.name)) {
+      const std::string tmp = "lf_o_" + prm.name;
+      tmps.emplace_back(tmp, out(prm.name));
+      a = prm.pointer ? "&" + tmp : tmp;
+    } else if (inputs.count(prm.name)) {
+      a = in(prm.name);
+    } else {
+      err = "kernel '" + k.name + "': declaration parameter '" + prm.name + "' is neither an input nor an output";
+      return false;
+    }
+    args += (args.empty() ? "" : ", ") + a;
+  }
+  if (declare)
+    for (const auto& [tmp, dst] : tmps) src << ind << "T " << dst << ";\n";
+  src << ind << "{\n";
+  for (const auto& [tmp, dst] : tmps) src << ind << "  T " << tmp << ";\n";
+  src << ind << "  " << di.function << "(" << args << ");\n";
+  for (const auto& [tmp, dst] : tmps) src << ind << "  " << dst << " = " << tmp << ";\n";
+  src << ind << "}\n";
+  return true;
+}
 
 bool analyse(Ctx& C) {
   const lf::Plan& P = C.P;
@@ -214,10 +302,8 @@ bool analyse(Ctx& C) {
     if (cg.kind != lf::RapKind::kernel) continue;
     const auto& k = rs.kernels[cg.kernel];
     if (k.associative) return fail("associative kernels need the reduction path (not in the generic executor)");
-    for (const auto& [op, pat] : k.outputs)
-      if (!k.bodies.count(op))
-        return fail("kernel '" + k.name + "' has no body for output '" + op +
-                    "' (the generic executor compiles `body:` expressions)");
+    std::string why;
+    if (!kernel_evaluable(k, C.sources, why)) return fail(why);
     const lf::Rap& rep = g.raps[cg.members[0]];
     std::vector<int> anchor(nd, 0);
     for (const auto& o : g.terms[rep.out_terms[0]].dims) anchor[o.dim] = o.offset;
@@ -273,24 +359,12 @@ bool analyse(Ctx& C) {
 // body expressions of group G's outputs, p_<param> bound to its inputs
 bool emit_bodies(Ctx& C, const Grp& G, std::ostream& src, const char* ind) {
   const auto& k = C.P.rs.kernels[G.kernel];
-  std::map<std::string, std::string> pv;
-  for (const auto& in : G.in) pv[in.param] = "p_" + in.param;
-  for (const auto& o : G.out) {
-    std::string err;
-    auto e = lf::parse_expr(k.bodies.at(o.param), err);
-    if (!e) {
-      C.error = "kernel '" + k.name + "' body of '" + o.param + "': " + err;
-      return false;
-    }
-    std::set<std::string> used;
-    lf::expr_vars(*e, used);
-    for (const auto& u : used)
-      if (!pv.count(u)) {
-        C.error = "kernel '" + k.name + "' body of '" + o.param + "' uses unknown name '" + u + "'";
-        return false;
-      }
-    src << ind << "const T q_" << o.param << " = "
-        << lf::emit_c(*e, C.T, [&](const std::string& n) { return pv.at(n); }) << ";\n";
+  std::string err;
+  if (!emit_kernel(
+          k, C.T, [](const std::string& n) { return "p_" + n; }, [](const std::string& n) { return "q_" + n; }, true,
+          src, ind, err)) {
+    C.error = err;
+    return false;
   }
   return true;
 }
@@ -966,7 +1040,7 @@ bool emit_fill(Ctx& C, JitProgram& out, std::ostream& fill) {
 // accumulation runs in element order, so the result equals run_naive's
 // sequential sweep bit for bit (no reassociation needed).
 // ---------------------------------------------------------------------------
-bool emit_nests(const lf::Plan& P, JitProgram& out, std::ostream& src, std::string& err) {
+bool emit_nests(const lf::Plan& P, const std::string& sources, JitProgram& out, std::ostream& src, std::string& err) {
   const auto& rs = P.rs;
   const auto& g = P.dag;
   const int nd = static_cast<int>(rs.loop_order.size());
@@ -1011,11 +1085,8 @@ bool emit_nests(const lf::Plan& P, JitProgram& out, std::ostream& src, std::stri
   };
   for (int r = 0; r < nr; ++r)
     if (g.raps[r].kind == lf::RapKind::kernel) {
-      const auto& k = rs.kernels[g.raps[r].kernel];
-      for (const auto& [op, pat] : k.outputs)
-        if (!k.bodies.count(op))
-          return fail("kernel '" + k.name + "' has no body for output '" + op +
-                      "' (the generic executor compiles `body:` expressions)");
+      std::string why;
+      if (!kernel_evaluable(rs.kernels[g.raps[r].kernel], sources, why)) return fail(why);
     }
   // ---- nests in dataflow order (kernel and store raps; loads go where read)
   std::set<int> nest_ids;
@@ -1164,27 +1235,16 @@ bool emit_nests(const lf::Plan& P, JitProgram& out, std::ostream& src, std::stri
     } else {
       const auto& k = rs.kernels[rap.kernel];
       for (int t : rap.in_terms) need(t);
-      for (size_t i = 0; i < k.outputs.size(); ++i) {
-        std::string e2;
-        auto e = lf::parse_expr(k.bodies.at(k.outputs[i].first), e2);
-        if (!e) {
-          okk = false;
-          err = "kernel '" + k.name + "': " + e2;
-          return;
-        }
-        std::map<std::string, std::string> pv;
-        for (size_t j = 0; j < k.inputs.size(); ++j) pv[k.inputs[j].first] = "v" + std::to_string(rap.in_terms[j]);
-        std::set<std::string> used;
-        lf::expr_vars(*e, used);
-        for (const auto& u : used)
-          if (!pv.count(u)) {
-            okk = false;
-            err = "kernel '" + k.name + "' body uses unknown name '" + u + "'";
-            return;
-          }
-        const int t = rap.out_terms[i];
-        o << ind << "const T v" << t << " = " << lf::emit_c(*e, T, [&](const std::string& n) { return pv.at(n); })
-          << ";\n";
+      std::map<std::string, std::string> pv, ov;
+      for (size_t j = 0; j < k.inputs.size(); ++j) pv[k.inputs[j].first] = "v" + std::to_string(rap.in_terms[j]);
+      for (size_t j = 0; j < k.outputs.size(); ++j) ov[k.outputs[j].first] = "v" + std::to_string(rap.out_terms[j]);
+      if (!emit_kernel(
+              k, T, [&](const std::string& n) { return pv.at(n); }, [&](const std::string& n) { return ov.at(n); },
+              true, o, ind, err)) {
+        okk = false;
+        return;
+      }
+      for (int t : rap.out_terms) {
         done[t] = 1;
         if (term_mat[t]) o << ind << G << mat_index(t) << " = v" << t << ";\n";
       }
@@ -1358,15 +1418,15 @@ bool emit_nests(const lf::Plan& P, JitProgram& out, std::ostream& src, std::stri
       for (size_t m = 0; m < reds.size(); ++m) {
         const auto& rap = g.raps[reds[m]];
         const auto& k = rs.kernels[rap.kernel];
-        std::string e2;
-        auto e = lf::parse_expr(k.bodies.at(k.outputs[0].first), e2);
-        if (!e) return fail("kernel '" + k.name + "': " + e2);
         std::map<std::string, std::string> pv;
         for (size_t i = 0; i < k.inputs.size(); ++i) {
           const bool is_elem = std::find(elem_in[m].begin(), elem_in[m].end(), (int)i) != elem_in[m].end();
           pv[k.inputs[i].first] = is_elem ? "lf_red[warp][" + std::to_string(m) + "][e]" : "acc" + std::to_string(m);
         }
-        src << "        acc" << m << " = " << lf::emit_c(*e, T, [&](const std::string& n) { return pv.at(n); }) << ";\n";
+        if (!emit_kernel(
+                k, T, [&](const std::string& n) { return pv.at(n); },
+                [&](const std::string&) { return "acc" + std::to_string(m); }, false, src, "        ", err))
+          return false;
       }
       src << "      }\n";
       src << "      __syncwarp();\n";
@@ -1390,13 +1450,13 @@ bool emit_nests(const lf::Plan& P, JitProgram& out, std::ostream& src, std::stri
 
 }  // namespace
 
-bool jit_generate(const lf::Plan& P, JitProgram& out) {
+bool jit_generate(const lf::Plan& P, JitProgram& out, const std::string& sources) {
   bool multi = !P.one_nest;
   for (const auto& k : P.rs.kernels) multi |= k.associative;
   if (multi) {
     std::ostringstream src;
     std::string err;
-    if (!emit_nests(P, out, src, err)) {
+    if (!emit_nests(P, sources, out, src, err)) {
       out.error = err;
       return false;
     }
@@ -1410,11 +1470,12 @@ bool jit_generate(const lf::Plan& P, JitProgram& out) {
       out.error = C.error;
       return false;
     }
-    out.source = src.str();
+    out.source = sources + src.str();
     out.march = false;
     return true;
   }
   Ctx C(P);
+  C.sources = sources;
   if (!analyse(C)) {
     out.error = C.error;
     return false;
@@ -1428,7 +1489,7 @@ bool jit_generate(const lf::Plan& P, JitProgram& out) {
     out.error = C.error;
     return false;
   }
-  out.source = src.str();
+  out.source = sources + src.str();
   return true;
 }
 

@@ -87,13 +87,14 @@ const Drv& drv() {
 
 }  // namespace
 
-std::shared_ptr<JitKernel> JitKernel::build(const lf::Plan& plan, std::string& why) {
+std::shared_ptr<JitKernel> JitKernel::build(const lf::Plan& plan, std::string& why, const std::string& kernel_source) {
   auto k = std::shared_ptr<JitKernel>(new JitKernel);
   if (plan.terminals.size() > 32) {
     why = "more than 32 terminals";
     return nullptr;
   }
-  if (!jit_generate(plan, k->prog_)) {
+  const std::string sources = embedded_userkernels() + (kernel_source.empty() ? "" : "// ---- kernel source given to the plan\n" + kernel_source + "\n");
+  if (!jit_generate(plan, k->prog_, sources)) {
     why = k->prog_.error;
     return nullptr;
   }

@@ -50,7 +50,9 @@ struct JitProgram {
   std::string error;  // why the chain is not supported
 };
 
-bool jit_generate(const lf::Plan& plan, JitProgram& out);
+// `sources`: user-kernel code (the shipped headers + the caller's) prepended
+// to the generated kernels; chains may name its functions instead of bodies
+bool jit_generate(const lf::Plan& plan, JitProgram& out, const std::string& sources);
 
 // kernel argument block, passed by value; must match `struct LfArgs` in the
 // generated source (codegen.cpp)
@@ -63,7 +65,7 @@ struct JitArgs {
 // A compiled chain; owned by one plan.
 class JitKernel {
  public:
-  static std::shared_ptr<JitKernel> build(const lf::Plan& plan, std::string& why);
+  static std::shared_ptr<JitKernel> build(const lf::Plan& plan, std::string& why, const std::string& kernel_source = "");
   int run(const ExecArgs& a, std::string& err);
   const JitProgram& program() const { return prog_; }
   ~JitKernel();

@@ -195,7 +195,9 @@ def test_signature_is_name_independent_but_offset_sensitive():
     moved = text.replace("fzm : fz[k?-1][j?][i?]", "fzm : fz[k?+1][j?][i?]")
     c = lf.Plan(moved, "c")
     assert c.report()["signature"] != a.report()["signature"]
-    assert c.executor == ""
+    # not the hand-written executor's chain any more: the generic executor
+    # compiles it with the shipped user kernels
+    assert c.executor.startswith("jit_") and c.executor != a.executor
 
 
 def test_ranges_rewrite_and_size_constraints():
@@ -203,7 +205,9 @@ def test_ranges_rewrite_and_size_constraints():
     assert p.terminals[0].extent == (10, 34, 66)
     assert p.executor == "heat3d_fused_tma"
     q = lf.Plan.with_ranges("heat3d", (8, 30, 64))  # N_j not a multiple of 16
-    assert q.executor == ""
+    # outside the hand-written kernel's constraints: the generic executor
+    # compiles the same chain with the shipped user kernels
+    assert q.executor == "jit_window_fused"
 
 
 FIXTURES = ["normalization", "cosmo", "laplace3"]
