@@ -183,6 +183,7 @@ def run_naive(spec_path, axioms: dict, steps: int = 1) -> dict:
     (R/SPEC.md:532-540)."""
     d = ref_dag(spec_path)
     n = [hi - lo for lo, hi in d["ranges"]]
+    lo = [r[0] for r in d["ranges"]]
     nd = len(n)
     raps, terms, kern = d["raps"], d["terms"], d["kernels"]
     pair = {g: a for g, a in d["iterate"]}
@@ -211,7 +212,7 @@ def run_naive(spec_path, axioms: dict, steps: int = 1) -> dict:
                 ext = d["externals"][rap["external"]]["extents"]
                 sl, axes = [], []
                 for k, (dim, shift) in enumerate(rap["slots"]):
-                    start = shift - ext[k][1]
+                    start = (lo[dim] if dim >= 0 else 0) + shift - ext[k][1]
                     if dim < 0:
                         sl.append(start)  # constant subscript
                     else:
@@ -263,14 +264,14 @@ def run_naive(spec_path, axioms: dict, steps: int = 1) -> dict:
                 ext = (d["externals"][pair[g]] if g in pair else d["externals"][g])["extents"]
                 sl, axes = [], []
                 for k, (dim, shift) in enumerate(rap["slots"]):
-                    start = shift - ext[k][1]
+                    start = lo[dim] + shift - ext[k][1]
                     sl.append(slice(start, start + n[dim]))
                     axes.append(dim)
                 v = np.broadcast_to(vals[rap["in"][0]], shape_of(set(axes)))
                 a[tuple(sl)] = v.reshape([n[dim] for dim in axes])
         for g, a_name in pair.items():
             modes = d["boundary"].get(g) or d["boundary"].get("*") or ["none"]
-            base = [b for _, b in d["externals"][a_name]["extents"]]
+            base = [b - l for (_, b), l in zip(d["externals"][a_name]["extents"], lo)]  # relative to the range start
             _fill(goals[g], modes, n, base)
             cur[a_name] = goals[g]
     return goals

@@ -226,8 +226,8 @@ const Variant& variant() {
 bool supports(const lf::Plan& plan, std::string& why) {
   const auto& r = plan.rs.ranges;
   for (const auto& rg : r)
-    if (rg.stride != 1) {
-      why = "biharmonic executor needs unit strides";
+    if (rg.stride != 1 || rg.lo != 0) {
+      why = "biharmonic executor needs unit strides and ranges starting at 0";
       return false;
     }
   long nj = r[0].trips(), ni = r[1].trips();

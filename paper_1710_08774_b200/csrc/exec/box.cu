@@ -212,8 +212,8 @@ __global__ void __launch_bounds__(32, OCC)
 bool supports(const lf::Plan& plan, std::string& why) {
   const auto& r = plan.rs.ranges;
   for (const auto& rg : r)
-    if (rg.stride != 1) {
-      why = "box executor needs unit strides";
+    if (rg.stride != 1 || rg.lo != 0) {
+      why = "box executor needs unit strides and ranges starting at 0";
       return false;
     }
   long ni = r[1].trips();

@@ -420,8 +420,8 @@ bool supports(const lf::Plan& plan, std::string& why) {
   const auto& r = plan.rs.ranges;
   long nk = r[0].trips(), nj = r[1].trips(), ni = r[2].trips();
   for (const auto& rg : r)
-    if (rg.stride != 1) {
-      why = "heat3d executor needs unit strides";
+    if (rg.stride != 1 || rg.lo != 0) {
+      why = "heat3d executor needs unit strides and ranges starting at 0";
       return false;
     }
   const int TY = variant().ty;

@@ -70,6 +70,7 @@ struct Ctx {
   const lf::Plan& P;
   std::string sources;  // user-kernel sources the generated code is compiled with
   int nd = 0;
+  std::vector<long> LO;  // range lower bounds: loop index = LO + trip
   std::string T;
   std::vector<long> N;
   std::vector<std::vector<int>> vmin, vmax;  // per var, per dim: term offset range
@@ -96,7 +97,7 @@ struct Ctx {
     std::string e;
     for (size_t s = 0; s < t.dims.size(); ++s) {
       const int d = t.dims[s];
-      const long off = extra[d] - t.base[s];
+      const long off = extra[d] - t.base[s] + LO[d];
       const std::string c = "(long long)(" + pos[d] + plus(off) + ")";
       const long p = pitch(t, s);
       e += (e.empty() ? "" : " + ") + c + (p != 1 ? " * " + std::to_string(p) + "LL" : "");
@@ -232,7 +233,11 @@ bool analyse(Ctx& C) {
   C.T = T;
   C.nd = nd;
   C.N.resize(nd);
-  for (int d = 0; d < nd; ++d) C.N[d] = rs.ranges[d].trips();
+  C.LO.resize(nd);
+  for (int d = 0; d < nd; ++d) {
+    C.N[d] = rs.ranges[d].trips();
+    C.LO[d] = rs.ranges[d].lo;
+  }
 
   // ---- per-variable term offset ranges (relative to the canonical cell)
   const size_t nv = P.vars.size();
@@ -664,7 +669,7 @@ bool emit_march(Ctx& C, JitProgram& out, std::ostream& src) {
       const auto& t = C.P.terminals[ip->ai];
       const auto ex = C.extra_of(static_cast<int>(v));
       std::vector<long> so(nd);  // storage coordinate = logical + so
-      for (int d = 0; d < nd; ++d) so[d] = ex[d] - t.base[d];
+      for (int d = 0; d < nd; ++d) so[d] = ex[d] - t.base[d] + C.LO[d];
       const long E0 = t.extent[0], E1 = nd > 1 ? t.extent[1] : 1, E2 = nd > 2 ? t.extent[2] : 1;
       const long BH = C.vmax[v][0] - C.vmin[v][0];
       const std::string sy = "(long long)(y" + plus(so[0]) + ")", sx1 = "(long long)(x1" + plus(so[1]) + ")",
@@ -823,7 +828,7 @@ bool emit_march(Ctx& C, JitProgram& out, std::ostream& src) {
       const auto& t = C.P.terminals[ip.ai];
       const auto ex = C.extra_of(static_cast<int>(v));
       std::vector<long> so(nd);
-      for (int d = 0; d < nd; ++d) so[d] = ex[d] - t.base[d];
+      for (int d = 0; d < nd; ++d) so[d] = ex[d] - t.base[d] + C.LO[d];
       const long E0 = t.extent[0], E1 = nd > 1 ? t.extent[1] : 1, E2 = nd > 2 ? t.extent[2] : 1, PL = E1 * E2;
       const long BH = C.vmax[v][0] - C.vmin[v][0];
       const long BW1 = C.vmax[v][1] - C.vmin[v][1], BW2 = nd > 2 ? C.vmax[v][2] - C.vmin[v][2] : 0;
@@ -956,7 +961,7 @@ bool emit_fill(Ctx& C, JitProgram& out, std::ostream& fill) {
     out.has_fill = true;
     std::vector<long> lo(nd), hi(nd), E(nd);  // ghost widths below / above the interior, extents
     for (int d = 0; d < nd; ++d) {
-      lo[d] = -t.base[d];
+      lo[d] = C.LO[d] - t.base[d];
       E[d] = t.extent[d];
       hi[d] = E[d] - C.N[d] - lo[d];
     }
@@ -1018,8 +1023,8 @@ bool emit_fill(Ctx& C, JitProgram& out, std::ostream& fill) {
     for (int s = 0; s < nd; ++s) {
       const long p = C.pitch(t, s);
       const std::string ps = p != 1 ? " * " + std::to_string(p) + "LL" : "";
-      dst += (s ? " + " : "") + std::string("(y") + std::to_string(s) + plus(-t.base[s]) + ")" + ps;
-      srci += (s ? " + " : "") + std::string("(z") + std::to_string(s) + plus(-t.base[s]) + ")" + ps;
+      dst += (s ? " + " : "") + std::string("(y") + std::to_string(s) + plus(C.LO[s] - t.base[s]) + ")" + ps;
+      srci += (s ? " + " : "") + std::string("(z") + std::to_string(s) + plus(C.LO[s] - t.base[s]) + ")" + ps;
     }
     fill << "      b[" << dst << "] = zero ? static_cast<T>(0) : sign * b[" << srci << "];\n";
     fill << "    }\n  }\n";
@@ -1465,7 +1470,11 @@ bool jit_generate(const lf::Plan& P, JitProgram& out, const std::string& sources
     C.nd = out.nd;
     C.T = out.type;
     C.N.resize(C.nd);
-    for (int d = 0; d < C.nd; ++d) C.N[d] = P.rs.ranges[d].trips();
+    C.LO.resize(C.nd);
+    for (int d = 0; d < C.nd; ++d) {
+      C.N[d] = P.rs.ranges[d].trips();
+      C.LO[d] = P.rs.ranges[d].lo;
+    }
     if (!emit_fill(C, out, src)) {
       out.error = C.error;
       return false;

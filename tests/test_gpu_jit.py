@@ -133,3 +133,25 @@ def test_inplace_host_path():
     u = u0.copy()
     plan.run_host([u, u], steps=3)
     assert np.array_equal(bits(u), bits(oracle.biharm(u0, 3)))
+
+
+@pytest.mark.parametrize("name,shift", [("biharm_body", (3, 5)), ("heat3d_body", (2, 1, 7)),
+                                        ("normalization_body", (4, 9))])
+def test_ranges_not_starting_at_zero(name, shift, tmp_path):
+    """Loop ranges [lo, hi) with lo != 0: terminal bases move with lo
+    (buffer_extents, storage.cpp:403-427); results equal the oracle's."""
+    import re
+    text = (SPECS / f"{name}.lf").read_text()
+    dims = re.findall(r"^    (\w+): \[0, (\d+)\]$", text, flags=re.M)
+    for (d, hi), s in zip(dims, shift):
+        text = text.replace(f"    {d}: [0, {hi}]", f"    {d}: [{s}, {int(hi) + s}]")
+    path = tmp_path / f"{name}_lo.lf"
+    path.write_text(text)
+    plan = lf.Plan.from_file(path)
+    assert plan.executor.startswith("jit_")
+    ax = CASES[name]()
+    steps = 2 if name != "normalization_body" else 1
+    got = run_device(plan, [ax[t.name] for t in plan.axioms], steps)
+    ref = generic.run_naive(path, ax, steps=steps)
+    for g, t in zip(got, plan.goals):
+        assert np.array_equal(bits(g), bits(ref[t.name])), t.name
