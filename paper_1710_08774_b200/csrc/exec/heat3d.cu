@@ -188,15 +188,18 @@ __global__ void __launch_bounds__(THREADS, 2)
         // periodic ghost refill by the owners of the wrapped cells
         if (wrap_lo_i) st_hint(rowp + p.ni, o[r][0], pol);
         if (wrap_hi_i) st_hint(rowp - 1, o[r][1], pol);
-        if (p.wrap_j && (j == 0 || j == p.nj - 1)) {
-          double* gr = plane + (long long)(j == 0 ? p.nj + 1 : 0) * p.pj + 1;
-          st_hint(gr + gi0, o[r][0], pol);
-          st_hint(gr + gi0 + 32, o[r][1], pol);
-        }
-        if (p.wrap_k && (k == 0 || k == p.nk - 1)) {
-          double* gr = out + (long long)(k == 0 ? p.nk + 1 : 0) * p.pk + (long long)(j + 1) * p.pj + 1;
-          st_hint(gr + gi0, o[r][0], pol);
-          st_hint(gr + gi0 + 32, o[r][1], pol);
+        // (a single interior row / plane is the image of both ghost faces)
+        for (int side = 0; side < 2; ++side) {
+          if (p.wrap_j && j == (side ? p.nj - 1 : 0)) {
+            double* gr = plane + (long long)(side ? 0 : p.nj + 1) * p.pj + 1;
+            st_hint(gr + gi0, o[r][0], pol);
+            st_hint(gr + gi0 + 32, o[r][1], pol);
+          }
+          if (p.wrap_k && k == (side ? p.nk - 1 : 0)) {
+            double* gr = out + (long long)(side ? 0 : p.nk + 1) * p.pk + (long long)(j + 1) * p.pj + 1;
+            st_hint(gr + gi0, o[r][0], pol);
+            st_hint(gr + gi0 + 32, o[r][1], pol);
+          }
         }
       }
 #pragma unroll
@@ -363,15 +366,17 @@ __global__ void __launch_bounds__(THREADS, 2)
           st_hint(rowp + gi0 + 32, o2[1], pol);
           if (wrap_lo_i) st_hint(rowp + p.ni, o2[0], pol);
           if (wrap_hi_i) st_hint(rowp - 1, o2[1], pol);
-          if (p.wrap_j && (j == 0 || j == p.nj - 1)) {
-            double* gr = plane + (long long)(j == 0 ? p.nj + 1 : 0) * p.pj + 1;
-            st_hint(gr + gi0, o2[0], pol);
-            st_hint(gr + gi0 + 32, o2[1], pol);
-          }
-          if (p.wrap_k && (k == 0 || k == p.nk - 1)) {
-            double* gr = out + (long long)(k == 0 ? p.nk + 1 : 0) * p.pk + (long long)(j + 1) * p.pj + 1;
-            st_hint(gr + gi0, o2[0], pol);
-            st_hint(gr + gi0 + 32, o2[1], pol);
+          for (int side = 0; side < 2; ++side) {
+            if (p.wrap_j && j == (side ? p.nj - 1 : 0)) {
+              double* gr = plane + (long long)(side ? 0 : p.nj + 1) * p.pj + 1;
+              st_hint(gr + gi0, o2[0], pol);
+              st_hint(gr + gi0 + 32, o2[1], pol);
+            }
+            if (p.wrap_k && k == (side ? p.nk - 1 : 0)) {
+              double* gr = out + (long long)(side ? 0 : p.nk + 1) * p.pk + (long long)(j + 1) * p.pj + 1;
+              st_hint(gr + gi0, o2[0], pol);
+              st_hint(gr + gi0 + 32, o2[1], pol);
+            }
           }
         }
       }

@@ -1,0 +1,67 @@
+"""Degenerate grids (one or a few cells per dimension) through whichever
+executor the dispatcher picks -- bit-exact against the C oracles."""
+import numpy as np
+import pytest
+
+import oracle
+import paper_1710_08774_b200 as lf
+from paper_1710_08774_b200 import inputs
+
+pytestmark = pytest.mark.gpu
+
+
+def bits(a):
+    a = np.ascontiguousarray(a)
+    return a.view(np.uint64 if a.dtype == np.float64 else np.uint32)
+
+
+def run(plan, axioms, steps):
+    import torch
+    ax = [torch.from_numpy(np.ascontiguousarray(a)).cuda() for a in axioms]
+    dt = {8: torch.float64, 4: torch.float32}
+    goals = [torch.full(t.extent, float("nan"), dtype=dt[t.elem_bytes], device="cuda") for t in plan.goals]
+    plan.run(ax + goals, steps=steps)
+    torch.cuda.synchronize()
+    return [g.cpu().numpy() for g in goals]
+
+
+def inner(a, h):
+    return a[tuple(slice(h, -h) for _ in range(a.ndim))]
+
+
+@pytest.mark.parametrize("shape", [(1, 1), (1, 7), (5, 1), (2, 3)])
+def test_biharm_tiny(shape):
+    plan = lf.Plan.with_ranges("biharmonic2d", shape)
+    assert plan.executor
+    u = inputs.biharm_input(*shape, seed=1)
+    (got,) = run(plan, [u], 3)
+    assert np.array_equal(bits(got), bits(oracle.biharm(u, 3)))
+
+
+@pytest.mark.parametrize("shape", [(1, 1, 1), (2, 3, 5), (1, 16, 64)])
+def test_heat3d_tiny(shape):
+    plan = lf.Plan.with_ranges("heat3d", shape)
+    assert plan.executor
+    u = inputs.heat3d_input(*shape, seed=2, sigma=1.0)
+    (got,) = run(plan, [u], 3)
+    assert np.array_equal(bits(inner(got, 1)), bits(inner(oracle.heat3d(u, 3), 1)))
+
+
+@pytest.mark.parametrize("shape", [(1, 1), (3, 7), (2, 128)])
+def test_box_tiny(shape):
+    plan = lf.Plan.with_ranges("box2x", shape)
+    assert plan.executor
+    img = inputs.box_input(*shape, seed=3)
+    (got,) = run(plan, [img], 1)
+    assert np.array_equal(bits(got), bits(oracle.box(img)))
+
+
+@pytest.mark.parametrize("shape", [(2, 3), (4, 5), (1, 9)])
+def test_hydro_tiny(shape):
+    plan = lf.Plan.with_ranges("hydro2d", shape)
+    assert plan.executor
+    st, dtdx = inputs.hydro_input(*shape, seed=4)
+    got = run(plan, st + [np.array([dtdx])], 2)
+    ref = oracle.hydro(st, dtdx, 2)
+    for v in range(4):
+        assert np.array_equal(bits(inner(got[v], 2)), bits(inner(ref[v], 2))), v
