@@ -65,3 +65,30 @@ def test_hydro_tiny(shape):
     ref = oracle.hydro(st, dtdx, 2)
     for v in range(4):
         assert np.array_equal(bits(inner(got[v], 2)), bits(inner(ref[v], 2))), v
+
+
+SPECS = lf.PKG_DIR.parent / "tests" / "specs"
+
+
+@pytest.mark.parametrize("name,shape", [("laplace3_body", (1,)), ("laplace3_body", (2,)), ("laplace3_body", (1025,)),
+                                        ("biharm_body", (1, 1)), ("heat3d_body", (1, 2, 3)),
+                                        ("normalization_body", (1, 1)), ("normalization_body", (3, 33)),
+                                        ("colsum_body", (1, 5)), ("multi_body", (1, 3))])
+def test_generic_tiny(name, shape):
+    from oracle import generic
+    text = lf.set_ranges((SPECS / f"{name}.lf").read_text(), shape)
+    path = SPECS / f"_tiny_{name}_{'x'.join(map(str, shape))}.lf"
+    path.write_text(text)
+    try:
+        plan = lf.Plan(text, path.name)
+        assert plan.executor.startswith("jit_")
+        rng = np.random.default_rng(5)
+        ax = {}
+        for t in plan.axioms:
+            ax[t.name] = rng.random(t.extent) if t.extent else np.array([0.5])
+        got = run(plan, [ax[t.name] for t in plan.axioms], 1)
+        ref = generic.run_naive(path, ax, steps=1)
+    finally:
+        path.unlink()
+    for g, t in zip(got, plan.goals):
+        assert np.array_equal(bits(g), bits(ref[t.name])), t.name
