@@ -131,6 +131,17 @@ def measured_fp64_peak():
     return out.value
 
 
+def ncu_pipe(workload):
+    """fp64-pipe and issue-slot utilisation of the kernel from its committed ncu summary"""
+    p = ROOT / "profiles" / f"r01_{workload}_ncu.json"
+    if not p.exists():
+        return None
+    d = json.loads(p.read_text())
+    return {"fp64_pipe_pct": d.get("sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active"),
+            "issue_active_pct": d.get("sm__issue_active.avg.pct_of_peak_sustained_elapsed"),
+            "source": f"profiles/{p.name} (ncu --set full)"}
+
+
 def ncu_traffic(workload):
     """DRAM bytes per launch from the committed ncu summary, if any."""
     p = ROOT / "profiles" / "traffic.json"
@@ -423,7 +434,10 @@ def main():
                     "peak_source": "measured live (tools/fp64_probe.cu: DFMA chains)",
                     "algorithmic_flops_per_cell_step": HYDRO_FLOPS_PER_CELL_STEP,
                     "hbm": {"achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                            "algorithmic_bytes_per_cell": bpc, "peak_source": peak_src}}
+                            "algorithmic_bytes_per_cell": bpc, "peak_source": peak_src},
+                    # each division / square root is ~10 fp64-pipe instructions: the
+                    # pipe itself is far busier than the algorithmic-flop fraction
+                    "pipe": ncu_pipe("hydro")}
 
     line = {
         "metric": metric, "value": value, "unit": "cell-updates/s", "n_gpus": world, "steps": args.steps,
