@@ -239,32 +239,51 @@ constexpr int APLANE = AX * AY;
 template <int S_, int KCH_>
 struct Cfg {
   static constexpr int S = S_, KCH = KCH_;
-  static constexpr int SMEM = S * STAGE_BYTES + 3 * APLANE * 8 + 2 * S * 8 + 128;
+  static constexpr int SMEM = S * STAGE_BYTES + 4 * APLANE * 8 + (3 * S + 8) * 8 + 128;
 };
 __device__ __forceinline__ int wrapn(int x, int n) { return x < 0 ? x + n : (x >= n ? x - n : x); }
 __device__ __forceinline__ void consumers_sync() { asm volatile("bar.sync 1, %0;" ::"r"(CWARPS * 32) : "memory"); }
 
+// Warp-specialised pipeline (no CTA-wide barrier): warp 8 streams input
+// planes by TMA; warps 0-3 compute first-step planes A into a 4-slot ring;
+// warps 4-7 compute the second step B from three A planes and store.
+// Barriers: full/empty (input ring, producer <-> A warps), afull/aempty
+// (A ring, A warps <-> B warps); A warps also patch the periodic images on
+// face tiles (named barrier among the four of them).
+constexpr int AW = 4, BW = 4;  // A and B warps
+constexpr int THREADS2 = (AW + BW + 2) * 32;  // + TMA producer warp + patch warp
+constexpr int ASLOTS = 4;
 template <class K>
-__global__ void __launch_bounds__(THREADS, 2)
+__global__ void __launch_bounds__(THREADS2, 2)
     heat3d_fused2(const __grid_constant__ CUtensorMap tin, const double* __restrict__ in, double* __restrict__ out,
                   const Params p) {
   constexpr int S = K::S;
   extern __shared__ __align__(128) unsigned char smem[];
   unsigned char* ring = smem;
   double* aring = reinterpret_cast<double*>(smem + S * STAGE_BYTES);
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + S * STAGE_BYTES + 3 * APLANE * 8);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + S * STAGE_BYTES + ASLOTS * APLANE * 8);
   uint64_t* empty = full + S;
+  uint64_t* afull = empty + S;
+  uint64_t* aempty = afull + ASLOTS;
+  uint64_t* pfull = aempty + ASLOTS;  // stage landed and (face tiles) patched
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], CWARPS);
+      mbar_init(&empty[s], AW);
     }
+    for (int s = 0; s < ASLOTS; ++s) {
+      mbar_init(&afull[s], AW);
+      mbar_init(&aempty[s], BW);
+    }
+    for (int s = 0; s < S; ++s) mbar_init(&pfull[s], 1);
     fence_barrier_init();
   }
   __syncthreads();
-  if (warp == CWARPS) {
-    // ---------------- producer: input planes k0-2 .. k0+kc+1, wrapped along k
+  auto stage = [&](int g) { return reinterpret_cast<double*>(ring + (g % S) * STAGE_BYTES); };
+  if (warp == AW + BW) {
+    // ---------------- producer warp: streams input planes k0-2 .. k0+kc+1
+    // (wrapped along k) by TMA, as far ahead as the ring allows
     if (lane == 0) {
       tma_prefetch_desc(&tin);
       int g = 0;
@@ -282,113 +301,214 @@ __global__ void __launch_bounds__(THREADS, 2)
     }
     return;
   }
-  const int tid = threadIdx.x;
-  const uint64_t pol = l2_evict_first_policy();
-  auto stage = [&](int g) { return reinterpret_cast<double*>(ring + (g % S) * STAGE_BYTES); };
-  int g = 0;
-  for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
-    const Unit w = unit_of<TY>(p, u);
-    const bool face = p.patch && (w.i0 == 0 || w.i0 + TX == p.ni || w.j0 == 0 || w.j0 + TY == p.nj);
-    const int gi0 = w.i0 + lane;
-    const bool wrap_lo_i = p.wrap_i && gi0 == 0;
-    const bool wrap_hi_i = p.wrap_i && gi0 + 32 == p.ni - 1;
-    for (int t = 0; t < w.kc + 4; ++t) {
-      const int gt = g + t;
-      mbar_wait(&full[gt % S], (gt / S) & 1);
-      if (face) {
-        // periodic images for the staged cells outside the domain
-        double* st = stage(gt);
-        const int kk = wrapn(w.k0 - 2 + t, p.nk);
-        for (int e = tid; e < LDI * RI; e += CWARPS * 32) {
-          const int r = e / LDI, c = e - r * LDI;
-          const int i = w.i0 - 3 + c, j = w.j0 - 2 + r;
-          if (i < 0 || i >= p.ni || j < 0 || j >= p.nj)
-            st[e] = in[(long long)(kk + 1) * p.pk + (long long)(wrapn(j, p.nj) + 1) * p.pj + wrapn(i, p.ni) + 1];
+  if (warp == AW + BW + 1) {
+    // ---------------- patch warp: publishes each landed plane on pfull, after
+    // replacing (on face tiles) the staged cells outside the domain by their
+    // periodic images -- so the patch's global loads stay off the A warps
+    int g = 0;
+    for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
+      const Unit w = unit_of<TY>(p, u);
+      const bool lo_i = w.i0 == 0, hi_i = w.i0 + TX == p.ni, lo_j = w.j0 == 0, hi_j = w.j0 + TY == p.nj;
+      const bool face = p.patch && (lo_i || hi_i || lo_j || hi_j);
+      for (int q = 0; q < w.kc + 4; ++q, ++g) {
+        const int slot = g % S;
+        mbar_wait(&full[slot], (g / S) & 1);
+        if (face) {
+          double* st = stage(g);
+          const long long kp = (long long)(wrapn(w.k0 - 2 + q, p.nk) + 1) * p.pk;
+          auto src = [&](int r, int c) {
+            const int i = w.i0 - 3 + c, j = w.j0 - 2 + r;
+            return __ldg(in + kp + (long long)(wrapn(j, p.nj) + 1) * p.pj + wrapn(i, p.ni) + 1);
+          };
+          // rows outside in j (two per face), columns outside in i (three per
+          // face): every load issued before any store, one latency per plane
+          constexpr int MR = (2 * LDI + 31) / 32, MC = (3 * RI + 31) / 32;
+          double vr[2][MR], vc[2][MC];
+#pragma unroll
+          for (int m = 0; m < MR; ++m) {
+            const int e = lane + 32 * m;
+            if (e < 2 * LDI) {
+              if (lo_j) vr[0][m] = src(e / LDI, e % LDI);
+              if (hi_j) vr[1][m] = src(RI - 2 + e / LDI, e % LDI);
+            }
+          }
+#pragma unroll
+          for (int m = 0; m < MC; ++m) {
+            const int e = lane + 32 * m;
+            if (e < 3 * RI) {
+              if (lo_i) vc[0][m] = src(e % RI, e / RI);
+              if (hi_i) vc[1][m] = src(e % RI, LDI - 3 + e / RI);
+            }
+          }
+#pragma unroll
+          for (int m = 0; m < MR; ++m) {
+            const int e = lane + 32 * m;
+            if (e < 2 * LDI) {
+              if (lo_j) st[(e / LDI) * LDI + e % LDI] = vr[0][m];
+              if (hi_j) st[(RI - 2 + e / LDI) * LDI + e % LDI] = vr[1][m];
+            }
+          }
+#pragma unroll
+          for (int m = 0; m < MC; ++m) {
+            const int e = lane + 32 * m;
+            if (e < 3 * RI) {
+              if (lo_i) st[(e % RI) * LDI + e / RI] = vc[0][m];
+              if (hi_i) st[(e % RI) * LDI + LDI - 3 + e / RI] = vc[1][m];
+            }
+          }
+          fence_proxy_async();  // generic writes before the slot's next TMA refill
         }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&pfull[slot]);
       }
-      consumers_sync();  // stage t complete (and patched); B of the last trip done with its A slot
-      if (t >= 2) {
-        // ---- A at input plane t-1 (logical k0-3+t) on the 66 x 18 ring tile
-        const double* sm = stage(gt - 2);
-        const double* sc = stage(gt - 1);
-        const double* sp = stage(gt);
-        double* ao = aring + ((t - 1) % 3) * APLANE;
-        for (int e = tid; e < APLANE; e += CWARPS * 32) {
-          const int b = e / AX, a = e - b * AX;
-          const int o = (b + 1) * LDI + a + 2;
-          const double uc = sc[o];
+    }
+    return;
+  }
+  int gi = 0, ga = 0;  // running input-plane and A-plane counters
+  if (warp < AW) {
+    // ---------------- A warps: first step on the 66 x 18 ring tile.  Thread
+    // t owns cells t + 128 m for the whole unit: the k-1 and k centres stay in
+    // registers, so a plane costs one centre + four in-plane loads per cell.
+    constexpr int MA = (APLANE + AW * 32 - 1) / (AW * 32);
+    const int tid = threadIdx.x;  // 0..127
+    auto off = [&](int m) {
+      const int e = min(tid + AW * 32 * m, APLANE - 1);
+      const int bb = e / AX, aa = e - bb * AX;
+      return (bb + 1) * LDI + aa + 2;
+    };
+    for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
+      const Unit w = unit_of<TY>(p, u);
+      double pv[MA], cv[MA];  // centres of input planes q-2, q-1
+      for (int q = 0; q < w.kc + 4; ++q) {
+        const int g = gi + q;
+        mbar_wait(&pfull[g % S], (g / S) & 1);
+        const double* sq = stage(g);
+        if (q < 2) {
+#pragma unroll
+          for (int m = 0; m < MA; ++m) (q == 0 ? pv : cv)[m] = sq[off(m)];
+          if (q == 0) {  // plane 0 lives on in registers only
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[g % S]);
+          }
+          continue;
+        }
+        // A(q-1) from planes q-2 (registers), q-1 (centres + in-plane), q (centres)
+        const int ai = ga + q - 2;
+        if (ai >= ASLOTS) mbar_wait(&aempty[ai % ASLOTS], ((ai / ASLOTS) & 1) ^ 1);
+        const double* sc = stage(g - 1);
+        double* ao = aring + (ai % ASLOTS) * APLANE;
+#pragma unroll
+        for (int m = 0; m < MA; ++m) {
+          const int e = tid + AW * 32 * m;
+          const int o = off(m);
+          const double uc = cv[m], up = sq[o];
           double fxp, fxm, fyp, fym, fzp, fzm, r;
           face_flux(sc[o + 1], uc, &fxp);
           face_flux(uc, sc[o - 1], &fxm);
           face_flux(sc[o + LDI], uc, &fyp);
           face_flux(uc, sc[o - LDI], &fym);
-          face_flux(sp[o], uc, &fzp);
-          face_flux(uc, sm[o], &fzm);
+          face_flux(up, uc, &fzp);
+          face_flux(uc, pv[m], &fzm);
           heat_divupd(uc, fxp, fxm, fyp, fym, fzp, fzm, &r);
-          ao[e] = r;
+          if (e < APLANE) ao[e] = r;
+          pv[m] = uc;
+          cv[m] = up;
         }
-        // input plane t-2 is no longer needed (A at t needs t-1, t, t+1);
-        // patched cells were written by the generic proxy: order them before
-        // the TMA refill of the slot
-        if (face) fence_proxy_async();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[(gt - 2) % S]);
-        consumers_sync();  // A plane t-1 complete
+        if (lane == 0) {
+          mbar_arrive(&afull[ai % ASLOTS]);
+          mbar_arrive(&empty[(g - 1) % S]);  // plane q-1's in-plane reads are done
+        }
       }
-      if (t >= 4) {
-        // ---- B at plane k = k0-4+t from A planes t-3, t-2, t-1
-        const double* am = aring + ((t - 3) % 3) * APLANE;
-        const double* ac = aring + ((t - 2) % 3) * APLANE;
-        const double* ap = aring + ((t - 1) % 3) * APLANE;
-        const int k = w.k0 - 4 + t;
-        double* plane = out + (long long)(k + 1) * p.pk;
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[(gi + w.kc + 3) % S]);
+      gi += w.kc + 4;
+      ga += w.kc + 2;
+    }
+    return;
+  }
+  // ---------------- B warps: second step on the 64 x 16 tile, 4 rows x 2
+  // cells per lane; the A(q-1) and A(q) centres of the lane's cells stay in
+  // registers
+  const int wb = warp - AW;
+  const uint64_t pol = l2_evict_first_policy();
+  for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
+    const Unit w = unit_of<TY>(p, u);
+    const int gi0 = w.i0 + lane;
+    const bool wrap_lo_i = p.wrap_i && gi0 == 0;
+    const bool wrap_hi_i = p.wrap_i && gi0 + 32 == p.ni - 1;
+    double am[4][2], ac[4][2];
+    for (int q = 2; q <= w.kc + 1; ++q) {
+      // B(q) from A(q-1), A(q), A(q+1) = A-ring indices ga+q-2, ga+q-1, ga+q
+      const int a0 = ga + q - 2;
+      if (q == 2) {
+        for (int d = 0; d < 2; ++d) mbar_wait(&afull[(a0 + d) % ASLOTS], ((a0 + d) / ASLOTS) & 1);
+        const double* s0 = aring + (a0 % ASLOTS) * APLANE;
+        const double* s1 = aring + ((a0 + 1) % ASLOTS) * APLANE;
 #pragma unroll
-        for (int rr = 0; rr < 2; ++rr) {
-          const int y = 2 * warp + rr;
-          const int j = w.j0 + y;
-          double o2[2];
+        for (int rr = 0; rr < 4; ++rr)
 #pragma unroll
           for (int c = 0; c < 2; ++c) {
-            const int x = lane + 32 * c;
-            const int o = (y + 1) * AX + x + 1;
-            const double uc = ac[o];
-            double fxp, fxm, fyp, fym, fzp, fzm;
-            face_flux(ac[o + 1], uc, &fxp);
-            face_flux(uc, ac[o - 1], &fxm);
-            face_flux(ac[o + AX], uc, &fyp);
-            face_flux(uc, ac[o - AX], &fym);
-            face_flux(ap[o], uc, &fzp);
-            face_flux(uc, am[o], &fzm);
-            heat_divupd(uc, fxp, fxm, fyp, fym, fzp, fzm, &o2[c]);
+            const int o = (4 * wb + rr + 1) * AX + lane + 32 * c + 1;
+            am[rr][c] = s0[o];
+            ac[rr][c] = s1[o];
           }
-          double* rowp = plane + (long long)(j + 1) * p.pj + 1;
-          st_hint(rowp + gi0, o2[0], pol);
-          st_hint(rowp + gi0 + 32, o2[1], pol);
-          if (wrap_lo_i) st_hint(rowp + p.ni, o2[0], pol);
-          if (wrap_hi_i) st_hint(rowp - 1, o2[1], pol);
-          for (int side = 0; side < 2; ++side) {
-            if (p.wrap_j && j == (side ? p.nj - 1 : 0)) {
-              double* gr = plane + (long long)(side ? 0 : p.nj + 1) * p.pj + 1;
-              st_hint(gr + gi0, o2[0], pol);
-              st_hint(gr + gi0 + 32, o2[1], pol);
-            }
-            if (p.wrap_k && k == (side ? p.nk - 1 : 0)) {
-              double* gr = out + (long long)(side ? 0 : p.nk + 1) * p.pk + (long long)(j + 1) * p.pj + 1;
-              st_hint(gr + gi0, o2[0], pol);
-              st_hint(gr + gi0 + 32, o2[1], pol);
-            }
+      }
+      mbar_wait(&afull[(a0 + 2) % ASLOTS], ((a0 + 2) / ASLOTS) & 1);
+      const double* sc = aring + ((a0 + 1) % ASLOTS) * APLANE;
+      const double* sp = aring + ((a0 + 2) % ASLOTS) * APLANE;
+      const int k = w.k0 - 2 + q;
+      double o2[4][2];
+#pragma unroll
+      for (int rr = 0; rr < 4; ++rr)
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          const int o = (4 * wb + rr + 1) * AX + lane + 32 * c + 1;
+          const double uc = ac[rr][c], up = sp[o];
+          double fxp, fxm, fyp, fym, fzp, fzm;
+          face_flux(sc[o + 1], uc, &fxp);
+          face_flux(uc, sc[o - 1], &fxm);
+          face_flux(sc[o + AX], uc, &fyp);
+          face_flux(uc, sc[o - AX], &fym);
+          face_flux(up, uc, &fzp);
+          face_flux(uc, am[rr][c], &fzm);
+          heat_divupd(uc, fxp, fxm, fyp, fym, fzp, fzm, &o2[rr][c]);
+          am[rr][c] = uc;
+          ac[rr][c] = up;
+        }
+      // A(q-1) lives on in registers only
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&aempty[a0 % ASLOTS]);
+      double* plane = out + (long long)(k + 1) * p.pk;
+#pragma unroll
+      for (int rr = 0; rr < 4; ++rr) {
+        const int j = w.j0 + 4 * wb + rr;
+        double* rowp = plane + (long long)(j + 1) * p.pj + 1;
+        st_hint(rowp + gi0, o2[rr][0], pol);
+        st_hint(rowp + gi0 + 32, o2[rr][1], pol);
+        if (wrap_lo_i) st_hint(rowp + p.ni, o2[rr][0], pol);
+        if (wrap_hi_i) st_hint(rowp - 1, o2[rr][1], pol);
+        for (int side = 0; side < 2; ++side) {
+          if (p.wrap_j && j == (side ? p.nj - 1 : 0)) {
+            double* gr = plane + (long long)(side ? 0 : p.nj + 1) * p.pj + 1;
+            st_hint(gr + gi0, o2[rr][0], pol);
+            st_hint(gr + gi0 + 32, o2[rr][1], pol);
+          }
+          if (p.wrap_k && k == (side ? p.nk - 1 : 0)) {
+            double* gr = out + (long long)(side ? 0 : p.nk + 1) * p.pk + (long long)(j + 1) * p.pj + 1;
+            st_hint(gr + gi0, o2[rr][0], pol);
+            st_hint(gr + gi0 + 32, o2[rr][1], pol);
           }
         }
       }
     }
-    // the unit's last two input planes were only read by the last A plane
-    if (face) fence_proxy_async();
+    // the unit's last two A planes were only read by its last B planes
     __syncwarp();
     if (lane == 0) {
-      mbar_arrive(&empty[(g + w.kc + 2) % S]);
-      mbar_arrive(&empty[(g + w.kc + 3) % S]);
+      mbar_arrive(&aempty[(ga + w.kc) % ASLOTS]);
+      mbar_arrive(&aempty[(ga + w.kc + 1) % ASLOTS]);
     }
-    g += w.kc + 4;
+    ga += w.kc + 2;
   }
 }
 }  // namespace tb
@@ -484,26 +604,27 @@ int launch_step(const double* in, double* out, int ni, int nj, int nk, int k_lo,
 
 // two steps per pass (whole periodic domain only: a slab's k ghosts come from
 // the caller's one-plane halo exchange)
-using TB = tb::Cfg<6, 32>;
 
-// opt-in (LF_HEAT3D_TB=1): measured slower than the single-step kernel this
-// round (188 vs 367 G cell-updates/s at 512^3: the periodic-image patching on
-// face tiles and two CTA barriers per plane dominate)
+// opt-in (LF_HEAT3D_TB=1): 382 vs 367 G cell-updates/s for the single-step
+// kernel at 512^3 -- within a few percent, because the pass is bound by
+// shared-memory traffic and latency rather than by the HBM bytes it saves
+//
 bool tb_enabled(int ni, int nj, int nk) {
   const char* e = std::getenv("LF_HEAT3D_TB");
   const bool on = e && std::atoi(e) != 0;
   return on && ni % TX == 0 && nj % tb::TY == 0 && nk >= 2 && ni >= TX && nj >= tb::TY;
 }
 
-int launch_pair(const double* in, double* out, int ni, int nj, int nk, cudaStream_t st, std::string& err) {
+template <class K>
+int launch_pair_k(const double* in, double* out, int ni, int nj, int nk, cudaStream_t st, std::string& err) {
   static int slots = 0;
   if (!slots) {
-    cudaError_t e = cudaFuncSetAttribute(tb::heat3d_fused2<TB>, cudaFuncAttributeMaxDynamicSharedMemorySize, TB::SMEM);
+    cudaError_t e = cudaFuncSetAttribute(tb::heat3d_fused2<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, K::SMEM);
     if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(heat3d pair)", err);
     int dev = 0, sms = 148, per_sm = 1;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tb::heat3d_fused2<TB>, THREADS, TB::SMEM);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tb::heat3d_fused2<K>, tb::THREADS2, K::SMEM);
     slots = sms * std::max(per_sm, 1);
   }
   CUtensorMap map;
@@ -520,13 +641,24 @@ int launch_pair(const double* in, double* out, int ni, int nj, int nk, cudaStrea
   p.tiles = (ni / TX) * (nj / tb::TY);
   p.k_lo = 0;
   p.k_hi = nk;
-  p.kchunks = std::max(1, (nk + TB::KCH - 1) / TB::KCH);
+  p.kchunks = std::max(1, (nk + K::KCH - 1) / K::KCH);
   p.units = p.tiles * p.kchunks;
   p.wrap_i = p.wrap_j = p.wrap_k = 1;
   p.patch = std::getenv("LF_HEAT3D_NOPATCH") ? 0 : 1;  // timing experiments only (wrong at the faces)
   const int ctas = std::min(p.units, slots);
-  tb::heat3d_fused2<TB><<<ctas, THREADS, TB::SMEM, st>>>(map, in, out, p);
+  tb::heat3d_fused2<K><<<ctas, tb::THREADS2, K::SMEM, st>>>(map, in, out, p);
   return cuda_status(cudaGetLastError(), "heat3d_fused2 launch", err);
+}
+
+// LF_HEAT3D_TBK: planes per work unit of the two-step pass (32 / 64 / 128; 64 measured best)
+int launch_pair(const double* in, double* out, int ni, int nj, int nk, cudaStream_t st, std::string& err) {
+  static const int kch = [] {
+    const char* e = std::getenv("LF_HEAT3D_TBK");
+    return e ? std::atoi(e) : 64;
+  }();
+  if (kch >= 128) return launch_pair_k<tb::Cfg<6, 128>>(in, out, ni, nj, nk, st, err);
+  if (kch >= 64) return launch_pair_k<tb::Cfg<6, 64>>(in, out, ni, nj, nk, st, err);
+  return launch_pair_k<tb::Cfg<6, 32>>(in, out, ni, nj, nk, st, err);
 }
 
 int run(const ExecArgs& a, std::string& err) {
