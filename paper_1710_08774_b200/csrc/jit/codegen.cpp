@@ -50,9 +50,14 @@ struct GIn {
   std::string param;
   int var;
   std::vector<int> rel;
+  int via = -1;  // index into Ctx::inlined: the value is that producer recomputed in place
 };
 struct GOut {
   std::string param;
+  int var;
+  std::vector<int> rel;
+};
+struct Load {
   int var;
   std::vector<int> rel;
 };
@@ -61,6 +66,7 @@ struct Grp {
   std::vector<int> gmin, gmax;
   std::vector<GIn> in;
   std::vector<GOut> out;
+  std::vector<Load> loads;  // distinct (variable, offset) reads, inlined producers expanded
   int shift = 0;  // lead along the outermost dimension (march schedule)
   int level = 1;  // dependency level (groups of one level share a barrier)
 };
@@ -77,6 +83,7 @@ struct Ctx {
   std::map<int, std::vector<int>> axiom_extra;
   std::vector<char> smem_var;  // kernel outputs read by some kernel
   std::vector<Grp> groups;     // kernel groups, dataflow order
+  std::vector<Grp> inlined;    // cheap producers recomputed inside their consumers
   std::string error;
 
   explicit Ctx(const lf::Plan& p) : P(p) {}
@@ -333,6 +340,101 @@ bool analyse(Ctx& C) {
     }
     C.groups.push_back(std::move(G));
   }
+  // ---- inline cheap producers (2D/3D): a body of at most two operations,
+  // read by kernels only at <= 2 offsets per output, whose own inputs are not
+  // inlined values, is recomputed at each read instead of stored -- e.g. the
+  // face fluxes u[+1]-u of the 3D heat chain: fewer shared-memory round trips
+  // than a window store + two loads, identical arithmetic per term
+  auto ops = [](const lf::Expr& e) {
+    std::function<int(const lf::Expr&)> f = [&](const lf::Expr& x) -> int {
+      int n = x.kind == lf::Expr::Num || x.kind == lf::Expr::Var ? 0 : 1;
+      for (const auto& a : x.args) n += f(*a);
+      return n;
+    };
+    return f(e);
+  };
+  std::vector<char> inl(C.groups.size(), 0);
+  if (nd >= 2 && !std::getenv("LF_JIT_NOINLINE")) {
+    for (size_t gi = 0; gi < C.groups.size(); ++gi) {
+      const Grp& Pg = C.groups[gi];
+      const auto& k = rs.kernels[Pg.kernel];
+      bool ok = true;
+      int cost = 0;
+      for (const auto& [op, pat] : k.outputs) {
+        if (!k.bodies.count(op)) {
+          ok = false;
+          break;
+        }
+        std::string e2;
+        auto e = lf::parse_expr(k.bodies.at(op), e2);
+        if (!e) {
+          ok = false;
+          break;
+        }
+        cost += ops(*e);
+      }
+      if (!ok || cost > 2) continue;
+      for (const auto& in : Pg.in)
+        for (size_t pj = 0; pj < C.groups.size(); ++pj)
+          if (inl[pj])
+            for (const auto& o2 : C.groups[pj].out) ok &= o2.var != in.var;
+      for (const auto& o : Pg.out) {
+        if (!C.smem_var[o.var] || C.terminal_of(o.var, true) >= 0) ok = false;
+        int reads = 0;
+        for (const auto& c : C.groups)
+          for (const auto& in : c.in) reads += in.var == o.var;
+        if (reads == 0 || reads > 2) ok = false;
+      }
+      // a producer's input must not itself be an inlined value
+      for (size_t pj = 0; pj < C.groups.size() && ok; ++pj)
+        if (inl[pj])
+          for (const auto& in : C.groups[pj].in)
+            for (const auto& o : Pg.out) ok &= in.var != o.var;
+      if (ok) inl[gi] = 1;
+    }
+  }
+  {
+    std::vector<Grp> kept;
+    std::vector<int> new_index(C.groups.size(), -1);
+    for (size_t gi = 0; gi < C.groups.size(); ++gi)
+      if (inl[gi]) {
+        new_index[gi] = static_cast<int>(C.inlined.size());
+        C.inlined.push_back(C.groups[gi]);
+      }
+    for (size_t gi = 0; gi < C.groups.size(); ++gi)
+      if (!inl[gi]) kept.push_back(C.groups[gi]);
+    for (auto& c : kept)
+      for (auto& in : c.in)
+        for (size_t pi = 0; pi < C.inlined.size(); ++pi)
+          for (const auto& o : C.inlined[pi].out)
+            if (o.var == in.var) in.via = static_cast<int>(pi);
+    for (const auto& pg : C.inlined)
+      for (const auto& o : pg.out) C.smem_var[o.var] = 0;
+    C.groups = std::move(kept);
+    // effective loads
+    for (auto& c : C.groups) {
+      auto add = [&](int var, const std::vector<int>& rel) {
+        for (const auto& l : c.loads)
+          if (l.var == var && l.rel == rel) return;
+        c.loads.push_back({var, rel});
+      };
+      for (const auto& in : c.in) {
+        if (in.via < 0) {
+          add(in.var, in.rel);
+          continue;
+        }
+        const Grp& pg = C.inlined[in.via];
+        std::vector<int> orel(nd, 0);
+        for (const auto& o : pg.out)
+          if (o.var == in.var) orel = o.rel;
+        for (const auto& pin : pg.in) {
+          std::vector<int> r(nd);
+          for (int d = 0; d < nd; ++d) r[d] = in.rel[d] - orel[d] + pin.rel[d];
+          add(pin.var, r);
+        }
+      }
+    }
+  }
   // ---- pipeline shifts along dim 0 (reverse dataflow order) and levels
   const int nG = static_cast<int>(C.groups.size());
   for (int gi = nG - 1; gi >= 0; --gi) {
@@ -341,7 +443,7 @@ bool analyse(Ctx& C) {
     int s = INT_MIN;
     for (const auto& o : G.out)
       for (int ci = gi + 1; ci < nG; ++ci)
-        for (const auto& in : C.groups[ci].in)
+        for (const auto& in : C.groups[ci].loads)
           if (in.var == o.var) {
             s = std::max(s, C.groups[ci].shift + in.rel[0] - o.rel[0]);
             any = true;
@@ -351,7 +453,7 @@ bool analyse(Ctx& C) {
   for (int gi = 0; gi < nG; ++gi) {
     Grp& G = C.groups[gi];
     G.level = 1;
-    for (const auto& in : G.in)
+    for (const auto& in : G.loads)
       for (int pi = 0; pi < gi; ++pi)
         for (const auto& o : C.groups[pi].out)
           if (o.var == in.var) G.level = std::max(G.level, C.groups[pi].level + 1);
@@ -411,7 +513,7 @@ bool emit_march(Ctx& C, JitProgram& out, std::ostream& src) {
   int PD = nd == 2 ? 3 : 2;
   if (const char* e = std::getenv("LF_JIT_PD")) PD = std::max(1, std::atoi(e));
   for (const auto& g : G)
-    for (const auto& in : g.in) {
+    for (const auto& in : g.loads) {
       lead[in.var] = std::max(lead[in.var], C.smem_var[in.var] ? INT_MIN : g.shift + in.rel[0]);
       old[in.var] = std::min(old[in.var], g.shift + in.rel[0]);
     }
@@ -744,7 +846,7 @@ bool emit_march(Ctx& C, JitProgram& out, std::ostream& src) {
       rbs[key] = nm;
       return nm;
     };
-    for (const auto& in : g.in)
+    for (const auto& in : g.loads)
       if (win[in.var] > 0) rb(in.var, in.rel[0]);
     for (const auto& o : g.out)
       if (C.smem_var[o.var]) rb(o.var, o.rel[0]);
@@ -761,14 +863,15 @@ bool emit_march(Ctx& C, JitProgram& out, std::ostream& src) {
     const int B = std::min(K, ILP);
     src << "        #pragma unroll\n";
     src << "        for (int kb = 0; kb < " << K << "; kb += " << B << ") {\n";
-    for (const auto& in : g.in) src << "        T a_" << in.param << "[" << B << "];\n";
+    for (size_t li = 0; li < g.loads.size(); ++li) src << "        T a_l" << li << "[" << B << "];\n";
     src << "        #pragma unroll\n";
     src << "        for (int kk = 0; kk < " << B << "; ++kk) {\n";
     src << "          const int k = kb + kk;\n";
     src << "          const int c1 = " << LANE << plus(lo[1]) << " + k * " << STEP << ";\n";
     src << "          const int x1 = o1 + c1;\n";
     src << "          if (act && c1 <= c1hi) {\n";
-    for (const auto& in : g.in) {
+    for (size_t li = 0; li < g.loads.size(); ++li) {
+      const Load& in = g.loads[li];
       std::string r;
       if (win[in.var] > 0) {
         r = "v" + std::to_string(in.var) + "[" + rb(in.var, in.rel[0]) + " + " + inplane(in.var, in.rel) + "]";
@@ -782,7 +885,7 @@ bool emit_march(Ctx& C, JitProgram& out, std::ostream& src) {
           r = "__ldg(t" + std::to_string(ti) + " + " + C.tidx(ti, pos, C.extra_of(in.var)) + ")";
         }
       }
-      src << "            a_" << in.param << "[kk] = " << r << ";\n";
+      src << "            a_l" << li << "[kk] = " << r << ";\n";
     }
     src << "          }\n        }\n";
     // phase 2: evaluate and store
@@ -792,7 +895,40 @@ bool emit_march(Ctx& C, JitProgram& out, std::ostream& src) {
     src << "          const int c1 = " << LANE << plus(lo[1]) << " + k * " << STEP << ";\n";
     src << "          const int x1 = o1 + c1;\n";
     src << "          if (act && c1 <= c1hi) {\n";
-    for (const auto& in : g.in) src << "            const T p_" << in.param << " = a_" << in.param << "[kk];\n";
+    auto load_index = [&](int var, const std::vector<int>& rel) {
+      for (size_t li = 0; li < g.loads.size(); ++li)
+        if (g.loads[li].var == var && g.loads[li].rel == rel) return static_cast<int>(li);
+      return -1;
+    };
+    for (size_t li = 0; li < g.loads.size(); ++li) src << "            const T l" << li << " = a_l" << li << "[kk];\n";
+    for (const auto& in : g.in) {
+      if (in.via < 0) {
+        src << "            const T p_" << in.param << " = l" << load_index(in.var, in.rel) << ";\n";
+        continue;
+      }
+      // the inlined producer, evaluated at this read's offset
+      const Grp& pg = C.inlined[in.via];
+      const auto& pk = C.P.rs.kernels[pg.kernel];
+      std::string oparam;
+      std::vector<int> orel(nd, 0);
+      for (const auto& o : pg.out)
+        if (o.var == in.var) {
+          oparam = o.param;
+          orel = o.rel;
+        }
+      std::map<std::string, std::string> pv;
+      for (const auto& pin : pg.in) {
+        std::vector<int> r(nd);
+        for (int d = 0; d < nd; ++d) r[d] = in.rel[d] - orel[d] + pin.rel[d];
+        pv[pin.param] = "l" + std::to_string(load_index(pin.var, r));
+      }
+      std::string e2;
+      auto e = lf::parse_expr(pk.bodies.at(oparam), e2);
+      if (!e) return (C.error = "kernel '" + pk.name + "': " + e2, false);
+      src << "            const T p_" << in.param << " = "
+          << lf::emit_c(*e, C.T, [&](const std::string& n) { return pv.at(n); }) << ";  // inlined '" << pk.name
+          << "'\n";
+    }
     if (!emit_bodies(C, g, src, "            ")) return false;
     for (const auto& o : g.out) {
       if (C.smem_var[o.var])
