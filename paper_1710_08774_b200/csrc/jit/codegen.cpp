@@ -737,6 +737,44 @@ bool emit_march(Ctx& C, JitProgram& out, std::ostream& src) {
   }
   for (size_t v = 0; v < nv; ++v)
     if (win[v] > 1) src << "  int b" << v << " = " << wrap(v, TS) << ";\n";
+  // register windows along the march (opt-in, LF_JIT_ROT=1): a thread keeps
+  // its cells for a whole segment, so a window value read at row offset s on
+  // trip t+1 is the one it read at s+1 on trip t -- only the newest row of
+  // each (variable, in-plane offset) set is loaded, the rest rotate through
+  // registers.  Measured slower on the BASELINE chains (biharm 163 vs 178 G,
+  // box 171 vs 219 G: the register cost outweighs the shared-memory loads
+  // saved), so off by default.
+  struct Rot {
+    int K = 1;
+    std::vector<int> from;  // load index whose previous-trip value this load takes (-1: load)
+    std::vector<char> keep;  // value carried to the next trip
+  };
+  std::vector<Rot> rot(G.size());
+  const bool use_rot = std::getenv("LF_JIT_ROT") && std::atoi(std::getenv("LF_JIT_ROT")) != 0;
+  for (size_t gi = 0; gi < G.size(); ++gi) {
+    const Grp& g = G[gi];
+    Rot& R = rot[gi];
+    R.K = (tile[1] + (g.gmax[1] - g.gmin[1]) + STEP - 1) / STEP;
+    R.from.assign(g.loads.size(), -1);
+    R.keep.assign(g.loads.size(), 0);
+    if (!use_rot || ILP != 1) continue;
+    for (size_t li = 0; li < g.loads.size(); ++li) {
+      const Load& a = g.loads[li];
+      if (win[a.var] <= 0) continue;
+      for (size_t lj = 0; lj < g.loads.size(); ++lj) {
+        const Load& b = g.loads[lj];
+        if (b.var != a.var || b.rel[0] != a.rel[0] + 1) continue;
+        bool same = true;
+        for (int d = 1; d < nd; ++d) same &= a.rel[d] == b.rel[d];
+        if (same) {
+          R.from[li] = static_cast<int>(lj);
+          R.keep[lj] = 1;
+        }
+      }
+    }
+    for (size_t lj = 0; lj < g.loads.size(); ++lj)
+      if (R.keep[lj]) src << "  T rw" << gi << "_" << lj << "[" << R.K << "];\n";
+  }
   // ---- axiom streaming: row `row` of staged var v into slot `slotexpr`
   auto emit_load = [&](size_t v, const std::string& row, const std::string& slotexpr, const char* ind) {
     std::vector<int> ext(nd), lo(nd);
@@ -836,6 +874,7 @@ bool emit_march(Ctx& C, JitProgram& out, std::ostream& src) {
     src << "    { // group " << gi << ": kernel '" << k.name << "', lead " << g.shift << ", level " << g.level << "\n";
     src << "      const int y = t" << plus(g.shift) << ";\n";
     src << "      if (y >= r0" << plus(g.gmin[0]) << " && y <= r1 - 1" << plus(g.gmax[0]) << ") {\n";
+    src << "        const bool first = y == r0" << plus(g.gmin[0]) << ";  // segment start: fill the register windows\n";
     std::map<std::pair<int, int>, std::string> rbs;
     auto rb = [&](int v, int r) {
       auto key = std::make_pair(v, r);
@@ -870,6 +909,8 @@ bool emit_march(Ctx& C, JitProgram& out, std::ostream& src) {
     src << "          const int c1 = " << LANE << plus(lo[1]) << " + k * " << STEP << ";\n";
     src << "          const int x1 = o1 + c1;\n";
     src << "          if (act && c1 <= c1hi) {\n";
+    std::vector<std::string> reads(g.loads.size());
+    bool any_rot = false;
     for (size_t li = 0; li < g.loads.size(); ++li) {
       const Load& in = g.loads[li];
       std::string r;
@@ -885,8 +926,24 @@ bool emit_march(Ctx& C, JitProgram& out, std::ostream& src) {
           r = "__ldg(t" + std::to_string(ti) + " + " + C.tidx(ti, pos, C.extra_of(in.var)) + ")";
         }
       }
-      src << "            a_l" << li << "[kk] = " << r << ";\n";
+      reads[li] = r;
+      any_rot |= rot[gi].from[li] >= 0;
     }
+    if (any_rot) {
+      // the branch is uniform: the first trip of a segment loads every row
+      src << "            if (first) {\n";
+      for (size_t li = 0; li < g.loads.size(); ++li) src << "              a_l" << li << "[kk] = " << reads[li] << ";\n";
+      src << "            } else {\n";
+      for (size_t li = 0; li < g.loads.size(); ++li)
+        src << "              a_l" << li << "[kk] = "
+            << (rot[gi].from[li] >= 0 ? "rw" + std::to_string(gi) + "_" + std::to_string(rot[gi].from[li]) + "[k]" : reads[li])
+            << ";\n";
+      src << "            }\n";
+    } else {
+      for (size_t li = 0; li < g.loads.size(); ++li) src << "            a_l" << li << "[kk] = " << reads[li] << ";\n";
+    }
+    for (size_t lj = 0; lj < g.loads.size(); ++lj)
+      if (rot[gi].keep[lj]) src << "            rw" << gi << "_" << lj << "[k] = a_l" << lj << "[kk];\n";
     src << "          }\n        }\n";
     // phase 2: evaluate and store
     src << "        #pragma unroll\n";

@@ -155,3 +155,16 @@ def test_ranges_not_starting_at_zero(name, shift, tmp_path):
     ref = generic.run_naive(path, ax, steps=steps)
     for g, t in zip(got, plan.goals):
         assert np.array_equal(bits(g), bits(ref[t.name])), t.name
+
+
+@pytest.mark.parametrize("name", ["biharm_body", "heat3d_body"])
+def test_register_window_rotation_is_exact(name, monkeypatch):
+    """LF_JIT_ROT=1 (opt-in): window rows rotate through registers across trips."""
+    monkeypatch.setenv("LF_JIT_ROT", "1")
+    plan = lf.Plan.from_file(SPECS / f"{name}.lf")
+    assert "rw0_" in plan.source or "rw1_" in plan.source
+    ax = CASES[name]()
+    got = run_device(plan, [ax[t.name] for t in plan.axioms], 3)
+    ref = generic.run_naive(SPECS / f"{name}.lf", ax, steps=3)
+    for g, t in zip(got, plan.goals):
+        assert np.array_equal(bits(g), bits(ref[t.name])), t.name
