@@ -65,12 +65,15 @@ struct lf_plan {
   std::vector<void*> dev;   // lf_run_host device terminals
   std::vector<void*> scratch;  // per goal; iterated goals only
   cudaStream_t stream = nullptr;
+  cudaStream_t h2d = nullptr, d2h = nullptr;  // copy streams of the pipelined host path
   ~lf_plan() {
     for (void* p : dev)
       if (p) cudaFree(p);
     for (void* p : scratch)
       if (p) cudaFree(p);
     if (stream) cudaStreamDestroy(stream);
+    if (h2d) cudaStreamDestroy(h2d);
+    if (d2h) cudaStreamDestroy(d2h);
   }
 };
 
@@ -325,6 +328,111 @@ int lf_run(const lf_plan* cplan, void* const* terms, int nterm, int steps, void*
   }
 }
 
+// Single-step host runs, pipelined: the outer dimension is cut into parts;
+// part p's input rows go up on one copy stream, the part is computed on the
+// plan's stream as soon as they (and the halo) have landed, and its finished
+// output rows come down on a second copy stream -- both PCIe directions and
+// the SMs busy at once instead of one after the other.  Every executor
+// computes row parts (lf_slab part ranges); ghost rows of the goals are
+// copied once all parts are done.
+static int run_host_pipelined(lf_plan* plan, void* const* terms, const std::vector<void*>& dterms, int parts,
+                              std::string& err) {
+  const auto& T = plan->plan.terminals;
+  const long n0 = plan->plan.rs.ranges[0].trips();
+  const long lo0 = plan->plan.rs.ranges[0].lo;
+  for (cudaStream_t* s : {&plan->h2d, &plan->d2h})
+    if (!*s) {
+      cudaError_t e = cudaStreamCreateWithFlags(s, cudaStreamNonBlocking);
+      if (e != cudaSuccess) return lfx::cuda_status(e, "cudaStreamCreate", err);
+    }
+  auto chunked = [&](const lf::Terminal& t) { return !t.dims.empty() && t.dims[0] == 0; };
+  auto row_bytes = [&](const lf::Terminal& t) {
+    int64_t b = t.elem_bytes;
+    for (size_t k = 1; k < t.extent.size(); ++k) b *= t.extent[k];
+    return b;
+  };
+  auto copy = [&](void* dst, const void* src, int64_t bytes, cudaMemcpyKind kind, cudaStream_t st) {
+    if (bytes <= 0) return LF_OK;
+    return lfx::cuda_status(cudaMemcpyAsync(dst, src, bytes, kind, st), "cudaMemcpyAsync(pipelined)", err);
+  };
+  std::vector<cudaEvent_t> up(parts), done(parts);
+  for (int p = 0; p < parts; ++p) {
+    cudaEventCreateWithFlags(&up[p], cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&done[p], cudaEventDisableTiming);
+  }
+  int st = LF_OK;
+  // inputs that do not span the outer dimension go up first, whole
+  for (size_t i = 0; i < T.size() && st == LF_OK; ++i)
+    if (!T[i].is_goal && !chunked(T[i])) st = copy(dterms[i], terms[i], terminal_bytes(T[i]), cudaMemcpyHostToDevice, plan->h2d);
+  std::vector<long> copied(T.size(), 0);  // storage rows already sent, per axiom
+  for (int p = 0; p < parts && st == LF_OK; ++p) {
+    const long a = n0 * p / parts, b = n0 * (p + 1) / parts;
+    // rows of every chunked axiom up to this part's last row plus the ghost/halo rows above it
+    for (size_t i = 0; i < T.size() && st == LF_OK; ++i) {
+      if (T[i].is_goal || !chunked(T[i])) continue;
+      const long e0 = T[i].extent[0], below = lo0 - T[i].base[0], above = e0 - n0 - below;
+      const long need = p == parts - 1 ? e0 : std::min(e0, b + below + above);
+      if (need > copied[i]) {
+        const int64_t rb = row_bytes(T[i]);
+        st = copy(static_cast<char*>(dterms[i]) + copied[i] * rb, static_cast<const char*>(terms[i]) + copied[i] * rb,
+                  (need - copied[i]) * rb, cudaMemcpyHostToDevice, plan->h2d);
+        copied[i] = need;
+      }
+    }
+    if (st != LF_OK) break;
+    cudaEventRecord(up[p], plan->h2d);
+    cudaStreamWaitEvent(plan->stream, up[p], 0);
+    lf_slab slab{0, n0, n0, a, b};
+    lfx::ExecArgs ea;
+    ea.plan = &plan->plan;
+    ea.terms = dterms.data();
+    ea.steps = 1;
+    ea.stream = plan->stream;
+    ea.slab = &slab;
+    ea.whole_domain_parts = true;
+    st = plan->exec ? plan->exec->run(ea, err) : plan->jit->run(ea, err);
+    if (st != LF_OK) break;
+    cudaEventRecord(done[p], plan->stream);
+    cudaStreamWaitEvent(plan->d2h, done[p], 0);
+    // this part's interior output rows
+    for (size_t i = 0; i < T.size() && st == LF_OK; ++i) {
+      if (!T[i].is_goal || !chunked(T[i])) continue;
+      const long below = lo0 - T[i].base[0];
+      const int64_t rb = row_bytes(T[i]);
+      st = copy(static_cast<char*>(terms[i]) + (a + below) * rb, static_cast<const char*>(dterms[i]) + (a + below) * rb,
+                (b - a) * rb, cudaMemcpyDeviceToHost, plan->d2h);
+    }
+  }
+  // once every part is done: ghost rows of the goals, and goals without an outer dimension
+  if (st == LF_OK) {
+    cudaStreamWaitEvent(plan->d2h, done[parts - 1], 0);
+    for (size_t i = 0; i < T.size() && st == LF_OK; ++i) {
+      if (!T[i].is_goal) continue;
+      if (!chunked(T[i])) {
+        st = copy(terms[i], dterms[i], terminal_bytes(T[i]), cudaMemcpyDeviceToHost, plan->d2h);
+        continue;
+      }
+      const long e0 = T[i].extent[0], below = lo0 - T[i].base[0];
+      const int64_t rb = row_bytes(T[i]);
+      st = copy(terms[i], dterms[i], below * rb, cudaMemcpyDeviceToHost, plan->d2h);
+      if (st == LF_OK)
+        st = copy(static_cast<char*>(terms[i]) + (n0 + below) * rb, static_cast<const char*>(dterms[i]) + (n0 + below) * rb,
+                  (e0 - n0 - below) * rb, cudaMemcpyDeviceToHost, plan->d2h);
+    }
+  }
+  cudaError_t e1 = cudaStreamSynchronize(plan->h2d);
+  cudaError_t e2 = cudaStreamSynchronize(plan->stream);
+  cudaError_t e3 = cudaStreamSynchronize(plan->d2h);
+  for (int p = 0; p < parts; ++p) {
+    cudaEventDestroy(up[p]);
+    cudaEventDestroy(done[p]);
+  }
+  if (st != LF_OK) return st;
+  for (cudaError_t e : {e1, e2, e3})
+    if (e != cudaSuccess) return lfx::cuda_status(e, "cudaStreamSynchronize(pipelined)", err);
+  return LF_OK;
+}
+
 int lf_run_host(const lf_plan* cplan, void* const* terms, int nterm, int steps) {
   try {
     g_err.clear();
@@ -359,6 +467,18 @@ int lf_run_host(const lf_plan* cplan, void* const* terms, int nterm, int steps) 
     if (steps > 1 && !inplace) {
       if ((st = ensure_scratch(plan, err)) != LF_OK) return fail(st, err);
       scratch = scratch_list(plan);
+    }
+    // single steps of large grids: copies in both directions overlap the parts' compute
+    {
+      const long n0 = plan->plan.rs.ranges[0].trips();
+      const bool nests = plan->jit && !plan->jit->program().nest_kernels.empty();
+      int parts = static_cast<int>(std::min<long>(16, n0 / 512));
+      if (const char* e = std::getenv("LF_HOST_PARTS")) parts = std::atoi(e);
+      if (steps == 1 && !inplace && !nests && parts >= 2) {
+        st = run_host_pipelined(plan, terms, dterms, parts, err);
+        if (st != LF_OK) return fail(st, err);
+        return LF_OK;
+      }
     }
     for (size_t i = 0; i < T.size(); ++i) {
       if (T[i].is_goal) continue;

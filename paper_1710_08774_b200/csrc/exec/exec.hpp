@@ -22,6 +22,7 @@ struct ExecArgs {
   cudaStream_t stream = nullptr;
   const lf_slab* slab = nullptr;  // nullptr: the whole domain
   void* const* scratch = nullptr;  // per iterated goal, same layout (steps > 1)
+  bool whole_domain_parts = false;  // slab = the whole domain, computed in row parts (pipelined host run)
 };
 
 struct Executor {

@@ -666,13 +666,15 @@ int run(const ExecArgs& a, std::string& err) {
   const int nj = (int)r[1].trips(), ni = (int)r[2].trips();
   const RowPart rp = row_part(a, (int)r[0].trips());
   const int nk = rp.rows;
-  const bool wrap_k = a.slab == nullptr;  // k ghosts of a slab come from the caller's halo exchange
+  // k ghosts of a slab come from the caller's halo exchange; the row parts of
+  // a pipelined host run cover the whole domain and wrap themselves
+  const bool wrap_k = a.slab == nullptr || a.whole_domain_parts;
   const double* src = static_cast<const double*>(a.terms[0]);
   double* goal = static_cast<double*>(a.terms[1]);
   double* scratch = a.steps > 1 ? static_cast<double*>(a.scratch[0]) : nullptr;
   // passes of one or two steps; they alternate goal/scratch so that the last
   // one lands in the goal and the axiom buffer is never written
-  const bool pairs = wrap_k && a.steps >= 2 && tb_enabled(ni, nj, nk);
+  const bool pairs = a.slab == nullptr && a.steps >= 2 && tb_enabled(ni, nj, nk);
   const int passes = pairs ? (a.steps + 1) / 2 : a.steps;
   for (int s = 0; s < passes; ++s) {
     const bool to_goal = ((passes - 1 - s) % 2) == 0;

@@ -1,0 +1,80 @@
+"""lf_run_host, single step, pipelined (row parts: H2D of part p+1, compute
+of part p and D2H of part p-1 overlap) -- bit-exact against the oracles,
+ghost rows included."""
+import numpy as np
+import pytest
+
+import oracle
+from oracle import generic
+import paper_1710_08774_b200 as lf
+from paper_1710_08774_b200 import inputs
+
+pytestmark = pytest.mark.gpu
+SPECS = lf.PKG_DIR.parent / "tests" / "specs"
+
+
+def bits(a):
+    a = np.ascontiguousarray(a)
+    return a.view(np.uint64 if a.dtype == np.float64 else np.uint32)
+
+
+@pytest.fixture(params=["3", "7"])
+def parts(request, monkeypatch):
+    monkeypatch.setenv("LF_HOST_PARTS", request.param)
+    return int(request.param)
+
+
+def test_box(parts):
+    plan = lf.Plan.with_ranges("box2x", (100, 256))
+    img = inputs.box_input(100, 256, seed=1)
+    out = np.full((100, 256), np.nan, np.float32)
+    plan.run_host([img, out], steps=1)
+    assert np.array_equal(bits(out), bits(oracle.box(img)))
+
+
+def test_biharm(parts):
+    plan = lf.Plan.with_ranges("biharmonic2d", (90, 256))
+    u = inputs.biharm_input(90, 256, seed=2)
+    out = np.full_like(u, np.nan)
+    plan.run_host([u, out], steps=1)
+    assert np.array_equal(bits(out), bits(oracle.biharm(u, 1)))
+
+
+def test_heat3d(parts):
+    plan = lf.Plan.with_ranges("heat3d", (20, 32, 128))
+    u = inputs.heat3d_input(20, 32, 128, seed=3, sigma=4.0)
+    out = np.full_like(u, np.nan)
+    plan.run_host([u, out], steps=1)
+    ref = oracle.heat3d(u, 1)
+    assert np.array_equal(bits(out[1:-1, 1:-1, 1:-1]), bits(ref[1:-1, 1:-1, 1:-1]))
+    # periodic ghost faces, including the k planes the first / last parts refill
+    for ax in range(3):
+        sl_g = [slice(1, -1)] * 3
+        sl_s = [slice(1, -1)] * 3
+        sl_g[ax], sl_s[ax] = 0, -2
+        assert np.array_equal(bits(out[tuple(sl_g)]), bits(out[tuple(sl_s)]))
+
+
+def test_hydro(parts):
+    plan = lf.Plan.with_ranges("hydro2d", (64, 256))
+    st, dtdx = inputs.hydro_input(64, 256, seed=4)
+    outs = [np.full_like(st[0], np.nan) for _ in range(4)]
+    plan.run_host(st + [np.array([dtdx])] + outs, steps=1)
+    ref = oracle.hydro(st, dtdx, 1)
+    for v in range(4):
+        assert np.array_equal(bits(outs[v]), bits(ref[v])), v
+
+
+def test_generic_executor(parts):
+    spec = lf.set_ranges((SPECS / "heat3d_body.lf").read_text(), (24, 20, 50))
+    path = SPECS / "_pipe_heat3d_body.lf"
+    path.write_text(spec)
+    try:
+        plan = lf.Plan(spec, "p.lf")
+        u = inputs.heat3d_input(24, 20, 50, seed=5, sigma=3.0)
+        out = np.full_like(u, np.nan)
+        plan.run_host([u, out], steps=1)
+        ref = generic.run_naive(path, {"g_u": u}, steps=1)["g_unew"]
+    finally:
+        path.unlink()
+    assert np.array_equal(bits(out), bits(ref))
