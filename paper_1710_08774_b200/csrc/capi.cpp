@@ -472,7 +472,7 @@ int lf_run_host(const lf_plan* cplan, void* const* terms, int nterm, int steps) 
     {
       const long n0 = plan->plan.rs.ranges[0].trips();
       const bool nests = plan->jit && !plan->jit->program().nest_kernels.empty();
-      int parts = static_cast<int>(std::min<long>(16, n0 / 512));
+      int parts = static_cast<int>(std::min<long>(32, n0 / 512));  // 32: measured best for the 16384^2 box pass
       if (const char* e = std::getenv("LF_HOST_PARTS")) parts = std::atoi(e);
       if (steps == 1 && !inplace && !nests && parts >= 2) {
         st = run_host_pipelined(plan, terms, dterms, parts, err);
