@@ -502,47 +502,6 @@ std::optional<Plan> make_plan(const RuleSet& rs_in, DiagList& diags) {
     }
   }
 
-  // ---- footprint polynomial (storage.cpp:161-190, 596-626) --------------------
-  {
-    std::map<std::vector<int>, long> terms;
-    std::set<std::string> counted;
-    for (const auto& v : P.vars) {
-      if (v.alias_of >= 0) continue;
-      std::vector<int> mono;
-      long coeff = 1;
-      if (v.scheme == Scheme::terminal) {
-        if (!counted.insert(v.external).second) continue;
-        mono = v.dims;
-      } else if (v.scheme == Scheme::full) {
-        mono = v.dims;
-      } else if (v.scheme == Scheme::scalar) {
-      } else {
-        for (size_t k = 0; k < v.dims.size(); ++k) {
-          if (v.dims[k] == v.rotating_dim)
-            coeff *= v.spans[k];
-          else if (v.dims[k] > v.rotating_dim)
-            mono.push_back(v.dims[k]);
-        }
-      }
-      std::sort(mono.begin(), mono.end());
-      terms[mono] += coeff;
-    }
-    std::vector<std::pair<std::vector<int>, long>> ord(terms.begin(), terms.end());
-    std::sort(ord.begin(), ord.end(), [](const auto& a, const auto& b) {
-      if (a.first.size() != b.first.size()) return a.first.size() > b.first.size();
-      return a.first < b.first;
-    });
-    std::string s;
-    for (const auto& [mono, c] : ord) {
-      if (!c) continue;
-      if (!s.empty()) s += " + ";
-      std::string m;
-      for (int d : mono) m += (m.empty() ? "" : "*") + std::string("N_") + rs.loop_order[d];
-      s += m.empty() ? std::to_string(c) : (c == 1 ? m : std::to_string(c) + "*" + m);
-    }
-    P.footprint = s.empty() ? "0" : s;
-  }
-
   // ---- alias chain and shadow windows (storage.cpp:453-524, 544-594) ----------
   for (const auto& [in_ext, out_ext] : rs.aliases) {
     std::set<int> start, target;
@@ -611,6 +570,8 @@ std::optional<Plan> make_plan(const RuleSet& rs_in, DiagList& diags) {
           break;
         }
       for (int d : vd) sh.spans.push_back(win[d].second - win[d].first + 1);
+      sh.dims = vd;
+      sh.rotating = rot;
       if (rot < 0) {
         sh.scheme = vd.empty() ? Scheme::full : Scheme::inner_circular;
         if (!vd.empty()) sh.spans.back() = 1;
@@ -622,6 +583,58 @@ std::optional<Plan> make_plan(const RuleSet& rs_in, DiagList& diags) {
       P.alias.push_back(std::move(e));
       P.shadows.push_back(std::move(sh));
     }
+  }
+
+  // ---- footprint polynomial (storage.cpp:161-190, 596-626) --------------------
+  {
+    std::map<std::vector<int>, long> terms;
+    std::set<std::string> counted;
+    for (const auto& v : P.vars) {
+      if (v.alias_of >= 0) continue;
+      std::vector<int> mono;
+      long coeff = 1;
+      if (v.scheme == Scheme::terminal) {
+        if (!counted.insert(v.external).second) continue;
+        mono = v.dims;
+      } else if (v.scheme == Scheme::full) {
+        mono = v.dims;
+      } else if (v.scheme == Scheme::scalar) {
+      } else {
+        for (size_t k = 0; k < v.dims.size(); ++k) {
+          if (v.dims[k] == v.rotating_dim)
+            coeff *= v.spans[k];
+          else if (v.dims[k] > v.rotating_dim)
+            mono.push_back(v.dims[k]);
+        }
+      }
+      std::sort(mono.begin(), mono.end());
+      terms[mono] += coeff;
+    }
+    // shadow windows of in-place aliases (storage.cpp:617-625)
+    for (const auto& sh : P.shadows) {
+      std::vector<int> mono;
+      long coeff = 1;
+      for (size_t k = 0; k < sh.dims.size(); ++k) {
+        if (sh.dims[k] == sh.rotating) coeff *= sh.spans[k];
+        else if (sh.rotating >= 0 && sh.dims[k] > sh.rotating) mono.push_back(sh.dims[k]);
+      }
+      std::sort(mono.begin(), mono.end());
+      terms[mono] += coeff;
+    }
+    std::vector<std::pair<std::vector<int>, long>> ord(terms.begin(), terms.end());
+    std::sort(ord.begin(), ord.end(), [](const auto& a, const auto& b) {
+      if (a.first.size() != b.first.size()) return a.first.size() > b.first.size();
+      return a.first < b.first;
+    });
+    std::string s;
+    for (const auto& [mono, c] : ord) {
+      if (!c) continue;
+      if (!s.empty()) s += " + ";
+      std::string m;
+      for (int d : mono) m += (m.empty() ? "" : "*") + std::string("N_") + rs.loop_order[d];
+      s += m.empty() ? std::to_string(c) : (c == 1 ? m : std::to_string(c) + "*" + m);
+    }
+    P.footprint = s.empty() ? "0" : s;
   }
 
   // ---- canonical chain signature ---------------------------------------------

@@ -286,7 +286,9 @@ struct AliasEntry {
 struct Shadow {
   int var = -1;
   Scheme scheme = Scheme::full;
+  std::vector<int> dims;    // the variable's loop dims
   std::vector<long> spans;  // per variable dim
+  int rotating = -1;        // first dim with a window > 1 (-1: a single cell)
 };
 
 struct Plan {
