@@ -50,6 +50,11 @@ def _box_inputs(sizes, seed=0):
     return [inputs.box_input(*sizes, seed=seed)]
 
 
+def _norm_inputs(sizes, seed=0):
+    rng = np.random.default_rng(seed)
+    return [rng.random((sizes[0], sizes[1] + 1)), np.zeros(sizes[0])]
+
+
 def _hydro_inputs(sizes, seed=0):
     from paper_1710_08774_b200 import inputs
     st, dtdx = inputs.hydro_input(*sizes, seed=seed)
@@ -97,6 +102,11 @@ WORKLOADS = {
                        gen=_biharm_inputs, slab=_biharm_slab, dtype="f64", halo=(2, 2, False)),
     "box_jit": dict(config_index=3, spec="examples/box_body", sizes=(16384, 16384), chain_steps=1,
                     gen=_box_inputs, slab=_box_slab, dtype="f32", halo=None),
+    # multi-nest plan: row sums of squared differences (a reduction), their root,
+    # and a broadcast divide -- 2 nests, 1 split (the paper's normalization example)
+    "normalization_jit": dict(config_index=None, spec="examples/normalization_body", sizes=(8192, 8192),
+                              chain_steps=1, gen=lambda sz, seed=0: _norm_inputs(sz, seed), slab=None,
+                              dtype="f64", halo=None),
     # in place (config.aliases, one buffer for u and unew): half the footprint
     "heat3d_jit_inplace": dict(config_index=1, spec="examples/heat3d_inplace", sizes=(512, 512, 512),
                                chain_steps=50, gen=_heat3d_inputs, slab=None, dtype="f64", halo=(1, 1, True),
@@ -232,6 +242,17 @@ def cpu_runner(name, w):
         img = w["gen"](sizes)[0]
         return (lambda: oracle.box(img, fused=True, threads=threads)), int(np.prod(sizes)), threads, \
             f"1 pass of {'x'.join(map(str, sizes))}"
+    if name == "normalization":
+        # numpy restatement of run_naive for this chain on a 512-row band (single thread)
+        q, z = w["gen"]((512, sizes[1]))
+
+        def run():
+            fl = (q[:, 1:] - q[:, :-1]) * (q[:, 1:] - q[:, :-1])
+            acc = z.copy()
+            for i in range(fl.shape[1]):
+                acc = acc + fl[:, i]
+            return fl / np.sqrt(acc)[:, None]
+        return run, 512 * sizes[1], 1, f"a 512x{sizes[1]} row band (numpy run_naive)"
     nj = max(16, min(sizes[0], 64))  # hydro: a full-width row band, 1 step
     st = w["gen"]((nj, sizes[1]))
     outs = [np.empty_like(a) for a in st[:4]]
@@ -283,7 +304,8 @@ def main():
     w = WORKLOADS[args.config]
     cells = int(np.prod(w["sizes"]))
     metric = "fused-chain cell-updates/s"
-    workload = f"BASELINE configs[{w['config_index']}] {w['spec']} " + "x".join(map(str, w["sizes"])) + \
+    origin = f"BASELINE configs[{w['config_index']}]" if w["config_index"] is not None else "extra (not a BASELINE config)"
+    workload = f"{origin} {w['spec']} " + "x".join(map(str, w["sizes"])) + \
         f", {w['chain_steps']} steps"
 
     if args.impl == "reference":
