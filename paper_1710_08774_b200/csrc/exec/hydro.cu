@@ -41,7 +41,8 @@ constexpr int STAGE_BYTES = 4 * ARR_BYTES;
 constexpr int NPRIM = W + 4;           // 131 prim columns
 constexpr int NQ = W + 2;              // 129 trace columns
 constexpr int XBUF = 4 * NPRIM + 8 * NQ + 4 * NT;  // doubles per x-sweep buffer
-constexpr int SMEM = S * STAGE_BYTES + XBUF * 8 + S * 8 + 128;
+constexpr int U1RING = 3 * 4 * NT;                 // x-swept state of rows r-1..r-3, per column (thread)
+constexpr int SMEM = S * STAGE_BYTES + XBUF * 8 + U1RING * 8 + S * 8 + 128;
 
 struct Params {
   int ni, nj;            // interior of this launch's domain (slab rows for multi-GPU)
@@ -96,7 +97,10 @@ __global__ void __launch_bounds__(NT, MINB) hydro_fused(const __grid_constant__ 
   extern __shared__ __align__(128) unsigned char smem[];
   unsigned char* ring = smem;
   double* xb0 = reinterpret_cast<double*>(smem + S * STAGE_BYTES);
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + S * STAGE_BYTES + XBUF * 8);
+  // each thread's own column of the x-swept state for the three rows the
+  // y-sweep lags behind -- in shared memory rather than 24 more registers
+  double* u1ring = reinterpret_cast<double*>(smem + S * STAGE_BYTES + XBUF * 8);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + S * STAGE_BYTES + XBUF * 8 + U1RING * 8);
   const int t = threadIdx.x;
   if (t == 0) pdl_trigger();
   pdl_wait();  // previous step's output (our input) complete, our output buffer free
@@ -149,7 +153,6 @@ __global__ void __launch_bounds__(NT, MINB) hydro_fused(const __grid_constant__ 
     double yqm[4];            // minus-face trace state of row r-2 (read at C of row r+... see below)
     double ypo[4], ypn[4];    // plus-face trace states of rows r-3 and r-2
     double yfp[4];            // flux of face (r-4)+1/2
-    double u1a[4], u1b[4], u1c[4];  // x-swept state rows r-1, r-2, r-3
     // benign states for the dummy y-problems before the pipeline fills
 #pragma unroll
     for (int a = 0; a < 4; ++a) {
@@ -219,7 +222,9 @@ __global__ void __launch_bounds__(NT, MINB) hydro_fused(const __grid_constant__ 
           if (tt >= 5) {
             // update of row r-3 from faces (r-4)+1/2 and (r-3)+1/2
             double o[4];
-            hy_update(u1c[0], u1c[2], u1c[1], u1c[3], yfp[0], yfp[1], yfp[2], yfp[3], f[0], f[1], f[2], f[3],
+            // row r-3's x-swept state: ring slot (r-3) % 3 == r % 3
+            const double* u1c = u1ring + (tt % 3) * 4 * NT + t;
+            hy_update(u1c[0], u1c[2 * NT], u1c[NT], u1c[3 * NT], yfp[0], yfp[1], yfp[2], yfp[3], f[0], f[1], f[2], f[3],
                       dtdx, &o[0], &o[2], &o[1], &o[3]);
             store_cell(p, sg.jb - 2 + tt - 3, i0 + t, o);
           }
@@ -258,9 +263,7 @@ __global__ void __launch_bounds__(NT, MINB) hydro_fused(const __grid_constant__ 
       for (int a = 0; a < 4; ++a) {
         yq2[a] = yq1[a];
         yq1[a] = yq[a];
-        u1c[a] = u1b[a];
-        u1b[a] = u1a[a];
-        u1a[a] = u1[a];
+        u1ring[(tt % 3) * 4 * NT + a * NT + t] = u1[a];
       }
     }
   }
