@@ -33,7 +33,7 @@ constexpr int W = NT - 1;              // cells per strip
 constexpr int H = 2;                   // radius of each sweep
 constexpr int BOXW = 132;              // staged columns from the even storage column <= i0 (131 used)
 constexpr int R = 2;                   // rows per stage
-constexpr int S = 3;                   // ring slots (compute per row >> load latency)
+constexpr int S = 2;                   // ring slots (compute per row >> load latency)
 constexpr int ARR_TX = BOXW * R * 8;   // bytes TMA delivers per array per stage
 constexpr int ARR_BYTES = (ARR_TX + 127) / 128 * 128;  // 128-B aligned array slots
 constexpr int STAGE_TX = 4 * ARR_TX;
@@ -42,7 +42,8 @@ constexpr int NPRIM = W + 4;           // 131 prim columns
 constexpr int NQ = W + 2;              // 129 trace columns
 constexpr int XBUF = 4 * NPRIM + 8 * NQ + 4 * NT;  // doubles per x-sweep buffer
 constexpr int U1RING = 3 * 4 * NT;                 // x-swept state of rows r-1..r-3, per column (thread)
-constexpr int SMEM = S * STAGE_BYTES + XBUF * 8 + U1RING * 8 + S * 8 + 128;
+constexpr int YQRING = 2 * 4 * NT;                 // y-sweep prims of rows r-1, r-2, per column
+constexpr int SMEM = S * STAGE_BYTES + XBUF * 8 + (U1RING + YQRING) * 8 + S * 8 + 128;
 
 struct Params {
   int ni, nj;            // interior of this launch's domain (slab rows for multi-GPU)
@@ -100,7 +101,8 @@ __global__ void __launch_bounds__(NT, MINB) hydro_fused(const __grid_constant__ 
   // each thread's own column of the x-swept state for the three rows the
   // y-sweep lags behind -- in shared memory rather than 24 more registers
   double* u1ring = reinterpret_cast<double*>(smem + S * STAGE_BYTES + XBUF * 8);
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + S * STAGE_BYTES + XBUF * 8 + U1RING * 8);
+  double* yqring = u1ring + U1RING;  // slot r % 2 holds row r's prims
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + S * STAGE_BYTES + XBUF * 8 + (U1RING + YQRING) * 8);
   const int t = threadIdx.x;
   if (t == 0) pdl_trigger();
   pdl_wait();  // previous step's output (our input) complete, our output buffer free
@@ -149,7 +151,6 @@ __global__ void __launch_bounds__(NT, MINB) hydro_fused(const __grid_constant__ 
     // solve of the same thread (two independent dependency chains per thread)
     const int T = sg.je - sg.jb + 2 * H + 1;
     // y-sweep windows of column i0 + t (indices relative to the marched row r)
-    double yq1[4], yq2[4];    // prims of rows r-1, r-2
     double yqm[4];            // minus-face trace state of row r-2 (read at C of row r+... see below)
     double ypo[4], ypn[4];    // plus-face trace states of rows r-3 and r-2
     double yfp[4];            // flux of face (r-4)+1/2
@@ -248,10 +249,14 @@ __global__ void __launch_bounds__(NT, MINB) hydro_fused(const __grid_constant__ 
       hy_constoprim(u1[0], u1[2], u1[1], u1[3], &yq[0], &yq[1], &yq[2], &yq[3]);
       if (tt >= 2) {
         double d[4], yp[4];
-        hy_slope(yq2[0], yq2[1], yq2[2], yq2[3], yq1[0], yq1[1], yq1[2], yq1[3], yq[0], yq[1], yq[2], yq[3], &d[0],
+        const double* yq1 = yqring + ((tt + 1) & 1) * 4 * NT + t;  // row r-1
+        const double* yq2 = yqring + (tt & 1) * 4 * NT + t;        // row r-2
+        hy_slope(yq2[0], yq2[NT], yq2[2 * NT], yq2[3 * NT], yq1[0], yq1[NT], yq1[2 * NT], yq1[3 * NT], yq[0], yq[1],
+                 yq[2], yq[3], &d[0],
                  &d[1], &d[2], &d[3]);
         // minus state of row r-1 is read by the y-face (r-2)+1/2 at C of the next row
-        hy_trace(yq1[0], yq1[1], yq1[2], yq1[3], d[0], d[1], d[2], d[3], dtdx, &yqm[0], &yqm[1], &yqm[2], &yqm[3],
+        hy_trace(yq1[0], yq1[NT], yq1[2 * NT], yq1[3 * NT], d[0], d[1], d[2], d[3], dtdx, &yqm[0], &yqm[1], &yqm[2],
+                 &yqm[3],
                  &yp[0], &yp[1], &yp[2], &yp[3]);
 #pragma unroll
         for (int a = 0; a < 4; ++a) {
@@ -261,8 +266,7 @@ __global__ void __launch_bounds__(NT, MINB) hydro_fused(const __grid_constant__ 
       }
 #pragma unroll
       for (int a = 0; a < 4; ++a) {
-        yq2[a] = yq1[a];
-        yq1[a] = yq[a];
+        yqring[(tt & 1) * 4 * NT + a * NT + t] = yq[a];  // row r over row r-2
         u1ring[(tt % 3) * 4 * NT + a * NT + t] = u1[a];
       }
     }
