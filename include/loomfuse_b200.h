@@ -93,7 +93,7 @@ int lf_plan_create(const char* spec_text, size_t len, const char* filename, lf_p
  * pointer or reference), as `__device__` (or __host__ __device__) functions.
  * A chain that no built-in executor implements is lowered by the generic
  * executor and compiled for sm_100a together with this source and the shipped
- * user-kernel headers (userkernels/*.h), so kernels need no `body:`.
+ * user-kernel headers (the userkernels/ directory), so kernels need no `body:`.
  * kernel_source may be NULL. */
 int lf_plan_create_ex(const char* spec_text, size_t len, const char* filename, const char* kernel_source,
                       size_t kernel_len, lf_plan** out);
@@ -120,9 +120,13 @@ int lf_plan_terminal(const lf_plan* plan, int idx, lf_terminal* out);
 int lf_plan_report(const lf_plan* plan, char* buf, size_t cap, size_t* needed);
 
 /* Name of the fused executor the plan dispatches to, or "" if none: a
- * hand-written sm_100a executor whose chain signature matches, else the
- * generic "jit_tiled_fused" executor (kernels with `body:` expressions,
- * lowered to CUDA and compiled for sm_100a by NVRTC at plan creation). */
+ * hand-written sm_100a executor whose chain signature matches and whose size
+ * constraints hold ("heat3d_fused_tma", "biharm2d_fused_tma",
+ * "box2x_fused_tma", "hydro2d_fused_tma"), else the generic executor, which
+ * lowers the chain to CUDA and compiles it for sm_100a with NVRTC at plan
+ * creation: "jit_window_fused" (2D/3D march with rolling windows),
+ * "jit_tiled_fused" (1D), "jit_nests_fused" (multi-nest plans: reductions and
+ * broadcast splits). */
 const char* lf_plan_executor(const lf_plan* plan);
 
 /* CUDA source the generic executor generated for this plan ("" otherwise). */
@@ -135,13 +139,18 @@ const char* lf_plan_source(const lf_plan* plan);
  * axiom of step s+1, ghost cells are refilled from `boundary:` after every
  * step, and the final state is left in the goal buffers.  Intermediate states
  * ping-pong between the goal buffer and a plan-owned scratch buffer, so the
- * axiom buffers are never written.  One multi-step run per plan at a time. */
+ * axiom buffers are never written -- except in place: passing ONE buffer for
+ * an axiom and its goal that `config: aliases:` declares runs the chain in
+ * place on the generic executor (LF_ERR_UNSUPPORTED otherwise).  One
+ * multi-step run per plan at a time. */
 int lf_run(const lf_plan* plan, void* const* terminals, int nterm, int steps, void* cuda_stream);
 
 /* Same on HOST buffers: copies axioms host->device, runs, copies goals
  * device->host, synchronises.  This is the drop-in for the emitted host
  * function <name>(terminals...) of R/SPEC.md:500.  Device buffers are owned
- * and cached by the plan.  Pinned host memory gives full copy bandwidth. */
+ * and cached by the plan.  Pinned host memory gives full copy bandwidth; a
+ * single step on a large grid is pipelined over row parts (host->device
+ * copies, compute and device->host copies overlap). */
 int lf_run_host(const lf_plan* plan, void* const* terminals, int nterm, int steps);
 
 /* One step on a slab of the outermost loop dimension (multi-GPU row/plane
