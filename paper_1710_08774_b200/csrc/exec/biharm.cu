@@ -28,12 +28,14 @@ constexpr int R = 3;                   // rows per stage (= register-window peri
 
 // Tunable shape: CPL columns per lane (strip = 32*CPL columns), S ring slots,
 // OCC resident CTAs per SM the register budget is sized for.
-template <int CPL_, int S_, int OCC_>
+// R4 = 4: rows staged four at a time and lap2 lagging lap1 by two rows (see
+// biharm_row4), else three at a time with lap2 one row behind.
+template <int CPL_, int S_, int OCC_, int R_ = 3>
 struct Cfg {
-  static constexpr int CPL = CPL_, S = S_, OCC = OCC_;
+  static constexpr int CPL = CPL_, S = S_, OCC = OCC_, RR = R_;
   static constexpr int SW = 32 * CPL;
   static constexpr int BOXW = SW + 2 * H;
-  static constexpr int STAGE_TX = BOXW * R * 8;
+  static constexpr int STAGE_TX = BOXW * RR * 8;
   static constexpr int STAGE_BYTES = (STAGE_TX + 127) / 128 * 128;
   static constexpr int SMEM = S * STAGE_BYTES + S * 8 + 64;
 };
@@ -121,20 +123,93 @@ __device__ __forceinline__ void biharm_row(Win<CPL>& w, const double* row, int t
   for (int h = 0; h < CPL / 2; ++h) st_hint2(orow + CPL * lane + 2 * h, o[2 * h], o[2 * h + 1], pol);
 }
 
+// Four-row variant: windows of four rows (row % 4, rows unrolled by 4) so
+// that lap2 can run two rows behind lap1 -- at marched row r, lap1 makes
+// L(r-1) while lap2 + update consume L(r-4..r-2) and u(r-3), all produced on
+// earlier rows: the two Laplacians of a row are independent dependency
+// chains instead of one chained after the other.
+template <int CPL>
+struct Win4 {
+  double u[4][CPL];
+  double ex[4][2];
+  double L[4][CPL];
+  double lex[4];
+  double uw[4], ue[4];
+  double lw[4], le[4];
+};
+
+template <int CPL, int P>
+__device__ __forceinline__ void biharm_row4(Win4<CPL>& w, const double* row, int t, int lane, int ex_col,
+                                            double* orow, uint64_t pol) {
+  constexpr int C = P, M1 = (P + 3) % 4, M2 = (P + 2) % 4, M3 = (P + 1) % 4;  // rows r, r-1, r-2, r-3 (= r-4: C)
+  {
+#pragma unroll
+    for (int h = 0; h < CPL / 2; ++h) {
+      const double2 a = lds2(row + CPL * lane + H + 2 * h);
+      w.u[C][2 * h] = a.x;
+      w.u[C][2 * h + 1] = a.y;
+    }
+    const double2 e = lds2(row + ex_col);
+    w.ex[C][0] = e.x;
+    w.ex[C][1] = e.y;
+    const double left = __shfl_up_sync(0xffffffffu, w.u[C][CPL - 1], 1);
+    const double right = __shfl_down_sync(0xffffffffu, w.u[C][0], 1);
+    w.uw[C] = lane == 0 ? e.y : left;
+    w.ue[C] = lane == 31 ? e.x : right;
+  }
+  double o[CPL];
+  const bool out_row = t >= 6;  // marched rows start at jb-3: output row r-3 >= jb
+  if (out_row) {
+    // ---- lap2 + update at row r-3 from L rows r-4 (slot C), r-3 (M3), r-2 (M2): all from earlier rows
+    const double* L0 = w.L[M3];
+#pragma unroll
+    for (int c = 0; c < CPL; ++c) {
+      double l2;
+      lap5(c == 0 ? w.lw[M3] : L0[c - 1], c == CPL - 1 ? w.le[M3] : L0[c + 1], w.L[C][c], w.L[M2][c], L0[c], &l2);
+      biharm_update(w.u[M3][c], l2, &o[c]);
+    }
+  }
+  if (t >= 2) {
+    // ---- lap1 at row r-1 into slot M1 (slot C keeps L(r-4) for the lap2 above)
+    const double* um = w.u[M1];
+    double* Ln = w.L[M1];
+#pragma unroll
+    for (int c = 0; c < CPL; ++c)
+      lap5(c == 0 ? w.uw[M1] : um[c - 1], c == CPL - 1 ? w.ue[M1] : um[c + 1], w.u[M2][c], w.u[C][c], um[c], &Ln[c]);
+    const bool lo = lane == 0;
+    const double hw = lo ? w.ex[M1][0] : um[CPL - 1];
+    const double he = lo ? um[0] : w.ex[M1][1];
+    const int hc = lo ? 1 : 0;
+    const double hs = hc ? w.ex[M2][1] : w.ex[M2][0];
+    const double hn = hc ? w.ex[C][1] : w.ex[C][0];
+    const double h0 = hc ? w.ex[M1][1] : w.ex[M1][0];
+    lap5(hw, he, hs, hn, h0, &w.lex[M1]);
+    const double left = __shfl_up_sync(0xffffffffu, Ln[CPL - 1], 1);
+    const double right = __shfl_down_sync(0xffffffffu, Ln[0], 1);
+    w.lw[M1] = lane == 0 ? w.lex[M1] : left;
+    w.le[M1] = lane == 31 ? w.lex[M1] : right;
+  }
+  if (out_row) {
+#pragma unroll
+    for (int h = 0; h < CPL / 2; ++h) st_hint2(orow + CPL * lane + 2 * h, o[2 * h], o[2 * h + 1], pol);
+  }
+}
+
 template <class K>
 __global__ void __launch_bounds__(32, K::OCC)
     biharm_fused(const __grid_constant__ CUtensorMap tin, double* __restrict__ out, const Params p) {
   constexpr int CPL = K::CPL, S = K::S, SW = K::SW, BOXW = K::BOXW, STAGE_BYTES = K::STAGE_BYTES;
-  constexpr int STAGE_TX = K::STAGE_TX;
+  constexpr int STAGE_TX = K::STAGE_TX, RR = K::RR;
   extern __shared__ __align__(128) unsigned char smem[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + S * STAGE_BYTES);
   const int lane = threadIdx.x;
 
   RowSeg seg[3];
   const int nseg = cta_segments(blockIdx.x, gridDim.x, p.strips, p.row_lo, p.row_hi, seg);
-  RowRing<R, S> rr;
-  // staged column 0 = logical i0 - 2 = storage i0; storage row = logical + 2
-  rr.init(seg, nseg, H, smem, full, STAGE_BYTES, STAGE_TX, 0, H, SW);
+  RowRing<RR, S> rr;
+  // staged column 0 = logical i0 - 2 = storage i0; storage row = logical + 2;
+  // the four-row variant marches one more row (its output lags by three)
+  rr.init(seg, nseg, RR == 4 ? H + 1 : H, smem, full, STAGE_BYTES, STAGE_TX, 0, H, SW);
   if (lane == 0) {
     for (int s = 0; s < S; ++s) mbar_init(&full[s], 1);
     fence_barrier_init();
@@ -149,27 +224,8 @@ __global__ void __launch_bounds__(32, K::OCC)
   const uint64_t pol = l2_evict_first_policy();
   // extra columns: lane 0 -> logical -2,-1 ; lane 31 -> SW, SW+1 ; others: harmless copy
   const int ex_col = lane == 0 ? 0 : (lane == 31 ? SW + H : CPL * lane + H);
-  int g = 0;
-  Win<CPL> w;
-  for (int k = 0; k < nseg; ++k) {
-    const RowSeg sg = seg[k];
-    const int T = sg.je - sg.jb + 2 * H;  // rows jb-2 .. je+1
-    // output row r-2 of marched row r = jb-2+t lives at storage row (jb-2+t-2)+2
-    double* orow = out + (long long)(sg.jb - 2) * p.pitch + H + sg.strip * SW;
-    for (int t0 = 0; t0 < T; t0 += R, ++g) {
-      rr.wait(g);
-      const double* st = reinterpret_cast<const double*>(rr.stage(g));
-      biharm_row<CPL, 0>(w, st, t0, lane, ex_col, orow, pol);
-      orow += p.pitch;
-      if (t0 + 1 < T) biharm_row<CPL, 1>(w, st + BOXW, t0 + 1, lane, ex_col, orow, pol);
-      orow += p.pitch;
-      if (t0 + 2 < T) biharm_row<CPL, 2>(w, st + 2 * BOXW, t0 + 2, lane, ex_col, orow, pol);
-      orow += p.pitch;
-      // every lane has consumed this stage: hand the slot to stage g + S
-      __syncwarp();
-      if (lane == 0) rr.issue(g + S, &tin);
-    }
-    // zero ghost ring of the goal buffer at the global edges
+  // zero ghost ring of the goal buffer at the global edges
+  auto ghost_ring = [&](const RowSeg& sg) {
     const bool lo_edge = sg.strip == 0, hi_edge = sg.strip == p.strips - 1;
     for (int jo = sg.jb; jo < sg.je; jo += 32) {
       const int j = jo + lane;
@@ -190,8 +246,56 @@ __global__ void __launch_bounds__(32, K::OCC)
         if (lane == 31 && hi_edge) st_hint2(o + SW, 0.0, 0.0, pol);
       }
     }
+  };
+  int g = 0;
+  if constexpr (RR == 3) {
+  Win<CPL> w;
+  for (int k = 0; k < nseg; ++k) {
+    const RowSeg sg = seg[k];
+    const int T = sg.je - sg.jb + 2 * H;  // rows jb-2 .. je+1
+    // output row r-2 of marched row r = jb-2+t lives at storage row (jb-2+t-2)+2
+    double* orow = out + (long long)(sg.jb - 2) * p.pitch + H + sg.strip * SW;
+    for (int t0 = 0; t0 < T; t0 += 3, ++g) {
+      rr.wait(g);
+      const double* st = reinterpret_cast<const double*>(rr.stage(g));
+      biharm_row<CPL, 0>(w, st, t0, lane, ex_col, orow, pol);
+      orow += p.pitch;
+      if (t0 + 1 < T) biharm_row<CPL, 1>(w, st + BOXW, t0 + 1, lane, ex_col, orow, pol);
+      orow += p.pitch;
+      if (t0 + 2 < T) biharm_row<CPL, 2>(w, st + 2 * BOXW, t0 + 2, lane, ex_col, orow, pol);
+      orow += p.pitch;
+      // every lane has consumed this stage: hand the slot to stage g + S
+      __syncwarp();
+      if (lane == 0) rr.issue(g + S, &tin);
+    }
+    ghost_ring(sg);
+  }
+  } else {
+  Win4<CPL> w;
+  for (int k = 0; k < nseg; ++k) {
+    const RowSeg sg = seg[k];
+    // rows jb-3 .. je+2 (the ring stages from jb-3: halo H+1); output row r-3
+    const int T = sg.je - sg.jb + 2 * H + 2;
+    double* orow = out + (long long)(sg.jb - 4) * p.pitch + H + sg.strip * SW;
+    for (int t0 = 0; t0 < T; t0 += 4, ++g) {
+      rr.wait(g);
+      const double* st = reinterpret_cast<const double*>(rr.stage(g));
+      biharm_row4<CPL, 0>(w, st, t0, lane, ex_col, orow, pol);
+      orow += p.pitch;
+      if (t0 + 1 < T) biharm_row4<CPL, 1>(w, st + BOXW, t0 + 1, lane, ex_col, orow, pol);
+      orow += p.pitch;
+      if (t0 + 2 < T) biharm_row4<CPL, 2>(w, st + 2 * BOXW, t0 + 2, lane, ex_col, orow, pol);
+      orow += p.pitch;
+      if (t0 + 3 < T) biharm_row4<CPL, 3>(w, st + 3 * BOXW, t0 + 3, lane, ex_col, orow, pol);
+      orow += p.pitch;
+      __syncwarp();
+      if (lane == 0) rr.issue(g + S, &tin);
+    }
+    ghost_ring(sg);
+  }
   }
 }
+
 
 // variant table (LF_BIHARM_VARIANT=<index> overrides the default for tuning runs)
 struct Variant {
@@ -199,10 +303,11 @@ struct Variant {
   int sw;
   void (*kernel)(CUtensorMap, double*, Params);
   int smem, occ;
+  int rows;  // rows per TMA stage (3 or 4)
 };
 template <class K>
 Variant make_variant(const char* n) {
-  return {n, K::SW, biharm_fused<K>, K::SMEM, K::OCC};
+  return {n, K::SW, biharm_fused<K>, K::SMEM, K::OCC, K::RR};
 }
 const Variant& variant() {
   static const Variant table[] = {
@@ -213,12 +318,16 @@ const Variant& variant() {
       make_variant<Cfg<4, 6, 10>>("cpl4_s6_occ10"), make_variant<Cfg<2, 10, 12>>("cpl2_s10_occ12"),
       make_variant<Cfg<2, 8, 12>>("cpl2_s8_occ12"), make_variant<Cfg<2, 12, 12>>("cpl2_s12_occ12"),
       make_variant<Cfg<2, 16, 10>>("cpl2_s16_occ10"), make_variant<Cfg<2, 6, 16>>("cpl2_s6_occ16"),
+      make_variant<Cfg<2, 9, 10, 4>>("cpl2_r4_s9_occ10"), make_variant<Cfg<2, 6, 12, 4>>("cpl2_r4_s6_occ12"),
+      make_variant<Cfg<2, 12, 8, 4>>("cpl2_r4_s12_occ8"), make_variant<Cfg<4, 6, 8, 4>>("cpl4_r4_s6_occ8"),
+      make_variant<Cfg<2, 6, 14, 4>>("cpl2_r4_s6_occ14"), make_variant<Cfg<2, 5, 14, 4>>("cpl2_r4_s5_occ14"),
+      make_variant<Cfg<2, 8, 12, 4>>("cpl2_r4_s8_occ12"), make_variant<Cfg<2, 7, 12, 4>>("cpl2_r4_s7_occ12"),
   };
   static int idx = [] {
     const char* e = std::getenv("LF_BIHARM_VARIANT");
-    // default cpl2_s12_occ10: best of the measured sweep (profiles/r01_biharm_variants.txt)
-    int i = e ? std::atoi(e) : 7;
-    return (i >= 0 && i < (int)(sizeof table / sizeof table[0])) ? i : 7;
+    // default cpl2_r4_s7_occ12: best of the measured sweep (profiles/r01_biharm_variants.txt)
+    int i = e ? std::atoi(e) : 21;
+    return (i >= 0 && i < (int)(sizeof table / sizeof table[0])) ? i : 21;
   }();
   return table[idx];
 }
@@ -253,7 +362,7 @@ int launch_step(const double* in, double* out, int ni, const RowPart& rp, cudaSt
   }
   CUtensorMap map;
   uint64_t dims[2] = {(uint64_t)ni + 4, (uint64_t)nj + 4};
-  uint32_t box[2] = {(uint32_t)(v.sw + 2 * H), R};
+  uint32_t box[2] = {(uint32_t)(v.sw + 2 * H), (uint32_t)v.rows};  // must match the kernel's stage bytes
   if (!make_tensor_map(&map, in, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 8, 2, dims, box, err)) return LF_ERR_CUDA;
   Params p;
   p.ni = ni;
