@@ -409,7 +409,12 @@ def main():
     # one pass over the grid per step, except where the executor fuses time
     # steps (heat3d: two-step passes on a whole domain); slabs step singly
     passes = plan.grid_passes(w["chain_steps"]) if world == 1 else w["chain_steps"]
-    launches = plan.launches(w["chain_steps"]) if world == 1 else plan.launches_per_step * w["chain_steps"]
+    if world == 1:
+        launches = plan.launches(w["chain_steps"])
+    elif w["halo"] is None:
+        launches = plan.launches_per_step * w["chain_steps"]
+    else:  # overlapped slab schedule: the two face parts and the interior, every step
+        launches = 3 * plan.launches_per_step * w["chain_steps"]
 
     def barrier():
         if world > 1:
