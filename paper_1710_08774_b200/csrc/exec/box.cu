@@ -10,6 +10,7 @@
 // arrive by TMA into an 8-slot ring; each output row leaves as one 16-B store
 // per lane.  Compulsory traffic: 4 B read + 4 B written per cell.
 #include <algorithm>
+#include <cstdlib>
 
 #include "../../userkernels/stencil_kernels.h"
 #include "common.cuh"
@@ -25,11 +26,14 @@ constexpr int H = 2;                   // chain radius
 constexpr int LPAD = H;                // staged left pad (the box starts at the terminal's first column)
 constexpr int BOXW = SW + 2 * LPAD;    // staged row: 132 floats = 528 B
 constexpr int R = 3;                   // rows per stage (= register-window period)
-constexpr int S = 8;                   // ring slots
 constexpr int STAGE_TX = BOXW * R * 4;
 constexpr int STAGE_BYTES = (STAGE_TX + 127) / 128 * 128;
-constexpr int SMEM = S * STAGE_BYTES + S * 8 + 64;
-constexpr int OCC = 16;
+// tunable: S ring slots, OCC resident CTAs per SM the register budget is sized for
+template <int S_, int OCC_>
+struct BoxCfg {
+  static constexpr int S = S_, OCC = OCC_;
+  static constexpr int SMEM = S * STAGE_BYTES + S * 8 + 64;
+};
 
 struct Params {
   int ni, nj;
@@ -154,8 +158,10 @@ __device__ __forceinline__ bool row_nn(const float* row, int lane, int ex_col) {
   return m <= 0x7EFFFFFFu;
 }
 
-__global__ void __launch_bounds__(32, OCC)
+template <class K>
+__global__ void __launch_bounds__(32, K::OCC)
     box_fused(const __grid_constant__ CUtensorMap tin, float* __restrict__ out, const Params p) {
+  constexpr int S = K::S;
   extern __shared__ __align__(128) unsigned char smem[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + S * STAGE_BYTES);
   const int lane = threadIdx.x;
@@ -224,16 +230,41 @@ bool supports(const lf::Plan& plan, std::string& why) {
   return true;
 }
 
+struct BoxVariant {
+  const char* name;
+  void (*kernel)(CUtensorMap, float*, Params);
+  int smem, occ;
+};
+template <class K>
+BoxVariant box_variant(const char* n) {
+  return {n, box_fused<K>, K::SMEM, K::OCC};
+}
+// LF_BOX_VARIANT=<index> overrides the default for tuning runs
+const BoxVariant& box_variant() {
+  static const BoxVariant table[] = {
+      box_variant<BoxCfg<8, 16>>("s8_occ16"),  box_variant<BoxCfg<6, 20>>("s6_occ20"),
+      box_variant<BoxCfg<12, 12>>("s12_occ12"), box_variant<BoxCfg<10, 14>>("s10_occ14"),
+      box_variant<BoxCfg<6, 24>>("s6_occ24"),  box_variant<BoxCfg<4, 24>>("s4_occ24"),
+  };
+  static int idx = [] {
+    const char* e = std::getenv("LF_BOX_VARIANT");
+    int i = e ? std::atoi(e) : 0;
+    return (i >= 0 && i < (int)(sizeof table / sizeof table[0])) ? i : 0;
+  }();
+  return table[idx];
+}
+
 int run(const ExecArgs& a, std::string& err) {
+  const BoxVariant& v = box_variant();
   static int slots = 0;
   if (!slots) {
-    cudaError_t e = cudaFuncSetAttribute(box_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
+    cudaError_t e = cudaFuncSetAttribute(v.kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, v.smem);
     if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(box)", err);
     int dev = 0, sms = 148, per_sm = 1;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, box_fused, 32, SMEM);
-    slots = sms * std::max(1, std::min(per_sm, OCC));
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, v.kernel, 32, v.smem);
+    slots = sms * std::max(1, std::min(per_sm, v.occ));
   }
   const auto& r = a.plan->rs.ranges;
   const int ni = (int)r[1].trips();
@@ -258,7 +289,7 @@ int run(const ExecArgs& a, std::string& err) {
   }
   // a single pass; `steps` re-applies the same pass (no iterate pairs)
   for (int s = 0; s < a.steps; ++s) {
-    box_fused<<<ctas, 32, SMEM, a.stream>>>(map, static_cast<float*>(a.terms[1]), p);
+    v.kernel<<<ctas, 32, v.smem, a.stream>>>(map, static_cast<float*>(a.terms[1]), p);
     int st = cuda_status(cudaGetLastError(), "box_fused launch", err);
     if (st != LF_OK) return st;
   }
