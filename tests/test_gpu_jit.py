@@ -38,6 +38,9 @@ CASES = {
                                    "g_zero": np.random.default_rng(4).random(37) * 0.1},
     "colsum_body": lambda: {"g_u": np.random.default_rng(5).random((47, 72)), "g_z": np.zeros(70),
                             "g_k": np.array([0.3])},
+    # a full reduction to a scalar (both loop dims, loop order) and its broadcast
+    "meansub_body": lambda: {"g_u": np.random.default_rng(7).random((23, 57)), "g_z": np.array([0.0]),
+                             "g_inv": np.array([1.0 / (23 * 57)])},
 }
 
 
