@@ -296,6 +296,9 @@ def main():
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-e2e", action="store_true", help="skip the end-to-end leg")
     ap.add_argument("--cpu-budget", type=float, default=10.0)
+    ap.add_argument("--slab-exchange", choices=["native", "torch"], default="native",
+                    help="multi-GPU halo exchange: lf_run_slabs (NCCL issued by the library, default) or "
+                         "torch.distributed P2P around lf_run_slab")
     ap.add_argument("--force-slabs", action="store_true",
                     help="testing: run the multi-GPU slab path (overlapped NCCL schedule) even on one GPU")
     args = ap.parse_args()
@@ -403,6 +406,13 @@ def main():
             def one_step():
                 for _ in range(w["chain_steps"]):
                     plan.run_slab(d_ax + d_goal, lo, hi, n0, stream=stream)
+        elif args.slab_exchange == "native":
+            # lf_run_slabs: faces first, NCCL send/recv of the faces on the
+            # library's side stream overlapped with the interior, per step
+            comm = lf.NcclComm.from_group(rank, world)
+
+            def one_step():
+                plan.run_slabs(d_ax + d_goal, comm, steps=w["chain_steps"], stream=stream)
         else:
             halo = slabs.Halo(*w["halo"])
             cur = [d_ax[i] for i in state]
@@ -486,7 +496,9 @@ def main():
         "vs_baseline": None, "dtype": w["dtype"], "data": "synthetic (seeded splitmix64, BASELINE.json shapes)",
         "config": {"workload": workload, "executor": plan.executor, "l2": "inputs larger than L2 (126 MB)",
                    "in_place": bool(w.get("inplace")),
-                   "parallelism": f"slab{world}" if slab_mode else "single-gpu"},
+                   "parallelism": f"slab{world}" if slab_mode else "single-gpu",
+                   **({"halo_exchange": args.slab_exchange if w["halo"] is not None else "none"}
+                      if slab_mode else {})},
         "roofline": roofline, "gpu_launches": launches * args.steps, "clocks": clk.summary(),
     }
 

@@ -158,6 +158,38 @@ int lf_run_host(const lf_plan* plan, void* const* terminals, int nterm, int step
 int lf_run_slab(const lf_plan* plan, void* const* terminals, int nterm, const lf_slab* slab,
                 void* cuda_stream);
 
+/* Native multi-GPU run: `steps` steps of rank `rank`'s slab
+ * of a `world`-rank decomposition of the outermost loop dimension -- rows
+ * [n*rank/world, n*(rank+1)/world) -- on device buffers sized for that slab
+ * (the planner's extents with the slab's row count along dim 0).  `nccl_comm`
+ * is an ncclComm_t of `world` ranks, one per GPU.  Every step computes the
+ * output rows the neighbours need first, exchanges them by NCCL send/recv on
+ * a library-owned high-priority stream (ring-wrapped when the boundary of
+ * dim 0 is periodic) while the interior rows are computed on `cuda_stream`,
+ * and orders the next step after both.  Iterated state ping-pongs through
+ * slab-sized plan scratch; the final state is left in the goal buffers.  NCCL
+ * is loaded at run time (libnccl.so.2; the process's copy when one is
+ * loaded).  Replaces the reference's external outer-level parallelism
+ * (R/PAPER.md:499). */
+int lf_run_slabs(const lf_plan* plan, void* nccl_comm, int rank, int world, void* const* terminals, int nterm,
+                 int steps, void* cuda_stream);
+
+/* The same decomposition with all `world` ranks on the current GPU, the
+ * exchange done by device copies: `terminals` holds world * nterm device
+ * pointers, rank-major.  Same geometry and schedule as lf_run_slabs, for
+ * testing the slab path on one GPU. */
+int lf_run_slabs_local(const lf_plan* plan, int world, void* const* terminals, int nterm, int steps,
+                       void* cuda_stream);
+
+/* NCCL communicator helpers for lf_run_slabs (the handles are ncclComm_t):
+ * a 128-byte unique id made on one rank and shared out of band, one rank's
+ * communicator from it, a one-rank communicator on the current device, and
+ * destruction. */
+int lf_nccl_unique_id(char id[128]);
+int lf_nccl_comm_init_rank(void** nccl_comm, int world, const char id[128], int rank);
+int lf_nccl_comm_init_single(void** nccl_comm);
+int lf_nccl_comm_destroy(void* nccl_comm);
+
 /* Bench accounting.  lf_plan_launches_per_step: kernel launches of one
  * single-step pass; lf_plan_compulsory_bytes_per_cell: algorithmic HBM bytes
  * per cell of one pass over the grid (terminals read once + written once);

@@ -39,6 +39,8 @@ ABI_SYMBOLS = (
     "lf_plan_launches_per_step", "lf_plan_compulsory_bytes_per_cell", "lf_plan_grid_passes", "lf_plan_launches",
     "lf_last_error",
     "lf_version", "lf_spec_print", "lf_plan_source",
+    "lf_run_slabs", "lf_run_slabs_local", "lf_nccl_unique_id", "lf_nccl_comm_init_rank",
+    "lf_nccl_comm_init_single", "lf_nccl_comm_destroy",
 )
 
 
@@ -100,6 +102,12 @@ def lib() -> ctypes.CDLL:
     L.lf_run.argtypes = [P, ctypes.POINTER(P), ctypes.c_int, ctypes.c_int, P]
     L.lf_run_host.argtypes = [P, ctypes.POINTER(P), ctypes.c_int, ctypes.c_int]
     L.lf_run_slab.argtypes = [P, ctypes.POINTER(P), ctypes.c_int, ctypes.POINTER(_Slab), P]
+    L.lf_run_slabs.argtypes = [P, P, ctypes.c_int, ctypes.c_int, ctypes.POINTER(P), ctypes.c_int, ctypes.c_int, P]
+    L.lf_run_slabs_local.argtypes = [P, ctypes.c_int, ctypes.POINTER(P), ctypes.c_int, ctypes.c_int, P]
+    L.lf_nccl_unique_id.argtypes = [ctypes.c_char_p]
+    L.lf_nccl_comm_init_rank.argtypes = [ctypes.POINTER(P), ctypes.c_int, ctypes.c_char_p, ctypes.c_int]
+    L.lf_nccl_comm_init_single.argtypes = [ctypes.POINTER(P)]
+    L.lf_nccl_comm_destroy.argtypes = [P]
     L.lf_plan_launches_per_step.argtypes = [P]
     L.lf_plan_compulsory_bytes_per_cell.argtypes = [P]
     L.lf_plan_compulsory_bytes_per_cell.restype = ctypes.c_double
@@ -270,6 +278,83 @@ class Plan:
         slab = _Slab(lo, hi, global_, p0, p1)
         _check(lib().lf_run_slab(self._h, self._ptrs(bufs), len(bufs), ctypes.byref(slab),
                                  _stream_handle(stream)))
+
+    def run_slabs(self, bufs: Sequence[Any], comm: "NcclComm", steps: int = 1, stream: Any = None) -> None:
+        """This rank's slab for `steps` steps, NCCL halo exchange inside (see run_slabs)."""
+        run_slabs(self, bufs, comm, steps, stream)
+
+    def slab_terminal_extent(self, idx: int, lo: int, hi: int, n0: int) -> tuple[int, ...]:
+        """Extent of terminal `idx` for a slab of rows [lo, hi) of an outer
+        dimension of n0 rows: the planner's halo with hi-lo rows."""
+        t = self.terminals[idx]
+        if not t.extent:
+            return ()
+        return (t.extent[0] - n0 + (hi - lo),) + tuple(t.extent[1:])
+
+
+class NcclComm:
+    """An NCCL communicator for ``Plan.run_slabs`` (one rank per GPU).
+
+    ``NcclComm.single()`` makes a one-rank communicator on the current device;
+    ``NcclComm.from_group(rank, world)`` creates one rank of a ``world``-rank
+    communicator, the unique id broadcast from rank 0 over the default
+    ``torch.distributed`` group (the plumbing only: the exchange itself is
+    issued by the library)."""
+
+    def __init__(self, handle: int, rank: int, world: int):
+        self.handle, self.rank, self.world = handle, rank, world
+
+    @staticmethod
+    def unique_id() -> bytes:
+        buf = ctypes.create_string_buffer(128)
+        _check(lib().lf_nccl_unique_id(buf))
+        return buf.raw
+
+    @classmethod
+    def init_rank(cls, world: int, uid: bytes, rank: int) -> "NcclComm":
+        h = ctypes.c_void_p()
+        _check(lib().lf_nccl_comm_init_rank(ctypes.byref(h), world, uid, rank))
+        return cls(h.value, rank, world)
+
+    @classmethod
+    def single(cls) -> "NcclComm":
+        h = ctypes.c_void_p()
+        _check(lib().lf_nccl_comm_init_single(ctypes.byref(h)))
+        return cls(h.value, 0, 1)
+
+    @classmethod
+    def from_group(cls, rank: int, world: int) -> "NcclComm":
+        import torch.distributed as dist
+        obj = [cls.unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        return cls.init_rank(world, obj[0], rank)
+
+    def destroy(self) -> None:
+        if self.handle:
+            _check(lib().lf_nccl_comm_destroy(self.handle))
+            self.handle = None
+
+
+def run_slabs(plan: "Plan", bufs: Sequence[Any], comm: NcclComm, steps: int = 1, stream: Any = None) -> None:
+    """``steps`` steps of this rank's slab (lf_run_slabs): rows
+    [n*rank/world, n*(rank+1)/world) of the outer dimension, buffers sized for
+    the slab, faces exchanged with the neighbours by NCCL overlapped with the
+    interior rows, the final state in the goal buffers."""
+    _check(lib().lf_run_slabs(plan._h, comm.handle, comm.rank, comm.world, plan._ptrs(bufs), len(bufs), steps,
+                              _stream_handle(stream)))
+
+
+def run_slabs_local(plan: "Plan", rank_bufs: Sequence[Sequence[Any]], steps: int = 1, stream: Any = None) -> None:
+    """All ranks of a slab decomposition on the current GPU, the exchange as
+    device copies (lf_run_slabs_local): the same schedule and halo geometry as
+    ``run_slabs``, testable on one GPU."""
+    nterm = len(plan.terminals)
+    if any(len(b) != nterm for b in rank_bufs):
+        raise ValueError(f"expected {nterm} buffers per rank (axioms then goals)")
+    flat = [_ptr(b) for bufs in rank_bufs for b in bufs]
+    arr = (ctypes.c_void_p * len(flat))(*flat)
+    _check(lib().lf_run_slabs_local(plan._h, len(rank_bufs), arr, nterm, steps,
+                                    _stream_handle(stream)))
 
 
 def print_spec(text: str, filename: str = "<input>") -> str:

@@ -7,7 +7,10 @@
 #include <algorithm>
 #include <cstdlib>
 #include <cstring>
+#include <dlfcn.h>
+#include <nccl.h>
 #include <memory>
+#include <functional>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -66,6 +69,9 @@ struct lf_plan {
   std::vector<void*> scratch;  // per goal; iterated goals only
   cudaStream_t stream = nullptr;
   cudaStream_t h2d = nullptr, d2h = nullptr;  // copy streams of the pipelined host path
+  cudaStream_t comm = nullptr;                // halo-exchange stream of lf_run_slabs
+  std::vector<void*> slab_scratch;            // lf_run_slabs ping-pong buffers (slab-sized)
+  std::vector<int64_t> slab_scratch_bytes;
   ~lf_plan() {
     for (void* p : dev)
       if (p) cudaFree(p);
@@ -74,10 +80,224 @@ struct lf_plan {
     if (stream) cudaStreamDestroy(stream);
     if (h2d) cudaStreamDestroy(h2d);
     if (d2h) cudaStreamDestroy(d2h);
+    if (comm) cudaStreamDestroy(comm);
+    for (void* p : slab_scratch)
+      if (p) cudaFree(p);
   }
 };
 
 namespace {
+
+// ---- NCCL through dlopen: no link-time dependency; the process's copy (e.g.
+// the one PyTorch loaded) is reused when present
+struct NcclApi {
+  void* h = nullptr;
+  ncclResult_t (*group_start)() = nullptr;
+  ncclResult_t (*group_end)() = nullptr;
+  ncclResult_t (*send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*unique_id)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*init_rank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*init_all)(ncclComm_t*, int, const int*) = nullptr;
+  ncclResult_t (*destroy)(ncclComm_t) = nullptr;
+  const char* (*error_string)(ncclResult_t) = nullptr;
+  std::string error;
+};
+
+const NcclApi& nccl() {
+  static NcclApi n;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    n.h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+    if (!n.h) n.h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_LOCAL);
+    if (!n.h) {
+      n.error = "libnccl.so.2 not found";
+      return;
+    }
+    auto sym = [&](const char* name) { return dlsym(n.h, name); };
+    n.group_start = reinterpret_cast<decltype(n.group_start)>(sym("ncclGroupStart"));
+    n.group_end = reinterpret_cast<decltype(n.group_end)>(sym("ncclGroupEnd"));
+    n.send = reinterpret_cast<decltype(n.send)>(sym("ncclSend"));
+    n.recv = reinterpret_cast<decltype(n.recv)>(sym("ncclRecv"));
+    n.unique_id = reinterpret_cast<decltype(n.unique_id)>(sym("ncclGetUniqueId"));
+    n.init_rank = reinterpret_cast<decltype(n.init_rank)>(sym("ncclCommInitRank"));
+    n.init_all = reinterpret_cast<decltype(n.init_all)>(sym("ncclCommInitAll"));
+    n.destroy = reinterpret_cast<decltype(n.destroy)>(sym("ncclCommDestroy"));
+    n.error_string = reinterpret_cast<decltype(n.error_string)>(sym("ncclGetErrorString"));
+    if (!n.group_start || !n.group_end || !n.send || !n.recv || !n.unique_id || !n.init_rank || !n.init_all ||
+        !n.destroy)
+      n.error = "libnccl.so.2 lacks the point-to-point API";
+  });
+  return n;
+}
+
+int nccl_status(ncclResult_t r, const char* what, std::string& err) {
+  if (r == ncclSuccess) return LF_OK;
+  const NcclApi& n = nccl();
+  err = std::string(what) + ": " + (n.error_string ? n.error_string(r) : ("ncclResult " + std::to_string(r)));
+  return LF_ERR_CUDA;
+}
+
+// ---- slab runs (lf_run_slabs): halo geometry and the overlapped schedule ----
+
+// Per terminal: the iterate pairing (goal -> axiom index) and, along the
+// outermost dim, the storage row size and the ghost rows below/above the
+// slab's own rows; whether dim 0 wraps (periodic boundary).
+struct SlabGeom {
+  std::vector<int> paired;
+  std::vector<int64_t> rb;
+  std::vector<long> below, above;
+  std::vector<char> periodic;
+  long halo_lo = 0, halo_hi = 0;  // max ghost rows below / above over the iterated terminals
+  long n0 = 0;
+};
+
+SlabGeom slab_geom(const lf::Plan& P) {
+  const auto& T = P.terminals;
+  const auto& rs = P.rs;
+  SlabGeom g;
+  g.n0 = rs.ranges[0].trips();
+  const long lo0 = rs.ranges[0].lo;
+  g.paired.assign(T.size(), -1);
+  g.rb.assign(T.size(), 0);
+  g.below.assign(T.size(), 0);
+  g.above.assign(T.size(), 0);
+  g.periodic.assign(T.size(), 0);
+  for (const auto& [gname, aname] : rs.iterate)
+    for (size_t i = 0; i < T.size(); ++i)
+      for (size_t a = 0; a < T.size(); ++a)
+        if (T[i].is_goal && T[i].name == gname && !T[a].is_goal && T[a].name == aname) g.paired[i] = (int)a;
+  for (size_t i = 0; i < T.size(); ++i) {
+    const auto& t = T[i];
+    if (t.extent.empty()) continue;
+    int64_t rb = t.elem_bytes;
+    for (size_t k = 1; k < t.extent.size(); ++k) rb *= t.extent[k];
+    g.rb[i] = rb;
+    g.below[i] = lo0 - t.base[0];
+    g.above[i] = t.extent[0] - g.n0 - g.below[i];
+    auto it = rs.boundary.find(t.name);
+    if (it == rs.boundary.end()) it = rs.boundary.find("*");
+    g.periodic[i] = it != rs.boundary.end() && !it->second.empty() && it->second[0] == lf::Boundary::periodic;
+    if (g.paired[i] >= 0) {
+      g.halo_lo = std::max(g.halo_lo, g.below[i]);
+      g.halo_hi = std::max(g.halo_hi, g.above[i]);
+    }
+  }
+  return g;
+}
+
+struct RankState {
+  int rank = 0;
+  long lo = 0, hi = 0;
+  void* const* terms = nullptr;
+  std::vector<void*> scratch;    // per terminal; iterated goals only
+  std::vector<void*> cur, bufs;  // this step's inputs / outputs
+};
+
+std::vector<int64_t> scratch_need(const SlabGeom& g, const RankState& r) {
+  std::vector<int64_t> need(g.paired.size(), 0);
+  for (size_t i = 0; i < g.paired.size(); ++i)
+    if (g.paired[i] >= 0) need[i] = g.rb[i] * (r.hi - r.lo + g.below[i] + g.above[i]);
+  return need;
+}
+
+int alloc_list(const std::vector<int64_t>& need, std::vector<void*>& out, std::string& err) {
+  out.assign(need.size(), nullptr);
+  for (size_t i = 0; i < need.size(); ++i)
+    if (need[i]) {
+      cudaError_t e = cudaMalloc(&out[i], need[i]);
+      if (e != cudaSuccess) {
+        for (void* q : out)
+          if (q) cudaFree(q);
+        out.clear();
+        return lfx::cuda_status(e, "cudaMalloc(slab scratch)", err);
+      }
+    }
+  return LF_OK;
+}
+
+int make_side_stream(cudaStream_t* s, std::string& err) {
+  int lowp = 0, highp = 0;
+  cudaDeviceGetStreamPriorityRange(&lowp, &highp);
+  cudaError_t e = cudaStreamCreateWithPriority(s, cudaStreamNonBlocking, highp);
+  return e == cudaSuccess ? LF_OK : lfx::cuda_status(e, "cudaStreamCreate", err);
+}
+
+int slab_check(const lf_plan* plan, const SlabGeom& g, int world, std::string& err) {
+  if (plan->plan.rs.ranges.empty()) {
+    err = "slab runs need a loop dimension";
+    return LF_ERR_UNSUPPORTED;
+  }
+  if (plan->jit && !plan->jit->program().nest_kernels.empty()) {
+    err = "multi-nest plans (reductions) run on the whole domain only";
+    return LF_ERR_UNSUPPORTED;
+  }
+  if (g.n0 < world) {
+    err = "more ranks than rows along the outer dimension";
+    return LF_ERR_SPEC;
+  }
+  return LF_OK;
+}
+
+// The overlapped schedule of every step, for each local rank: the output rows
+// its neighbours need ([0, halo_hi) and [rows - halo_lo, rows)) first, then
+// the exchange on `side` while the interior rows are computed on `stream`;
+// the next step waits for both.  Iterated goals ping-pong between the goal
+// buffers and the rank's scratch so the last step lands in the goals.
+int run_slabs_core(lf_plan* plan, const SlabGeom& g, std::vector<RankState>& R, int steps, cudaStream_t stream,
+                   cudaStream_t side,
+                   const std::function<int(std::vector<RankState>&, cudaStream_t, std::string&)>& exchange,
+                   std::string& err) {
+  const size_t nt = g.paired.size();
+  for (auto& r : R) r.cur.assign(r.terms, r.terms + nt);
+  cudaEvent_t faces_done, exchanged;
+  cudaEventCreateWithFlags(&faces_done, cudaEventDisableTiming);
+  cudaEventCreateWithFlags(&exchanged, cudaEventDisableTiming);
+  auto launch = [&](RankState& r, long plo, long phi) {
+    lf_slab slab{r.lo, r.hi, g.n0, plo, phi};
+    lfx::ExecArgs ea;
+    ea.plan = &plan->plan;
+    ea.terms = r.bufs.data();
+    ea.steps = 1;
+    ea.stream = stream;
+    ea.slab = &slab;
+    return plan->exec ? plan->exec->run(ea, err) : plan->jit->run(ea, err);
+  };
+  int st = LF_OK;
+  for (int s = 0; s < steps && st == LF_OK; ++s) {
+    const bool to_goal = ((steps - 1 - s) % 2) == 0;
+    for (auto& r : R) {
+      r.bufs = r.cur;
+      for (size_t i = 0; i < nt; ++i)
+        if (plan->plan.terminals[i].is_goal) r.bufs[i] = (to_goal || g.paired[i] < 0) ? r.terms[i] : r.scratch[i];
+    }
+    std::vector<char> split(R.size());
+    for (size_t k = 0; k < R.size() && st == LF_OK; ++k) {
+      const long rows = R[k].hi - R[k].lo;
+      split[k] = rows > g.halo_lo + g.halo_hi && (g.halo_lo || g.halo_hi);
+      if (!split[k]) {
+        st = launch(R[k], 0, rows);
+        continue;
+      }
+      if (g.halo_hi) st = launch(R[k], 0, g.halo_hi);
+      if (st == LF_OK && g.halo_lo) st = launch(R[k], rows - g.halo_lo, rows);
+    }
+    if (st != LF_OK) break;
+    cudaEventRecord(faces_done, stream);
+    cudaStreamWaitEvent(side, faces_done, 0);
+    if ((st = exchange(R, side, err)) != LF_OK) break;
+    cudaEventRecord(exchanged, side);
+    for (size_t k = 0; k < R.size() && st == LF_OK; ++k)
+      if (split[k]) st = launch(R[k], g.halo_hi, R[k].hi - R[k].lo - g.halo_lo);
+    cudaStreamWaitEvent(stream, exchanged, 0);
+    for (auto& r : R)
+      for (size_t i = 0; i < nt; ++i)
+        if (g.paired[i] >= 0) r.cur[g.paired[i]] = r.bufs[i];
+  }
+  cudaEventDestroy(faces_done);
+  cudaEventDestroy(exchanged);
+  return st;
+}
 
 int64_t terminal_bytes(const lf::Terminal& t) {
   int64_t n = t.elem_bytes;
@@ -528,6 +748,195 @@ int lf_run_slab(const lf_plan* cplan, void* const* terms, int nterm, const lf_sl
     a.slab = slab;
     std::string err;
     st = cplan->exec ? cplan->exec->run(a, err) : cplan->jit->run(a, err);
+    if (st != LF_OK) return fail(st, err);
+    return LF_OK;
+  } catch (const std::exception& e) {
+    return fail(LF_ERR_INTERNAL, std::string("internal error: ") + e.what());
+  }
+}
+
+// ---- native multi-GPU: slabs of the outer dimension, NCCL halo exchange ----
+
+int lf_nccl_unique_id(char id[128]) {
+  g_err.clear();
+  const NcclApi& n = nccl();
+  if (!n.error.empty()) return fail(LF_ERR_UNSUPPORTED, n.error);
+  ncclUniqueId u;
+  std::string err;
+  int st = nccl_status(n.unique_id(&u), "ncclGetUniqueId", err);
+  if (st != LF_OK) return fail(st, err);
+  static_assert(sizeof(u.internal) == 128, "NCCL unique id size");
+  std::memcpy(id, u.internal, 128);
+  return LF_OK;
+}
+
+int lf_nccl_comm_init_rank(void** comm, int world, const char id[128], int rank) {
+  g_err.clear();
+  const NcclApi& n = nccl();
+  if (!n.error.empty()) return fail(LF_ERR_UNSUPPORTED, n.error);
+  if (!comm || world < 1 || rank < 0 || rank >= world) return fail(LF_ERR_SPEC, "invalid communicator arguments");
+  ncclUniqueId u;
+  std::memcpy(u.internal, id, 128);
+  ncclComm_t c = nullptr;
+  std::string err;
+  int st = nccl_status(n.init_rank(&c, world, u, rank), "ncclCommInitRank", err);
+  if (st != LF_OK) return fail(st, err);
+  *comm = c;
+  return LF_OK;
+}
+
+int lf_nccl_comm_init_single(void** comm) {
+  g_err.clear();
+  const NcclApi& n = nccl();
+  if (!n.error.empty()) return fail(LF_ERR_UNSUPPORTED, n.error);
+  int dev = 0;
+  cudaGetDevice(&dev);
+  ncclComm_t c = nullptr;
+  std::string err;
+  int st = nccl_status(n.init_all(&c, 1, &dev), "ncclCommInitAll", err);
+  if (st != LF_OK) return fail(st, err);
+  *comm = c;
+  return LF_OK;
+}
+
+int lf_nccl_comm_destroy(void* comm) {
+  g_err.clear();
+  const NcclApi& n = nccl();
+  if (!n.error.empty()) return fail(LF_ERR_UNSUPPORTED, n.error);
+  std::string err;
+  int st = nccl_status(n.destroy(static_cast<ncclComm_t>(comm)), "ncclCommDestroy", err);
+  return st == LF_OK ? LF_OK : fail(st, err);
+}
+
+int lf_run_slabs(const lf_plan* cplan, void* comm, int rank, int world, void* const* terms, int nterm, int steps,
+                 void* cuda_stream) {
+  try {
+    g_err.clear();
+    int st = check_run_args(cplan, terms, nterm, steps);
+    if (st != LF_OK) return st;
+    const NcclApi& n = nccl();
+    if (!n.error.empty()) return fail(LF_ERR_UNSUPPORTED, n.error);
+    if (!comm || world < 1 || rank < 0 || rank >= world) return fail(LF_ERR_SPEC, "invalid communicator arguments");
+    if (shares_buffer(cplan, terms)) return fail(LF_ERR_UNSUPPORTED, "slab runs need distinct axiom and goal buffers");
+    lf_plan* plan = const_cast<lf_plan*>(cplan);
+    std::lock_guard<std::mutex> lk(plan->mu);
+    std::string err;
+    SlabGeom g = slab_geom(plan->plan);
+    if ((st = slab_check(plan, g, world, err)) != LF_OK) return fail(st, err);
+    cudaStream_t stream = static_cast<cudaStream_t>(cuda_stream);
+    if (!plan->comm && (st = make_side_stream(&plan->comm, err)) != LF_OK) return fail(st, err);
+    std::vector<RankState> R(1);
+    R[0].rank = rank;
+    R[0].lo = g.n0 * rank / world;
+    R[0].hi = g.n0 * (rank + 1) / world;
+    R[0].terms = terms;
+    if (steps > 1) {
+      std::vector<int64_t> need = scratch_need(g, R[0]);
+      if (plan->slab_scratch_bytes != need) {
+        for (void* q : plan->slab_scratch)
+          if (q) cudaFree(q);
+        plan->slab_scratch.clear();
+        plan->slab_scratch_bytes.clear();
+        std::vector<void*> fresh;
+        if ((st = alloc_list(need, fresh, err)) != LF_OK) return fail(st, err);
+        plan->slab_scratch = fresh;
+        plan->slab_scratch_bytes = need;
+      }
+      R[0].scratch = plan->slab_scratch;
+    }
+    ncclComm_t c = static_cast<ncclComm_t>(comm);
+    auto exchange = [&](std::vector<RankState>& rs, cudaStream_t side, std::string& e) {
+      RankState& r = rs[0];
+      const long rows = r.hi - r.lo;
+      int s2 = nccl_status(n.group_start(), "ncclGroupStart", e);
+      for (size_t i = 0; i < g.paired.size() && s2 == LF_OK; ++i) {
+        if (g.paired[i] < 0) continue;
+        const int64_t rb = g.rb[i];
+        const long below = g.below[i], above = g.above[i];
+        const int up = r.rank + 1 < world ? r.rank + 1 : (g.periodic[i] ? 0 : -1);
+        const int down = r.rank > 0 ? r.rank - 1 : (g.periodic[i] ? world - 1 : -1);
+        char* d = static_cast<char*>(r.bufs[i]);
+        if (up >= 0 && below)  // my last `below` rows -> up's lower ghosts
+          s2 = nccl_status(n.send(d + rows * rb, below * rb, ncclUint8, up, c, side), "ncclSend", e);
+        if (s2 == LF_OK && down >= 0 && below)  // my lower ghosts <- down's last rows
+          s2 = nccl_status(n.recv(d, below * rb, ncclUint8, down, c, side), "ncclRecv", e);
+        if (s2 == LF_OK && down >= 0 && above)  // my first `above` rows -> down's upper ghosts
+          s2 = nccl_status(n.send(d + below * rb, above * rb, ncclUint8, down, c, side), "ncclSend", e);
+        if (s2 == LF_OK && up >= 0 && above)  // my upper ghosts <- up's first rows
+          s2 = nccl_status(n.recv(d + (below + rows) * rb, above * rb, ncclUint8, up, c, side), "ncclRecv", e);
+      }
+      int s3 = nccl_status(n.group_end(), "ncclGroupEnd", e);
+      return s2 != LF_OK ? s2 : s3;
+    };
+    st = run_slabs_core(plan, g, R, steps, stream, plan->comm, exchange, err);
+    if (st != LF_OK) return fail(st, err);
+    return LF_OK;
+  } catch (const std::exception& e) {
+    return fail(LF_ERR_INTERNAL, std::string("internal error: ") + e.what());
+  }
+}
+
+int lf_run_slabs_local(const lf_plan* cplan, int world, void* const* terms, int nterm, int steps, void* cuda_stream) {
+  try {
+    g_err.clear();
+    if (!cplan) return fail(LF_ERR_SPEC, "null plan");
+    if (world < 1 || !terms) return fail(LF_ERR_SPEC, "invalid rank count");
+    for (int r = 0; r < world; ++r) {
+      int st = check_run_args(cplan, terms + (size_t)r * nterm, nterm, steps);
+      if (st != LF_OK) return st;
+      if (shares_buffer(cplan, terms + (size_t)r * nterm))
+        return fail(LF_ERR_UNSUPPORTED, "slab runs need distinct axiom and goal buffers");
+    }
+    lf_plan* plan = const_cast<lf_plan*>(cplan);
+    std::lock_guard<std::mutex> lk(plan->mu);
+    std::string err;
+    SlabGeom g = slab_geom(plan->plan);
+    int st = slab_check(plan, g, world, err);
+    if (st != LF_OK) return fail(st, err);
+    cudaStream_t stream = static_cast<cudaStream_t>(cuda_stream);
+    if (!plan->comm && (st = make_side_stream(&plan->comm, err)) != LF_OK) return fail(st, err);
+    std::vector<RankState> R(world);
+    std::vector<void*> owned;
+    for (int r = 0; r < world && st == LF_OK; ++r) {
+      R[r].rank = r;
+      R[r].lo = g.n0 * r / world;
+      R[r].hi = g.n0 * (r + 1) / world;
+      R[r].terms = terms + (size_t)r * nterm;
+      if (steps > 1) {
+        st = alloc_list(scratch_need(g, R[r]), R[r].scratch, err);
+        for (void* q : R[r].scratch) owned.push_back(q);
+      }
+    }
+    // the exchange as device copies between the ranks' slabs (all on this GPU)
+    auto exchange = [&](std::vector<RankState>& rs, cudaStream_t side, std::string& e) {
+      for (int r = 0; r < world; ++r)
+        for (size_t i = 0; i < g.paired.size(); ++i) {
+          if (g.paired[i] < 0) continue;
+          const int64_t rb = g.rb[i];
+          const long below = g.below[i], above = g.above[i];
+          const int up = r + 1 < world ? r + 1 : (g.periodic[i] ? 0 : -1);
+          const int down = r > 0 ? r - 1 : (g.periodic[i] ? world - 1 : -1);
+          char* d = static_cast<char*>(rs[r].bufs[i]);
+          const long rows = rs[r].hi - rs[r].lo;
+          cudaError_t ce = cudaSuccess;
+          if (down >= 0 && below) {
+            const long drows = rs[down].hi - rs[down].lo;
+            ce = cudaMemcpyAsync(d, static_cast<char*>(rs[down].bufs[i]) + drows * rb, below * rb,
+                                 cudaMemcpyDeviceToDevice, side);
+          }
+          if (ce == cudaSuccess && up >= 0 && above)
+            ce = cudaMemcpyAsync(d + (below + rows) * rb, static_cast<char*>(rs[up].bufs[i]) + below * rb,
+                                 above * rb, cudaMemcpyDeviceToDevice, side);
+          if (ce != cudaSuccess) return lfx::cuda_status(ce, "cudaMemcpyAsync(halo)", e);
+        }
+      return LF_OK;
+    };
+    if (st == LF_OK) st = run_slabs_core(plan, g, R, steps, stream, plan->comm, exchange, err);
+    if (!owned.empty()) {
+      cudaStreamSynchronize(stream);
+      for (void* q : owned)
+        if (q) cudaFree(q);
+    }
     if (st != LF_OK) return fail(st, err);
     return LF_OK;
   } catch (const std::exception& e) {

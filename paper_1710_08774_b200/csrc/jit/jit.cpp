@@ -324,8 +324,23 @@ int JitKernel::run(const ExecArgs& a, std::string& err) {
   args.n0 = rp.rows;
   args.row_lo = rp.lo;
   args.row_hi = rp.hi;
-  args.top = rp.top;
-  args.bottom = rp.bottom;
+  // ghost rows of dim 0 (the fill kernel's top/bottom regions): refilled by
+  // the part that computes the face rows they mirror -- except a periodic
+  // dim 0, whose images are the far face: on a slab they arrive by the
+  // caller's halo exchange, on a whole domain computed in row parts they are
+  // filled once the last part is done
+  bool periodic0 = false;
+  for (const auto& [gname, mode] : rs.boundary)
+    if (!mode.empty() && mode[0] == lf::Boundary::periodic) periodic0 = true;
+  const bool first_part = rp.lo == 0, last_part = rp.hi == rp.rows;
+  if (!periodic0) {
+    args.top = rp.top && first_part;
+    args.bottom = rp.bottom && last_part;
+  } else if (!a.slab || a.whole_domain_parts) {
+    args.top = args.bottom = last_part;
+  } else {
+    args.top = args.bottom = 0;
+  }
   dim3 grid(1, 1, 1);
   const long rows = rp.hi - rp.lo;
   if (rows <= 0) return LF_OK;
