@@ -23,9 +23,19 @@
 #include "../../userkernels/hydro_kernels.h"
 #include "common.cuh"
 #include "exec.hpp"
+#include "fastmath.cuh"
 #include "rowstream.cuh"
 
 namespace lfx {
+// the same user kernels with branch-free divisions / square roots that flag
+// operands outside their exact range (fastmath.cuh); every call below checks
+// the flag and recomputes with the plain kernels above when it is set
+namespace hf {
+#define HY_FAST 1
+#undef LF_USERKERNELS_HYDRO_H
+#include "../../userkernels/hydro_kernels.h"
+#undef HY_FAST
+}  // namespace hf
 namespace {
 
 constexpr int NT = 128;                // threads per CTA = x-faces per row
@@ -44,6 +54,32 @@ constexpr int XBUF = 4 * NPRIM + 8 * NQ + 4 * NT;  // doubles per x-sweep buffer
 constexpr int U1RING = 3 * 4 * NT;                 // x-swept state of rows r-1..r-3, per column (thread)
 constexpr int YQRING = 2 * 4 * NT;                 // y-sweep prims of rows r-1, r-2, per column
 constexpr int SMEM = S * STAGE_BYTES + XBUF * 8 + (U1RING + YQRING) * 8 + S * 8 + 128;
+
+// out-of-line fallbacks of the fast paths (rarely taken: keep their
+// registers out of the hot loop)
+struct D4 {
+  double v[4];
+};
+__device__ __noinline__ D4 slow_riemann(double rl, double nl, double tl, double pl, double rr, double nr, double tr,
+                                        double pr) {
+  D4 g;
+  hy_riemann(rl, nl, tl, pl, rr, nr, tr, pr, &g.v[0], &g.v[1], &g.v[2], &g.v[3]);
+  return g;
+}
+__device__ __noinline__ D4 slow_constoprim(double r, double mn, double mt, double e) {
+  D4 q;
+  hy_constoprim(r, mn, mt, e, &q.v[0], &q.v[1], &q.v[2], &q.v[3]);
+  return q;
+}
+struct D8 {
+  double v[8];
+};
+__device__ __noinline__ D8 slow_trace(double r, double n, double t, double p, double dr, double dn, double dt,
+                                      double dp, double dtdx) {
+  D8 o;
+  hy_trace(r, n, t, p, dr, dn, dt, dp, dtdx, &o.v[0], &o.v[1], &o.v[2], &o.v[3], &o.v[4], &o.v[5], &o.v[6], &o.v[7]);
+  return o;
+}
 
 struct Params {
   int ni, nj;            // interior of this launch's domain (slab rows for multi-GPU)
@@ -176,9 +212,16 @@ __global__ void __launch_bounds__(NT, MINB) hydro_fused(const __grid_constant__ 
       double* xf = xp + 4 * NQ;         // [4][NT]     face fluxes, face c <-> (i0-1+c)+1/2
 
       // ---- A. x: conservative -> primitive on 131 columns
-      for (int c = t; c < NPRIM; c += NT)
-        hy_constoprim(row[0][c], row[1][c], row[2][c], row[3][c], &xq[c], &xq[NPRIM + c], &xq[2 * NPRIM + c],
-                      &xq[3 * NPRIM + c]);
+      for (int c = t; c < NPRIM; c += NT) {
+        unsigned bad = 0;
+        hf::hy_constoprim(row[0][c], row[1][c], row[2][c], row[3][c], &xq[c], &xq[NPRIM + c], &xq[2 * NPRIM + c],
+                          &xq[3 * NPRIM + c], &bad);
+        if (bad) {
+          const D4 q = slow_constoprim(row[0][c], row[1][c], row[2][c], row[3][c]);
+#pragma unroll
+          for (int a = 0; a < 4; ++a) xq[a * NPRIM + c] = q.v[a];
+        }
+      }
       __syncthreads();
       if (pending >= 0) {  // every thread is past the last read of stage `pending`
         if (t == 0) issue(pending + S);
@@ -190,9 +233,19 @@ __global__ void __launch_bounds__(NT, MINB) hydro_fused(const __grid_constant__ 
         hy_slope(xq[c], xq[NPRIM + c], xq[2 * NPRIM + c], xq[3 * NPRIM + c], xq[c + 1], xq[NPRIM + c + 1],
                  xq[2 * NPRIM + c + 1], xq[3 * NPRIM + c + 1], xq[c + 2], xq[NPRIM + c + 2],
                  xq[2 * NPRIM + c + 2], xq[3 * NPRIM + c + 2], &d[0], &d[1], &d[2], &d[3]);
-        hy_trace(xq[c + 1], xq[NPRIM + c + 1], xq[2 * NPRIM + c + 1], xq[3 * NPRIM + c + 1], d[0], d[1], d[2], d[3],
-                 dtdx, &xm[c], &xm[NQ + c], &xm[2 * NQ + c], &xm[3 * NQ + c], &xp[c], &xp[NQ + c],
-                 &xp[2 * NQ + c], &xp[3 * NQ + c]);
+        unsigned bad = 0;
+        hf::hy_trace(xq[c + 1], xq[NPRIM + c + 1], xq[2 * NPRIM + c + 1], xq[3 * NPRIM + c + 1], d[0], d[1], d[2],
+                     d[3], dtdx, &xm[c], &xm[NQ + c], &xm[2 * NQ + c], &xm[3 * NQ + c], &xp[c], &xp[NQ + c],
+                     &xp[2 * NQ + c], &xp[3 * NQ + c], &bad);
+        if (bad) {
+          const D8 o = slow_trace(xq[c + 1], xq[NPRIM + c + 1], xq[2 * NPRIM + c + 1], xq[3 * NPRIM + c + 1], d[0],
+                                  d[1], d[2], d[3], dtdx);
+#pragma unroll
+          for (int a = 0; a < 4; ++a) {
+            xm[a * NQ + c] = o.v[a];
+            xp[a * NQ + c] = o.v[4 + a];
+          }
+        }
       }
       __syncthreads();
       // ---- C. two independent Riemann solves per thread:
@@ -203,19 +256,32 @@ __global__ void __launch_bounds__(NT, MINB) hydro_fused(const __grid_constant__ 
         // per thread (the y-problem of a non-owning thread or of the pipeline's
         // first rows is a benign dummy whose result is dropped)
         const bool yface = owns && tt >= 4;
-        hy_rp cx, cy;
-        double psx = hy_riemann_init(xp[t], xp[NQ + t], xp[3 * NQ + t], xm[t + 1], xm[NQ + t + 1],
-                                     xm[3 * NQ + t + 1], &cx);
-        double psy = hy_riemann_init(ypo[0], ypo[1], ypo[3], yqm[0], yqm[1], yqm[3], &cy);
+        // branch-free fast paths; a flagged problem is re-solved with the plain kernels
+        unsigned bx = 0, by = 0;
+        hf::hy_rp cx, cy;
+        double psx = hf::hy_riemann_init(xp[t], xp[NQ + t], xp[3 * NQ + t], xm[t + 1], xm[NQ + t + 1],
+                                         xm[3 * NQ + t + 1], &cx, &bx);
+        double psy = hf::hy_riemann_init(ypo[0], ypo[1], ypo[3], yqm[0], yqm[1], yqm[3], &cy, &by);
 #pragma unroll 2
         for (int it = 0; it < HY_NITER; ++it) {
-          psx = hy_riemann_newton(&cx, psx);
-          psy = hy_riemann_newton(&cy, psy);
+          psx = hf::hy_riemann_newton(&cx, psx, &bx);
+          psy = hf::hy_riemann_newton(&cy, psy, &by);
         }
         double gx[4], gy[4];
-        hy_riemann_sample(&cx, psx, xp[t], xp[2 * NQ + t], xm[t + 1], xm[2 * NQ + t + 1], &gx[0], &gx[1], &gx[2],
-                          &gx[3]);
-        hy_riemann_sample(&cy, psy, ypo[0], ypo[2], yqm[0], yqm[2], &gy[0], &gy[1], &gy[2], &gy[3]);
+        hf::hy_riemann_sample(&cx, psx, xp[t], xp[2 * NQ + t], xm[t + 1], xm[2 * NQ + t + 1], &gx[0], &gx[1],
+                              &gx[2], &gx[3], &bx);
+        hf::hy_riemann_sample(&cy, psy, ypo[0], ypo[2], yqm[0], yqm[2], &gy[0], &gy[1], &gy[2], &gy[3], &by);
+        if (bx) {
+          const D4 g4 = slow_riemann(xp[t], xp[NQ + t], xp[2 * NQ + t], xp[3 * NQ + t], xm[t + 1], xm[NQ + t + 1],
+                                     xm[2 * NQ + t + 1], xm[3 * NQ + t + 1]);
+#pragma unroll
+          for (int a = 0; a < 4; ++a) gx[a] = g4.v[a];
+        }
+        if (by) {
+          const D4 g4 = slow_riemann(ypo[0], ypo[1], ypo[2], ypo[3], yqm[0], yqm[1], yqm[2], yqm[3]);
+#pragma unroll
+          for (int a = 0; a < 4; ++a) gy[a] = g4.v[a];
+        }
         hy_flux(gx[0], gx[1], gx[2], gx[3], &xf[t], &xf[NT + t], &xf[2 * NT + t], &xf[3 * NT + t]);
         if (yface) {
           double f[4];
@@ -246,7 +312,13 @@ __global__ void __launch_bounds__(NT, MINB) hydro_fused(const __grid_constant__ 
                 xf[3 * NT + t], xf[t + 1], xf[NT + t + 1], xf[2 * NT + t + 1], xf[3 * NT + t + 1], dtdx, &u1[0],
                 &u1[1], &u1[2], &u1[3]);
       double yq[4];
-      hy_constoprim(u1[0], u1[2], u1[1], u1[3], &yq[0], &yq[1], &yq[2], &yq[3]);
+      unsigned bad = 0;
+      hf::hy_constoprim(u1[0], u1[2], u1[1], u1[3], &yq[0], &yq[1], &yq[2], &yq[3], &bad);
+      if (bad) {
+        const D4 q = slow_constoprim(u1[0], u1[2], u1[1], u1[3]);
+#pragma unroll
+        for (int a = 0; a < 4; ++a) yq[a] = q.v[a];
+      }
       if (tt >= 2) {
         double d[4], yp[4];
         const double* yq1 = yqring + ((tt + 1) & 1) * 4 * NT + t;  // row r-1
@@ -255,9 +327,17 @@ __global__ void __launch_bounds__(NT, MINB) hydro_fused(const __grid_constant__ 
                  yq[2], yq[3], &d[0],
                  &d[1], &d[2], &d[3]);
         // minus state of row r-1 is read by the y-face (r-2)+1/2 at C of the next row
-        hy_trace(yq1[0], yq1[NT], yq1[2 * NT], yq1[3 * NT], d[0], d[1], d[2], d[3], dtdx, &yqm[0], &yqm[1], &yqm[2],
-                 &yqm[3],
-                 &yp[0], &yp[1], &yp[2], &yp[3]);
+        bad = 0;
+        hf::hy_trace(yq1[0], yq1[NT], yq1[2 * NT], yq1[3 * NT], d[0], d[1], d[2], d[3], dtdx, &yqm[0], &yqm[1],
+                     &yqm[2], &yqm[3], &yp[0], &yp[1], &yp[2], &yp[3], &bad);
+        if (bad) {
+          const D8 o = slow_trace(yq1[0], yq1[NT], yq1[2 * NT], yq1[3 * NT], d[0], d[1], d[2], d[3], dtdx);
+#pragma unroll
+          for (int a = 0; a < 4; ++a) {
+            yqm[a] = o.v[a];
+            yp[a] = o.v[4 + a];
+          }
+        }
 #pragma unroll
         for (int a = 0; a < 4; ++a) {
           ypo[a] = ypn[a];  // plus state of row r-2 (for the face (r-2)+1/2 at the next row)
@@ -292,13 +372,15 @@ bool supports(const lf::Plan& plan, std::string& why) {
 int launch_step(const double* const in[4], double* const out[4], const double* dtdx, int ni, const RowPart& rp,
                 cudaStream_t st, std::string& err) {
   const int nj = rp.rows;
-  // LF_HYDRO_VARIANT: register budget for 2 / 3 / 4 (default) CTAs per SM: on
-  // this latency-bound fp64 code 4 resident CTAs beat the spill-free budget
+  // LF_HYDRO_VARIANT: register budget for 2 / 3 (default) / 4 CTAs per SM.
+  // With the branch-free divisions the Riemann phase keeps the fp64 pipe busy
+  // from fewer warps: 3 CTAs at 168 registers (no spills) beat 4 CTAs at 128
+  // (96 B of spills) -- profiles/r01_hydro_variants.txt
   static void (*kern)(Maps, Params) = nullptr;
   static int slots = 0;
   if (!slots) {
     const char* v = std::getenv("LF_HYDRO_VARIANT");
-    const int var = v ? std::atoi(v) : 2;
+    const int var = v ? std::atoi(v) : 1;
     kern = var == 0 ? hydro_fused<2> : (var == 2 ? hydro_fused<4> : hydro_fused<3>);
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
     if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(hydro)", err);
