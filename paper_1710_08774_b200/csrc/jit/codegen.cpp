@@ -476,16 +476,50 @@ bool emit_bodies(Ctx& C, const Grp& G, std::ostream& src, const char* ind) {
   return true;
 }
 
-void emit_prelude(Ctx& C, std::ostream& src, int threads, int min_blocks = 1) {
+void emit_prelude(Ctx& C, std::ostream& src, int threads, int min_blocks = 1, bool ws = false) {
   const auto& terms = C.P.terminals;
-  src << "// generated by loomfuse-b200 (csrc/jit/codegen.cpp) for chain '" << C.P.rs.name << "'\n";
-  src << "typedef " << C.T << " T;\n";
-  src << "__device__ __forceinline__ T lf_min(T a, T b) { return a < b ? a : b; }\n";
-  src << "__device__ __forceinline__ T lf_max(T a, T b) { return a > b ? a : b; }\n";
-  // must match lfx::Args in jit.cpp (passed by value)
-  src << "struct LfArgs { void* t[32]; long long n0; int row_lo, row_hi, top, bottom, chunk, inplace; };\n";
-  src << "extern \"C\" __global__ void __launch_bounds__(" << threads << ", " << min_blocks << ") lf_jit_step(const LfArgs a) {\n";
-  src << "  extern __shared__ __align__(16) unsigned char lf_smem[];\n";
+  if (!ws) {
+    src << "// generated by loomfuse-b200 (csrc/jit/codegen.cpp) for chain '" << C.P.rs.name << "'\n";
+    src << "typedef " << C.T << " T;\n";
+    src << "__device__ __forceinline__ T lf_min(T a, T b) { return a < b ? a : b; }\n";
+    src << "__device__ __forceinline__ T lf_max(T a, T b) { return a > b ? a : b; }\n";
+    // must match lfx::Args in jit.cpp (passed by value)
+    src << "struct LfArgs { void* t[32]; long long n0; int row_lo, row_hi, top, bottom, chunk, inplace; };\n";
+    src << "extern \"C\" __global__ void __launch_bounds__(" << threads << ", " << min_blocks
+        << ") lf_jit_step(const LfArgs a) {\n";
+    src << "  extern __shared__ __align__(16) unsigned char lf_smem[];\n";
+  } else {
+    // warp-specialised variant: tensor maps of the streamed axioms (must match
+    // lfx::JitMaps in jit.cpp) and the mbarrier / TMA primitives it uses
+    src << R"(struct __align__(64) LfTmap { unsigned long long w[16]; };
+struct LfMaps { LfTmap m[)" << kJitMaxMaps << R"(]; };
+__device__ __forceinline__ unsigned lf_s32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void lf_mbar_init(unsigned long long* b, unsigned n) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"(lf_s32(b)), "r"(n) : "memory");
+}
+__device__ __forceinline__ void lf_mbar_expect(unsigned long long* b, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(lf_s32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void lf_mbar_arrive(unsigned long long* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" :: "r"(lf_s32(b)) : "memory");
+}
+__device__ __forceinline__ void lf_mbar_wait(unsigned long long* b, unsigned parity) {
+  asm volatile("{\n .reg .pred p;\n LFW: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra LFW;\n}\n"
+               :: "r"(lf_s32(b)), "r"(parity) : "memory");
+}
+__device__ __forceinline__ void lf_tma2(void* dst, const LfTmap* m, unsigned long long* b, int c0, int c1) {
+  asm volatile("cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];"
+               :: "r"(lf_s32(dst)), "l"(m), "r"(lf_s32(b)), "r"(c0), "r"(c1) : "memory");
+}
+__device__ __forceinline__ void lf_tma3(void* dst, const LfTmap* m, unsigned long long* b, int c0, int c1, int c2) {
+  asm volatile("cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];"
+               :: "r"(lf_s32(dst)), "l"(m), "r"(lf_s32(b)), "r"(c0), "r"(c1), "r"(c2) : "memory");
+}
+)";
+    src << "extern \"C\" __global__ void __launch_bounds__(" << threads << ", " << min_blocks
+        << ") lf_jit_step_ws(const LfArgs a, const __grid_constant__ LfMaps lf_maps) {\n";
+    src << "  extern __shared__ __align__(128) unsigned char lf_smem[];\n";
+  }
   src << "  const long long N0 = a.n0;\n";
   for (int d = 1; d < C.nd; ++d) src << "  const long long N" << d << " = " << C.N[d] << ";\n";
   for (size_t i = 0; i < terms.size(); ++i) {
@@ -500,7 +534,14 @@ void emit_prelude(Ctx& C, std::ostream& src, int threads, int min_blocks = 1) {
 // ---------------------------------------------------------------------------
 // 2D / 3D: march the outermost dimension with rolling windows
 // ---------------------------------------------------------------------------
-bool emit_march(Ctx& C, JitProgram& out, std::ostream& src) {
+// ws: the warp-specialised variant (lf_jit_step_ws), emitted after the plain
+// one with the same tile: one producer warp streams the full-rank axioms by
+// TMA into their windows (a ring of PD + 1 trip stages on full / empty
+// mbarriers) while 8 consumer warps evaluate the groups; consumers meet only
+// at named barriers between dependency levels (intermediate windows one row
+// deeper so a trip's writes never hit rows the previous trip still reads), so
+// a single-level chain runs with no CTA-wide barrier at all.
+bool emit_march(Ctx& C, JitProgram& out, std::ostream& src, bool ws = false) {
   const int nd = C.nd;
   const int NT = 256;
   const int eb = out.elem_bytes;
@@ -522,7 +563,7 @@ bool emit_march(Ctx& C, JitProgram& out, std::ostream& src) {
       if (C.smem_var[o.var]) lead[o.var] = g.shift + o.rel[0];
   for (size_t v = 0; v < nv; ++v) {
     if (C.smem_var[v]) {
-      win[v] = lead[v] - old[v] + 1;
+      win[v] = lead[v] - old[v] + 1 + (ws ? 1 : 0);
     } else if (old[v] != INT_MAX && C.staged_axiom(static_cast<int>(v)) >= 0) {
       staged[v] = C.staged_axiom(static_cast<int>(v));
       win[v] = lead[v] - old[v] + 1 + PD;  // + the rows in flight
@@ -540,17 +581,37 @@ bool emit_march(Ctx& C, JitProgram& out, std::ostream& src) {
   std::vector<int> tile(nd, 1);
   std::vector<size_t> soff(nv, 0);
   size_t smem = 0;
+  // ws: a staged axiom's innermost row is fetched as nbox TMA boxes of bw
+  // elements (box rows <= 256 elements, 128-B multiples so every box lands
+  // 128-B aligned); its smem row is nbox * bw wide
+  auto tma_box = [&](size_t v, int& nbox, int& bw) {
+    const int w = tile[nd - 1] + (C.vmax[v][nd - 1] - C.vmin[v][nd - 1]);
+    const int al = 128 / eb;
+    nbox = (w + 255) / 256;
+    bw = ((w + nbox - 1) / nbox + al - 1) / al * al;
+    if (bw > 256) nbox = (w + 255) / 256 + 1, bw = ((w + nbox - 1) / nbox + al - 1) / al * al;
+  };
+  auto wdim = [&](size_t v, int d) {
+    int w = tile[d] + (C.vmax[v][d] - C.vmin[v][d]);
+    if (ws && staged[v] >= 0 && d == nd - 1) {
+      int nb = 1, bw = w;
+      tma_box(v, nb, bw);
+      w = nb * bw;
+    }
+    return w;
+  };
   auto plane = [&](size_t v) {
     size_t n = 1;
-    for (int d = 1; d < nd; ++d) n *= tile[d] + (C.vmax[v][d] - C.vmin[v][d]);
+    for (int d = 1; d < nd; ++d) n *= wdim(v, d);
     return n;
   };
   auto layout = [&] {
     smem = 0;
+    const size_t al = ws ? 128 : 16;
     for (size_t v = 0; v < nv; ++v) {
       if (win[v] <= 0) continue;
       soff[v] = smem;
-      smem += (win[v] * plane(v) * eb + 15) / 16 * 16;
+      smem += (win[v] * plane(v) * eb + al - 1) / al * al;
     }
   };
   // widths: the outermost inner dimension first; defaults sized for >= 2 CTAs/SM
@@ -560,7 +621,7 @@ bool emit_march(Ctx& C, JitProgram& out, std::ostream& src) {
     int r = 0, w = 0;
     if (std::sscanf(e, "%dx%d", &r, &w) == 2 && r > 0 && w > 0) rows_in = r, wide = w;
   }
-  for (;;) {
+  for (; !ws;) {
     if (nd == 2) {
       tile[1] = std::max(32, wide - span_in[1]);
     } else {
@@ -577,12 +638,21 @@ bool emit_march(Ctx& C, JitProgram& out, std::ostream& src) {
       break;
     }
   }
+  if (ws) {
+    tile = out.tile;
+    layout();
+    if (smem > 200 * 1024) return false;
+    out.ws_smem_bytes = smem + 16 * (PD + 1);  // + the stage mbarriers
+    out.ws_threads = NT + 32;
+  }
   if (smem > 200 * 1024) return (C.error = "chain needs too much on-chip storage for one tile", false);
+  if (!ws) {
   out.tile = tile;
   out.tile[0] = 1;
   out.smem_bytes = smem;
   out.threads = NT;
   out.march = true;
+  }
   // trip range relative to the chunk [r0, r1): t in [r0 + TS, r1 - 1 + TE]
   int TS = INT_MAX, TE = INT_MIN;
   for (const auto& g : G) {
@@ -591,27 +661,30 @@ bool emit_march(Ctx& C, JitProgram& out, std::ostream& src) {
   }
   for (size_t v = 0; v < nv; ++v)
     if (staged[v] >= 0) TS = std::min(TS, C.vmin[v][0] - lead[v]);
-  out.prologue = TE - TS;
-  {
+  const int cps = std::max<int>(1, std::min<int>(2048 / NT, static_cast<int>((227 * 1024) / (smem + 1024))));
+  if (!ws) {
+    out.prologue = TE - TS;
     long inner = 1;
     for (int d = 1; d < nd; ++d) inner *= (C.N[d] + tile[d] - 1) / tile[d];
     out.inner_tiles = inner;
+    out.ctas_per_sm = cps;
+    out.chunk = nd == 3 ? 64 : 1 << 30;  // rows per chunk of the work order (2D: whole tiles)
   }
-  out.ctas_per_sm = std::max<int>(1, std::min<int>(2048 / NT, static_cast<int>((227 * 1024) / (smem + 1024))));
-  out.chunk = nd == 3 ? 64 : 1 << 30;  // rows per chunk of the work order (2D: whole tiles)
 
-  int minb = std::min(out.ctas_per_sm, 2);  // register cap; 2 measured best
+  int minb = std::min(cps, 2);  // register cap; 2 measured best
   if (const char* e = std::getenv("LF_JIT_MINB")) minb = std::max(1, std::atoi(e));
-  emit_prelude(C, src, NT, minb);
+  emit_prelude(C, src, ws ? NT + 32 : NT, minb, ws);
+  // ws: warp 0 is the producer, consumer thread c = threadIdx.x - 32
+  const char* TID = ws ? "((int)threadIdx.x - 32)" : "threadIdx.x";
   if (nd == 3)
-    src << "  const int tx = threadIdx.x & 63, ty = threadIdx.x >> 6;\n";
+    src << "  const int tx = " << TID << " & 63, ty = " << TID << " >> 6;\n";
   else
-    src << "  const int tx = threadIdx.x;\n";
+    src << "  const int tx = " << TID << ";\n";
   for (size_t v = 0; v < nv; ++v)
     if (win[v] > 0)
       src << "  T* __restrict__ v" << v << " = reinterpret_cast<T*>(lf_smem + " << soff[v] << ");  // '"
           << C.P.vars[v].name << "': " << win[v] << " rows x " << plane(v) << "\n";
-  auto width = [&](size_t v, int d) { return tile[d] + (C.vmax[v][d] - C.vmin[v][d]); };
+  auto width = [&](size_t v, int d) { return wdim(v, d); };
   // in-plane offset of var v at tile-relative cell (c_d + rel_d)
   auto inplane = [&](size_t v, const std::vector<int>& rel) {
     std::string e;
@@ -651,10 +724,12 @@ bool emit_march(Ctx& C, JitProgram& out, std::ostream& src) {
     int ai, gi, slot;
   };
   std::vector<IP> ips;
-  out.inplace.clear();
-  out.inplace_error.clear();
+  if (!ws) {
+    out.inplace.clear();
+    out.inplace_error.clear();
+  }
   const int nterm = static_cast<int>(C.P.terminals.size());
-  for (const auto& [in_ext, out_ext] : C.P.rs.aliases) {
+  for (const auto& [in_ext, out_ext] : ws ? decltype(C.P.rs.aliases){} : C.P.rs.aliases) {
     int ai = -1, gi = -1;
     for (int i = 0; i < nterm; ++i) {
       if (!C.P.terminals[i].is_goal && C.P.terminals[i].name == in_ext) ai = i;
@@ -702,6 +777,29 @@ bool emit_march(Ctx& C, JitProgram& out, std::ostream& src) {
         << "]);  // in-place bands of '" << C.P.vars[ip.v].name << "'\n"
         << "  const T* __restrict__ cb" << ip.slot << "_1 = reinterpret_cast<const T*>(a.t[" << ip.slot + 1 << "]);\n"
         << "  const T* __restrict__ cb" << ip.slot << "_2 = reinterpret_cast<const T*>(a.t[" << ip.slot + 2 << "]);\n";
+  // ws: trip-stage ring (full: producer -> consumers, empty: consumers -> producer)
+  const int NS = PD + 1;
+  std::vector<size_t> tv;  // TMA-staged vars, in map order
+  for (size_t v = 0; v < nv; ++v)
+    if (ws && staged[v] >= 0) tv.push_back(v);
+  if (ws) {
+    src << "  unsigned long long* lf_full = reinterpret_cast<unsigned long long*>(lf_smem + " << smem << ");\n";
+    src << "  unsigned long long* lf_empty = lf_full + " << NS << ";\n";
+    src << "  if (threadIdx.x == 0) {\n";
+    src << "    for (int i = 0; i < " << NS << "; ++i) { lf_mbar_init(&lf_full[i], 1); lf_mbar_init(&lf_empty[i], "
+        << NT / 32 << "); }\n";
+    src << "    asm volatile(\"fence.mbarrier_init.release.cluster;\" ::: \"memory\");\n";
+    for (size_t k = 0; k < tv.size(); ++k)
+      src << "    asm volatile(\"prefetch.tensormap [%0];\" :: \"l\"(&lf_maps.m[" << k << "]) : \"memory\");\n";
+    src << "  }\n";
+    src << "  __syncthreads();\n";
+    src << "  const bool producer = threadIdx.x < 32;\n";
+    src << "  if (producer && threadIdx.x != 0) return;\n";
+    src << "  unsigned lf_g = 0;  // trip counter across segments: stage lf_g % " << NS << "\n";
+    // window slots advance continuously across segments (one ring per variable)
+    for (size_t v = 0; v < nv; ++v)
+      if (win[v] > 1) src << "  int b" << v << " = 0;\n";
+  }
   src << "  const int rows = a.row_hi - a.row_lo;\n";
   src << "  const long long total = (long long)rows * " << out.inner_tiles << ";\n";
   src << "  const long long per = (total + gridDim.x - 1) / gridDim.x;\n";
@@ -735,8 +833,9 @@ bool emit_march(Ctx& C, JitProgram& out, std::ostream& src) {
     const long nt = (C.N[d] + tile[d] - 1) / tile[d];
     src << "  const int o" << d << " = (bt % " << nt << ") * " << tile[d] << "; bt /= " << nt << ";\n";
   }
-  for (size_t v = 0; v < nv; ++v)
-    if (win[v] > 1) src << "  int b" << v << " = " << wrap(v, TS) << ";\n";
+  if (!ws)
+    for (size_t v = 0; v < nv; ++v)
+      if (win[v] > 1) src << "  int b" << v << " = " << wrap(v, TS) << ";\n";
   // register windows along the march (opt-in, LF_JIT_ROT=1): a thread keeps
   // its cells for a whole segment, so a window value read at row offset s on
   // trip t+1 is the one it read at s+1 on trip t -- only the newest row of
@@ -750,7 +849,7 @@ bool emit_march(Ctx& C, JitProgram& out, std::ostream& src) {
     std::vector<char> keep;  // value carried to the next trip
   };
   std::vector<Rot> rot(G.size());
-  const bool use_rot = std::getenv("LF_JIT_ROT") && std::atoi(std::getenv("LF_JIT_ROT")) != 0;
+  const bool use_rot = !ws && std::getenv("LF_JIT_ROT") && std::atoi(std::getenv("LF_JIT_ROT")) != 0;
   for (size_t gi = 0; gi < G.size(); ++gi) {
     const Grp& g = G[gi];
     Rot& R = rot[gi];
@@ -845,6 +944,7 @@ bool emit_march(Ctx& C, JitProgram& out, std::ostream& src) {
         << inplane(v, std::vector<int>(nd, 0)) << ") * " << eb << "), \"l\"(sp) : \"memory\");\n";
     src << I << "        }\n" << I << "      }\n" << I << "    }\n" << I << "  }\n" << I << "}\n";
   };
+  if (!ws) {
   for (int p = 0; p < PD; ++p) {
     for (size_t v = 0; v < nv; ++v)
       if (staged[v] >= 0)
@@ -857,12 +957,64 @@ bool emit_march(Ctx& C, JitProgram& out, std::ostream& src) {
   for (size_t v = 0; v < nv; ++v)
     if (staged[v] >= 0) emit_load(v, "t" + plus(PD + lead[v]), rowbase(v, PD + lead[v]), "    ");
   src << "    asm volatile(\"cp.async.commit_group;\" ::: \"memory\");\n";
+  } else {
+  src << "  for (int t = r0 + (" << TS << "); t <= r1 - 1 + (" << TE << "); ++t, ++lf_g) {\n";
+  src << "    const unsigned stg = lf_g % " << NS << ", par = (lf_g / " << NS << ") & 1;\n";
+  src << "    if (producer) {\n";
+  // the stage's previous occupant: trip lf_g - NS, whose window rows this trip's loads overwrite
+  src << "      if (lf_g >= " << NS << ") lf_mbar_wait(&lf_empty[stg], par ^ 1);\n";
+  src << "      unsigned bytes = 0;\n";
+  for (size_t k = 0; k < tv.size(); ++k) {
+    const size_t v = tv[k];
+    int nb = 1, bw = 1;
+    tma_box(v, nb, bw);
+    size_t box = static_cast<size_t>(nb) * bw * eb;
+    if (nd == 3) box *= width(v, 1);
+    src << "      const int y" << k << " = t" << plus(lead[v]) << ";\n";
+    src << "      const bool in" << k << " = y" << k << " >= r0" << plus(C.vmin[v][0]) << " && y" << k << " <= r1 - 1"
+        << plus(C.vmax[v][0]) << ";\n";
+    src << "      if (in" << k << ") bytes += " << box << "u;\n";
+  }
+  src << "      asm volatile(\"fence.proxy.async.shared::cta;\" ::: \"memory\");\n";
+  src << "      lf_mbar_expect(&lf_full[stg], bytes);\n";
+  for (size_t k = 0; k < tv.size(); ++k) {
+    const size_t v = tv[k];
+    const int ti = staged[v];
+    const auto& t = C.P.terminals[ti];
+    const auto ex = C.extra_of(static_cast<int>(v));
+    auto so = [&](int d) { return static_cast<long>(ex[d]) - t.base[d] + C.LO[d]; };  // storage = logical + so
+    int nb = 1, bw = 1;
+    tma_box(v, nb, bw);
+    src << "      if (in" << k << ") {\n";
+    src << "        T* dst = v" << v << " + " << rowbase(v, lead[v]) << ";\n";
+    if (nd == 3) {
+      src << "        lf_tma3(dst, &lf_maps.m[" << k << "], &lf_full[stg], o2" << plus(C.vmin[v][2] + so(2)) << ", o1"
+          << plus(C.vmin[v][1] + so(1)) << ", y" << k << plus(so(0)) << ");\n";
+    } else {
+      for (int b = 0; b < nb; ++b)
+        src << "        lf_tma2(dst + " << b * bw << ", &lf_maps.m[" << k << "], &lf_full[stg], o1"
+            << plus(C.vmin[v][1] + so(1) + b * bw) << ", y" << k << plus(so(0)) << ");\n";
+    }
+    src << "      }\n";
+    JitProgram::Tma tm;
+    tm.term = ti;
+    tm.rank = nd;
+    for (int d = 0; d < nd; ++d) tm.extent[d] = t.extent[nd - 1 - d];  // innermost first
+    tm.box[0] = static_cast<unsigned>(bw);
+    tm.box[1] = nd == 3 ? static_cast<unsigned>(width(v, 1)) : 1u;
+    tm.box[2] = 1;
+    out.ws_maps.push_back(tm);
+  }
+  src << "    } else {\n";
+  src << "    lf_mbar_wait(&lf_full[stg], par);\n";
+  }
   int level = 1;
   for (size_t gi = 0; gi < G.size(); ++gi) {
     const Grp& g = G[gi];
     const auto& k = C.P.rs.kernels[g.kernel];
     if (g.level != level) {
-      src << "    __syncthreads();\n";
+      src << (ws ? "    asm volatile(\"bar.sync 1, " + std::to_string(NT) + ";\" ::: \"memory\");\n"
+                 : std::string("    __syncthreads();\n"));
       level = g.level;
     }
     std::vector<int> ext(nd), lo(nd);
@@ -1004,11 +1156,19 @@ bool emit_march(Ctx& C, JitProgram& out, std::ostream& src) {
     }
     src << "          }\n        }\n        }\n      }\n    }\n";
   }
+  if (ws) {
+    // this warp is done with the trip's window rows
+    src << "    __syncwarp();\n";
+    src << "    if ((threadIdx.x & 31) == 0) lf_mbar_arrive(&lf_empty[stg]);\n";
+    src << "    }\n";
+  }
   for (size_t v = 0; v < nv; ++v)
     if (win[v] > 1) src << "    b" << v << " = b" << v << " == " << (win[v] - 1) << " ? 0 : b" << v << " + 1;\n";
   src << "  }\n";
-  src << "  asm volatile(\"cp.async.wait_group 0;\" ::: \"memory\");\n";
-  src << "  __syncthreads();\n";
+  if (!ws) {
+    src << "  asm volatile(\"cp.async.wait_group 0;\" ::: \"memory\");\n";
+    src << "  __syncthreads();\n";
+  }
   src << "  }\n";
   src << "}\n";
   // ---- in-place: capture the bands other units read before this step writes
@@ -1690,6 +1850,30 @@ bool jit_generate(const lf::Plan& P, JitProgram& out, const std::string& sources
   if (!ok || !emit_fill(C, out, src)) {
     out.error = C.error;
     return false;
+  }
+  // the warp-specialised variant, where every streamed axiom can be fetched by
+  // TMA: a dense terminal in loop-dimension order with 16-B row pitches, no
+  // in-place aliases (those keep the band-capturing loader)
+  bool ws_ok = C.nd >= 2 && C.P.rs.aliases.empty() && !(std::getenv("LF_JIT_WS") && std::atoi(std::getenv("LF_JIT_WS")) == 0);
+  int nstaged = 0;
+  for (size_t v = 0; ws_ok && v < C.P.vars.size(); ++v) {
+    const int ti = C.staged_axiom(static_cast<int>(v));
+    if (ti < 0) continue;
+    ++nstaged;
+    const auto& t = C.P.terminals[ti];
+    for (int d = 0; d < C.nd; ++d) ws_ok &= t.dims[d] == d;
+    ws_ok &= (t.extent[C.nd - 1] * out.elem_bytes) % 16 == 0;
+  }
+  ws_ok &= nstaged > 0 && nstaged <= kJitMaxMaps;
+  if (ws_ok) {
+    std::ostringstream ws;
+    out.ws_maps.clear();
+    if (emit_march(C, out, ws, true) && !out.ws_maps.empty() && static_cast<int>(out.ws_maps.size()) <= kJitMaxMaps) {
+      out.has_ws = true;
+      src << ws.str();
+    } else {
+      out.ws_maps.clear();
+    }
   }
   out.source = sources + src.str();
   return true;

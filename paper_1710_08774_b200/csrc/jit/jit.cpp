@@ -5,6 +5,8 @@
 // executors: -fmad=false, IEEE division and square root.
 #include "jit.hpp"
 
+#include "../exec/common.cuh"
+
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <dlfcn.h>
@@ -268,8 +270,31 @@ int JitKernel::run_nests(const ExecArgs& a, std::string& err) {
   return LF_OK;
 }
 
-int JitKernel::launch(void* fn, dim3 grid, dim3 block, size_t smem, cudaStream_t st, void* args, std::string& err) {
-  void* params[] = {args};
+// tensor maps of the streamed axioms for this launch's buffers; false (plain
+// kernel) when a buffer is not 16-B aligned or the driver refuses a map
+bool JitKernel::ws_maps(const std::vector<void*>& bufs, long rows, JitMaps& maps, std::string& err) {
+  static const bool off = std::getenv("LF_JIT_WS") && std::atoi(std::getenv("LF_JIT_WS")) == 0;
+  if (off) return false;
+  const CUtensorMapDataType dt = prog_.elem_bytes == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
+  const long n0 = plan_rows_;
+  for (size_t k = 0; k < prog_.ws_maps.size(); ++k) {
+    const auto& m = prog_.ws_maps[k];
+    const void* base = bufs[m.term];
+    if (reinterpret_cast<uintptr_t>(base) % 16) return false;
+    uint64_t dims[3] = {m.extent[0], m.extent[1], m.extent[2]};
+    // outermost extent of the launch domain: a slab holds rows + the terminal's halo rows
+    dims[m.rank - 1] = static_cast<uint64_t>(static_cast<long>(m.extent[m.rank - 1]) - n0 + rows);
+    std::string e;
+    if (!make_tensor_map(reinterpret_cast<CUtensorMap*>(&maps.m[k]), base, dt, prog_.elem_bytes, m.rank, dims, m.box, e))
+      return false;
+  }
+  (void)err;
+  return true;
+}
+
+int JitKernel::launch(void* fn, dim3 grid, dim3 block, size_t smem, cudaStream_t st, void* args, std::string& err,
+                      void* args2) {
+  void* params[] = {args, args2};
   CUresult r = drv().launch(static_cast<CUfunction>(fn), grid.x, grid.y, grid.z, block.x, block.y, block.z,
                             static_cast<unsigned>(smem), reinterpret_cast<CUstream>(st), params, nullptr);
   if (r != CUDA_SUCCESS) {
@@ -313,12 +338,18 @@ int JitKernel::run(const ExecArgs& a, std::string& err) {
       step_ = f;
       d.attr(static_cast<CUfunction>(step_), CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES,
              static_cast<int>(prog_.smem_bytes));
+      if (prog_.has_ws && d.get(&f, m, "lf_jit_step_ws") == CUDA_SUCCESS) {
+        step_ws_ = f;
+        d.attr(static_cast<CUfunction>(step_ws_), CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES,
+               static_cast<int>(prog_.ws_smem_bytes));
+      }
     }
   }
   if (!prog_.nest_kernels.empty()) return run_nests(a, err);
   const auto& rs = a.plan->rs;
   const auto& T = a.plan->terminals;
   const RowPart rp = row_part(a, (int)rs.ranges[0].trips());
+  plan_rows_ = rs.ranges[0].trips();
   JitArgs args;
   std::memset(&args, 0, sizeof args);
   args.n0 = rp.rows;
@@ -354,6 +385,14 @@ int JitKernel::run(const ExecArgs& a, std::string& err) {
       if (d.occupancy(&occ, static_cast<CUfunction>(step_), prog_.threads, prog_.smem_bytes) != CUDA_SUCCESS || occ < 1)
         occ = prog_.ctas_per_sm;
       resident_ = std::max(1, sms) * std::max(1, occ);
+      if (step_ws_) {
+        int ows = 0;
+        if (d.occupancy(&ows, static_cast<CUfunction>(step_ws_), prog_.ws_threads, prog_.ws_smem_bytes) != CUDA_SUCCESS ||
+            ows < 1)
+          step_ws_ = nullptr;  // cannot be resident: keep the plain kernel
+        else
+          resident_ws_ = std::max(1, sms) * ows;
+      }
     }
     long chunk = std::min<long>(prog_.chunk, rows);
     if (const char* e = std::getenv("LF_JIT_CHUNK")) chunk = std::max(1L, std::min<long>(rows, std::atol(e)));
@@ -397,7 +436,15 @@ int JitKernel::run(const ExecArgs& a, std::string& err) {
     for (size_t i = 0; i < T.size(); ++i)
       if (T[i].is_goal) bufs[i] = (to_goal || iter_axiom[i] < 0) ? a.terms[i] : scratch[i];
     for (size_t i = 0; i < T.size(); ++i) args.t[i] = bufs[i];
-    int st = launch(step_, grid, dim3(prog_.threads), prog_.smem_bytes, a.stream, &args, err);
+    int st = LF_OK;
+    JitMaps maps;
+    if (prog_.march && step_ws_ && ws_maps(bufs, rp.rows, maps, err)) {
+      dim3 gws = grid;
+      gws.x = static_cast<unsigned>(std::max<long>(1, std::min<long>(resident_ws_, rows * prog_.inner_tiles / 16)));
+      st = launch(step_ws_, gws, dim3(prog_.ws_threads), prog_.ws_smem_bytes, a.stream, &args, err, &maps);
+    } else {
+      st = launch(step_, grid, dim3(prog_.threads), prog_.smem_bytes, a.stream, &args, err);
+    }
     if (st != LF_OK) return st;
     if (fill_ && prog_.has_fill) {
       st = launch(fill_, dim3(592), dim3(256), 0, a.stream, &args, err);

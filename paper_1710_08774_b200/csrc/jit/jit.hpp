@@ -4,6 +4,7 @@
 
 #include <cuda_runtime.h>
 
+#include <cstdint>
 #include <memory>
 #include <string>
 #include <vector>
@@ -18,6 +19,10 @@ struct NestLaunch {
   bool reduction = false;  // warp per parallel cell (true) or thread per cell
   long long units = 0;     // parallel cells
 };
+
+// streamed axioms the warp-specialised march can fetch by TMA (tensor maps
+// passed by value next to the argument block)
+constexpr int kJitMaxMaps = 8;
 
 struct JitProgram {
   // config.aliases pairs the executor can run in place (one buffer):
@@ -47,6 +52,18 @@ struct JitProgram {
   // multi-nest plans: one kernel per nest, materialised cross-nest variables
   std::vector<NestLaunch> nest_kernels;
   std::vector<size_t> mat_bytes;
+  // warp-specialised march (lf_jit_step_ws): one TMA map per streamed axiom,
+  // extents innermost first (the outermost one is the launch domain's at run time)
+  struct Tma {
+    int term = -1;
+    int rank = 0;
+    uint64_t extent[3] = {1, 1, 1};
+    unsigned box[3] = {1, 1, 1};
+  };
+  bool has_ws = false;
+  std::vector<Tma> ws_maps;
+  size_t ws_smem_bytes = 0;
+  int ws_threads = 288;
   std::string error;  // why the chain is not supported
 };
 
@@ -62,6 +79,15 @@ struct JitArgs {
   int row_lo, row_hi, top, bottom, chunk, inplace;
 };
 
+// tensor maps of the warp-specialised march, passed by value as its second
+// kernel parameter (`struct LfMaps` in the generated source)
+struct alignas(64) JitMap {
+  unsigned long long w[16];
+};
+struct JitMaps {
+  JitMap m[kJitMaxMaps];
+};
+
 // A compiled chain; owned by one plan.
 class JitKernel {
  public:
@@ -74,16 +100,21 @@ class JitKernel {
   JitProgram prog_;
   void* module_ = nullptr;  // CUmodule
   void* step_ = nullptr;    // CUfunction
+  void* step_ws_ = nullptr; // warp-specialised variant (TMA producer warp)
   void* fill_ = nullptr;
   void* capture_ = nullptr;
   std::vector<void*> bands_;        // in-place band copies
   std::vector<size_t> band_bytes_;
   int resident_ = 0;  // CTAs resident at once (occupancy x SMs)
+  int resident_ws_ = 0;
   std::vector<void*> nest_fns_;
   std::vector<void*> mats_;  // device buffers of materialised variables
   std::vector<char> cubin_;
-  int launch(void* fn, dim3 grid, dim3 block, size_t smem, cudaStream_t st, void* args, std::string& err);
+  int launch(void* fn, dim3 grid, dim3 block, size_t smem, cudaStream_t st, void* args, std::string& err,
+             void* args2 = nullptr);
   int run_nests(const ExecArgs& a, std::string& err);
+  bool ws_maps(const std::vector<void*>& bufs, long rows, JitMaps& maps, std::string& err);
+  long plan_rows_ = 0;  // trips of the outermost loop dimension (whole domain)
   int run_inplace(const ExecArgs& a, JitArgs& args, std::string& err);
 };
 
