@@ -805,12 +805,17 @@ bool emit_march(Ctx& C, JitProgram& out, std::ostream& src, bool ws = false) {
   src << "  const long long per = (total + gridDim.x - 1) / gridDim.x;\n";
   src << "  long long s = (long long)blockIdx.x * per;\n";
   src << "  const long long s_end = min(total, s + per);\n";
-  src << "  const long long units = a.inplace ? (long long)((rows + a.chunk - 1) / a.chunk) * " << out.inner_tiles
+  // ws: always whole (chunk, tile) units dealt round-robin, chunk-major, so the
+  // CTAs running at one time hold neighbouring tiles of the same rows: halo
+  // rows are fetched once and hit in L2, and the row segments neighbouring
+  // tiles write into shared sectors meet in L2 before eviction
+  const char* UNITS = ws ? "true" : "a.inplace";
+  src << "  const long long units = " << UNITS << " ? (long long)((rows + a.chunk - 1) / a.chunk) * " << out.inner_tiles
       << " : 0;\n";
   src << "  long long u = blockIdx.x;\n";
   src << "  for (;;) {\n";
   src << "  int bt, r0_, r1_;\n";
-  src << "  if (a.inplace) {\n";
+  src << "  if (" << UNITS << ") {\n";
   src << "    if (u >= units) break;\n";
   src << "    const int ci = (int)(u / " << out.inner_tiles << ");\n";
   src << "    bt = (int)(u % " << out.inner_tiles << ");\n";
