@@ -340,11 +340,15 @@ bool analyse(Ctx& C) {
     }
     C.groups.push_back(std::move(G));
   }
-  // ---- inline cheap producers (2D/3D): a body of at most two operations,
-  // read by kernels only at <= 2 offsets per output, whose own inputs are not
-  // inlined values, is recomputed at each read instead of stored -- e.g. the
-  // face fluxes u[+1]-u of the 3D heat chain: fewer shared-memory round trips
-  // than a window store + two loads, identical arithmetic per term
+  // ---- inline producers (2D/3D) whose own inputs are not inlined values:
+  // cheap ones (a body of at most two operations, read by kernels only at <= 2
+  // offsets per output) are recomputed at each read instead of stored -- e.g.
+  // the face fluxes u[+1]-u of the 3D heat chain: fewer shared-memory round
+  // trips than a window store + two loads, identical arithmetic per term; and
+  // any producer whose outputs are each read exactly once (HFAV's scalar
+  // contraction, storage.cpp:319-399 with span 1 -- e.g. L2 of the biharmonic
+  // chain) is evaluated inside its consumer: no recomputation, no window, one
+  // dependency level (and barrier) fewer
   auto ops = [](const lf::Expr& e) {
     std::function<int(const lf::Expr&)> f = [&](const lf::Expr& x) -> int {
       int n = x.kind == lf::Expr::Num || x.kind == lf::Expr::Var ? 0 : 1;
@@ -373,7 +377,15 @@ bool analyse(Ctx& C) {
         }
         cost += ops(*e);
       }
-      if (!ok || cost > 2) continue;
+      if (!ok) continue;
+      bool once = true;
+      for (const auto& o : Pg.out) {
+        int reads = 0;
+        for (const auto& c : C.groups)
+          for (const auto& in : c.in) reads += in.var == o.var;
+        once &= reads == 1;
+      }
+      if (cost > 2 && !once) continue;
       for (const auto& in : Pg.in)
         for (size_t pj = 0; pj < C.groups.size(); ++pj)
           if (inl[pj])

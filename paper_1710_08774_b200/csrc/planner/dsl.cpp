@@ -3,6 +3,8 @@
 // Parsed once into a tree and emitted as fully parenthesised C so that the
 // evaluation order is fixed; min/max are `a < b ? a : b` / `a > b ? a : b`.
 #include <cctype>
+#include <cmath>
+#include <cstdio>
 #include <cstdlib>
 
 #include "dsl.hpp"
@@ -162,6 +164,32 @@ void expr_vars(const Expr& e, std::set<std::string>& out) {
   for (const auto& a : e.args) expr_vars(*a, out);
 }
 
+// Division by a literal, strength-reduced where the result is provably the
+// IEEE quotient: a power of two becomes a multiplication by its exact
+// reciprocal (both round the same real number once), and fp32 division by 3
+// becomes lf_div3f (userkernels/stencil_kernels.h: one multiply and an FMA
+// correction, checked bit-identical for all 2^32 inputs by oracle/div3check).
+// Empty: keep the division.
+static std::string div_by_literal(const std::string& num, const std::string& lit, bool f) {
+  char* end = nullptr;
+  const double c = std::strtod(lit.c_str(), &end);
+  if (!end || *end || !std::isfinite(c) || c == 0.0) return "";
+  if (f && static_cast<double>(static_cast<float>(c)) != c) return "";
+  int ex = 0;
+  const double m = std::frexp(c, &ex);  // c = m * 2^ex, |m| in [0.5, 1)
+  if (std::fabs(m) == 0.5) {
+    const int k = ex - 1;  // |c| = 2^k; 1/c = 2^-k must be a normal number of the type
+    if (f ? (k >= -126 && k <= 126) : (k >= -1022 && k <= 1022)) {
+      char buf[64];
+      std::snprintf(buf, sizeof buf, "%s0x1p%d%s", m < 0 ? "-" : "", -k, f ? "f" : "");
+      return "(" + num + " * " + buf + ")";
+    }
+    return "";
+  }
+  if (f && c == 3.0) return "lf_div3f(" + num + ")";
+  return "";
+}
+
 std::string emit_c(const Expr& e, const std::string& type, const std::function<std::string(const std::string&)>& var) {
   const bool f = type == "float";
   auto A = [&](int k) { return emit_c(*e.args[k], type, var); };
@@ -172,7 +200,12 @@ std::string emit_c(const Expr& e, const std::string& type, const std::function<s
     case Expr::Add: return "(" + A(0) + " + " + A(1) + ")";
     case Expr::Sub: return "(" + A(0) + " - " + A(1) + ")";
     case Expr::Mul: return "(" + A(0) + " * " + A(1) + ")";
-    case Expr::Div: return "(" + A(0) + " / " + A(1) + ")";
+    case Expr::Div:
+      if (e.args[1]->kind == Expr::Num) {
+        const std::string r = div_by_literal(A(0), e.args[1]->text, f);
+        if (!r.empty()) return r;
+      }
+      return "(" + A(0) + " / " + A(1) + ")";
     case Expr::Call:
       if (e.text == "sqrt") return std::string(f ? "sqrtf(" : "sqrt(") + A(0) + ")";
       if (e.text == "abs") return std::string(f ? "fabsf(" : "fabs(") + A(0) + ")";

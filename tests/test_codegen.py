@@ -1,0 +1,61 @@
+"""Generated-source checks of the generic executor (no GPU: plans compile with
+NVRTC here): the warp-specialised march is emitted where every streamed axiom
+can be fetched by TMA, single-read producers are evaluated inside their
+consumer (scalar contraction), and divisions by literals are strength-reduced
+only where the result is provably the IEEE quotient.  Numerics are checked on
+the GPU (tests/test_gpu_jit.py)."""
+import re
+
+import paper_1710_08774_b200 as lf
+
+SPECS = lf.PKG_DIR.parent / "tests" / "specs"
+
+
+def kernels(plan):
+    src = plan.source
+    plain = src[src.index("lf_jit_step("):]
+    ws = src[src.index("lf_jit_step_ws("):] if "lf_jit_step_ws(" in src else ""
+    return plain, ws
+
+
+def test_warp_specialised_variant_for_streamed_axioms():
+    for name in ("heat3d_body", "biharm_body"):
+        plain, ws = kernels(lf.Plan.from_file(SPECS / f"{name}.lf"))
+        assert ws, name
+        assert ("lf_tma2(" in ws or "lf_tma3(" in ws) and "lf_mbar_wait(&lf_full" in ws
+        assert "__syncthreads();\n  const bool producer" in ws  # the only CTA-wide barrier: after mbarrier init
+        assert ws.count("__syncthreads") == 1
+
+
+def test_unaligned_row_pitch_keeps_the_plain_kernel():
+    # g_img of box_body.lf: 74 floats per row = 296 B, not a 16-B multiple (TMA strides)
+    plain, ws = kernels(lf.Plan.from_file(SPECS / "box_body.lf"))
+    assert plain and not ws
+
+
+def test_single_level_chain_has_no_consumer_barrier():
+    _, ws = kernels(lf.Plan.from_file(SPECS / "heat3d_body.lf"))
+    assert "bar.sync" not in ws  # fluxes inlined: one group, one level
+
+
+def test_in_place_chains_keep_the_band_loader():
+    plain, ws = kernels(lf.Plan.from_file(SPECS / "heat3d_inplace.lf"))
+    assert not ws and "cp.async.ca.shared.global" in plain
+
+
+def test_single_read_producer_is_evaluated_in_its_consumer():
+    plain, ws = kernels(lf.Plan.from_file(SPECS / "biharm_body.lf"))
+    groups = re.findall(r"// group \d+: kernel '(\w+)'", ws)
+    assert groups == ["lap1", "upd"]  # lap2 (read once, at offset 0) runs inside upd
+    assert "'L2'" not in ws and "inlined 'lap2'" in ws
+    assert ws.count("bar.sync") == 1
+
+
+def test_division_by_literal_strength_reduction():
+    plain, _ = kernels(lf.Plan.from_file(SPECS / "divs_body.lf"))
+    assert "lf_div3f(" in plain                      # fp32 / 3 (oracle/div3check: exhaustive)
+    assert "* 0x1p-2f" in plain and "* 0x1p1f" in plain  # / 4, / 0.5: exact reciprocals
+    assert "/ static_cast<float>(7.0)" in plain       # not provable: stays a division
+    assert "/ static_cast<float>(1.0e-30)" in plain   # not a power of two
+    plain64, _ = kernels(lf.Plan.from_file(SPECS / "biharm_body.lf"))
+    assert "lf_div3f" not in plain64

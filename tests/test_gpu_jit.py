@@ -27,12 +27,23 @@ def run_device(plan, axioms, steps):
     return [g.cpu().numpy() for g in goals]
 
 
+def _div_operands(shape, seed):
+    rng = np.random.default_rng(seed)
+    x = (rng.standard_normal(shape) * 10.0 ** rng.uniform(-44, 37, size=shape)).astype(np.float32)
+    x.flat[::7] = 0.0
+    x.flat[3::11] = -0.0
+    return x
+
+
 CASES = {
     "biharm_body": lambda: {"g_u": inputs.biharm_input(40, 72, seed=5)},
     "heat3d_body": lambda: {"g_u": inputs.heat3d_input(9, 12, 40, seed=6, sigma=3.0)},
     "box_body": lambda: {"g_img": inputs.box_input(33, 70, seed=7)},
     "multi_body": lambda: {"g_x": np.random.default_rng(1).random((21, 52)), "g_scale": np.array([0.75])},
     "laplace3_body": lambda: {"g_x": np.random.default_rng(2).random(1002)},
+    # divisions by literals, strength-reduced (powers of two, fp32 / 3): magnitudes
+    # across the float range incl. zeros, signed zeros and subnormal results
+    "divs_body": lambda: {"g_x": _div_operands((31, 85), seed=8)},
     # multi-nest plans: reductions (inner and outer dim) and broadcast splits
     "normalization_body": lambda: {"g_q": np.random.default_rng(3).random((37, 151)),
                                    "g_zero": np.random.default_rng(4).random(37) * 0.1},
