@@ -652,6 +652,20 @@ bool emit_march(Ctx& C, JitProgram& out, std::ostream& src, bool ws = false) {
   }
   if (ws) {
     tile = out.tile;
+    if (nd == 3) {
+      // TMA stages the halo, so the 64 x 4 consumer lanes need only cover the
+      // groups' own extents: a 64-column tile of 16 rows when the groups are
+      // pointwise in the plane (e.g. heat3d after inlining), full 32-B sectors
+      // per stored row segment and four rows per lane
+      int gs[3] = {0, 0, 0};
+      for (const auto& g : G)
+        for (int d = 1; d < nd; ++d) gs[d] = std::max(gs[d], g.gmax[d] - g.gmin[d]);
+      std::vector<int> keep = tile;
+      tile[2] = 64 - gs[2];
+      tile[1] = std::max(1, 16 - gs[1]);
+      layout();
+      if (smem > 100 * 1024) tile = keep;
+    }
     layout();
     if (smem > 200 * 1024) return false;
     out.ws_smem_bytes = smem + 16 * (PD + 1);  // + the stage mbarriers
@@ -674,10 +688,11 @@ bool emit_march(Ctx& C, JitProgram& out, std::ostream& src, bool ws = false) {
   for (size_t v = 0; v < nv; ++v)
     if (staged[v] >= 0) TS = std::min(TS, C.vmin[v][0] - lead[v]);
   const int cps = std::max<int>(1, std::min<int>(2048 / NT, static_cast<int>((227 * 1024) / (smem + 1024))));
+  long inner = 1;
+  for (int d = 1; d < nd; ++d) inner *= (C.N[d] + tile[d] - 1) / tile[d];
+  if (ws) out.ws_inner_tiles = inner;
   if (!ws) {
     out.prologue = TE - TS;
-    long inner = 1;
-    for (int d = 1; d < nd; ++d) inner *= (C.N[d] + tile[d] - 1) / tile[d];
     out.inner_tiles = inner;
     out.ctas_per_sm = cps;
     out.chunk = nd == 3 ? 64 : 1 << 30;  // rows per chunk of the work order (2D: whole tiles)
@@ -813,7 +828,7 @@ bool emit_march(Ctx& C, JitProgram& out, std::ostream& src, bool ws = false) {
       if (win[v] > 1) src << "  int b" << v << " = 0;\n";
   }
   src << "  const int rows = a.row_hi - a.row_lo;\n";
-  src << "  const long long total = (long long)rows * " << out.inner_tiles << ";\n";
+  src << "  const long long total = (long long)rows * " << inner << ";\n";
   src << "  const long long per = (total + gridDim.x - 1) / gridDim.x;\n";
   src << "  long long s = (long long)blockIdx.x * per;\n";
   src << "  const long long s_end = min(total, s + per);\n";
@@ -822,21 +837,21 @@ bool emit_march(Ctx& C, JitProgram& out, std::ostream& src, bool ws = false) {
   // rows are fetched once and hit in L2, and the row segments neighbouring
   // tiles write into shared sectors meet in L2 before eviction
   const char* UNITS = ws ? "true" : "a.inplace";
-  src << "  const long long units = " << UNITS << " ? (long long)((rows + a.chunk - 1) / a.chunk) * " << out.inner_tiles
+  src << "  const long long units = " << UNITS << " ? (long long)((rows + a.chunk - 1) / a.chunk) * " << inner
       << " : 0;\n";
   src << "  long long u = blockIdx.x;\n";
   src << "  for (;;) {\n";
   src << "  int bt, r0_, r1_;\n";
   src << "  if (" << UNITS << ") {\n";
   src << "    if (u >= units) break;\n";
-  src << "    const int ci = (int)(u / " << out.inner_tiles << ");\n";
-  src << "    bt = (int)(u % " << out.inner_tiles << ");\n";
+  src << "    const int ci = (int)(u / " << inner << ");\n";
+  src << "    bt = (int)(u % " << inner << ");\n";
   src << "    r0_ = a.row_lo + ci * a.chunk;\n";
   src << "    r1_ = min(r0_ + a.chunk, a.row_hi);\n";
   src << "    u += gridDim.x;\n";
   src << "  } else {\n";
   src << "    if (s >= s_end) break;\n";
-  src << "    const long long cs = (long long)a.chunk * " << out.inner_tiles << ";\n";
+  src << "    const long long cs = (long long)a.chunk * " << inner << ";\n";
   src << "    const int ci = (int)(s / cs);\n";
   src << "    const int rc = min(a.chunk, rows - ci * a.chunk);\n";
   src << "    const long long off = s - ci * cs;\n";

@@ -442,12 +442,12 @@ int JitKernel::run(const ExecArgs& a, std::string& err) {
       // whole (chunk, tile) units round-robin over one resident wave: about
       // one unit per CTA (3D: at most 64 rows), at least 8 pipeline depths long
       JitArgs wa = args;
-      long chunk = (rows * prog_.inner_tiles + resident_ws_ - 1) / resident_ws_;
+      long chunk = (rows * prog_.ws_inner_tiles + resident_ws_ - 1) / resident_ws_;
       if (prog_.nd == 3) chunk = std::min<long>(chunk, prog_.chunk);
       chunk = std::min(rows, std::max(chunk, 8L * std::max(1, prog_.prologue)));
       if (const char* e = std::getenv("LF_JIT_CHUNK")) chunk = std::max(1L, std::min<long>(rows, std::atol(e)));
       wa.chunk = static_cast<int>(chunk);
-      const long units = (rows + chunk - 1) / chunk * prog_.inner_tiles;
+      const long units = (rows + chunk - 1) / chunk * prog_.ws_inner_tiles;
       dim3 gws(static_cast<unsigned>(std::max<long>(1, std::min<long>(resident_ws_, units))));
       st = launch(step_ws_, gws, dim3(prog_.ws_threads), prog_.ws_smem_bytes, a.stream, &wa, err, &maps);
     } else {

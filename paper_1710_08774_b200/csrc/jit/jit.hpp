@@ -63,6 +63,7 @@ struct JitProgram {
   bool has_ws = false;
   std::vector<Tma> ws_maps;
   size_t ws_smem_bytes = 0;
+  long ws_inner_tiles = 1;  // the variant's own inner tiling
   int ws_threads = 288;
   std::string error;  // why the chain is not supported
 };
