@@ -583,6 +583,25 @@ bool emit_march(Ctx& C, JitProgram& out, std::ostream& src, bool ws = false) {
     if (win[v] > 0 && (win[v] > 64 || old[v] < -60 || lead[v] > 60))
       return (C.error = "pipeline window deeper than 64 rows", false);
   }
+  // ws: TMA box origins must be 16-B aligned along the contiguous dimension.
+  // Tiles are a multiple of `al` elements there, and each streamed axiom's
+  // window starts up to al - 1 elements further left (its range is widened
+  // for this emission only) so that origin = tile start + a multiple of al.
+  struct RestoreVmin {
+    Ctx& c;
+    std::vector<std::vector<int>> saved;
+    ~RestoreVmin() { c.vmin = saved; }
+  } restore_vmin{C, C.vmin};
+  const int al = 16 / eb;
+  if (ws)
+    for (size_t v = 0; v < nv; ++v) {
+      if (staged[v] < 0) continue;
+      const auto& t = C.P.terminals[staged[v]];
+      const int d = nd - 1;
+      const long so = C.extra_of(static_cast<int>(v))[d] - t.base[d] + C.LO[d];
+      const long m = ((C.vmin[v][d] + so) % al + al) % al;
+      C.vmin[v][d] -= static_cast<int>(m);
+    }
   // inner tile: cells per plane of the widest window a multiple of the block
   int span_in[3] = {0, 0, 0};
   for (size_t v = 0; v < nv; ++v)
@@ -661,11 +680,12 @@ bool emit_march(Ctx& C, JitProgram& out, std::ostream& src, bool ws = false) {
       for (const auto& g : G)
         for (int d = 1; d < nd; ++d) gs[d] = std::max(gs[d], g.gmax[d] - g.gmin[d]);
       std::vector<int> keep = tile;
-      tile[2] = 64 - gs[2];
+      tile[2] = (64 - gs[2]) / al * al;
       tile[1] = std::max(1, 16 - gs[1]);
       layout();
       if (smem > 100 * 1024) tile = keep;
     }
+    tile[nd - 1] = std::max(al, tile[nd - 1] / al * al);
     layout();
     if (smem > 200 * 1024) return false;
     out.ws_smem_bytes = smem + 16 * (PD + 1);  // + the stage mbarriers
@@ -832,11 +852,12 @@ bool emit_march(Ctx& C, JitProgram& out, std::ostream& src, bool ws = false) {
   src << "  const long long per = (total + gridDim.x - 1) / gridDim.x;\n";
   src << "  long long s = (long long)blockIdx.x * per;\n";
   src << "  const long long s_end = min(total, s + per);\n";
-  // ws: always whole (chunk, tile) units dealt round-robin, chunk-major, so the
-  // CTAs running at one time hold neighbouring tiles of the same rows: halo
-  // rows are fetched once and hit in L2, and the row segments neighbouring
-  // tiles write into shared sectors meet in L2 before eviction
-  const char* UNITS = ws ? "true" : "a.inplace";
+  // whole (chunk, tile) units dealt round-robin, chunk-major, so the CTAs
+  // running at one time hold neighbouring tiles of the same rows: halo rows
+  // are fetched once and hit in L2, and the row segments neighbouring tiles
+  // write into shared sectors meet in L2 before eviction (LF_JIT_SPAN_ORDER=1:
+  // the earlier equal-span order, plain kernel only, for comparison)
+  const char* UNITS = ws || !std::getenv("LF_JIT_SPAN_ORDER") ? "true" : "a.inplace";
   src << "  const long long units = " << UNITS << " ? (long long)((rows + a.chunk - 1) / a.chunk) * " << inner
       << " : 0;\n";
   src << "  long long u = blockIdx.x;\n";

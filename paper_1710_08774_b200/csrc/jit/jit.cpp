@@ -394,11 +394,18 @@ int JitKernel::run(const ExecArgs& a, std::string& err) {
           resident_ws_ = std::max(1, sms) * ows;
       }
     }
-    long chunk = std::min<long>(prog_.chunk, rows);
+    // whole (chunk, tile) units round-robin over one resident wave: about one
+    // unit per CTA (3D: at most 64 rows), at least 8 pipeline depths long
+    static const bool span_order = std::getenv("LF_JIT_SPAN_ORDER") != nullptr;
+    long chunk = (rows * prog_.inner_tiles + resident_ - 1) / resident_;
+    if (prog_.nd == 3) chunk = std::min<long>(chunk, prog_.chunk);
+    chunk = std::min(rows, std::max(chunk, 8L * std::max(1, prog_.prologue)));
+    if (span_order) chunk = std::min<long>(prog_.chunk, rows);
     if (const char* e = std::getenv("LF_JIT_CHUNK")) chunk = std::max(1L, std::min<long>(rows, std::atol(e)));
     const long total = rows * prog_.inner_tiles;
     args.chunk = static_cast<int>(chunk);
-    grid.x = static_cast<unsigned>(std::max<long>(1, std::min<long>(resident_, total / 16)));
+    const long units = (rows + chunk - 1) / chunk * prog_.inner_tiles;
+    grid.x = static_cast<unsigned>(std::max<long>(1, std::min<long>(resident_, span_order ? total / 16 : units)));
   } else {
     grid.x = static_cast<unsigned>((rows + prog_.tile[0] - 1) / prog_.tile[0]);
   }
