@@ -70,6 +70,7 @@ struct lf_plan {
   cudaStream_t stream = nullptr;
   cudaStream_t h2d = nullptr, d2h = nullptr;  // copy streams of the pipelined host path
   cudaStream_t comm = nullptr;                // halo-exchange stream of lf_run_slabs
+  cudaStream_t comm2 = nullptr;               // second face stream (parallel schedule)
   std::vector<void*> slab_scratch;            // lf_run_slabs ping-pong buffers (slab-sized)
   std::vector<int64_t> slab_scratch_bytes;
   ~lf_plan() {
@@ -81,6 +82,7 @@ struct lf_plan {
     if (h2d) cudaStreamDestroy(h2d);
     if (d2h) cudaStreamDestroy(d2h);
     if (comm) cudaStreamDestroy(comm);
+    if (comm2) cudaStreamDestroy(comm2);
     for (void* p : slab_scratch)
       if (p) cudaFree(p);
   }
@@ -239,11 +241,20 @@ int slab_check(const lf_plan* plan, const SlabGeom& g, int world, std::string& e
   return LF_OK;
 }
 
-// The overlapped schedule of every step, for each local rank: the output rows
-// its neighbours need ([0, halo_hi) and [rows - halo_lo, rows)) first, then
-// the exchange on `side` while the interior rows are computed on `stream`;
-// the next step waits for both.  Iterated goals ping-pong between the goal
-// buffers and the rank's scratch so the last step lands in the goals.
+// The overlapped schedule of every step, for each local rank: first the
+// output rows its neighbours need -- [0, halo_hi) and [rows - halo_lo, rows),
+// the two faces launched side by side on the high-priority streams `side` and
+// `side2` -- then the exchange on `side`, overlapped with the interior rows on
+// `stream`; the next step waits for both.  Iterated goals ping-pong between the
+// goal buffers and the rank's scratch so the last step lands in the goals.
+// LF_SLAB_SCHEDULE selects the variant (tools/slab_probe.py measures them):
+//   parallel (default)  faces side by side, then the interior next to the exchange;
+//   serial              both faces on `stream`, then the interior;
+//   concurrent          faces and exchange on `side` while the interior already
+//                       runs on `stream` (disjoint output rows, same inputs) --
+//                       best for thin slabs, but the faces then compete with the
+//                       interior for SM slots and HBM (heat3d 512^3: 0.79 of
+//                       the single-domain rate, against 0.96 for serial).
 int run_slabs_core(lf_plan* plan, const SlabGeom& g, std::vector<RankState>& R, int steps, cudaStream_t stream,
                    cudaStream_t side,
                    const std::function<int(std::vector<RankState>&, cudaStream_t, std::string&)>& exchange,
@@ -253,16 +264,35 @@ int run_slabs_core(lf_plan* plan, const SlabGeom& g, std::vector<RankState>& R, 
   cudaEvent_t faces_done, exchanged;
   cudaEventCreateWithFlags(&faces_done, cudaEventDisableTiming);
   cudaEventCreateWithFlags(&exchanged, cudaEventDisableTiming);
-  auto launch = [&](RankState& r, long plo, long phi) {
+  auto launch = [&](RankState& r, long plo, long phi, cudaStream_t on) {
     lf_slab slab{r.lo, r.hi, g.n0, plo, phi};
     lfx::ExecArgs ea;
     ea.plan = &plan->plan;
     ea.terms = r.bufs.data();
     ea.steps = 1;
-    ea.stream = stream;
+    ea.stream = on;
     ea.slab = &slab;
     return plan->exec ? plan->exec->run(ea, err) : plan->jit->run(ea, err);
   };
+  // LF_SLAB_SCHEDULE: parallel (default) | serial | concurrent -- see above
+  static const int sched = [] {
+    const char* e = std::getenv("LF_SLAB_SCHEDULE");
+    if (e && std::string(e) == "serial") return 1;
+    if (e && std::string(e) == "concurrent") return 2;
+    return 0;
+  }();
+  cudaStream_t side2 = side;
+  if (sched == 0) {
+    if (!plan->comm2 && make_side_stream(&plan->comm2, err) != LF_OK) return LF_ERR_CUDA;
+    side2 = plan->comm2;
+  }
+  cudaEvent_t mark, face2;
+  cudaEventCreateWithFlags(&mark, cudaEventDisableTiming);
+  cudaEventCreateWithFlags(&face2, cudaEventDisableTiming);
+  // the side streams start after whatever the caller queued before the run
+  cudaEventRecord(mark, stream);
+  cudaStreamWaitEvent(side, mark, 0);
+  if (side2 != side) cudaStreamWaitEvent(side2, mark, 0);
   int st = LF_OK;
   for (int s = 0; s < steps && st == LF_OK; ++s) {
     const bool to_goal = ((steps - 1 - s) % 2) == 0;
@@ -272,28 +302,43 @@ int run_slabs_core(lf_plan* plan, const SlabGeom& g, std::vector<RankState>& R, 
         if (plan->plan.terminals[i].is_goal) r.bufs[i] = (to_goal || g.paired[i] < 0) ? r.terms[i] : r.scratch[i];
     }
     std::vector<char> split(R.size());
+    const cudaStream_t top = sched == 1 ? stream : side, bottom = sched == 1 ? stream : side2;
     for (size_t k = 0; k < R.size() && st == LF_OK; ++k) {
       const long rows = R[k].hi - R[k].lo;
       split[k] = rows > g.halo_lo + g.halo_hi && (g.halo_lo || g.halo_hi);
       if (!split[k]) {
-        st = launch(R[k], 0, rows);
+        st = launch(R[k], 0, rows, top);
         continue;
       }
-      if (g.halo_hi) st = launch(R[k], 0, g.halo_hi);
-      if (st == LF_OK && g.halo_lo) st = launch(R[k], rows - g.halo_lo, rows);
+      if (g.halo_hi) st = launch(R[k], 0, g.halo_hi, top);
+      if (st == LF_OK && g.halo_lo) st = launch(R[k], rows - g.halo_lo, rows, bottom);
     }
     if (st != LF_OK) break;
-    cudaEventRecord(faces_done, stream);
-    cudaStreamWaitEvent(side, faces_done, 0);
+    if (sched == 1) {  // faces done on the main stream: hand them to the exchange
+      cudaEventRecord(faces_done, stream);
+      cudaStreamWaitEvent(side, faces_done, 0);
+    } else if (side2 != side) {  // both face streams joined on `side`
+      cudaEventRecord(face2, side2);
+      cudaStreamWaitEvent(side, face2, 0);
+    }
+    cudaEventRecord(faces_done, side);
     if ((st = exchange(R, side, err)) != LF_OK) break;
     cudaEventRecord(exchanged, side);
+    if (sched == 0) cudaStreamWaitEvent(stream, faces_done, 0);  // interior after the faces, next to the exchange
     for (size_t k = 0; k < R.size() && st == LF_OK; ++k)
-      if (split[k]) st = launch(R[k], g.halo_hi, R[k].hi - R[k].lo - g.halo_lo);
+      if (split[k]) st = launch(R[k], g.halo_hi, R[k].hi - R[k].lo - g.halo_lo, stream);
     cudaStreamWaitEvent(stream, exchanged, 0);
+    if (sched != 1) {  // next step's faces: after this step's interior (input rows, ping-pong buffer)
+      cudaEventRecord(mark, stream);
+      cudaStreamWaitEvent(side, mark, 0);
+      if (side2 != side) cudaStreamWaitEvent(side2, mark, 0);
+    }
     for (auto& r : R)
       for (size_t i = 0; i < nt; ++i)
         if (g.paired[i] >= 0) r.cur[g.paired[i]] = r.bufs[i];
   }
+  cudaEventDestroy(mark);
+  cudaEventDestroy(face2);
   cudaEventDestroy(faces_done);
   cudaEventDestroy(exchanged);
   return st;
