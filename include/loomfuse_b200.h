@@ -163,10 +163,11 @@ int lf_run_slab(const lf_plan* plan, void* const* terminals, int nterm, const lf
  * [n*rank/world, n*(rank+1)/world) -- on device buffers sized for that slab
  * (the planner's extents with the slab's row count along dim 0).  `nccl_comm`
  * is an ncclComm_t of `world` ranks, one per GPU.  Every step computes the
- * output rows the neighbours need first, exchanges them by NCCL send/recv on
- * a library-owned high-priority stream (ring-wrapped when the boundary of
- * dim 0 is periodic) while the interior rows are computed on `cuda_stream`,
- * and orders the next step after both.  Iterated state ping-pongs through
+ * output rows the neighbours need first (the two faces side by side on two
+ * library-owned high-priority streams), exchanges them by NCCL send/recv on
+ * one of them (ring-wrapped when the boundary of dim 0 is periodic) while the
+ * interior rows are computed on `cuda_stream`, and orders the next step after
+ * both.  Iterated state ping-pongs through
  * slab-sized plan scratch; the final state is left in the goal buffers.  NCCL
  * is loaded at run time (libnccl.so.2; the process's copy when one is
  * loaded).  Replaces the reference's external outer-level parallelism
