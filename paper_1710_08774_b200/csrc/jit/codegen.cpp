@@ -902,7 +902,7 @@ bool emit_march(Ctx& C, JitProgram& out, std::ostream& src, bool ws = false) {
     std::vector<char> keep;  // value carried to the next trip
   };
   std::vector<Rot> rot(G.size());
-  const bool use_rot = !ws && std::getenv("LF_JIT_ROT") && std::atoi(std::getenv("LF_JIT_ROT")) != 0;
+  const bool use_rot = std::getenv("LF_JIT_ROT") && std::atoi(std::getenv("LF_JIT_ROT")) != 0;
   for (size_t gi = 0; gi < G.size(); ++gi) {
     const Grp& g = G[gi];
     Rot& R = rot[gi];
