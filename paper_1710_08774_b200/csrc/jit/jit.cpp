@@ -270,6 +270,30 @@ int JitKernel::run_nests(const ExecArgs& a, std::string& err) {
   return LF_OK;
 }
 
+// Rows per (chunk, tile) unit of the round-robin work order: the chunk count n
+// minimising waves(n) x (rows per chunk + pipeline fill), waves(n) =
+// ceil(n * inner / resident) -- a unit count just above a multiple of the
+// resident CTAs would otherwise leave a nearly empty last wave (Hydro2D named
+// kernels: 306 units on 296 CTAs ran at half speed).  max_chunk caps the rows
+// of a unit (3D: L2 locality of the planes a unit streams).
+static long pick_chunk(long rows, long inner, long resident, long fill, long max_chunk) {
+  long best_n = 1;
+  double best = -1;
+  const long n_lo = std::max(1L, (rows + max_chunk - 1) / max_chunk);
+  const long n_hi = std::max(n_lo, std::min(rows, n_lo + 4 * std::max(1L, resident)));
+  for (long n = n_lo; n <= n_hi; ++n) {
+    const long chunk = (rows + n - 1) / n;
+    const long units = (rows + chunk - 1) / chunk * inner;
+    const long waves = (units + resident - 1) / resident;
+    const double t = static_cast<double>(waves) * static_cast<double>(chunk + fill);
+    if (best < 0 || t < best - 1e-9) {
+      best = t;
+      best_n = n;
+    }
+  }
+  return (rows + best_n - 1) / best_n;
+}
+
 // tensor maps of the streamed axioms for this launch's buffers; false (plain
 // kernel) when a buffer is not 16-B aligned or the driver refuses a map
 bool JitKernel::ws_maps(const std::vector<void*>& bufs, long rows, JitMaps& maps, std::string& err) {
@@ -387,19 +411,22 @@ int JitKernel::run(const ExecArgs& a, std::string& err) {
       resident_ = std::max(1, sms) * std::max(1, occ);
       if (step_ws_) {
         int ows = 0;
+        // keep the plain kernel when the variant cannot be resident, or fits a
+        // single CTA per SM where the plain one fits more (its deeper windows
+        // cost shared memory, and one CTA cannot hide its own level barriers:
+        // the 12-kernel Hydro2D chain runs 2.0 G cell-steps/s warp-specialised
+        // at 1 CTA/SM against 3.6 G plain at 2; heat3d, 2 vs 3 CTAs/SM, is
+        // faster warp-specialised: 310 vs 276 G)
         if (d.occupancy(&ows, static_cast<CUfunction>(step_ws_), prog_.ws_threads, prog_.ws_smem_bytes) != CUDA_SUCCESS ||
-            ows < 1)
-          step_ws_ = nullptr;  // cannot be resident: keep the plain kernel
+            ows < 1 || (ows < 2 && occ >= 2))
+          step_ws_ = nullptr;
         else
           resident_ws_ = std::max(1, sms) * ows;
       }
     }
-    // whole (chunk, tile) units round-robin over one resident wave: about one
-    // unit per CTA (3D: at most 64 rows), at least 8 pipeline depths long
+    // whole (chunk, tile) units round-robin over the resident CTAs
     static const bool span_order = std::getenv("LF_JIT_SPAN_ORDER") != nullptr;
-    long chunk = (rows * prog_.inner_tiles + resident_ - 1) / resident_;
-    if (prog_.nd == 3) chunk = std::min<long>(chunk, prog_.chunk);
-    chunk = std::min(rows, std::max(chunk, 8L * std::max(1, prog_.prologue)));
+    long chunk = pick_chunk(rows, prog_.inner_tiles, resident_, prog_.prologue, prog_.nd == 3 ? prog_.chunk : rows);
     if (span_order) chunk = std::min<long>(prog_.chunk, rows);
     if (const char* e = std::getenv("LF_JIT_CHUNK")) chunk = std::max(1L, std::min<long>(rows, std::atol(e)));
     const long total = rows * prog_.inner_tiles;
@@ -446,12 +473,10 @@ int JitKernel::run(const ExecArgs& a, std::string& err) {
     int st = LF_OK;
     JitMaps maps;
     if (prog_.march && step_ws_ && ws_maps(bufs, rp.rows, maps, err)) {
-      // whole (chunk, tile) units round-robin over one resident wave: about
-      // one unit per CTA (3D: at most 64 rows), at least 8 pipeline depths long
+      // whole (chunk, tile) units round-robin over the resident CTAs
       JitArgs wa = args;
-      long chunk = (rows * prog_.ws_inner_tiles + resident_ws_ - 1) / resident_ws_;
-      if (prog_.nd == 3) chunk = std::min<long>(chunk, prog_.chunk);
-      chunk = std::min(rows, std::max(chunk, 8L * std::max(1, prog_.prologue)));
+      long chunk = pick_chunk(rows, prog_.ws_inner_tiles, resident_ws_, prog_.prologue,
+                              prog_.nd == 3 ? prog_.chunk : rows);
       if (const char* e = std::getenv("LF_JIT_CHUNK")) chunk = std::max(1L, std::min<long>(rows, std::atol(e)));
       wa.chunk = static_cast<int>(chunk);
       const long units = (rows + chunk - 1) / chunk * prog_.ws_inner_tiles;
