@@ -87,6 +87,7 @@ struct Params {
   long long pitch;       // ni + 4
   int strips;
   int ghost_top, ghost_bottom;  // refill reflective ghost rows at these faces
+  unsigned force_slow;          // 1: take every exact fallback (LF_HYDRO_FORCE_SLOW, tests)
   const double* dtdx;    // rank-0 terminal g_dtdx
   double* out[4];
 };
@@ -213,7 +214,7 @@ __global__ void __launch_bounds__(NT, MINB) hydro_fused(const __grid_constant__ 
 
       // ---- A. x: conservative -> primitive on 131 columns
       for (int c = t; c < NPRIM; c += NT) {
-        unsigned bad = 0;
+        unsigned bad = p.force_slow;
         hf::hy_constoprim(row[0][c], row[1][c], row[2][c], row[3][c], &xq[c], &xq[NPRIM + c], &xq[2 * NPRIM + c],
                           &xq[3 * NPRIM + c], &bad);
         if (bad) {
@@ -233,7 +234,7 @@ __global__ void __launch_bounds__(NT, MINB) hydro_fused(const __grid_constant__ 
         hy_slope(xq[c], xq[NPRIM + c], xq[2 * NPRIM + c], xq[3 * NPRIM + c], xq[c + 1], xq[NPRIM + c + 1],
                  xq[2 * NPRIM + c + 1], xq[3 * NPRIM + c + 1], xq[c + 2], xq[NPRIM + c + 2],
                  xq[2 * NPRIM + c + 2], xq[3 * NPRIM + c + 2], &d[0], &d[1], &d[2], &d[3]);
-        unsigned bad = 0;
+        unsigned bad = p.force_slow;
         hf::hy_trace(xq[c + 1], xq[NPRIM + c + 1], xq[2 * NPRIM + c + 1], xq[3 * NPRIM + c + 1], d[0], d[1], d[2],
                      d[3], dtdx, &xm[c], &xm[NQ + c], &xm[2 * NQ + c], &xm[3 * NQ + c], &xp[c], &xp[NQ + c],
                      &xp[2 * NQ + c], &xp[3 * NQ + c], &bad);
@@ -257,7 +258,7 @@ __global__ void __launch_bounds__(NT, MINB) hydro_fused(const __grid_constant__ 
         // first rows is a benign dummy whose result is dropped)
         const bool yface = owns && tt >= 4;
         // branch-free fast paths; a flagged problem is re-solved with the plain kernels
-        unsigned bx = 0, by = 0;
+        unsigned bx = p.force_slow, by = p.force_slow;
         hf::hy_rp cx, cy;
         double psx = hf::hy_riemann_init(xp[t], xp[NQ + t], xp[3 * NQ + t], xm[t + 1], xm[NQ + t + 1],
                                          xm[3 * NQ + t + 1], &cx, &bx);
@@ -312,7 +313,7 @@ __global__ void __launch_bounds__(NT, MINB) hydro_fused(const __grid_constant__ 
                 xf[3 * NT + t], xf[t + 1], xf[NT + t + 1], xf[2 * NT + t + 1], xf[3 * NT + t + 1], dtdx, &u1[0],
                 &u1[1], &u1[2], &u1[3]);
       double yq[4];
-      unsigned bad = 0;
+      unsigned bad = p.force_slow;
       hf::hy_constoprim(u1[0], u1[2], u1[1], u1[3], &yq[0], &yq[1], &yq[2], &yq[3], &bad);
       if (bad) {
         const D4 q = slow_constoprim(u1[0], u1[2], u1[1], u1[3]);
@@ -327,7 +328,7 @@ __global__ void __launch_bounds__(NT, MINB) hydro_fused(const __grid_constant__ 
                  yq[2], yq[3], &d[0],
                  &d[1], &d[2], &d[3]);
         // minus state of row r-1 is read by the y-face (r-2)+1/2 at C of the next row
-        bad = 0;
+        bad = p.force_slow;
         hf::hy_trace(yq1[0], yq1[NT], yq1[2 * NT], yq1[3 * NT], d[0], d[1], d[2], d[3], dtdx, &yqm[0], &yqm[1],
                      &yqm[2], &yqm[3], &yp[0], &yp[1], &yp[2], &yp[3], &bad);
         if (bad) {
@@ -406,6 +407,8 @@ int launch_step(const double* const in[4], double* const out[4], const double* d
   p.ghost_top = rp.top;
   p.ghost_bottom = rp.bottom;
   p.dtdx = dtdx;
+  static const unsigned force_slow = std::getenv("LF_HYDRO_FORCE_SLOW") ? 1u : 0u;
+  p.force_slow = force_slow;
   for (int a = 0; a < 4; ++a) p.out[a] = out[a];
   const long long work = (long long)p.strips * (rp.hi - rp.lo);
   // each CTA must get at most 3 row segments (rowstream.cuh): at least
