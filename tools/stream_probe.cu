@@ -46,6 +46,35 @@ __global__ void __launch_bounds__(32) copy_strips(const double* __restrict__ in,
   }
 }
 
+// NW warps per CTA marching NW adjacent sub-strips of 32*CPL columns in lockstep
+template <int CPL, int NW>
+__global__ void __launch_bounds__(32 * NW) copy_strips_nw(const double* __restrict__ in, double* __restrict__ out,
+                                                          int n, long long pitch, int strips, int out_shift) {
+  const int lane = threadIdx.x & 31, wq = threadIdx.x >> 5;
+  const long long total = (long long)strips * n;
+  long long a = total * blockIdx.x / gridDim.x, b = total * (blockIdx.x + 1) / gridDim.x;
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  while (a < b) {
+    const int s = (int)(a / n);
+    const long long end = b < (long long)(s + 1) * n ? b : (long long)(s + 1) * n;
+    const int jb = (int)(a - (long long)s * n), je = (int)(end - (long long)s * n);
+    for (int j = jb; j < je; ++j) {
+      const long long col = (long long)s * 32 * CPL * NW + wq * 32 * CPL + CPL * lane;
+      const double* src = in + (long long)(j + 2) * pitch + 2 + col;
+      double* dst = out + (long long)(j + 2) * pitch + out_shift + col;
+#pragma unroll
+      for (int h = 0; h < CPL / 2; ++h) {
+        const double2 v = __ldg(reinterpret_cast<const double2*>(src) + h);
+        asm volatile("st.global.L2::cache_hint.v2.f64 [%0], {%1, %2}, %3;" ::"l"(dst + 2 * h), "d"(v.x), "d"(v.y),
+                     "l"(pol)
+                     : "memory");
+      }
+    }
+    a = end;
+  }
+}
+
 template <class F>
 float time_ms(F f, int reps = 10) {
   cudaEvent_t s, e;
@@ -72,6 +101,16 @@ void strips(const double* in, double* out, int n, long long pitch, int occ, int 
   printf("strips cpl=%d ef=%d occ=%2d shift=%d: %8.1f GB/s (%.3f ms)\n", CPL, EF, occ, shift, bytes / ms * 1e-6, ms);
 }
 
+template <int CPL, int NW>
+void strips_nw(const double* in, double* out, int n, long long pitch, int occ, int sms) {
+  const int nstrips = n / (32 * CPL * NW);
+  int ctas = sms * occ;
+  if (ctas >= nstrips) ctas = ctas / nstrips * nstrips;
+  const float ms = time_ms([&] { copy_strips_nw<CPL, NW><<<ctas, 32 * NW>>>(in, out, n, pitch, nstrips, 2); });
+  const double bytes = 2.0 * 8.0 * n * (double)n;
+  printf("strips cpl=%d nw=%d occ=%2d (CTAs/SM): %8.1f GB/s (%.3f ms)\n", CPL, NW, occ, bytes / ms * 1e-6, ms);
+}
+
 int main(int argc, char** argv) {
   const int n = argc > 1 ? atoi(argv[1]) : 16384;
   const long long pitch = n + 4;
@@ -87,6 +126,11 @@ int main(int argc, char** argv) {
     copy_linear<<<sms * 8, 256>>>(reinterpret_cast<const double2*>(in), reinterpret_cast<double2*>(out), n2);
   });
   printf("linear copy: %8.1f GB/s (%.3f ms, %lld B)\n", 2.0 * elems * 8 / ms * 1e-6, ms, elems * 8);
+  for (int occ : {4, 6, 8, 12}) {
+    strips_nw<2, 2>(in, out, n, pitch, occ, sms);
+    strips_nw<2, 4>(in, out, n, pitch, occ / 2 > 0 ? occ / 2 : 1, sms);
+    strips_nw<4, 2>(in, out, n, pitch, occ, sms);
+  }
   for (int occ : {8, 12, 16, 24}) {
     strips<2, true>(in, out, n, pitch, occ, 2, sms);
     strips<2, true>(in, out, n, pitch, occ, 0, sms);
