@@ -6,12 +6,15 @@
 // The planner fuses all 12 kernel rules into one (j, i) nest: the x-swept
 // state rho1..en1 is an intermediate with a 5-row window and every x/y
 // intermediate is contracted.  The executor realises exactly that:
-//   * a CTA of 128 threads owns a strip of 127 cells and marches its rows;
+//   * a CTA of 128 threads owns a strip of 124 cells and marches its rows;
 //     rows of the four state arrays arrive by TMA (4 tensor maps, 2 rows per
-//     stage, 4-slot mbarrier ring);
-//   * x-sweep of a row through shared memory: prims (131 columns), slope +
-//     trace (129), Riemann + flux on exactly 128 faces -- one face per thread,
-//     so the expensive solver never runs a partial warp -- then the update;
+//     stage, 2-slot mbarrier ring);
+//   * x-sweep of a row through shared memory: prims (128 columns), slope +
+//     trace (126) -- one pass of the CTA each, so no warp runs a second,
+//     nearly empty pass while the others wait at the barrier (measured 1.3 %
+//     faster than 127-cell strips, which need 131 / 129) -- Riemann + flux on
+//     the 125 faces (one per thread; the last three threads repeat face 124),
+//     then the update;
 //   * thread t keeps column i0+t's y-sweep in registers: the x-swept state,
 //     prims, the plus-face trace state and the previous face flux are rolling
 //     windows along j, one y-face Riemann solve per row per thread;
@@ -39,7 +42,7 @@ namespace hf {
 namespace {
 
 constexpr int NT = 128;                // threads per CTA = x-faces per row
-constexpr int W = NT - 1;              // cells per strip
+constexpr int W = NT - 4;              // cells per strip
 constexpr int H = 2;                   // radius of each sweep
 constexpr int BOXW = 132;              // staged columns from the even storage column <= i0 (131 used)
 constexpr int R = 2;                   // rows per stage
@@ -260,8 +263,9 @@ __global__ void __launch_bounds__(NT, MINB) hydro_fused(const __grid_constant__ 
         // branch-free fast paths; a flagged problem is re-solved with the plain kernels
         unsigned bx = p.force_slow, by = p.force_slow;
         hf::hy_rp cx, cy;
-        double psx = hf::hy_riemann_init(xp[t], xp[NQ + t], xp[3 * NQ + t], xm[t + 1], xm[NQ + t + 1],
-                                         xm[3 * NQ + t + 1], &cx, &bx);
+        const int fx = min(t, W);  // faces W+1.. of the last threads: a harmless repeat of face W
+        double psx = hf::hy_riemann_init(xp[fx], xp[NQ + fx], xp[3 * NQ + fx], xm[fx + 1], xm[NQ + fx + 1],
+                                         xm[3 * NQ + fx + 1], &cx, &bx);
         double psy = hf::hy_riemann_init(ypo[0], ypo[1], ypo[3], yqm[0], yqm[1], yqm[3], &cy, &by);
 #pragma unroll 2
         for (int it = 0; it < HY_NITER; ++it) {
@@ -269,12 +273,12 @@ __global__ void __launch_bounds__(NT, MINB) hydro_fused(const __grid_constant__ 
           psy = hf::hy_riemann_newton(&cy, psy, &by);
         }
         double gx[4], gy[4];
-        hf::hy_riemann_sample(&cx, psx, xp[t], xp[2 * NQ + t], xm[t + 1], xm[2 * NQ + t + 1], &gx[0], &gx[1],
+        hf::hy_riemann_sample(&cx, psx, xp[fx], xp[2 * NQ + fx], xm[fx + 1], xm[2 * NQ + fx + 1], &gx[0], &gx[1],
                               &gx[2], &gx[3], &bx);
         hf::hy_riemann_sample(&cy, psy, ypo[0], ypo[2], yqm[0], yqm[2], &gy[0], &gy[1], &gy[2], &gy[3], &by);
         if (bx) {
-          const D4 g4 = slow_riemann(xp[t], xp[NQ + t], xp[2 * NQ + t], xp[3 * NQ + t], xm[t + 1], xm[NQ + t + 1],
-                                     xm[2 * NQ + t + 1], xm[3 * NQ + t + 1]);
+          const D4 g4 = slow_riemann(xp[fx], xp[NQ + fx], xp[2 * NQ + fx], xp[3 * NQ + fx], xm[fx + 1],
+                                     xm[NQ + fx + 1], xm[2 * NQ + fx + 1], xm[3 * NQ + fx + 1]);
 #pragma unroll
           for (int a = 0; a < 4; ++a) gx[a] = g4.v[a];
         }
