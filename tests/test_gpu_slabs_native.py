@@ -168,3 +168,18 @@ def test_slab_run_argument_errors():
     with pytest.raises(lf.LoomfuseError) as e:
         lf.run_slabs_local(plan, [bufs] * 5, steps=1)  # more ranks than planes
     assert e.value.code == lf.LF_ERR_SPEC
+
+
+@pytest.mark.parametrize("schedule", ["serial", "concurrent"])
+def test_alternative_slab_schedules_match_whole_domain(schedule):
+    """The selectable slab schedules (LF_SLAB_SCHEDULE, read once per process;
+    the default `parallel` one runs everywhere above) give the same bits: the
+    decomposition tests of this file, re-run in a subprocess."""
+    import os
+    import subprocess
+    import sys
+    env = dict(os.environ, LF_SLAB_SCHEDULE=schedule)
+    r = subprocess.run([sys.executable, "-m", "pytest", __file__, "-q", "-m", "gpu", "-k",
+                        "local_slab_decomposition or nccl_one_rank"], env=env, capture_output=True, text=True,
+                       timeout=600, cwd=str(Path(__file__).parents[1]))
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
