@@ -758,6 +758,12 @@ bool emit_march(Ctx& C, JitProgram& out, std::ostream& src, bool ws = false) {
   const int STEP = nd == 3 ? NT / 64 : NT;
   int ILP = 1;  // cells whose operands are loaded before any is evaluated (1 measured best)
   if (const char* e = std::getenv("LF_JIT_ILP")) ILP = std::max(1, std::atoi(e));
+  // 2D, opt-in (LF_JIT_VEC=2): adjacent columns per thread sharing their
+  // window loads.  Exact, but measured slower (biharm 157 vs 222 G, box 244 vs
+  // 274 G): lanes two elements apart make every shared-memory load a 2-way
+  // bank conflict and the shared operands cost registers.
+  int VEC = 1;
+  if (const char* e = std::getenv("LF_JIT_VEC")) VEC = std::max(1, std::atoi(e));
   const char* LANE = nd == 3 ? "ty" : "tx";
   // ---- persistent CTAs: each takes an equal share of the (row chunk, inner
   // tile, row) space in that order and marches it as one or more segments,
@@ -1102,6 +1108,112 @@ bool emit_march(Ctx& C, JitProgram& out, std::ostream& src, bool ws = false) {
       src << "        const bool act = true;\n";
     }
     src << "        const int c1hi = min(" << (lo[1] + ext[1] - 1) << ", " << (C.N[1] - 1 + g.gmax[1]) << " - o1);\n";
+    auto load_index = [&](int var, const std::vector<int>& rel) {
+      for (size_t li = 0; li < g.loads.size(); ++li)
+        if (g.loads[li].var == var && g.loads[li].rel == rel) return static_cast<int>(li);
+      return -1;
+    };
+    // evaluation of one cell from its loaded operands l<li>, then its stores
+    auto emit_eval = [&](const std::string& I) -> bool {
+    for (const auto& in : g.in) {
+      if (in.via < 0) {
+        src << I << "const T p_" << in.param << " = l" << load_index(in.var, in.rel) << ";\n";
+        continue;
+      }
+      // the inlined producer, evaluated at this read's offset
+      const Grp& pg = C.inlined[in.via];
+      const auto& pk = C.P.rs.kernels[pg.kernel];
+      std::string oparam;
+      std::vector<int> orel(nd, 0);
+      for (const auto& o : pg.out)
+        if (o.var == in.var) {
+          oparam = o.param;
+          orel = o.rel;
+        }
+      std::map<std::string, std::string> pv;
+      for (const auto& pin : pg.in) {
+        std::vector<int> r(nd);
+        for (int d = 0; d < nd; ++d) r[d] = in.rel[d] - orel[d] + pin.rel[d];
+        pv[pin.param] = "l" + std::to_string(load_index(pin.var, r));
+      }
+      std::string e2;
+      auto e = lf::parse_expr(pk.bodies.at(oparam), e2);
+      if (!e) return (C.error = "kernel '" + pk.name + "': " + e2, false);
+      src << I << "const T p_" << in.param << " = "
+          << lf::emit_c(*e, C.T, [&](const std::string& n) { return pv.at(n); }) << ";  // inlined '" << pk.name
+          << "'\n";
+    }
+    if (!emit_bodies(C, g, src, I.c_str())) return false;
+    for (const auto& o : g.out) {
+      if (C.smem_var[o.var])
+        src << I << "v" << o.var << "[" << rb(o.var, o.rel[0]) << " + " << inplane(o.var, o.rel) << "] = q_"
+            << o.param << ";\n";
+      const int ti = C.terminal_of(o.var, true);
+      if (ti < 0) continue;
+      // goal: own chunk rows, own tile cells, inside the domain
+      src << I << "if (y" << plus(o.rel[0]) << " >= r0 && y" << plus(o.rel[0]) << " < r1";
+      for (int d = 1; d < nd; ++d)
+        src << " && c" << d << plus(o.rel[d]) << " >= 0 && c" << d << plus(o.rel[d]) << " < " << tile[d] << " && x" << d
+            << plus(o.rel[d]) << " < N" << d;
+      std::vector<std::string> pos;
+      for (int d = 0; d < nd; ++d) pos.push_back((d == 0 ? std::string("y") : "x" + std::to_string(d)) + plus(o.rel[d]));
+      src << ") t" << ti << "[" << C.tidx(ti, pos, std::vector<int>(nd, 0)) << "] = q_" << o.param << ";\n";
+    }
+      return true;
+    };
+    // 2D: V adjacent columns per thread; window operands are loaded once per
+    // distinct (variable, row, column) over the V cells and shared between them
+    const int V = nd == 2 && !use_rot && ILP == 1 ? VEC : 1;
+    if (V > 1) {
+      const int KV = (ext[1] + STEP * V - 1) / (STEP * V);
+      src << "        #pragma unroll\n";
+      src << "        for (int k = 0; k < " << KV << "; ++k) {\n";
+      src << "          const int cb = " << V << " * tx" << plus(lo[1]) << " + k * " << STEP * V << ";\n";
+      std::map<std::tuple<int, int, int>, int> need;  // (var, row offset, column offset) -> first cell needing it
+      for (const auto& in : g.loads)
+        if (win[in.var] > 0)
+          for (int v = 0; v < V; ++v) {
+            const auto key = std::make_tuple(in.var, in.rel[0], v + in.rel[1]);
+            auto it = need.find(key);
+            if (it == need.end() || it->second > v) need[key] = v;
+          }
+      auto uname = [](int var, int r, int u) {
+        return "w" + std::to_string(var) + "_" + (r < 0 ? "m" + std::to_string(-r) : std::to_string(r)) + "_" +
+               (u < 0 ? "m" + std::to_string(-u) : std::to_string(u));
+      };
+      for (const auto& [key, v0] : need) {
+        const auto [var, r, u] = key;
+        src << "          const T " << uname(var, r, u) << " = cb" << plus(v0) << " <= c1hi ? v" << var << "["
+            << rb(var, r) << " + cb" << plus(u - C.vmin[var][1]) << "] : T(0);\n";
+      }
+      for (int v = 0; v < V; ++v) {
+        src << "          { const int c1 = cb" << plus(v) << ";\n";
+        src << "            const int x1 = o1 + c1;\n";
+        src << "            if (c1 <= c1hi) {\n";
+        for (size_t li = 0; li < g.loads.size(); ++li) {
+          const Load& in = g.loads[li];
+          if (win[in.var] > 0) {
+            src << "            const T l" << li << " = " << uname(in.var, in.rel[0], v + in.rel[1]) << ";\n";
+          } else {
+            const int ti = C.terminal_of(in.var, false);
+            std::string r;
+            if (C.P.terminals[ti].dims.empty()) {
+              r = "s" + std::to_string(ti);
+            } else {
+              std::vector<std::string> pos;
+              for (int d = 0; d < nd; ++d)
+                pos.push_back((d == 0 ? std::string("y") : "x" + std::to_string(d)) + plus(in.rel[d]));
+              r = "__ldg(t" + std::to_string(ti) + " + " + C.tidx(ti, pos, C.extra_of(in.var)) + ")";
+            }
+            src << "            const T l" << li << " = " << r << ";\n";
+          }
+        }
+        if (!emit_eval("            ")) return false;
+        src << "            }\n          }\n";
+      }
+      src << "        }\n      }\n    }\n";
+      continue;
+    }
     // phase 1: every operand of the K cells this thread owns (independent loads)
     // in batches of ILP cells (bounded register footprint)
     const int B = std::min(K, ILP);
@@ -1157,56 +1269,8 @@ bool emit_march(Ctx& C, JitProgram& out, std::ostream& src, bool ws = false) {
     src << "          const int c1 = " << LANE << plus(lo[1]) << " + k * " << STEP << ";\n";
     src << "          const int x1 = o1 + c1;\n";
     src << "          if (act && c1 <= c1hi) {\n";
-    auto load_index = [&](int var, const std::vector<int>& rel) {
-      for (size_t li = 0; li < g.loads.size(); ++li)
-        if (g.loads[li].var == var && g.loads[li].rel == rel) return static_cast<int>(li);
-      return -1;
-    };
     for (size_t li = 0; li < g.loads.size(); ++li) src << "            const T l" << li << " = a_l" << li << "[kk];\n";
-    for (const auto& in : g.in) {
-      if (in.via < 0) {
-        src << "            const T p_" << in.param << " = l" << load_index(in.var, in.rel) << ";\n";
-        continue;
-      }
-      // the inlined producer, evaluated at this read's offset
-      const Grp& pg = C.inlined[in.via];
-      const auto& pk = C.P.rs.kernels[pg.kernel];
-      std::string oparam;
-      std::vector<int> orel(nd, 0);
-      for (const auto& o : pg.out)
-        if (o.var == in.var) {
-          oparam = o.param;
-          orel = o.rel;
-        }
-      std::map<std::string, std::string> pv;
-      for (const auto& pin : pg.in) {
-        std::vector<int> r(nd);
-        for (int d = 0; d < nd; ++d) r[d] = in.rel[d] - orel[d] + pin.rel[d];
-        pv[pin.param] = "l" + std::to_string(load_index(pin.var, r));
-      }
-      std::string e2;
-      auto e = lf::parse_expr(pk.bodies.at(oparam), e2);
-      if (!e) return (C.error = "kernel '" + pk.name + "': " + e2, false);
-      src << "            const T p_" << in.param << " = "
-          << lf::emit_c(*e, C.T, [&](const std::string& n) { return pv.at(n); }) << ";  // inlined '" << pk.name
-          << "'\n";
-    }
-    if (!emit_bodies(C, g, src, "            ")) return false;
-    for (const auto& o : g.out) {
-      if (C.smem_var[o.var])
-        src << "            v" << o.var << "[" << rb(o.var, o.rel[0]) << " + " << inplane(o.var, o.rel) << "] = q_"
-            << o.param << ";\n";
-      const int ti = C.terminal_of(o.var, true);
-      if (ti < 0) continue;
-      // goal: own chunk rows, own tile cells, inside the domain
-      src << "            if (y" << plus(o.rel[0]) << " >= r0 && y" << plus(o.rel[0]) << " < r1";
-      for (int d = 1; d < nd; ++d)
-        src << " && c" << d << plus(o.rel[d]) << " >= 0 && c" << d << plus(o.rel[d]) << " < " << tile[d] << " && x" << d
-            << plus(o.rel[d]) << " < N" << d;
-      std::vector<std::string> pos;
-      for (int d = 0; d < nd; ++d) pos.push_back((d == 0 ? std::string("y") : "x" + std::to_string(d)) + plus(o.rel[d]));
-      src << ") t" << ti << "[" << C.tidx(ti, pos, std::vector<int>(nd, 0)) << "] = q_" << o.param << ";\n";
-    }
+    if (!emit_eval("            ")) return false;
     src << "          }\n        }\n        }\n      }\n    }\n";
   }
   if (ws) {

@@ -121,3 +121,18 @@ def test_random_chain_matches_generic_oracle(seed, tmp_path):
     view = np.uint64 if got.dtype == np.float64 else np.uint32
     bad = np.count_nonzero(got.view(view) != np.ascontiguousarray(ref).view(view))
     assert bad == 0, f"seed {seed}: {bad} cells differ\n{text}"
+
+
+@pytest.mark.gpu
+def test_random_chains_with_opt_in_vector_columns():
+    """LF_JIT_VEC=2 (2D: two adjacent columns per thread sharing window loads,
+    opt-in) on the same random chains, in a subprocess (the knob is read at
+    plan creation)."""
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+    env = dict(os.environ, LF_JIT_VEC="2")
+    r = subprocess.run([sys.executable, "-m", "pytest", __file__, "-q", "-m", "gpu", "-k", "matches_generic_oracle"],
+                       env=env, capture_output=True, text=True, timeout=600, cwd=str(Path(__file__).parents[1]))
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
