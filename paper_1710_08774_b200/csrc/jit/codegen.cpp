@@ -1784,6 +1784,8 @@ bool emit_nests(const lf::Plan& P, const std::string& sources, JitProgram& out, 
       src << "  }\n}\n";
     } else {
       // ---- reduction nest: warp per parallel cell, reduced dims in order
+      int LFB = 2;  // element blocks of 32 in flight per warp (LF_JIT_RED_BLOCKS; 104 -> 117 G at 2, no gain beyond)
+      if (const char* e = std::getenv("LF_JIT_RED_BLOCKS")) LFB = std::max(1, std::atoi(e));
       std::set<int> Pd;
       for (int d : space)
         if (!R.count(d)) Pd.insert(d);
@@ -1826,7 +1828,7 @@ bool emit_nests(const lf::Plan& P, const std::string& sources, JitProgram& out, 
       }
       src << "extern \"C\" __global__ void __launch_bounds__(256) " << fn << "(const LfArgs a) {\n";
       pointers(src);
-      src << "  __shared__ T lf_red[8][" << reds.size() << "][32];\n";
+      src << "  __shared__ T lf_red[8][" << LFB << "][" << reds.size() << "][32];\n";
       src << "  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;\n";
       src << "  for (long long pc = blockIdx.x * 8LL + warp; pc < " << pcells << "LL; pc += gridDim.x * 8LL) {\n";
       src << "    long long rem = pc;\n";
@@ -1857,16 +1859,19 @@ bool emit_nests(const lf::Plan& P, const std::string& sources, JitProgram& out, 
         }
         src << "    T acc" << m << " = v" << ct << ";\n";
       }
-      // element loop
-      src << "    for (long long rb = 0; rb < " << rcount << "LL; rb += 32) {\n";
-      src << "      const bool ok = rb + lane < " << rcount << "LL;\n";
-      src << "      long long rr = ok ? rb + lane : " << (rcount - 1) << "LL;\n";
+      // element loop, LFB blocks of 32 elements per iteration: the element code
+      // (global loads) of every block is issued before the ordered
+      // accumulation of the first, so a warp keeps LFB blocks of loads in
+      // flight instead of idling on memory after each 32-element accumulation
+      std::ostringstream stage;  // one block's elements into lf_red[warp][LFBUF]
+      stage << "      const bool ok = rb + lane < " << rcount << "LL;\n";
+      stage << "      long long rr = ok ? rb + lane : " << (rcount - 1) << "LL;\n";
       for (int d = nd - 1; d >= 0; --d)
-        if (R.count(d)) src << "      const int x" << d << " = (int)(rr % " << N[d] << "); rr /= " << N[d] << ";\n";
+        if (R.count(d)) stage << "      const int x" << d << " = (int)(rr % " << N[d] << "); rr /= " << N[d] << ";\n";
       std::ostringstream el;
       for (int r : topo)
         if (in_nest[r] && cls[r] == 1) emit_rap(r, nv, el, "      ", okk, "ok");
-      src << el.str();
+      stage << el.str();
       // element operands of each reduction into shared memory, then the ordered accumulation
       std::vector<std::vector<int>> elem_in(reds.size());
       for (size_t m = 0; m < reds.size(); ++m) {
@@ -1880,15 +1885,27 @@ bool emit_nests(const lf::Plan& P, const std::string& sources, JitProgram& out, 
           if (ti.ident == to.ident && ti.dims == to.dims && !(ti == to)) continue;
           const int pr = g.producer[t];
           if (pr >= 0 && g.raps[pr].kind == lf::RapKind::kernel && nest_of(pr) != nv && !done[t]) {
-            src << "      const T v" << t << " = " << mat_index(t) << ";\n";
+            stage << "      const T v" << t << " = " << mat_index(t) << ";\n";
             done[t] = 1;
           }
-          src << "      lf_red[warp][" << m << "][lane] = v" << t << ";\n";
+          stage << "      lf_red[warp][LFBUF][" << m << "][lane] = v" << t << ";\n";
           elem_in[m].push_back(static_cast<int>(i));
         }
       }
+      const std::string stage_text = stage.str();
+      src << "    for (long long rb0 = 0; rb0 < " << rcount << "LL; rb0 += " << 32 * LFB << ") {\n";
+      for (int h = 0; h < LFB; ++h) {
+        std::string t = stage_text;
+        for (size_t pos; (pos = t.find("LFBUF")) != std::string::npos;) t.replace(pos, 5, std::to_string(h));
+        src << "      if (rb0 + " << 32 * h << " < " << rcount << "LL) {\n";
+        src << "      const long long rb = rb0 + " << 32 * h << ";\n";
+        src << t;
+        src << "      }\n";
+      }
       src << "      __syncwarp();\n";
-      src << "      const int cnt = (int)min(32LL, " << rcount << "LL - rb);\n";
+      src << "      for (int h = 0; h < " << LFB << "; ++h) {\n";
+      src << "      const long long rb = rb0 + 32 * h;\n";
+      src << "      const int cnt = (int)max(0LL, min(32LL, " << rcount << "LL - rb));\n";
       src << "      for (int e = 0; e < cnt; ++e) {\n";
       for (size_t m = 0; m < reds.size(); ++m) {
         const auto& rap = g.raps[reds[m]];
@@ -1896,13 +1913,14 @@ bool emit_nests(const lf::Plan& P, const std::string& sources, JitProgram& out, 
         std::map<std::string, std::string> pv;
         for (size_t i = 0; i < k.inputs.size(); ++i) {
           const bool is_elem = std::find(elem_in[m].begin(), elem_in[m].end(), (int)i) != elem_in[m].end();
-          pv[k.inputs[i].first] = is_elem ? "lf_red[warp][" + std::to_string(m) + "][e]" : "acc" + std::to_string(m);
+          pv[k.inputs[i].first] = is_elem ? "lf_red[warp][h][" + std::to_string(m) + "][e]" : "acc" + std::to_string(m);
         }
         if (!emit_kernel(
                 k, T, [&](const std::string& n) { return pv.at(n); },
                 [&](const std::string&) { return "acc" + std::to_string(m); }, false, src, "        ", err))
           return false;
       }
+      src << "      }\n";
       src << "      }\n";
       src << "      __syncwarp();\n";
       src << "    }\n";
