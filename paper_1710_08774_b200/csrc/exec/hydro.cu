@@ -11,8 +11,9 @@
 //     stage, 2-slot mbarrier ring);
 //   * x-sweep of a row through shared memory: prims (128 columns), slope +
 //     trace (126) -- one pass of the CTA each, so no warp runs a second,
-//     nearly empty pass while the others wait at the barrier (measured 1.3 %
-//     faster than 127-cell strips, which need 131 / 129) -- Riemann + flux on
+//     nearly empty pass while the others wait at the barrier (127-cell strips
+//     need 131 / 129; same speed in a same-box A/B, fewer barrier stalls) --
+//     Riemann + flux on
 //     the 125 faces (one per thread; the last three threads repeat face 124),
 //     then the update;
 //   * thread t keeps column i0+t's y-sweep in registers: the x-swept state,
