@@ -499,7 +499,7 @@ void emit_prelude(Ctx& C, std::ostream& src, int threads, int min_blocks = 1, bo
     src << "struct LfArgs { void* t[32]; long long n0; int row_lo, row_hi, top, bottom, chunk, inplace; };\n";
     src << "extern \"C\" __global__ void __launch_bounds__(" << threads << ", " << min_blocks
         << ") lf_jit_step(const LfArgs a) {\n";
-    src << "  extern __shared__ __align__(16) unsigned char lf_smem[];\n";
+    src << "  extern __shared__ __align__(128) unsigned char lf_smem[];\n";  // one declaration for both march kernels
   } else {
     // warp-specialised variant: tensor maps of the streamed axioms (must match
     // lfx::JitMaps in jit.cpp) and the mbarrier / TMA primitives it uses
