@@ -46,6 +46,7 @@ struct Params {
   long long pitch;    // ni + 4
   int strips;         // ni / SW
   int write_ghost_top, write_ghost_bottom;
+  int store_policy;   // L2 policy of the output stores (l2_store_policy)
 };
 
 template <int CPL>
@@ -221,7 +222,7 @@ __global__ void __launch_bounds__(32, K::OCC)
     for (int g = 0; g < S; ++g) rr.issue(g, &tin);
   __syncwarp();
 
-  const uint64_t pol = l2_evict_first_policy();
+  const uint64_t pol = l2_store_policy(p.store_policy);
   // extra columns: lane 0 -> logical -2,-1 ; lane 31 -> SW, SW+1 ; others: harmless copy
   const int ex_col = lane == 0 ? 0 : (lane == 31 ? SW + H : CPL * lane + H);
   // zero ghost ring of the goal buffer at the global edges
@@ -373,6 +374,14 @@ int launch_step(const double* in, double* out, int ni, const RowPart& rp, cudaSt
   p.row_hi = rp.hi;
   p.write_ghost_top = rp.top;
   p.write_ghost_bottom = rp.bottom;
+  // evict_last: the output of an iteration is the next one's input and 134 MB
+  // of it at 4096^2 nearly fits the 126 MB L2 -- same-box A/B 321 -> 340 G
+  // (evict_first) at 4096^2, 289 -> 295 G at 16384^2 (LF_BIHARM_STORE_POLICY)
+  static const int store_policy = [] {
+    const char* e = std::getenv("LF_BIHARM_STORE_POLICY");
+    return e ? std::atoi(e) : 2;
+  }();
+  p.store_policy = store_policy;
   // at least ~16 rows per CTA so the 4 priming rows stay a small fraction
   const int ctas = rowstream_ctas(slots, p.strips, rp.hi - rp.lo);
   if ((long long)ctas * 2 < p.strips) {

@@ -52,6 +52,7 @@ struct Params {
   int units;            // tiles * kchunks
   int wrap_i, wrap_j, wrap_k;  // refill periodic ghosts along this dim
   int patch;                   // two-step pass: patch periodic images on face tiles
+  int store_policy;            // L2 policy of the output stores (l2_store_policy)
 };
 
 // Work unit u = (k chunk, column tile), k-chunk major: at any moment all
@@ -113,7 +114,7 @@ __global__ void __launch_bounds__(THREADS, 2)
   }
 
   // ---------------- consumers: warp w owns rows RPW*w .. RPW*w+RPW-1; lane owns cells lane, lane+32
-  const uint64_t pol = l2_evict_first_policy();
+  const uint64_t pol = l2_store_policy(p.store_policy);
   const int r0 = RPW * warp;
   auto stage = [&](int g) { return reinterpret_cast<const double*>(ring + (g % S) * STAGE_BYTES); };
   auto at = [&](const double* sp, int row, int col) { return sp[row * LD + col]; };
@@ -591,6 +592,13 @@ int launch_step(const double* in, double* out, int ni, int nj, int nk, int k_lo,
   p.k_hi = k_hi;
   p.kchunks = std::max(1, (k_hi - k_lo + v.kch - 1) / v.kch);
   p.units = p.tiles * p.kchunks;
+  // evict_normal: same-box A/B 348.5 -> 351.2 G against evict_first; evict_last
+  // (the 1 GB output cannot stay in L2) 343 G (LF_HEAT3D_STORE_POLICY)
+  static const int store_policy = [] {
+    const char* e = std::getenv("LF_HEAT3D_STORE_POLICY");
+    return e ? std::atoi(e) : 1;
+  }();
+  p.store_policy = store_policy;
   p.wrap_i = 1;
   p.wrap_j = 1;
   p.wrap_k = wrap_k ? 1 : 0;
@@ -643,6 +651,7 @@ int launch_pair_k(const double* in, double* out, int ni, int nj, int nk, cudaStr
   p.k_hi = nk;
   p.kchunks = std::max(1, (nk + K::KCH - 1) / K::KCH);
   p.units = p.tiles * p.kchunks;
+  p.store_policy = 0;
   p.wrap_i = p.wrap_j = p.wrap_k = 1;
   p.patch = std::getenv("LF_HEAT3D_NOPATCH") ? 0 : 1;  // timing experiments only (wrong at the faces)
   const int ctas = std::min(p.units, slots);
