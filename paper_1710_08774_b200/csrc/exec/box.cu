@@ -40,6 +40,8 @@ struct Params {
   int row_lo, row_hi;   // rows this launch computes
   long long out_pitch;  // ni
   int strips;
+  int load_policy;      // -1: plain TMA fetches, else l2_store_policy mode for the fetched lines
+  int store_policy;     // L2 policy of the output stores
 };
 
 struct Win {
@@ -171,6 +173,10 @@ __global__ void __launch_bounds__(32, K::OCC)
   RowRing<R, S> rr;
   // staged column 0 = logical i0 - 2 = storage i0; storage row = logical + 2
   rr.init(seg, nseg, H, smem, full, STAGE_BYTES, STAGE_TX, 0, H, SW);
+  if (p.load_policy >= 0) {
+    rr.load_hint = true;
+    rr.load_pol = l2_store_policy(p.load_policy);
+  }
   if (lane == 0) {
     for (int s = 0; s < S; ++s) mbar_init(&full[s], 1);
     fence_barrier_init();
@@ -179,7 +185,7 @@ __global__ void __launch_bounds__(32, K::OCC)
   }
   __syncwarp();
 
-  const uint64_t pol = l2_evict_first_policy();
+  const uint64_t pol = l2_store_policy(p.store_policy);
   // extra columns: lane 0 -> logical -2,-1 (staged 0,1); lane 31 -> SW, SW+1 (staged SW+2, SW+3)
   const int ex_col = lane == 0 ? LPAD - 2 : (lane == 31 ? LPAD + SW : LPAD + CPL * lane);
   int g = 0;
@@ -282,6 +288,19 @@ int run(const ExecArgs& a, std::string& err) {
   p.row_hi = rp.hi;
   p.out_pitch = ni;
   p.strips = ni / SW;
+  // L2 policies (same-box A/B, 16384^2): evict_normal-hinted fetches and
+  // stores 654 -> 662 G against plain fetches + evict_first stores; evict_first
+  // fetches 608 G
+  static const int load_policy = [] {
+    const char* e = std::getenv("LF_BOX_LOAD_POLICY");
+    return e ? std::atoi(e) : 1;
+  }();
+  static const int store_policy = [] {
+    const char* e = std::getenv("LF_BOX_STORE_POLICY");
+    return e ? std::atoi(e) : 1;
+  }();
+  p.load_policy = load_policy;
+  p.store_policy = store_policy;
   const int ctas = rowstream_ctas(slots, p.strips, rp.hi - rp.lo);
   if ((long long)ctas * 2 < p.strips) {
     err = "row range too short for the resident grid";

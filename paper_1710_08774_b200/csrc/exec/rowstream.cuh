@@ -91,6 +91,8 @@ struct RowRing {
     }
   }
   // lane 0 only: TMA for global stage g into slot g % S
+  bool load_hint = false;  // fetch with an L2 cache policy (load_pol)
+  uint64_t load_pol = 0;
   __device__ void issue(int g, const CUtensorMap* map) const {
     if (g >= total) return;
     int k = 0, gg = g;
@@ -98,8 +100,12 @@ struct RowRing {
     const int slot = g % S;
     fence_proxy_async();
     mbar_arrive_expect_tx(&full[slot], tx_bytes);
-    tma_load_2d(ring + slot * stage_bytes, map, &full[slot], col0 + seg[k].strip * strip_w,
-                row0 + seg[k].jb - H + gg * R);
+    if (load_hint)
+      tma_load_2d_hint(ring + slot * stage_bytes, map, &full[slot], col0 + seg[k].strip * strip_w,
+                       row0 + seg[k].jb - H + gg * R, load_pol);
+    else
+      tma_load_2d(ring + slot * stage_bytes, map, &full[slot], col0 + seg[k].strip * strip_w,
+                  row0 + seg[k].jb - H + gg * R);
   }
   __device__ void wait(int g) const { mbar_wait(&full[g % S], (g / S) & 1); }
   __device__ const unsigned char* stage(int g) const { return ring + (g % S) * stage_bytes; }
