@@ -84,7 +84,6 @@ def _hydro_slab(sizes, lo, hi, reduce_max):
 
 
 WORKLOADS = {
-    # BASELINE.json configs[1] -- the default bench line
     "heat3d": dict(config_index=1, spec="heat3d", sizes=(512, 512, 512), chain_steps=50,
                    gen=_heat3d_inputs, slab=_heat3d_slab, dtype="f64", halo=(1, 1, True)),
     "biharm": dict(config_index=0, spec="biharmonic2d", sizes=(4096, 4096), chain_steps=100,
@@ -93,6 +92,7 @@ WORKLOADS = {
                 gen=_box_inputs, slab=_box_slab, dtype="f32", halo=None),
     "hydro": dict(config_index=2, spec="hydro2d", sizes=(4096, 4096), chain_steps=20,
                   gen=_hydro_inputs, slab=_hydro_slab, dtype="f64", halo=(2, 2, False)),
+    # BASELINE.json configs[4] -- the default bench line (the metric's 1/2/4/8-GPU grid)
     "hydro_large": dict(config_index=4, spec="hydro2d", sizes=(32768, 32768), chain_steps=10,
                         gen=_hydro_inputs, slab=_hydro_slab, dtype="f64", halo=(2, 2, False)),
     # the same chains written with `body:` expressions: the generic NVRTC path
@@ -221,27 +221,39 @@ class ClockSampler:
 
 
 # --------------------------------------------------------------------- CPU legs
-def cpu_runner(name, w):
-    """The HFAV-style fused CPU schedule (oracle/) on one bounded unit of the
-    workload with all host threads: returns (run, cell-updates per run, text)."""
+# bounded CPU samples of each workload: (rows of the outer dimension kept, ...)
+# -- a full-width band for the 2D chains, a plane band for heat3d
+NAIVE_SAMPLE = {"heat3d": (32, 512, 512), "biharm": (512, 4096), "box": (1024, 16384), "hydro": (16, None)}
+
+
+def cpu_runner(name, w, naive=False):
+    """One bounded unit of the workload on the CPU: the HFAV-style fused CPU
+    schedule on all host threads (naive=False), or run_naive (R/SPEC.md:532-540,
+    every intermediate materialised, one thread).  Both from oracle/ built with
+    -march=native on this host.  Returns (run, cell-updates per run, threads, text)."""
     import oracle
-    name = name.replace("_jit", "").replace("_inplace", "")
-    threads = oracle.max_threads()
+    name = name.replace("_jit", "").replace("_inplace", "").replace("_large", "")
+    threads = 1 if naive else oracle.max_threads()
     sizes = w["sizes"]
+    if naive:
+        sizes = tuple(n if n is not None else sizes[-1] for n in NAIVE_SAMPLE.get(name, sizes))
+    what = "run_naive" if naive else "fused CPU schedule"
     if name == "heat3d":
         u = w["gen"](sizes)[0]
         o = np.empty_like(u)
-        return (lambda: oracle.heat3d_step(u, o, threads=threads)), int(np.prod(sizes)), threads, \
-            f"1 time step of {'x'.join(map(str, sizes))}"
+        run = (lambda: oracle.heat3d(u, 1, native=True)) if naive else \
+            (lambda: oracle.heat3d_step(u, o, threads=threads, native=True))
+        return run, int(np.prod(sizes)), threads, f"1 time step of {'x'.join(map(str, sizes))} ({what})"
     if name == "biharm":
         u = w["gen"](sizes)[0]
         o = np.zeros_like(u)
-        return (lambda: oracle.biharm_step(u, o, threads=threads)), int(np.prod(sizes)), threads, \
-            f"1 iteration of {'x'.join(map(str, sizes))}"
+        run = (lambda: oracle.biharm(u, 1, native=True)) if naive else \
+            (lambda: oracle.biharm_step(u, o, threads=threads, native=True))
+        return run, int(np.prod(sizes)), threads, f"1 iteration of {'x'.join(map(str, sizes))} ({what})"
     if name == "box":
         img = w["gen"](sizes)[0]
-        return (lambda: oracle.box(img, fused=True, threads=threads)), int(np.prod(sizes)), threads, \
-            f"1 pass of {'x'.join(map(str, sizes))}"
+        return (lambda: oracle.box(img, fused=not naive, threads=threads, native=True)), int(np.prod(sizes)), \
+            threads, f"1 pass of {'x'.join(map(str, sizes))} ({what})"
     if name == "normalization":
         # numpy restatement of run_naive for this chain on a 512-row band (single thread)
         q, z = w["gen"]((512, sizes[1]))
@@ -253,16 +265,19 @@ def cpu_runner(name, w):
                 acc = acc + fl[:, i]
             return fl / np.sqrt(acc)[:, None]
         return run, 512 * sizes[1], 1, f"a 512x{sizes[1]} row band (numpy run_naive)"
-    nj = max(16, min(sizes[0], 64))  # hydro: a full-width row band, 1 step
+    # hydro: a full-width row band, 1 step (x-sweep then y-sweep)
+    nj = sizes[0] if naive else max(16, min(sizes[0], 64))
     st = w["gen"]((nj, sizes[1]))
     outs = [np.empty_like(a) for a in st[:4]]
-    return (lambda: oracle.hydro_step(st[:4], outs, float(st[4][0]), threads=threads)), nj * sizes[1], \
-        threads, f"1 step of a {nj}x{sizes[1]} row band"
+    dtdx = float(st[4][0])
+    run = (lambda: oracle.hydro(st[:4], dtdx, 1, native=True)) if naive else \
+        (lambda: oracle.hydro_step(st[:4], outs, dtdx, threads=threads, native=True))
+    return run, nj * sizes[1], threads, f"1 step of a {nj}x{sizes[1]} row band ({what})"
 
 
-def cpu_sample(name, w, budget_s=10.0):
+def cpu_sample(name, w, budget_s=10.0, naive=False):
     """Repeat the CPU unit for ~budget_s; returns (cell-updates/s, threads, text)."""
-    run, cells, threads, unit = cpu_runner(name, w)
+    run, cells, threads, unit = cpu_runner(name, w, naive=naive)
     run()  # warm
     t0 = time.perf_counter()
     reps = 0
@@ -272,7 +287,19 @@ def cpu_sample(name, w, budget_s=10.0):
         if time.perf_counter() - t0 >= budget_s:
             break
     dt = time.perf_counter() - t0
-    return cells * reps / dt, threads, f"{reps} x {unit} (fused CPU schedule, {threads} threads, {dt:.1f} s)"
+    return cells * reps / dt, threads, f"{reps} x {unit}, {threads} thread(s), {dt:.1f} s"
+
+
+def host_cpu():
+    """CPU model, physical cores, logical CPUs usable, OMP_NUM_THREADS."""
+    try:
+        import psutil
+        phys = psutil.cpu_count(logical=False)
+    except Exception:
+        phys = None
+    return {"cpu": cpu_model(), "physical_cores": phys, "logical_cpus": len(os.sched_getaffinity(0)),
+            "omp_num_threads": os.environ.get("OMP_NUM_THREADS"),
+            "build": "gcc -O3 -march=native -ffp-contract=off -fopenmp (oracle/, built on this host)"}
 
 
 def cpu_model():
@@ -285,6 +312,56 @@ def cpu_model():
     return "unknown"
 
 
+
+# small grid and step count of the N-GPU self-check (dim 0 divisible by 1, 2, 4, 8)
+PARITY_2D, PARITY_3D = ((512, 512), 3), ((64, 64, 64), 3)
+
+
+def slab_parity(w, lf, comm, rank, world, dev, stream):
+    """GPU(N) == GPU(1) on a small grid: every rank runs its slab through
+    lf_run_slabs (the same NCCL exchange as the timed run), the interior rows
+    are gathered to rank 0 and compared bit for bit with a whole-domain lf_run
+    of the same input (ghost columns included).  Returns True/False on rank 0,
+    None where the chain has no exchange."""
+    import torch
+    import torch.distributed as dist
+    from paper_1710_08774_b200 import slabs
+    if w["halo"] is None:
+        return None
+    sizes, steps = PARITY_3D if len(w["sizes"]) == 3 else PARITY_2D
+    plan = lf.Plan.with_ranges(w["spec"], sizes)
+    n0 = sizes[0]
+    lo, hi = slabs.slab_range(n0, rank, world)
+
+    def reduce_max(x):
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+    local = w["slab"](sizes, lo, hi, reduce_max)
+    d_ax = [torch.from_numpy(np.ascontiguousarray(h)).to(dev) for h in local]
+    d_goal = []
+    for t in plan.goals:
+        ext = list(t.extent)
+        ext[0] = ext[0] - n0 + (hi - lo)
+        d_goal.append(torch.full(ext, float("nan"), dtype=getattr(torch, str(t.dtype)), device=dev))
+    plan.run_slabs(d_ax + d_goal, comm, steps=steps, stream=stream)
+    torch.cuda.synchronize()
+    g0 = [-t.base[0] for t in plan.goals]  # ghost rows before the slab's first row
+    mine = torch.stack([g[o:o + (hi - lo)] for g, o in zip(d_goal, g0)])
+    parts = [torch.empty_like(mine) for _ in range(world)]
+    dist.all_gather(parts, mine)
+    if rank != 0:
+        return None
+    whole_in = w["gen"](sizes)
+    ax = [torch.from_numpy(np.ascontiguousarray(h)).to(dev) for h in whole_in[:len(plan.axioms)]]
+    goals = [torch.full(t.extent, float("nan"), dtype=getattr(torch, str(t.dtype)), device=dev) for t in plan.goals]
+    plan.run(ax + goals, steps=steps, stream=stream)
+    torch.cuda.synchronize()
+    ref = torch.stack([g[o:o + n0] for g, o in zip(goals, g0)])
+    got = torch.cat(parts, dim=1)
+    return bool(torch.equal(got.view(torch.int64) if got.dtype == torch.float64 else got.view(torch.int32),
+                            ref.view(torch.int64) if ref.dtype == torch.float64 else ref.view(torch.int32)))
+
 # --------------------------------------------------------------------- main
 def main():
     ap = argparse.ArgumentParser()
@@ -292,7 +369,8 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="loomfuse", choices=["loomfuse", "reference"])
-    ap.add_argument("--config", default="heat3d", choices=sorted(WORKLOADS))
+    ap.add_argument("--config", default="hydro_large", choices=sorted(WORKLOADS),
+                    help="default: BASELINE configs[4], the grid the metric is quoted on (1/2/4/8 GPUs)")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-e2e", action="store_true", help="skip the end-to-end leg")
     ap.add_argument("--cpu-budget", type=float, default=10.0)
@@ -312,6 +390,10 @@ def main():
     origin = f"BASELINE configs[{w['config_index']}]" if w["config_index"] is not None else "extra (not a BASELINE config)"
     workload = f"{origin} {w['spec']} " + "x".join(map(str, w["sizes"])) + \
         f", {w['chain_steps']} steps"
+    slab_mode = world > 1 or args.force_slabs
+    # one config dict for both arms (--impl loomfuse / reference): same keys, same values
+    config = {"workload": workload, "l2": "inputs larger than L2 (126 MB)", "in_place": bool(w.get("inplace")),
+              "parallelism": f"slab{world}" if slab_mode else "single-gpu"}
 
     if args.impl == "reference":
         if rank != 0:
@@ -324,16 +406,17 @@ def main():
             run()
         dt = (time.perf_counter() - t0) / args.steps
         value = unit_cells / dt
-        sample = f"{args.steps} x {unit} (fused CPU schedule, {threads} threads)"
+        sample = f"{args.steps} x {unit}, {threads} threads"
         line = {
             "impl": "reference", "metric": metric, "value": value, "unit": "cell-updates/s",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": dt * 1e3,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": w["dtype"], "data": "synthetic (seeded splitmix64, BASELINE.json shapes)",
-            "config": {"workload": workload, "cpu": cpu_model(), "threads": threads},
+            "config": config, "executor": "HFAV fused CPU schedule (oracle/ port; the reference's executor is "
+                                          "absent from the snapshot)",
             "cpu_baseline": {"value": value, "unit": "cell-updates/s", "cores": threads, "kind": "port",
-                             "sample": sample},
+                             "sample": sample, **host_cpu()},
             "e2e": {"value": value, "unit": "cell-updates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         }
         print(json.dumps(line), flush=True)
@@ -343,7 +426,6 @@ def main():
     import paper_1710_08774_b200 as lf
     from paper_1710_08774_b200 import slabs
 
-    slab_mode = world > 1 or args.force_slabs
     # stdout carries exactly one JSON line: everything native code prints while
     # we run (the NCCL version banner of the first communicator, ...) goes to
     # stderr; the saved descriptor is restored for the final print
@@ -430,6 +512,11 @@ def main():
                 # face rows first, their NCCL exchange overlapped with the interior rows
                 slabs.run_slabs_overlapped(launch, cur, nxt, w["chain_steps"], halo, rank, world, hi - lo,
                                            comm_stream=comm)
+    parity = None
+    if slab_mode and w["halo"] is not None:
+        # N-GPU self-check before timing (printed as "slab_parity")
+        pcomm = comm if args.slab_exchange == "native" else lf.NcclComm.from_group(rank, world)
+        parity = slab_parity(w, lf, pcomm, rank, world, dev, stream)
     # one pass over the grid per step, except where the executor fuses time
     # steps (heat3d: two-step passes on a whole domain); slabs step singly
     passes = plan.grid_passes(w["chain_steps"]) if not slab_mode else w["chain_steps"]
@@ -494,13 +581,12 @@ def main():
         "metric": metric, "value": value, "unit": "cell-updates/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": w["dtype"], "data": "synthetic (seeded splitmix64, BASELINE.json shapes)",
-        "config": {"workload": workload, "executor": plan.executor, "l2": "inputs larger than L2 (126 MB)",
-                   "in_place": bool(w.get("inplace")),
-                   "parallelism": f"slab{world}" if slab_mode else "single-gpu",
-                   **({"halo_exchange": args.slab_exchange if w["halo"] is not None else "none"}
-                      if slab_mode else {})},
+        "config": config, "executor": plan.executor,
+        **({"halo_exchange": args.slab_exchange if w["halo"] is not None else "none"} if slab_mode else {}),
         "roofline": roofline, "gpu_launches": launches * args.steps, "clocks": clk.summary(),
     }
+    if slab_mode:
+        line["slab_parity"] = parity
 
     # ---------------- end-to-end through the host-buffer ABI call ----------------
     e2e_bytes = sum(t.bytes for t in plan.terminals)
@@ -516,21 +602,60 @@ def main():
         else:
             outs = [torch.empty(t.extent, dtype=tdt(t)).pin_memory() for t in plan.goals]
         hb = [p.numpy() for p in pinned] + [o.numpy() for o in outs]
-        for _ in range(max(1, args.warmup)):
+        # a step moves every terminal over PCIe: bound the repetitions on the big grids
+        e2e_steps, e2e_warm = (min(args.steps, 3), 1) if e2e_bytes > 10e9 else (args.steps, max(1, args.warmup))
+        for _ in range(e2e_warm):
             plan.run_host(hb, steps=w["chain_steps"])
         t0 = time.perf_counter()
-        for _ in range(args.steps):
+        for _ in range(e2e_steps):
             plan.run_host(hb, steps=w["chain_steps"])
-        e2e_s = (time.perf_counter() - t0) / args.steps
+        e2e_s = (time.perf_counter() - t0) / e2e_steps
         line["e2e"] = {"value": cells * w["chain_steps"] / e2e_s, "unit": "cell-updates/s",
                        "h2d_bytes_per_step": int(sum(t.bytes for t in plan.axioms)),
                        "d2h_bytes_per_step": int(sum(t.bytes for t in plan.goals)),
-                       "ms_per_step": e2e_s * 1e3, "api": "lf_run_host"}
+                       "ms_per_step": e2e_s * 1e3, "steps": e2e_steps, "warmup": e2e_warm,
+                       "api": "lf_run_host (pinned host buffers; H2D, every chain step, D2H inside the timed call)"}
+    elif not args.no_e2e and slab_mode and w["halo"] is not None and args.slab_exchange == "native":
+        # N GPUs end to end: every rank copies its slab's axioms up from pinned
+        # host memory, runs lf_run_slabs, copies its goals back; max over ranks
+        h_ax = [t.cpu().pin_memory() for t in d_ax]
+        h_goal = [torch.empty(t.shape, dtype=t.dtype).pin_memory() for t in d_goal]
+
+        def e2e_step():
+            for hsrc, dst in zip(h_ax, d_ax):
+                dst.copy_(hsrc, non_blocking=True)
+            plan.run_slabs(d_ax + d_goal, comm, steps=w["chain_steps"], stream=stream)
+            for src, hdst in zip(d_goal, h_goal):
+                hdst.copy_(src, non_blocking=True)
+            torch.cuda.synchronize()
+        e2e_steps = min(args.steps, 3)
+        e2e_step()
+        barrier()
+        t0 = time.perf_counter()
+        for _ in range(e2e_steps):
+            e2e_step()
+        barrier()
+        e2e_s = torch.tensor([(time.perf_counter() - t0) / e2e_steps], dtype=torch.float64, device=dev)
+        torch.distributed.all_reduce(e2e_s, op=torch.distributed.ReduceOp.MAX)
+        e2e_s = float(e2e_s.item())
+        h2d = torch.tensor([sum(t.numel() * t.element_size() for t in h_ax)], dtype=torch.float64, device=dev)
+        d2h = torch.tensor([sum(t.numel() * t.element_size() for t in h_goal)], dtype=torch.float64, device=dev)
+        torch.distributed.all_reduce(h2d)
+        torch.distributed.all_reduce(d2h)
+        line["e2e"] = {"value": cells * w["chain_steps"] / e2e_s, "unit": "cell-updates/s",
+                       "h2d_bytes_per_step": int(h2d.item()), "d2h_bytes_per_step": int(d2h.item()),
+                       "ms_per_step": e2e_s * 1e3, "steps": e2e_steps, "warmup": 1,
+                       "api": "per rank: pinned H2D of the slab, lf_run_slabs (NCCL halo exchange), D2H; "
+                              "max over ranks"}
     # ---------------- CPU baseline (rank 0, N=1 only) ----------------
     if rank == 0 and world == 1 and not args.no_cpu:
         rate, threads, sample = cpu_sample(args.config, w, budget_s=args.cpu_budget)
         line["cpu_baseline"] = {"value": rate, "unit": "cell-updates/s", "cores": threads, "kind": "port",
-                                "sample": sample, "cpu": cpu_model()}
+                                "sample": sample, **host_cpu()}
+        if args.config != "normalization_jit":
+            nrate, nthreads, nsample = cpu_sample(args.config, w, budget_s=args.cpu_budget / 2, naive=True)
+            line["cpu_baseline"]["run_naive"] = {"value": nrate, "unit": "cell-updates/s", "cores": nthreads,
+                                                 "sample": nsample}
     sys.stdout.flush()
     os.dup2(json_fd, 1)
     if rank == 0:

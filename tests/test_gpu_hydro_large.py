@@ -1,0 +1,86 @@
+"""BASELINE configs[4] at its own size: Hydro2D on the 32768 x 32768 grid (34 GB
+of state) on one GPU, 2 steps, bit-exact against the CPU oracle (SURVEY.md
+8(d): "CPU oracle == GPU on <= 2 steps").
+
+The oracle cannot hold the grid three times over in host memory, so it checks
+full-width row bands: the band's rows plus 2 rows per step on each side (a
+step's dependency cone along j) come from the same seeded initial state, the
+fused CPU schedule advances that strip, and the rows of the band -- ghost
+columns included, and the reflective ghost rows at the two global faces --
+must equal the GPU's bit for bit.  Rows further than 2*(steps-1) from the
+strip's cut edges never see the strip's own (mirrored) ghost rows, so they are
+exact.  Size-independent properties cover the whole grid: mass and energy are
+conserved by the reflective walls, density and pressure stay positive."""
+import numpy as np
+import pytest
+
+import oracle
+import paper_1710_08774_b200 as lf
+from paper_1710_08774_b200 import inputs
+
+pytestmark = pytest.mark.gpu
+
+N = 32768
+STEPS = 2
+CHUNK = 2048
+
+
+def bits(a):
+    return np.ascontiguousarray(a).view(np.uint64)
+
+
+@pytest.fixture(scope="module")
+def large_run():
+    import torch
+    free, _ = torch.cuda.mem_get_info()
+    need = 3 * 4 * (N + 4) ** 2 * 8  # axioms + goals + the plan's ping-pong scratch
+    if free < need * 1.05:
+        pytest.skip(f"needs {need / 1e9:.0f} GB of device memory, {free / 1e9:.0f} GB free")
+    # the initial state, generated band by band straight into device memory
+    ax = [torch.empty((N + 4, N + 4), dtype=torch.float64, device="cuda") for _ in range(4)]
+    smax = 0.0
+    for r0 in range(-2, N + 2, CHUNK):
+        r1 = min(N + 2, r0 + CHUNK)
+        rows, m = inputs.hydro_rows(N, N, r0, r1)
+        smax = max(smax, m)
+        for a, h in zip(ax, rows):
+            a[r0 + 2:r1 + 2].copy_(torch.from_numpy(h))
+    dtdx = 0.5 / smax
+    mass0 = [float(ax[v][2:-2, 2:-2].sum()) for v in (0, 3)]
+    plan = lf.Plan.with_ranges("hydro2d", (N, N))
+    assert plan.executor == "hydro2d_fused_tma"
+    goals = [torch.full_like(ax[0], float("nan")) for _ in range(4)]
+    plan.run(ax + [torch.tensor([dtdx], dtype=torch.float64, device="cuda")] + goals, steps=STEPS)
+    torch.cuda.synchronize()
+    del ax
+    torch.cuda.empty_cache()
+    return goals, dtdx, mass0
+
+
+@pytest.mark.parametrize("band", [(0, 40), (N // 2 - 24, N // 2 + 24), (12345, 12371), (N - 40, N)])
+def test_row_bands_match_the_cpu_oracle(large_run, band):
+    goals, dtdx, _ = large_run
+    a, b = band
+    A, B = max(0, a - 2 * STEPS), min(N, b + 2 * STEPS)
+    strip, _ = inputs.hydro_rows(N, N, A - 2, B + 2)
+    ref = oracle.hydro(strip, dtdx, STEPS, fused=True)
+    # storage rows to compare: the band, plus the ghost rows at a global face
+    lo = a + 2 - (2 if a == 0 else 0)
+    hi = b + 2 + (2 if b == N else 0)
+    for v in range(4):
+        got = goals[v][lo:hi].cpu().numpy()
+        want = ref[v][lo - A:hi - A]
+        assert np.array_equal(bits(got), bits(want)), (v, band, int(np.count_nonzero(got != want)))
+
+
+def test_whole_grid_conserves_and_stays_physical(large_run):
+    import torch
+    goals, _, mass0 = large_run
+    for v, m0 in zip((0, 3), mass0):
+        assert float(goals[v][2:-2, 2:-2].sum()) == pytest.approx(m0, rel=1e-12)
+    assert not any(bool(torch.isnan(g).any()) for g in goals), "a cell was never written"
+    assert float(goals[0][2:-2, 2:-2].min()) > 0.0
+    # total energy above kinetic energy: positive pressure everywhere
+    for r in range(2, N + 2, CHUNK):
+        rho, mx, my, e = (g[r:r + CHUNK, 2:-2] for g in goals)
+        assert float((e - 0.5 * (mx * mx + my * my) / rho).min()) > 0.0

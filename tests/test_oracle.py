@@ -89,3 +89,22 @@ def test_fault_injection_wrong_window_is_detected():
     shifted = np.roll(u, 1, axis=0)
     bad = oracle.biharm(shifted, 1)
     assert not bits_equal(good, bad)
+
+
+@pytest.mark.parametrize("band", [(0, 10), (50, 70), (97, 128)])
+def test_hydro_row_band_cone_equals_the_whole_grid(band):
+    """The band check of tests/test_gpu_hydro_large.py: a strip of the band's
+    rows plus 2 rows per step each side, cut from the initial state, advanced
+    by the fused CPU schedule, reproduces the whole-grid run on the band's rows
+    (ghost rows at the global faces included) bit for bit."""
+    n, steps = 128, 2
+    st, dtdx = inputs.hydro_input(n, 96, seed=5)
+    whole = oracle.hydro(st, dtdx, steps, fused=True)
+    a, b = band
+    A, B = max(0, a - 2 * steps), min(n, b + 2 * steps)
+    strip = [np.ascontiguousarray(x[A:B + 4]) for x in st]
+    ref = oracle.hydro(strip, dtdx, steps, fused=True)
+    lo = a + 2 - (2 if a == 0 else 0)
+    hi = b + 2 + (2 if b == n else 0)
+    for v in range(4):
+        assert np.array_equal(whole[v][lo:hi].view(np.uint64), ref[v][lo - A:hi - A].view(np.uint64))
