@@ -6,7 +6,7 @@
 // sweep and cell one constoprim, slope, trace, Riemann solve (one face per
 // cell), flux and update -- the composition oracle/hydro.c uses
 // (hydro.c:77-101 x-sweep, 108-133 y-sweep).  Every + - * / and sqrt counts
-// as one flop (the usual convention; fabs, min/max selects, negation and
+// as one flop and fma as two (the usual convention; fabs, min/max selects, negation and
 // comparisons are not flops).  The counts are averaged over seeded states
 // spanning the workload's range (shocks and rarefactions, both Riemann
 // sampling branches).  bench.py uses the printed per-cell-step figure as the
@@ -38,6 +38,8 @@ static inline bool operator<=(Fd a, Fd b) { ++g.cmp; return a.v <= b.v; }
 static inline bool operator>=(Fd a, Fd b) { ++g.cmp; return a.v >= b.v; }
 static inline bool operator==(Fd a, Fd b) { ++g.cmp; return a.v == b.v; }
 static inline Fd sqrt(Fd a) { ++g.sqrt; return Fd(std::sqrt(a.v)); }
+// a fused multiply-add is a multiplication and an addition (two flops)
+static inline Fd fma(Fd a, Fd b, Fd c) { ++g.mul; ++g.add; return Fd(std::fma(a.v, b.v, c.v)); }
 static inline Fd fabs(Fd a) { return Fd(std::fabs(a.v)); }
 
 #define double Fd

@@ -166,6 +166,44 @@ def _fill(a, modes, n, base):
                 a[tuple(dst)] = -a[tuple(src)] if m == "odd" else a[tuple(src)]
 
 
+_DECL = re.compile(r"^\s*\w[\w\s\*&]*?\b(\w+)\s*\((.*)\)\s*$")
+
+
+def call_named(kernel, ins):
+    """Outputs of a kernel given by its `declaration:` only: the user-kernel
+    function of userkernels/*.h (oracle/kernels_ffi.c) applied element by
+    element to the broadcast inputs, parameters passed in declaration order."""
+    import ctypes
+    from . import lib
+    m = _DECL.match(kernel["declaration"])
+    if not m:
+        raise ValueError(f"cannot read declaration {kernel['declaration']!r}")
+    fn = getattr(lib(), "lfk_" + m.group(1), None)
+    if fn is None:
+        raise KeyError(f"no element-wise wrapper for user kernel {m.group(1)!r} (oracle/kernels_ffi.c)")
+    params = []
+    for piece in m.group(2).split(","):
+        words = re.findall(r"\w+", piece)
+        params.append((words[-1], np.float32 if "float" in words[:-1] else np.float64))
+    arrays = np.broadcast_arrays(*[np.asarray(v) for v in ins])
+    shape = arrays[0].shape if arrays else ()
+    by_name = dict(zip(kernel["inputs"], arrays))
+    outs = {o: None for o in kernel["outputs"]}
+    args = []
+    for name, dt in params:
+        if name in by_name:
+            a = np.ascontiguousarray(by_name[name], dtype=dt)
+            by_name[name] = a
+        else:
+            a = outs[name] = np.empty(shape, dtype=dt)
+        args.append(a)
+    ptrs = (ctypes.c_void_p * len(args))(*[a.ctypes.data for a in args])
+    fn.argtypes = [ctypes.c_long, ctypes.POINTER(ctypes.c_void_p)]
+    if fn(int(np.prod(shape, dtype=np.int64)), ptrs) != 0:
+        raise RuntimeError(f"lfk_{m.group(1)} failed")
+    return [outs[o] for o in kernel["outputs"]]
+
+
 def _term_axes(term, nd):
     """loop dims a term spans (others are broadcast axes of length 1)"""
     return {dim for dim, _ in term["dims"]}
@@ -254,6 +292,11 @@ def run_naive(spec_path, axioms: dict, steps: int = 1) -> dict:
                             env[pname] = v[tuple(ix)] if v.ndim == nd else v
                         acc = np.asarray(eval_body(bodies[rap["kernel"]][o_name], env, dt), dtype=dt)
                     vals[rap["out"][0]] = acc
+                    continue
+                if not bodies[rap["kernel"]]:
+                    # a named kernel: the shipped user-kernel function itself, element-wise
+                    for t, v in zip(rap["out"], call_named(k, ins)):
+                        vals[t] = v
                     continue
                 env = dict(zip(k["inputs"], ins))
                 for o, t in zip(k["outputs"], rap["out"]):

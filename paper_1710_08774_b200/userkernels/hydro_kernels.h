@@ -13,9 +13,19 @@
  * (rho, rho*u, rho*v, E) and the y-sweep (rho, rho*v, rho*u, E).
  *
  * As with stencil_kernels.h, the same source runs in the CPU oracle and is
- * inlined into the sm_100a executor.  Only + - * / sqrt fabs and comparisons
- * are used (all correctly rounded on both sides), fixed iteration counts, no
- * early exits -- so the two schedules agree bit for bit.
+ * inlined into the sm_100a executor.  Only + - * / sqrt fma fabs and
+ * comparisons are used -- each correctly rounded on both sides, fma() being
+ * the single-rounding fused multiply-add of C99 / IEEE 754-2008 -- with fixed
+ * iteration counts and no early exits, so the two schedules agree bit for bit.
+ * The expressions are written in fused multiply-add form where a product
+ * feeds a sum (as an optimising compiler would contract them), and every
+ * quantity the solver needs more than once is formed once:
+ *   * the Lagrangian wave speed of a shock, W = C sqrt(1 + k (p* - p)/p), is
+ *     carried as W^2 = gamma rho (p + k (p* - p)) -- one fma per Newton step
+ *     and no division by p (gamma k = (gamma+1)/2);
+ *   * the Newton step z_l z_r / (z_l + z_r) (u*_l - u*_r), z = 2W^3/(W^2+C^2),
+ *     is written over one common denominator (2 sqrt + 1 division per step);
+ *   * the star density rho W^2 / (W^2 + rho (p - p*)) is one division.
  */
 #ifndef LF_USERKERNELS_HYDRO_H
 #define LF_USERKERNELS_HYDRO_H
@@ -44,7 +54,7 @@
 #define HY_SQRT(x) sqrt(x)
 #endif
 
-#if defined(__CUDACC__)
+#if defined(__CUDACC__) || defined(__CUDACC_RTC__)
 #define LF_HD __host__ __device__ __forceinline__
 #else
 #include <math.h>
@@ -52,12 +62,16 @@
 #endif
 
 #define HY_GAMMA 1.4
+#define HY_GM1 0.4         /* gamma - 1 */
+#define HY_GOGM1 3.5       /* gamma / (gamma - 1) */
+#define HY_GK 1.2          /* gamma k = gamma (gamma+1)/(2 gamma) = (gamma+1)/2 */
 #define HY_SMALLR 1e-10
 #define HY_SMALLP 1e-12
 #define HY_SMALLC 1e-10
 #define HY_NITER 10
 
 LF_HD double hy_max(double a, double b) { return a > b ? a : b; }
+LF_HD double hy_min(double a, double b) { return a < b ? a : b; }
 /* a / b for a denominator that is finite and nonzero (every division of this
  * chain): a zero numerator returns a * b, which is the same signed zero as the
  * quotient.  Keeps the exactly-zero differences of states at rest (velocities,
@@ -73,20 +87,18 @@ LF_HD double hy_div(double a, double b HY_BAD_PARAM) {
   return a / b;
 #endif
 }
-LF_HD double hy_min(double a, double b) { return a < b ? a : b; }
 
-/* conservative -> primitive (density, normal & transverse velocity, pressure) */
+/* conservative -> primitive (density, normal & transverse velocity, pressure):
+ * p = (gamma-1) (e - |m|^2 / (2 rho)) */
 LF_HD void hy_constoprim(double r, double mn, double mt, double e, double* qr, double* qn, double* qt,
                          double* qp HY_BAD_PARAM) {
   const double rr = hy_max(r, HY_SMALLR);
   const double inv = HY_QUOT(1.0, rr);
-  const double un = mn * inv;
-  const double ut = mt * inv;
-  const double ek = 0.5 * rr * (un * un + ut * ut);
+  const double m2 = fma(mn, mn, mt * mt);
   *qr = rr;
-  *qn = un;
-  *qt = ut;
-  *qp = hy_max((HY_GAMMA - 1.0) * (e - ek), HY_SMALLP);
+  *qn = mn * inv;
+  *qt = mt * inv;
+  *qp = hy_max(HY_GM1 * fma(-0.5 * inv, m2, e), HY_SMALLP);
 }
 
 /* minmod-limited slope from the left and right differences */
@@ -105,97 +117,109 @@ LF_HD void hy_slope(double rm, double nm, double tm, double pm, double r0, doubl
 
 /* MUSCL-Hancock predictor: evolve the cell's primitive state by half a time
  * step with the primitive Euler equations, then extrapolate to the left
- * (minus) and right (plus) faces. */
+ * (minus) and right (plus) faces: q -/+ dq/2 + dt/2 A(q) dq/dx. */
 LF_HD void hy_trace(double r, double n, double t, double p, double dr, double dn, double dt, double dp,
                     double dtdx, double* mr, double* mn, double* mt, double* mp, double* pr, double* pn,
                     double* pt, double* pp HY_BAD_PARAM) {
   const double h = -0.5 * dtdx;
-  const double sr = h * (n * dr + r * dn);
-  const double sn = h * (n * dn + hy_div(dp, r HY_BAD_ARG));
+  const double sr = h * fma(n, dr, r * dn);
+  const double sn = h * fma(n, dn, hy_div(dp, r HY_BAD_ARG));
   const double st = h * (n * dt);
-  const double sp = h * (n * dp + HY_GAMMA * p * dn);
-  *mr = hy_max(r - 0.5 * dr + sr, HY_SMALLR);
-  *mn = n - 0.5 * dn + sn;
-  *mt = t - 0.5 * dt + st;
-  *mp = hy_max(p - 0.5 * dp + sp, HY_SMALLP);
-  *pr = hy_max(r + 0.5 * dr + sr, HY_SMALLR);
-  *pn = n + 0.5 * dn + sn;
-  *pt = t + 0.5 * dt + st;
-  *pp = hy_max(p + 0.5 * dp + sp, HY_SMALLP);
+  const double sp = h * fma(n, dp, (HY_GAMMA * p) * dn);
+  *mr = hy_max(fma(-0.5, dr, r) + sr, HY_SMALLR);
+  *mn = fma(-0.5, dn, n) + sn;
+  *mt = fma(-0.5, dt, t) + st;
+  *mp = hy_max(fma(-0.5, dp, p) + sp, HY_SMALLP);
+  *pr = hy_max(fma(0.5, dr, r) + sr, HY_SMALLR);
+  *pn = fma(0.5, dn, n) + sn;
+  *pt = fma(0.5, dt, t) + st;
+  *pp = hy_max(fma(0.5, dp, p) + sp, HY_SMALLP);
 }
 
 /* Godunov state at a face from left/right primitive states: two-shock
- * approximation of the exact Riemann problem, p* by HY_NITER Newton steps on
- * the Lagrangian wave speeds w = c*sqrt(1 + k (p*-p)/p), then sampling at
- * x/t = 0 with a linear fan.  z = 2w^3/(w^2+c^2) enters only through
- * z_l z_r / (z_l + z_r) = 1 / (1/z_l + 1/z_r), and the step is written over
- * one common denominator, so a Newton step costs 2 sqrt + 1 division.
+ * approximation of the exact Riemann problem, p* by HY_NITER Newton steps,
+ * then sampling at x/t = 0 with a linear fan.
+ *
+ * With W^2 = A(p*) = gamma rho (p + k (p* - p)) = C^2 + gamma k rho (p* - p),
+ * C^2 = gamma p rho, the step p* += z_l z_r / (z_l + z_r) (u*_l - u*_r),
+ * u*_l - u*_r = (nl - nr) - (p*-pl)/W_l - (p*-pr)/W_r and
+ * z = 2 W^3 / (W^2 + C^2), is over one common denominator
+ *   A_l A_r [ (nl-nr) W_l W_r - (p*-pl) W_r - (p*-pr) W_l ]
+ *   ----------------------------------------------------------------
+ *   (A_l + C_l^2)/2 W_r A_r + (A_r + C_r^2)/2 W_l A_l
  *
  * The solver is split into init / newton / sample so an executor can advance
  * two independent problems in one loop (hy_riemann is exactly
  * init + HY_NITER x newton + sample, so results are identical). */
 typedef struct {
-  double nl, pl, nr, pr;       /* normal velocities and pressures */
-  double cl, cr, cl2, cr2;     /* Lagrangian sound speeds rho*c and squares */
-  double kpl, kpr;             /* (gamma+1)/(2 gamma) / p */
+  double nl, pl, nr, pr; /* normal velocities and pressures */
+  double dn;             /* nl - nr */
+  double cl2, cr2;       /* C^2 = gamma p rho (Lagrangian sound speed squared) */
+  double gkl, gkr;       /* gamma k rho: dA/dp* */
+  double hcl2, hcr2;     /* C^2 / 2 */
 } hy_rp;
 
 LF_HD double hy_riemann_init(double rl, double nl, double pl, double rr, double nr, double pr, hy_rp* c HY_BAD_PARAM) {
-  const double k = (HY_GAMMA + 1.0) / (2.0 * HY_GAMMA);
   c->nl = nl;
   c->pl = pl;
   c->nr = nr;
   c->pr = pr;
-  c->cl = HY_SQRT(HY_GAMMA * pl * rl);
-  c->cr = HY_SQRT(HY_GAMMA * pr * rr);
-  c->cl2 = c->cl * c->cl;
-  c->cr2 = c->cr * c->cr;
-  c->kpl = HY_QUOT(k, pl);
-  c->kpr = HY_QUOT(k, pr);
-  return hy_max(HY_QUOT(c->cr * pl + c->cl * pr + c->cl * c->cr * (nl - nr), c->cl + c->cr), HY_SMALLP);
+  c->dn = nl - nr;
+  c->cl2 = (HY_GAMMA * pl) * rl;
+  c->cr2 = (HY_GAMMA * pr) * rr;
+  c->gkl = HY_GK * rl;
+  c->gkr = HY_GK * rr;
+  c->hcl2 = 0.5 * c->cl2;
+  c->hcr2 = 0.5 * c->cr2;
+  /* acoustic (linearised) first guess */
+  const double cl = HY_SQRT(c->cl2);
+  const double cr = HY_SQRT(c->cr2);
+  return hy_max(HY_QUOT(fma(cr, pl, cl * pr) + (cl * cr) * c->dn, cl + cr), HY_SMALLP);
 }
 
 LF_HD double hy_riemann_newton(const hy_rp* c, double ps HY_BAD_PARAM) {
-  const double wl = c->cl * HY_SQRT(1.0 + c->kpl * (ps - c->pl));
-  const double wr = c->cr * HY_SQRT(1.0 + c->kpr * (ps - c->pr));
-  /* (u*_l - u*_r) / (1/z_l + 1/z_r) over one common denominator:
-   *   u*_l - u*_r = ((nl - nr) wl wr - (ps - pl) wr - (ps - pr) wl) / (wl wr)
-   *   1/z_l + 1/z_r = ((wl^2 + cl^2) wr^3 + (wr^2 + cr^2) wl^3) / (2 wl^3 wr^3)
-   * so a Newton step costs 2 sqrt + 1 division. */
-  const double wl2 = wl * wl, wr2 = wr * wr;
-  const double num = 2.0 * wl2 * wr2 * ((c->nl - c->nr) * wl * wr - (ps - c->pl) * wr - (ps - c->pr) * wl);
-  const double den = (wl2 + c->cl2) * (wr2 * wr) + (wr2 + c->cr2) * (wl2 * wl);
+  const double dl = ps - c->pl, dr = ps - c->pr;
+  const double al = fma(c->gkl, dl, c->cl2);
+  const double ar = fma(c->gkr, dr, c->cr2);
+  const double wl = HY_SQRT(al);
+  const double wr = HY_SQRT(ar);
+  const double inner = fma(fma(c->dn, wl, -dl), wr, -(dr * wl));
+  const double num = (al * ar) * inner;
+  const double den = fma(fma(0.5, al, c->hcl2), wr * ar, fma(0.5, ar, c->hcr2) * (wl * al));
   return hy_max(ps + hy_div(num, den HY_BAD_ARG), HY_SMALLP);
 }
 
 LF_HD void hy_riemann_sample(const hy_rp* c, double ps, double rl, double tl, double rr, double tr, double* gr,
                              double* gn, double* gt, double* gp HY_BAD_PARAM) {
-  const double wl = c->cl * HY_SQRT(1.0 + c->kpl * (ps - c->pl));
-  const double wr = c->cr * HY_SQRT(1.0 + c->kpr * (ps - c->pr));
-  const double us = hy_div(wl * c->nl + wr * c->nr + c->pl - c->pr, wl + wr HY_BAD_ARG);
+  const double al = fma(c->gkl, ps - c->pl, c->cl2);
+  const double ar = fma(c->gkr, ps - c->pr, c->cr2);
+  const double wl = HY_SQRT(al);
+  const double wr = HY_SQRT(ar);
+  const double us = hy_div(fma(wl, c->nl, wr * c->nr) + (c->pl - c->pr), wl + wr HY_BAD_ARG);
   const int left = us > 0.0;
   const double ro = left ? rl : rr;
   const double uo = left ? c->nl : -c->nr; /* velocity along the sampled wave direction */
   const double po = left ? c->pl : c->pr;
   const double wo = left ? wl : wr;
+  const double ao = left ? al : ar;        /* W^2 of the sampled wave */
   const double to = left ? tl : tr;
   const double uss = left ? us : -us;
   const double iro = HY_QUOT(1.0, ro);
-  const double co = HY_SQRT(HY_GAMMA * po * iro);
-  const double rstar = hy_max(HY_QUOT(ro, 1.0 + hy_div(ro * (po - ps), wo * wo HY_BAD_ARG)), HY_SMALLR);
+  const double co = HY_SQRT((HY_GAMMA * po) * iro);
+  const double rstar = hy_max(HY_QUOT(ro * ao, fma(ro, po - ps, ao)), HY_SMALLR);
   const double cstar = HY_SQRT(HY_QUOT(HY_GAMMA * ps, rstar));
   double spout = co - uo;
   double spin = cstar - uss;
   if (ps >= po) {
-    const double ushock = wo * iro - uo;
+    const double ushock = fma(wo, iro, -uo);
     spout = ushock;
     spin = ushock;
   }
   const double scr = hy_max(spout - spin, HY_SMALLC + fabs(spout + spin));
-  const double frac = hy_min(hy_max(0.5 * (1.0 + hy_div(spout + spin, scr HY_BAD_ARG)), 0.0), 1.0);
-  double r = frac * rstar + (1.0 - frac) * ro;
-  double u = frac * uss + (1.0 - frac) * uo;
-  double p = frac * ps + (1.0 - frac) * po;
+  const double frac = hy_min(hy_max(fma(0.5, hy_div(spout + spin, scr HY_BAD_ARG), 0.5), 0.0), 1.0);
+  double r = fma(frac, rstar - ro, ro);
+  double u = fma(frac, uss - uo, uo);
+  double p = fma(frac, ps - po, po);
   if (spout < 0.0) {
     r = ro;
     u = uo;
@@ -220,24 +244,25 @@ LF_HD void hy_riemann(double rl, double nl, double tl, double pl, double rr, dou
   hy_riemann_sample(&c, ps, rl, tl, rr, tr, gr, gn, gt, gp HY_BAD_ARG);
 }
 
-/* conservative flux through the face from the Godunov state */
+/* conservative flux through the face from the Godunov state:
+ * (rho u, rho u^2 + p, rho u t, u (E + p)), E + p = gamma/(gamma-1) p + rho |u|^2 / 2 */
 LF_HD void hy_flux(double r, double n, double t, double p, double* fr, double* fn, double* ft, double* fe) {
   const double m = r * n;
-  const double et = p * (1.0 / (HY_GAMMA - 1.0)) + 0.5 * r * (n * n + t * t);
+  const double ke = (0.5 * r) * fma(n, n, t * t);
   *fr = m;
-  *fn = m * n + p;
+  *fn = fma(m, n, p);
   *ft = m * t;
-  *fe = n * (et + p);
+  *fe = n * fma(p, HY_GOGM1, ke);
 }
 
 /* conservative update of one cell from its two face fluxes */
 LF_HD void hy_update(double r, double mn, double mt, double e, double frm, double fnm, double ftm, double fem,
                      double frp, double fnp, double ftp, double fep, double dtdx, double* ro, double* no,
                      double* to, double* eo) {
-  *ro = r + dtdx * (frm - frp);
-  *no = mn + dtdx * (fnm - fnp);
-  *to = mt + dtdx * (ftm - ftp);
-  *eo = e + dtdx * (fem - fep);
+  *ro = fma(dtdx, frm - frp, r);
+  *no = fma(dtdx, fnm - fnp, mn);
+  *to = fma(dtdx, ftm - ftp, mt);
+  *eo = fma(dtdx, fem - fep, e);
 }
 
 #endif

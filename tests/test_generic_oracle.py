@@ -108,3 +108,20 @@ def test_multi_nest_body_chains_plan_to_the_nest_executor():
         assert p.report()["nests"] == nests and p.report()["splits"] == 1
         assert p.executor == "jit_nests_fused", s
         assert "lf_nest0" in p.source and "lf_red" in p.source
+
+
+@pytest.mark.parametrize("shape,steps", [((9, 14), 3), ((16, 6), 1)])
+def test_generic_named_hydro_matches_c_oracle(shape, steps, tmp_path):
+    """Hydro2D has no `body:` form: its 12 rules name the user-kernel functions.
+    run_naive over the reference's inference DAG calls those functions element
+    by element (oracle/kernels_ffi.c) and must reproduce the C restatement of
+    the chain bit for bit, reflective ghost ring included."""
+    need_ref()
+    spec = tmp_path / "hydro2d.lf"
+    spec.write_text(lf.set_ranges(lf.spec_path("hydro2d").read_text(), shape))
+    st, dtdx = inputs.hydro_input(*shape, seed=shape[0] * 7 + 1)
+    ax = {"g_rho": st[0], "g_mx": st[1], "g_my": st[2], "g_E": st[3], "g_dtdx": np.array([dtdx])}
+    g = generic.run_naive(spec, ax, steps=steps)
+    ref = oracle.hydro(st, dtdx, steps)
+    for v, name in enumerate(("g_rho_n", "g_mx_n", "g_my_n", "g_E_n")):
+        assert np.array_equal(g[name].view(np.uint64), ref[v].view(np.uint64)), name

@@ -9,7 +9,9 @@ without needing /root/reference at test time.
                         chains' outputs come from the generic run_naive over the
                         dataflow DAG the REFERENCE's inference derives
                         (oracle/generic.py + refplan --dag) on their `body:`
-                        forms; Hydro2D (no body form) from the C oracle.
+                        forms; Hydro2D from the same run_naive with its named
+                        user kernels (hydro_kernels.h, element-wise through
+                        oracle/kernels_ffi.c) over the reference's DAG.
 
 Run in the CPU container (needs /root/reference):  python tools/make_golden.py
 """
@@ -68,9 +70,17 @@ def numerics():
         arrays = {f"in_{k}": v for k, v in ax.items()}
         arrays.update({f"out_{k}": v for k, v in goals.items()})
         np.savez_compressed(out / f"{case}.npz", sizes=np.array(sizes), steps=np.array(steps), **arrays)
-    # Hydro2D: the C oracle (the chain has no body form)
-    st, dtdx = inputs.hydro_input(12, 20, seed=8)
-    ref = oracle.hydro(st, dtdx, 2)
+    # Hydro2D: the 12 named kernels evaluated over the reference's inference DAG
+    sizes = (12, 20)
+    st, dtdx = inputs.hydro_input(*sizes, seed=8)
+    tmp = SPECS / "_golden_hydro2d.lf"
+    tmp.write_text(lf.set_ranges(lf.spec_path("hydro2d").read_text(), sizes))
+    try:
+        g = generic.run_naive(tmp, {"g_rho": st[0], "g_mx": st[1], "g_my": st[2], "g_E": st[3],
+                                    "g_dtdx": np.array([dtdx])}, steps=2)
+    finally:
+        tmp.unlink()
+    ref = [g[n] for n in ("g_rho_n", "g_mx_n", "g_my_n", "g_E_n")]
     np.savez_compressed(out / "hydro.npz", sizes=np.array((12, 20)), steps=np.array(2), dtdx=np.array([dtdx]),
                         **{f"in_{v}": st[v] for v in range(4)}, **{f"out_{v}": ref[v] for v in range(4)})
 
