@@ -127,7 +127,7 @@ def measured_peak():
 
 # Hydro2D: algorithmic flops per cell-step of the user kernels as written
 # (oracle/flopcount.cpp, pinned by tests/test_flopcount.py; + - * / sqrt = 1)
-HYDRO_FLOPS_PER_CELL_STEP = 821.3264
+HYDRO_FLOPS_PER_CELL_STEP = 853.3264
 
 
 def measured_fp64_peak():

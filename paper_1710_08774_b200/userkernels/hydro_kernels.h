@@ -24,33 +24,37 @@
  *     carried as W^2 = gamma rho (p + k (p* - p)) -- one fma per Newton step
  *     and no division by p (gamma k = (gamma+1)/2);
  *   * the Newton step z_l z_r / (z_l + z_r) (u*_l - u*_r), z = 2W^3/(W^2+C^2),
- *     is written over one common denominator (2 sqrt + 1 division per step);
- *   * the star density rho W^2 / (W^2 + rho (p - p*)) is one division.
+ *     is written over one common denominator (2 sqrt + 1 reciprocal per step);
+ *   * the star density rho W^2 / (W^2 + rho (p - p*)) is one quotient;
+ *   * every quotient a / b is formed as a * (1/b) from the correctly rounded
+ *     reciprocal (two roundings; b > 0 in every case, so the sign of a zero
+ *     numerator carries through exactly as in a / b), and the Newton update
+ *     p* + num/den as fma(num, 1/den, p*).
  */
 #ifndef LF_USERKERNELS_HYDRO_H
 #define LF_USERKERNELS_HYDRO_H
 
-/* Divisions and square roots go through HY_QUOT / HY_SQRT.  By default they
- * are the plain operators.  An sm_100a executor may include this header a
+/* Reciprocals and square roots go through HY_RCP / HY_SQRT.  By default they
+ * are the plain operators (1.0 / b, sqrt).  An sm_100a executor may include this header a
  * second time, inside its own namespace and with HY_FAST defined (after
- * csrc/exec/fastmath.cuh): every function that divides or takes a root then
+ * csrc/exec/fastmath.cuh): every function that takes a reciprocal or a root then
  * takes a trailing `unsigned* hy_bad`, uses the branch-free fast paths of
  * fastmath.cuh, and sets *hy_bad when an operand left the range where those
  * equal the IEEE operation -- the executor then recomputes with the plain
  * build.  Same expressions, same operation order: the arithmetic is unchanged. */
 #undef HY_BAD_PARAM
 #undef HY_BAD_ARG
-#undef HY_QUOT
+#undef HY_RCP
 #undef HY_SQRT
 #ifdef HY_FAST
 #define HY_BAD_PARAM , unsigned* hy_bad
 #define HY_BAD_ARG , hy_bad
-#define HY_QUOT(a, b) lf_div_fast((a), (b), hy_bad)
+#define HY_RCP(b) lf_rcp_fast((b), hy_bad)
 #define HY_SQRT(x) lf_sqrt_fast((x), hy_bad)
 #else
 #define HY_BAD_PARAM
 #define HY_BAD_ARG
-#define HY_QUOT(a, b) ((a) / (b))
+#define HY_RCP(b) (1.0 / (b))
 #define HY_SQRT(x) sqrt(x)
 #endif
 
@@ -72,28 +76,12 @@
 
 LF_HD double hy_max(double a, double b) { return a > b ? a : b; }
 LF_HD double hy_min(double a, double b) { return a < b ? a : b; }
-/* a / b for a denominator that is finite and nonzero (every division of this
- * chain): a zero numerator returns a * b, which is the same signed zero as the
- * quotient.  Keeps the exactly-zero differences of states at rest (velocities,
- * pressure jumps, slopes) off the device's division slow path. */
-LF_HD double hy_div(double a, double b HY_BAD_PARAM) {
-#ifdef HY_FAST
-  unsigned slow = 0;
-  const double q = lf_div_fast(a, b, &slow);
-  *hy_bad |= a == 0.0 ? 0u : slow;
-  return a == 0.0 ? a * b : q;
-#else
-  if (a == 0.0) return a * b;
-  return a / b;
-#endif
-}
-
 /* conservative -> primitive (density, normal & transverse velocity, pressure):
  * p = (gamma-1) (e - |m|^2 / (2 rho)) */
 LF_HD void hy_constoprim(double r, double mn, double mt, double e, double* qr, double* qn, double* qt,
                          double* qp HY_BAD_PARAM) {
   const double rr = hy_max(r, HY_SMALLR);
-  const double inv = HY_QUOT(1.0, rr);
+  const double inv = HY_RCP(rr);
   const double m2 = fma(mn, mn, mt * mt);
   *qr = rr;
   *qn = mn * inv;
@@ -123,7 +111,7 @@ LF_HD void hy_trace(double r, double n, double t, double p, double dr, double dn
                     double* pt, double* pp HY_BAD_PARAM) {
   const double h = -0.5 * dtdx;
   const double sr = h * fma(n, dr, r * dn);
-  const double sn = h * fma(n, dn, hy_div(dp, r HY_BAD_ARG));
+  const double sn = h * fma(n, dn, dp * HY_RCP(r));
   const double st = h * (n * dt);
   const double sp = h * fma(n, dp, (HY_GAMMA * p) * dn);
   *mr = hy_max(fma(-0.5, dr, r) + sr, HY_SMALLR);
@@ -174,7 +162,7 @@ LF_HD double hy_riemann_init(double rl, double nl, double pl, double rr, double 
   /* acoustic (linearised) first guess */
   const double cl = HY_SQRT(c->cl2);
   const double cr = HY_SQRT(c->cr2);
-  return hy_max(HY_QUOT(fma(cr, pl, cl * pr) + (cl * cr) * c->dn, cl + cr), HY_SMALLP);
+  return hy_max((fma(cr, pl, cl * pr) + (cl * cr) * c->dn) * HY_RCP(cl + cr), HY_SMALLP);
 }
 
 LF_HD double hy_riemann_newton(const hy_rp* c, double ps HY_BAD_PARAM) {
@@ -186,7 +174,7 @@ LF_HD double hy_riemann_newton(const hy_rp* c, double ps HY_BAD_PARAM) {
   const double inner = fma(fma(c->dn, wl, -dl), wr, -(dr * wl));
   const double num = (al * ar) * inner;
   const double den = fma(fma(0.5, al, c->hcl2), wr * ar, fma(0.5, ar, c->hcr2) * (wl * al));
-  return hy_max(ps + hy_div(num, den HY_BAD_ARG), HY_SMALLP);
+  return hy_max(fma(num, HY_RCP(den), ps), HY_SMALLP);
 }
 
 LF_HD void hy_riemann_sample(const hy_rp* c, double ps, double rl, double tl, double rr, double tr, double* gr,
@@ -195,7 +183,7 @@ LF_HD void hy_riemann_sample(const hy_rp* c, double ps, double rl, double tl, do
   const double ar = fma(c->gkr, ps - c->pr, c->cr2);
   const double wl = HY_SQRT(al);
   const double wr = HY_SQRT(ar);
-  const double us = hy_div(fma(wl, c->nl, wr * c->nr) + (c->pl - c->pr), wl + wr HY_BAD_ARG);
+  const double us = (fma(wl, c->nl, wr * c->nr) + (c->pl - c->pr)) * HY_RCP(wl + wr);
   const int left = us > 0.0;
   const double ro = left ? rl : rr;
   const double uo = left ? c->nl : -c->nr; /* velocity along the sampled wave direction */
@@ -204,10 +192,10 @@ LF_HD void hy_riemann_sample(const hy_rp* c, double ps, double rl, double tl, do
   const double ao = left ? al : ar;        /* W^2 of the sampled wave */
   const double to = left ? tl : tr;
   const double uss = left ? us : -us;
-  const double iro = HY_QUOT(1.0, ro);
+  const double iro = HY_RCP(ro);
   const double co = HY_SQRT((HY_GAMMA * po) * iro);
-  const double rstar = hy_max(HY_QUOT(ro * ao, fma(ro, po - ps, ao)), HY_SMALLR);
-  const double cstar = HY_SQRT(HY_QUOT(HY_GAMMA * ps, rstar));
+  const double rstar = hy_max((ro * ao) * HY_RCP(fma(ro, po - ps, ao)), HY_SMALLR);
+  const double cstar = HY_SQRT((HY_GAMMA * ps) * HY_RCP(rstar));
   double spout = co - uo;
   double spin = cstar - uss;
   if (ps >= po) {
@@ -216,7 +204,7 @@ LF_HD void hy_riemann_sample(const hy_rp* c, double ps, double rl, double tl, do
     spin = ushock;
   }
   const double scr = hy_max(spout - spin, HY_SMALLC + fabs(spout + spin));
-  const double frac = hy_min(hy_max(fma(0.5, hy_div(spout + spin, scr HY_BAD_ARG), 0.5), 0.0), 1.0);
+  const double frac = hy_min(hy_max(fma(0.5, (spout + spin) * HY_RCP(scr), 0.5), 0.0), 1.0);
   double r = fma(frac, rstar - ro, ro);
   double u = fma(frac, uss - uo, uo);
   double p = fma(frac, ps - po, po);

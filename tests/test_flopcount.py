@@ -13,4 +13,4 @@ def test_hydro_flops_per_cell_step_matches_the_count():
     assert abs(d["flops_per_cell_step"] - bench.HYDRO_FLOPS_PER_CELL_STEP) < 1e-3
     # 10 Newton steps of 2 sqrt + 1 division dominate (fma = 2 flops): O(10^3) per cell-step
     per = d["per_cell_sweep"]
-    assert per["sqrt"] == 26 and 17 <= per["div"] <= 19  # zero numerators multiply (hy_div)
+    assert per["sqrt"] == 26 and per["div"] == 18  # quotients as reciprocal x numerator
