@@ -35,10 +35,31 @@ namespace lfx {
 // operands outside their exact range (fastmath.cuh); every call below checks
 // the flag and recomputes with the plain kernels above when it is set
 namespace hf {
+// the chain's 64-bit constants as constant-bank operands (same values): as
+// literals they are rematerialised into uniform registers inside the loops
+// (same-box A/B: +4 %)
+__constant__ double kGamma = HY_GAMMA, kGm1 = HY_GM1, kGk = HY_GK, kSmallR = HY_SMALLR, kSmallP = HY_SMALLP,
+                    kSmallC = HY_SMALLC;
+#undef HY_GAMMA
+#undef HY_GM1
+#undef HY_GK
+#undef HY_SMALLR
+#undef HY_SMALLP
+#undef HY_SMALLC
+#define HY_GAMMA kGamma
+#define HY_GM1 kGm1
+#define HY_GK kGk
+#define HY_SMALLR kSmallR
+#define HY_SMALLP kSmallP
+#define HY_SMALLC kSmallC
 #define HY_FAST 1
+#undef LF_HD
+#define LF_HD __device__ __forceinline__
 #undef LF_USERKERNELS_HYDRO_H
 #include "../../userkernels/hydro_kernels.h"
 #undef HY_FAST
+#undef LF_HD
+#define LF_HD __host__ __device__ __forceinline__
 }  // namespace hf
 namespace {
 

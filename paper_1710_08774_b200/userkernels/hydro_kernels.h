@@ -58,13 +58,19 @@
 #define HY_SQRT(x) sqrt(x)
 #endif
 
+#ifndef LF_HD
 #if defined(__CUDACC__) || defined(__CUDACC_RTC__)
 #define LF_HD __host__ __device__ __forceinline__
 #else
 #include <math.h>
 #define LF_HD static inline
 #endif
+#endif
 
+/* Physical constants.  An executor may define them first as names bound to
+ * the same values (e.g. device constant memory, so they are instruction
+ * operands instead of rematerialised 64-bit immediates). */
+#ifndef HY_GAMMA
 #define HY_GAMMA 1.4
 #define HY_GM1 0.4         /* gamma - 1 */
 #define HY_GOGM1 3.5       /* gamma / (gamma - 1) */
@@ -72,6 +78,7 @@
 #define HY_SMALLR 1e-10
 #define HY_SMALLP 1e-12
 #define HY_SMALLC 1e-10
+#endif
 #define HY_NITER 10
 
 LF_HD double hy_max(double a, double b) { return a > b ? a : b; }
