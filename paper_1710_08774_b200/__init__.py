@@ -252,9 +252,53 @@ class Plan:
         return [t for t in self.terminals if t.is_goal]
 
     # ---- execution -----------------------------------------------------------
-    def _ptrs(self, bufs: Sequence[Any]):
+    @property
+    def outer_trips(self) -> int:
+        """Trips of the outermost loop dimension (the one slabs split)."""
+        if not hasattr(self, "_outer"):
+            lo, hi, stride = self.report()["ranges"][0]
+            self._outer = (hi - lo) // stride
+        return self._outer
+
+    def _ptrs(self, bufs: Sequence[Any], device: bool = True, rows: tuple[int, int, int] | None = None):
+        """Pointer array of the terminal buffers, axioms then goals.  Tensors
+        and arrays are checked against the terminal they stand for: C-contiguous,
+        its element size, exactly its bytes (a slab's rows (lo, hi) of an n0-row
+        outer dimension when `rows` is given), and -- for the device entry
+        points -- a CUDA tensor on the current device.  Raw integer pointers
+        are passed through unchecked."""
         if len(bufs) != len(self.terminals):
             raise ValueError(f"expected {len(self.terminals)} buffers (axioms then goals), got {len(bufs)}")
+        for i, (b, t) in enumerate(zip(bufs, self.terminals)):
+            if isinstance(b, int):
+                continue
+            want = t.bytes
+            if rows is not None and t.extent:
+                lo, hi, n0 = rows
+                want = int(np.prod(self.slab_terminal_extent(i, lo, hi, n0))) * t.elem_bytes
+            if hasattr(b, "data_ptr"):  # torch tensor
+                if device:
+                    import torch
+                    if not b.is_cuda:
+                        raise ValueError(f"{t.name}: expected a CUDA tensor, got one on {b.device}")
+                    if b.device.index != torch.cuda.current_device():
+                        raise ValueError(f"{t.name}: expected a CUDA tensor on the current device "
+                                         f"{torch.cuda.current_device()}, got one on {b.device}")
+                if not b.is_contiguous():
+                    raise ValueError(f"{t.name}: tensor must be contiguous")
+                size, nbytes = b.element_size(), b.numel() * b.element_size()
+            elif isinstance(b, np.ndarray):
+                if device:
+                    raise ValueError(f"{t.name}: a host array passed to a device entry point (use run_host)")
+                if not b.flags.c_contiguous:
+                    raise ValueError(f"{t.name}: host arrays must be C-contiguous")
+                size, nbytes = b.itemsize, b.nbytes
+            else:
+                raise TypeError(f"{t.name}: cannot take a buffer pointer from {type(b).__name__}")
+            if size != t.elem_bytes:
+                raise ValueError(f"{t.name}: element size {size} B, the terminal's type {t.type!r} is {t.elem_bytes} B")
+            if nbytes != want:
+                raise ValueError(f"{t.name}: expected {want} bytes, got {nbytes}")
         arr = (ctypes.c_void_p * len(bufs))(*[_ptr(b) for b in bufs])
         return arr
 
@@ -265,10 +309,7 @@ class Plan:
 
     def run_host(self, arrays: Sequence[np.ndarray], steps: int = 1) -> None:
         """Host arrays in, goals written back (the emitted function's contract)."""
-        for a, t in zip(arrays, self.terminals):
-            if isinstance(a, np.ndarray) and a.nbytes != t.bytes:
-                raise ValueError(f"{t.name}: expected {t.bytes} bytes, got {a.nbytes}")
-        _check(lib().lf_run_host(self._h, self._ptrs(arrays), len(arrays), steps))
+        _check(lib().lf_run_host(self._h, self._ptrs(arrays, device=False), len(arrays), steps))
 
     def run_slab(self, bufs: Sequence[Any], lo: int, hi: int, global_: int, stream: Any = None,
                  part: tuple[int, int] | None = None) -> None:
@@ -276,7 +317,7 @@ class Plan:
         `part` = slab-local rows to compute (default: all)."""
         p0, p1 = part if part is not None else (0, 0)
         slab = _Slab(lo, hi, global_, p0, p1)
-        _check(lib().lf_run_slab(self._h, self._ptrs(bufs), len(bufs), ctypes.byref(slab),
+        _check(lib().lf_run_slab(self._h, self._ptrs(bufs, rows=(lo, hi, global_)), len(bufs), ctypes.byref(slab),
                                  _stream_handle(stream)))
 
     def run_slabs(self, bufs: Sequence[Any], comm: "NcclComm", steps: int = 1, stream: Any = None) -> None:
@@ -340,7 +381,10 @@ def run_slabs(plan: "Plan", bufs: Sequence[Any], comm: NcclComm, steps: int = 1,
     [n*rank/world, n*(rank+1)/world) of the outer dimension, buffers sized for
     the slab, faces exchanged with the neighbours by NCCL overlapped with the
     interior rows, the final state in the goal buffers."""
-    _check(lib().lf_run_slabs(plan._h, comm.handle, comm.rank, comm.world, plan._ptrs(bufs), len(bufs), steps,
+    n0 = plan.outer_trips
+    lo, hi = n0 * comm.rank // comm.world, n0 * (comm.rank + 1) // comm.world
+    _check(lib().lf_run_slabs(plan._h, comm.handle, comm.rank, comm.world, plan._ptrs(bufs, rows=(lo, hi, n0)),
+                              len(bufs), steps,
                               _stream_handle(stream)))
 
 
@@ -351,6 +395,9 @@ def run_slabs_local(plan: "Plan", rank_bufs: Sequence[Sequence[Any]], steps: int
     nterm = len(plan.terminals)
     if any(len(b) != nterm for b in rank_bufs):
         raise ValueError(f"expected {nterm} buffers per rank (axioms then goals)")
+    n0, world = plan.outer_trips, len(rank_bufs)
+    for r, bufs in enumerate(rank_bufs):
+        plan._ptrs(bufs, rows=(n0 * r // world, n0 * (r + 1) // world, n0))  # validation only
     flat = [_ptr(b) for bufs in rank_bufs for b in bufs]
     arr = (ctypes.c_void_p * len(flat))(*flat)
     _check(lib().lf_run_slabs_local(plan._h, len(rank_bufs), arr, nterm, steps,

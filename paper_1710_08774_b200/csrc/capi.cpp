@@ -238,6 +238,14 @@ int slab_check(const lf_plan* plan, const SlabGeom& g, int world, std::string& e
     err = "more ranks than rows along the outer dimension";
     return LF_ERR_SPEC;
   }
+  // every rank must own at least as many rows as a neighbour's ghost band:
+  // the exchange sends a rank's own outermost rows (single hop)
+  const long need = std::max(g.halo_lo, g.halo_hi);
+  if (g.n0 / world < need) {
+    err = "slabs of " + std::to_string(g.n0 / world) + " row(s) are thinner than the " + std::to_string(need) +
+          "-row halo exchanged with each neighbour (use fewer ranks)";
+    return LF_ERR_SPEC;
+  }
   return LF_OK;
 }
 
@@ -785,6 +793,8 @@ int lf_run_slab(const lf_plan* cplan, void* const* terms, int nterm, const lf_sl
     if (slab->part_hi == slab->part_lo && slab->part_lo != 0) return LF_OK;  // empty part
     if (shares_buffer(cplan, terms))
       return fail(LF_ERR_UNSUPPORTED, "slab runs need distinct axiom and goal buffers (in-place runs cover the whole domain)");
+    // the generic executor's lazily created state (module, bands) is per plan
+    std::lock_guard<std::mutex> lk(const_cast<lf_plan*>(cplan)->mu);
     lfx::ExecArgs a;
     a.plan = &cplan->plan;
     a.terms = terms;

@@ -356,16 +356,11 @@ bool supports(const lf::Plan& plan, std::string& why) {
 int launch_step(const double* in, double* out, int ni, const RowPart& rp, cudaStream_t st, std::string& err) {
   const int nj = rp.rows;
   const Variant& v = variant();
-  static int slots = 0;
-  if (!slots) {
-    cudaError_t e = cudaFuncSetAttribute(v.kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, v.smem);
-    if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(biharm)", err);
-    int dev = 0, sms = 148, per_sm = 1;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, v.kernel, 32, v.smem);
-    slots = sms * std::max(1, std::min(per_sm, v.occ));
-  }
+  static LaunchCache cache;  // the variant is fixed per process (LF_BIHARM_VARIANT)
+  int slots = 0;
+  if (int s = resident_slots(cache, reinterpret_cast<const void*>(v.kernel), 32, v.smem, v.occ,
+                             "cudaFuncSetAttribute(biharm)", &slots, err))
+    return s;
   CUtensorMap map;
   uint64_t dims[2] = {(uint64_t)ni + 4, (uint64_t)nj + 4};
   uint32_t box[2] = {(uint32_t)(v.sw + 2 * H), (uint32_t)v.rows};  // must match the kernel's stage bytes

@@ -262,16 +262,11 @@ const BoxVariant& box_variant() {
 
 int run(const ExecArgs& a, std::string& err) {
   const BoxVariant& v = box_variant();
-  static int slots = 0;
-  if (!slots) {
-    cudaError_t e = cudaFuncSetAttribute(v.kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, v.smem);
-    if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(box)", err);
-    int dev = 0, sms = 148, per_sm = 1;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, v.kernel, 32, v.smem);
-    slots = sms * std::max(1, std::min(per_sm, v.occ));
-  }
+  static LaunchCache cache;  // the variant is fixed per process (LF_BOX_VARIANT)
+  int slots = 0;
+  if (int s = resident_slots(cache, reinterpret_cast<const void*>(v.kernel), 32, v.smem, v.occ,
+                             "cudaFuncSetAttribute(box)", &slots, err))
+    return s;
   const auto& r = a.plan->rs.ranges;
   const int ni = (int)r[1].trips();
   const RowPart rp = row_part(a, (int)r[0].trips());  // slab rows: halo rows supplied by the caller

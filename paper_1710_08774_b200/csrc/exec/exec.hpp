@@ -7,6 +7,7 @@
 
 #include <cuda_runtime.h>
 
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -49,6 +50,19 @@ const std::string& embedded_userkernels();
 
 // helpers shared by the executors
 int cuda_status(cudaError_t e, const char* what, std::string& err);
+
+// Device-dependent launch setup of one kernel -- its dynamic shared-memory
+// attribute and the number of CTAs resident at once (SMs x occupancy, capped
+// at `occ_cap` per SM when > 0) -- done once per device ordinal, thread-safe.
+// A process may drive several GPUs (one per host thread or in turn).
+constexpr int kMaxDevices = 64;
+struct LaunchCache {
+  std::once_flag once[kMaxDevices];
+  int slots[kMaxDevices] = {};
+  cudaError_t err[kMaxDevices] = {};
+};
+int resident_slots(LaunchCache& cache, const void* kernel, int threads, int smem, int occ_cap, const char* what,
+                   int* slots, std::string& err);
 
 // rows of the outer dimension one launch computes (slab-local; whole slab when
 // no part is given) and the slab's row count

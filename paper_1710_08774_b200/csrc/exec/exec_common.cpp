@@ -1,5 +1,6 @@
 // Host helpers shared by the executors: TMA descriptor encoding through the
 // runtime's driver entry point, CUDA error mapping.
+#include <algorithm>
 #include <cstdlib>
 #include <mutex>
 
@@ -12,6 +13,29 @@ int cuda_status(cudaError_t e, const char* what, std::string& err) {
   if (e == cudaSuccess) return LF_OK;
   err = std::string(what) + ": " + cudaGetErrorName(e) + " (" + cudaGetErrorString(e) + ")";
   return LF_ERR_CUDA;
+}
+
+int resident_slots(LaunchCache& cache, const void* kernel, int threads, int smem, int occ_cap, const char* what,
+                   int* slots, std::string& err) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return cuda_status(e, "cudaGetDevice", err);
+  if (dev < 0 || dev >= kMaxDevices) {
+    err = "device ordinal out of range";
+    return LF_ERR_CUDA;
+  }
+  std::call_once(cache.once[dev], [&] {
+    cudaError_t x = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    int sms = 148, per_sm = 1;
+    if (x == cudaSuccess) x = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (x == cudaSuccess) x = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, smem);
+    per_sm = std::max(1, occ_cap > 0 ? std::min(per_sm, occ_cap) : per_sm);
+    cache.slots[dev] = sms * per_sm;
+    cache.err[dev] = x;
+  });
+  if (cache.err[dev] != cudaSuccess) return cuda_status(cache.err[dev], what, err);
+  *slots = cache.slots[dev];
+  return LF_OK;
 }
 
 static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {

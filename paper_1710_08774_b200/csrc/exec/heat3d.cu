@@ -55,6 +55,31 @@ struct Params {
   int store_policy;            // L2 policy of the output stores (l2_store_policy)
 };
 
+// A row's two output columns (gi0, gi0 + 32 of cell row (k, j)) and their
+// periodic images in the ghost layer: every combination of the own and the
+// wrapped index along k, j and i -- the face images, and the edge and corner
+// images as compositions of the face maps (the ghost fill of the oracle,
+// oracle/stencils.c) -- so every cell of the goal buffer is written.  A single
+// interior row / plane is the image of both ghost faces.
+__device__ __forceinline__ void store_images(double* out, const Params& p, int k, int j, int gi0, double v0,
+                                             double v1, bool wrap_lo_i, bool wrap_hi_i, uint64_t pol) {
+  int ks[3], js[3], nk = 0, nj = 0;
+  ks[nk++] = k + 1;
+  if (p.wrap_k && k == 0) ks[nk++] = p.nk + 1;
+  if (p.wrap_k && k == p.nk - 1) ks[nk++] = 0;
+  js[nj++] = j + 1;
+  if (p.wrap_j && j == 0) js[nj++] = p.nj + 1;
+  if (p.wrap_j && j == p.nj - 1) js[nj++] = 0;
+  for (int a = 0; a < nk; ++a)
+    for (int b = 0; b < nj; ++b) {
+      double* rowp = out + (long long)ks[a] * p.pk + (long long)js[b] * p.pj + 1;  // logical i = 0
+      st_hint(rowp + gi0, v0, pol);
+      st_hint(rowp + gi0 + 32, v1, pol);
+      if (wrap_lo_i) st_hint(rowp + p.ni, v0, pol);
+      if (wrap_hi_i) st_hint(rowp - 1, v1, pol);
+    }
+}
+
 // Work unit u = (k chunk, column tile), k-chunk major: at any moment all
 // persistent CTAs are inside the same one or two k chunks, so the halo rows a
 // CTA stages were staged moments earlier by its neighbours and hit in L2.
@@ -179,29 +204,10 @@ __global__ void __launch_bounds__(THREADS, 2)
       // plane k fully consumed: hand the slot back to the producer before the stores
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[g % S]);
-      double* plane = out + (long long)(k + 1) * p.pk;
 #pragma unroll
       for (int r = 0; r < RPW; ++r) {
         const int j = w.j0 + r0 + r;
-        double* rowp = plane + (long long)(j + 1) * p.pj + 1;  // logical i = 0
-        st_hint(rowp + gi0, o[r][0], pol);
-        st_hint(rowp + gi0 + 32, o[r][1], pol);
-        // periodic ghost refill by the owners of the wrapped cells
-        if (wrap_lo_i) st_hint(rowp + p.ni, o[r][0], pol);
-        if (wrap_hi_i) st_hint(rowp - 1, o[r][1], pol);
-        // (a single interior row / plane is the image of both ghost faces)
-        for (int side = 0; side < 2; ++side) {
-          if (p.wrap_j && j == (side ? p.nj - 1 : 0)) {
-            double* gr = plane + (long long)(side ? 0 : p.nj + 1) * p.pj + 1;
-            st_hint(gr + gi0, o[r][0], pol);
-            st_hint(gr + gi0 + 32, o[r][1], pol);
-          }
-          if (p.wrap_k && k == (side ? p.nk - 1 : 0)) {
-            double* gr = out + (long long)(side ? 0 : p.nk + 1) * p.pk + (long long)(j + 1) * p.pj + 1;
-            st_hint(gr + gi0, o[r][0], pol);
-            st_hint(gr + gi0 + 32, o[r][1], pol);
-          }
-        }
+        store_images(out, p, k, j, gi0, o[r][0], o[r][1], wrap_lo_i, wrap_hi_i, pol);
       }
 #pragma unroll
       for (int r = 0; r < RPW; ++r)
@@ -480,27 +486,10 @@ __global__ void __launch_bounds__(THREADS2, 2)
       // A(q-1) lives on in registers only
       __syncwarp();
       if (lane == 0) mbar_arrive(&aempty[a0 % ASLOTS]);
-      double* plane = out + (long long)(k + 1) * p.pk;
 #pragma unroll
       for (int rr = 0; rr < 4; ++rr) {
         const int j = w.j0 + 4 * wb + rr;
-        double* rowp = plane + (long long)(j + 1) * p.pj + 1;
-        st_hint(rowp + gi0, o2[rr][0], pol);
-        st_hint(rowp + gi0 + 32, o2[rr][1], pol);
-        if (wrap_lo_i) st_hint(rowp + p.ni, o2[rr][0], pol);
-        if (wrap_hi_i) st_hint(rowp - 1, o2[rr][1], pol);
-        for (int side = 0; side < 2; ++side) {
-          if (p.wrap_j && j == (side ? p.nj - 1 : 0)) {
-            double* gr = plane + (long long)(side ? 0 : p.nj + 1) * p.pj + 1;
-            st_hint(gr + gi0, o2[rr][0], pol);
-            st_hint(gr + gi0 + 32, o2[rr][1], pol);
-          }
-          if (p.wrap_k && k == (side ? p.nk - 1 : 0)) {
-            double* gr = out + (long long)(side ? 0 : p.nk + 1) * p.pk + (long long)(j + 1) * p.pj + 1;
-            st_hint(gr + gi0, o2[rr][0], pol);
-            st_hint(gr + gi0 + 32, o2[rr][1], pol);
-          }
-        }
+        store_images(out, p, k, j, gi0, o2[rr][0], o2[rr][1], wrap_lo_i, wrap_hi_i, pol);
       }
     }
     // the unit's last two A planes were only read by its last B planes
@@ -566,16 +555,11 @@ bool supports(const lf::Plan& plan, std::string& why) {
 int launch_step(const double* in, double* out, int ni, int nj, int nk, int k_lo, int k_hi, bool wrap_k,
                 cudaStream_t st, std::string& err) {
   const Variant& v = variant();
-  static int slots = 0;
-  if (!slots) {
-    cudaError_t e = cudaFuncSetAttribute(v.kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, v.smem);
-    if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(heat3d)", err);
-    int dev = 0, sms = 148, per_sm = 1;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, v.kernel, THREADS, v.smem);
-    slots = sms * std::max(per_sm, 1);
-  }
+  static LaunchCache cache;  // the variant is fixed per process (LF_HEAT3D_VARIANT)
+  int slots = 0;
+  if (int s = resident_slots(cache, reinterpret_cast<const void*>(v.kernel), THREADS, v.smem, 0,
+                             "cudaFuncSetAttribute(heat3d)", &slots, err))
+    return s;
   CUtensorMap map;
   uint64_t dims[3] = {(uint64_t)ni + 2, (uint64_t)nj + 2, (uint64_t)nk + 2};
   uint32_t box[3] = {LD, (uint32_t)(v.ty + 2), 1};
@@ -625,16 +609,11 @@ bool tb_enabled(int ni, int nj, int nk) {
 
 template <class K>
 int launch_pair_k(const double* in, double* out, int ni, int nj, int nk, cudaStream_t st, std::string& err) {
-  static int slots = 0;
-  if (!slots) {
-    cudaError_t e = cudaFuncSetAttribute(tb::heat3d_fused2<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, K::SMEM);
-    if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(heat3d pair)", err);
-    int dev = 0, sms = 148, per_sm = 1;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tb::heat3d_fused2<K>, tb::THREADS2, K::SMEM);
-    slots = sms * std::max(per_sm, 1);
-  }
+  static LaunchCache cache;
+  int slots = 0;
+  if (int s = resident_slots(cache, reinterpret_cast<const void*>(tb::heat3d_fused2<K>), tb::THREADS2, K::SMEM, 0,
+                             "cudaFuncSetAttribute(heat3d pair)", &slots, err))
+    return s;
   CUtensorMap map;
   uint64_t dims[3] = {(uint64_t)ni + 2, (uint64_t)nj + 2, (uint64_t)nk + 2};
   uint32_t box[3] = {tb::LDI, tb::RI, 1};

@@ -403,20 +403,16 @@ int launch_step(const double* const in[4], double* const out[4], const double* d
   // With the branch-free divisions the Riemann phase keeps the fp64 pipe busy
   // from fewer warps: 3 CTAs at 168 registers (no spills) beat 4 CTAs at 128
   // (96 B of spills) -- profiles/r01_hydro_variants.txt
-  static void (*kern)(Maps, Params) = nullptr;
-  static int slots = 0;
-  if (!slots) {
+  static void (*const kern)(Maps, Params) = [] {
     const char* v = std::getenv("LF_HYDRO_VARIANT");
     const int var = v ? std::atoi(v) : 1;
-    kern = var == 0 ? hydro_fused<2> : (var == 2 ? hydro_fused<4> : hydro_fused<3>);
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
-    if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(hydro)", err);
-    int dev = 0, sms = 148, per_sm = 1;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NT, SMEM);
-    slots = sms * std::max(1, per_sm);
-  }
+    return var == 0 ? hydro_fused<2> : (var == 2 ? hydro_fused<4> : hydro_fused<3>);
+  }();
+  static LaunchCache cache;
+  int slots = 0;
+  if (int s = resident_slots(cache, reinterpret_cast<const void*>(kern), NT, SMEM, 0, "cudaFuncSetAttribute(hydro)",
+                             &slots, err))
+    return s;
   Maps maps;
   uint64_t dims[2] = {(uint64_t)ni + 4, (uint64_t)nj + 4};
   uint32_t box[2] = {BOXW, R};

@@ -334,8 +334,21 @@ int JitKernel::run(const ExecArgs& a, std::string& err) {
     err = "CUDA driver entry points unavailable";
     return LF_ERR_CUDA;
   }
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) {
+    err = "cudaGetDevice failed";
+    return LF_ERR_CUDA;
+  }
+  if (module_ && dev != device_) {
+    // the module, its functions and the plan-owned device buffers belong to
+    // the context they were created in
+    err = "this plan's generated kernels are loaded on device " + std::to_string(device_) +
+          "; create one plan per device (current device " + std::to_string(dev) + ")";
+    return LF_ERR_UNSUPPORTED;
+  }
   if (!module_) {
     cudaFree(nullptr);  // make sure the primary context exists
+    device_ = dev;
     CUmodule m;
     CUresult r = d.load(&m, cubin_.data());
     if (r != CUDA_SUCCESS) {

@@ -99,7 +99,8 @@ class JitKernel {
 
  private:
   JitProgram prog_;
-  void* module_ = nullptr;  // CUmodule
+  void* module_ = nullptr;  // CUmodule, loaded into the context of device_ at the first run
+  int device_ = -1;
   void* step_ = nullptr;    // CUfunction
   void* step_ws_ = nullptr; // warp-specialised variant (TMA producer warp)
   void* fill_ = nullptr;

@@ -40,6 +40,11 @@ def exchange(bufs: Sequence[torch.Tensor], halo: Halo, rank: int, world: int, gr
     receives are issued in one fixed order (send-up, send-down / recv-down,
     recv-up) so they pair off correctly.
     """
+    for b in bufs:
+        n = b.shape[0] - halo.lo - halo.hi
+        if n < max(halo.lo, halo.hi):
+            raise ValueError(f"a slab of {n} row(s) is thinner than the {max(halo.lo, halo.hi)}-row halo "
+                             "exchanged with each neighbour (use fewer ranks)")
     if world == 1:
         if halo.periodic:
             for b in bufs:

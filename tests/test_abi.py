@@ -62,3 +62,38 @@ def test_terminal_layout_matches_inputs():
     r = lf.Plan.with_ranges("box2x", (8, 12))
     assert inputs.box_input(8, 12).shape == r.terminals[0].extent
     assert r.terminals[0].dtype == np.float32
+
+
+def test_slabs_thinner_than_the_halo_are_rejected():
+    """A rank must own at least as many rows as the ghost band it sends its
+    neighbours (Hydro2D / biharmonic halo: 2 rows): 3 ranks over 5 rows is
+    refused before any device work, natively and in slabs.py."""
+    p = lf.Plan.with_ranges("hydro2d", (5, 16))
+    n = len(p.terminals)
+    ptrs = (ctypes.c_void_p * (3 * n))(*range(16, 16 * (3 * n + 1), 16))  # distinct, never dereferenced
+    assert lf.lib().lf_run_slabs_local(p._h, 3, ptrs, n, 2, None) == lf.LF_ERR_SPEC
+    assert "halo" in lf.lib().lf_last_error().decode()
+    import torch
+    from paper_1710_08774_b200 import slabs
+    with pytest.raises(ValueError, match="halo"):
+        slabs.exchange([torch.zeros(5, 4)], slabs.Halo(2, 2, False), 0, 1)
+
+
+def test_buffer_arguments_are_checked_against_the_terminals():
+    """Plan.run / run_host / run_slab refuse buffers that do not match the
+    terminal they stand for (wrong dtype, size, layout or device
+    would otherwise read or write out of bounds)."""
+    import torch
+    p = lf.Plan.with_ranges("biharmonic2d", (16, 32))
+    t = p.terminals[0]
+    good = np.zeros(t.extent, np.float64)
+    with pytest.raises(ValueError, match="expected"):
+        p.run_host([good, np.zeros((4, 4))], steps=1)  # wrong size
+    with pytest.raises(ValueError, match="element size"):
+        p.run_host([good, np.zeros(t.extent, np.float32)], steps=1)
+    with pytest.raises(ValueError, match="contiguous"):
+        p.run_host([good, np.zeros((t.extent[1], t.extent[0])).T], steps=1)
+    with pytest.raises(ValueError, match="host array"):
+        p.run([good, good.copy()])
+    with pytest.raises(ValueError, match="CUDA tensor"):
+        p.run([torch.zeros(t.extent, dtype=torch.float64)] * 2)
