@@ -396,8 +396,9 @@ def run_slabs_local(plan: "Plan", rank_bufs: Sequence[Sequence[Any]], steps: int
     if any(len(b) != nterm for b in rank_bufs):
         raise ValueError(f"expected {nterm} buffers per rank (axioms then goals)")
     n0, world = plan.outer_trips, len(rank_bufs)
-    for r, bufs in enumerate(rank_bufs):
-        plan._ptrs(bufs, rows=(n0 * r // world, n0 * (r + 1) // world, n0))  # validation only
+    if world <= n0:  # (more ranks than rows: the library reports LF_ERR_SPEC)
+        for r, bufs in enumerate(rank_bufs):
+            plan._ptrs(bufs, rows=(n0 * r // world, n0 * (r + 1) // world, n0))  # validation only
     flat = [_ptr(b) for bufs in rank_bufs for b in bufs]
     arr = (ctypes.c_void_p * len(flat))(*flat)
     _check(lib().lf_run_slabs_local(plan._h, len(rank_bufs), arr, nterm, steps,
