@@ -18,6 +18,7 @@
 // Ghost refill of iterated goals (`config: boundary:`) is a second kernel that
 // visits ghost cells only.
 #include <algorithm>
+#include <cstring>
 #include <cctype>
 #include <climits>
 #include <functional>
@@ -583,6 +584,12 @@ bool emit_march(Ctx& C, JitProgram& out, std::ostream& src, bool ws = false) {
     if (win[v] > 0 && (win[v] > 64 || old[v] < -60 || lead[v] > 60))
       return (C.error = "pipeline window deeper than 64 rows", false);
   }
+  // fault injection for the differential tests (R/"deliberately
+  // corrupted rotation span (span-1) -> mismatch reported"): LF_JIT_FAULT=
+  // span:<intermediate> emits that variable's rolling window one row short
+  if (const char* f = std::getenv("LF_JIT_FAULT"); f && std::strncmp(f, "span:", 5) == 0)
+    for (size_t v = 0; v < nv; ++v)
+      if (C.smem_var[v] && win[v] > 1 && C.P.vars[v].name == f + 5) win[v] -= 1;
   // ws: TMA box origins must be 16-B aligned along the contiguous dimension.
   // Tiles are a multiple of `al` elements there, and each streamed axiom's
   // window starts up to al - 1 elements further left (its range is widened

@@ -182,3 +182,27 @@ def test_register_window_rotation_is_exact(name, monkeypatch):
     ref = generic.run_naive(SPECS / f"{name}.lf", ax, steps=3)
     for g, t in zip(got, plan.goals):
         assert np.array_equal(bits(g), bits(ref[t.name])), t.name
+
+
+def test_fault_injection_corrupted_span_is_caught(monkeypatch):
+    """R/SPEC.md:557 fault injection: the same chain emitted with one rolling
+    window a row short (LF_JIT_FAULT=span:L, the corrupted rotation span the
+    SPEC names) no longer matches run_naive, and the first mismatching trip is
+    the witness; the uncorrupted plan stays bit-exact."""
+    shape = (48, 160)
+    text = lf.set_ranges((lf.SPEC_DIR / "examples" / "biharm_body.lf").read_text(), shape)
+    u = inputs.biharm_input(*shape, seed=9)
+    ref = oracle.biharm(u, 1)
+    monkeypatch.setenv("LF_JIT_WS", "0")  # plain march: windows are exactly the contraction span
+    good = lf.Plan(text, "biharm_body.lf")
+    assert np.array_equal(bits(run_device(good, [u], 1)[0]), bits(ref))
+    monkeypatch.setenv("LF_JIT_FAULT", "span:L")
+    bad = lf.Plan(text, "biharm_body_fault.lf")
+    L = lf.lib()
+    src_good, src_bad = L.lf_plan_source(good._h).decode(), L.lf_plan_source(bad._h).decode()
+    assert src_good != src_bad  # the window is emitted one row shorter
+    got = run_device(bad, [u], 1)[0]
+    diff = np.argwhere(bits(got) != bits(ref))
+    assert diff.size > 0, "a corrupted rotation span went unnoticed"
+    witness = tuple(int(x) for x in diff[0])
+    assert 2 <= witness[0] < shape[0] + 2  # a trip (row) of the interior
