@@ -70,6 +70,7 @@ def lib(native: bool = False) -> ctypes.CDLL:
             L.lfo_hydro_naive.argtypes = [PP, PP, Lg, Lg, ctypes.c_double, I]
             L.lfo_hydro_fused.argtypes = [PP, PP, Lg, Lg, ctypes.c_double, I, I]
             L.lfo_hydro_fused_step.argtypes = [PP, PP, Lg, Lg, ctypes.c_double, I]
+            L.lfo_hydro_adaptive.argtypes = [PP, PP, Lg, Lg, ctypes.POINTER(ctypes.c_double), I, I, I]
         _libs[native] = L
     return _libs[native]
 
@@ -147,6 +148,19 @@ def hydro(state, dtdx: float, steps: int, fused: bool = False, threads: int = 0,
     else:
         _ok(lib(native).lfo_hydro_naive(pin, pout, nj, ni, dtdx, steps))
     return outs
+
+
+def hydro_adaptive(state, dtdx: float, steps: int, fused: bool = False, threads: int = 0):
+    """`steps` steps with the CFL time step (specs/hydro2d_adaptive.lf): returns
+    (state after the last step, the dt/dx that state gives)."""
+    nj, ni = state[0].shape[0] - 4, state[0].shape[1] - 4
+    ins = [np.ascontiguousarray(a, dtype=np.float64) for a in state]
+    outs = [np.empty_like(a) for a in ins]
+    PA = ctypes.c_void_p * 4
+    d = ctypes.c_double(dtdx)
+    _ok(lib().lfo_hydro_adaptive(PA(*[_p(a) for a in ins]), PA(*[_p(a) for a in outs]), nj, ni, ctypes.byref(d),
+                                 steps, 1 if fused else 0, threads))
+    return outs, d.value
 
 
 def hydro_step(state, outs, dtdx: float, threads: int = 0, native: bool = False) -> None:

@@ -290,7 +290,10 @@ def run_naive(spec_path, axioms: dict, steps: int = 1) -> dict:
                                 if v.ndim == nd and v.shape[a] > 1:
                                     ix[a] = slice(p, p + 1)
                             env[pname] = v[tuple(ix)] if v.ndim == nd else v
-                        acc = np.asarray(eval_body(bodies[rap["kernel"]][o_name], env, dt), dtype=dt)
+                        if bodies[rap["kernel"]]:
+                            acc = np.asarray(eval_body(bodies[rap["kernel"]][o_name], env, dt), dtype=dt)
+                        else:  # a named kernel: the user-kernel function, element-wise
+                            acc = call_named(k, [env[pn] for pn in k["inputs"]])[0]
                     vals[rap["out"][0]] = acc
                     continue
                 if not bodies[rap["kernel"]]:
@@ -313,6 +316,9 @@ def run_naive(spec_path, axioms: dict, steps: int = 1) -> dict:
                 v = np.broadcast_to(vals[rap["in"][0]], shape_of(set(axes)))
                 a[tuple(sl)] = v.reshape([n[dim] for dim in axes])
         for g, a_name in pair.items():
+            if not d["externals"][a_name]["extents"]:  # a rank-0 terminal: no ghosts
+                cur[a_name] = goals[g]
+                continue
             modes = d["boundary"].get(g) or d["boundary"].get("*") or ["none"]
             base = [b - l for (_, b), l in zip(d["externals"][a_name]["extents"], lo)]  # relative to the range start
             _fill(goals[g], modes, n, base)

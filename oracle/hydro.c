@@ -279,4 +279,61 @@ int lfo_hydro_fused(const double* const in[4], double* const out[4], long nj, lo
   free(buf);
   return 0;
 }
+/* ======================================================================== */
+/* adaptive time step (specs/hydro2d_adaptive.lf)                            */
+/* ======================================================================== */
+
+/* the CFL reduction over the interior of a state: cfl_init, then cfl_max of
+ * every cell's cfl_speed in loop order (j, i) -- run_naive's sequential sweep
+ * of the associative group -- and cfl_dt */
+static double cfl_dtdx(double* const U[4], long nj, long ni) {
+  const long P = ni + 4;
+  double m;
+  hy_cfl_init(&m);
+  for (long j = 0; j < nj; ++j)
+    for (long i = 0; i < ni; ++i) {
+      double sp;
+      hy_cfl_speed(AT(U[0], j, i), AT(U[1], j, i), AT(U[2], j, i), AT(U[3], j, i), &sp);
+      hy_cfl_max(m, sp, &m);
+    }
+  double d;
+  hy_cfl_dt(m, &d);
+  return d;
+}
+
+/* `steps` adaptive steps: step s runs with dt/dx_s (dtdx_io in: dt/dx_0), and
+ * dt/dx_{s+1} comes from the CFL condition on its result; dtdx_io out: the
+ * dt/dx the state after the last step gives (the chain's g_dtdx_n goal) */
+int lfo_hydro_adaptive(const double* const in[4], double* const out[4], long nj, long ni, double* dtdx_io, int steps,
+                       int fused, int threads) {
+  const size_t n = (size_t)(nj + 4) * (ni + 4);
+  if (threads <= 0) threads = omp_get_max_threads();
+  double* buf = (double*)malloc(8 * n * sizeof(double));
+  if (!buf) return 3;
+  double *A[4], *B[4];
+  for (int v = 0; v < 4; ++v) {
+    A[v] = buf + v * n;
+    B[v] = buf + (4 + v) * n;
+    memcpy(A[v], in[v], n * sizeof(double));
+  }
+  double dtdx = *dtdx_io;
+  for (int s = 0; s < steps; ++s) {
+    int st = fused ? (hydro_fused_step((const double* const*)A, B, nj, ni, dtdx, threads), 0)
+                   : lfo_hydro_naive((const double* const*)A, B, nj, ni, dtdx, 1);
+    if (st) {
+      free(buf);
+      return st;
+    }
+    dtdx = cfl_dtdx(B, nj, ni);
+    for (int v = 0; v < 4; ++v) {
+      double* t = A[v];
+      A[v] = B[v];
+      B[v] = t;
+    }
+  }
+  for (int v = 0; v < 4; ++v) memcpy(out[v], A[v], n * sizeof(double));
+  *dtdx_io = dtdx;
+  free(buf);
+  return 0;
+}
 #undef AT

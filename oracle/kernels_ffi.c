@@ -79,3 +79,23 @@ int lfk_box3(long n, void** args) {
   for (long e = 0; e < n; ++e) box3(F(0)[e], F(1)[e], F(2)[e], &F(3)[e]);
   return 0;
 }
+
+int lfk_hy_cfl_speed(long n, void** args) {
+  for (long e = 0; e < n; ++e) hy_cfl_speed(D(0)[e], D(1)[e], D(2)[e], D(3)[e], &D(4)[e]);
+  return 0;
+}
+
+int lfk_hy_cfl_init(long n, void** args) {
+  for (long e = 0; e < n; ++e) hy_cfl_init(&D(0)[e]);
+  return 0;
+}
+
+int lfk_hy_cfl_max(long n, void** args) {
+  for (long e = 0; e < n; ++e) hy_cfl_max(D(0)[e], D(1)[e], &D(2)[e]);
+  return 0;
+}
+
+int lfk_hy_cfl_dt(long n, void** args) {
+  for (long e = 0; e < n; ++e) hy_cfl_dt(D(0)[e], &D(1)[e]);
+  return 0;
+}

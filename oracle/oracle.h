@@ -65,6 +65,9 @@ int lfo_hydro_fused(const double* const in[4], double* const out[4], long nj, lo
                     double dtdx, int steps, int threads);
 int lfo_hydro_fused_step(const double* const in[4], double* const out[4], long nj, long ni,
                          double dtdx, int threads);
+/* configs 3/5 with the adaptive time step (specs/hydro2d_adaptive.lf) */
+int lfo_hydro_adaptive(const double* const in[4], double* const out[4], long nj, long ni, double* dtdx_io, int steps,
+                       int fused, int threads);
 
 int lfo_max_threads(void);
 

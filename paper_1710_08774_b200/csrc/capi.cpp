@@ -98,6 +98,8 @@ struct NcclApi {
   ncclResult_t (*group_end)() = nullptr;
   ncclResult_t (*send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*all_reduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                             cudaStream_t) = nullptr;
   ncclResult_t (*unique_id)(ncclUniqueId*) = nullptr;
   ncclResult_t (*init_rank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
   ncclResult_t (*init_all)(ncclComm_t*, int, const int*) = nullptr;
@@ -121,14 +123,15 @@ const NcclApi& nccl() {
     n.group_end = reinterpret_cast<decltype(n.group_end)>(sym("ncclGroupEnd"));
     n.send = reinterpret_cast<decltype(n.send)>(sym("ncclSend"));
     n.recv = reinterpret_cast<decltype(n.recv)>(sym("ncclRecv"));
+    n.all_reduce = reinterpret_cast<decltype(n.all_reduce)>(sym("ncclAllReduce"));
     n.unique_id = reinterpret_cast<decltype(n.unique_id)>(sym("ncclGetUniqueId"));
     n.init_rank = reinterpret_cast<decltype(n.init_rank)>(sym("ncclCommInitRank"));
     n.init_all = reinterpret_cast<decltype(n.init_all)>(sym("ncclCommInitAll"));
     n.destroy = reinterpret_cast<decltype(n.destroy)>(sym("ncclCommDestroy"));
     n.error_string = reinterpret_cast<decltype(n.error_string)>(sym("ncclGetErrorString"));
     if (!n.group_start || !n.group_end || !n.send || !n.recv || !n.unique_id || !n.init_rank || !n.init_all ||
-        !n.destroy)
-      n.error = "libnccl.so.2 lacks the point-to-point API";
+        !n.destroy || !n.all_reduce)
+      n.error = "libnccl.so.2 lacks the point-to-point / all-reduce API";
   });
   return n;
 }
@@ -150,6 +153,7 @@ struct SlabGeom {
   std::vector<int64_t> rb;
   std::vector<long> below, above;
   std::vector<char> periodic;
+  std::vector<int64_t> elem;       // element bytes per terminal
   long halo_lo = 0, halo_hi = 0;  // max ghost rows below / above over the iterated terminals
   long n0 = 0;
 };
@@ -165,6 +169,8 @@ SlabGeom slab_geom(const lf::Plan& P) {
   g.below.assign(T.size(), 0);
   g.above.assign(T.size(), 0);
   g.periodic.assign(T.size(), 0);
+  g.elem.assign(T.size(), 0);
+  for (size_t i = 0; i < T.size(); ++i) g.elem[i] = T[i].elem_bytes;
   for (const auto& [gname, aname] : rs.iterate)
     for (size_t i = 0; i < T.size(); ++i)
       for (size_t a = 0; a < T.size(); ++a)
@@ -199,7 +205,7 @@ struct RankState {
 std::vector<int64_t> scratch_need(const SlabGeom& g, const RankState& r) {
   std::vector<int64_t> need(g.paired.size(), 0);
   for (size_t i = 0; i < g.paired.size(); ++i)
-    if (g.paired[i] >= 0) need[i] = g.rb[i] * (r.hi - r.lo + g.below[i] + g.above[i]);
+    if (g.paired[i] >= 0) need[i] = g.rb[i] ? g.rb[i] * (r.hi - r.lo + g.below[i] + g.above[i]) : g.elem[i];
   return need;
 }
 
@@ -263,15 +269,27 @@ int slab_check(const lf_plan* plan, const SlabGeom& g, int world, std::string& e
 //                       best for thin slabs, but the faces then compete with the
 //                       interior for SM slots and HBM (heat3d 512^3: 0.79 of
 //                       the single-domain rate, against 0.96 for serial).
+// Executors with per-step MAX reductions (Executor::max_reduce, the adaptive
+// CFL time step): the rank-0 iterated goal slots are zeroed before each step
+// (the local ranks of one device share one slot), `combine` merges the ranks'
+// maxima after the step (NCCL MAX all-reduce; nullptr when the ranks share
+// the slot), and the executor finalises the last one into every rank's goal.
 int run_slabs_core(lf_plan* plan, const SlabGeom& g, std::vector<RankState>& R, int steps, cudaStream_t stream,
                    cudaStream_t side,
                    const std::function<int(std::vector<RankState>&, cudaStream_t, std::string&)>& exchange,
-                   std::string& err) {
+                   std::string& err,
+                   const std::function<int(void* slot, cudaStream_t, std::string&)>& combine = nullptr) {
   const size_t nt = g.paired.size();
+  const bool mr = plan->exec && plan->exec->max_reduce;
+  std::vector<size_t> scalars;  // rank-0 iterated goals
+  if (mr)
+    for (size_t i = 0; i < nt; ++i)
+      if (g.paired[i] >= 0 && !g.rb[i]) scalars.push_back(i);
   for (auto& r : R) r.cur.assign(r.terms, r.terms + nt);
   cudaEvent_t faces_done, exchanged;
   cudaEventCreateWithFlags(&faces_done, cudaEventDisableTiming);
   cudaEventCreateWithFlags(&exchanged, cudaEventDisableTiming);
+  int step_no = 0;
   auto launch = [&](RankState& r, long plo, long phi, cudaStream_t on) {
     lf_slab slab{r.lo, r.hi, g.n0, plo, phi};
     lfx::ExecArgs ea;
@@ -280,6 +298,7 @@ int run_slabs_core(lf_plan* plan, const SlabGeom& g, std::vector<RankState>& R, 
     ea.steps = 1;
     ea.stream = on;
     ea.slab = &slab;
+    ea.raw_max_input = mr && step_no > 0;
     return plan->exec ? plan->exec->run(ea, err) : plan->jit->run(ea, err);
   };
   // LF_SLAB_SCHEDULE: parallel (default) | serial | concurrent -- see above
@@ -303,11 +322,24 @@ int run_slabs_core(lf_plan* plan, const SlabGeom& g, std::vector<RankState>& R, 
   if (side2 != side) cudaStreamWaitEvent(side2, mark, 0);
   int st = LF_OK;
   for (int s = 0; s < steps && st == LF_OK; ++s) {
+    step_no = s;
     const bool to_goal = ((steps - 1 - s) % 2) == 0;
     for (auto& r : R) {
       r.bufs = r.cur;
       for (size_t i = 0; i < nt; ++i)
         if (plan->plan.terminals[i].is_goal) r.bufs[i] = (to_goal || g.paired[i] < 0) ? r.terms[i] : r.scratch[i];
+    }
+    if (!scalars.empty()) {
+      for (size_t i : scalars) {
+        for (auto& r : R) r.bufs[i] = R[0].bufs[i];  // one accumulation slot per device
+        if (cudaMemsetAsync(R[0].bufs[i], 0, g.elem[i], stream) != cudaSuccess) {
+          err = "cudaMemsetAsync(reduction slot) failed";
+          st = LF_ERR_CUDA;
+        }
+      }
+      cudaEventRecord(mark, stream);  // the faces start after the zeroing
+      cudaStreamWaitEvent(side, mark, 0);
+      if (side2 != side) cudaStreamWaitEvent(side2, mark, 0);
     }
     std::vector<char> split(R.size());
     const cudaStream_t top = sched == 1 ? stream : side, bottom = sched == 1 ? stream : side2;
@@ -336,6 +368,9 @@ int run_slabs_core(lf_plan* plan, const SlabGeom& g, std::vector<RankState>& R, 
     for (size_t k = 0; k < R.size() && st == LF_OK; ++k)
       if (split[k]) st = launch(R[k], g.halo_hi, R[k].hi - R[k].lo - g.halo_lo, stream);
     cudaStreamWaitEvent(stream, exchanged, 0);
+    if (combine)
+      for (size_t i : scalars)
+        if (st == LF_OK) st = combine(R[0].bufs[i], stream, err);
     if (sched != 1) {  // next step's faces: after this step's interior (input rows, ping-pong buffer)
       cudaEventRecord(mark, stream);
       cudaStreamWaitEvent(side, mark, 0);
@@ -344,6 +379,22 @@ int run_slabs_core(lf_plan* plan, const SlabGeom& g, std::vector<RankState>& R, 
     for (auto& r : R)
       for (size_t i = 0; i < nt; ++i)
         if (g.paired[i] >= 0) r.cur[g.paired[i]] = r.bufs[i];
+  }
+  if (st == LF_OK && !scalars.empty()) {
+    // the last step wrote the goal slot of rank 0: finalise, then hand every
+    // other local rank its copy
+    lfx::ExecArgs ea;
+    ea.plan = &plan->plan;
+    ea.terms = R[0].terms;
+    ea.stream = stream;
+    if (plan->exec->finalize) st = plan->exec->finalize(ea, err);
+    for (size_t k = 1; k < R.size() && st == LF_OK; ++k)
+      for (size_t i : scalars)
+        if (cudaMemcpyAsync(R[k].terms[i], R[0].terms[i], g.elem[i], cudaMemcpyDeviceToDevice, stream) !=
+            cudaSuccess) {
+          err = "cudaMemcpyAsync(reduction result) failed";
+          st = LF_ERR_CUDA;
+        }
   }
   cudaEventDestroy(mark);
   cudaEventDestroy(face2);
@@ -747,7 +798,8 @@ int lf_run_host(const lf_plan* cplan, void* const* terms, int nterm, int steps) 
       const bool nests = plan->jit && !plan->jit->program().nest_kernels.empty();
       int parts = static_cast<int>(std::min<long>(32, n0 / 512));  // 32: measured best for the 16384^2 box pass
       if (const char* e = std::getenv("LF_HOST_PARTS")) parts = std::atoi(e);
-      if (steps == 1 && !inplace && !nests && parts >= 2) {
+      const bool reduces = plan->exec && plan->exec->max_reduce;
+      if (steps == 1 && !inplace && !nests && !reduces && parts >= 2) {
         st = run_host_pipelined(plan, terms, dterms, parts, err);
         if (st != LF_OK) return fail(st, err);
         return LF_OK;
@@ -793,6 +845,10 @@ int lf_run_slab(const lf_plan* cplan, void* const* terms, int nterm, const lf_sl
     if (slab->part_hi == slab->part_lo && slab->part_lo != 0) return LF_OK;  // empty part
     if (shares_buffer(cplan, terms))
       return fail(LF_ERR_UNSUPPORTED, "slab runs need distinct axiom and goal buffers (in-place runs cover the whole domain)");
+    if (cplan->exec && cplan->exec->max_reduce)
+      return fail(LF_ERR_UNSUPPORTED, "this chain reduces over the whole grid every step (" +
+                                          std::string(cplan->exec->name) +
+                                          "): run its slabs through lf_run_slabs / lf_run_slabs_local");
     // the generic executor's lazily created state (module, bands) is per plan
     std::lock_guard<std::mutex> lk(const_cast<lf_plan*>(cplan)->mu);
     lfx::ExecArgs a;
@@ -923,7 +979,12 @@ int lf_run_slabs(const lf_plan* cplan, void* comm, int rank, int world, void* co
       int s3 = nccl_status(n.group_end(), "ncclGroupEnd", e);
       return s2 != LF_OK ? s2 : s3;
     };
-    st = run_slabs_core(plan, g, R, steps, stream, plan->comm, exchange, err);
+    // per-step MAX reductions (the adaptive CFL time step): one all-reduce of
+    // the rank's raw maximum, in place, before the next step reads it
+    auto combine = [&](void* slot, cudaStream_t on, std::string& e) {
+      return nccl_status(n.all_reduce(slot, slot, 1, ncclFloat64, ncclMax, c, on), "ncclAllReduce", e);
+    };
+    st = run_slabs_core(plan, g, R, steps, stream, plan->comm, exchange, err, combine);
     if (st != LF_OK) return fail(st, err);
     return LF_OK;
   } catch (const std::exception& e) {

@@ -24,6 +24,9 @@ struct ExecArgs {
   const lf_slab* slab = nullptr;  // nullptr: the whole domain
   void* const* scratch = nullptr;  // per iterated goal, same layout (steps > 1)
   bool whole_domain_parts = false;  // slab = the whole domain, computed in row parts (pipelined host run)
+  // max_reduce executors under a slab driver: the rank-0 iterated axioms hold
+  // the previous step's (combined) raw maxima, not final values
+  bool raw_max_input = false;
 };
 
 struct Executor {
@@ -38,6 +41,12 @@ struct Executor {
   // passes over the grid `steps` steps take (temporal blocking fuses several
   // steps into one pass); nullptr: one pass per step
   int (*passes)(const lf::Plan&, int steps, bool slab) = nullptr;
+  // rank-0 iterated goals are per-step MAX reductions over the cells (the
+  // CFL time step): under a slab driver they are zeroed before each step,
+  // combined across ranks after it (MAX), and `finalize` turns the last raw
+  // maximum into the goal's value; a whole-domain run() does all of it itself
+  bool max_reduce = false;
+  int (*finalize)(const ExecArgs&, std::string& err) = nullptr;
 };
 
 // all executors compiled into this library

@@ -106,6 +106,12 @@ __device__ __noinline__ D8 slow_trace(double r, double n, double t, double p, do
   return o;
 }
 
+__device__ __noinline__ double slow_cfl_speed(double r, double mx, double my, double e) {
+  double sp;
+  hy_cfl_speed(r, mx, my, e, &sp);
+  return sp;
+}
+
 struct Params {
   int ni, nj;            // interior of this launch's domain (slab rows for multi-GPU)
   int row_lo, row_hi;    // rows this launch computes
@@ -113,7 +119,9 @@ struct Params {
   int strips;
   int ghost_top, ghost_bottom;  // refill reflective ghost rows at these faces
   unsigned force_slow;          // 1: take every exact fallback (LF_HYDRO_FORCE_SLOW, tests)
-  const double* dtdx;    // rank-0 terminal g_dtdx
+  const double* dtdx;    // rank-0 terminal g_dtdx (or, adaptive, the previous step's CFL maximum)
+  int dtdx_is_max;       // adaptive steps after the first: dt/dx = CFL / *dtdx
+  unsigned long long* cfl_acc;  // adaptive: this step's CFL maximum (double bits, atomicMax; zeroed by the host)
   double* out[4];
 };
 
@@ -155,7 +163,8 @@ __device__ __forceinline__ void store_cell(const Params& p, int j, int i, const 
   }
 }
 
-template <int MINB>
+// ADAPT: also reduce the CFL speed of every stored cell (specs/hydro2d_adaptive.lf)
+template <int MINB, bool ADAPT = false>
 __global__ void __launch_bounds__(NT, MINB) hydro_fused(const __grid_constant__ Maps maps, const Params p) {
   extern __shared__ __align__(128) unsigned char smem[];
   unsigned char* ring = smem;
@@ -168,7 +177,8 @@ __global__ void __launch_bounds__(NT, MINB) hydro_fused(const __grid_constant__ 
   const int t = threadIdx.x;
   if (t == 0) pdl_trigger();
   pdl_wait();  // previous step's output (our input) complete, our output buffer free
-  const double dtdx = *p.dtdx;
+  const double dtdx = ADAPT && p.dtdx_is_max ? HY_CFL / *p.dtdx : *p.dtdx;  // hy_cfl_dt of the previous step
+  double cfl = 0.0;  // ADAPT: fastest signal speed over the cells this thread stored
 
   // ---- segment list (strip-major row ranges) and stage bookkeeping
   RowSeg seg[3];
@@ -321,6 +331,13 @@ __global__ void __launch_bounds__(NT, MINB) hydro_fused(const __grid_constant__ 
             hy_update(u1c[0], u1c[2 * NT], u1c[NT], u1c[3 * NT], yfp[0], yfp[1], yfp[2], yfp[3], f[0], f[1], f[2], f[3],
                       dtdx, &o[0], &o[2], &o[1], &o[3]);
             store_cell(p, sg.jb - 2 + tt - 3, i0 + t, o);
+            if constexpr (ADAPT) {
+              double sp;
+              unsigned bs = p.force_slow;
+              hf::hy_cfl_speed(o[0], o[1], o[2], o[3], &sp, &bs);
+              if (bs) sp = slow_cfl_speed(o[0], o[1], o[2], o[3]);
+              cfl = hy_max(cfl, sp);
+            }
           }
 #pragma unroll
           for (int a = 0; a < 4; ++a) yfp[a] = f[a];
@@ -378,6 +395,13 @@ __global__ void __launch_bounds__(NT, MINB) hydro_fused(const __grid_constant__ 
       }
     }
   }
+  if constexpr (ADAPT) {
+    // the maximum is exact in any order: one atomic per warp on the bit
+    // pattern (non-negative doubles order like their bits)
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) cfl = hy_max(cfl, __shfl_xor_sync(0xffffffffu, cfl, o));
+    if ((t & 31) == 0) atomicMax(p.cfl_acc, static_cast<unsigned long long>(__double_as_longlong(cfl)));
+  }
 }
 
 bool supports(const lf::Plan& plan, std::string& why) {
@@ -396,8 +420,11 @@ bool supports(const lf::Plan& plan, std::string& why) {
   return true;
 }
 
+// dt/dx from the CFL maximum in place (hy_cfl_dt): the chain's g_dtdx_n goal
+__global__ void cfl_finalize(double* slot) { hy_cfl_dt(*slot, slot); }
+
 int launch_step(const double* const in[4], double* const out[4], const double* dtdx, int ni, const RowPart& rp,
-                cudaStream_t st, std::string& err) {
+                cudaStream_t st, std::string& err, unsigned long long* cfl_acc = nullptr, bool dtdx_is_max = false) {
   const int nj = rp.rows;
   // LF_HYDRO_VARIANT: register budget for 2 / 3 (default) / 4 CTAs per SM.
   // With the branch-free divisions the Riemann phase keeps the fp64 pipe busy
@@ -408,10 +435,11 @@ int launch_step(const double* const in[4], double* const out[4], const double* d
     const int var = v ? std::atoi(v) : 1;
     return var == 0 ? hydro_fused<2> : (var == 2 ? hydro_fused<4> : hydro_fused<3>);
   }();
-  static LaunchCache cache;
+  void (*const k)(Maps, Params) = cfl_acc ? hydro_fused<3, true> : kern;
+  static LaunchCache cache, cache_adapt;
   int slots = 0;
-  if (int s = resident_slots(cache, reinterpret_cast<const void*>(kern), NT, SMEM, 0, "cudaFuncSetAttribute(hydro)",
-                             &slots, err))
+  if (int s = resident_slots(cfl_acc ? cache_adapt : cache, reinterpret_cast<const void*>(k), NT, SMEM, 0,
+                             "cudaFuncSetAttribute(hydro)", &slots, err))
     return s;
   Maps maps;
   uint64_t dims[2] = {(uint64_t)ni + 4, (uint64_t)nj + 4};
@@ -429,6 +457,8 @@ int launch_step(const double* const in[4], double* const out[4], const double* d
   p.ghost_top = rp.top;
   p.ghost_bottom = rp.bottom;
   p.dtdx = dtdx;
+  p.dtdx_is_max = dtdx_is_max ? 1 : 0;
+  p.cfl_acc = cfl_acc;
   static const unsigned force_slow = std::getenv("LF_HYDRO_FORCE_SLOW") ? 1u : 0u;
   p.force_slow = force_slow;
   for (int a = 0; a < 4; ++a) p.out[a] = out[a];
@@ -441,7 +471,7 @@ int launch_step(const double* const in[4], double* const out[4], const double* d
     err = "row range too short for the resident grid";
     return LF_ERR_UNSUPPORTED;
   }
-  return cuda_status(launch_pdl(kern, dim3(ctas), dim3(NT), SMEM, st, maps, p), "hydro_fused launch", err);
+  return cuda_status(launch_pdl(k, dim3(ctas), dim3(NT), SMEM, st, maps, p), "hydro_fused launch", err);
 }
 
 int run(const ExecArgs& a, std::string& err) {
@@ -467,8 +497,56 @@ int run(const ExecArgs& a, std::string& err) {
   return LF_OK;
 }
 
+// Adaptive time step (specs/hydro2d_adaptive.lf, terminals g_rho g_mx g_my g_E
+// g_dtdx | g_rho_n g_mx_n g_my_n g_E_n g_dtdx_n).  Each step reduces the CFL
+// maximum of its new state into its dt/dx goal slot (zeroed first); the next
+// step divides it into dt/dx itself.  On a whole domain the last slot is
+// finalised here; a slab driver (lf_run_slabs) zeroes, combines the ranks'
+// maxima (MAX all-reduce) and finalises itself -- Executor::max_reduce.
+int run_adaptive(const ExecArgs& a, std::string& err) {
+  const auto& r = a.plan->rs.ranges;
+  const int ni = (int)r[1].trips();
+  const RowPart rp = row_part(a, (int)r[0].trips());
+  const double* src[4];
+  double* goal[4];
+  double* scr[4] = {nullptr, nullptr, nullptr, nullptr};
+  for (int v = 0; v < 4; ++v) {
+    src[v] = static_cast<const double*>(a.terms[v]);
+    goal[v] = static_cast<double*>(a.terms[5 + v]);
+    if (a.steps > 1) scr[v] = static_cast<double*>(a.scratch[v]);
+  }
+  const double* dsrc = static_cast<const double*>(a.terms[4]);
+  double* dgoal = static_cast<double*>(a.terms[9]);
+  double* dscr = a.steps > 1 ? static_cast<double*>(a.scratch[4]) : nullptr;
+  if (a.slab)  // one step of a slab driver's schedule: no zeroing, no finalising here
+    return launch_step(src, goal, dsrc, ni, rp, a.stream, err, reinterpret_cast<unsigned long long*>(dgoal),
+                       a.raw_max_input);
+  bool is_max = false;
+  for (int s = 0; s < a.steps; ++s) {
+    const bool to_goal = ((a.steps - 1 - s) % 2) == 0;
+    double* const* dst = to_goal ? goal : scr;
+    double* dd = to_goal ? dgoal : dscr;
+    cudaError_t e = cudaMemsetAsync(dd, 0, sizeof(double), a.stream);
+    if (e != cudaSuccess) return cuda_status(e, "cudaMemsetAsync(cfl)", err);
+    int stt = launch_step(src, dst, dsrc, ni, rp, a.stream, err, reinterpret_cast<unsigned long long*>(dd), is_max);
+    if (stt != LF_OK) return stt;
+    for (int v = 0; v < 4; ++v) src[v] = dst[v];
+    dsrc = dd;
+    is_max = true;
+  }
+  cfl_finalize<<<1, 1, 0, a.stream>>>(dgoal);
+  return cuda_status(cudaGetLastError(), "cfl_finalize launch", err);
+}
+
+int finalize_adaptive(const ExecArgs& a, std::string& err) {
+  cfl_finalize<<<1, 1, 0, a.stream>>>(static_cast<double*>(a.terms[9]));
+  return cuda_status(cudaGetLastError(), "cfl_finalize launch", err);
+}
+
 }  // namespace
 
 extern const Executor hydro_executor = {"hydro2d_fused_tma", "hydro2d.lf", 1, 64.0, supports, run};
+extern const Executor hydro_adaptive_executor = {"hydro2d_adaptive_fused_tma", "hydro2d_adaptive.lf", 1, 64.0,
+                                                 supports, run_adaptive, nullptr, true, finalize_adaptive};
 
 }  // namespace lfx

@@ -260,4 +260,21 @@ LF_HD void hy_update(double r, double mn, double mt, double e, double frm, doubl
   *eo = fma(dtdx, fem - fep, e);
 }
 
+/* ---- adaptive time step (specs/hydro2d_adaptive.lf): the CFL condition ---- */
+#ifndef HY_CFL
+#define HY_CFL 0.5
+#endif
+
+/* fastest signal speed of a cell, max(|u|, |v|) + c with c = sqrt(gamma p / rho) */
+LF_HD void hy_cfl_speed(double r, double mx, double my, double e, double* s HY_BAD_PARAM) {
+  double qr, qu, qv, qp;
+  hy_constoprim(r, mx, my, e, &qr, &qu, &qv, &qp HY_BAD_ARG);
+  const double c = HY_SQRT((HY_GAMMA * qp) * HY_RCP(qr));
+  *s = hy_max(fabs(qu), fabs(qv)) + c;
+}
+/* the reduction: seed, combine (exact and order-independent), and dt/dx */
+LF_HD void hy_cfl_init(double* m) { *m = 0.0; }
+LF_HD void hy_cfl_max(double c, double s, double* o) { *o = hy_max(c, s); }
+LF_HD void hy_cfl_dt(double m, double* d) { *d = HY_CFL / m; }
+
 #endif

@@ -125,3 +125,21 @@ def test_generic_named_hydro_matches_c_oracle(shape, steps, tmp_path):
     ref = oracle.hydro(st, dtdx, steps)
     for v, name in enumerate(("g_rho_n", "g_mx_n", "g_my_n", "g_E_n")):
         assert np.array_equal(g[name].view(np.uint64), ref[v].view(np.uint64)), name
+
+
+@pytest.mark.parametrize("shape,steps", [((12, 20), 3), ((9, 14), 2)])
+def test_generic_adaptive_hydro_matches_c_oracle(shape, steps, tmp_path):
+    """The adaptive-dt chain (specs/hydro2d_adaptive.lf): the CFL speed, an
+    associative MAX reduction seeded by a kernel with no inputs, and the dt/dx
+    broadcast through an iterate pair -- run_naive over the reference's DAG
+    equals the C oracle's fused step + sequential reduction, dt/dx included."""
+    need_ref()
+    spec = tmp_path / "hydro2d_adaptive.lf"
+    spec.write_text(lf.set_ranges(lf.spec_path("hydro2d_adaptive").read_text(), shape))
+    st, dtdx = inputs.hydro_input(*shape, seed=shape[0])
+    ax = {"g_rho": st[0], "g_mx": st[1], "g_my": st[2], "g_E": st[3], "g_dtdx": np.array([dtdx])}
+    g = generic.run_naive(spec, ax, steps=steps)
+    ref, dref = oracle.hydro_adaptive(st, dtdx, steps)
+    for v, name in enumerate(("g_rho_n", "g_mx_n", "g_my_n", "g_E_n")):
+        assert np.array_equal(g[name].view(np.uint64), ref[v].view(np.uint64)), name
+    assert float(g["g_dtdx_n"].reshape(-1)[0]) == dref

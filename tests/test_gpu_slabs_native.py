@@ -26,8 +26,8 @@ def _case(name, shape):
     elif name == "biharm":
         plan = lf.Plan.with_ranges("biharmonic2d", shape)
         ax = [inputs.biharm_input(*shape, seed=4)]
-    elif name == "hydro":
-        plan = lf.Plan.with_ranges("hydro2d", shape)
+    elif name in ("hydro", "hydro_adaptive"):
+        plan = lf.Plan.with_ranges("hydro2d" if name == "hydro" else "hydro2d_adaptive", shape)
         st, dtdx = inputs.hydro_input(*shape, seed=5)
         ax = list(st) + [np.array(dtdx, dtype=np.float64)]
     elif name == "heat3d_jit":
@@ -75,6 +75,11 @@ def _assemble(plan, rank_bufs, ranges, n0):
     out = []
     na = len(plan.axioms)
     for k, t in enumerate(plan.goals):
+        if not t.extent:  # a rank-0 goal (the adaptive chain's dt/dx): every rank holds the same value
+            vals = [bufs[na + k].cpu().numpy() for bufs in rank_bufs]
+            assert all(np.array_equal(v, vals[0]) for v in vals)
+            out.append(vals[0])
+            continue
         below = -t.base[0]
         above = t.extent[0] - n0 - below
         g = np.empty(t.extent)
@@ -116,6 +121,7 @@ CASES = [
     ("heat3d", (9, 32, 64), 2, [4]),
     ("biharm", (30, 64), 3, [2, 3]),
     ("hydro", (24, 64), 2, [2, 3]),
+    ("hydro_adaptive", (24, 64), 3, [2, 3]),  # + one MAX reduction per step across the ranks
     ("heat3d_jit", (10, 12, 40), 3, [2]),
     ("biharm_jit", (26, 70), 2, [3]),
 ]
@@ -140,7 +146,8 @@ def test_local_slab_decomposition_matches_whole_domain(name, shape, steps, world
 
 
 @pytest.mark.parametrize("name,shape,steps", [("heat3d", (12, 16, 40), 3), ("biharm", (30, 64), 2),
-                                              ("hydro", (16, 48), 3), ("heat3d_jit", (8, 12, 40), 2)])
+                                              ("hydro", (16, 48), 3), ("hydro_adaptive", (16, 48), 3),
+                                              ("heat3d_jit", (8, 12, 40), 2)])
 def test_nccl_one_rank_matches_whole_domain(name, shape, steps):
     import torch
     plan, ax = _case(name, shape)

@@ -108,3 +108,15 @@ def test_hydro_row_band_cone_equals_the_whole_grid(band):
     hi = b + 2 + (2 if b == n else 0)
     for v in range(4):
         assert np.array_equal(whole[v][lo:hi].view(np.uint64), ref[v][lo - A:hi - A].view(np.uint64))
+
+
+@pytest.mark.parametrize("nj,ni,steps,threads", [(8, 8, 1, 1), (16, 24, 3, 3), (33, 17, 2, 4)])
+def test_hydro_adaptive_naive_equals_fused(nj, ni, steps, threads):
+    st, dtdx = inputs.hydro_input(nj, ni, seed=nj + ni)
+    a, da = oracle.hydro_adaptive(st, dtdx, steps)
+    b, db = oracle.hydro_adaptive(st, dtdx, steps, fused=True, threads=threads)
+    assert all(bits_equal(x, y) for x, y in zip(a, b)) and da == db
+    # one adaptive step with the initial dt/dx is the fixed-dt step
+    f = oracle.hydro(st, dtdx, 1)
+    c, _ = oracle.hydro_adaptive(st, dtdx, 1)
+    assert all(bits_equal(x, y) for x, y in zip(f, c))

@@ -81,6 +81,17 @@ def numerics():
     finally:
         tmp.unlink()
     ref = [g[n] for n in ("g_rho_n", "g_mx_n", "g_my_n", "g_E_n")]
+    # ... and the adaptive-dt chain (CFL reduction, rank-0 dt/dx goal), 3 steps
+    tmp.write_text(lf.set_ranges(lf.spec_path("hydro2d_adaptive").read_text(), sizes))
+    try:
+        ga = generic.run_naive(tmp, {"g_rho": st[0], "g_mx": st[1], "g_my": st[2], "g_E": st[3],
+                                     "g_dtdx": np.array([dtdx])}, steps=3)
+    finally:
+        tmp.unlink()
+    np.savez_compressed(out / "hydro_adaptive.npz", sizes=np.array(sizes), steps=np.array(3), dtdx=np.array([dtdx]),
+                        **{f"in_{v}": st[v] for v in range(4)},
+                        **{f"out_{v}": ga[n] for v, n in enumerate(("g_rho_n", "g_mx_n", "g_my_n", "g_E_n"))},
+                        out_dtdx=np.asarray(ga["g_dtdx_n"]).reshape(1))
     np.savez_compressed(out / "hydro.npz", sizes=np.array((12, 20)), steps=np.array(2), dtdx=np.array([dtdx]),
                         **{f"in_{v}": st[v] for v in range(4)}, **{f"out_{v}": ref[v] for v in range(4)})
 
