@@ -95,6 +95,10 @@ WORKLOADS = {
     # BASELINE.json configs[4] -- the default bench line (the metric's 1/2/4/8-GPU grid)
     "hydro_large": dict(config_index=4, spec="hydro2d", sizes=(32768, 32768), chain_steps=10,
                         gen=_hydro_inputs, slab=_hydro_slab, dtype="f64", halo=(2, 2, False)),
+    # configs[4] with the adaptive CFL time step (specs/hydro2d_adaptive.lf): one
+    # MAX reduction per step fused into the executor (+ an all-reduce per step on N GPUs)
+    "hydro_large_adaptive": dict(config_index=None, spec="hydro2d_adaptive", sizes=(32768, 32768), chain_steps=10,
+                                 gen=_hydro_inputs, slab=_hydro_slab, dtype="f64", halo=(2, 2, False)),
     # the same chains written with `body:` expressions: the generic NVRTC path
     "heat3d_jit": dict(config_index=1, spec="examples/heat3d_body", sizes=(512, 512, 512), chain_steps=50,
                        gen=_heat3d_inputs, slab=_heat3d_slab, dtype="f64", halo=(1, 1, True)),
@@ -142,10 +146,11 @@ def measured_fp64_peak():
 
 
 def ncu_pipe(workload):
-    """fp64-pipe and issue-slot utilisation of the kernel from its committed ncu summary"""
-    p = ROOT / "profiles" / f"r01_{workload}_ncu.json"
-    if not p.exists():
+    """fp64-pipe and issue-slot utilisation of the kernel from its newest committed ncu summary"""
+    cands = sorted((ROOT / "profiles").glob(f"r0*_{workload}_ncu.json"))
+    if not cands:
         return None
+    p = cands[-1]
     d = json.loads(p.read_text())
     return {"fp64_pipe_pct": d.get("sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active"),
             "issue_active_pct": d.get("sm__issue_active.avg.pct_of_peak_sustained_elapsed"),
@@ -232,7 +237,7 @@ def cpu_runner(name, w, naive=False):
     every intermediate materialised, one thread).  Both from oracle/ built with
     -march=native on this host.  Returns (run, cell-updates per run, threads, text)."""
     import oracle
-    name = name.replace("_jit", "").replace("_inplace", "").replace("_large", "")
+    name = name.replace("_jit", "").replace("_inplace", "").replace("_large", "").replace("_adaptive", "")
     threads = 1 if naive else oracle.max_threads()
     sizes = w["sizes"]
     if naive:
@@ -563,7 +568,7 @@ def main():
                 "traffic": ncu_traffic(args.config), "peak_source": peak_src,
                 "algorithmic_bytes_per_cell": bpc, "cell_updates_per_pass": w["chain_steps"] / max(1, passes),
                 "passes": passes}
-    if w["spec"] == "hydro2d":
+    if w["spec"].startswith("hydro2d"):
         # compute-bound chain: the fp64 roofline is the binding one; HBM kept beside it
         fpk = measured_fp64_peak()
         tf = HYDRO_FLOPS_PER_CELL_STEP * cells_local * w["chain_steps"] / (ms / 1e3) / 1e12
@@ -575,7 +580,7 @@ def main():
                             "algorithmic_bytes_per_cell": bpc, "peak_source": peak_src},
                     # each division / square root is ~10 fp64-pipe instructions: the
                     # pipe itself is far busier than the algorithmic-flop fraction
-                    "pipe": ncu_pipe("hydro")}
+                    "pipe": ncu_pipe(args.config)}
 
     line = {
         "metric": metric, "value": value, "unit": "cell-updates/s", "n_gpus": world, "steps": args.steps,
