@@ -302,12 +302,22 @@ int run_slabs_core(lf_plan* plan, const SlabGeom& g, std::vector<RankState>& R, 
     return plan->exec ? plan->exec->run(ea, err) : plan->jit->run(ea, err);
   };
   // LF_SLAB_SCHEDULE: parallel (default) | serial | concurrent -- see above
-  static const int sched = [] {
+  static const int sched_env = [] {
     const char* e = std::getenv("LF_SLAB_SCHEDULE");
     if (e && std::string(e) == "serial") return 1;
     if (e && std::string(e) == "concurrent") return 2;
-    return 0;
+    if (e && std::string(e) == "whole") return 3;
+    if (e && std::string(e) == "parallel") return 0;
+    return -1;
   }();
+  // default: `whole` (one launch per rank and step, then the exchange) when a
+  // step's compute dwarfs the face launches it would otherwise split off --
+  // a pipeline fill of a few rows per launch and a partly idle grid -- i.e.
+  // for slabs of many rows; `parallel` for thin slabs, whose exchange is worth
+  // hiding behind the interior (tools/slab_probe.py, profiles/r02_slab_schedules.txt)
+  long min_rows = g.n0;
+  for (const auto& r : R) min_rows = std::min(min_rows, r.hi - r.lo);
+  const int sched = sched_env >= 0 ? sched_env : (min_rows >= 1024 ? 3 : 0);
   cudaStream_t side2 = side;
   if (sched == 0) {
     if (!plan->comm2 && make_side_stream(&plan->comm2, err) != LF_OK) return LF_ERR_CUDA;
@@ -340,6 +350,22 @@ int run_slabs_core(lf_plan* plan, const SlabGeom& g, std::vector<RankState>& R, 
       cudaEventRecord(mark, stream);  // the faces start after the zeroing
       cudaStreamWaitEvent(side, mark, 0);
       if (side2 != side) cudaStreamWaitEvent(side2, mark, 0);
+    }
+    if (sched == 3) {  // whole: one launch per rank, then the exchange, the next step after it
+      for (size_t k = 0; k < R.size() && st == LF_OK; ++k) st = launch(R[k], 0, R[k].hi - R[k].lo, stream);
+      if (st != LF_OK) break;
+      cudaEventRecord(faces_done, stream);
+      cudaStreamWaitEvent(side, faces_done, 0);
+      if ((st = exchange(R, side, err)) != LF_OK) break;
+      cudaEventRecord(exchanged, side);
+      cudaStreamWaitEvent(stream, exchanged, 0);
+      if (combine)
+        for (size_t i : scalars)
+          if (st == LF_OK) st = combine(R[0].bufs[i], stream, err);
+      for (auto& r : R)
+        for (size_t i = 0; i < nt; ++i)
+          if (g.paired[i] >= 0) r.cur[g.paired[i]] = r.bufs[i];
+      continue;
     }
     std::vector<char> split(R.size());
     const cudaStream_t top = sched == 1 ? stream : side, bottom = sched == 1 ? stream : side2;

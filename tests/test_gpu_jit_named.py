@@ -102,3 +102,37 @@ def test_caller_kernel_source():
     (got,) = run(plan, [u], 2)
     ref = generic.run_naive(SPECS / "biharm_body.lf", {"g_u": u}, steps=2)["g_unew"]
     assert np.array_equal(bits(got), bits(ref))
+
+
+# the user's own kernels of the paper's normalization example (R/PAPER.md:66),
+# passed as CUDA source with the plan (the rule file only names them)
+NORMALIZATION_KERNELS = """
+__device__ void flux(double a, double b, double* f) { *f = (b - a) * (b - a); }
+__device__ void accinit(double z, double* a) { *a = z; }
+__device__ void accum(double c, double f, double* o) { *o = c + f; }
+__device__ void root(double t, double* r) { *r = sqrt(t); }
+__device__ void normalize(double f, double r, double* o) { *o = f / r; }
+"""
+
+
+@pytest.mark.parametrize("shape", [(64, 128), (37, 300), (5, 1000)])
+def test_paper_normalization_as_written(shape, tmp_path):
+    """tests/specs/normalization.lf exactly as the paper writes it -- five
+    declaration-only kernels, a reduction over i, its root and a broadcast
+    divide: 2 nests, 1 split (R/SPEC.md:633) -- runs on the generic
+    executor's multi-nest path with the caller's kernel source, bit-exact
+    against run_naive over the reference's DAG of the same rules (their
+    `body:` twins in normalization_body.lf)."""
+    named = lf.set_ranges((SPECS / "normalization.lf").read_text(), shape)
+    plan = lf.Plan(named, "normalization.lf", kernel_source=NORMALIZATION_KERNELS)
+    r = plan.report()
+    assert (r["nests"], r["splits"]) == (2, 1)
+    assert plan.executor == "jit_nests_fused"
+    rng = np.random.default_rng(shape[1])
+    q = rng.random((shape[0], shape[1] + 1))
+    z = np.zeros(shape[0])
+    got = run(plan, [q, z], 1)[0]
+    body = tmp_path / "normalization_body.lf"
+    body.write_text(lf.set_ranges((SPECS / "normalization_body.lf").read_text(), shape))
+    ref = generic.run_naive(body, {"g_q": q, "g_zero": z}, steps=1)["g_out"]
+    assert np.array_equal(bits(got), bits(ref))
