@@ -63,10 +63,17 @@ __constant__ double kGamma = HY_GAMMA, kGm1 = HY_GM1, kGk = HY_GK, kSmallR = HY_
 }  // namespace hf
 namespace {
 
-constexpr int NT = 128;                // threads per CTA = x-faces per row
+#ifndef LF_HYDRO_NT
+#define LF_HYDRO_NT 128
+#endif
+#ifndef LF_HYDRO_UNROLL
+#define LF_HYDRO_UNROLL 2
+#endif
+constexpr int NT = LF_HYDRO_NT;         // threads per CTA = x-faces per row
+constexpr int UNROLL = LF_HYDRO_UNROLL; // Newton steps per unrolled loop body
 constexpr int W = NT - 4;              // cells per strip
 constexpr int H = 2;                   // radius of each sweep
-constexpr int BOXW = 132;              // staged columns from the even storage column <= i0 (131 used)
+constexpr int BOXW = NT + 4;           // staged columns from the even storage column <= i0 (NT + 3 used)
 constexpr int R = 2;                   // rows per stage
 constexpr int S = 2;                   // ring slots (compute per row >> load latency)
 constexpr int ARR_TX = BOXW * R * 8;   // bytes TMA delivers per array per stage
@@ -299,7 +306,7 @@ __global__ void __launch_bounds__(NT, MINB) hydro_fused(const __grid_constant__ 
         double psx = hf::hy_riemann_init(xp[fx], xp[NQ + fx], xp[3 * NQ + fx], xm[fx + 1], xm[NQ + fx + 1],
                                          xm[3 * NQ + fx + 1], &cx, &bx);
         double psy = hf::hy_riemann_init(ypo[0], ypo[1], ypo[3], yqm[0], yqm[1], yqm[3], &cy, &by);
-#pragma unroll 2
+#pragma unroll UNROLL
         for (int it = 0; it < HY_NITER; ++it) {
           psx = hf::hy_riemann_newton(&cx, psx, &bx);
           psy = hf::hy_riemann_newton(&cy, psy, &by);
