@@ -678,15 +678,18 @@ int lf_run(const lf_plan* cplan, void* const* terms, int nterm, int steps, void*
   }
 }
 
-// Single-step host runs, pipelined: the outer dimension is cut into parts;
-// part p's input rows go up on one copy stream, the part is computed on the
-// plan's stream as soon as they (and the halo) have landed, and its finished
-// output rows come down on a second copy stream -- both PCIe directions and
-// the SMs busy at once instead of one after the other.  Every executor
-// computes row parts (lf_slab part ranges); ghost rows of the goals are
-// copied once all parts are done.
+// Host runs of large grids, pipelined: the outer dimension is cut into parts.
+// The FIRST step computes part p as soon as its input rows (and the halo above
+// them) have come up on one copy stream; the LAST step sends part p's finished
+// rows down on a second copy stream while part p+1 is computed; the steps in
+// between are whole-domain launches.  So the PCIe transfers overlap the first
+// and the last step's compute (for one step: both directions and the SMs at
+// once) instead of preceding and following the whole run.  Every executor
+// computes row parts (lf_slab part ranges); iterated state ping-pongs through
+// the plan's scratch so the last step lands in the goals; ghost rows of the
+// goals are copied once all parts are done.
 static int run_host_pipelined(lf_plan* plan, void* const* terms, const std::vector<void*>& dterms, int parts,
-                              std::string& err) {
+                              int steps, std::string& err) {
   const auto& T = plan->plan.terminals;
   const long n0 = plan->plan.rs.ranges[0].trips();
   const long lo0 = plan->plan.rs.ranges[0].lo;
@@ -705,6 +708,40 @@ static int run_host_pipelined(lf_plan* plan, void* const* terms, const std::vect
     if (bytes <= 0) return LF_OK;
     return lfx::cuda_status(cudaMemcpyAsync(dst, src, bytes, kind, st), "cudaMemcpyAsync(pipelined)", err);
   };
+  // iterate pairs: goal terminal -> axiom terminal
+  std::vector<int> axiom_of(T.size(), -1);
+  for (const auto& [gname, aname] : plan->plan.rs.iterate)
+    for (size_t i = 0; i < T.size(); ++i)
+      for (size_t a = 0; a < T.size(); ++a)
+        if (T[i].is_goal && T[i].name == gname && !T[a].is_goal && T[a].name == aname) axiom_of[i] = (int)a;
+  // device buffers of step s: inputs = the previous step's outputs for the
+  // iterated axioms; outputs = goals or scratch, alternating so that the last
+  // step writes the goals
+  std::vector<void*> cur(dterms);
+  auto step_bufs = [&](int s) {
+    std::vector<void*> b(cur);
+    const bool to_goal = ((steps - 1 - s) % 2) == 0;
+    for (size_t i = 0; i < T.size(); ++i)
+      if (T[i].is_goal && axiom_of[i] >= 0 && !to_goal) b[i] = plan->scratch[i];
+    return b;
+  };
+  auto advance = [&](const std::vector<void*>& b) {
+    for (size_t i = 0; i < T.size(); ++i)
+      if (axiom_of[i] >= 0) cur[axiom_of[i]] = b[i];
+  };
+  auto run_part = [&](std::vector<void*>& b, long a, long e, bool whole) {
+    lf_slab slab{0, n0, n0, a, e};
+    lfx::ExecArgs ea;
+    ea.plan = &plan->plan;
+    ea.terms = b.data();
+    ea.steps = 1;
+    ea.stream = plan->stream;
+    if (!whole) {
+      ea.slab = &slab;
+      ea.whole_domain_parts = true;
+    }
+    return plan->exec ? plan->exec->run(ea, err) : plan->jit->run(ea, err);
+  };
   std::vector<cudaEvent_t> up(parts), done(parts);
   for (int p = 0; p < parts; ++p) {
     cudaEventCreateWithFlags(&up[p], cudaEventDisableTiming);
@@ -714,43 +751,58 @@ static int run_host_pipelined(lf_plan* plan, void* const* terms, const std::vect
   // inputs that do not span the outer dimension go up first, whole
   for (size_t i = 0; i < T.size() && st == LF_OK; ++i)
     if (!T[i].is_goal && !chunked(T[i])) st = copy(dterms[i], terms[i], terminal_bytes(T[i]), cudaMemcpyHostToDevice, plan->h2d);
-  std::vector<long> copied(T.size(), 0);  // storage rows already sent, per axiom
-  for (int p = 0; p < parts && st == LF_OK; ++p) {
-    const long a = n0 * p / parts, b = n0 * (p + 1) / parts;
-    // rows of every chunked axiom up to this part's last row plus the ghost/halo rows above it
-    for (size_t i = 0; i < T.size() && st == LF_OK; ++i) {
-      if (T[i].is_goal || !chunked(T[i])) continue;
-      const long e0 = T[i].extent[0], below = lo0 - T[i].base[0], above = e0 - n0 - below;
-      const long need = p == parts - 1 ? e0 : std::min(e0, b + below + above);
-      if (need > copied[i]) {
-        const int64_t rb = row_bytes(T[i]);
-        st = copy(static_cast<char*>(dterms[i]) + copied[i] * rb, static_cast<const char*>(terms[i]) + copied[i] * rb,
-                  (need - copied[i]) * rb, cudaMemcpyHostToDevice, plan->h2d);
-        copied[i] = need;
-      }
-    }
-    if (st != LF_OK) break;
-    cudaEventRecord(up[p], plan->h2d);
-    cudaStreamWaitEvent(plan->stream, up[p], 0);
-    lf_slab slab{0, n0, n0, a, b};
-    lfx::ExecArgs ea;
-    ea.plan = &plan->plan;
-    ea.terms = dterms.data();
-    ea.steps = 1;
-    ea.stream = plan->stream;
-    ea.slab = &slab;
-    ea.whole_domain_parts = true;
-    st = plan->exec ? plan->exec->run(ea, err) : plan->jit->run(ea, err);
-    if (st != LF_OK) break;
+  auto part_rows = [&](int p) { return std::make_pair(n0 * p / parts, n0 * (p + 1) / parts); };
+  auto send_down = [&](const std::vector<void*>& b, int p) {
+    const auto [a, e] = part_rows(p);
     cudaEventRecord(done[p], plan->stream);
     cudaStreamWaitEvent(plan->d2h, done[p], 0);
-    // this part's interior output rows
     for (size_t i = 0; i < T.size() && st == LF_OK; ++i) {
       if (!T[i].is_goal || !chunked(T[i])) continue;
       const long below = lo0 - T[i].base[0];
       const int64_t rb = row_bytes(T[i]);
-      st = copy(static_cast<char*>(terms[i]) + (a + below) * rb, static_cast<const char*>(dterms[i]) + (a + below) * rb,
-                (b - a) * rb, cudaMemcpyDeviceToHost, plan->d2h);
+      st = copy(static_cast<char*>(terms[i]) + (a + below) * rb, static_cast<const char*>(b[i]) + (a + below) * rb,
+                (e - a) * rb, cudaMemcpyDeviceToHost, plan->d2h);
+    }
+  };
+  // ---- first step: parts as their rows arrive
+  {
+    std::vector<void*> b = step_bufs(0);
+    std::vector<long> copied(T.size(), 0);  // storage rows already sent, per axiom
+    for (int p = 0; p < parts && st == LF_OK; ++p) {
+      const auto [a, e] = part_rows(p);
+      // rows of every chunked axiom up to this part's last row plus the ghost/halo rows above it
+      for (size_t i = 0; i < T.size() && st == LF_OK; ++i) {
+        if (T[i].is_goal || !chunked(T[i])) continue;
+        const long e0 = T[i].extent[0], below = lo0 - T[i].base[0], above = e0 - n0 - below;
+        const long need = p == parts - 1 ? e0 : std::min(e0, e + below + above);
+        if (need > copied[i]) {
+          const int64_t rb = row_bytes(T[i]);
+          st = copy(static_cast<char*>(dterms[i]) + copied[i] * rb, static_cast<const char*>(terms[i]) + copied[i] * rb,
+                    (need - copied[i]) * rb, cudaMemcpyHostToDevice, plan->h2d);
+          copied[i] = need;
+        }
+      }
+      if (st != LF_OK) break;
+      cudaEventRecord(up[p], plan->h2d);
+      cudaStreamWaitEvent(plan->stream, up[p], 0);
+      if ((st = run_part(b, a, e, false)) != LF_OK) break;
+      if (steps == 1) send_down(b, p);
+    }
+    advance(b);
+  }
+  // ---- the steps in between: whole-domain launches
+  for (int s = 1; s < steps - 1 && st == LF_OK; ++s) {
+    std::vector<void*> b = step_bufs(s);
+    st = run_part(b, 0, n0, true);
+    advance(b);
+  }
+  // ---- last step: parts, each sent down as soon as it is done
+  if (steps > 1 && st == LF_OK) {
+    std::vector<void*> b = step_bufs(steps - 1);
+    for (int p = 0; p < parts && st == LF_OK; ++p) {
+      const auto [a, e] = part_rows(p);
+      if ((st = run_part(b, a, e, false)) != LF_OK) break;
+      send_down(b, p);
     }
   }
   // once every part is done: ghost rows of the goals, and goals without an outer dimension
@@ -818,15 +870,15 @@ int lf_run_host(const lf_plan* cplan, void* const* terms, int nterm, int steps) 
       if ((st = ensure_scratch(plan, err)) != LF_OK) return fail(st, err);
       scratch = scratch_list(plan);
     }
-    // single steps of large grids: copies in both directions overlap the parts' compute
+    // large grids: the copies overlap the first and the last step's compute
     {
       const long n0 = plan->plan.rs.ranges[0].trips();
       const bool nests = plan->jit && !plan->jit->program().nest_kernels.empty();
       int parts = static_cast<int>(std::min<long>(32, n0 / 512));  // 32: measured best for the 16384^2 box pass
       if (const char* e = std::getenv("LF_HOST_PARTS")) parts = std::atoi(e);
       const bool reduces = plan->exec && plan->exec->max_reduce;
-      if (steps == 1 && !inplace && !nests && !reduces && parts >= 2) {
-        st = run_host_pipelined(plan, terms, dterms, parts, err);
+      if (!inplace && !nests && !reduces && parts >= 2) {
+        st = run_host_pipelined(plan, terms, dterms, parts, steps, err);
         if (st != LF_OK) return fail(st, err);
         return LF_OK;
       }

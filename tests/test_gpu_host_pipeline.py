@@ -1,6 +1,8 @@
-"""lf_run_host, single step, pipelined (row parts: H2D of part p+1, compute
-of part p and D2H of part p-1 overlap) -- bit-exact against the oracles,
-ghost rows included."""
+"""lf_run_host, pipelined (row parts: the first step computes part p while
+part p+1 comes up, the last step sends part p down while part p+1 is computed;
+one step overlaps both directions) -- bit-exact against the oracles, ghost rows
+included, for single steps and for multi-step runs (2, 3 and 4 steps: the
+ping-pong through the plan's scratch ends in the goals either way)."""
 import numpy as np
 import pytest
 
@@ -78,3 +80,34 @@ def test_generic_executor(parts):
     finally:
         path.unlink()
     assert np.array_equal(bits(out), bits(ref))
+
+
+@pytest.mark.parametrize("steps", [2, 3, 4])
+def test_multistep_biharm_heat3d_hydro(parts, steps):
+    plan = lf.Plan.with_ranges("biharmonic2d", (90, 256))
+    u = inputs.biharm_input(90, 256, seed=12)
+    out = np.full_like(u, np.nan)
+    plan.run_host([u, out], steps=steps)
+    assert np.array_equal(bits(out), bits(oracle.biharm(u, steps)))
+    plan = lf.Plan.with_ranges("heat3d", (20, 32, 128))
+    u = inputs.heat3d_input(20, 32, 128, seed=13, sigma=4.0)
+    out = np.full_like(u, np.nan)
+    plan.run_host([u, out], steps=steps)
+    assert np.array_equal(bits(out), bits(oracle.heat3d(u, steps)))
+    plan = lf.Plan.with_ranges("hydro2d", (64, 256))
+    st, dtdx = inputs.hydro_input(64, 256, seed=14)
+    outs = [np.full_like(st[0], np.nan) for _ in range(4)]
+    plan.run_host(st + [np.array([dtdx])] + outs, steps=steps)
+    ref = oracle.hydro(st, dtdx, steps)
+    for v in range(4):
+        assert np.array_equal(bits(outs[v]), bits(ref[v])), v
+
+
+def test_multistep_generic_executor(parts):
+    spec = lf.set_ranges((SPECS / "biharm_body.lf").read_text(), (60, 100))
+    plan = lf.Plan(spec, "b.lf")
+    assert plan.executor.startswith("jit_")
+    u = inputs.biharm_input(60, 100, seed=15)
+    out = np.full_like(u, np.nan)
+    plan.run_host([u, out], steps=3)
+    assert np.array_equal(bits(out), bits(oracle.biharm(u, 3)))
