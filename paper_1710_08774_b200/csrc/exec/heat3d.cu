@@ -61,23 +61,38 @@ struct Params {
 // images as compositions of the face maps (the ghost fill of the oracle,
 // oracle/stencils.c) -- so every cell of the goal buffer is written.  A single
 // interior row / plane is the image of both ghost faces.
-__device__ __forceinline__ void store_images(double* out, const Params& p, int k, int j, int gi0, double v0,
-                                             double v1, bool wrap_lo_i, bool wrap_hi_i, uint64_t pol) {
+__device__ __noinline__ void store_ghost_images(double* out, long long pk, long long pj, int ni, int nk_, int nj_,
+                                                bool wrap_k, bool wrap_j, int k, int j, int gi0, double v0, double v1,
+                                                bool wrap_lo_i, bool wrap_hi_i, uint64_t pol) {
   int ks[3], js[3], nk = 0, nj = 0;
   ks[nk++] = k + 1;
-  if (p.wrap_k && k == 0) ks[nk++] = p.nk + 1;
-  if (p.wrap_k && k == p.nk - 1) ks[nk++] = 0;
+  if (wrap_k && k == 0) ks[nk++] = nk_ + 1;
+  if (wrap_k && k == nk_ - 1) ks[nk++] = 0;
   js[nj++] = j + 1;
-  if (p.wrap_j && j == 0) js[nj++] = p.nj + 1;
-  if (p.wrap_j && j == p.nj - 1) js[nj++] = 0;
+  if (wrap_j && j == 0) js[nj++] = nj_ + 1;
+  if (wrap_j && j == nj_ - 1) js[nj++] = 0;
   for (int a = 0; a < nk; ++a)
     for (int b = 0; b < nj; ++b) {
-      double* rowp = out + (long long)ks[a] * p.pk + (long long)js[b] * p.pj + 1;  // logical i = 0
+      if (a == 0 && b == 0) continue;  // the cell's own row: stored by the caller
+      double* rowp = out + (long long)ks[a] * pk + (long long)js[b] * pj + 1;  // logical i = 0
       st_hint(rowp + gi0, v0, pol);
       st_hint(rowp + gi0 + 32, v1, pol);
-      if (wrap_lo_i) st_hint(rowp + p.ni, v0, pol);
+      if (wrap_lo_i) st_hint(rowp + ni, v0, pol);
       if (wrap_hi_i) st_hint(rowp - 1, v1, pol);
     }
+}
+__device__ __forceinline__ void store_images(double* out, const Params& p, int k, int j, int gi0, double v0,
+                                             double v1, bool wrap_lo_i, bool wrap_hi_i, uint64_t pol) {
+  double* rowp = out + (long long)(k + 1) * p.pk + (long long)(j + 1) * p.pj + 1;  // logical i = 0
+  st_hint(rowp + gi0, v0, pol);
+  st_hint(rowp + gi0 + 32, v1, pol);
+  if (wrap_lo_i) st_hint(rowp + p.ni, v0, pol);
+  if (wrap_hi_i) st_hint(rowp - 1, v1, pol);
+  // rows on a wrapped k or j face also have images in the ghost planes / rows
+  // (out of line: only the boundary rows take it)
+  if ((p.wrap_k && (k == 0 || k == p.nk - 1)) || (p.wrap_j && (j == 0 || j == p.nj - 1)))
+    store_ghost_images(out, p.pk, p.pj, p.ni, p.nk, p.nj, p.wrap_k, p.wrap_j, k, j, gi0, v0, v1, wrap_lo_i, wrap_hi_i,
+                       pol);
 }
 
 // Work unit u = (k chunk, column tile), k-chunk major: at any moment all
