@@ -30,99 +30,12 @@
 #include <sstream>
 
 #include "../planner/dsl.hpp"
+#include "codegen_ctx.hpp"
 #include "jit.hpp"
 
 namespace lfx {
 
-namespace {
-
-std::string elem_type(const std::string& t) {
-  if (t.find("double") != std::string::npos) return "double";
-  if (t.find("float") != std::string::npos) return "float";
-  return "";
-}
-
-std::string plus(long off) {
-  if (!off) return "";
-  return (off > 0 ? " + " : " - ") + std::to_string(std::labs(off));
-}
-
-struct GIn {
-  std::string param;
-  int var;
-  std::vector<int> rel;
-  int via = -1;  // index into Ctx::inlined: the value is that producer recomputed in place
-};
-struct GOut {
-  std::string param;
-  int var;
-  std::vector<int> rel;
-};
-struct Load {
-  int var;
-  std::vector<int> rel;
-};
-struct Grp {
-  int kernel;
-  std::vector<int> gmin, gmax;
-  std::vector<GIn> in;
-  std::vector<GOut> out;
-  std::vector<Load> loads;  // distinct (variable, offset) reads, inlined producers expanded
-  int shift = 0;  // lead along the outermost dimension (march schedule)
-  int level = 1;  // dependency level (groups of one level share a barrier)
-};
-
-// everything the emitters share
-struct Ctx {
-  const lf::Plan& P;
-  std::string sources;  // user-kernel sources the generated code is compiled with
-  int nd = 0;
-  std::vector<long> LO;  // range lower bounds: loop index = LO + trip
-  std::string T;
-  std::vector<long> N;
-  std::vector<std::vector<int>> vmin, vmax;  // per var, per dim: term offset range
-  std::map<int, std::vector<int>> axiom_extra;
-  std::vector<char> smem_var;  // kernel outputs read by some kernel
-  std::vector<Grp> groups;     // kernel groups, dataflow order
-  std::vector<Grp> inlined;    // cheap producers recomputed inside their consumers
-  std::string error;
-
-  explicit Ctx(const lf::Plan& p) : P(p) {}
-
-  int terminal_of(int v, bool goal) const {
-    for (size_t i = 0; i < P.terminals.size(); ++i)
-      if (P.terminals[i].var == v && P.terminals[i].is_goal == goal) return static_cast<int>(i);
-    return -1;
-  }
-  long pitch(const lf::Terminal& t, size_t slot) const {
-    long p = 1;
-    for (size_t k = slot + 1; k < t.extent.size(); ++k) p *= t.extent[k];
-    return p;
-  }
-  // flat index of terminal `ti` at term-frame position pos[d] (+ extra[d])
-  std::string tidx(int ti, const std::vector<std::string>& pos, const std::vector<int>& extra) const {
-    const auto& t = P.terminals[ti];
-    std::string e;
-    for (size_t s = 0; s < t.dims.size(); ++s) {
-      const int d = t.dims[s];
-      const long off = extra[d] - t.base[s] + LO[d];
-      const std::string c = "(long long)(" + pos[d] + plus(off) + ")";
-      const long p = pitch(t, s);
-      e += (e.empty() ? "" : " + ") + c + (p != 1 ? " * " + std::to_string(p) + "LL" : "");
-    }
-    return e.empty() ? std::string("0") : e;
-  }
-  std::vector<int> extra_of(int v) const {
-    auto it = axiom_extra.find(v);
-    return it == axiom_extra.end() ? std::vector<int>(nd, 0) : it->second;
-  }
-  // full-rank axiom terminal backing variable v (or -1)
-  int staged_axiom(int v) const {
-    const int ti = terminal_of(v, false);
-    if (ti < 0 || (int)P.terminals[ti].dims.size() != nd) return -1;
-    return ti;
-  }
-};
+namespace cg {
 
 // Kernel evaluation: a `body:` expression per output (R/SPEC.md:82), or a
 // call of the function the declaration names (R/PAPER.md:58-62: value
@@ -489,22 +402,10 @@ bool emit_bodies(Ctx& C, const Grp& G, std::ostream& src, const char* ind) {
   return true;
 }
 
-void emit_prelude(Ctx& C, std::ostream& src, int threads, int min_blocks = 1, bool ws = false) {
-  const auto& terms = C.P.terminals;
-  if (!ws) {
-    src << "// generated by loomfuse-b200 (csrc/jit/codegen.cpp) for chain '" << C.P.rs.name << "'\n";
-    src << "typedef " << C.T << " T;\n";
-    src << "__device__ __forceinline__ T lf_min(T a, T b) { return a < b ? a : b; }\n";
-    src << "__device__ __forceinline__ T lf_max(T a, T b) { return a > b ? a : b; }\n";
-    // must match lfx::Args in jit.cpp (passed by value)
-    src << "struct LfArgs { void* t[32]; long long n0; int row_lo, row_hi, top, bottom, chunk, inplace; };\n";
-    src << "extern \"C\" __global__ void __launch_bounds__(" << threads << ", " << min_blocks
-        << ") lf_jit_step(const LfArgs a) {\n";
-    src << "  extern __shared__ __align__(128) unsigned char lf_smem[];\n";  // one declaration for both march kernels
-  } else {
-    // warp-specialised variant: tensor maps of the streamed axioms (must match
-    // lfx::JitMaps in jit.cpp) and the mbarrier / TMA primitives it uses
-    src << R"(struct __align__(64) LfTmap { unsigned long long w[16]; };
+void emit_tma_helpers(std::ostream& src) {
+  // tensor maps of the streamed axioms (must match lfx::JitMaps in jit.cpp)
+  // and the mbarrier / TMA primitives of the warp-specialised marches
+  src << R"(struct __align__(64) LfTmap { unsigned long long w[16]; };
 struct LfMaps { LfTmap m[)" << kJitMaxMaps << R"(]; };
 __device__ __forceinline__ unsigned lf_s32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void lf_mbar_init(unsigned long long* b, unsigned n) {
@@ -529,10 +430,28 @@ __device__ __forceinline__ void lf_tma3(void* dst, const LfTmap* m, unsigned lon
                :: "r"(lf_s32(dst)), "l"(m), "r"(lf_s32(b)), "r"(c0), "r"(c1), "r"(c2) : "memory");
 }
 )";
+}
+
+// kernel signature and the terminal pointers.  kernel == nullptr: the first
+// kernel of the module (lf_jit_step), preceded by the module prelude; else a
+// variant taking the tensor maps of its streamed axioms (emit_tma_helpers
+// must precede it)
+void emit_prelude(Ctx& C, std::ostream& src, int threads, int min_blocks, const char* kernel) {
+  const auto& terms = C.P.terminals;
+  if (!kernel) {
+    src << "// generated by loomfuse-b200 (csrc/jit/codegen.cpp) for chain '" << C.P.rs.name << "'\n";
+    src << "typedef " << C.T << " T;\n";
+    src << "__device__ __forceinline__ T lf_min(T a, T b) { return a < b ? a : b; }\n";
+    src << "__device__ __forceinline__ T lf_max(T a, T b) { return a > b ? a : b; }\n";
+    // must match lfx::Args in jit.cpp (passed by value)
+    src << "struct LfArgs { void* t[32]; long long n0; int row_lo, row_hi, top, bottom, chunk, inplace; };\n";
     src << "extern \"C\" __global__ void __launch_bounds__(" << threads << ", " << min_blocks
-        << ") lf_jit_step_ws(const LfArgs a, const __grid_constant__ LfMaps lf_maps) {\n";
-    src << "  extern __shared__ __align__(128) unsigned char lf_smem[];\n";
+        << ") lf_jit_step(const LfArgs a) {\n";
+  } else {
+    src << "extern \"C\" __global__ void __launch_bounds__(" << threads << ", " << min_blocks << ") " << kernel
+        << "(const LfArgs a, const __grid_constant__ LfMaps lf_maps) {\n";
   }
+  src << "  extern __shared__ __align__(128) unsigned char lf_smem[];\n";  // one declaration for every march kernel
   src << "  const long long N0 = a.n0;\n";
   for (int d = 1; d < C.nd; ++d) src << "  const long long N" << d << " = " << C.N[d] << ";\n";
   for (size_t i = 0; i < terms.size(); ++i) {
@@ -727,7 +646,7 @@ bool emit_march(Ctx& C, JitProgram& out, std::ostream& src, bool ws = false) {
 
   int minb = std::min(cps, 2);  // register cap; 2 measured best
   if (const char* e = std::getenv("LF_JIT_MINB")) minb = std::max(1, std::atoi(e));
-  emit_prelude(C, src, ws ? NT + 32 : NT, minb, ws);
+  emit_prelude(C, src, ws ? NT + 32 : NT, minb, ws ? "lf_jit_step_ws" : nullptr);
   // ws: warp 0 is the producer, consumer thread c = threadIdx.x - 32
   const char* TID = ws ? "((int)threadIdx.x - 32)" : "threadIdx.x";
   if (nd == 3)
@@ -1368,7 +1287,7 @@ bool emit_tiled(Ctx& C, JitProgram& out, std::ostream& src) {
   out.march = false;
   out.inplace.clear();
   out.inplace_error = C.P.rs.aliases.empty() ? "" : "in-place runs need a 2D/3D chain (the 1D path reads axioms in place)";
-  emit_prelude(C, src, NT);
+  emit_prelude(C, src, NT, 1, nullptr);
   src << "  const long long o0 = (long long)a.row_lo + (long long)blockIdx.x * " << tile << ";\n";
   for (size_t v = 0; v < nv; ++v)
     if (C.smem_var[v]) src << "  T* __restrict__ v" << v << " = reinterpret_cast<T*>(lf_smem + " << soff[v] << ");\n";
@@ -1948,7 +1867,9 @@ bool emit_nests(const lf::Plan& P, const std::string& sources, JitProgram& out, 
   return true;
 }
 
-}  // namespace
+}  // namespace cg
+
+using namespace cg;
 
 bool jit_generate(const lf::Plan& P, JitProgram& out, const std::string& sources) {
   bool multi = !P.one_nest;
@@ -2008,13 +1929,29 @@ bool jit_generate(const lf::Plan& P, JitProgram& out, const std::string& sources
   }
   ws_ok &= nstaged > 0 && nstaged <= kJitMaxMaps;
   if (ws_ok) {
+    std::string variants;
     std::ostringstream ws;
     out.ws_maps.clear();
     if (emit_march(C, out, ws, true) && !out.ws_maps.empty() && static_cast<int>(out.ws_maps.size()) <= kJitMaxMaps) {
       out.has_ws = true;
-      src << ws.str();
+      variants += ws.str();
     } else {
       out.ws_maps.clear();
+    }
+    // 2D: the register march (LF_JIT_RM=0: off)
+    std::ostringstream rm;
+    const bool rm_off = std::getenv("LF_JIT_RM") && std::atoi(std::getenv("LF_JIT_RM")) == 0;
+    if (C.nd == 2 && !rm_off && emit_rmarch(C, out, rm) && !out.rm_maps.empty() &&
+        static_cast<int>(out.rm_maps.size()) <= kJitMaxMaps) {
+      out.has_rm = true;
+      variants += rm.str();
+    } else {
+      out.rm_maps.clear();  // the chain keeps the marches above
+      out.has_rm = false;
+    }
+    if (!variants.empty()) {
+      emit_tma_helpers(src);
+      src << variants;
     }
   }
   out.source = sources + src.str();

@@ -1,0 +1,472 @@
+// Generic executor, part 3: the register march of 2D chains (lf_jit_step_rm).
+//
+// The HFAV schedule of codegen.cpp's marches (a CTA marches the outer
+// dimension, callsite group g computes row t + s_g at trip t, s_g the pipeline
+// shift of shifts.cpp:8-79, each intermediate kept for the W_v rows of its
+// contraction, storage.cpp:319-399), with the storage moved one level closer
+// to the ALUs:
+//
+//  * every consumer warp owns a strip of tw output columns and computes its
+//    own halo, so warps never wait for one another: no CTA barrier at all;
+//  * a lane owns V adjacent cells of the strip (V = 4 fp32 / 2 fp64 by
+//    default): streamed axioms are read from their shared-memory ring (filled
+//    by the producer warp's TMA row boxes, as in lf_jit_step_ws) with 16-B
+//    vector loads, neighbours along the row come from the adjacent lanes by
+//    warp shuffles;
+//  * intermediates live in registers: variable v keeps its last W_v rows as
+//    T R_v[W_v][V], rotated once per trip.
+//
+// Lanes near the strip edges receive shuffled values from outside the warp
+// (junk); the tile width is chosen so that every cell a group must produce is
+// at least the accumulated stencil reach away from the edges (margins A_g / B_g
+// below), and only those cells are stored.
+#include <algorithm>
+#include <climits>
+#include <cstdlib>
+#include <cstring>
+#include <map>
+#include <set>
+#include <sstream>
+#include <tuple>
+
+#include "../planner/dsl.hpp"
+#include "codegen_ctx.hpp"
+
+namespace lfx::cg {
+
+namespace {
+
+long floordiv(long a, long b) { return a >= 0 ? a / b : -((-a + b - 1) / b); }
+
+std::string num(long v) { return v < 0 ? "m" + std::to_string(-v) : std::to_string(v); }
+
+}  // namespace
+
+bool emit_rmarch(Ctx& C, JitProgram& out, std::ostream& src) {
+  if (C.nd != 2 || !C.P.rs.aliases.empty()) return false;
+  const int eb = out.elem_bytes;
+  const int CH = 16 / eb;  // elements per 16-B chunk
+  int V = eb == 8 ? 2 : 4;
+  if (const char* e = std::getenv("LF_JIT_RM_V")) V = std::atoi(e);
+  if (V < CH || V % CH || V > 16) return false;
+  int NW = 8;  // consumer warps per CTA
+  if (const char* e = std::getenv("LF_JIT_RM_WARPS")) NW = std::max(1, std::min(16, std::atoi(e)));
+  int PD = 3;
+  if (const char* e = std::getenv("LF_JIT_PD")) PD = std::max(1, std::atoi(e));
+  const int NS = PD + 1;
+  const size_t nv = C.P.vars.size();
+  const auto& G = C.groups;
+  if (G.empty()) return false;
+  for (const auto& g : G)
+    for (const auto& o : g.out)
+      if (o.rel[1] != 0) return false;  // outputs at the group's anchor column only
+
+  // ---- rows: streamed axioms in a shared-memory ring (+ PD rows in flight),
+  // intermediates in registers (exactly the contraction span)
+  std::vector<int> lead(nv, INT_MIN), old(nv, INT_MAX), win(nv, 0), staged(nv, -1);
+  for (const auto& g : G)
+    for (const auto& in : g.loads) {
+      lead[in.var] = std::max(lead[in.var], C.smem_var[in.var] ? INT_MIN : g.shift + in.rel[0]);
+      old[in.var] = std::min(old[in.var], g.shift + in.rel[0]);
+    }
+  for (const auto& g : G)
+    for (const auto& o : g.out)
+      if (C.smem_var[o.var]) lead[o.var] = g.shift + o.rel[0];
+  int reg_words = 0;
+  for (size_t v = 0; v < nv; ++v) {
+    if (C.smem_var[v]) {
+      if (old[v] == INT_MAX) return false;
+      win[v] = lead[v] - old[v] + 1;
+      reg_words += win[v] * V * eb / 4;
+    } else if (old[v] != INT_MAX && C.staged_axiom(static_cast<int>(v)) >= 0) {
+      staged[v] = C.staged_axiom(static_cast<int>(v));
+      win[v] = lead[v] - old[v] + 1 + PD;
+    }
+    if (win[v] > 0 && (win[v] > 64 || old[v] < -60 || lead[v] > 60)) return false;
+  }
+  if (reg_words > 96) return false;  // register windows would spill
+  // fault injection (R/SPEC.md:557, as in emit_march): the named intermediate
+  // keeps one row fewer than its contraction span
+  std::vector<int> drop(nv, 0);
+  if (const char* f = std::getenv("LF_JIT_FAULT"); f && std::strncmp(f, "span:", 5) == 0)
+    for (size_t v = 0; v < nv; ++v)
+      if (C.smem_var[v] && win[v] > 1 && C.P.vars[v].name == f + 5) {
+        drop[v] = 1;
+        win[v] -= 1;
+      }
+
+  // ---- columns.  A lane's cells are c = cs + lane * V + i (warp-strip
+  // relative).  A_g / B_g: how far from the lane span's left / right end group
+  // g's values are still exact -- each shuffle across the warp edge eats the
+  // reach of the read: a register variable at column offset dr, or a streamed
+  // row (whose lane vectors start rho_v cells left of the lane's first cell)
+  // at rho_v + dr.  The first goal fixes the lane alignment (its 16-B chunks
+  // start at lane cells): cs = res (mod CH)
+  int goal_ti = -1;
+  for (const auto& g : G)
+    for (const auto& o : g.out)
+      if (goal_ti < 0 && C.terminal_of(o.var, true) >= 0) goal_ti = C.terminal_of(o.var, true);
+  if (goal_ti < 0) return false;
+  auto goal_so = [&](int ti) { return -C.P.terminals[ti].base[1] + C.LO[1]; };  // storage col = logical + so
+  std::vector<int> vmin1(nv, 0), vmax1(nv, 0);
+  for (size_t v = 0; v < nv; ++v) {
+    if (staged[v] < 0) continue;
+    const auto& t = C.P.terminals[staged[v]];
+    const long so = C.extra_of(static_cast<int>(v))[1] - t.base[1] + C.LO[1];
+    vmin1[v] = C.vmin[v][1];
+    vmax1[v] = C.vmax[v][1];
+    vmin1[v] -= static_cast<int>(((vmin1[v] + so) % CH + CH) % CH);  // TMA box origin 16-B aligned
+  }
+  std::vector<long> base_al(nv, 0), rho(nv, 0);
+  std::vector<int> A(G.size(), 0), B(G.size(), 0);
+  auto margins = [&](long cs) {
+    for (size_t v = 0; v < nv; ++v)
+      if (staged[v] >= 0) {
+        const long D = cs - vmin1[v];
+        base_al[v] = floordiv(D, CH) * CH;
+        rho[v] = D - base_al[v];
+      }
+    std::map<int, std::pair<int, int>> margin;  // register variable -> (A, B) of its producer
+    for (size_t gi = 0; gi < G.size(); ++gi) {
+      int a = 0, b = 0;
+      for (const auto& ld : G[gi].loads) {
+        if (C.smem_var[ld.var]) {
+          const auto [pa, pb] = margin.at(ld.var);
+          a = std::max(a, pa - ld.rel[1]);
+          b = std::max(b, pb + ld.rel[1]);
+        } else if (staged[ld.var] >= 0) {
+          a = std::max(a, static_cast<int>(-(rho[ld.var] + ld.rel[1])));
+          b = std::max(b, static_cast<int>(rho[ld.var] + ld.rel[1]));
+        }
+      }
+      A[gi] = a;
+      B[gi] = b;
+      for (const auto& o : G[gi].out)
+        if (C.smem_var[o.var]) margin[o.var] = {a, b};
+    }
+  };
+  const long res = ((-goal_so(goal_ti)) % CH + CH) % CH;
+  long cs = LONG_MAX;
+  for (size_t gi = 0; gi < G.size(); ++gi) cs = std::min<long>(cs, G[gi].gmin[1]);
+  cs = res + floordiv(cs - res, CH) * CH;
+  for (int it = 0;; ++it) {
+    margins(cs);
+    bool ok = true;
+    for (size_t gi = 0; gi < G.size(); ++gi) ok &= G[gi].gmin[1] >= cs + A[gi];
+    if (ok) break;
+    if (it > 8) return false;
+    cs -= CH;
+  }
+  long tw = LONG_MAX;
+  for (size_t gi = 0; gi < G.size(); ++gi) tw = std::min<long>(tw, cs + 32L * V - B[gi] - G[gi].gmax[1]);
+  tw = tw / CH * CH;
+  if (tw < 2 * CH || tw < 4) return false;
+  if (const char* e = std::getenv("LF_JIT_RM_TW")) tw = std::min<long>(tw, std::max(CH, std::atoi(e) / CH * CH));
+  const long T1 = NW * tw;  // CTA tile
+  const long inner = (C.N[1] + T1 - 1) / T1;
+
+  // ---- shared memory: the streamed axioms' rings (TMA boxes of <= 256
+  // elements, 128-B multiples), 16-B aligned windows, guard pads for the
+  // junk lanes' reads just outside a window
+  std::vector<int> nbox(nv, 1), bw(nv, 0);
+  std::vector<long> soff(nv, 0);
+  long lo_idx = 0, hi_over = 0;
+  for (size_t v = 0; v < nv; ++v) {
+    if (staged[v] < 0) continue;
+    const int w = static_cast<int>(T1) + vmax1[v] - vmin1[v];
+    const int al = 128 / eb;
+    nbox[v] = (w + 255) / 256;
+    bw[v] = ((w + nbox[v] - 1) / nbox[v] + al - 1) / al * al;
+    if (bw[v] > 256) nbox[v] += 1, bw[v] = ((w + nbox[v] - 1) / nbox[v] + al - 1) / al * al;
+    // lane vectors span [base_al, (NW-1) tw + 32 V + base_al)
+    lo_idx = std::min(lo_idx, base_al[v]);
+    hi_over = std::max(hi_over, (NW - 1) * tw + 32L * V + base_al[v] - static_cast<long>(nbox[v]) * bw[v]);
+  }
+  const size_t pad_front = static_cast<size_t>((-lo_idx * eb + 127) / 128 * 128);
+  size_t smem = pad_front;
+  for (size_t v = 0; v < nv; ++v) {
+    if (staged[v] < 0) continue;
+    soff[v] = smem;
+    smem += (static_cast<size_t>(win[v]) * nbox[v] * bw[v] * eb + 127) / 128 * 128;
+  }
+  smem += static_cast<size_t>((std::max(0L, hi_over) * eb + 127) / 128 * 128);
+  if (smem == pad_front) return false;  // nothing streamed
+  if (smem + 16 * NS > 200 * 1024) return false;
+  out.rm_smem_bytes = smem + 16 * NS;
+  out.rm_threads = 32 * (NW + 1);
+  out.rm_inner_tiles = inner;
+  out.rm_maps.clear();
+
+  // trip range relative to the chunk [r0, r1)
+  int TS = INT_MAX, TE = INT_MIN;
+  for (const auto& g : G) {
+    TS = std::min(TS, g.gmin[0] - g.shift);
+    TE = std::max(TE, g.gmax[0] - g.shift);
+  }
+  for (size_t v = 0; v < nv; ++v)
+    if (staged[v] >= 0) TS = std::min(TS, C.vmin[v][0] - lead[v]);
+
+  int minb = 2;
+  if (const char* e = std::getenv("LF_JIT_RM_MINB")) minb = std::max(1, std::atoi(e));
+  emit_prelude(C, src, out.rm_threads, minb, "lf_jit_step_rm");
+  const std::string VT = eb == 8 ? "double2" : "float4";
+  const char* comp[4] = {"x", "y", "z", "w"};
+  src << "  // register march: " << NW << " consumer warps x " << tw << "-column strips, " << V
+      << " cells per lane (lane span starts at column " << cs << " of the strip)\n";
+  for (size_t v = 0; v < nv; ++v)
+    if (staged[v] >= 0)
+      src << "  T* __restrict__ v" << v << " = reinterpret_cast<T*>(lf_smem + " << soff[v] << ");  // '"
+          << C.P.vars[v].name << "': " << win[v] << " rows x " << nbox[v] * bw[v] << "\n";
+  src << "  unsigned long long* lf_full = reinterpret_cast<unsigned long long*>(lf_smem + " << smem << ");\n";
+  src << "  unsigned long long* lf_empty = lf_full + " << NS << ";\n";
+  src << "  if (threadIdx.x == 0) {\n";
+  src << "    for (int i = 0; i < " << NS << "; ++i) { lf_mbar_init(&lf_full[i], 1); lf_mbar_init(&lf_empty[i], " << NW
+      << "); }\n";
+  src << "    asm volatile(\"fence.mbarrier_init.release.cluster;\" ::: \"memory\");\n";
+  {
+    int k = 0;
+    for (size_t v = 0; v < nv; ++v)
+      if (staged[v] >= 0)
+        src << "    asm volatile(\"prefetch.tensormap [%0];\" :: \"l\"(&lf_maps.m[" << k++ << "]) : \"memory\");\n";
+  }
+  src << "  }\n  __syncthreads();\n";
+  src << "  const bool producer = threadIdx.x < 32;\n";
+  src << "  if (producer && threadIdx.x != 0) return;\n";
+  src << "  const int warp = (int)(threadIdx.x >> 5) - 1, lane = threadIdx.x & 31;\n";
+  src << "  const int wl = warp * " << tw << " + lane * " << V << ";  // lane's first cell - lane-span start, CTA tile relative\n";
+  src << "  unsigned lf_g = 0;\n";
+  for (size_t v = 0; v < nv; ++v)
+    if (staged[v] >= 0) src << "  int b" << v << " = 0;\n";
+  for (size_t v = 0; v < nv; ++v)
+    if (C.smem_var[v]) src << "  T R" << v << "[" << win[v] << "][" << V << "];  // '" << C.P.vars[v].name << "'\n";
+  src << "  const int rows = a.row_hi - a.row_lo;\n";
+  src << "  const long long units = (long long)((rows + a.chunk - 1) / a.chunk) * " << inner << ";\n";
+  src << "  for (long long u = blockIdx.x; u < units; u += gridDim.x) {\n";
+  src << "  const int ci = (int)(u / " << inner << "), bt = (int)(u % " << inner << ");\n";
+  src << "  const int r0 = a.row_lo + ci * a.chunk, r1 = min(r0 + a.chunk, a.row_hi);\n";
+  src << "  const int o1 = bt * " << T1 << ";\n";
+  src << "  const int ow = o1 + warp * " << tw << ";  // this warp's strip\n";
+  src << "  const bool wact = ow < " << C.N[1] << ";\n";
+
+  auto rowbase = [&](size_t v, int off) -> std::string {
+    const int W = win[v];
+    if (W == 1) return "0";
+    const int o = ((off % W) + W) % W;
+    const std::string b = "b" + std::to_string(v);
+    const std::string sum = o ? "(" + b + " + " + std::to_string(o) + ")" : b;
+    const std::string sl =
+        o ? "(" + sum + " >= " + std::to_string(W) + " ? " + sum + " - " + std::to_string(W) + " : " + sum + ")" : b;
+    return sl + " * " + std::to_string(nbox[v] * bw[v]);
+  };
+
+  src << "  for (int t = r0 + (" << TS << "); t <= r1 - 1 + (" << TE << "); ++t, ++lf_g) {\n";
+  src << "    const unsigned stg = lf_g % " << NS << ", par = (lf_g / " << NS << ") & 1;\n";
+  // ---- producer: one TMA row box set per streamed axiom per trip
+  src << "    if (producer) {\n";
+  src << "      if (lf_g >= " << NS << ") lf_mbar_wait(&lf_empty[stg], par ^ 1);\n";
+  src << "      unsigned bytes = 0;\n";
+  {
+    int k = 0;
+    for (size_t v = 0; v < nv; ++v) {
+      if (staged[v] < 0) continue;
+      src << "      const int y" << k << " = t" << plus(lead[v]) << ";\n";
+      src << "      const bool in" << k << " = y" << k << " >= r0" << plus(C.vmin[v][0]) << " && y" << k << " <= r1 - 1"
+          << plus(C.vmax[v][0]) << ";\n";
+      src << "      if (in" << k << ") bytes += " << static_cast<size_t>(nbox[v]) * bw[v] * eb << "u;\n";
+      ++k;
+    }
+  }
+  src << "      asm volatile(\"fence.proxy.async.shared::cta;\" ::: \"memory\");\n";
+  src << "      lf_mbar_expect(&lf_full[stg], bytes);\n";
+  {
+    int k = 0;
+    for (size_t v = 0; v < nv; ++v) {
+      if (staged[v] < 0) continue;
+      const int ti = staged[v];
+      const auto& t = C.P.terminals[ti];
+      const auto ex = C.extra_of(static_cast<int>(v));
+      auto so = [&](int d) { return static_cast<long>(ex[d]) - t.base[d] + C.LO[d]; };
+      src << "      if (in" << k << ") {\n";
+      src << "        T* dst = v" << v << " + " << rowbase(v, lead[v]) << ";\n";
+      for (int b = 0; b < nbox[v]; ++b)
+        src << "        lf_tma2(dst + " << b * bw[v] << ", &lf_maps.m[" << k << "], &lf_full[stg], o1"
+            << plus(vmin1[v] + so(1) + b * bw[v]) << ", y" << k << plus(so(0)) << ");\n";
+      src << "      }\n";
+      JitProgram::Tma tm;
+      tm.term = ti;
+      tm.rank = 2;
+      tm.extent[0] = t.extent[1];
+      tm.extent[1] = t.extent[0];
+      tm.box[0] = static_cast<unsigned>(bw[v]);
+      tm.box[1] = 1;
+      out.rm_maps.push_back(tm);
+      ++k;
+    }
+  }
+  src << "    } else {\n";
+  src << "    lf_mbar_wait(&lf_full[stg], par);\n";
+  src << "    if (wact) {\n";
+
+  // ---- consumers: the groups in dataflow order
+  for (size_t gi = 0; gi < G.size(); ++gi) {
+    const Grp& g = G[gi];
+    const auto& k = C.P.rs.kernels[g.kernel];
+    src << "    { // group " << gi << ": kernel '" << k.name << "', lead " << g.shift << ", exact on lane-span cells ["
+        << A[gi] << ", " << 32 * V - B[gi] << ")\n";
+    src << "      const int y = t" << plus(g.shift) << ";\n";
+    src << "      if (y >= r0" << plus(g.gmin[0]) << " && y <= r1 - 1" << plus(g.gmax[0]) << ") {\n";
+    // vectors of the streamed rows this group reads
+    std::map<std::pair<int, int>, std::string> vec;  // (var, row offset) -> register array
+    auto vector_of = [&](int var, int r) {
+      auto key = std::make_pair(var, r);
+      auto it = vec.find(key);
+      if (it != vec.end()) return it->second;
+      const std::string nm = "S" + std::to_string(var) + "_" + num(r);
+      src << "        T " << nm << "[" << V << "];\n";
+      src << "        { const T* p = v" << var << " + " << rowbase(static_cast<size_t>(var), g.shift + r) << " + wl"
+          << plus(base_al[var]) << ";\n";
+      for (int c = 0; c < V / CH; ++c) {
+        src << "          const " << VT << " c" << c << " = *reinterpret_cast<const " << VT << "*>(p + " << c * CH << ");";
+        for (int e = 0; e < CH; ++e) src << " " << nm << "[" << c * CH + e << "] = c" << c << "." << comp[e] << ";";
+        src << "\n";
+      }
+      src << "        }\n";
+      vec[key] = nm;
+      return nm;
+    };
+    // value of variable `var` at (row r, column i + dr) of this lane: own
+    // registers, or a shuffle from the lane that holds it
+    std::map<std::tuple<int, int, int>, std::string> elems;
+    auto elem = [&](int var, int r, int dr, int i) -> std::string {
+      long e;
+      std::string arr;
+      if (staged[var] >= 0) {
+        arr = vector_of(var, r);
+        e = rho[var] + i + dr;
+      } else if (C.smem_var[var]) {
+        const int slot = std::max(0, g.shift + r - old[var] - drop[var]);
+        arr = "R" + std::to_string(var) + "[" + std::to_string(slot) + "]";
+        e = i + dr;
+      } else {
+        const int ti = C.terminal_of(var, false);
+        if (C.P.terminals[ti].dims.empty()) return "s" + std::to_string(ti);
+        std::vector<std::string> pos = {"y" + plus(r), "(ow + " + std::to_string(cs) + " + lane * " + std::to_string(V) +
+                                                           plus(i + dr) + ")"};
+        return "__ldg(t" + std::to_string(ti) + " + " + C.tidx(ti, pos, C.extra_of(var)) + ")";
+      }
+      const long q = floordiv(e, V), m = e - q * V;
+      const std::string own = arr + "[" + std::to_string(m) + "]";
+      if (q == 0) return own;
+      auto key = std::make_tuple(var, r, static_cast<int>(e));
+      auto it = elems.find(key);
+      if (it != elems.end()) return it->second;
+      const std::string nm = "X" + std::to_string(var) + "_" + num(r) + "_" + num(e);
+      src << "        const T " << nm << " = "
+          << (q > 0 ? "__shfl_down_sync(0xffffffffu, " + own + ", " + std::to_string(q) + ")"
+                    : "__shfl_up_sync(0xffffffffu, " + own + ", " + std::to_string(-q) + ")")
+          << ";\n";
+      elems[key] = nm;
+      return nm;
+    };
+    // every operand first (vector loads and shuffles are warp-wide), then the cells
+    std::vector<std::vector<std::string>> opnd(V, std::vector<std::string>(g.loads.size()));
+    for (int i = 0; i < V; ++i)
+      for (size_t li = 0; li < g.loads.size(); ++li)
+        opnd[i][li] = elem(g.loads[li].var, g.loads[li].rel[0], g.loads[li].rel[1], i);
+    auto load_index = [&](int var, const std::vector<int>& rel) {
+      for (size_t li = 0; li < g.loads.size(); ++li)
+        if (g.loads[li].var == var && g.loads[li].rel == rel) return static_cast<int>(li);
+      return -1;
+    };
+    std::vector<std::pair<int, const GOut*>> goals;  // (terminal, output)
+    for (const auto& o : g.out) {
+      const int ti = C.terminal_of(o.var, true);
+      if (ti >= 0) {
+        goals.emplace_back(ti, &o);
+        src << "        T G" << gi << "_" << o.param << "[" << V << "];\n";
+      }
+    }
+    for (int i = 0; i < V; ++i) {
+      src << "        { // cell " << i << "\n";
+      for (const auto& in : g.in) {
+        if (in.via < 0) {
+          src << "          const T p_" << in.param << " = " << opnd[i][load_index(in.var, in.rel)] << ";\n";
+          continue;
+        }
+        const Grp& pg = C.inlined[in.via];
+        const auto& pk = C.P.rs.kernels[pg.kernel];
+        std::string oparam;
+        std::vector<int> orel(2, 0);
+        for (const auto& o : pg.out)
+          if (o.var == in.var) {
+            oparam = o.param;
+            orel = o.rel;
+          }
+        std::map<std::string, std::string> pv;
+        for (const auto& pin : pg.in) {
+          std::vector<int> r(2);
+          for (int d = 0; d < 2; ++d) r[d] = in.rel[d] - orel[d] + pin.rel[d];
+          pv[pin.param] = opnd[i][load_index(pin.var, r)];
+        }
+        std::string e2;
+        auto e = lf::parse_expr(pk.bodies.at(oparam), e2);
+        if (!e) return (C.error = "kernel '" + pk.name + "': " + e2, false);
+        src << "          const T p_" << in.param << " = "
+            << lf::emit_c(*e, C.T, [&](const std::string& n) { return pv.at(n); }) << ";  // inlined '" << pk.name
+            << "'\n";
+      }
+      if (!emit_bodies(C, g, src, "          ")) return false;
+      for (const auto& o : g.out) {
+        if (C.smem_var[o.var])
+          src << "          R" << o.var << "[" << std::max(0, g.shift + o.rel[0] - old[o.var] - drop[o.var]) << "][" << i
+              << "] = q_" << o.param << ";\n";
+        if (C.terminal_of(o.var, true) >= 0) src << "          G" << gi << "_" << o.param << "[" << i << "] = q_" << o.param << ";\n";
+      }
+      src << "        }\n";
+    }
+    // goal rows: own chunk rows, own strip cells, inside the domain
+    for (const auto& [ti, o] : goals) {
+      const auto& t = C.P.terminals[ti];
+      const long so = goal_so(ti);
+      const bool vec_ok = ((cs + so) % CH + CH) % CH == 0 && t.extent[1] % CH == 0;
+      src << "        { const int yy = y" << plus(o->rel[0]) << ";\n";
+      src << "          const int c = " << cs << " + lane * " << V << ", x = ow + c;\n";
+      src << "          if (yy >= r0 && yy < r1) {\n";
+      src << "            T* gp = t" << ti << " + " << C.tidx(ti, {"yy", "x"}, std::vector<int>(2, 0)) << ";\n";
+      const std::string gv = "G" + std::to_string(gi) + "_" + o->param;
+      if (vec_ok) {
+        src << "            if (c >= 0 && c + " << V << " <= " << tw << " && x + " << V << " <= " << C.N[1] << ") {\n";
+        for (int c = 0; c < V / CH; ++c) {
+          src << "              " << VT << " w" << c << ";";
+          for (int e = 0; e < CH; ++e) src << " w" << c << "." << comp[e] << " = " << gv << "[" << c * CH + e << "];";
+          src << " *reinterpret_cast<" << VT << "*>(gp + " << c * CH << ") = w" << c << ";\n";
+        }
+        src << "            } else {\n";
+      } else {
+        src << "            {\n";
+      }
+      src << "              #pragma unroll\n";
+      src << "              for (int i = 0; i < " << V << "; ++i)\n";
+      src << "                if (c + i >= 0 && c + i < " << tw << " && x + i < " << C.N[1] << ") gp[i] = " << gv << "[i];\n";
+      src << "            }\n          }\n        }\n";
+    }
+    src << "      }\n    }\n";
+  }
+  src << "    }\n";  // wact
+  src << "    __syncwarp();\n";
+  src << "    if (lane == 0) lf_mbar_arrive(&lf_empty[stg]);\n";
+  // rotate the register windows: row t + off of trip t is row (t+1) + (off-1)
+  for (size_t v = 0; v < nv; ++v)
+    if (C.smem_var[v] && win[v] > 1)
+      src << "    #pragma unroll\n    for (int k = 0; k < " << win[v] - 1 << "; ++k)\n      #pragma unroll\n"
+          << "      for (int i = 0; i < " << V << "; ++i) R" << v << "[k][i] = R" << v << "[k + 1][i];\n";
+  src << "    }\n";  // consumer
+  for (size_t v = 0; v < nv; ++v)
+    if (staged[v] >= 0 && win[v] > 1) src << "    b" << v << " = b" << v << " == " << (win[v] - 1) << " ? 0 : b" << v << " + 1;\n";
+  src << "  }\n";  // trips
+  src << "  }\n";  // units
+  src << "}\n";
+  return true;
+}
+
+}  // namespace lfx::cg

@@ -296,13 +296,14 @@ static long pick_chunk(long rows, long inner, long resident, long fill, long max
 
 // tensor maps of the streamed axioms for this launch's buffers; false (plain
 // kernel) when a buffer is not 16-B aligned or the driver refuses a map
-bool JitKernel::ws_maps(const std::vector<void*>& bufs, long rows, JitMaps& maps, std::string& err) {
+bool JitKernel::tma_maps(const std::vector<JitProgram::Tma>& list, const std::vector<void*>& bufs, long rows,
+                         JitMaps& maps) {
   static const bool off = std::getenv("LF_JIT_WS") && std::atoi(std::getenv("LF_JIT_WS")) == 0;
   if (off) return false;
   const CUtensorMapDataType dt = prog_.elem_bytes == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
   const long n0 = plan_rows_;
-  for (size_t k = 0; k < prog_.ws_maps.size(); ++k) {
-    const auto& m = prog_.ws_maps[k];
+  for (size_t k = 0; k < list.size(); ++k) {
+    const auto& m = list[k];
     const void* base = bufs[m.term];
     if (reinterpret_cast<uintptr_t>(base) % 16) return false;
     uint64_t dims[3] = {m.extent[0], m.extent[1], m.extent[2]};
@@ -312,7 +313,6 @@ bool JitKernel::ws_maps(const std::vector<void*>& bufs, long rows, JitMaps& maps
     if (!make_tensor_map(reinterpret_cast<CUtensorMap*>(&maps.m[k]), base, dt, prog_.elem_bytes, m.rank, dims, m.box, e))
       return false;
   }
-  (void)err;
   return true;
 }
 
@@ -380,6 +380,11 @@ int JitKernel::run(const ExecArgs& a, std::string& err) {
         d.attr(static_cast<CUfunction>(step_ws_), CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES,
                static_cast<int>(prog_.ws_smem_bytes));
       }
+      if (prog_.has_rm && d.get(&f, m, "lf_jit_step_rm") == CUDA_SUCCESS) {
+        step_rm_ = f;
+        d.attr(static_cast<CUfunction>(step_rm_), CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES,
+               static_cast<int>(prog_.rm_smem_bytes));
+      }
     }
   }
   if (!prog_.nest_kernels.empty()) return run_nests(a, err);
@@ -436,6 +441,14 @@ int JitKernel::run(const ExecArgs& a, std::string& err) {
         else
           resident_ws_ = std::max(1, sms) * ows;
       }
+      if (step_rm_) {
+        int orm = 0;
+        if (d.occupancy(&orm, static_cast<CUfunction>(step_rm_), prog_.rm_threads, prog_.rm_smem_bytes) != CUDA_SUCCESS ||
+            orm < 1)
+          step_rm_ = nullptr;
+        else
+          resident_rm_ = std::max(1, sms) * orm;
+      }
     }
     // whole (chunk, tile) units round-robin over the resident CTAs
     static const bool span_order = std::getenv("LF_JIT_SPAN_ORDER") != nullptr;
@@ -485,7 +498,19 @@ int JitKernel::run(const ExecArgs& a, std::string& err) {
     for (size_t i = 0; i < T.size(); ++i) args.t[i] = bufs[i];
     int st = LF_OK;
     JitMaps maps;
-    if (prog_.march && step_ws_ && ws_maps(bufs, rp.rows, maps, err)) {
+    // the register march stores its goal rows in 16-B vectors
+    bool goals_aligned = true;
+    for (size_t i = 0; i < T.size(); ++i)
+      if (T[i].is_goal) goals_aligned &= reinterpret_cast<uintptr_t>(bufs[i]) % 16 == 0;
+    if (prog_.march && step_rm_ && goals_aligned && tma_maps(prog_.rm_maps, bufs, rp.rows, maps)) {
+      JitArgs wa = args;
+      long chunk = pick_chunk(rows, prog_.rm_inner_tiles, resident_rm_, prog_.prologue, rows);
+      if (const char* e = std::getenv("LF_JIT_CHUNK")) chunk = std::max(1L, std::min<long>(rows, std::atol(e)));
+      wa.chunk = static_cast<int>(chunk);
+      const long units = (rows + chunk - 1) / chunk * prog_.rm_inner_tiles;
+      dim3 grm(static_cast<unsigned>(std::max<long>(1, std::min<long>(resident_rm_, units))));
+      st = launch(step_rm_, grm, dim3(prog_.rm_threads), prog_.rm_smem_bytes, a.stream, &wa, err, &maps);
+    } else if (prog_.march && step_ws_ && tma_maps(prog_.ws_maps, bufs, rp.rows, maps)) {
       // whole (chunk, tile) units round-robin over the resident CTAs
       JitArgs wa = args;
       long chunk = pick_chunk(rows, prog_.ws_inner_tiles, resident_ws_, prog_.prologue,

@@ -65,6 +65,13 @@ struct JitProgram {
   size_t ws_smem_bytes = 0;
   long ws_inner_tiles = 1;  // the variant's own inner tiling
   int ws_threads = 288;
+  // 2D register march (lf_jit_step_rm, codegen_rm.cpp): warp strips, register
+  // windows, no CTA barriers; preferred over lf_jit_step_ws where it compiles
+  bool has_rm = false;
+  std::vector<Tma> rm_maps;
+  size_t rm_smem_bytes = 0;
+  long rm_inner_tiles = 1;
+  int rm_threads = 288;
   std::string error;  // why the chain is not supported
 };
 
@@ -103,19 +110,21 @@ class JitKernel {
   int device_ = -1;
   void* step_ = nullptr;    // CUfunction
   void* step_ws_ = nullptr; // warp-specialised variant (TMA producer warp)
+  void* step_rm_ = nullptr; // 2D register march (TMA producer warp, warp strips)
   void* fill_ = nullptr;
   void* capture_ = nullptr;
   std::vector<void*> bands_;        // in-place band copies
   std::vector<size_t> band_bytes_;
   int resident_ = 0;  // CTAs resident at once (occupancy x SMs)
   int resident_ws_ = 0;
+  int resident_rm_ = 0;
   std::vector<void*> nest_fns_;
   std::vector<void*> mats_;  // device buffers of materialised variables
   std::vector<char> cubin_;
   int launch(void* fn, dim3 grid, dim3 block, size_t smem, cudaStream_t st, void* args, std::string& err,
              void* args2 = nullptr);
   int run_nests(const ExecArgs& a, std::string& err);
-  bool ws_maps(const std::vector<void*>& bufs, long rows, JitMaps& maps, std::string& err);
+  bool tma_maps(const std::vector<JitProgram::Tma>& list, const std::vector<void*>& bufs, long rows, JitMaps& maps);
   long plan_rows_ = 0;  // trips of the outermost loop dimension (whole domain)
   int run_inplace(const ExecArgs& a, JitArgs& args, std::string& err);
 };

@@ -11,11 +11,32 @@ import paper_1710_08774_b200 as lf
 SPECS = lf.PKG_DIR.parent / "tests" / "specs"
 
 
+def _kernel(src, name):
+    if name + "(" not in src:
+        return ""
+    body = src[src.index(name + "("):]
+    nxt = body.find('extern "C" __global__', 1)
+    return body if nxt < 0 else body[:nxt]
+
+
 def kernels(plan):
     src = plan.source
-    plain = src[src.index("lf_jit_step("):]
-    ws = src[src.index("lf_jit_step_ws("):] if "lf_jit_step_ws(" in src else ""
-    return plain, ws
+    return _kernel(src, "lf_jit_step"), _kernel(src, "lf_jit_step_ws")
+
+
+def test_register_march_for_2d_chains():
+    """2D chains get lf_jit_step_rm: warp strips with intermediates in
+    register windows, neighbours by shuffles, no CTA barrier in the march."""
+    for name in ("biharm_body", "multi_body"):
+        rm = _kernel(lf.Plan.from_file(SPECS / f"{name}.lf").source, "lf_jit_step_rm")
+        assert rm, name
+        assert "lf_tma2(" in rm and "lf_mbar_wait(&lf_full" in rm
+        assert rm.count("__syncthreads") == 1 and "bar.sync" not in rm
+    rm = _kernel(lf.Plan.from_file(SPECS / "biharm_body.lf").source, "lf_jit_step_rm")
+    assert "__shfl_down_sync" in rm and "__shfl_up_sync" in rm
+    assert "T R" in rm and "double2" in rm  # register windows, 16-B vector loads
+    # 3D chains keep the shared-memory window marches
+    assert "lf_jit_step_rm(" not in lf.Plan.from_file(SPECS / "heat3d_body.lf").source
 
 
 def test_warp_specialised_variant_for_streamed_axioms():
