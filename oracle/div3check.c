@@ -1,7 +1,11 @@
 /*
  * Exhaustive check (test infrastructure): the FMA-based quotient the device
- * uses for x / 3.0f (userkernels/stencil_kernels.h: lf_div3f) equals the IEEE
- * division for every one of the 2^32 float bit patterns.  Host fmaf is the
+ * uses for x / 3.0f (userkernels/stencil_kernels.h: lf_div3f, and its packed
+ * fp32x2 form in the generic executor) equals the IEEE division for every one
+ * of the 2^32 float bit patterns.  The residual is formed negated,
+ * t = RN(3q - x), and applied as RN(q - t r): signed zeros then come out right
+ * without a test (x = -0: t = +0, q - t r = -0 + -0), so only infinities
+ * (t = NaN) keep the plain product.  Host fmaf is the
  * correctly rounded fused multiply-add, as __fmaf_rn is on the GPU.
  * Usage: div3check [stride]  (stride > 1 samples every stride-th pattern)
  */
@@ -14,9 +18,9 @@
 static inline float div3_device_sequence(float x) {
   const float r = 0x1.555556p-2f;
   const float q = x * r;
-  const float e = fmaf(-q, 3.0f, x);
-  const float q1 = fmaf(e, r, q);
-  return (x == 0.0f || isinf(x)) ? q : q1;
+  const float t = fmaf(q, 3.0f, -x);
+  const float q1 = fmaf(t, -r, q);
+  return isinf(q) ? q : q1;
 }
 
 int main(int argc, char** argv) {

@@ -443,6 +443,15 @@ void emit_prelude(Ctx& C, std::ostream& src, int threads, int min_blocks, const 
     src << "typedef " << C.T << " T;\n";
     src << "__device__ __forceinline__ T lf_min(T a, T b) { return a < b ? a : b; }\n";
     src << "__device__ __forceinline__ T lf_max(T a, T b) { return a > b ? a : b; }\n";
+    if (C.T == "float")  // fp32x2 helpers of lf::emit_c2: lanewise, the scalar operations' rounding
+      src << R"(__device__ __forceinline__ float2 lf_f2(float c) { return make_float2(c, c); }
+__device__ __forceinline__ float2 lf_neg2(float2 a) { return make_float2(-a.x, -a.y); }
+__device__ __forceinline__ float2 lf_div2(float2 a, float2 b) { return make_float2(a.x / b.x, a.y / b.y); }
+__device__ __forceinline__ float2 lf_sqrt2(float2 a) { return make_float2(sqrtf(a.x), sqrtf(a.y)); }
+__device__ __forceinline__ float2 lf_abs2(float2 a) { return make_float2(fabsf(a.x), fabsf(a.y)); }
+__device__ __forceinline__ float2 lf_min2(float2 a, float2 b) { return make_float2(lf_min(a.x, b.x), lf_min(a.y, b.y)); }
+__device__ __forceinline__ float2 lf_max2(float2 a, float2 b) { return make_float2(lf_max(a.x, b.x), lf_max(a.y, b.y)); }
+)";
     // must match lfx::Args in jit.cpp (passed by value)
     src << "struct LfArgs { void* t[32]; long long n0; int row_lo, row_hi, top, bottom, chunk, inplace; };\n";
     src << "extern \"C\" __global__ void __launch_bounds__(" << threads << ", " << min_blocks

@@ -25,6 +25,8 @@
 #include <cstdlib>
 #include <cstring>
 #include <map>
+#include <memory>
+#include <numeric>
 #include <set>
 #include <sstream>
 #include <tuple>
@@ -259,7 +261,35 @@ bool emit_rmarch(Ctx& C, JitProgram& out, std::ostream& src) {
     return sl + " * " + std::to_string(nbox[v] * bw[v]);
   };
 
-  src << "  for (int t = r0 + (" << TS << "); t <= r1 - 1 + (" << TE << "); ++t, ++lf_g) {\n";
+  for (size_t v = 0; v < nv; ++v) {
+    if (staged[v] < 0) continue;
+    const auto& t = C.P.terminals[staged[v]];
+    JitProgram::Tma tm;
+    tm.term = staged[v];
+    tm.rank = 2;
+    tm.extent[0] = t.extent[1];
+    tm.extent[1] = t.extent[0];
+    tm.box[0] = static_cast<unsigned>(bw[v]);
+    tm.box[1] = 1;
+    out.rm_maps.push_back(tm);
+  }
+  // register windows rotate by renaming: the trip loop is unrolled U = lcm(W_v)
+  // times and copy u keeps the row of logical slot k in R_v[(k + u) % W_v] (no
+  // moves); windows whose lcm exceeds 6 shift by moves at the end of each trip
+  int U = 1;
+  for (size_t v = 0; v < nv; ++v)
+    if (C.smem_var[v] && win[v] > 1) U = std::lcm(U, win[v]);
+  if (U > 6 || (std::getenv("LF_JIT_RM_UNROLL") && std::atoi(std::getenv("LF_JIT_RM_UNROLL")) == 0)) U = 1;
+  int cu = 0;  // the copy being emitted
+  auto phys = [&](int v, int k) { return U == 1 ? k : (k + cu) % win[v]; };
+  const std::string trip_end = "r1 - 1 + (" + std::to_string(TE) + ")";
+  if (U == 1) {
+    src << "  for (int t = r0 + (" << TS << "); t <= " << trip_end << "; ++t) {\n";
+  } else {
+    src << "  for (int t0 = r0 + (" << TS << "); t0 <= " << trip_end << "; t0 += " << U << ") {\n";
+  }
+  for (cu = 0; cu < U; ++cu) {
+  if (U > 1) src << "  { const int t = t0 + " << cu << ";  // copy " << cu << "\n  if (t > " << trip_end << ") break;\n";
   src << "    const unsigned stg = lf_g % " << NS << ", par = (lf_g / " << NS << ") & 1;\n";
   // ---- producer: one TMA row box set per streamed axiom per trip
   src << "    if (producer) {\n";
@@ -292,14 +322,6 @@ bool emit_rmarch(Ctx& C, JitProgram& out, std::ostream& src) {
         src << "        lf_tma2(dst + " << b * bw[v] << ", &lf_maps.m[" << k << "], &lf_full[stg], o1"
             << plus(vmin1[v] + so(1) + b * bw[v]) << ", y" << k << plus(so(0)) << ");\n";
       src << "      }\n";
-      JitProgram::Tma tm;
-      tm.term = ti;
-      tm.rank = 2;
-      tm.extent[0] = t.extent[1];
-      tm.extent[1] = t.extent[0];
-      tm.box[0] = static_cast<unsigned>(bw[v]);
-      tm.box[1] = 1;
-      out.rm_maps.push_back(tm);
       ++k;
     }
   }
@@ -345,7 +367,7 @@ bool emit_rmarch(Ctx& C, JitProgram& out, std::ostream& src) {
         e = rho[var] + i + dr;
       } else if (C.smem_var[var]) {
         const int slot = std::max(0, g.shift + r - old[var] - drop[var]);
-        arr = "R" + std::to_string(var) + "[" + std::to_string(slot) + "]";
+        arr = "R" + std::to_string(var) + "[" + std::to_string(phys(var, slot)) + "]";
         e = i + dr;
       } else {
         const int ti = C.terminal_of(var, false);
@@ -386,7 +408,74 @@ bool emit_rmarch(Ctx& C, JitProgram& out, std::ostream& src) {
         src << "        T G" << gi << "_" << o.param << "[" << V << "];\n";
       }
     }
-    for (int i = 0; i < V; ++i) {
+    // fp32, opt-in (LF_JIT_RM_PACK=1): cells in pairs on the packed fp32x2
+    // pipe when every output (and every inlined producer) has a body.  Exact,
+    // but measured slower on the box chain (430 vs 484 G: forming the register
+    // pairs costs moves), so scalar cells by default
+    bool packed = C.T == "float" && V % 2 == 0 && std::getenv("LF_JIT_RM_PACK") && std::atoi(std::getenv("LF_JIT_RM_PACK")) != 0;
+    for (const auto& [op, pat] : k.outputs) packed &= k.bodies.count(op) > 0;
+    std::set<std::string> kin;
+    for (const auto& [ip, pat] : k.inputs) kin.insert(ip);
+    std::vector<std::pair<std::string, std::unique_ptr<lf::Expr>>> bodies;
+    for (const auto& [op, pat] : k.outputs) {
+      if (!packed) break;
+      std::string e2;
+      auto e = lf::parse_expr(k.bodies.at(op), e2);
+      std::set<std::string> used;
+      if (e) lf::expr_vars(*e, used);
+      for (const auto& u : used) packed &= kin.count(u) > 0;
+      if (!e) packed = false;
+      else bodies.emplace_back(op, std::move(e));
+    }
+    for (const auto& in : g.in)
+      if (in.via >= 0)
+        for (const auto& o : C.inlined[in.via].out)
+          if (o.var == in.var) packed &= C.P.rs.kernels[C.inlined[in.via].kernel].bodies.count(o.param) > 0;
+    for (int j = 0; packed && j < V; j += 2) {
+      src << "        { // cells " << j << ", " << j + 1 << " (fp32x2)\n";
+      auto pair = [&](int li) { return "make_float2(" + opnd[j][li] + ", " + opnd[j + 1][li] + ")"; };
+      for (const auto& in : g.in) {
+        if (in.via < 0) {
+          src << "          const float2 p_" << in.param << " = " << pair(load_index(in.var, in.rel)) << ";\n";
+          continue;
+        }
+        const Grp& pg = C.inlined[in.via];
+        const auto& pk = C.P.rs.kernels[pg.kernel];
+        std::string oparam;
+        std::vector<int> orel(2, 0);
+        for (const auto& o : pg.out)
+          if (o.var == in.var) {
+            oparam = o.param;
+            orel = o.rel;
+          }
+        std::map<std::string, std::string> pv;
+        for (const auto& pin : pg.in) {
+          std::vector<int> r(2);
+          for (int d = 0; d < 2; ++d) r[d] = in.rel[d] - orel[d] + pin.rel[d];
+          pv[pin.param] = pair(load_index(pin.var, r));
+        }
+        std::string e2;
+        auto e = lf::parse_expr(pk.bodies.at(oparam), e2);
+        if (!e) return (C.error = "kernel '" + pk.name + "': " + e2, false);
+        src << "          const float2 p_" << in.param << " = "
+            << lf::emit_c2(*e, [&](const std::string& n) { return pv.at(n); }) << ";  // inlined '" << pk.name << "'\n";
+      }
+      for (const auto& [op, e] : bodies)
+        src << "          const float2 q_" << op << " = " << lf::emit_c2(*e, [](const std::string& n) { return "p_" + n; })
+            << ";\n";
+      for (const auto& o : g.out) {
+        for (int h = 0; h < 2; ++h) {
+          const char* lane_c = h ? ".y" : ".x";
+          if (C.smem_var[o.var])
+            src << "          R" << o.var << "[" << phys(o.var, std::max(0, g.shift + o.rel[0] - old[o.var] - drop[o.var])) << "]["
+                << j + h << "] = q_" << o.param << lane_c << ";\n";
+          if (C.terminal_of(o.var, true) >= 0)
+            src << "          G" << gi << "_" << o.param << "[" << j + h << "] = q_" << o.param << lane_c << ";\n";
+        }
+      }
+      src << "        }\n";
+    }
+    for (int i = 0; i < V && !packed; ++i) {
       src << "        { // cell " << i << "\n";
       for (const auto& in : g.in) {
         if (in.via < 0) {
@@ -418,7 +507,7 @@ bool emit_rmarch(Ctx& C, JitProgram& out, std::ostream& src) {
       if (!emit_bodies(C, g, src, "          ")) return false;
       for (const auto& o : g.out) {
         if (C.smem_var[o.var])
-          src << "          R" << o.var << "[" << std::max(0, g.shift + o.rel[0] - old[o.var] - drop[o.var]) << "][" << i
+          src << "          R" << o.var << "[" << phys(o.var, std::max(0, g.shift + o.rel[0] - old[o.var] - drop[o.var])) << "][" << i
               << "] = q_" << o.param << ";\n";
         if (C.terminal_of(o.var, true) >= 0) src << "          G" << gi << "_" << o.param << "[" << i << "] = q_" << o.param << ";\n";
       }
@@ -456,13 +545,16 @@ bool emit_rmarch(Ctx& C, JitProgram& out, std::ostream& src) {
   src << "    __syncwarp();\n";
   src << "    if (lane == 0) lf_mbar_arrive(&lf_empty[stg]);\n";
   // rotate the register windows: row t + off of trip t is row (t+1) + (off-1)
-  for (size_t v = 0; v < nv; ++v)
+  for (size_t v = 0; v < nv && U == 1; ++v)
     if (C.smem_var[v] && win[v] > 1)
       src << "    #pragma unroll\n    for (int k = 0; k < " << win[v] - 1 << "; ++k)\n      #pragma unroll\n"
           << "      for (int i = 0; i < " << V << "; ++i) R" << v << "[k][i] = R" << v << "[k + 1][i];\n";
   src << "    }\n";  // consumer
   for (size_t v = 0; v < nv; ++v)
     if (staged[v] >= 0 && win[v] > 1) src << "    b" << v << " = b" << v << " == " << (win[v] - 1) << " ? 0 : b" << v << " + 1;\n";
+  src << "    ++lf_g;\n";
+  if (U > 1) src << "  }\n";  // copy
+  }
   src << "  }\n";  // trips
   src << "  }\n";  // units
   src << "}\n";

@@ -170,11 +170,12 @@ void expr_vars(const Expr& e, std::set<std::string>& out) {
 // becomes lf_div3f (userkernels/stencil_kernels.h: one multiply and an FMA
 // correction, checked bit-identical for all 2^32 inputs by oracle/div3check).
 // Empty: keep the division.
-static std::string div_by_literal(const std::string& num, const std::string& lit, bool f) {
+enum class LitDiv { none, pow2, three };
+static LitDiv literal_divisor(const std::string& lit, bool f, std::string& recip) {
   char* end = nullptr;
   const double c = std::strtod(lit.c_str(), &end);
-  if (!end || *end || !std::isfinite(c) || c == 0.0) return "";
-  if (f && static_cast<double>(static_cast<float>(c)) != c) return "";
+  if (!end || *end || !std::isfinite(c) || c == 0.0) return LitDiv::none;
+  if (f && static_cast<double>(static_cast<float>(c)) != c) return LitDiv::none;
   int ex = 0;
   const double m = std::frexp(c, &ex);  // c = m * 2^ex, |m| in [0.5, 1)
   if (std::fabs(m) == 0.5) {
@@ -182,11 +183,22 @@ static std::string div_by_literal(const std::string& num, const std::string& lit
     if (f ? (k >= -126 && k <= 126) : (k >= -1022 && k <= 1022)) {
       char buf[64];
       std::snprintf(buf, sizeof buf, "%s0x1p%d%s", m < 0 ? "-" : "", -k, f ? "f" : "");
-      return "(" + num + " * " + buf + ")";
+      recip = buf;
+      return LitDiv::pow2;
     }
-    return "";
+    return LitDiv::none;
   }
-  if (f && c == 3.0) return "lf_div3f(" + num + ")";
+  if (f && c == 3.0) return LitDiv::three;
+  return LitDiv::none;
+}
+
+static std::string div_by_literal(const std::string& num, const std::string& lit, bool f) {
+  std::string recip;
+  switch (literal_divisor(lit, f, recip)) {
+    case LitDiv::pow2: return "(" + num + " * " + recip + ")";
+    case LitDiv::three: return "lf_div3f(" + num + ")";
+    case LitDiv::none: break;
+  }
   return "";
 }
 
@@ -211,6 +223,39 @@ std::string emit_c(const Expr& e, const std::string& type, const std::function<s
       if (e.text == "abs") return std::string(f ? "fabsf(" : "fabs(") + A(0) + ")";
       if (e.text == "min") return "lf_min(" + A(0) + ", " + A(1) + ")";
       return "lf_max(" + A(0) + ", " + A(1) + ")";
+  }
+  return "?";
+}
+
+// fp32x2: the expression on two cells at once.  + and * map to the lanewise
+// FADD2 / FMUL2 (a - b is a + (-b), as IEEE defines it), x / 3 to lf_div3f2,
+// a power-of-two divisor to the product with its exact reciprocal; the other
+// operations go lane by lane through the lf_*2 helpers the generated module
+// defines -- each lane rounds exactly as emit_c's scalar code.
+std::string emit_c2(const Expr& e, const std::function<std::string(const std::string&)>& var) {
+  auto A = [&](int k) { return emit_c2(*e.args[k], var); };
+  switch (e.kind) {
+    case Expr::Num: return "lf_f2(static_cast<float>(" + (e.text.find_first_of(".eE") == std::string::npos ? e.text + ".0" : e.text) + "))";
+    case Expr::Var: return var(e.text);
+    case Expr::Neg: return "lf_neg2(" + A(0) + ")";
+    case Expr::Add: return "__fadd2_rn(" + A(0) + ", " + A(1) + ")";
+    case Expr::Sub: return "__fadd2_rn(" + A(0) + ", lf_neg2(" + A(1) + "))";
+    case Expr::Mul: return "__fmul2_rn(" + A(0) + ", " + A(1) + ")";
+    case Expr::Div:
+      if (e.args[1]->kind == Expr::Num) {
+        std::string recip;
+        switch (literal_divisor(e.args[1]->text, true, recip)) {
+          case LitDiv::pow2: return "__fmul2_rn(" + A(0) + ", lf_f2(" + recip + "))";
+          case LitDiv::three: return "lf_div3f2(" + A(0) + ")";
+          case LitDiv::none: break;
+        }
+      }
+      return "lf_div2(" + A(0) + ", " + A(1) + ")";
+    case Expr::Call:
+      if (e.text == "sqrt") return "lf_sqrt2(" + A(0) + ")";
+      if (e.text == "abs") return "lf_abs2(" + A(0) + ")";
+      if (e.text == "min") return "lf_min2(" + A(0) + ", " + A(1) + ")";
+      return "lf_max2(" + A(0) + ", " + A(1) + ")";
   }
   return "?";
 }

@@ -20,5 +20,9 @@ void expr_vars(const Expr& e, std::set<std::string>& out);
 // fully parenthesised C in element type `type` ("double" / "float");
 // `var` maps a parameter name to its C expression
 std::string emit_c(const Expr& e, const std::string& type, const std::function<std::string(const std::string&)>& var);
+// fp32 only: the same expression on a float2 pair of cells (packed FADD2 /
+// FMUL2 / FFMA2 where lanewise exact, per-lane helpers lf_*2 otherwise);
+// `var` maps a parameter name to a float2 expression
+std::string emit_c2(const Expr& e, const std::function<std::string(const std::string&)>& var);
 
 }  // namespace lf

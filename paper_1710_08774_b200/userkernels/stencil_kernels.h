@@ -50,21 +50,38 @@ LF_HD void heat_divupd(double c, double fxp, double fxm, double fyp, double fym,
 
 /* x / 3.0f, correctly rounded.  The device computes the IEEE quotient with
  * one multiply by RN(1/3) and an FMA residual correction instead of the
- * generic division subroutine (rcp + Newton + slow-path call); the sequence
- * is exhaustively checked bit-identical to `x / 3.0f` for all 2^32 inputs
- * (oracle/div3check.c, tests/test_div3.py).  Zeros and infinities keep the
- * plain product, which is exact for them. */
+ * generic division subroutine (rcp + Newton + slow-path call):
+ *   q = RN(x r),  t = RN(3 q - x),  q1 = RN(q - t r)
+ * The sequence is exhaustively checked bit-identical to `x / 3.0f` for all
+ * 2^32 inputs (oracle/div3check.c, tests/test_div3.py).  Forming the residual
+ * negated gives signed zeros right with no test (x = -0: t = +0, q1 = -0);
+ * infinities (t = NaN) keep the plain product, which is exact for them. */
 LF_HD float lf_div3f(float x) {
 #if defined(__CUDA_ARCH__)
   const float r = 0x1.555556p-2f; /* RN(1/3) */
   const float q = __fmul_rn(x, r);
-  const float e = __fmaf_rn(-q, 3.0f, x);
-  const float q1 = __fmaf_rn(e, r, q);
-  return (x == 0.0f || isinf(x)) ? q : q1;
+  const float t = __fmaf_rn(q, 3.0f, -x);
+  const float q1 = __fmaf_rn(t, -r, q);
+  return isinf(q) ? q : q1;
 #else
   return x / 3.0f;
 #endif
 }
+
+#if defined(__CUDACC__)
+/* the same sequence on fp32x2 pairs (FMUL2 / FFMA2; lanewise identical) */
+__device__ __forceinline__ float2 lf_div3f2(float2 x) {
+#if defined(__CUDA_ARCH__)
+  const float2 r = make_float2(0x1.555556p-2f, 0x1.555556p-2f);
+  const float2 q = __fmul2_rn(x, r);
+  const float2 t = __ffma2_rn(q, make_float2(3.0f, 3.0f), make_float2(-x.x, -x.y));
+  const float2 q1 = __ffma2_rn(t, make_float2(-0x1.555556p-2f, -0x1.555556p-2f), q);
+  return make_float2(isinf(q.x) ? q.x : q1.x, isinf(q.y) ? q.y : q1.y);
+#else
+  return x; /* host pass: device only */
+#endif
+}
+#endif
 
 /* one 3-tap pass; a,b,c are the -1,0,+1 neighbours along the pass axis */
 LF_HD void box3(float a, float b, float c, float* o) { *o = lf_div3f(a + b + c); }
