@@ -472,6 +472,62 @@ __device__ __forceinline__ float2 lf_max2(float2 a, float2 b) { return make_floa
   }
 }
 
+// In place (config.aliases, one buffer): a kernel copying, before each step,
+// the rows at chunk boundaries and the columns at tile boundaries (`tile`: the
+// march's inner tile) that one (chunk, tile) unit reads but another writes, for
+// each aliased axiom (variable, terminal) into the band buffers a.t[slot],
+// a.t[slot + 1], a.t[slot + 2] (rows, dim-1 columns, dim-2 columns)
+void emit_capture(Ctx& C, const char* name, const std::vector<std::pair<size_t, int>>& caps,
+                  const std::vector<int>& slots, const std::vector<int>& tile, std::ostream& src) {
+  const int nd = C.nd;
+  src << "extern \"C\" __global__ void " << name << "(const LfArgs a) {\n";
+  src << "  const long long N0 = a.n0;\n";
+  src << "  const int nch = (int)((N0 + a.chunk - 1) / a.chunk);\n";
+  for (size_t q = 0; q < caps.size(); ++q) {
+    const size_t v = caps[q].first;
+    const int slot = slots[q];
+    const auto& t = C.P.terminals[caps[q].second];
+    const auto ex = C.extra_of(static_cast<int>(v));
+    std::vector<long> so(nd);
+    for (int d = 0; d < nd; ++d) so[d] = ex[d] - t.base[d] + C.LO[d];
+    const long E0 = t.extent[0], E1 = nd > 1 ? t.extent[1] : 1, E2 = nd > 2 ? t.extent[2] : 1, PL = E1 * E2;
+    const long BH = C.vmax[v][0] - C.vmin[v][0];
+    const long BW1 = C.vmax[v][1] - C.vmin[v][1], BW2 = nd > 2 ? C.vmax[v][2] - C.vmin[v][2] : 0;
+    const long NT1 = (C.N[1] + tile[1] - 1) / tile[1], NT2 = nd > 2 ? (C.N[2] + tile[2] - 1) / tile[2] : 1;
+    const long nc1 = (NT1 - 1) * BW1 * E0 * E2, nc2 = nd > 2 ? (NT2 - 1) * BW2 * E0 * E1 : 0;
+    src << "  {\n";
+    src << "    const T* m = reinterpret_cast<const T*>(a.t[" << caps[q].second << "]);\n";
+    src << "    T* rb = reinterpret_cast<T*>(a.t[" << slot << "]);\n";
+    src << "    T* c1 = reinterpret_cast<T*>(a.t[" << slot + 1 << "]);\n";
+    src << "    T* c2 = reinterpret_cast<T*>(a.t[" << slot + 2 << "]);\n";
+    src << "    const long long nrb = (long long)max(0, nch - 1) * " << BH * PL << "LL;\n";
+    src << "    const long long tot = nrb + " << (nc1 + nc2) << "LL;\n";
+    src << "    for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < tot; idx += (long long)gridDim.x * blockDim.x) {\n";
+    src << "      if (idx < nrb) {\n";
+    src << "        const long long p = idx % " << PL << "LL, r = idx / " << PL << "LL;\n";
+    src << "        const long long y = (r / " << BH << " + 1) * (long long)a.chunk" << plus(C.vmin[v][0]) << " + r % " << BH << ";\n";
+    src << "        rb[idx] = m[(y" << plus(so[0]) << ") * " << PL << "LL + p];\n";
+    src << "      } else if (idx < nrb + " << nc1 << "LL) {\n";
+    src << "        long long j = idx - nrb;\n";
+    src << "        const long long z2 = j % " << E2 << "LL; j /= " << E2 << "LL;\n";
+    src << "        const long long zy = j % " << E0 << "LL; j /= " << E0 << "LL;\n";
+    src << "        const long long x1 = (j / " << std::max(1L, BW1) << " + 1) * " << tile[1] << plus(C.vmin[v][1]) << " + j % "
+        << std::max(1L, BW1) << ";\n";
+    src << "        c1[idx - nrb] = m[zy * " << PL << "LL + (x1" << plus(so[1]) << ") * " << E2 << "LL + z2];\n";
+    if (nd == 3) {
+      src << "      } else {\n";
+      src << "        long long j = idx - nrb - " << nc1 << "LL;\n";
+      src << "        const long long z1 = j % " << E1 << "LL; j /= " << E1 << "LL;\n";
+      src << "        const long long zy = j % " << E0 << "LL; j /= " << E0 << "LL;\n";
+      src << "        const long long x2 = (j / " << std::max(1L, BW2) << " + 1) * " << tile[2] << plus(C.vmin[v][2]) << " + j % "
+          << std::max(1L, BW2) << ";\n";
+      src << "        c2[idx - nrb - " << nc1 << "LL] = m[zy * " << PL << "LL + z1 * " << E2 << "LL + (x2" << plus(so[2]) << ")];\n";
+    }
+    src << "      }\n    }\n  }\n";
+  }
+  src << "}\n";
+}
+
 // ---------------------------------------------------------------------------
 // 2D / 3D: march the outermost dimension with rolling windows
 // ---------------------------------------------------------------------------
@@ -1225,51 +1281,11 @@ bool emit_march(Ctx& C, JitProgram& out, std::ostream& src, bool ws = false) {
   src << "}\n";
   // ---- in-place: capture the bands other units read before this step writes
   if (!ips.empty()) {
-    src << "extern \"C\" __global__ void lf_jit_capture(const LfArgs a) {\n";
-    src << "  const long long N0 = a.n0;\n";
-    src << "  const int nch = (int)((N0 + a.chunk - 1) / a.chunk);\n";
-    for (const auto& ip : ips) {
-      const size_t v = ip.v;
-      const auto& t = C.P.terminals[ip.ai];
-      const auto ex = C.extra_of(static_cast<int>(v));
-      std::vector<long> so(nd);
-      for (int d = 0; d < nd; ++d) so[d] = ex[d] - t.base[d] + C.LO[d];
-      const long E0 = t.extent[0], E1 = nd > 1 ? t.extent[1] : 1, E2 = nd > 2 ? t.extent[2] : 1, PL = E1 * E2;
-      const long BH = C.vmax[v][0] - C.vmin[v][0];
-      const long BW1 = C.vmax[v][1] - C.vmin[v][1], BW2 = nd > 2 ? C.vmax[v][2] - C.vmin[v][2] : 0;
-      const long NT1 = (C.N[1] + tile[1] - 1) / tile[1], NT2 = nd > 2 ? (C.N[2] + tile[2] - 1) / tile[2] : 1;
-      const long nc1 = (NT1 - 1) * BW1 * E0 * E2, nc2 = nd > 2 ? (NT2 - 1) * BW2 * E0 * E1 : 0;
-      src << "  {\n";
-      src << "    const T* m = reinterpret_cast<const T*>(a.t[" << ip.ai << "]);\n";
-      src << "    T* rb = reinterpret_cast<T*>(a.t[" << ip.slot << "]);\n";
-      src << "    T* c1 = reinterpret_cast<T*>(a.t[" << ip.slot + 1 << "]);\n";
-      src << "    T* c2 = reinterpret_cast<T*>(a.t[" << ip.slot + 2 << "]);\n";
-      src << "    const long long nrb = (long long)max(0, nch - 1) * " << BH * PL << "LL;\n";
-      src << "    const long long tot = nrb + " << (nc1 + nc2) << "LL;\n";
-      src << "    for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < tot; idx += (long long)gridDim.x * blockDim.x) {\n";
-      src << "      if (idx < nrb) {\n";
-      src << "        const long long p = idx % " << PL << "LL, r = idx / " << PL << "LL;\n";
-      src << "        const long long y = (r / " << BH << " + 1) * (long long)a.chunk" << plus(C.vmin[v][0]) << " + r % " << BH << ";\n";
-      src << "        rb[idx] = m[(y" << plus(so[0]) << ") * " << PL << "LL + p];\n";
-      src << "      } else if (idx < nrb + " << nc1 << "LL) {\n";
-      src << "        long long j = idx - nrb;\n";
-      src << "        const long long z2 = j % " << E2 << "LL; j /= " << E2 << "LL;\n";
-      src << "        const long long zy = j % " << E0 << "LL; j /= " << E0 << "LL;\n";
-      src << "        const long long x1 = (j / " << std::max(1L, BW1) << " + 1) * " << tile[1] << plus(C.vmin[v][1]) << " + j % "
-          << std::max(1L, BW1) << ";\n";
-      src << "        c1[idx - nrb] = m[zy * " << PL << "LL + (x1" << plus(so[1]) << ") * " << E2 << "LL + z2];\n";
-      if (nd == 3) {
-        src << "      } else {\n";
-        src << "        long long j = idx - nrb - " << nc1 << "LL;\n";
-        src << "        const long long z1 = j % " << E1 << "LL; j /= " << E1 << "LL;\n";
-        src << "        const long long zy = j % " << E0 << "LL; j /= " << E0 << "LL;\n";
-        src << "        const long long x2 = (j / " << std::max(1L, BW2) << " + 1) * " << tile[2] << plus(C.vmin[v][2]) << " + j % "
-            << std::max(1L, BW2) << ";\n";
-        src << "        c2[idx - nrb - " << nc1 << "LL] = m[zy * " << PL << "LL + z1 * " << E2 << "LL + (x2" << plus(so[2]) << ")];\n";
-      }
-      src << "      }\n    }\n  }\n";
-    }
-    src << "}\n";
+    std::vector<std::pair<size_t, int>> caps;  // (variable, terminal)
+    for (const auto& ip : ips) caps.push_back({ip.v, ip.ai});
+    std::vector<int> slots;
+    for (const auto& ip : ips) slots.push_back(ip.slot);
+    emit_capture(C, "lf_jit_capture", caps, slots, tile, src);
   }
   return true;
 }
@@ -1926,22 +1942,24 @@ bool jit_generate(const lf::Plan& P, JitProgram& out, const std::string& sources
   // the warp-specialised variant, where every streamed axiom can be fetched by
   // TMA: a dense terminal in loop-dimension order with 16-B row pitches, no
   // in-place aliases (those keep the band-capturing loader)
-  bool ws_ok = C.nd >= 2 && C.P.rs.aliases.empty() && !(std::getenv("LF_JIT_WS") && std::atoi(std::getenv("LF_JIT_WS")) == 0);
+  bool tma_ok = C.nd >= 2 && !(std::getenv("LF_JIT_WS") && std::atoi(std::getenv("LF_JIT_WS")) == 0);
   int nstaged = 0;
-  for (size_t v = 0; ws_ok && v < C.P.vars.size(); ++v) {
+  for (size_t v = 0; tma_ok && v < C.P.vars.size(); ++v) {
     const int ti = C.staged_axiom(static_cast<int>(v));
     if (ti < 0) continue;
     ++nstaged;
     const auto& t = C.P.terminals[ti];
-    for (int d = 0; d < C.nd; ++d) ws_ok &= t.dims[d] == d;
-    ws_ok &= (t.extent[C.nd - 1] * out.elem_bytes) % 16 == 0;
+    for (int d = 0; d < C.nd; ++d) tma_ok &= t.dims[d] == d;
+    tma_ok &= (t.extent[C.nd - 1] * out.elem_bytes) % 16 == 0;
   }
-  ws_ok &= nstaged > 0 && nstaged <= kJitMaxMaps;
-  if (ws_ok) {
+  tma_ok &= nstaged > 0 && nstaged <= kJitMaxMaps;
+  if (tma_ok) {
     std::string variants;
     std::ostringstream ws;
     out.ws_maps.clear();
-    if (emit_march(C, out, ws, true) && !out.ws_maps.empty() && static_cast<int>(out.ws_maps.size()) <= kJitMaxMaps) {
+    // in-place aliases keep the band-capturing plain march in 3D
+    if (C.P.rs.aliases.empty() && emit_march(C, out, ws, true) && !out.ws_maps.empty() &&
+        static_cast<int>(out.ws_maps.size()) <= kJitMaxMaps) {
       out.has_ws = true;
       variants += ws.str();
     } else {

@@ -112,6 +112,10 @@ void emit_prelude(Ctx& C, std::ostream& src, int threads, int min_blocks, const 
 // mbarrier / TMA device helpers and the tensor-map parameter block (emitted
 // once, before the first kernel that takes LfMaps)
 void emit_tma_helpers(std::ostream& src);
+// in place: the band-capture kernel `name` for the aliased axioms caps =
+// (variable, terminal), band buffers at a.t[slots[q] .. slots[q] + 2], inner tile `tile`
+void emit_capture(Ctx& C, const char* name, const std::vector<std::pair<size_t, int>>& caps,
+                  const std::vector<int>& slots, const std::vector<int>& tile, std::ostream& src);
 // 2D register march (lf_jit_step_rm); false when the chain does not fit it
 bool emit_rmarch(Ctx& C, JitProgram& out, std::ostream& src);
 

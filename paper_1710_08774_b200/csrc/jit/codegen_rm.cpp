@@ -44,8 +44,81 @@ std::string num(long v) { return v < 0 ? "m" + std::to_string(-v) : std::to_stri
 
 }  // namespace
 
+// In place: the column band around an internal tile boundary e holds the
+// cells neighbouring tiles read, [e + lo1, e + hi1), widened to whole 32-B
+// sectors of the grid row, so no grid sector is left half written until the
+// commit (a partly written sector costs L2 a read-modify-write).  Logical
+// columns [zs(e), ze(e)); at most bw columns.
+struct Zone {
+  long so1 = 0, se = 4, lo1 = 0, hi1 = 0, bw = 0;
+  std::string zs(const std::string& e) const {
+    return "((((" + e + ")" + plus(lo1 + so1) + ") & ~" + std::to_string(se - 1) + ")" + plus(-so1) + ")";
+  }
+  std::string ze(const std::string& e) const {
+    return "((((" + e + ")" + plus(hi1 + so1 + se - 1) + ") & ~" + std::to_string(se - 1) + ")" + plus(-so1) + ")";
+  }
+};
+Zone zone_of(const Ctx& C, size_t v, int ti, int eb) {
+  Zone z;
+  z.so1 = -C.P.terminals[ti].base[1] + C.LO[1];
+  z.se = 32 / eb;
+  z.lo1 = C.vmin[v][1];
+  z.hi1 = C.vmax[v][1];
+  z.bw = z.hi1 - z.lo1 + 2 * (z.se - 1);
+  return z;
+}
+
+// In place, 2D: after the step, copy the deferred boundary writes from the
+// band buffers into the grid -- the row bands (full rows around the internal
+// chunk boundaries, domain columns) and the column bands (around the internal
+// tile boundaries of width `tile1`, rows outside every row band)
+void emit_commit2(Ctx& C, const char* name, const std::vector<std::pair<size_t, int>>& caps,
+                  const std::vector<int>& slots, int tile1, std::ostream& src) {
+  // one block per band row (its domain columns), then one thread per
+  // (band column, row) pair
+  src << "extern \"C\" __global__ void " << name << "(const LfArgs a) {\n";
+  src << "  const int N0 = (int)a.n0;\n";
+  src << "  const int nch = (N0 + a.chunk - 1) / a.chunk;\n";
+  for (size_t q = 0; q < caps.size(); ++q) {
+    const size_t v = caps[q].first;
+    const auto& t = C.P.terminals[caps[q].second];
+    const long so0 = -t.base[0] + C.LO[0], so1 = -t.base[1] + C.LO[1];
+    const long E1 = t.extent[1], E0 = t.extent[0];
+    const long lo0 = C.vmin[v][0], hi0 = C.vmax[v][0], lo1 = C.vmin[v][1], hi1 = C.vmax[v][1];
+    const Zone z = zone_of(C, v, caps[q].second, static_cast<int>(t.elem_bytes));
+    const long BH = hi0 - lo0, BW = z.bw;
+    const long NT = (C.N[1] + tile1 - 1) / tile1;
+    (void)lo1;
+    (void)hi1;
+    src << "  {\n";
+    src << "    T* m = reinterpret_cast<T*>(a.t[" << caps[q].second << "]);\n";
+    src << "    const T* rb = reinterpret_cast<const T*>(a.t[" << slots[q] << "]);\n";
+    src << "    const T* cb = reinterpret_cast<const T*>(a.t[" << slots[q] + 1 << "]);\n";
+    src << "    const int nrr = max(0, nch - 1) * " << BH << ";  // band rows\n";
+    src << "    const int ncol = (N0 * " << (NT - 1) * BW << " + blockDim.x - 1) / blockDim.x;  // blocks of (band column, row) pairs\n";
+    src << "    for (int task = blockIdx.x; task < nrr + ncol; task += gridDim.x) {\n";
+    src << "      if (task < nrr) {\n";
+    src << "        const int y = (task / " << BH << " + 1) * a.chunk" << plus(lo0) << " + task % " << BH << ";\n";
+    src << "        if (y < 0 || y >= N0) continue;\n";
+    src << "        T* d = m + (long long)(y" << plus(so0) << ") * " << E1 << "LL" << plus(so1) << ";\n";
+    src << "        const T* sr = rb + (long long)task * " << E1 << "LL" << plus(so1) << ";\n";
+    src << "        for (int x = threadIdx.x; x < " << C.N[1] << "; x += blockDim.x) d[x] = sr[x];\n";
+    src << "      } else {\n";
+    src << "        const int p = (task - nrr) * blockDim.x + threadIdx.x;\n";
+    src << "        if (p >= N0 * " << (NT - 1) * BW << ") continue;\n";
+    src << "        const int kc = p / N0, y = p - kc * N0;  // band column kc = k * BW + c\n";
+    src << "        const int bb = (y" << plus(-lo0) << ") / a.chunk * a.chunk;  // the one boundary whose row band could hold y\n";
+    src << "        if (bb > 0 && bb < N0 && y < bb" << plus(hi0) << ") continue;  // committed with the row band\n";
+    src << "        const int e = (kc / " << BW << " + 1) * " << tile1 << ", x = " << z.zs("e") << " + kc % " << BW << ";\n";
+    src << "        if (x >= 0 && x < " << C.N[1] << " && x < " << z.ze("e") << ") m[(long long)(y" << plus(so0) << ") * " << E1 << "LL" << plus(so1)
+        << " + x] = cb[(long long)kc * " << E0 << " + y" << plus(so0) << "];\n";
+    src << "      }\n    }\n  }\n";
+  }
+  src << "}\n";
+}
+
 bool emit_rmarch(Ctx& C, JitProgram& out, std::ostream& src) {
-  if (C.nd != 2 || !C.P.rs.aliases.empty()) return false;
+  if (C.nd != 2) return false;
   const int eb = out.elem_bytes;
   const int CH = 16 / eb;  // elements per 16-B chunk
   int V = eb == 8 ? 2 : 4;
@@ -198,6 +271,68 @@ bool emit_rmarch(Ctx& C, JitProgram& out, std::ostream& src) {
   out.rm_threads = 32 * (NW + 1);
   out.rm_inner_tiles = inner;
   out.rm_maps.clear();
+  // in place (config.aliases, the caller passes one buffer): whole (chunk,
+  // CTA tile) units that defer their boundary writes.  A unit's cells that a
+  // neighbouring unit still reads during the step -- rows within the read
+  // reach of an internal chunk boundary, columns within that of an internal
+  // tile boundary -- go to band buffers instead of the grid, and a commit
+  // kernel copies them in after the step.  So the grid a unit streams from
+  // holds the step's input everywhere another unit looks, every row is one
+  // TMA box as out of place, and no halo needs patching.  Bands use the plain
+  // march's argument slots (row bands full width, [boundary][row][col]; column
+  // bands column-major, [boundary][col within the band][row], so an edge lane's
+  // writes down the march fill whole sectors).
+  struct IP {
+    size_t v;
+    int ai, gi, slot;
+  };
+  std::vector<IP> ips;
+  out.rm_inplace.clear();
+  {
+    const int nterm = static_cast<int>(C.P.terminals.size());
+    for (const auto& [in_ext, out_ext] : C.P.rs.aliases) {
+      int ai = -1, gi = -1;
+      for (int i = 0; i < nterm; ++i) {
+        if (!C.P.terminals[i].is_goal && C.P.terminals[i].name == in_ext) ai = i;
+        if (C.P.terminals[i].is_goal && C.P.terminals[i].name == out_ext) gi = i;
+      }
+      if (ai < 0 || gi < 0) continue;
+      const int v = C.P.terminals[ai].var;
+      const auto& t = C.P.terminals[ai];
+      if (v < 0 || staged[v] < 0 || t.extent != C.P.terminals[gi].extent || t.base != C.P.terminals[gi].base) {
+        out.rm_inplace.clear();
+        ips.clear();
+        break;
+      }
+      IP ip{static_cast<size_t>(v), ai, gi, nterm + 3 * static_cast<int>(ips.size())};
+      if (ip.slot + 3 > 32) {
+        out.rm_inplace.clear();
+        ips.clear();
+        break;
+      }
+      ips.push_back(ip);
+      JitProgram::Inplace q;
+      q.ai = ai;
+      q.gi = gi;
+      q.bh = C.vmax[v][0] - C.vmin[v][0];
+      q.bw1 = static_cast<int>(zone_of(C, static_cast<size_t>(v), gi, eb).bw);
+      if (T1 < 2 * q.bw1) {  // zones of neighbouring boundaries must not meet
+        out.rm_inplace.clear();
+        ips.clear();
+        break;
+      }
+      q.e0 = t.extent[0];
+      q.e1 = t.extent[1];
+      q.t1 = static_cast<int>(T1);
+      q.n1 = C.N[1];
+      out.rm_inplace.push_back(q);
+    }
+  }
+  auto ip_of_goal = [&](int ti) -> const IP* {
+    for (const auto& ip : ips)
+      if (ip.gi == ti) return &ip;
+    return nullptr;
+  };
 
   // trip range relative to the chunk [r0, r1)
   int TS = INT_MAX, TE = INT_MIN;
@@ -208,7 +343,7 @@ bool emit_rmarch(Ctx& C, JitProgram& out, std::ostream& src) {
   for (size_t v = 0; v < nv; ++v)
     if (staged[v] >= 0) TS = std::min(TS, C.vmin[v][0] - lead[v]);
 
-  int minb = 2;
+  int minb = 3;  // <= 72 registers: 3 CTAs of 9 warps per SM (the in-place store path needs 75 uncapped)
   if (const char* e = std::getenv("LF_JIT_RM_MINB")) minb = std::max(1, std::atoi(e));
   emit_prelude(C, src, out.rm_threads, minb, "lf_jit_step_rm");
   const std::string VT = eb == 8 ? "double2" : "float4";
@@ -249,6 +384,29 @@ bool emit_rmarch(Ctx& C, JitProgram& out, std::ostream& src) {
   src << "  const int o1 = bt * " << T1 << ";\n";
   src << "  const int ow = o1 + warp * " << tw << ";  // this warp's strip\n";
   src << "  const bool wact = ow < " << C.N[1] << ";\n";
+  // in place: which of this lane's cells fall in a column band, and where in
+  // the band they go -- fixed for the unit, so the march only tests a mask
+  for (size_t q = 0; q < ips.size(); ++q) {
+    const int v = static_cast<int>(ips[q].v);
+    const auto& t = C.P.terminals[ips[q].gi];
+    const long so0 = -t.base[0] + C.LO[0];
+    const Zone z = zone_of(C, ips[q].v, ips[q].gi, eb);
+    src << "  unsigned zm" << q << " = 0;\n";
+    src << "  long long zb" << q << "[" << V << "];\n";
+    src << "  if (a.inplace && (warp == 0 || warp == " << NW - 1 << ")) {\n";
+    src << "    #pragma unroll\n";
+    src << "    for (int i = 0; i < " << V << "; ++i) {\n";
+    src << "      const int c = " << cs << " + lane * " << V << " + i, xi = ow + c;\n";
+    src << "      int e = -1;\n";
+    src << "      if (c >= 0 && c < " << tw << " && xi < " << C.N[1] << ") {\n";
+    src << "        if (o1 > 0 && xi < " << z.ze("o1") << ") e = o1;\n";
+    src << "        else if (o1 + " << T1 << " < " << C.N[1] << " && xi >= " << z.zs("o1 + " + std::to_string(T1)) << ") e = o1 + " << T1 << ";\n";
+    src << "      }\n";
+    src << "      zb" << q << "[i] = e < 0 ? 0 : ((long long)(e / " << T1 << " - 1) * " << z.bw << " + (xi - " << z.zs("e")
+        << ")) * " << t.extent[0] << "LL" << plus(so0) << ";\n";
+    src << "      if (e >= 0) zm" << q << " |= 1u << i;\n";
+    src << "    }\n  }\n";
+  }
 
   auto rowbase = [&](size_t v, int off) -> std::string {
     const int W = win[v];
@@ -273,6 +431,7 @@ bool emit_rmarch(Ctx& C, JitProgram& out, std::ostream& src) {
     tm.box[1] = 1;
     out.rm_maps.push_back(tm);
   }
+
   // register windows rotate by renaming: the trip loop is unrolled U = lcm(W_v)
   // times and copy u keeps the row of logical slot k in R_v[(k + u) % W_v] (no
   // moves); windows whose lcm exceeds 6 shift by moves at the end of each trip
@@ -523,6 +682,31 @@ bool emit_rmarch(Ctx& C, JitProgram& out, std::ostream& src) {
       src << "          if (yy >= r0 && yy < r1) {\n";
       src << "            T* gp = t" << ti << " + " << C.tidx(ti, {"yy", "x"}, std::vector<int>(2, 0)) << ";\n";
       const std::string gv = "G" + std::to_string(gi) + "_" + o->param;
+      const IP* ip = ip_of_goal(ti);
+      if (ip) {
+        // in place: deferred boundary writes (row zone: the whole row into the
+        // row band; column zone: those cells into the column band)
+        const int v = static_cast<int>(ip->v);
+        const int lo0 = C.vmin[v][0], hi0 = C.vmax[v][0], lo1 = C.vmin[v][1], hi1 = C.vmax[v][1];
+        const size_t q = static_cast<size_t>(ip - ips.data());
+        src << "            if (a.inplace) {\n";
+        src << "              int b = -1;\n";
+        src << "              if (r0 > 0 && yy < r0" << plus(hi0) << ") b = r0;\n";
+        src << "              else if (r1 < N0 && yy >= r1" << plus(lo0) << ") b = r1;\n";
+        src << "              if (b >= 0) gp = reinterpret_cast<T*>(a.t[" << ip->slot << "]) + ((long long)(b / a.chunk - 1) * "
+            << hi0 - lo0 << " + (yy - b" << plus(-lo0) << ")) * " << t.extent[1] << "LL + (x" << plus(so) << ");\n";
+        src << "              else if (zm" << q << ") {  // cells in a column band\n";
+        src << "                T* cb = reinterpret_cast<T*>(a.t[" << ip->slot + 1 << "]) + yy;\n";
+        src << "                #pragma unroll\n";
+        src << "                for (int i = 0; i < " << V << "; ++i) {\n";
+        src << "                  if ((zm" << q << " >> i) & 1) cb[zb" << q << "[i]] = " << gv << "[i];\n";
+        src << "                  else if (c + i >= 0 && c + i < " << tw << " && x + i < " << C.N[1] << ") gp[i] = " << gv << "[i];\n";
+        src << "                }\n";
+        src << "                gp = nullptr;\n";
+        src << "              }\n";
+        src << "            }\n";
+        src << "            if (gp)\n";
+      }
       if (vec_ok) {
         src << "            if (c >= 0 && c + " << V << " <= " << tw << " && x + " << V << " <= " << C.N[1] << ") {\n";
         for (int c = 0; c < V / CH; ++c) {
@@ -558,6 +742,15 @@ bool emit_rmarch(Ctx& C, JitProgram& out, std::ostream& src) {
   src << "  }\n";  // trips
   src << "  }\n";  // units
   src << "}\n";
+  if (!ips.empty()) {
+    std::vector<std::pair<size_t, int>> caps;
+    std::vector<int> slots;
+    for (const auto& ip : ips) {
+      caps.push_back({ip.v, ip.gi});
+      slots.push_back(ip.slot);
+    }
+    emit_commit2(C, "lf_jit_commit_rm", caps, slots, static_cast<int>(T1), src);
+  }
   return true;
 }
 

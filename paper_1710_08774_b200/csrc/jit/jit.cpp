@@ -142,26 +142,15 @@ JitKernel::~JitKernel() {
 // chunk boundaries and the columns at tile boundaries that a unit reads but
 // another unit writes, and the step reads those cells from the copies.  The
 // copies are O(surface) -- the grid itself is never duplicated.
-int JitKernel::run_inplace(const ExecArgs& a, JitArgs& args, std::string& err) {
-  const auto& rs = a.plan->rs;
-  const auto& T = a.plan->terminals;
-  if (a.slab && (a.slab->lo != 0 || a.slab->hi != a.slab->global || a.slab->part_hi > a.slab->part_lo)) {
-    err = "in-place runs cover the whole domain (no slabs)";
-    return LF_ERR_UNSUPPORTED;
-  }
-  if (!capture_) {
-    err = "in-place capture kernel missing";
-    return LF_ERR_INTERNAL;
-  }
-  const long rows = rs.ranges[0].trips();
-  // chunk: about two units per resident CTA, at least 8 pipeline depths
-  long chunk = (rows * prog_.inner_tiles + 2L * resident_ - 1) / (2L * resident_);
-  chunk = std::min(rows, std::max(chunk, 8L * std::max(1, prog_.prologue)));
-  if (const char* e = std::getenv("LF_JIT_CHUNK")) chunk = std::max(1L, std::min<long>(rows, std::atol(e)));
-  const long nch = (rows + chunk - 1) / chunk;
+static long pick_chunk(long rows, long inner, long resident, long fill, long max_chunk);
+
+// band buffers of an in-place launch: per aliased axiom, the rows at the nch-1
+// internal chunk boundaries and the columns at the internal boundaries of the
+// inner tiles the descriptors name
+int JitKernel::bands_for(const std::vector<JitProgram::Inplace>& list, long nch, long, std::string& err) {
   const size_t eb = static_cast<size_t>(prog_.elem_bytes);
   std::vector<size_t> need;
-  for (const auto& q : prog_.inplace) {
+  for (const auto& q : list) {
     const long nt1 = (q.n1 + q.t1 - 1) / q.t1, nt2 = (q.n2 + q.t2 - 1) / q.t2;
     need.push_back(std::max<long>(0, nch - 1) * q.bh * q.e1 * q.e2 * eb);
     need.push_back(std::max<long>(0, nt1 - 1) * q.bw1 * q.e0 * q.e2 * eb);
@@ -180,12 +169,70 @@ int JitKernel::run_inplace(const ExecArgs& a, JitArgs& args, std::string& err) {
     }
     band_bytes_ = need;
   }
+  return LF_OK;
+}
+
+int JitKernel::run_inplace(const ExecArgs& a, JitArgs& args, std::string& err) {
+  const auto& rs = a.plan->rs;
+  const auto& T = a.plan->terminals;
+  if (a.slab && (a.slab->lo != 0 || a.slab->hi != a.slab->global || a.slab->part_hi > a.slab->part_lo)) {
+    err = "in-place runs cover the whole domain (no slabs)";
+    return LF_ERR_UNSUPPORTED;
+  }
+  if (!capture_) {
+    err = "in-place capture kernel missing";
+    return LF_ERR_INTERNAL;
+  }
+  const long rows = rs.ranges[0].trips();
   args.n0 = rows;
   args.row_lo = 0;
   args.row_hi = static_cast<int>(rows);
   args.top = args.bottom = 1;
-  args.chunk = static_cast<int>(chunk);
   args.inplace = 1;
+  // the register march (2D), when it covers every aliased pair: units defer
+  // their boundary writes to the bands, lf_jit_commit_rm copies them in after
+  // the step (codegen_rm.cpp)
+  if (step_rm_ && commit_rm_ && prog_.rm_inplace.size() == prog_.inplace.size()) {
+    long chunk = pick_chunk(rows, prog_.rm_inner_tiles, resident_rm_, prog_.prologue, rows);
+    long bh = 1;
+    for (const auto& q : prog_.rm_inplace) bh = std::max<long>(bh, q.bh);
+    chunk = std::min(rows, std::max({chunk, 8L * std::max(1, prog_.prologue), bh}));
+    if (const char* e = std::getenv("LF_JIT_CHUNK")) chunk = std::max(bh, std::min<long>(rows, std::atol(e)));
+    const long nch = (rows + chunk - 1) / chunk;
+    int st = bands_for(prog_.rm_inplace, nch, 0, err);
+    if (st != LF_OK) return st;
+    args.chunk = static_cast<int>(chunk);
+    for (size_t i = 0; i < T.size(); ++i) args.t[i] = a.terms[i];
+    for (size_t k = 0; k < bands_.size(); ++k) args.t[T.size() + k] = bands_[k];
+    JitMaps maps;
+    bool goals_aligned = true;
+    for (size_t i = 0; i < T.size(); ++i)
+      if (T[i].is_goal) goals_aligned &= reinterpret_cast<uintptr_t>(a.terms[i]) % 16 == 0;
+    std::vector<void*> bufs(a.terms, a.terms + T.size());
+    if (goals_aligned && tma_maps(prog_.rm_maps, bufs, rows, maps)) {
+      const long units = nch * prog_.rm_inner_tiles;
+      const dim3 grid(static_cast<unsigned>(std::max<long>(1, std::min<long>(resident_rm_, units))));
+      for (int s = 0; s < a.steps; ++s) {
+        st = launch(step_rm_, grid, dim3(prog_.rm_threads), prog_.rm_smem_bytes, a.stream, &args, err, &maps);
+        if (st != LF_OK) return st;
+        st = launch(commit_rm_, dim3(592), dim3(256), 0, a.stream, &args, err);
+        if (st != LF_OK) return st;
+        if (fill_ && prog_.has_fill) {
+          st = launch(fill_, dim3(592), dim3(256), 0, a.stream, &args, err);
+          if (st != LF_OK) return st;
+        }
+      }
+      return LF_OK;
+    }
+  }
+  // chunk: about two units per resident CTA, at least 8 pipeline depths
+  long chunk = (rows * prog_.inner_tiles + 2L * resident_ - 1) / (2L * resident_);
+  chunk = std::min(rows, std::max(chunk, 8L * std::max(1, prog_.prologue)));
+  if (const char* e = std::getenv("LF_JIT_CHUNK")) chunk = std::max(1L, std::min<long>(rows, std::atol(e)));
+  const long nch = (rows + chunk - 1) / chunk;
+  int bst = bands_for(prog_.inplace, nch, 0, err);
+  if (bst != LF_OK) return bst;
+  args.chunk = static_cast<int>(chunk);
   for (size_t i = 0; i < T.size(); ++i) args.t[i] = a.terms[i];
   for (size_t k = 0; k < bands_.size(); ++k) args.t[T.size() + k] = bands_[k];
   const long units = nch * prog_.inner_tiles;
@@ -297,18 +344,20 @@ static long pick_chunk(long rows, long inner, long resident, long fill, long max
 // tensor maps of the streamed axioms for this launch's buffers; false (plain
 // kernel) when a buffer is not 16-B aligned or the driver refuses a map
 bool JitKernel::tma_maps(const std::vector<JitProgram::Tma>& list, const std::vector<void*>& bufs, long rows,
-                         JitMaps& maps) {
+                         JitMaps& maps, long boundaries) {
   static const bool off = std::getenv("LF_JIT_WS") && std::atoi(std::getenv("LF_JIT_WS")) == 0;
   if (off) return false;
   const CUtensorMapDataType dt = prog_.elem_bytes == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
   const long n0 = plan_rows_;
   for (size_t k = 0; k < list.size(); ++k) {
     const auto& m = list[k];
-    const void* base = bufs[m.term];
+    const void* base = bufs[m.band >= 0 ? m.band : m.term];
     if (reinterpret_cast<uintptr_t>(base) % 16) return false;
     uint64_t dims[3] = {m.extent[0], m.extent[1], m.extent[2]};
-    // outermost extent of the launch domain: a slab holds rows + the terminal's halo rows
-    dims[m.rank - 1] = static_cast<uint64_t>(static_cast<long>(m.extent[m.rank - 1]) - n0 + rows);
+    if (m.band >= 0)  // in-place row bands: band_rows per internal chunk boundary
+      dims[m.rank - 1] = static_cast<uint64_t>(std::max(1L, boundaries * m.band_rows));
+    else  // outermost extent of the launch domain: a slab holds rows + the terminal's halo rows
+      dims[m.rank - 1] = static_cast<uint64_t>(static_cast<long>(m.extent[m.rank - 1]) - n0 + rows);
     std::string e;
     if (!make_tensor_map(reinterpret_cast<CUtensorMap*>(&maps.m[k]), base, dt, prog_.elem_bytes, m.rank, dims, m.box, e))
       return false;
@@ -359,6 +408,7 @@ int JitKernel::run(const ExecArgs& a, std::string& err) {
     CUfunction f;
     if (d.get(&f, m, "lf_jit_fill") == CUDA_SUCCESS) fill_ = f;
     if (d.get(&f, m, "lf_jit_capture") == CUDA_SUCCESS) capture_ = f;
+    if (d.get(&f, m, "lf_jit_commit_rm") == CUDA_SUCCESS) commit_rm_ = f;
     if (!prog_.nest_kernels.empty()) {
       for (const auto& nk : prog_.nest_kernels) {
         if (d.get(&f, m, nk.fn.c_str()) != CUDA_SUCCESS) {

@@ -56,6 +56,10 @@ struct JitProgram {
   // extents innermost first (the outermost one is the launch domain's at run time)
   struct Tma {
     int term = -1;
+    // >= 0: an in-place row-band buffer a.t[band] instead of a terminal; its
+    // rows are band_rows per internal chunk boundary (known at launch)
+    int band = -1;
+    int band_rows = 0;
     int rank = 0;
     uint64_t extent[3] = {1, 1, 1};
     unsigned box[3] = {1, 1, 1};
@@ -69,6 +73,7 @@ struct JitProgram {
   // windows, no CTA barriers; preferred over lf_jit_step_ws where it compiles
   bool has_rm = false;
   std::vector<Tma> rm_maps;
+  std::vector<Inplace> rm_inplace;  // as `inplace`, for the register march's tile
   size_t rm_smem_bytes = 0;
   long rm_inner_tiles = 1;
   int rm_threads = 288;
@@ -124,7 +129,12 @@ class JitKernel {
   int launch(void* fn, dim3 grid, dim3 block, size_t smem, cudaStream_t st, void* args, std::string& err,
              void* args2 = nullptr);
   int run_nests(const ExecArgs& a, std::string& err);
-  bool tma_maps(const std::vector<JitProgram::Tma>& list, const std::vector<void*>& bufs, long rows, JitMaps& maps);
+  // bufs: the launch's argument slots (terminals, then in-place bands);
+  // boundaries: internal chunk boundaries of an in-place launch (band rows)
+  bool tma_maps(const std::vector<JitProgram::Tma>& list, const std::vector<void*>& bufs, long rows, JitMaps& maps,
+                long boundaries = 0);
+  void* commit_rm_ = nullptr;  // in-place register march: deferred boundary writes into the grid
+  int bands_for(const std::vector<JitProgram::Inplace>& list, long nch, long nt_of_tile1, std::string& err);
   long plan_rows_ = 0;  // trips of the outermost loop dimension (whole domain)
   int run_inplace(const ExecArgs& a, JitArgs& args, std::string& err);
 };

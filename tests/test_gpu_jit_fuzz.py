@@ -124,15 +124,19 @@ def test_random_chain_matches_generic_oracle(seed, tmp_path):
 
 
 @pytest.mark.gpu
-def test_random_chains_with_opt_in_vector_columns():
-    """LF_JIT_VEC=2 (2D: two adjacent columns per thread sharing window loads,
-    opt-in) on the same random chains, in a subprocess (the knob is read at
-    plan creation)."""
+@pytest.mark.parametrize("knob", ["LF_JIT_VEC=2", "LF_JIT_RM_PACK=1", "LF_JIT_RM_UNROLL=0"])
+def test_random_chains_with_opt_in_variants(knob):
+    """Opt-in / comparison variants on the same random chains, in a subprocess
+    (the knobs are read at plan creation): LF_JIT_VEC=2 (plain march, two
+    adjacent columns per thread sharing window loads), LF_JIT_RM_PACK=1
+    (register march, fp32 cells in fp32x2 pairs), LF_JIT_RM_UNROLL=0
+    (register windows shifted by moves instead of renamed)."""
     import os
     import subprocess
     import sys
     from pathlib import Path
-    env = dict(os.environ, LF_JIT_VEC="2")
+    k, v = knob.split("=")
+    env = dict(os.environ, **{k: v})
     r = subprocess.run([sys.executable, "-m", "pytest", __file__, "-q", "-m", "gpu", "-k", "matches_generic_oracle"],
                        env=env, capture_output=True, text=True, timeout=600, cwd=str(Path(__file__).parents[1]))
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
