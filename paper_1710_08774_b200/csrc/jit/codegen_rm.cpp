@@ -74,9 +74,10 @@ Zone zone_of(const Ctx& C, size_t v, int ti, int eb) {
 // tile boundaries of width `tile1`, rows outside every row band)
 void emit_commit2(Ctx& C, const char* name, const std::vector<std::pair<size_t, int>>& caps,
                   const std::vector<int>& slots, int tile1, std::ostream& src) {
-  // one block per band row (its domain columns), then one thread per
-  // (band column, row) pair
-  src << "extern \"C\" __global__ void " << name << "(const LfArgs a) {\n";
+  // flat over the band cells -- (band row, domain column) pairs, then (band
+  // column, row) pairs -- four per thread, a block per 1024; the launch covers
+  // the largest band set (jit.cpp)
+  src << "extern \"C\" __global__ void __launch_bounds__(256) " << name << "(const LfArgs a) {\n";
   src << "  const int N0 = (int)a.n0;\n";
   src << "  const int nch = (N0 + a.chunk - 1) / a.chunk;\n";
   for (size_t q = 0; q < caps.size(); ++q) {
@@ -84,34 +85,31 @@ void emit_commit2(Ctx& C, const char* name, const std::vector<std::pair<size_t, 
     const auto& t = C.P.terminals[caps[q].second];
     const long so0 = -t.base[0] + C.LO[0], so1 = -t.base[1] + C.LO[1];
     const long E1 = t.extent[1], E0 = t.extent[0];
-    const long lo0 = C.vmin[v][0], hi0 = C.vmax[v][0], lo1 = C.vmin[v][1], hi1 = C.vmax[v][1];
+    const long lo0 = C.vmin[v][0], hi0 = C.vmax[v][0];
     const Zone z = zone_of(C, v, caps[q].second, static_cast<int>(t.elem_bytes));
     const long BH = hi0 - lo0, BW = z.bw;
     const long NT = (C.N[1] + tile1 - 1) / tile1;
-    (void)lo1;
-    (void)hi1;
     src << "  {\n";
     src << "    T* m = reinterpret_cast<T*>(a.t[" << caps[q].second << "]);\n";
     src << "    const T* rb = reinterpret_cast<const T*>(a.t[" << slots[q] << "]);\n";
     src << "    const T* cb = reinterpret_cast<const T*>(a.t[" << slots[q] + 1 << "]);\n";
-    src << "    const int nrr = max(0, nch - 1) * " << BH << ";  // band rows\n";
-    src << "    const int ncol = (N0 * " << (NT - 1) * BW << " + blockDim.x - 1) / blockDim.x;  // blocks of (band column, row) pairs\n";
-    src << "    for (int task = blockIdx.x; task < nrr + ncol; task += gridDim.x) {\n";
-    src << "      if (task < nrr) {\n";
-    src << "        const int y = (task / " << BH << " + 1) * a.chunk" << plus(lo0) << " + task % " << BH << ";\n";
-    src << "        if (y < 0 || y >= N0) continue;\n";
-    src << "        T* d = m + (long long)(y" << plus(so0) << ") * " << E1 << "LL" << plus(so1) << ";\n";
-    src << "        const T* sr = rb + (long long)task * " << E1 << "LL" << plus(so1) << ";\n";
-    src << "        for (int x = threadIdx.x; x < " << C.N[1] << "; x += blockDim.x) d[x] = sr[x];\n";
-    src << "      } else {\n";
-    src << "        const int p = (task - nrr) * blockDim.x + threadIdx.x;\n";
-    src << "        if (p >= N0 * " << (NT - 1) * BW << ") continue;\n";
-    src << "        const int kc = p / N0, y = p - kc * N0;  // band column kc = k * BW + c\n";
+    src << "    const long long nr = (long long)max(0, nch - 1) * " << BH * C.N[1] << ";  // row-band cells\n";
+    src << "    const long long nc = (long long)N0 * " << (NT - 1) * BW << ";  // column-band cells\n";
+    src << "    #pragma unroll\n";
+    src << "    for (int j = 0; j < 4; ++j) {\n";
+    src << "      const long long p = (long long)blockIdx.x * 1024 + j * 256 + threadIdx.x;\n";
+    src << "      if (p < nr) {\n";
+    src << "        const int r = (int)(p / " << C.N[1] << "), x = (int)(p - (long long)r * " << C.N[1] << ");\n";
+    src << "        const int y = (r / " << BH << " + 1) * a.chunk" << plus(lo0) << " + r % " << BH << ";\n";
+    src << "        if (y >= 0 && y < N0) m[(long long)(y" << plus(so0) << ") * " << E1 << "LL" << plus(so1) << " + x] = rb[(long long)r * "
+        << E1 << "LL" << plus(so1) << " + x];\n";
+    src << "      } else if (p - nr < nc) {\n";
+    src << "        const int kc = (int)((p - nr) / N0), y = (int)(p - nr - (long long)kc * N0);  // band column kc = k * bw + c\n";
     src << "        const int bb = (y" << plus(-lo0) << ") / a.chunk * a.chunk;  // the one boundary whose row band could hold y\n";
-    src << "        if (bb > 0 && bb < N0 && y < bb" << plus(hi0) << ") continue;  // committed with the row band\n";
     src << "        const int e = (kc / " << BW << " + 1) * " << tile1 << ", x = " << z.zs("e") << " + kc % " << BW << ";\n";
-    src << "        if (x >= 0 && x < " << C.N[1] << " && x < " << z.ze("e") << ") m[(long long)(y" << plus(so0) << ") * " << E1 << "LL" << plus(so1)
-        << " + x] = cb[(long long)kc * " << E0 << " + y" << plus(so0) << "];\n";
+    src << "        if (!(bb > 0 && bb < N0 && y < bb" << plus(hi0) << ") && x >= 0 && x < " << C.N[1] << " && x < " << z.ze("e")
+        << ") m[(long long)(y" << plus(so0) << ") * " << E1 << "LL" << plus(so1) << " + x] = cb[(long long)kc * " << E0 << " + y"
+        << plus(so0) << "];\n";
     src << "      }\n    }\n  }\n";
   }
   src << "}\n";
@@ -690,12 +688,13 @@ bool emit_rmarch(Ctx& C, JitProgram& out, std::ostream& src) {
         const int lo0 = C.vmin[v][0], hi0 = C.vmax[v][0], lo1 = C.vmin[v][1], hi1 = C.vmax[v][1];
         const size_t q = static_cast<size_t>(ip - ips.data());
         src << "            if (a.inplace) {\n";
-        src << "              int b = -1;\n";
-        src << "              if (r0 > 0 && yy < r0" << plus(hi0) << ") b = r0;\n";
-        src << "              else if (r1 < N0 && yy >= r1" << plus(lo0) << ") b = r1;\n";
-        src << "              if (b >= 0) gp = reinterpret_cast<T*>(a.t[" << ip->slot << "]) + ((long long)(b / a.chunk - 1) * "
-            << hi0 - lo0 << " + (yy - b" << plus(-lo0) << ")) * " << t.extent[1] << "LL + (x" << plus(so) << ");\n";
-        src << "              else if (zm" << q << ") {  // cells in a column band\n";
+        src << "              int br = -1;  // row of the row band (band k - 1 at chunk boundary k)\n";
+        src << "              if (r0 > 0 && yy < r0" << plus(hi0) << ") br = (ci - 1) * " << hi0 - lo0 << " + (yy - r0" << plus(-lo0) << ");\n";
+        src << "              else if (r1 < N0 && yy >= r1" << plus(lo0) << ") br = ci * " << hi0 - lo0 << " + (yy - r1" << plus(-lo0)
+            << ");\n";
+        src << "              if (br >= 0) gp = reinterpret_cast<T*>(a.t[" << ip->slot << "]) + (long long)br * " << t.extent[1]
+            << "LL + (x" << plus(so) << ");\n";
+        src << "              if (br < 0 && zm" << q << ") {  // cells in a column band\n";
         src << "                T* cb = reinterpret_cast<T*>(a.t[" << ip->slot + 1 << "]) + yy;\n";
         src << "                #pragma unroll\n";
         src << "                for (int i = 0; i < " << V << "; ++i) {\n";

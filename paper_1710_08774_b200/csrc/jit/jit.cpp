@@ -212,10 +212,14 @@ int JitKernel::run_inplace(const ExecArgs& a, JitArgs& args, std::string& err) {
     if (goals_aligned && tma_maps(prog_.rm_maps, bufs, rows, maps)) {
       const long units = nch * prog_.rm_inner_tiles;
       const dim3 grid(static_cast<unsigned>(std::max<long>(1, std::min<long>(resident_rm_, units))));
+      long band_cells = 1;  // the commit kernel's flat index space (largest aliased pair)
+      for (const auto& q : prog_.rm_inplace)
+        band_cells = std::max(band_cells, (nch - 1) * q.bh * q.n1 + rows * ((q.n1 + q.t1 - 1) / q.t1 - 1) * q.bw1);
+      const unsigned commit_blocks = static_cast<unsigned>((band_cells + 1023) / 1024);
       for (int s = 0; s < a.steps; ++s) {
         st = launch(step_rm_, grid, dim3(prog_.rm_threads), prog_.rm_smem_bytes, a.stream, &args, err, &maps);
         if (st != LF_OK) return st;
-        st = launch(commit_rm_, dim3(592), dim3(256), 0, a.stream, &args, err);
+        st = launch(commit_rm_, dim3(commit_blocks), dim3(256), 0, a.stream, &args, err);
         if (st != LF_OK) return st;
         if (fill_ && prog_.has_fill) {
           st = launch(fill_, dim3(592), dim3(256), 0, a.stream, &args, err);
