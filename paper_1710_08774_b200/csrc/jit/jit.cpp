@@ -63,6 +63,7 @@ struct Drv {
   PFN_cuModuleLoadData_v2000 load = nullptr;
   PFN_cuModuleGetFunction_v2000 get = nullptr;
   PFN_cuLaunchKernel_v4000 launch = nullptr;
+  PFN_cuLaunchKernelEx_v11060 launch_ex = nullptr;
   PFN_cuFuncSetAttribute_v9000 attr = nullptr;
   PFN_cuModuleUnload_v2000 unload = nullptr;
   PFN_cuOccupancyMaxActiveBlocksPerMultiprocessor_v6050 occupancy = nullptr;
@@ -83,6 +84,7 @@ const Drv& drv() {
            get("cuFuncSetAttribute", reinterpret_cast<void**>(&d.attr)) &&
            get("cuModuleUnload", reinterpret_cast<void**>(&d.unload)) &&
            get("cuOccupancyMaxActiveBlocksPerMultiprocessor", reinterpret_cast<void**>(&d.occupancy));
+    if (!get("cuLaunchKernelEx", reinterpret_cast<void**>(&d.launch_ex))) d.launch_ex = nullptr;
   });
   return d;
 }
@@ -372,8 +374,34 @@ bool JitKernel::tma_maps(const std::vector<JitProgram::Tma>& list, const std::ve
 int JitKernel::launch(void* fn, dim3 grid, dim3 block, size_t smem, cudaStream_t st, void* args, std::string& err,
                       void* args2) {
   void* params[] = {args, args2};
-  CUresult r = drv().launch(static_cast<CUfunction>(fn), grid.x, grid.y, grid.z, block.x, block.y, block.z,
-                            static_cast<unsigned>(smem), reinterpret_cast<CUstream>(st), params, nullptr);
+  // programmatic dependent launch: every generated kernel starts with
+  // griddepcontrol.wait + launch_dependents (lf_pdl), so the next launch of
+  // the step (ghost fill, commit, the next step) is set up while this one
+  // drains (LF_NO_PDL=1: plain stream order)
+  static const bool no_pdl = std::getenv("LF_NO_PDL") != nullptr;
+  CUresult r;
+  if (drv().launch_ex && !no_pdl) {
+    CUlaunchAttribute attr;
+    std::memset(&attr, 0, sizeof attr);
+    attr.id = CU_LAUNCH_ATTRIBUTE_PROGRAMMATIC_STREAM_SERIALIZATION;
+    attr.value.programmaticStreamSerializationAllowed = 1;
+    CUlaunchConfig cfg;
+    std::memset(&cfg, 0, sizeof cfg);
+    cfg.gridDimX = grid.x;
+    cfg.gridDimY = grid.y;
+    cfg.gridDimZ = grid.z;
+    cfg.blockDimX = block.x;
+    cfg.blockDimY = block.y;
+    cfg.blockDimZ = block.z;
+    cfg.sharedMemBytes = static_cast<unsigned>(smem);
+    cfg.hStream = reinterpret_cast<CUstream>(st);
+    cfg.attrs = &attr;
+    cfg.numAttrs = 1;
+    r = drv().launch_ex(&cfg, static_cast<CUfunction>(fn), params, nullptr);
+  } else {
+    r = drv().launch(static_cast<CUfunction>(fn), grid.x, grid.y, grid.z, block.x, block.y, block.z,
+                     static_cast<unsigned>(smem), reinterpret_cast<CUstream>(st), params, nullptr);
+  }
   if (r != CUDA_SUCCESS) {
     err = "cuLaunchKernel failed with CUresult " + std::to_string(static_cast<int>(r));
     return LF_ERR_CUDA;
