@@ -203,6 +203,15 @@ double lf_plan_compulsory_bytes_per_cell(const lf_plan* plan);
 int lf_plan_grid_passes(const lf_plan* plan, int steps);
 int lf_plan_launches(const lf_plan* plan, int steps);
 
+/* Tuning / A-B switches (names LF_*): set `value` as the
+ * in-process value of switch `name`, overriding the environment variable of
+ * that name; value == NULL drops the override.  A switch takes effect where it
+ * is read -- plan creation (code generation, executor choice) or the next run.
+ * No switch changes results (every variant is bit-exact).  Returns
+ * LF_ERR_SPEC for a name outside the LF_ namespace.  (No reference
+ * counterpart: the reference has no executor to tune.) */
+int lf_set_option(const char* name, const char* value);
+
 /* Thread-local message of the last failing call on this thread ("" if none). */
 const char* lf_last_error(void);
 

@@ -40,7 +40,7 @@ ABI_SYMBOLS = (
     "lf_last_error",
     "lf_version", "lf_spec_print", "lf_plan_source",
     "lf_run_slabs", "lf_run_slabs_local", "lf_nccl_unique_id", "lf_nccl_comm_init_rank",
-    "lf_nccl_comm_init_single", "lf_nccl_comm_destroy",
+    "lf_nccl_comm_init_single", "lf_nccl_comm_destroy", "lf_set_option",
 )
 
 
@@ -90,6 +90,7 @@ def lib() -> ctypes.CDLL:
                                     ctypes.c_size_t, ctypes.POINTER(P)]
     L.lf_spec_print.argtypes = [ctypes.c_char_p, ctypes.c_size_t, ctypes.c_char_p, ctypes.c_char_p,
                                 ctypes.c_size_t, ctypes.POINTER(ctypes.c_size_t)]
+    L.lf_set_option.argtypes = [ctypes.c_char_p, ctypes.c_char_p]
     L.lf_plan_destroy.argtypes = [P]
     L.lf_plan_destroy.restype = None
     L.lf_plan_num_terminals.argtypes = [P]
@@ -405,6 +406,28 @@ def run_slabs_local(plan: "Plan", rank_bufs: Sequence[Sequence[Any]], steps: int
                                     _stream_handle(stream)))
 
 
+def set_option(name: str, value: "str | int | None") -> None:
+    """Set a tuning / A-B switch (an LF_* name) in this process,
+    overriding the environment variable of that name; None drops the
+    override.  Switches take effect where they are read: plan creation or the
+    next run.  No switch changes results."""
+    _check(lib().lf_set_option(name.encode(), None if value is None else str(value).encode()))
+
+
+class option:
+    """Context manager: `with lf.option("LF_JIT_RM", 0): plan = lf.Plan(...)`."""
+
+    def __init__(self, name: str, value: "str | int | None"):
+        self.name, self.value = name, value
+
+    def __enter__(self):
+        set_option(self.name, self.value)
+        return self
+
+    def __exit__(self, *exc):
+        set_option(self.name, None)
+
+
 def print_spec(text: str, filename: str = "<input>") -> str:
     """Canonical text of a rule file (lf_spec_print; round-trips through parse)."""
     L = lib()
@@ -452,4 +475,5 @@ def set_ranges(text: str, sizes: Sequence[int]) -> str:
     return "\n".join(out) + "\n"
 
 
-__all__ = ["Plan", "Terminal", "LoomfuseError", "lib", "spec_path", "set_ranges", "print_spec", "ABI_SYMBOLS"]
+__all__ = ["Plan", "Terminal", "LoomfuseError", "lib", "spec_path", "set_ranges", "print_spec", "ABI_SYMBOLS",
+           "set_option", "option"]

@@ -302,8 +302,8 @@ int run_slabs_core(lf_plan* plan, const SlabGeom& g, std::vector<RankState>& R, 
     return plan->exec ? plan->exec->run(ea, err) : plan->jit->run(ea, err);
   };
   // LF_SLAB_SCHEDULE: parallel (default) | serial | concurrent -- see above
-  static const int sched_env = [] {
-    const char* e = std::getenv("LF_SLAB_SCHEDULE");
+  const int sched_env = [] {
+    const char* e = lfx::option("LF_SLAB_SCHEDULE");
     if (e && std::string(e) == "serial") return 1;
     if (e && std::string(e) == "concurrent") return 2;
     if (e && std::string(e) == "whole") return 3;
@@ -484,6 +484,12 @@ const char* lf_last_error(void) { return g_err.c_str(); }
 
 const char* lf_version(void) { return "loomfuse-b200 0.1 (sm_100a)"; }
 
+int lf_set_option(const char* name, const char* value) {
+  if (lfx::set_option(name, value, value ? 0 : 1) != 0)
+    return fail(LF_ERR_SPEC, std::string("lf_set_option: '") + (name ? name : "(null)") + "' is not an LF_* switch");
+  return LF_OK;
+}
+
 int lf_plan_create(const char* spec_text, size_t len, const char* filename, lf_plan** out) {
   return lf_plan_create_ex(spec_text, len, filename, nullptr, 0, out);
 }
@@ -507,7 +513,7 @@ int lf_plan_create_ex(const char* spec_text, size_t len, const char* filename, c
     p->report = p->plan.report_json();
     std::string why = "no built-in executor implements this chain";
     // LF_NO_BUILTIN=1: skip the hand-written executors (A/B runs of the generic one)
-    static const bool no_builtin = std::getenv("LF_NO_BUILTIN") && std::atoi(std::getenv("LF_NO_BUILTIN")) != 0;
+    const bool no_builtin = lfx::option("LF_NO_BUILTIN") && std::atoi(lfx::option("LF_NO_BUILTIN")) != 0;
     for (const auto& s : signed_executors()) {
       if (no_builtin) break;
       if (!s.error.empty()) {
@@ -875,7 +881,7 @@ int lf_run_host(const lf_plan* cplan, void* const* terms, int nterm, int steps) 
       const long n0 = plan->plan.rs.ranges[0].trips();
       const bool nests = plan->jit && !plan->jit->program().nest_kernels.empty();
       int parts = static_cast<int>(std::min<long>(32, n0 / 512));  // 32: measured best for the 16384^2 box pass
-      if (const char* e = std::getenv("LF_HOST_PARTS")) parts = std::atoi(e);
+      if (const char* e = lfx::option("LF_HOST_PARTS")) parts = std::atoi(e);
       const bool reduces = plan->exec && plan->exec->max_reduce;
       if (!inplace && !nests && !reduces && parts >= 2) {
         st = run_host_pipelined(plan, terms, dterms, parts, steps, err);

@@ -330,7 +330,7 @@ const Variant& variant() {
       make_variant<Cfg<2, 8, 12, 4>>("cpl2_r4_s8_occ12"), make_variant<Cfg<2, 7, 12, 4>>("cpl2_r4_s7_occ12"),
   };
   static int idx = [] {
-    const char* e = std::getenv("LF_BIHARM_VARIANT");
+    const char* e = lfx::option("LF_BIHARM_VARIANT");
     // default cpl2_r4_s7_occ12: best of the measured sweep (profiles/r01_biharm_variants.txt)
     int i = e ? std::atoi(e) : 21;
     return (i >= 0 && i < (int)(sizeof table / sizeof table[0])) ? i : 21;
@@ -378,14 +378,14 @@ int launch_step(const double* in, double* out, int ni, const RowPart& rp, cudaSt
   // of it at 4096^2 nearly fits the 126 MB L2 -- same-box A/B 321 -> 340 G
   // (evict_first) at 4096^2, 289 -> 295 G at 16384^2 (LF_BIHARM_STORE_POLICY)
   static const int store_policy = [] {
-    const char* e = std::getenv("LF_BIHARM_STORE_POLICY");
+    const char* e = lfx::option("LF_BIHARM_STORE_POLICY");
     return e ? std::atoi(e) : 2;
   }();
   p.store_policy = store_policy;
   // TMA fetches with an explicit evict_normal hint: same-box A/B 341 -> 346 G
   // at 4096^2, 292 -> 298 G at 16384^2 against plain fetches (evict_first 334 G)
   static const int load_policy = [] {
-    const char* e = std::getenv("LF_BIHARM_LOAD_POLICY");
+    const char* e = lfx::option("LF_BIHARM_LOAD_POLICY");
     return e ? std::atoi(e) : 1;
   }();
   p.load_policy = load_policy;

@@ -253,7 +253,7 @@ const BoxVariant& box_variant() {
       box_variant<BoxCfg<6, 24>>("s6_occ24"),  box_variant<BoxCfg<4, 24>>("s4_occ24"),
   };
   static int idx = [] {
-    const char* e = std::getenv("LF_BOX_VARIANT");
+    const char* e = lfx::option("LF_BOX_VARIANT");
     int i = e ? std::atoi(e) : 0;
     return (i >= 0 && i < (int)(sizeof table / sizeof table[0])) ? i : 0;
   }();
@@ -287,11 +287,11 @@ int run(const ExecArgs& a, std::string& err) {
   // stores 654 -> 662 G against plain fetches + evict_first stores; evict_first
   // fetches 608 G
   static const int load_policy = [] {
-    const char* e = std::getenv("LF_BOX_LOAD_POLICY");
+    const char* e = lfx::option("LF_BOX_LOAD_POLICY");
     return e ? std::atoi(e) : 1;
   }();
   static const int store_policy = [] {
-    const char* e = std::getenv("LF_BOX_STORE_POLICY");
+    const char* e = lfx::option("LF_BOX_STORE_POLICY");
     return e ? std::atoi(e) : 1;
   }();
   p.load_policy = load_policy;

@@ -14,6 +14,8 @@
 
 namespace lfx {
 
+const char* option(const char* name);  // LF_* tuning switch (options.cpp)
+
 // ------------------------------------------------------------------ device
 #if defined(__CUDACC__)
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -162,7 +164,7 @@ cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t s
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
-  static const bool off = std::getenv("LF_NO_PDL") != nullptr;  // A/B switch for tuning runs
+  const bool off = lfx::option("LF_NO_PDL") != nullptr;  // A/B switch for tuning runs
   cfg.attrs = attr;
   cfg.numAttrs = off ? 0 : 1;
   return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);

@@ -16,6 +16,13 @@
 
 namespace lfx {
 
+// LF_* tuning switch: the lf_set_option override if one is set, else the
+// environment (options.cpp)
+const char* option(const char* name);
+// value == nullptr: the switch reads as unset whatever the environment says;
+// clear: drop the override (the environment applies again)
+int set_option(const char* name, const char* value, int clear);
+
 struct ExecArgs {
   const lf::Plan* plan = nullptr;
   void* const* terms = nullptr;  // device pointers, axioms then goals

@@ -538,7 +538,7 @@ const Variant& variant() {
       make_variant<Cfg<2, 4, 16>>("rpw2_s4_k16"), make_variant<Cfg<2, 6, 12>>("rpw2_s6_k12"),
   };
   static int idx = [] {
-    const char* e = std::getenv("LF_HEAT3D_VARIANT");
+    const char* e = lfx::option("LF_HEAT3D_VARIANT");
     // default rpw2_s6_k16: best of the measured sweep (profiles/r01_heat3d_variants.txt)
     int i = e ? std::atoi(e) : 3;
     return (i >= 0 && i < (int)(sizeof table / sizeof table[0])) ? i : 3;
@@ -594,7 +594,7 @@ int launch_step(const double* in, double* out, int ni, int nj, int nk, int k_lo,
   // evict_normal: same-box A/B 348.5 -> 351.2 G against evict_first; evict_last
   // (the 1 GB output cannot stay in L2) 343 G (LF_HEAT3D_STORE_POLICY)
   static const int store_policy = [] {
-    const char* e = std::getenv("LF_HEAT3D_STORE_POLICY");
+    const char* e = lfx::option("LF_HEAT3D_STORE_POLICY");
     return e ? std::atoi(e) : 1;
   }();
   p.store_policy = store_policy;
@@ -617,7 +617,7 @@ int launch_step(const double* in, double* out, int ni, int nj, int nk, int k_lo,
 // shared-memory traffic and latency rather than by the HBM bytes it saves
 //
 bool tb_enabled(int ni, int nj, int nk) {
-  const char* e = std::getenv("LF_HEAT3D_TB");
+  const char* e = lfx::option("LF_HEAT3D_TB");
   const bool on = e && std::atoi(e) != 0;
   return on && ni % TX == 0 && nj % tb::TY == 0 && nk >= 2 && ni >= TX && nj >= tb::TY;
 }
@@ -647,7 +647,7 @@ int launch_pair_k(const double* in, double* out, int ni, int nj, int nk, cudaStr
   p.units = p.tiles * p.kchunks;
   p.store_policy = 0;
   p.wrap_i = p.wrap_j = p.wrap_k = 1;
-  p.patch = std::getenv("LF_HEAT3D_NOPATCH") ? 0 : 1;  // timing experiments only (wrong at the faces)
+  p.patch = lfx::option("LF_HEAT3D_NOPATCH") ? 0 : 1;  // timing experiments only (wrong at the faces)
   const int ctas = std::min(p.units, slots);
   tb::heat3d_fused2<K><<<ctas, tb::THREADS2, K::SMEM, st>>>(map, in, out, p);
   return cuda_status(cudaGetLastError(), "heat3d_fused2 launch", err);
@@ -656,7 +656,7 @@ int launch_pair_k(const double* in, double* out, int ni, int nj, int nk, cudaStr
 // LF_HEAT3D_TBK: planes per work unit of the two-step pass (32 / 64 / 128; 64 measured best)
 int launch_pair(const double* in, double* out, int ni, int nj, int nk, cudaStream_t st, std::string& err) {
   static const int kch = [] {
-    const char* e = std::getenv("LF_HEAT3D_TBK");
+    const char* e = lfx::option("LF_HEAT3D_TBK");
     return e ? std::atoi(e) : 64;
   }();
   if (kch >= 128) return launch_pair_k<tb::Cfg<6, 128>>(in, out, ni, nj, nk, st, err);

@@ -438,7 +438,7 @@ int launch_step(const double* const in[4], double* const out[4], const double* d
   // from fewer warps: 3 CTAs at 168 registers (no spills) beat 4 CTAs at 128
   // (96 B of spills) -- profiles/r01_hydro_variants.txt
   static void (*const kern)(Maps, Params) = [] {
-    const char* v = std::getenv("LF_HYDRO_VARIANT");
+    const char* v = lfx::option("LF_HYDRO_VARIANT");
     const int var = v ? std::atoi(v) : 1;
     return var == 0 ? hydro_fused<2> : (var == 2 ? hydro_fused<4> : hydro_fused<3>);
   }();
@@ -466,7 +466,7 @@ int launch_step(const double* const in[4], double* const out[4], const double* d
   p.dtdx = dtdx;
   p.dtdx_is_max = dtdx_is_max ? 1 : 0;
   p.cfl_acc = cfl_acc;
-  static const unsigned force_slow = std::getenv("LF_HYDRO_FORCE_SLOW") ? 1u : 0u;
+  const unsigned force_slow = lfx::option("LF_HYDRO_FORCE_SLOW") ? 1u : 0u;
   p.force_slow = force_slow;
   for (int a = 0; a < 4; ++a) p.out[a] = out[a];
   const long long work = (long long)p.strips * (rp.hi - rp.lo);

@@ -272,7 +272,7 @@ bool analyse(Ctx& C) {
     return f(e);
   };
   std::vector<char> inl(C.groups.size(), 0);
-  if (nd >= 2 && !std::getenv("LF_JIT_NOINLINE")) {
+  if (nd >= 2 && !lfx::option("LF_JIT_NOINLINE")) {
     for (size_t gi = 0; gi < C.groups.size(); ++gi) {
       const Grp& Pg = C.groups[gi];
       const auto& k = rs.kernels[Pg.kernel];
@@ -549,7 +549,7 @@ bool emit_march(Ctx& C, JitProgram& out, std::ostream& src, bool ws = false) {
   std::vector<int> lead(nv, INT_MIN), old(nv, INT_MAX), win(nv, 0), staged(nv, -1);
   // axiom rows are requested PD trips before they are read
   int PD = nd == 2 || ws ? 3 : 2;  // measured: 3D plain 2, warp-specialised 3 (324 vs 308 G)
-  if (const char* e = std::getenv("LF_JIT_PD")) PD = std::max(1, std::atoi(e));
+  if (const char* e = lfx::option("LF_JIT_PD")) PD = std::max(1, std::atoi(e));
   for (const auto& g : G)
     for (const auto& in : g.loads) {
       lead[in.var] = std::max(lead[in.var], C.smem_var[in.var] ? INT_MIN : g.shift + in.rel[0]);
@@ -571,7 +571,7 @@ bool emit_march(Ctx& C, JitProgram& out, std::ostream& src, bool ws = false) {
   // fault injection for the differential tests (R/"deliberately
   // corrupted rotation span (span-1) -> mismatch reported"): LF_JIT_FAULT=
   // span:<intermediate> emits that variable's rolling window one row short
-  if (const char* f = std::getenv("LF_JIT_FAULT"); f && std::strncmp(f, "span:", 5) == 0)
+  if (const char* f = lfx::option("LF_JIT_FAULT"); f && std::strncmp(f, "span:", 5) == 0)
     for (size_t v = 0; v < nv; ++v)
       if (C.smem_var[v] && win[v] > 1 && C.P.vars[v].name == f + 5) win[v] -= 1;
   // ws: TMA box origins must be 16-B aligned along the contiguous dimension.
@@ -639,7 +639,7 @@ bool emit_march(Ctx& C, JitProgram& out, std::ostream& src, bool ws = false) {
   // widths: the outermost inner dimension first; defaults sized for >= 2 CTAs/SM
   int wide = eb == 8 ? 512 : 1024;
   int rows_in = 16;
-  if (const char* e = std::getenv("LF_JIT_TILE")) {  // experiments: "<rows>x<width>"
+  if (const char* e = lfx::option("LF_JIT_TILE")) {  // experiments: "<rows>x<width>"
     int r = 0, w = 0;
     if (std::sscanf(e, "%dx%d", &r, &w) == 2 && r > 0 && w > 0) rows_in = r, wide = w;
   }
@@ -710,7 +710,7 @@ bool emit_march(Ctx& C, JitProgram& out, std::ostream& src, bool ws = false) {
   }
 
   int minb = std::min(cps, 2);  // register cap; 2 measured best
-  if (const char* e = std::getenv("LF_JIT_MINB")) minb = std::max(1, std::atoi(e));
+  if (const char* e = lfx::option("LF_JIT_MINB")) minb = std::max(1, std::atoi(e));
   emit_prelude(C, src, ws ? NT + 32 : NT, minb, ws ? "lf_jit_step_ws" : nullptr);
   // ws: warp 0 is the producer, consumer thread c = threadIdx.x - 32
   const char* TID = ws ? "((int)threadIdx.x - 32)" : "threadIdx.x";
@@ -748,13 +748,13 @@ bool emit_march(Ctx& C, JitProgram& out, std::ostream& src, bool ws = false) {
   // 3D: a 64-wide column per thread x 4 row lanes; 2D: 256 columns per pass
   const int STEP = nd == 3 ? NT / 64 : NT;
   int ILP = 1;  // cells whose operands are loaded before any is evaluated (1 measured best)
-  if (const char* e = std::getenv("LF_JIT_ILP")) ILP = std::max(1, std::atoi(e));
+  if (const char* e = lfx::option("LF_JIT_ILP")) ILP = std::max(1, std::atoi(e));
   // 2D, opt-in (LF_JIT_VEC=2): adjacent columns per thread sharing their
   // window loads.  Exact, but measured slower (biharm 157 vs 222 G, box 244 vs
   // 274 G): lanes two elements apart make every shared-memory load a 2-way
   // bank conflict and the shared operands cost registers.
   int VEC = 1;
-  if (const char* e = std::getenv("LF_JIT_VEC")) VEC = std::max(1, std::atoi(e));
+  if (const char* e = lfx::option("LF_JIT_VEC")) VEC = std::max(1, std::atoi(e));
   const char* LANE = nd == 3 ? "ty" : "tx";
   // ---- persistent CTAs: each takes an equal share of the (row chunk, inner
   // tile, row) space in that order and marches it as one or more segments,
@@ -854,7 +854,7 @@ bool emit_march(Ctx& C, JitProgram& out, std::ostream& src, bool ws = false) {
   // are fetched once and hit in L2, and the row segments neighbouring tiles
   // write into shared sectors meet in L2 before eviction (LF_JIT_SPAN_ORDER=1:
   // the earlier equal-span order, plain kernel only, for comparison)
-  const char* UNITS = ws || !std::getenv("LF_JIT_SPAN_ORDER") ? "true" : "a.inplace";
+  const char* UNITS = ws || !lfx::option("LF_JIT_SPAN_ORDER") ? "true" : "a.inplace";
   src << "  const long long units = " << UNITS << " ? (long long)((rows + a.chunk - 1) / a.chunk) * " << inner
       << " : 0;\n";
   src << "  long long u = blockIdx.x;\n";
@@ -899,7 +899,7 @@ bool emit_march(Ctx& C, JitProgram& out, std::ostream& src, bool ws = false) {
     std::vector<char> keep;  // value carried to the next trip
   };
   std::vector<Rot> rot(G.size());
-  const bool use_rot = std::getenv("LF_JIT_ROT") && std::atoi(std::getenv("LF_JIT_ROT")) != 0;
+  const bool use_rot = lfx::option("LF_JIT_ROT") && std::atoi(lfx::option("LF_JIT_ROT")) != 0;
   for (size_t gi = 0; gi < G.size(); ++gi) {
     const Grp& g = G[gi];
     Rot& R = rot[gi];
@@ -1736,7 +1736,7 @@ bool emit_nests(const lf::Plan& P, const std::string& sources, JitProgram& out, 
     } else {
       // ---- reduction nest: warp per parallel cell, reduced dims in order
       int LFB = 2;  // element blocks of 32 in flight per warp (LF_JIT_RED_BLOCKS; 104 -> 117 G at 2, no gain beyond)
-      if (const char* e = std::getenv("LF_JIT_RED_BLOCKS")) LFB = std::max(1, std::atoi(e));
+      if (const char* e = lfx::option("LF_JIT_RED_BLOCKS")) LFB = std::max(1, std::atoi(e));
       std::set<int> Pd;
       for (int d : space)
         if (!R.count(d)) Pd.insert(d);
@@ -1971,7 +1971,7 @@ bool jit_generate(const lf::Plan& P, JitProgram& out, const std::string& sources
   // the warp-specialised variant, where every streamed axiom can be fetched by
   // TMA: a dense terminal in loop-dimension order with 16-B row pitches, no
   // in-place aliases (those keep the band-capturing loader)
-  bool tma_ok = C.nd >= 2 && !(std::getenv("LF_JIT_WS") && std::atoi(std::getenv("LF_JIT_WS")) == 0);
+  bool tma_ok = C.nd >= 2 && !(lfx::option("LF_JIT_WS") && std::atoi(lfx::option("LF_JIT_WS")) == 0);
   int nstaged = 0;
   for (size_t v = 0; tma_ok && v < C.P.vars.size(); ++v) {
     const int ti = C.staged_axiom(static_cast<int>(v));
@@ -1996,7 +1996,7 @@ bool jit_generate(const lf::Plan& P, JitProgram& out, const std::string& sources
     }
     // 2D: the register march (LF_JIT_RM=0: off)
     std::ostringstream rm;
-    const bool rm_off = std::getenv("LF_JIT_RM") && std::atoi(std::getenv("LF_JIT_RM")) == 0;
+    const bool rm_off = lfx::option("LF_JIT_RM") && std::atoi(lfx::option("LF_JIT_RM")) == 0;
     if (C.nd == 2 && !rm_off && emit_rmarch(C, out, rm) && !out.rm_maps.empty() &&
         static_cast<int>(out.rm_maps.size()) <= kJitMaxMaps) {
       out.has_rm = true;

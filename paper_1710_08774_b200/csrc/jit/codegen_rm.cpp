@@ -120,12 +120,12 @@ bool emit_rmarch(Ctx& C, JitProgram& out, std::ostream& src) {
   const int eb = out.elem_bytes;
   const int CH = 16 / eb;  // elements per 16-B chunk
   int V = eb == 8 ? 2 : 4;
-  if (const char* e = std::getenv("LF_JIT_RM_V")) V = std::atoi(e);
+  if (const char* e = lfx::option("LF_JIT_RM_V")) V = std::atoi(e);
   if (V < CH || V % CH || V > 16) return false;
   int NW = 8;  // consumer warps per CTA
-  if (const char* e = std::getenv("LF_JIT_RM_WARPS")) NW = std::max(1, std::min(16, std::atoi(e)));
+  if (const char* e = lfx::option("LF_JIT_RM_WARPS")) NW = std::max(1, std::min(16, std::atoi(e)));
   int PD = 3;
-  if (const char* e = std::getenv("LF_JIT_PD")) PD = std::max(1, std::atoi(e));
+  if (const char* e = lfx::option("LF_JIT_PD")) PD = std::max(1, std::atoi(e));
   const int NS = PD + 1;
   const size_t nv = C.P.vars.size();
   const auto& G = C.groups;
@@ -161,7 +161,7 @@ bool emit_rmarch(Ctx& C, JitProgram& out, std::ostream& src) {
   // fault injection (R/SPEC.md:557, as in emit_march): the named intermediate
   // keeps one row fewer than its contraction span
   std::vector<int> drop(nv, 0);
-  if (const char* f = std::getenv("LF_JIT_FAULT"); f && std::strncmp(f, "span:", 5) == 0)
+  if (const char* f = lfx::option("LF_JIT_FAULT"); f && std::strncmp(f, "span:", 5) == 0)
     for (size_t v = 0; v < nv; ++v)
       if (C.smem_var[v] && win[v] > 1 && C.P.vars[v].name == f + 5) {
         drop[v] = 1;
@@ -234,7 +234,7 @@ bool emit_rmarch(Ctx& C, JitProgram& out, std::ostream& src) {
   for (size_t gi = 0; gi < G.size(); ++gi) tw = std::min<long>(tw, cs + 32L * V - B[gi] - G[gi].gmax[1]);
   tw = tw / CH * CH;
   if (tw < 2 * CH || tw < 4) return false;
-  if (const char* e = std::getenv("LF_JIT_RM_TW")) tw = std::min<long>(tw, std::max(CH, std::atoi(e) / CH * CH));
+  if (const char* e = lfx::option("LF_JIT_RM_TW")) tw = std::min<long>(tw, std::max(CH, std::atoi(e) / CH * CH));
   const long T1 = NW * tw;  // CTA tile
   const long inner = (C.N[1] + T1 - 1) / T1;
 
@@ -342,7 +342,7 @@ bool emit_rmarch(Ctx& C, JitProgram& out, std::ostream& src) {
     if (staged[v] >= 0) TS = std::min(TS, C.vmin[v][0] - lead[v]);
 
   int minb = 3;  // <= 72 registers: 3 CTAs of 9 warps per SM (the in-place store path needs 75 uncapped)
-  if (const char* e = std::getenv("LF_JIT_RM_MINB")) minb = std::max(1, std::atoi(e));
+  if (const char* e = lfx::option("LF_JIT_RM_MINB")) minb = std::max(1, std::atoi(e));
   emit_prelude(C, src, out.rm_threads, minb, "lf_jit_step_rm");
   const std::string VT = eb == 8 ? "double2" : "float4";
   const char* comp[4] = {"x", "y", "z", "w"};
@@ -436,7 +436,7 @@ bool emit_rmarch(Ctx& C, JitProgram& out, std::ostream& src) {
   int U = 1;
   for (size_t v = 0; v < nv; ++v)
     if (C.smem_var[v] && win[v] > 1) U = std::lcm(U, win[v]);
-  if (U > 6 || (std::getenv("LF_JIT_RM_UNROLL") && std::atoi(std::getenv("LF_JIT_RM_UNROLL")) == 0)) U = 1;
+  if (U > 6 || (lfx::option("LF_JIT_RM_UNROLL") && std::atoi(lfx::option("LF_JIT_RM_UNROLL")) == 0)) U = 1;
   int cu = 0;  // the copy being emitted
   auto phys = [&](int v, int k) { return U == 1 ? k : (k + cu) % win[v]; };
   const std::string trip_end = "r1 - 1 + (" + std::to_string(TE) + ")";
@@ -569,7 +569,7 @@ bool emit_rmarch(Ctx& C, JitProgram& out, std::ostream& src) {
     // pipe when every output (and every inlined producer) has a body.  Exact,
     // but measured slower on the box chain (430 vs 484 G: forming the register
     // pairs costs moves), so scalar cells by default
-    bool packed = C.T == "float" && V % 2 == 0 && std::getenv("LF_JIT_RM_PACK") && std::atoi(std::getenv("LF_JIT_RM_PACK")) != 0;
+    bool packed = C.T == "float" && V % 2 == 0 && lfx::option("LF_JIT_RM_PACK") && std::atoi(lfx::option("LF_JIT_RM_PACK")) != 0;
     for (const auto& [op, pat] : k.outputs) packed &= k.bodies.count(op) > 0;
     std::set<std::string> kin;
     for (const auto& [ip, pat] : k.inputs) kin.insert(ip);

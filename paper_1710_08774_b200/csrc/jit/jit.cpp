@@ -199,7 +199,7 @@ int JitKernel::run_inplace(const ExecArgs& a, JitArgs& args, std::string& err) {
     long bh = 1;
     for (const auto& q : prog_.rm_inplace) bh = std::max<long>(bh, q.bh);
     chunk = std::min(rows, std::max({chunk, 8L * std::max(1, prog_.prologue), bh}));
-    if (const char* e = std::getenv("LF_JIT_CHUNK")) chunk = std::max(bh, std::min<long>(rows, std::atol(e)));
+    if (const char* e = lfx::option("LF_JIT_CHUNK")) chunk = std::max(bh, std::min<long>(rows, std::atol(e)));
     const long nch = (rows + chunk - 1) / chunk;
     int st = bands_for(prog_.rm_inplace, nch, 0, err);
     if (st != LF_OK) return st;
@@ -234,7 +234,7 @@ int JitKernel::run_inplace(const ExecArgs& a, JitArgs& args, std::string& err) {
   // chunk: about two units per resident CTA, at least 8 pipeline depths
   long chunk = (rows * prog_.inner_tiles + 2L * resident_ - 1) / (2L * resident_);
   chunk = std::min(rows, std::max(chunk, 8L * std::max(1, prog_.prologue)));
-  if (const char* e = std::getenv("LF_JIT_CHUNK")) chunk = std::max(1L, std::min<long>(rows, std::atol(e)));
+  if (const char* e = lfx::option("LF_JIT_CHUNK")) chunk = std::max(1L, std::min<long>(rows, std::atol(e)));
   const long nch = (rows + chunk - 1) / chunk;
   int bst = bands_for(prog_.inplace, nch, 0, err);
   if (bst != LF_OK) return bst;
@@ -351,7 +351,7 @@ static long pick_chunk(long rows, long inner, long resident, long fill, long max
 // kernel) when a buffer is not 16-B aligned or the driver refuses a map
 bool JitKernel::tma_maps(const std::vector<JitProgram::Tma>& list, const std::vector<void*>& bufs, long rows,
                          JitMaps& maps, long boundaries) {
-  static const bool off = std::getenv("LF_JIT_WS") && std::atoi(std::getenv("LF_JIT_WS")) == 0;
+  const bool off = lfx::option("LF_JIT_WS") && std::atoi(lfx::option("LF_JIT_WS")) == 0;
   if (off) return false;
   const CUtensorMapDataType dt = prog_.elem_bytes == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
   const long n0 = plan_rows_;
@@ -378,7 +378,7 @@ int JitKernel::launch(void* fn, dim3 grid, dim3 block, size_t smem, cudaStream_t
   // griddepcontrol.wait + launch_dependents (lf_pdl), so the next launch of
   // the step (ghost fill, commit, the next step) is set up while this one
   // drains (LF_NO_PDL=1: plain stream order)
-  static const bool no_pdl = std::getenv("LF_NO_PDL") != nullptr;
+  const bool no_pdl = lfx::option("LF_NO_PDL") != nullptr;
   CUresult r;
   if (drv().launch_ex && !no_pdl) {
     CUlaunchAttribute attr;
@@ -533,10 +533,10 @@ int JitKernel::run(const ExecArgs& a, std::string& err) {
       }
     }
     // whole (chunk, tile) units round-robin over the resident CTAs
-    static const bool span_order = std::getenv("LF_JIT_SPAN_ORDER") != nullptr;
+    const bool span_order = lfx::option("LF_JIT_SPAN_ORDER") != nullptr;
     long chunk = pick_chunk(rows, prog_.inner_tiles, resident_, prog_.prologue, prog_.nd == 3 ? prog_.chunk : rows);
     if (span_order) chunk = std::min<long>(prog_.chunk, rows);
-    if (const char* e = std::getenv("LF_JIT_CHUNK")) chunk = std::max(1L, std::min<long>(rows, std::atol(e)));
+    if (const char* e = lfx::option("LF_JIT_CHUNK")) chunk = std::max(1L, std::min<long>(rows, std::atol(e)));
     const long total = rows * prog_.inner_tiles;
     args.chunk = static_cast<int>(chunk);
     const long units = (rows + chunk - 1) / chunk * prog_.inner_tiles;
@@ -587,7 +587,7 @@ int JitKernel::run(const ExecArgs& a, std::string& err) {
     if (prog_.march && step_rm_ && goals_aligned && tma_maps(prog_.rm_maps, bufs, rp.rows, maps)) {
       JitArgs wa = args;
       long chunk = pick_chunk(rows, prog_.rm_inner_tiles, resident_rm_, prog_.prologue, rows);
-      if (const char* e = std::getenv("LF_JIT_CHUNK")) chunk = std::max(1L, std::min<long>(rows, std::atol(e)));
+      if (const char* e = lfx::option("LF_JIT_CHUNK")) chunk = std::max(1L, std::min<long>(rows, std::atol(e)));
       wa.chunk = static_cast<int>(chunk);
       const long units = (rows + chunk - 1) / chunk * prog_.rm_inner_tiles;
       dim3 grm(static_cast<unsigned>(std::max<long>(1, std::min<long>(resident_rm_, units))));
@@ -597,7 +597,7 @@ int JitKernel::run(const ExecArgs& a, std::string& err) {
       JitArgs wa = args;
       long chunk = pick_chunk(rows, prog_.ws_inner_tiles, resident_ws_, prog_.prologue,
                               prog_.nd == 3 ? prog_.chunk : rows);
-      if (const char* e = std::getenv("LF_JIT_CHUNK")) chunk = std::max(1L, std::min<long>(rows, std::atol(e)));
+      if (const char* e = lfx::option("LF_JIT_CHUNK")) chunk = std::max(1L, std::min<long>(rows, std::atol(e)));
       wa.chunk = static_cast<int>(chunk);
       const long units = (rows + chunk - 1) / chunk * prog_.ws_inner_tiles;
       dim3 gws(static_cast<unsigned>(std::max<long>(1, std::min<long>(resident_ws_, units))));

@@ -80,3 +80,19 @@ def test_division_by_literal_strength_reduction():
     assert "/ static_cast<float>(1.0e-30)" in plain   # not a power of two
     plain64, _ = kernels(lf.Plan.from_file(SPECS / "biharm_body.lf"))
     assert "lf_div3f" not in plain64
+
+
+def test_switches_set_in_process_override_the_environment(monkeypatch):
+    """lf_set_option: a tuning switch set in-process wins over the environment
+    and takes effect at the next plan creation; dropping it restores the
+    environment's value; names outside LF_* are refused."""
+    spec = SPECS / "biharm_body.lf"
+    assert "lf_jit_step_rm(" in lf.Plan.from_file(spec).source
+    monkeypatch.setenv("LF_JIT_RM", "0")
+    assert "lf_jit_step_rm(" not in lf.Plan.from_file(spec).source
+    with lf.option("LF_JIT_RM", "1"):
+        assert "lf_jit_step_rm(" in lf.Plan.from_file(spec).source
+    assert "lf_jit_step_rm(" not in lf.Plan.from_file(spec).source  # the environment again
+    import pytest
+    with pytest.raises(lf.LoomfuseError):
+        lf.set_option("PATH", "x")

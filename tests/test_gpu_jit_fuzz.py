@@ -124,19 +124,16 @@ def test_random_chain_matches_generic_oracle(seed, tmp_path):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("knob", ["LF_JIT_VEC=2", "LF_JIT_RM_PACK=1", "LF_JIT_RM_UNROLL=0"])
-def test_random_chains_with_opt_in_variants(knob):
-    """Opt-in / comparison variants on the same random chains, in a subprocess
-    (the knobs are read at plan creation): LF_JIT_VEC=2 (plain march, two
-    adjacent columns per thread sharing window loads), LF_JIT_RM_PACK=1
-    (register march, fp32 cells in fp32x2 pairs), LF_JIT_RM_UNROLL=0
-    (register windows shifted by moves instead of renamed)."""
-    import os
-    import subprocess
-    import sys
-    from pathlib import Path
+@pytest.mark.parametrize("knob", ["LF_JIT_VEC=2", "LF_JIT_RM_PACK=1", "LF_JIT_RM_UNROLL=0", "LF_JIT_RM=0", "LF_JIT_WS=0"])
+def test_random_chains_with_opt_in_variants(knob, tmp_path):
+    """Opt-in / comparison variants on the same random chains (the knobs are
+    read at plan creation; set in-process with lf.option): LF_JIT_VEC=2 (plain
+    march, two adjacent columns per thread sharing window loads),
+    LF_JIT_RM_PACK=1 (register march, fp32 cells in fp32x2 pairs),
+    LF_JIT_RM_UNROLL=0 (register windows shifted by moves instead of renamed),
+    LF_JIT_RM=0 / LF_JIT_WS=0 (the warp-specialised / plain smem-window
+    marches where the register march / TMA would run)."""
     k, v = knob.split("=")
-    env = dict(os.environ, **{k: v})
-    r = subprocess.run([sys.executable, "-m", "pytest", __file__, "-q", "-m", "gpu", "-k", "matches_generic_oracle"],
-                       env=env, capture_output=True, text=True, timeout=600, cwd=str(Path(__file__).parents[1]))
-    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+    with lf.option(k, v):
+        for seed in range(48):
+            test_random_chain_matches_generic_oracle(seed, tmp_path)

@@ -177,16 +177,13 @@ def test_slab_run_argument_errors():
     assert e.value.code == lf.LF_ERR_SPEC
 
 
-@pytest.mark.parametrize("schedule", ["serial", "concurrent"])
+@pytest.mark.parametrize("schedule", ["serial", "concurrent", "whole", "parallel"])
 def test_alternative_slab_schedules_match_whole_domain(schedule):
-    """The selectable slab schedules (LF_SLAB_SCHEDULE, read once per process;
-    the default `parallel` one runs everywhere above) give the same bits: the
-    decomposition tests of this file, re-run in a subprocess."""
-    import os
-    import subprocess
-    import sys
-    env = dict(os.environ, LF_SLAB_SCHEDULE=schedule)
-    r = subprocess.run([sys.executable, "-m", "pytest", __file__, "-q", "-m", "gpu", "-k",
-                        "local_slab_decomposition or nccl_one_rank"], env=env, capture_output=True, text=True,
-                       timeout=600, cwd=str(Path(__file__).parents[1]))
-    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+    """Every selectable slab schedule (LF_SLAB_SCHEDULE, set in-process with
+    lf.option; the default picks `whole` for slabs of >= 1024 rows, else
+    `parallel`) gives the same bits: the decomposition tests of this file."""
+    with lf.option("LF_SLAB_SCHEDULE", schedule):
+        for case in CASES:
+            test_local_slab_decomposition_matches_whole_domain(*case)
+        for name, shape, steps in [("heat3d", (12, 16, 40), 3), ("biharm", (30, 64), 2), ("hydro", (16, 48), 3)]:
+            test_nccl_one_rank_matches_whole_domain(name, shape, steps)
