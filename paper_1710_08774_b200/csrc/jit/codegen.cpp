@@ -538,17 +538,146 @@ void emit_capture(Ctx& C, const char* name, const std::vector<std::pair<size_t, 
 // at named barriers between dependency levels (intermediate windows one row
 // deeper so a trip's writes never hit rows the previous trip still reads), so
 // a single-level chain runs with no CTA-wide barrier at all.
-bool emit_march(Ctx& C, JitProgram& out, std::ostream& src, bool ws = false) {
-  const int nd = C.nd;
+//
+// The emitter is a class: windows() sizes each variable's rolling window,
+// geometry() picks the inner tile and the shared-memory layout, head() writes
+// the kernel head and the persistent work order, trips() the per-trip loads
+// (cp.async) or producer (TMA), group() one callsite group, tail() the
+// window advance; capture() the in-place band copy kernel.
+namespace {
+class March {
+ public:
+  March(Ctx& c, JitProgram& o, std::ostream& s, bool w)
+      : C(c), out(o), src(s), ws(w), nd(c.nd), eb(o.elem_bytes), al(16 / o.elem_bytes), nv(c.P.vars.size()),
+        G(c.groups), saved_vmin(c.vmin) {}
+  ~March() { C.vmin = saved_vmin; }  // the ws emission widens streamed windows for itself only
+  bool emit() {
+    if (!windows() || !geometry()) return false;
+    head();
+    trips();
+    int level = 1;
+    for (size_t gi = 0; gi < G.size(); ++gi)
+      if (!group(gi, level)) return false;
+    tail();
+    capture();
+    return true;
+  }
+
+ private:
+  struct IP {
+    size_t v;
+    int ai, gi, slot;
+  };
+  struct Rot {
+    int K = 1;
+    std::vector<int> from;  // load index whose previous-trip value this load takes (-1: load)
+    std::vector<char> keep;  // value carried to the next trip
+  };
+  Ctx& C;
+  JitProgram& out;
+  std::ostream& src;
+  const bool ws;
+  const int nd;
   const int NT = 256;
-  const int eb = out.elem_bytes;
-  const size_t nv = C.P.vars.size();
-  auto& G = C.groups;
+  const int eb;
+  const int al;  // elements per 16 B
+  const size_t nv;
+  std::vector<Grp>& G;
+  std::vector<std::vector<int>> saved_vmin;
   // window bookkeeping along dim 0: lead (newest row written at trip t is
   // t + lead) and oldest row read at trip t (t + old)
-  std::vector<int> lead(nv, INT_MIN), old(nv, INT_MAX), win(nv, 0), staged(nv, -1);
+  std::vector<int> lead, old, win, staged;
+  int PD = 3;  // axiom rows are requested PD trips before they are read
+  std::vector<int> tile;
+  std::vector<size_t> soff;
+  size_t smem = 0;
+  int TS = 0, TE = 0, cps = 1;
+  long inner = 1;
+  int STEP = 1, ILP = 1, VEC = 1, NS = 1;
+  const char* LANE = "tx";
+  bool use_rot = false;
+  std::vector<Rot> rot;
+  std::vector<IP> ips;
+  std::vector<size_t> tv;  // TMA-staged vars, in map order
+
+  bool windows();
+  bool geometry();
+  void head();
+  void trips();
+  bool group(size_t gi, int& level);
+  void tail();
+  void capture();
+  void emit_load(size_t v, const std::string& row, const std::string& slotexpr, const char* ind);
+  // ws: a staged axiom's innermost row is fetched as nbox TMA boxes of bw
+  // elements (box rows <= 256 elements, 128-B multiples so every box lands
+  // 128-B aligned); its smem row is nbox * bw wide
+  void tma_box(size_t v, int& nbox, int& bw) const {
+    const int w = tile[nd - 1] + (C.vmax[v][nd - 1] - C.vmin[v][nd - 1]);
+    const int al = 128 / eb;
+    nbox = (w + 255) / 256;
+    bw = ((w + nbox - 1) / nbox + al - 1) / al * al;
+    if (bw > 256) nbox = (w + 255) / 256 + 1, bw = ((w + nbox - 1) / nbox + al - 1) / al * al;
+  }
+  int wdim(size_t v, int d) const {
+    int w = tile[d] + (C.vmax[v][d] - C.vmin[v][d]);
+    if (ws && staged[v] >= 0 && d == nd - 1) {
+      int nb = 1, bw = w;
+      tma_box(v, nb, bw);
+      w = nb * bw;
+    }
+    return w;
+  }
+  int width(size_t v, int d) const { return wdim(v, d); }
+  size_t plane(size_t v) const {
+    size_t n = 1;
+    for (int d = 1; d < nd; ++d) n *= wdim(v, d);
+    return n;
+  }
+  void layout() {
+    smem = 0;
+    const size_t al = ws ? 128 : 16;
+    for (size_t v = 0; v < nv; ++v) {
+      if (win[v] <= 0) continue;
+      soff[v] = smem;
+      smem += (win[v] * plane(v) * eb + al - 1) / al * al;
+    }
+  }
+  // in-plane offset of var v at tile-relative cell (c_d + rel_d)
+  std::string inplane(size_t v, const std::vector<int>& rel) const {
+    std::string e;
+    for (int d = 1; d < nd; ++d) {
+      const std::string c = "(c" + std::to_string(d) + plus(rel[d] - C.vmin[v][d]) + ")";
+      e = e.empty() ? c : "(" + e + ") * " + std::to_string(width(v, d)) + " + " + c;
+    }
+    return e;
+  }
+  // rolling-window slots: b<v> = slot of row t, advanced once per trip; the
+  // slot of row t + off is b<v> + (off mod W) with one conditional wrap
+  int wrap(size_t v, int off) const { return ((off % win[v]) + win[v]) % win[v]; }
+  std::string rowbase(size_t v, int off) const {
+    if (win[v] == 1) return "0";
+    const int o = wrap(v, off);
+    const std::string b = "b" + std::to_string(v);
+    const std::string sum = o ? "(" + b + " + " + std::to_string(o) + ")" : b;
+    const std::string sl = o ? "(" + sum + " >= " + std::to_string(win[v]) + " ? " + sum + " - " + std::to_string(win[v]) +
+                                   " : " + sum + ")"
+                             : b;
+    return sl + " * " + std::to_string(plane(v));
+  }
+  const IP* ip_of(size_t v) const {
+    for (const auto& ip : ips)
+      if (ip.v == v) return &ip;
+    return nullptr;
+  }
+};
+
+bool March::windows() {
+  lead.assign(nv, INT_MIN);
+  old.assign(nv, INT_MAX);
+  win.assign(nv, 0);
+  staged.assign(nv, -1);
   // axiom rows are requested PD trips before they are read
-  int PD = nd == 2 || ws ? 3 : 2;  // measured: 3D plain 2, warp-specialised 3 (324 vs 308 G)
+  PD = nd == 2 || ws ? 3 : 2;  // measured: 3D plain 2, warp-specialised 3 (324 vs 308 G)
   if (const char* e = lfx::option("LF_JIT_PD")) PD = std::max(1, std::atoi(e));
   for (const auto& g : G)
     for (const auto& in : g.loads) {
@@ -578,12 +707,7 @@ bool emit_march(Ctx& C, JitProgram& out, std::ostream& src, bool ws = false) {
   // Tiles are a multiple of `al` elements there, and each streamed axiom's
   // window starts up to al - 1 elements further left (its range is widened
   // for this emission only) so that origin = tile start + a multiple of al.
-  struct RestoreVmin {
-    Ctx& c;
-    std::vector<std::vector<int>> saved;
-    ~RestoreVmin() { c.vmin = saved; }
-  } restore_vmin{C, C.vmin};
-  const int al = 16 / eb;
+  // (restored by ~March)
   if (ws)
     for (size_t v = 0; v < nv; ++v) {
       if (staged[v] < 0) continue;
@@ -593,6 +717,10 @@ bool emit_march(Ctx& C, JitProgram& out, std::ostream& src, bool ws = false) {
       const long m = ((C.vmin[v][d] + so) % al + al) % al;
       C.vmin[v][d] -= static_cast<int>(m);
     }
+  return true;
+}
+
+bool March::geometry() {
   // inner tile: cells per plane of the widest window a multiple of the block
   int span_in[3] = {0, 0, 0};
   for (size_t v = 0; v < nv; ++v)
@@ -600,42 +728,9 @@ bool emit_march(Ctx& C, JitProgram& out, std::ostream& src, bool ws = false) {
       for (int d = 1; d < nd; ++d) span_in[d] = std::max(span_in[d], C.vmax[v][d] - C.vmin[v][d]);
   for (const auto& g : G)
     for (int d = 1; d < nd; ++d) span_in[d] = std::max(span_in[d], g.gmax[d] - g.gmin[d]);
-  std::vector<int> tile(nd, 1);
-  std::vector<size_t> soff(nv, 0);
-  size_t smem = 0;
-  // ws: a staged axiom's innermost row is fetched as nbox TMA boxes of bw
-  // elements (box rows <= 256 elements, 128-B multiples so every box lands
-  // 128-B aligned); its smem row is nbox * bw wide
-  auto tma_box = [&](size_t v, int& nbox, int& bw) {
-    const int w = tile[nd - 1] + (C.vmax[v][nd - 1] - C.vmin[v][nd - 1]);
-    const int al = 128 / eb;
-    nbox = (w + 255) / 256;
-    bw = ((w + nbox - 1) / nbox + al - 1) / al * al;
-    if (bw > 256) nbox = (w + 255) / 256 + 1, bw = ((w + nbox - 1) / nbox + al - 1) / al * al;
-  };
-  auto wdim = [&](size_t v, int d) {
-    int w = tile[d] + (C.vmax[v][d] - C.vmin[v][d]);
-    if (ws && staged[v] >= 0 && d == nd - 1) {
-      int nb = 1, bw = w;
-      tma_box(v, nb, bw);
-      w = nb * bw;
-    }
-    return w;
-  };
-  auto plane = [&](size_t v) {
-    size_t n = 1;
-    for (int d = 1; d < nd; ++d) n *= wdim(v, d);
-    return n;
-  };
-  auto layout = [&] {
-    smem = 0;
-    const size_t al = ws ? 128 : 16;
-    for (size_t v = 0; v < nv; ++v) {
-      if (win[v] <= 0) continue;
-      soff[v] = smem;
-      smem += (win[v] * plane(v) * eb + al - 1) / al * al;
-    }
-  };
+  tile.assign(nd, 1);
+  soff.assign(nv, 0);
+  smem = 0;
   // widths: the outermost inner dimension first; defaults sized for >= 2 CTAs/SM
   int wide = eb == 8 ? 512 : 1024;
   int rows_in = 16;
@@ -691,15 +786,16 @@ bool emit_march(Ctx& C, JitProgram& out, std::ostream& src, bool ws = false) {
   out.march = true;
   }
   // trip range relative to the chunk [r0, r1): t in [r0 + TS, r1 - 1 + TE]
-  int TS = INT_MAX, TE = INT_MIN;
+  TS = INT_MAX;
+  TE = INT_MIN;
   for (const auto& g : G) {
     TS = std::min(TS, g.gmin[0] - g.shift);
     TE = std::max(TE, g.gmax[0] - g.shift);
   }
   for (size_t v = 0; v < nv; ++v)
     if (staged[v] >= 0) TS = std::min(TS, C.vmin[v][0] - lead[v]);
-  const int cps = std::max<int>(1, std::min<int>(2048 / NT, static_cast<int>((227 * 1024) / (smem + 1024))));
-  long inner = 1;
+  cps = std::max<int>(1, std::min<int>(2048 / NT, static_cast<int>((227 * 1024) / (smem + 1024))));
+  inner = 1;
   for (int d = 1; d < nd; ++d) inner *= (C.N[d] + tile[d] - 1) / tile[d];
   if (ws) out.ws_inner_tiles = inner;
   if (!ws) {
@@ -709,6 +805,10 @@ bool emit_march(Ctx& C, JitProgram& out, std::ostream& src, bool ws = false) {
     out.chunk = nd == 3 ? 64 : 1 << 30;  // rows per chunk of the work order (2D: whole tiles)
   }
 
+  return true;
+}
+
+void March::head() {
   int minb = std::min(cps, 2);  // register cap; 2 measured best
   if (const char* e = lfx::option("LF_JIT_MINB")) minb = std::max(1, std::atoi(e));
   emit_prelude(C, src, ws ? NT + 32 : NT, minb, ws ? "lf_jit_step_ws" : nullptr);
@@ -722,40 +822,17 @@ bool emit_march(Ctx& C, JitProgram& out, std::ostream& src, bool ws = false) {
     if (win[v] > 0)
       src << "  T* __restrict__ v" << v << " = reinterpret_cast<T*>(lf_smem + " << soff[v] << ");  // '"
           << C.P.vars[v].name << "': " << win[v] << " rows x " << plane(v) << "\n";
-  auto width = [&](size_t v, int d) { return wdim(v, d); };
-  // in-plane offset of var v at tile-relative cell (c_d + rel_d)
-  auto inplane = [&](size_t v, const std::vector<int>& rel) {
-    std::string e;
-    for (int d = 1; d < nd; ++d) {
-      const std::string c = "(c" + std::to_string(d) + plus(rel[d] - C.vmin[v][d]) + ")";
-      e = e.empty() ? c : "(" + e + ") * " + std::to_string(width(v, d)) + " + " + c;
-    }
-    return e;
-  };
-  // rolling-window slots: b<v> = slot of row t, advanced once per trip; the
-  // slot of row t + off is b<v> + (off mod W) with one conditional wrap
-  auto wrap = [&](size_t v, int off) { return ((off % win[v]) + win[v]) % win[v]; };
-  auto rowbase = [&](size_t v, int off) -> std::string {
-    if (win[v] == 1) return "0";
-    const int o = wrap(v, off);
-    const std::string b = "b" + std::to_string(v);
-    const std::string sum = o ? "(" + b + " + " + std::to_string(o) + ")" : b;
-    const std::string sl = o ? "(" + sum + " >= " + std::to_string(win[v]) + " ? " + sum + " - " + std::to_string(win[v]) +
-                                   " : " + sum + ")"
-                             : b;
-    return sl + " * " + std::to_string(plane(v));
-  };
   // 3D: a 64-wide column per thread x 4 row lanes; 2D: 256 columns per pass
-  const int STEP = nd == 3 ? NT / 64 : NT;
-  int ILP = 1;  // cells whose operands are loaded before any is evaluated (1 measured best)
+  STEP = nd == 3 ? NT / 64 : NT;
+  ILP = 1;  // cells whose operands are loaded before any is evaluated (1 measured best)
   if (const char* e = lfx::option("LF_JIT_ILP")) ILP = std::max(1, std::atoi(e));
   // 2D, opt-in (LF_JIT_VEC=2): adjacent columns per thread sharing their
   // window loads.  Exact, but measured slower (biharm 157 vs 222 G, box 244 vs
   // 274 G): lanes two elements apart make every shared-memory load a 2-way
   // bank conflict and the shared operands cost registers.
-  int VEC = 1;
+  VEC = 1;
   if (const char* e = lfx::option("LF_JIT_VEC")) VEC = std::max(1, std::atoi(e));
-  const char* LANE = nd == 3 ? "ty" : "tx";
+  LANE = nd == 3 ? "ty" : "tx";
   // ---- persistent CTAs: each takes an equal share of the (row chunk, inner
   // tile, row) space in that order and marches it as one or more segments,
   // so neighbouring tiles run at the same time and share halos in L2
@@ -763,11 +840,7 @@ bool emit_march(Ctx& C, JitProgram& out, std::ostream& src, bool ws = false) {
     if (staged[v] >= 0) src << "  const unsigned sb" << v << " = (unsigned)__cvta_generic_to_shared(v" << v << ");\n";
   // in-place (config.aliases, caller passes one buffer): whole (chunk, tile)
   // units so that every cross-unit read hits a band captured before the step
-  struct IP {
-    size_t v;
-    int ai, gi, slot;
-  };
-  std::vector<IP> ips;
+  ips.clear();
   if (!ws) {
     out.inplace.clear();
     out.inplace_error.clear();
@@ -811,19 +884,14 @@ bool emit_march(Ctx& C, JitProgram& out, std::ostream& src, bool ws = false) {
     q.n2 = nd > 2 ? C.N[2] : 1;
     out.inplace.push_back(q);
   }
-  auto ip_of = [&](size_t v) -> const IP* {
-    for (const auto& ip : ips)
-      if (ip.v == v) return &ip;
-    return nullptr;
-  };
   for (const auto& ip : ips)
     src << "  const T* __restrict__ rb" << ip.slot << " = reinterpret_cast<const T*>(a.t[" << ip.slot
         << "]);  // in-place bands of '" << C.P.vars[ip.v].name << "'\n"
         << "  const T* __restrict__ cb" << ip.slot << "_1 = reinterpret_cast<const T*>(a.t[" << ip.slot + 1 << "]);\n"
         << "  const T* __restrict__ cb" << ip.slot << "_2 = reinterpret_cast<const T*>(a.t[" << ip.slot + 2 << "]);\n";
   // ws: trip-stage ring (full: producer -> consumers, empty: consumers -> producer)
-  const int NS = PD + 1;
-  std::vector<size_t> tv;  // TMA-staged vars, in map order
+  NS = PD + 1;
+  tv.clear();  // TMA-staged vars, in map order
   for (size_t v = 0; v < nv; ++v)
     if (ws && staged[v] >= 0) tv.push_back(v);
   if (ws) {
@@ -893,13 +961,8 @@ bool emit_march(Ctx& C, JitProgram& out, std::ostream& src, bool ws = false) {
   // registers.  Measured slower on the BASELINE chains (biharm 163 vs 178 G,
   // box 171 vs 219 G: the register cost outweighs the shared-memory loads
   // saved), so off by default.
-  struct Rot {
-    int K = 1;
-    std::vector<int> from;  // load index whose previous-trip value this load takes (-1: load)
-    std::vector<char> keep;  // value carried to the next trip
-  };
-  std::vector<Rot> rot(G.size());
-  const bool use_rot = lfx::option("LF_JIT_ROT") && std::atoi(lfx::option("LF_JIT_ROT")) != 0;
+  rot.assign(G.size(), Rot{});
+  use_rot = lfx::option("LF_JIT_ROT") && std::atoi(lfx::option("LF_JIT_ROT")) != 0;
   for (size_t gi = 0; gi < G.size(); ++gi) {
     const Grp& g = G[gi];
     Rot& R = rot[gi];
@@ -924,76 +987,79 @@ bool emit_march(Ctx& C, JitProgram& out, std::ostream& src, bool ws = false) {
     for (size_t lj = 0; lj < g.loads.size(); ++lj)
       if (R.keep[lj]) src << "  T rw" << gi << "_" << lj << "[" << R.K << "];\n";
   }
-  // ---- axiom streaming: row `row` of staged var v into slot `slotexpr`
-  auto emit_load = [&](size_t v, const std::string& row, const std::string& slotexpr, const char* ind) {
-    std::vector<int> ext(nd), lo(nd);
-    for (int d = 1; d < nd; ++d) {
-      ext[d] = width(v, d);
-      lo[d] = C.vmin[v][d];
-    }
-    const int K = (ext[1] + STEP - 1) / STEP;
-    std::string I(ind);
-    src << I << "{ const int y = " << row << ";\n";
-    src << I << "  if (y >= r0" << plus(C.vmin[v][0]) << " && y <= r1 - 1" << plus(C.vmax[v][0]) << ") {\n";
-    src << I << "    const unsigned dst = sb" << v << " + (" << slotexpr << ") * " << eb << ";\n";
+}
+
+void March::emit_load(size_t v, const std::string& row, const std::string& slotexpr, const char* ind) {
+  std::vector<int> ext(nd), lo(nd);
+  for (int d = 1; d < nd; ++d) {
+    ext[d] = width(v, d);
+    lo[d] = C.vmin[v][d];
+  }
+  const int K = (ext[1] + STEP - 1) / STEP;
+  std::string I(ind);
+  src << I << "{ const int y = " << row << ";\n";
+  src << I << "  if (y >= r0" << plus(C.vmin[v][0]) << " && y <= r1 - 1" << plus(C.vmax[v][0]) << ") {\n";
+  src << I << "    const unsigned dst = sb" << v << " + (" << slotexpr << ") * " << eb << ";\n";
+  if (nd == 3) {
+    src << I << "    const int c2 = tx" << plus(lo[2]) << ";\n";
+    src << I << "    const int x2 = o2 + c2;\n";
+    src << I << "    if (tx < " << ext[2] << " && x2 <= " << (C.N[2] - 1 + C.vmax[v][2]) << ") {\n";
+  } else {
+    src << I << "    {\n";
+  }
+  src << I << "      const int c1hi = min(" << (lo[1] + ext[1] - 1) << ", " << (C.N[1] - 1 + C.vmax[v][1]) << " - o1);\n";
+  src << I << "      #pragma unroll\n";
+  src << I << "      for (int k = 0; k < " << K << "; ++k) {\n";
+  src << I << "        const int c1 = " << LANE << plus(lo[1]) << " + k * " << STEP << ";\n";
+  src << I << "        if (c1 <= c1hi) {\n";
+  src << I << "          const int x1 = o1 + c1;\n";
+  std::vector<std::string> pos = {"y"};
+  for (int d = 1; d < nd; ++d) pos.push_back("x" + std::to_string(d));
+  src << I << "          const T* sp = t" << staged[v] << " + " << C.tidx(staged[v], pos, C.extra_of(static_cast<int>(v)))
+      << ";\n";
+  if (const IP* ip = ip_of(v)) {
+    // in-place: a cell another unit writes during this step comes from its band
+    const auto& t = C.P.terminals[ip->ai];
+    const auto ex = C.extra_of(static_cast<int>(v));
+    std::vector<long> so(nd);  // storage coordinate = logical + so
+    for (int d = 0; d < nd; ++d) so[d] = ex[d] - t.base[d] + C.LO[d];
+    const long E0 = t.extent[0], E1 = nd > 1 ? t.extent[1] : 1, E2 = nd > 2 ? t.extent[2] : 1;
+    const long BH = C.vmax[v][0] - C.vmin[v][0];
+    const std::string sy = "(long long)(y" + plus(so[0]) + ")", sx1 = "(long long)(x1" + plus(so[1]) + ")",
+                      sx2 = nd > 2 ? "(long long)(x2" + plus(so[2]) + ")" : "0LL";
+    const std::string sl = std::to_string(ip->slot);
+    src << I << "          if (a.inplace) {\n";
+    src << I << "            if (y < r0 || y >= r1) {\n";
+    src << I << "              if (y >= 0 && y < N0) {\n";
+    src << I << "                const int b = y < r0 ? r0 : r1;\n";
+    src << I << "                sp = rb" << sl << " + ((long long)(b / a.chunk - 1) * " << BH << " + (y - b" << plus(-C.vmin[v][0])
+        << ")) * " << (E1 * E2) << "LL + " << sx1 << " * " << E2 << "LL + " << sx2 << ";\n";
+    src << I << "              }\n";
+    src << I << "            } else if (x1 < o1 || x1 >= o1 + " << tile[1] << ") {\n";
+    src << I << "              if (x1 >= 0 && x1 < N1) {\n";
+    src << I << "                const int e = x1 < o1 ? o1 : o1 + " << tile[1] << ";\n";
+    src << I << "                sp = cb" << sl << "_1 + (((long long)(e / " << tile[1] << " - 1) * "
+        << (C.vmax[v][1] - C.vmin[v][1]) << " + (x1 - e" << plus(-C.vmin[v][1]) << ")) * " << E0 << "LL + " << sy
+        << ") * " << E2 << "LL + " << sx2 << ";\n";
+    src << I << "              }\n";
     if (nd == 3) {
-      src << I << "    const int c2 = tx" << plus(lo[2]) << ";\n";
-      src << I << "    const int x2 = o2 + c2;\n";
-      src << I << "    if (tx < " << ext[2] << " && x2 <= " << (C.N[2] - 1 + C.vmax[v][2]) << ") {\n";
-    } else {
-      src << I << "    {\n";
-    }
-    src << I << "      const int c1hi = min(" << (lo[1] + ext[1] - 1) << ", " << (C.N[1] - 1 + C.vmax[v][1]) << " - o1);\n";
-    src << I << "      #pragma unroll\n";
-    src << I << "      for (int k = 0; k < " << K << "; ++k) {\n";
-    src << I << "        const int c1 = " << LANE << plus(lo[1]) << " + k * " << STEP << ";\n";
-    src << I << "        if (c1 <= c1hi) {\n";
-    src << I << "          const int x1 = o1 + c1;\n";
-    std::vector<std::string> pos = {"y"};
-    for (int d = 1; d < nd; ++d) pos.push_back("x" + std::to_string(d));
-    src << I << "          const T* sp = t" << staged[v] << " + " << C.tidx(staged[v], pos, C.extra_of(static_cast<int>(v)))
-        << ";\n";
-    if (const IP* ip = ip_of(v)) {
-      // in-place: a cell another unit writes during this step comes from its band
-      const auto& t = C.P.terminals[ip->ai];
-      const auto ex = C.extra_of(static_cast<int>(v));
-      std::vector<long> so(nd);  // storage coordinate = logical + so
-      for (int d = 0; d < nd; ++d) so[d] = ex[d] - t.base[d] + C.LO[d];
-      const long E0 = t.extent[0], E1 = nd > 1 ? t.extent[1] : 1, E2 = nd > 2 ? t.extent[2] : 1;
-      const long BH = C.vmax[v][0] - C.vmin[v][0];
-      const std::string sy = "(long long)(y" + plus(so[0]) + ")", sx1 = "(long long)(x1" + plus(so[1]) + ")",
-                        sx2 = nd > 2 ? "(long long)(x2" + plus(so[2]) + ")" : "0LL";
-      const std::string sl = std::to_string(ip->slot);
-      src << I << "          if (a.inplace) {\n";
-      src << I << "            if (y < r0 || y >= r1) {\n";
-      src << I << "              if (y >= 0 && y < N0) {\n";
-      src << I << "                const int b = y < r0 ? r0 : r1;\n";
-      src << I << "                sp = rb" << sl << " + ((long long)(b / a.chunk - 1) * " << BH << " + (y - b" << plus(-C.vmin[v][0])
-          << ")) * " << (E1 * E2) << "LL + " << sx1 << " * " << E2 << "LL + " << sx2 << ";\n";
+      src << I << "            } else if (x2 < o2 || x2 >= o2 + " << tile[2] << ") {\n";
+      src << I << "              if (x2 >= 0 && x2 < N2) {\n";
+      src << I << "                const int e = x2 < o2 ? o2 : o2 + " << tile[2] << ";\n";
+      src << I << "                sp = cb" << sl << "_2 + (((long long)(e / " << tile[2] << " - 1) * "
+          << (C.vmax[v][2] - C.vmin[v][2]) << " + (x2 - e" << plus(-C.vmin[v][2]) << ")) * " << E0 << "LL + " << sy
+          << ") * " << E1 << "LL + " << sx1 << ";\n";
       src << I << "              }\n";
-      src << I << "            } else if (x1 < o1 || x1 >= o1 + " << tile[1] << ") {\n";
-      src << I << "              if (x1 >= 0 && x1 < N1) {\n";
-      src << I << "                const int e = x1 < o1 ? o1 : o1 + " << tile[1] << ";\n";
-      src << I << "                sp = cb" << sl << "_1 + (((long long)(e / " << tile[1] << " - 1) * "
-          << (C.vmax[v][1] - C.vmin[v][1]) << " + (x1 - e" << plus(-C.vmin[v][1]) << ")) * " << E0 << "LL + " << sy
-          << ") * " << E2 << "LL + " << sx2 << ";\n";
-      src << I << "              }\n";
-      if (nd == 3) {
-        src << I << "            } else if (x2 < o2 || x2 >= o2 + " << tile[2] << ") {\n";
-        src << I << "              if (x2 >= 0 && x2 < N2) {\n";
-        src << I << "                const int e = x2 < o2 ? o2 : o2 + " << tile[2] << ";\n";
-        src << I << "                sp = cb" << sl << "_2 + (((long long)(e / " << tile[2] << " - 1) * "
-            << (C.vmax[v][2] - C.vmin[v][2]) << " + (x2 - e" << plus(-C.vmin[v][2]) << ")) * " << E0 << "LL + " << sy
-            << ") * " << E1 << "LL + " << sx1 << ";\n";
-        src << I << "              }\n";
-      }
-      src << I << "            }\n";
-      src << I << "          }\n";
     }
-    src << I << "          asm volatile(\"cp.async.ca.shared.global [%0], [%1], " << eb << ";\" :: \"r\"(dst + ("
-        << inplane(v, std::vector<int>(nd, 0)) << ") * " << eb << "), \"l\"(sp) : \"memory\");\n";
-    src << I << "        }\n" << I << "      }\n" << I << "    }\n" << I << "  }\n" << I << "}\n";
-  };
+    src << I << "            }\n";
+    src << I << "          }\n";
+  }
+  src << I << "          asm volatile(\"cp.async.ca.shared.global [%0], [%1], " << eb << ";\" :: \"r\"(dst + ("
+      << inplane(v, std::vector<int>(nd, 0)) << ") * " << eb << "), \"l\"(sp) : \"memory\");\n";
+  src << I << "        }\n" << I << "      }\n" << I << "    }\n" << I << "  }\n" << I << "}\n";
+}
+
+void March::trips() {
   if (!ws) {
   for (int p = 0; p < PD; ++p) {
     for (size_t v = 0; v < nv; ++v)
@@ -1058,212 +1124,217 @@ bool emit_march(Ctx& C, JitProgram& out, std::ostream& src, bool ws = false) {
   src << "    } else {\n";
   src << "    lf_mbar_wait(&lf_full[stg], par);\n";
   }
-  int level = 1;
-  for (size_t gi = 0; gi < G.size(); ++gi) {
-    const Grp& g = G[gi];
-    const auto& k = C.P.rs.kernels[g.kernel];
-    if (g.level != level) {
-      src << (ws ? "    asm volatile(\"bar.sync 1, " + std::to_string(NT) + ";\" ::: \"memory\");\n"
-                 : std::string("    __syncthreads();\n"));
-      level = g.level;
-    }
-    std::vector<int> ext(nd), lo(nd);
-    for (int d = 1; d < nd; ++d) {
-      ext[d] = tile[d] + (g.gmax[d] - g.gmin[d]);
-      lo[d] = g.gmin[d];
-    }
-    const int K = (ext[1] + STEP - 1) / STEP;
-    src << "    { // group " << gi << ": kernel '" << k.name << "', lead " << g.shift << ", level " << g.level << "\n";
-    src << "      const int y = t" << plus(g.shift) << ";\n";
-    src << "      if (y >= r0" << plus(g.gmin[0]) << " && y <= r1 - 1" << plus(g.gmax[0]) << ") {\n";
-    src << "        const bool first = y == r0" << plus(g.gmin[0]) << ";  // segment start: fill the register windows\n";
-    std::map<std::pair<int, int>, std::string> rbs;
-    auto rb = [&](int v, int r) {
-      auto key = std::make_pair(v, r);
-      auto it = rbs.find(key);
-      if (it != rbs.end()) return it->second;
-      std::string nm = "rb" + std::to_string(v) + "_" + (r < 0 ? "m" + std::to_string(-r) : std::to_string(r));
-      src << "        const int " << nm << " = " << rowbase(v, g.shift + r) << ";\n";
-      rbs[key] = nm;
-      return nm;
-    };
-    for (const auto& in : g.loads)
-      if (win[in.var] > 0) rb(in.var, in.rel[0]);
-    for (const auto& o : g.out)
-      if (C.smem_var[o.var]) rb(o.var, o.rel[0]);
-    if (nd == 3) {
-      src << "        const int c2 = tx" << plus(lo[2]) << ";\n";
-      src << "        const int x2 = o2 + c2;\n";
-      src << "        const bool act = tx < " << ext[2] << " && x2 <= " << (C.N[2] - 1 + g.gmax[2]) << ";\n";
-    } else {
-      src << "        const bool act = true;\n";
-    }
-    src << "        const int c1hi = min(" << (lo[1] + ext[1] - 1) << ", " << (C.N[1] - 1 + g.gmax[1]) << " - o1);\n";
-    auto load_index = [&](int var, const std::vector<int>& rel) {
-      for (size_t li = 0; li < g.loads.size(); ++li)
-        if (g.loads[li].var == var && g.loads[li].rel == rel) return static_cast<int>(li);
-      return -1;
-    };
-    // evaluation of one cell from its loaded operands l<li>, then its stores
-    auto emit_eval = [&](const std::string& I) -> bool {
-    for (const auto& in : g.in) {
-      if (in.via < 0) {
-        src << I << "const T p_" << in.param << " = l" << load_index(in.var, in.rel) << ";\n";
-        continue;
-      }
-      // the inlined producer, evaluated at this read's offset
-      const Grp& pg = C.inlined[in.via];
-      const auto& pk = C.P.rs.kernels[pg.kernel];
-      std::string oparam;
-      std::vector<int> orel(nd, 0);
-      for (const auto& o : pg.out)
-        if (o.var == in.var) {
-          oparam = o.param;
-          orel = o.rel;
-        }
-      std::map<std::string, std::string> pv;
-      for (const auto& pin : pg.in) {
-        std::vector<int> r(nd);
-        for (int d = 0; d < nd; ++d) r[d] = in.rel[d] - orel[d] + pin.rel[d];
-        pv[pin.param] = "l" + std::to_string(load_index(pin.var, r));
-      }
-      std::string e2;
-      auto e = lf::parse_expr(pk.bodies.at(oparam), e2);
-      if (!e) return (C.error = "kernel '" + pk.name + "': " + e2, false);
-      src << I << "const T p_" << in.param << " = "
-          << lf::emit_c(*e, C.T, [&](const std::string& n) { return pv.at(n); }) << ";  // inlined '" << pk.name
-          << "'\n";
-    }
-    if (!emit_bodies(C, g, src, I.c_str())) return false;
-    for (const auto& o : g.out) {
-      if (C.smem_var[o.var])
-        src << I << "v" << o.var << "[" << rb(o.var, o.rel[0]) << " + " << inplane(o.var, o.rel) << "] = q_"
-            << o.param << ";\n";
-      const int ti = C.terminal_of(o.var, true);
-      if (ti < 0) continue;
-      // goal: own chunk rows, own tile cells, inside the domain
-      src << I << "if (y" << plus(o.rel[0]) << " >= r0 && y" << plus(o.rel[0]) << " < r1";
-      for (int d = 1; d < nd; ++d)
-        src << " && c" << d << plus(o.rel[d]) << " >= 0 && c" << d << plus(o.rel[d]) << " < " << tile[d] << " && x" << d
-            << plus(o.rel[d]) << " < N" << d;
-      std::vector<std::string> pos;
-      for (int d = 0; d < nd; ++d) pos.push_back((d == 0 ? std::string("y") : "x" + std::to_string(d)) + plus(o.rel[d]));
-      src << ") t" << ti << "[" << C.tidx(ti, pos, std::vector<int>(nd, 0)) << "] = q_" << o.param << ";\n";
-    }
-      return true;
-    };
-    // 2D: V adjacent columns per thread; window operands are loaded once per
-    // distinct (variable, row, column) over the V cells and shared between them
-    const int V = nd == 2 && !use_rot && ILP == 1 ? VEC : 1;
-    if (V > 1) {
-      const int KV = (ext[1] + STEP * V - 1) / (STEP * V);
-      src << "        #pragma unroll\n";
-      src << "        for (int k = 0; k < " << KV << "; ++k) {\n";
-      src << "          const int cb = " << V << " * tx" << plus(lo[1]) << " + k * " << STEP * V << ";\n";
-      std::map<std::tuple<int, int, int>, int> need;  // (var, row offset, column offset) -> first cell needing it
-      for (const auto& in : g.loads)
-        if (win[in.var] > 0)
-          for (int v = 0; v < V; ++v) {
-            const auto key = std::make_tuple(in.var, in.rel[0], v + in.rel[1]);
-            auto it = need.find(key);
-            if (it == need.end() || it->second > v) need[key] = v;
-          }
-      auto uname = [](int var, int r, int u) {
-        return "w" + std::to_string(var) + "_" + (r < 0 ? "m" + std::to_string(-r) : std::to_string(r)) + "_" +
-               (u < 0 ? "m" + std::to_string(-u) : std::to_string(u));
-      };
-      for (const auto& [key, v0] : need) {
-        const auto [var, r, u] = key;
-        src << "          const T " << uname(var, r, u) << " = cb" << plus(v0) << " <= c1hi ? v" << var << "["
-            << rb(var, r) << " + cb" << plus(u - C.vmin[var][1]) << "] : T(0);\n";
-      }
-      for (int v = 0; v < V; ++v) {
-        src << "          { const int c1 = cb" << plus(v) << ";\n";
-        src << "            const int x1 = o1 + c1;\n";
-        src << "            if (c1 <= c1hi) {\n";
-        for (size_t li = 0; li < g.loads.size(); ++li) {
-          const Load& in = g.loads[li];
-          if (win[in.var] > 0) {
-            src << "            const T l" << li << " = " << uname(in.var, in.rel[0], v + in.rel[1]) << ";\n";
-          } else {
-            const int ti = C.terminal_of(in.var, false);
-            std::string r;
-            if (C.P.terminals[ti].dims.empty()) {
-              r = "s" + std::to_string(ti);
-            } else {
-              std::vector<std::string> pos;
-              for (int d = 0; d < nd; ++d)
-                pos.push_back((d == 0 ? std::string("y") : "x" + std::to_string(d)) + plus(in.rel[d]));
-              r = "__ldg(t" + std::to_string(ti) + " + " + C.tidx(ti, pos, C.extra_of(in.var)) + ")";
-            }
-            src << "            const T l" << li << " = " << r << ";\n";
-          }
-        }
-        if (!emit_eval("            ")) return false;
-        src << "            }\n          }\n";
-      }
-      src << "        }\n      }\n    }\n";
+}
+
+// one callsite group: row t + shift of its outputs, its cells of the tile
+bool March::group(size_t gi, int& level) {
+  const Grp& g = G[gi];
+  const auto& k = C.P.rs.kernels[g.kernel];
+  if (g.level != level) {
+    src << (ws ? "    asm volatile(\"bar.sync 1, " + std::to_string(NT) + ";\" ::: \"memory\");\n"
+               : std::string("    __syncthreads();\n"));
+    level = g.level;
+  }
+  std::vector<int> ext(nd), lo(nd);
+  for (int d = 1; d < nd; ++d) {
+    ext[d] = tile[d] + (g.gmax[d] - g.gmin[d]);
+    lo[d] = g.gmin[d];
+  }
+  const int K = (ext[1] + STEP - 1) / STEP;
+  src << "    { // group " << gi << ": kernel '" << k.name << "', lead " << g.shift << ", level " << g.level << "\n";
+  src << "      const int y = t" << plus(g.shift) << ";\n";
+  src << "      if (y >= r0" << plus(g.gmin[0]) << " && y <= r1 - 1" << plus(g.gmax[0]) << ") {\n";
+  src << "        const bool first = y == r0" << plus(g.gmin[0]) << ";  // segment start: fill the register windows\n";
+  std::map<std::pair<int, int>, std::string> rbs;
+  auto rb = [&](int v, int r) {
+    auto key = std::make_pair(v, r);
+    auto it = rbs.find(key);
+    if (it != rbs.end()) return it->second;
+    std::string nm = "rb" + std::to_string(v) + "_" + (r < 0 ? "m" + std::to_string(-r) : std::to_string(r));
+    src << "        const int " << nm << " = " << rowbase(v, g.shift + r) << ";\n";
+    rbs[key] = nm;
+    return nm;
+  };
+  for (const auto& in : g.loads)
+    if (win[in.var] > 0) rb(in.var, in.rel[0]);
+  for (const auto& o : g.out)
+    if (C.smem_var[o.var]) rb(o.var, o.rel[0]);
+  if (nd == 3) {
+    src << "        const int c2 = tx" << plus(lo[2]) << ";\n";
+    src << "        const int x2 = o2 + c2;\n";
+    src << "        const bool act = tx < " << ext[2] << " && x2 <= " << (C.N[2] - 1 + g.gmax[2]) << ";\n";
+  } else {
+    src << "        const bool act = true;\n";
+  }
+  src << "        const int c1hi = min(" << (lo[1] + ext[1] - 1) << ", " << (C.N[1] - 1 + g.gmax[1]) << " - o1);\n";
+  auto load_index = [&](int var, const std::vector<int>& rel) {
+    for (size_t li = 0; li < g.loads.size(); ++li)
+      if (g.loads[li].var == var && g.loads[li].rel == rel) return static_cast<int>(li);
+    return -1;
+  };
+  // evaluation of one cell from its loaded operands l<li>, then its stores
+  auto emit_eval = [&](const std::string& I) -> bool {
+  for (const auto& in : g.in) {
+    if (in.via < 0) {
+      src << I << "const T p_" << in.param << " = l" << load_index(in.var, in.rel) << ";\n";
       continue;
     }
-    // phase 1: every operand of the K cells this thread owns (independent loads)
-    // in batches of ILP cells (bounded register footprint)
-    const int B = std::min(K, ILP);
+    // the inlined producer, evaluated at this read's offset
+    const Grp& pg = C.inlined[in.via];
+    const auto& pk = C.P.rs.kernels[pg.kernel];
+    std::string oparam;
+    std::vector<int> orel(nd, 0);
+    for (const auto& o : pg.out)
+      if (o.var == in.var) {
+        oparam = o.param;
+        orel = o.rel;
+      }
+    std::map<std::string, std::string> pv;
+    for (const auto& pin : pg.in) {
+      std::vector<int> r(nd);
+      for (int d = 0; d < nd; ++d) r[d] = in.rel[d] - orel[d] + pin.rel[d];
+      pv[pin.param] = "l" + std::to_string(load_index(pin.var, r));
+    }
+    std::string e2;
+    auto e = lf::parse_expr(pk.bodies.at(oparam), e2);
+    if (!e) return (C.error = "kernel '" + pk.name + "': " + e2, false);
+    src << I << "const T p_" << in.param << " = "
+        << lf::emit_c(*e, C.T, [&](const std::string& n) { return pv.at(n); }) << ";  // inlined '" << pk.name
+        << "'\n";
+  }
+  if (!emit_bodies(C, g, src, I.c_str())) return false;
+  for (const auto& o : g.out) {
+    if (C.smem_var[o.var])
+      src << I << "v" << o.var << "[" << rb(o.var, o.rel[0]) << " + " << inplane(o.var, o.rel) << "] = q_"
+          << o.param << ";\n";
+    const int ti = C.terminal_of(o.var, true);
+    if (ti < 0) continue;
+    // goal: own chunk rows, own tile cells, inside the domain
+    src << I << "if (y" << plus(o.rel[0]) << " >= r0 && y" << plus(o.rel[0]) << " < r1";
+    for (int d = 1; d < nd; ++d)
+      src << " && c" << d << plus(o.rel[d]) << " >= 0 && c" << d << plus(o.rel[d]) << " < " << tile[d] << " && x" << d
+          << plus(o.rel[d]) << " < N" << d;
+    std::vector<std::string> pos;
+    for (int d = 0; d < nd; ++d) pos.push_back((d == 0 ? std::string("y") : "x" + std::to_string(d)) + plus(o.rel[d]));
+    src << ") t" << ti << "[" << C.tidx(ti, pos, std::vector<int>(nd, 0)) << "] = q_" << o.param << ";\n";
+  }
+    return true;
+  };
+  // 2D: V adjacent columns per thread; window operands are loaded once per
+  // distinct (variable, row, column) over the V cells and shared between them
+  const int V = nd == 2 && !use_rot && ILP == 1 ? VEC : 1;
+  if (V > 1) {
+    const int KV = (ext[1] + STEP * V - 1) / (STEP * V);
     src << "        #pragma unroll\n";
-    src << "        for (int kb = 0; kb < " << K << "; kb += " << B << ") {\n";
-    for (size_t li = 0; li < g.loads.size(); ++li) src << "        T a_l" << li << "[" << B << "];\n";
-    src << "        #pragma unroll\n";
-    src << "        for (int kk = 0; kk < " << B << "; ++kk) {\n";
-    src << "          const int k = kb + kk;\n";
-    src << "          const int c1 = " << LANE << plus(lo[1]) << " + k * " << STEP << ";\n";
-    src << "          const int x1 = o1 + c1;\n";
-    src << "          if (act && c1 <= c1hi) {\n";
-    std::vector<std::string> reads(g.loads.size());
-    bool any_rot = false;
-    for (size_t li = 0; li < g.loads.size(); ++li) {
-      const Load& in = g.loads[li];
-      std::string r;
-      if (win[in.var] > 0) {
-        r = "v" + std::to_string(in.var) + "[" + rb(in.var, in.rel[0]) + " + " + inplane(in.var, in.rel) + "]";
-      } else {
-        const int ti = C.terminal_of(in.var, false);
-        if (C.P.terminals[ti].dims.empty()) {
-          r = "s" + std::to_string(ti);
+    src << "        for (int k = 0; k < " << KV << "; ++k) {\n";
+    src << "          const int cb = " << V << " * tx" << plus(lo[1]) << " + k * " << STEP * V << ";\n";
+    std::map<std::tuple<int, int, int>, int> need;  // (var, row offset, column offset) -> first cell needing it
+    for (const auto& in : g.loads)
+      if (win[in.var] > 0)
+        for (int v = 0; v < V; ++v) {
+          const auto key = std::make_tuple(in.var, in.rel[0], v + in.rel[1]);
+          auto it = need.find(key);
+          if (it == need.end() || it->second > v) need[key] = v;
+        }
+    auto uname = [](int var, int r, int u) {
+      return "w" + std::to_string(var) + "_" + (r < 0 ? "m" + std::to_string(-r) : std::to_string(r)) + "_" +
+             (u < 0 ? "m" + std::to_string(-u) : std::to_string(u));
+    };
+    for (const auto& [key, v0] : need) {
+      const auto [var, r, u] = key;
+      src << "          const T " << uname(var, r, u) << " = cb" << plus(v0) << " <= c1hi ? v" << var << "["
+          << rb(var, r) << " + cb" << plus(u - C.vmin[var][1]) << "] : T(0);\n";
+    }
+    for (int v = 0; v < V; ++v) {
+      src << "          { const int c1 = cb" << plus(v) << ";\n";
+      src << "            const int x1 = o1 + c1;\n";
+      src << "            if (c1 <= c1hi) {\n";
+      for (size_t li = 0; li < g.loads.size(); ++li) {
+        const Load& in = g.loads[li];
+        if (win[in.var] > 0) {
+          src << "            const T l" << li << " = " << uname(in.var, in.rel[0], v + in.rel[1]) << ";\n";
         } else {
-          std::vector<std::string> pos;
-          for (int d = 0; d < nd; ++d) pos.push_back((d == 0 ? std::string("y") : "x" + std::to_string(d)) + plus(in.rel[d]));
-          r = "__ldg(t" + std::to_string(ti) + " + " + C.tidx(ti, pos, C.extra_of(in.var)) + ")";
+          const int ti = C.terminal_of(in.var, false);
+          std::string r;
+          if (C.P.terminals[ti].dims.empty()) {
+            r = "s" + std::to_string(ti);
+          } else {
+            std::vector<std::string> pos;
+            for (int d = 0; d < nd; ++d)
+              pos.push_back((d == 0 ? std::string("y") : "x" + std::to_string(d)) + plus(in.rel[d]));
+            r = "__ldg(t" + std::to_string(ti) + " + " + C.tidx(ti, pos, C.extra_of(in.var)) + ")";
+          }
+          src << "            const T l" << li << " = " << r << ";\n";
         }
       }
-      reads[li] = r;
-      any_rot |= rot[gi].from[li] >= 0;
+      if (!emit_eval("            ")) return false;
+      src << "            }\n          }\n";
     }
-    if (any_rot) {
-      // the branch is uniform: the first trip of a segment loads every row
-      src << "            if (first) {\n";
-      for (size_t li = 0; li < g.loads.size(); ++li) src << "              a_l" << li << "[kk] = " << reads[li] << ";\n";
-      src << "            } else {\n";
-      for (size_t li = 0; li < g.loads.size(); ++li)
-        src << "              a_l" << li << "[kk] = "
-            << (rot[gi].from[li] >= 0 ? "rw" + std::to_string(gi) + "_" + std::to_string(rot[gi].from[li]) + "[k]" : reads[li])
-            << ";\n";
-      src << "            }\n";
-    } else {
-      for (size_t li = 0; li < g.loads.size(); ++li) src << "            a_l" << li << "[kk] = " << reads[li] << ";\n";
-    }
-    for (size_t lj = 0; lj < g.loads.size(); ++lj)
-      if (rot[gi].keep[lj]) src << "            rw" << gi << "_" << lj << "[k] = a_l" << lj << "[kk];\n";
-    src << "          }\n        }\n";
-    // phase 2: evaluate and store
-    src << "        #pragma unroll\n";
-    src << "        for (int kk = 0; kk < " << B << "; ++kk) {\n";
-    src << "          const int k = kb + kk;\n";
-    src << "          const int c1 = " << LANE << plus(lo[1]) << " + k * " << STEP << ";\n";
-    src << "          const int x1 = o1 + c1;\n";
-    src << "          if (act && c1 <= c1hi) {\n";
-    for (size_t li = 0; li < g.loads.size(); ++li) src << "            const T l" << li << " = a_l" << li << "[kk];\n";
-    if (!emit_eval("            ")) return false;
-    src << "          }\n        }\n        }\n      }\n    }\n";
+    src << "        }\n      }\n    }\n";
+    return true;
   }
+  // phase 1: every operand of the K cells this thread owns (independent loads)
+  // in batches of ILP cells (bounded register footprint)
+  const int B = std::min(K, ILP);
+  src << "        #pragma unroll\n";
+  src << "        for (int kb = 0; kb < " << K << "; kb += " << B << ") {\n";
+  for (size_t li = 0; li < g.loads.size(); ++li) src << "        T a_l" << li << "[" << B << "];\n";
+  src << "        #pragma unroll\n";
+  src << "        for (int kk = 0; kk < " << B << "; ++kk) {\n";
+  src << "          const int k = kb + kk;\n";
+  src << "          const int c1 = " << LANE << plus(lo[1]) << " + k * " << STEP << ";\n";
+  src << "          const int x1 = o1 + c1;\n";
+  src << "          if (act && c1 <= c1hi) {\n";
+  std::vector<std::string> reads(g.loads.size());
+  bool any_rot = false;
+  for (size_t li = 0; li < g.loads.size(); ++li) {
+    const Load& in = g.loads[li];
+    std::string r;
+    if (win[in.var] > 0) {
+      r = "v" + std::to_string(in.var) + "[" + rb(in.var, in.rel[0]) + " + " + inplane(in.var, in.rel) + "]";
+    } else {
+      const int ti = C.terminal_of(in.var, false);
+      if (C.P.terminals[ti].dims.empty()) {
+        r = "s" + std::to_string(ti);
+      } else {
+        std::vector<std::string> pos;
+        for (int d = 0; d < nd; ++d) pos.push_back((d == 0 ? std::string("y") : "x" + std::to_string(d)) + plus(in.rel[d]));
+        r = "__ldg(t" + std::to_string(ti) + " + " + C.tidx(ti, pos, C.extra_of(in.var)) + ")";
+      }
+    }
+    reads[li] = r;
+    any_rot |= rot[gi].from[li] >= 0;
+  }
+  if (any_rot) {
+    // the branch is uniform: the first trip of a segment loads every row
+    src << "            if (first) {\n";
+    for (size_t li = 0; li < g.loads.size(); ++li) src << "              a_l" << li << "[kk] = " << reads[li] << ";\n";
+    src << "            } else {\n";
+    for (size_t li = 0; li < g.loads.size(); ++li)
+      src << "              a_l" << li << "[kk] = "
+          << (rot[gi].from[li] >= 0 ? "rw" + std::to_string(gi) + "_" + std::to_string(rot[gi].from[li]) + "[k]" : reads[li])
+          << ";\n";
+    src << "            }\n";
+  } else {
+    for (size_t li = 0; li < g.loads.size(); ++li) src << "            a_l" << li << "[kk] = " << reads[li] << ";\n";
+  }
+  for (size_t lj = 0; lj < g.loads.size(); ++lj)
+    if (rot[gi].keep[lj]) src << "            rw" << gi << "_" << lj << "[k] = a_l" << lj << "[kk];\n";
+  src << "          }\n        }\n";
+  // phase 2: evaluate and store
+  src << "        #pragma unroll\n";
+  src << "        for (int kk = 0; kk < " << B << "; ++kk) {\n";
+  src << "          const int k = kb + kk;\n";
+  src << "          const int c1 = " << LANE << plus(lo[1]) << " + k * " << STEP << ";\n";
+  src << "          const int x1 = o1 + c1;\n";
+  src << "          if (act && c1 <= c1hi) {\n";
+  for (size_t li = 0; li < g.loads.size(); ++li) src << "            const T l" << li << " = a_l" << li << "[kk];\n";
+  if (!emit_eval("            ")) return false;
+  src << "          }\n        }\n        }\n      }\n    }\n";
+  return true;
+}
+
+void March::tail() {
   if (ws) {
     // this warp is done with the trip's window rows
     src << "    __syncwarp();\n";
@@ -1279,6 +1350,9 @@ bool emit_march(Ctx& C, JitProgram& out, std::ostream& src, bool ws = false) {
   }
   src << "  }\n";
   src << "}\n";
+}
+
+void March::capture() {
   // ---- in-place: capture the bands other units read before this step writes
   if (!ips.empty()) {
     std::vector<std::pair<size_t, int>> caps;  // (variable, terminal)
@@ -1287,7 +1361,12 @@ bool emit_march(Ctx& C, JitProgram& out, std::ostream& src, bool ws = false) {
     for (const auto& ip : ips) slots.push_back(ip.slot);
     emit_capture(C, "lf_jit_capture", caps, slots, tile, src);
   }
-  return true;
+}
+}  // namespace
+
+bool emit_march(Ctx& C, JitProgram& out, std::ostream& src, bool ws = false) {
+  March m(C, out, src, ws);
+  return m.emit();
 }
 
 // ---------------------------------------------------------------------------
