@@ -1977,11 +1977,12 @@ using namespace cg;
 
 // Programmatic dependent launch (jit.cpp launches with programmatic stream
 // serialization): every generated kernel first waits for the previous grid of
-// the stream (its inputs written, its outputs free).  The single-wave kernels
-// (the persistent marches, ghost fill, in-place capture / commit) then let the
-// next launch be scheduled at once; the multi-wave nest kernels do not (the
-// next grid's waiting CTAs would take the slots of their later waves:
-// normalization 117 -> 110 G measured).  Inserted as each kernel's first statement.
+// the stream (its inputs written, its outputs free).  The persistent march
+// kernels then let the next launch (the light ghost fill / in-place commit) be
+// scheduled at once; the other kernels only wait: a multi-wave nest kernel's
+// dependents would take the slots of its later waves (normalization 117 ->
+// 110 G), and early-launched march CTAs behind a fill or capture cost the 3D
+// in-place chain 9 % (136 -> 124 G).  Inserted as each kernel's first statement.
 static std::string with_pdl(const std::string& src) {
   std::string out =
       "__device__ __forceinline__ void lf_pdl_wait() { asm volatile(\"griddepcontrol.wait;\" ::: \"memory\"); }\n"
@@ -1995,9 +1996,9 @@ static std::string with_pdl(const std::string& src) {
     if (k == std::string::npos) break;
     const size_t brace = src.find(") {\n", k);
     if (brace == std::string::npos) break;
-    const bool wave = src.substr(k, brace - k).find(" lf_nest") != std::string::npos;
+    const bool march = src.substr(k, brace - k).find(" lf_jit_step") != std::string::npos;
     out += src.substr(pos, brace + 4 - pos);
-    out += wave ? "  lf_pdl_wait();\n" : "  lf_pdl();\n";
+    out += march ? "  lf_pdl();\n" : "  lf_pdl_wait();\n";
     pos = brace + 4;
   }
   out += src.substr(pos);
