@@ -115,20 +115,97 @@ void emit_commit2(Ctx& C, const char* name, const std::vector<std::pair<size_t, 
   src << "}\n";
 }
 
-bool emit_rmarch(Ctx& C, JitProgram& out, std::ostream& src) {
-  if (C.nd != 2) return false;
-  const int eb = out.elem_bytes;
-  const int CH = 16 / eb;  // elements per 16-B chunk
-  int V = eb == 8 ? 2 : 4;
+// The register-march emitter (lf_jit_step_rm): rows() sizes the rolling
+// windows (a shared-memory ring per streamed axiom, registers per
+// intermediate), columns() the lane span and strip width from the groups'
+// exactness margins, layout() the shared memory, inplace() the deferred-write
+// bands, head() the kernel head and the per-unit setup, trips() the unrolled
+// trip loop: producer() the TMA row boxes, group() one callsite group,
+// copy_tail() the window rotation; commit() the in-place commit kernel.
+class RMarch {
+ public:
+  RMarch(Ctx& c, JitProgram& o, std::ostream& s)
+      : C(c), out(o), src(s), eb(o.elem_bytes), CH(16 / o.elem_bytes), nv(c.P.vars.size()), G(c.groups) {}
+  bool emit() {
+    if (C.nd != 2) return false;
+    if (!rows() || !columns() || !layout()) return false;
+    inplace();
+    trip_range();
+    head();
+    maps();
+    if (!trips()) return false;
+    commit();
+    return true;
+  }
+
+ private:
+  struct IP {
+    size_t v;
+    int ai, gi, slot;
+  };
+  Ctx& C;
+  JitProgram& out;
+  std::ostream& src;
+  const int eb, CH;  // element bytes, elements per 16-B chunk
+  const size_t nv;
+  const std::vector<Grp>& G;
+  const std::string VT = eb == 8 ? "double2" : "float4";
+  const char* comp[4] = {"x", "y", "z", "w"};
+  int V = 4, NW = 8, PD = 3, NS = 4;  // cells per lane, consumer warps, trips in flight, ring stages
+  std::vector<int> lead, old, win, staged, drop;
+  int goal_ti = -1;
+  std::vector<int> vmin1, vmax1, A, B;
+  std::vector<long> base_al, rho;
+  long cs = 0, tw = 0, T1 = 0, inner = 1;
+  std::vector<int> nbox, bw;
+  std::vector<long> soff;
+  size_t smem = 0;
+  std::vector<IP> ips;
+  int TS = 0, TE = 0;
+  int U = 1, cu = 0;  // trip-loop unroll (register-window renaming), the copy being emitted
+  std::string trip_end;
+
+  bool rows();
+  bool columns();
+  bool layout();
+  void inplace();
+  void trip_range();
+  void head();
+  void maps();
+  bool trips();
+  void producer();
+  bool group(size_t gi);
+  void store_goals(size_t gi, const std::vector<std::pair<int, const GOut*>>& goals);
+  void copy_tail();
+  void commit();
+  long goal_so(int ti) const { return -C.P.terminals[ti].base[1] + C.LO[1]; }  // storage col = logical + so
+  int phys(int v, int k) const { return U == 1 ? k : (k + cu) % win[v]; }
+  const IP* ip_of_goal(int ti) const {
+    for (const auto& ip : ips)
+      if (ip.gi == ti) return &ip;
+    return nullptr;
+  }
+  std::string rowbase(size_t v, int off) const {
+    const int W = win[v];
+    if (W == 1) return "0";
+    const int o = ((off % W) + W) % W;
+    const std::string b = "b" + std::to_string(v);
+    const std::string sum = o ? "(" + b + " + " + std::to_string(o) + ")" : b;
+    const std::string sl =
+        o ? "(" + sum + " >= " + std::to_string(W) + " ? " + sum + " - " + std::to_string(W) + " : " + sum + ")" : b;
+    return sl + " * " + std::to_string(nbox[v] * bw[v]);
+  }
+};
+
+bool RMarch::rows() {
+  V = eb == 8 ? 2 : 4;
   if (const char* e = lfx::option("LF_JIT_RM_V")) V = std::atoi(e);
   if (V < CH || V % CH || V > 16) return false;
-  int NW = 8;  // consumer warps per CTA
+  NW = 8;  // consumer warps per CTA
   if (const char* e = lfx::option("LF_JIT_RM_WARPS")) NW = std::max(1, std::min(16, std::atoi(e)));
-  int PD = 3;
+  PD = 3;
   if (const char* e = lfx::option("LF_JIT_PD")) PD = std::max(1, std::atoi(e));
-  const int NS = PD + 1;
-  const size_t nv = C.P.vars.size();
-  const auto& G = C.groups;
+  NS = PD + 1;
   if (G.empty()) return false;
   for (const auto& g : G)
     for (const auto& o : g.out)
@@ -136,7 +213,10 @@ bool emit_rmarch(Ctx& C, JitProgram& out, std::ostream& src) {
 
   // ---- rows: streamed axioms in a shared-memory ring (+ PD rows in flight),
   // intermediates in registers (exactly the contraction span)
-  std::vector<int> lead(nv, INT_MIN), old(nv, INT_MAX), win(nv, 0), staged(nv, -1);
+  lead.assign(nv, INT_MIN);
+  old.assign(nv, INT_MAX);
+  win.assign(nv, 0);
+  staged.assign(nv, -1);
   for (const auto& g : G)
     for (const auto& in : g.loads) {
       lead[in.var] = std::max(lead[in.var], C.smem_var[in.var] ? INT_MIN : g.shift + in.rel[0]);
@@ -160,7 +240,7 @@ bool emit_rmarch(Ctx& C, JitProgram& out, std::ostream& src) {
   if (reg_words > 96) return false;  // register windows would spill
   // fault injection (R/SPEC.md:557, as in emit_march): the named intermediate
   // keeps one row fewer than its contraction span
-  std::vector<int> drop(nv, 0);
+  drop.assign(nv, 0);
   if (const char* f = lfx::option("LF_JIT_FAULT"); f && std::strncmp(f, "span:", 5) == 0)
     for (size_t v = 0; v < nv; ++v)
       if (C.smem_var[v] && win[v] > 1 && C.P.vars[v].name == f + 5) {
@@ -168,6 +248,10 @@ bool emit_rmarch(Ctx& C, JitProgram& out, std::ostream& src) {
         win[v] -= 1;
       }
 
+  return true;
+}
+
+bool RMarch::columns() {
   // ---- columns.  A lane's cells are c = cs + lane * V + i (warp-strip
   // relative).  A_g / B_g: how far from the lane span's left / right end group
   // g's values are still exact -- each shuffle across the warp edge eats the
@@ -175,13 +259,13 @@ bool emit_rmarch(Ctx& C, JitProgram& out, std::ostream& src) {
   // row (whose lane vectors start rho_v cells left of the lane's first cell)
   // at rho_v + dr.  The first goal fixes the lane alignment (its 16-B chunks
   // start at lane cells): cs = res (mod CH)
-  int goal_ti = -1;
+  goal_ti = -1;
   for (const auto& g : G)
     for (const auto& o : g.out)
       if (goal_ti < 0 && C.terminal_of(o.var, true) >= 0) goal_ti = C.terminal_of(o.var, true);
   if (goal_ti < 0) return false;
-  auto goal_so = [&](int ti) { return -C.P.terminals[ti].base[1] + C.LO[1]; };  // storage col = logical + so
-  std::vector<int> vmin1(nv, 0), vmax1(nv, 0);
+  vmin1.assign(nv, 0);
+  vmax1.assign(nv, 0);
   for (size_t v = 0; v < nv; ++v) {
     if (staged[v] < 0) continue;
     const auto& t = C.P.terminals[staged[v]];
@@ -190,8 +274,10 @@ bool emit_rmarch(Ctx& C, JitProgram& out, std::ostream& src) {
     vmax1[v] = C.vmax[v][1];
     vmin1[v] -= static_cast<int>(((vmin1[v] + so) % CH + CH) % CH);  // TMA box origin 16-B aligned
   }
-  std::vector<long> base_al(nv, 0), rho(nv, 0);
-  std::vector<int> A(G.size(), 0), B(G.size(), 0);
+  base_al.assign(nv, 0);
+  rho.assign(nv, 0);
+  A.assign(G.size(), 0);
+  B.assign(G.size(), 0);
   auto margins = [&](long cs) {
     for (size_t v = 0; v < nv; ++v)
       if (staged[v] >= 0) {
@@ -219,7 +305,7 @@ bool emit_rmarch(Ctx& C, JitProgram& out, std::ostream& src) {
     }
   };
   const long res = ((-goal_so(goal_ti)) % CH + CH) % CH;
-  long cs = LONG_MAX;
+  cs = LONG_MAX;
   for (size_t gi = 0; gi < G.size(); ++gi) cs = std::min<long>(cs, G[gi].gmin[1]);
   cs = res + floordiv(cs - res, CH) * CH;
   for (int it = 0;; ++it) {
@@ -230,19 +316,24 @@ bool emit_rmarch(Ctx& C, JitProgram& out, std::ostream& src) {
     if (it > 8) return false;
     cs -= CH;
   }
-  long tw = LONG_MAX;
+  tw = LONG_MAX;
   for (size_t gi = 0; gi < G.size(); ++gi) tw = std::min<long>(tw, cs + 32L * V - B[gi] - G[gi].gmax[1]);
   tw = tw / CH * CH;
   if (tw < 2 * CH || tw < 4) return false;
   if (const char* e = lfx::option("LF_JIT_RM_TW")) tw = std::min<long>(tw, std::max(CH, std::atoi(e) / CH * CH));
-  const long T1 = NW * tw;  // CTA tile
-  const long inner = (C.N[1] + T1 - 1) / T1;
+  T1 = NW * tw;  // CTA tile
+  inner = (C.N[1] + T1 - 1) / T1;
 
+  return true;
+}
+
+bool RMarch::layout() {
   // ---- shared memory: the streamed axioms' rings (TMA boxes of <= 256
   // elements, 128-B multiples), 16-B aligned windows, guard pads for the
   // junk lanes' reads just outside a window
-  std::vector<int> nbox(nv, 1), bw(nv, 0);
-  std::vector<long> soff(nv, 0);
+  nbox.assign(nv, 1);
+  bw.assign(nv, 0);
+  soff.assign(nv, 0);
   long lo_idx = 0, hi_over = 0;
   for (size_t v = 0; v < nv; ++v) {
     if (staged[v] < 0) continue;
@@ -256,7 +347,7 @@ bool emit_rmarch(Ctx& C, JitProgram& out, std::ostream& src) {
     hi_over = std::max(hi_over, (NW - 1) * tw + 32L * V + base_al[v] - static_cast<long>(nbox[v]) * bw[v]);
   }
   const size_t pad_front = static_cast<size_t>((-lo_idx * eb + 127) / 128 * 128);
-  size_t smem = pad_front;
+  smem = pad_front;
   for (size_t v = 0; v < nv; ++v) {
     if (staged[v] < 0) continue;
     soff[v] = smem;
@@ -269,6 +360,10 @@ bool emit_rmarch(Ctx& C, JitProgram& out, std::ostream& src) {
   out.rm_threads = 32 * (NW + 1);
   out.rm_inner_tiles = inner;
   out.rm_maps.clear();
+  return true;
+}
+
+void RMarch::inplace() {
   // in place (config.aliases, the caller passes one buffer): whole (chunk,
   // CTA tile) units that defer their boundary writes.  A unit's cells that a
   // neighbouring unit still reads during the step -- rows within the read
@@ -280,11 +375,7 @@ bool emit_rmarch(Ctx& C, JitProgram& out, std::ostream& src) {
   // march's argument slots (row bands full width, [boundary][row][col]; column
   // bands column-major, [boundary][col within the band][row], so an edge lane's
   // writes down the march fill whole sectors).
-  struct IP {
-    size_t v;
-    int ai, gi, slot;
-  };
-  std::vector<IP> ips;
+  ips.clear();
   out.rm_inplace.clear();
   {
     const int nterm = static_cast<int>(C.P.terminals.size());
@@ -326,14 +417,12 @@ bool emit_rmarch(Ctx& C, JitProgram& out, std::ostream& src) {
       out.rm_inplace.push_back(q);
     }
   }
-  auto ip_of_goal = [&](int ti) -> const IP* {
-    for (const auto& ip : ips)
-      if (ip.gi == ti) return &ip;
-    return nullptr;
-  };
+}
 
+void RMarch::trip_range() {
   // trip range relative to the chunk [r0, r1)
-  int TS = INT_MAX, TE = INT_MIN;
+  TS = INT_MAX;
+  TE = INT_MIN;
   for (const auto& g : G) {
     TS = std::min(TS, g.gmin[0] - g.shift);
     TE = std::max(TE, g.gmax[0] - g.shift);
@@ -341,11 +430,12 @@ bool emit_rmarch(Ctx& C, JitProgram& out, std::ostream& src) {
   for (size_t v = 0; v < nv; ++v)
     if (staged[v] >= 0) TS = std::min(TS, C.vmin[v][0] - lead[v]);
 
+}
+
+void RMarch::head() {
   int minb = 3;  // <= 72 registers: 3 CTAs of 9 warps per SM (the in-place store path needs 75 uncapped)
   if (const char* e = lfx::option("LF_JIT_RM_MINB")) minb = std::max(1, std::atoi(e));
   emit_prelude(C, src, out.rm_threads, minb, "lf_jit_step_rm");
-  const std::string VT = eb == 8 ? "double2" : "float4";
-  const char* comp[4] = {"x", "y", "z", "w"};
   src << "  // register march: " << NW << " consumer warps x " << tw << "-column strips, " << V
       << " cells per lane (lane span starts at column " << cs << " of the strip)\n";
   for (size_t v = 0; v < nv; ++v)
@@ -406,17 +496,9 @@ bool emit_rmarch(Ctx& C, JitProgram& out, std::ostream& src) {
     src << "    }\n  }\n";
   }
 
-  auto rowbase = [&](size_t v, int off) -> std::string {
-    const int W = win[v];
-    if (W == 1) return "0";
-    const int o = ((off % W) + W) % W;
-    const std::string b = "b" + std::to_string(v);
-    const std::string sum = o ? "(" + b + " + " + std::to_string(o) + ")" : b;
-    const std::string sl =
-        o ? "(" + sum + " >= " + std::to_string(W) + " ? " + sum + " - " + std::to_string(W) + " : " + sum + ")" : b;
-    return sl + " * " + std::to_string(nbox[v] * bw[v]);
-  };
+}
 
+void RMarch::maps() {
   for (size_t v = 0; v < nv; ++v) {
     if (staged[v] < 0) continue;
     const auto& t = C.P.terminals[staged[v]];
@@ -433,13 +515,14 @@ bool emit_rmarch(Ctx& C, JitProgram& out, std::ostream& src) {
   // register windows rotate by renaming: the trip loop is unrolled U = lcm(W_v)
   // times and copy u keeps the row of logical slot k in R_v[(k + u) % W_v] (no
   // moves); windows whose lcm exceeds 6 shift by moves at the end of each trip
-  int U = 1;
+  U = 1;
   for (size_t v = 0; v < nv; ++v)
     if (C.smem_var[v] && win[v] > 1) U = std::lcm(U, win[v]);
   if (U > 6 || (lfx::option("LF_JIT_RM_UNROLL") && std::atoi(lfx::option("LF_JIT_RM_UNROLL")) == 0)) U = 1;
-  int cu = 0;  // the copy being emitted
-  auto phys = [&](int v, int k) { return U == 1 ? k : (k + cu) % win[v]; };
-  const std::string trip_end = "r1 - 1 + (" + std::to_string(TE) + ")";
+  trip_end = "r1 - 1 + (" + std::to_string(TE) + ")";
+}
+
+bool RMarch::trips() {
   if (U == 1) {
     src << "  for (int t = r0 + (" << TS << "); t <= " << trip_end << "; ++t) {\n";
   } else {
@@ -448,7 +531,18 @@ bool emit_rmarch(Ctx& C, JitProgram& out, std::ostream& src) {
   for (cu = 0; cu < U; ++cu) {
   if (U > 1) src << "  { const int t = t0 + " << cu << ";  // copy " << cu << "\n  if (t > " << trip_end << ") break;\n";
   src << "    const unsigned stg = lf_g % " << NS << ", par = (lf_g / " << NS << ") & 1;\n";
-  // ---- producer: one TMA row box set per streamed axiom per trip
+    producer();
+    for (size_t gi = 0; gi < G.size(); ++gi)
+      if (!group(gi)) return false;
+    copy_tail();
+  }
+  src << "  }\n";  // trips
+  src << "  }\n";  // units
+  src << "}\n";
+  return true;
+}
+
+void RMarch::producer() {
   src << "    if (producer) {\n";
   src << "      if (lf_g >= " << NS << ") lf_mbar_wait(&lf_empty[stg], par ^ 1);\n";
   src << "      unsigned bytes = 0;\n";
@@ -486,244 +580,255 @@ bool emit_rmarch(Ctx& C, JitProgram& out, std::ostream& src) {
   src << "    lf_mbar_wait(&lf_full[stg], par);\n";
   src << "    if (wact) {\n";
 
-  // ---- consumers: the groups in dataflow order
-  for (size_t gi = 0; gi < G.size(); ++gi) {
-    const Grp& g = G[gi];
-    const auto& k = C.P.rs.kernels[g.kernel];
-    src << "    { // group " << gi << ": kernel '" << k.name << "', lead " << g.shift << ", exact on lane-span cells ["
-        << A[gi] << ", " << 32 * V - B[gi] << ")\n";
-    src << "      const int y = t" << plus(g.shift) << ";\n";
-    src << "      if (y >= r0" << plus(g.gmin[0]) << " && y <= r1 - 1" << plus(g.gmax[0]) << ") {\n";
-    // vectors of the streamed rows this group reads
-    std::map<std::pair<int, int>, std::string> vec;  // (var, row offset) -> register array
-    auto vector_of = [&](int var, int r) {
-      auto key = std::make_pair(var, r);
-      auto it = vec.find(key);
-      if (it != vec.end()) return it->second;
-      const std::string nm = "S" + std::to_string(var) + "_" + num(r);
-      src << "        T " << nm << "[" << V << "];\n";
-      src << "        { const T* p = v" << var << " + " << rowbase(static_cast<size_t>(var), g.shift + r) << " + wl"
-          << plus(base_al[var]) << ";\n";
-      for (int c = 0; c < V / CH; ++c) {
-        src << "          const " << VT << " c" << c << " = *reinterpret_cast<const " << VT << "*>(p + " << c * CH << ");";
-        for (int e = 0; e < CH; ++e) src << " " << nm << "[" << c * CH + e << "] = c" << c << "." << comp[e] << ";";
-        src << "\n";
-      }
-      src << "        }\n";
-      vec[key] = nm;
-      return nm;
-    };
-    // value of variable `var` at (row r, column i + dr) of this lane: own
-    // registers, or a shuffle from the lane that holds it
-    std::map<std::tuple<int, int, int>, std::string> elems;
-    auto elem = [&](int var, int r, int dr, int i) -> std::string {
-      long e;
-      std::string arr;
-      if (staged[var] >= 0) {
-        arr = vector_of(var, r);
-        e = rho[var] + i + dr;
-      } else if (C.smem_var[var]) {
-        const int slot = std::max(0, g.shift + r - old[var] - drop[var]);
-        arr = "R" + std::to_string(var) + "[" + std::to_string(phys(var, slot)) + "]";
-        e = i + dr;
-      } else {
-        const int ti = C.terminal_of(var, false);
-        if (C.P.terminals[ti].dims.empty()) return "s" + std::to_string(ti);
-        std::vector<std::string> pos = {"y" + plus(r), "(ow + " + std::to_string(cs) + " + lane * " + std::to_string(V) +
-                                                           plus(i + dr) + ")"};
-        return "__ldg(t" + std::to_string(ti) + " + " + C.tidx(ti, pos, C.extra_of(var)) + ")";
-      }
-      const long q = floordiv(e, V), m = e - q * V;
-      const std::string own = arr + "[" + std::to_string(m) + "]";
-      if (q == 0) return own;
-      auto key = std::make_tuple(var, r, static_cast<int>(e));
-      auto it = elems.find(key);
-      if (it != elems.end()) return it->second;
-      const std::string nm = "X" + std::to_string(var) + "_" + num(r) + "_" + num(e);
-      src << "        const T " << nm << " = "
-          << (q > 0 ? "__shfl_down_sync(0xffffffffu, " + own + ", " + std::to_string(q) + ")"
-                    : "__shfl_up_sync(0xffffffffu, " + own + ", " + std::to_string(-q) + ")")
-          << ";\n";
-      elems[key] = nm;
-      return nm;
-    };
-    // every operand first (vector loads and shuffles are warp-wide), then the cells
-    std::vector<std::vector<std::string>> opnd(V, std::vector<std::string>(g.loads.size()));
-    for (int i = 0; i < V; ++i)
-      for (size_t li = 0; li < g.loads.size(); ++li)
-        opnd[i][li] = elem(g.loads[li].var, g.loads[li].rel[0], g.loads[li].rel[1], i);
-    auto load_index = [&](int var, const std::vector<int>& rel) {
-      for (size_t li = 0; li < g.loads.size(); ++li)
-        if (g.loads[li].var == var && g.loads[li].rel == rel) return static_cast<int>(li);
-      return -1;
-    };
-    std::vector<std::pair<int, const GOut*>> goals;  // (terminal, output)
-    for (const auto& o : g.out) {
-      const int ti = C.terminal_of(o.var, true);
-      if (ti >= 0) {
-        goals.emplace_back(ti, &o);
-        src << "        T G" << gi << "_" << o.param << "[" << V << "];\n";
-      }
+}
+
+// one callsite group of the consumer warps
+bool RMarch::group(size_t gi) {
+  const Grp& g = G[gi];
+  const auto& k = C.P.rs.kernels[g.kernel];
+  src << "    { // group " << gi << ": kernel '" << k.name << "', lead " << g.shift << ", exact on lane-span cells ["
+      << A[gi] << ", " << 32 * V - B[gi] << ")\n";
+  src << "      const int y = t" << plus(g.shift) << ";\n";
+  src << "      if (y >= r0" << plus(g.gmin[0]) << " && y <= r1 - 1" << plus(g.gmax[0]) << ") {\n";
+  // vectors of the streamed rows this group reads
+  std::map<std::pair<int, int>, std::string> vec;  // (var, row offset) -> register array
+  auto vector_of = [&](int var, int r) {
+    auto key = std::make_pair(var, r);
+    auto it = vec.find(key);
+    if (it != vec.end()) return it->second;
+    const std::string nm = "S" + std::to_string(var) + "_" + num(r);
+    src << "        T " << nm << "[" << V << "];\n";
+    src << "        { const T* p = v" << var << " + " << rowbase(static_cast<size_t>(var), g.shift + r) << " + wl"
+        << plus(base_al[var]) << ";\n";
+    for (int c = 0; c < V / CH; ++c) {
+      src << "          const " << VT << " c" << c << " = *reinterpret_cast<const " << VT << "*>(p + " << c * CH << ");";
+      for (int e = 0; e < CH; ++e) src << " " << nm << "[" << c * CH + e << "] = c" << c << "." << comp[e] << ";";
+      src << "\n";
     }
-    // fp32, opt-in (LF_JIT_RM_PACK=1): cells in pairs on the packed fp32x2
-    // pipe when every output (and every inlined producer) has a body.  Exact,
-    // but measured slower on the box chain (430 vs 484 G: forming the register
-    // pairs costs moves), so scalar cells by default
-    bool packed = C.T == "float" && V % 2 == 0 && lfx::option("LF_JIT_RM_PACK") && std::atoi(lfx::option("LF_JIT_RM_PACK")) != 0;
-    for (const auto& [op, pat] : k.outputs) packed &= k.bodies.count(op) > 0;
-    std::set<std::string> kin;
-    for (const auto& [ip, pat] : k.inputs) kin.insert(ip);
-    std::vector<std::pair<std::string, std::unique_ptr<lf::Expr>>> bodies;
-    for (const auto& [op, pat] : k.outputs) {
-      if (!packed) break;
-      std::string e2;
-      auto e = lf::parse_expr(k.bodies.at(op), e2);
-      std::set<std::string> used;
-      if (e) lf::expr_vars(*e, used);
-      for (const auto& u : used) packed &= kin.count(u) > 0;
-      if (!e) packed = false;
-      else bodies.emplace_back(op, std::move(e));
+    src << "        }\n";
+    vec[key] = nm;
+    return nm;
+  };
+  // value of variable `var` at (row r, column i + dr) of this lane: own
+  // registers, or a shuffle from the lane that holds it
+  std::map<std::tuple<int, int, int>, std::string> elems;
+  auto elem = [&](int var, int r, int dr, int i) -> std::string {
+    long e;
+    std::string arr;
+    if (staged[var] >= 0) {
+      arr = vector_of(var, r);
+      e = rho[var] + i + dr;
+    } else if (C.smem_var[var]) {
+      const int slot = std::max(0, g.shift + r - old[var] - drop[var]);
+      arr = "R" + std::to_string(var) + "[" + std::to_string(phys(var, slot)) + "]";
+      e = i + dr;
+    } else {
+      const int ti = C.terminal_of(var, false);
+      if (C.P.terminals[ti].dims.empty()) return "s" + std::to_string(ti);
+      std::vector<std::string> pos = {"y" + plus(r), "(ow + " + std::to_string(cs) + " + lane * " + std::to_string(V) +
+                                                         plus(i + dr) + ")"};
+      return "__ldg(t" + std::to_string(ti) + " + " + C.tidx(ti, pos, C.extra_of(var)) + ")";
     }
-    for (const auto& in : g.in)
-      if (in.via >= 0)
-        for (const auto& o : C.inlined[in.via].out)
-          if (o.var == in.var) packed &= C.P.rs.kernels[C.inlined[in.via].kernel].bodies.count(o.param) > 0;
-    for (int j = 0; packed && j < V; j += 2) {
-      src << "        { // cells " << j << ", " << j + 1 << " (fp32x2)\n";
-      auto pair = [&](int li) { return "make_float2(" + opnd[j][li] + ", " + opnd[j + 1][li] + ")"; };
-      for (const auto& in : g.in) {
-        if (in.via < 0) {
-          src << "          const float2 p_" << in.param << " = " << pair(load_index(in.var, in.rel)) << ";\n";
-          continue;
-        }
-        const Grp& pg = C.inlined[in.via];
-        const auto& pk = C.P.rs.kernels[pg.kernel];
-        std::string oparam;
-        std::vector<int> orel(2, 0);
-        for (const auto& o : pg.out)
-          if (o.var == in.var) {
-            oparam = o.param;
-            orel = o.rel;
-          }
-        std::map<std::string, std::string> pv;
-        for (const auto& pin : pg.in) {
-          std::vector<int> r(2);
-          for (int d = 0; d < 2; ++d) r[d] = in.rel[d] - orel[d] + pin.rel[d];
-          pv[pin.param] = pair(load_index(pin.var, r));
-        }
-        std::string e2;
-        auto e = lf::parse_expr(pk.bodies.at(oparam), e2);
-        if (!e) return (C.error = "kernel '" + pk.name + "': " + e2, false);
-        src << "          const float2 p_" << in.param << " = "
-            << lf::emit_c2(*e, [&](const std::string& n) { return pv.at(n); }) << ";  // inlined '" << pk.name << "'\n";
-      }
-      for (const auto& [op, e] : bodies)
-        src << "          const float2 q_" << op << " = " << lf::emit_c2(*e, [](const std::string& n) { return "p_" + n; })
-            << ";\n";
-      for (const auto& o : g.out) {
-        for (int h = 0; h < 2; ++h) {
-          const char* lane_c = h ? ".y" : ".x";
-          if (C.smem_var[o.var])
-            src << "          R" << o.var << "[" << phys(o.var, std::max(0, g.shift + o.rel[0] - old[o.var] - drop[o.var])) << "]["
-                << j + h << "] = q_" << o.param << lane_c << ";\n";
-          if (C.terminal_of(o.var, true) >= 0)
-            src << "          G" << gi << "_" << o.param << "[" << j + h << "] = q_" << o.param << lane_c << ";\n";
-        }
-      }
-      src << "        }\n";
+    const long q = floordiv(e, V), m = e - q * V;
+    const std::string own = arr + "[" + std::to_string(m) + "]";
+    if (q == 0) return own;
+    auto key = std::make_tuple(var, r, static_cast<int>(e));
+    auto it = elems.find(key);
+    if (it != elems.end()) return it->second;
+    const std::string nm = "X" + std::to_string(var) + "_" + num(r) + "_" + num(e);
+    src << "        const T " << nm << " = "
+        << (q > 0 ? "__shfl_down_sync(0xffffffffu, " + own + ", " + std::to_string(q) + ")"
+                  : "__shfl_up_sync(0xffffffffu, " + own + ", " + std::to_string(-q) + ")")
+        << ";\n";
+    elems[key] = nm;
+    return nm;
+  };
+  // every operand first (vector loads and shuffles are warp-wide), then the cells
+  std::vector<std::vector<std::string>> opnd(V, std::vector<std::string>(g.loads.size()));
+  for (int i = 0; i < V; ++i)
+    for (size_t li = 0; li < g.loads.size(); ++li)
+      opnd[i][li] = elem(g.loads[li].var, g.loads[li].rel[0], g.loads[li].rel[1], i);
+  auto load_index = [&](int var, const std::vector<int>& rel) {
+    for (size_t li = 0; li < g.loads.size(); ++li)
+      if (g.loads[li].var == var && g.loads[li].rel == rel) return static_cast<int>(li);
+    return -1;
+  };
+  std::vector<std::pair<int, const GOut*>> goals;  // (terminal, output)
+  for (const auto& o : g.out) {
+    const int ti = C.terminal_of(o.var, true);
+    if (ti >= 0) {
+      goals.emplace_back(ti, &o);
+      src << "        T G" << gi << "_" << o.param << "[" << V << "];\n";
     }
-    for (int i = 0; i < V && !packed; ++i) {
-      src << "        { // cell " << i << "\n";
-      for (const auto& in : g.in) {
-        if (in.via < 0) {
-          src << "          const T p_" << in.param << " = " << opnd[i][load_index(in.var, in.rel)] << ";\n";
-          continue;
-        }
-        const Grp& pg = C.inlined[in.via];
-        const auto& pk = C.P.rs.kernels[pg.kernel];
-        std::string oparam;
-        std::vector<int> orel(2, 0);
-        for (const auto& o : pg.out)
-          if (o.var == in.var) {
-            oparam = o.param;
-            orel = o.rel;
-          }
-        std::map<std::string, std::string> pv;
-        for (const auto& pin : pg.in) {
-          std::vector<int> r(2);
-          for (int d = 0; d < 2; ++d) r[d] = in.rel[d] - orel[d] + pin.rel[d];
-          pv[pin.param] = opnd[i][load_index(pin.var, r)];
-        }
-        std::string e2;
-        auto e = lf::parse_expr(pk.bodies.at(oparam), e2);
-        if (!e) return (C.error = "kernel '" + pk.name + "': " + e2, false);
-        src << "          const T p_" << in.param << " = "
-            << lf::emit_c(*e, C.T, [&](const std::string& n) { return pv.at(n); }) << ";  // inlined '" << pk.name
-            << "'\n";
-      }
-      if (!emit_bodies(C, g, src, "          ")) return false;
-      for (const auto& o : g.out) {
-        if (C.smem_var[o.var])
-          src << "          R" << o.var << "[" << phys(o.var, std::max(0, g.shift + o.rel[0] - old[o.var] - drop[o.var])) << "][" << i
-              << "] = q_" << o.param << ";\n";
-        if (C.terminal_of(o.var, true) >= 0) src << "          G" << gi << "_" << o.param << "[" << i << "] = q_" << o.param << ";\n";
-      }
-      src << "        }\n";
-    }
-    // goal rows: own chunk rows, own strip cells, inside the domain
-    for (const auto& [ti, o] : goals) {
-      const auto& t = C.P.terminals[ti];
-      const long so = goal_so(ti);
-      const bool vec_ok = ((cs + so) % CH + CH) % CH == 0 && t.extent[1] % CH == 0;
-      src << "        { const int yy = y" << plus(o->rel[0]) << ";\n";
-      src << "          const int c = " << cs << " + lane * " << V << ", x = ow + c;\n";
-      src << "          if (yy >= r0 && yy < r1) {\n";
-      src << "            T* gp = t" << ti << " + " << C.tidx(ti, {"yy", "x"}, std::vector<int>(2, 0)) << ";\n";
-      const std::string gv = "G" + std::to_string(gi) + "_" + o->param;
-      const IP* ip = ip_of_goal(ti);
-      if (ip) {
-        // in place: deferred boundary writes (row zone: the whole row into the
-        // row band; column zone: those cells into the column band)
-        const int v = static_cast<int>(ip->v);
-        const int lo0 = C.vmin[v][0], hi0 = C.vmax[v][0], lo1 = C.vmin[v][1], hi1 = C.vmax[v][1];
-        const size_t q = static_cast<size_t>(ip - ips.data());
-        src << "            if (a.inplace) {\n";
-        src << "              int br = -1;  // row of the row band (band k - 1 at chunk boundary k)\n";
-        src << "              if (r0 > 0 && yy < r0" << plus(hi0) << ") br = (ci - 1) * " << hi0 - lo0 << " + (yy - r0" << plus(-lo0) << ");\n";
-        src << "              else if (r1 < N0 && yy >= r1" << plus(lo0) << ") br = ci * " << hi0 - lo0 << " + (yy - r1" << plus(-lo0)
-            << ");\n";
-        src << "              if (br >= 0) gp = reinterpret_cast<T*>(a.t[" << ip->slot << "]) + (long long)br * " << t.extent[1]
-            << "LL + (x" << plus(so) << ");\n";
-        src << "              if (br < 0 && zm" << q << ") {  // cells in a column band\n";
-        src << "                T* cb = reinterpret_cast<T*>(a.t[" << ip->slot + 1 << "]) + yy;\n";
-        src << "                #pragma unroll\n";
-        src << "                for (int i = 0; i < " << V << "; ++i) {\n";
-        src << "                  if ((zm" << q << " >> i) & 1) cb[zb" << q << "[i]] = " << gv << "[i];\n";
-        src << "                  else if (c + i >= 0 && c + i < " << tw << " && x + i < " << C.N[1] << ") gp[i] = " << gv << "[i];\n";
-        src << "                }\n";
-        src << "                gp = nullptr;\n";
-        src << "              }\n";
-        src << "            }\n";
-        src << "            if (gp)\n";
-      }
-      if (vec_ok) {
-        src << "            if (c >= 0 && c + " << V << " <= " << tw << " && x + " << V << " <= " << C.N[1] << ") {\n";
-        for (int c = 0; c < V / CH; ++c) {
-          src << "              " << VT << " w" << c << ";";
-          for (int e = 0; e < CH; ++e) src << " w" << c << "." << comp[e] << " = " << gv << "[" << c * CH + e << "];";
-          src << " *reinterpret_cast<" << VT << "*>(gp + " << c * CH << ") = w" << c << ";\n";
-        }
-        src << "            } else {\n";
-      } else {
-        src << "            {\n";
-      }
-      src << "              #pragma unroll\n";
-      src << "              for (int i = 0; i < " << V << "; ++i)\n";
-      src << "                if (c + i >= 0 && c + i < " << tw << " && x + i < " << C.N[1] << ") gp[i] = " << gv << "[i];\n";
-      src << "            }\n          }\n        }\n";
-    }
-    src << "      }\n    }\n";
   }
+  // fp32, opt-in (LF_JIT_RM_PACK=1): cells in pairs on the packed fp32x2
+  // pipe when every output (and every inlined producer) has a body.  Exact,
+  // but measured slower on the box chain (430 vs 484 G: forming the register
+  // pairs costs moves), so scalar cells by default
+  bool packed = C.T == "float" && V % 2 == 0 && lfx::option("LF_JIT_RM_PACK") && std::atoi(lfx::option("LF_JIT_RM_PACK")) != 0;
+  for (const auto& [op, pat] : k.outputs) packed &= k.bodies.count(op) > 0;
+  std::set<std::string> kin;
+  for (const auto& [ip, pat] : k.inputs) kin.insert(ip);
+  std::vector<std::pair<std::string, std::unique_ptr<lf::Expr>>> bodies;
+  for (const auto& [op, pat] : k.outputs) {
+    if (!packed) break;
+    std::string e2;
+    auto e = lf::parse_expr(k.bodies.at(op), e2);
+    std::set<std::string> used;
+    if (e) lf::expr_vars(*e, used);
+    for (const auto& u : used) packed &= kin.count(u) > 0;
+    if (!e) packed = false;
+    else bodies.emplace_back(op, std::move(e));
+  }
+  for (const auto& in : g.in)
+    if (in.via >= 0)
+      for (const auto& o : C.inlined[in.via].out)
+        if (o.var == in.var) packed &= C.P.rs.kernels[C.inlined[in.via].kernel].bodies.count(o.param) > 0;
+  for (int j = 0; packed && j < V; j += 2) {
+    src << "        { // cells " << j << ", " << j + 1 << " (fp32x2)\n";
+    auto pair = [&](int li) { return "make_float2(" + opnd[j][li] + ", " + opnd[j + 1][li] + ")"; };
+    for (const auto& in : g.in) {
+      if (in.via < 0) {
+        src << "          const float2 p_" << in.param << " = " << pair(load_index(in.var, in.rel)) << ";\n";
+        continue;
+      }
+      const Grp& pg = C.inlined[in.via];
+      const auto& pk = C.P.rs.kernels[pg.kernel];
+      std::string oparam;
+      std::vector<int> orel(2, 0);
+      for (const auto& o : pg.out)
+        if (o.var == in.var) {
+          oparam = o.param;
+          orel = o.rel;
+        }
+      std::map<std::string, std::string> pv;
+      for (const auto& pin : pg.in) {
+        std::vector<int> r(2);
+        for (int d = 0; d < 2; ++d) r[d] = in.rel[d] - orel[d] + pin.rel[d];
+        pv[pin.param] = pair(load_index(pin.var, r));
+      }
+      std::string e2;
+      auto e = lf::parse_expr(pk.bodies.at(oparam), e2);
+      if (!e) return (C.error = "kernel '" + pk.name + "': " + e2, false);
+      src << "          const float2 p_" << in.param << " = "
+          << lf::emit_c2(*e, [&](const std::string& n) { return pv.at(n); }) << ";  // inlined '" << pk.name << "'\n";
+    }
+    for (const auto& [op, e] : bodies)
+      src << "          const float2 q_" << op << " = " << lf::emit_c2(*e, [](const std::string& n) { return "p_" + n; })
+          << ";\n";
+    for (const auto& o : g.out) {
+      for (int h = 0; h < 2; ++h) {
+        const char* lane_c = h ? ".y" : ".x";
+        if (C.smem_var[o.var])
+          src << "          R" << o.var << "[" << phys(o.var, std::max(0, g.shift + o.rel[0] - old[o.var] - drop[o.var])) << "]["
+              << j + h << "] = q_" << o.param << lane_c << ";\n";
+        if (C.terminal_of(o.var, true) >= 0)
+          src << "          G" << gi << "_" << o.param << "[" << j + h << "] = q_" << o.param << lane_c << ";\n";
+      }
+    }
+    src << "        }\n";
+  }
+  for (int i = 0; i < V && !packed; ++i) {
+    src << "        { // cell " << i << "\n";
+    for (const auto& in : g.in) {
+      if (in.via < 0) {
+        src << "          const T p_" << in.param << " = " << opnd[i][load_index(in.var, in.rel)] << ";\n";
+        continue;
+      }
+      const Grp& pg = C.inlined[in.via];
+      const auto& pk = C.P.rs.kernels[pg.kernel];
+      std::string oparam;
+      std::vector<int> orel(2, 0);
+      for (const auto& o : pg.out)
+        if (o.var == in.var) {
+          oparam = o.param;
+          orel = o.rel;
+        }
+      std::map<std::string, std::string> pv;
+      for (const auto& pin : pg.in) {
+        std::vector<int> r(2);
+        for (int d = 0; d < 2; ++d) r[d] = in.rel[d] - orel[d] + pin.rel[d];
+        pv[pin.param] = opnd[i][load_index(pin.var, r)];
+      }
+      std::string e2;
+      auto e = lf::parse_expr(pk.bodies.at(oparam), e2);
+      if (!e) return (C.error = "kernel '" + pk.name + "': " + e2, false);
+      src << "          const T p_" << in.param << " = "
+          << lf::emit_c(*e, C.T, [&](const std::string& n) { return pv.at(n); }) << ";  // inlined '" << pk.name
+          << "'\n";
+    }
+    if (!emit_bodies(C, g, src, "          ")) return false;
+    for (const auto& o : g.out) {
+      if (C.smem_var[o.var])
+        src << "          R" << o.var << "[" << phys(o.var, std::max(0, g.shift + o.rel[0] - old[o.var] - drop[o.var])) << "][" << i
+            << "] = q_" << o.param << ";\n";
+      if (C.terminal_of(o.var, true) >= 0) src << "          G" << gi << "_" << o.param << "[" << i << "] = q_" << o.param << ";\n";
+    }
+    src << "        }\n";
+  }
+  store_goals(gi, goals);
+  src << "      }\n    }\n";
+  return true;
+}
+
+// goal rows of group gi: own chunk rows, own strip cells, inside the domain;
+// in place, the deferred boundary cells to their bands
+void RMarch::store_goals(size_t gi, const std::vector<std::pair<int, const GOut*>>& goals) {
+  for (const auto& [ti, o] : goals) {
+    const auto& t = C.P.terminals[ti];
+    const long so = goal_so(ti);
+    const bool vec_ok = ((cs + so) % CH + CH) % CH == 0 && t.extent[1] % CH == 0;
+    src << "        { const int yy = y" << plus(o->rel[0]) << ";\n";
+    src << "          const int c = " << cs << " + lane * " << V << ", x = ow + c;\n";
+    src << "          if (yy >= r0 && yy < r1) {\n";
+    src << "            T* gp = t" << ti << " + " << C.tidx(ti, {"yy", "x"}, std::vector<int>(2, 0)) << ";\n";
+    const std::string gv = "G" + std::to_string(gi) + "_" + o->param;
+    const IP* ip = ip_of_goal(ti);
+    if (ip) {
+      // in place: deferred boundary writes (row zone: the whole row into the
+      // row band; column zone: those cells into the column band)
+      const int v = static_cast<int>(ip->v);
+      const int lo0 = C.vmin[v][0], hi0 = C.vmax[v][0], lo1 = C.vmin[v][1], hi1 = C.vmax[v][1];
+      const size_t q = static_cast<size_t>(ip - ips.data());
+      src << "            if (a.inplace) {\n";
+      src << "              int br = -1;  // row of the row band (band k - 1 at chunk boundary k)\n";
+      src << "              if (r0 > 0 && yy < r0" << plus(hi0) << ") br = (ci - 1) * " << hi0 - lo0 << " + (yy - r0" << plus(-lo0) << ");\n";
+      src << "              else if (r1 < N0 && yy >= r1" << plus(lo0) << ") br = ci * " << hi0 - lo0 << " + (yy - r1" << plus(-lo0)
+          << ");\n";
+      src << "              if (br >= 0) gp = reinterpret_cast<T*>(a.t[" << ip->slot << "]) + (long long)br * " << t.extent[1]
+          << "LL + (x" << plus(so) << ");\n";
+      src << "              if (br < 0 && zm" << q << ") {  // cells in a column band\n";
+      src << "                T* cb = reinterpret_cast<T*>(a.t[" << ip->slot + 1 << "]) + yy;\n";
+      src << "                #pragma unroll\n";
+      src << "                for (int i = 0; i < " << V << "; ++i) {\n";
+      src << "                  if ((zm" << q << " >> i) & 1) cb[zb" << q << "[i]] = " << gv << "[i];\n";
+      src << "                  else if (c + i >= 0 && c + i < " << tw << " && x + i < " << C.N[1] << ") gp[i] = " << gv << "[i];\n";
+      src << "                }\n";
+      src << "                gp = nullptr;\n";
+      src << "              }\n";
+      src << "            }\n";
+      src << "            if (gp)\n";
+    }
+    if (vec_ok) {
+      src << "            if (c >= 0 && c + " << V << " <= " << tw << " && x + " << V << " <= " << C.N[1] << ") {\n";
+      for (int c = 0; c < V / CH; ++c) {
+        src << "              " << VT << " w" << c << ";";
+        for (int e = 0; e < CH; ++e) src << " w" << c << "." << comp[e] << " = " << gv << "[" << c * CH + e << "];";
+        src << " *reinterpret_cast<" << VT << "*>(gp + " << c * CH << ") = w" << c << ";\n";
+      }
+      src << "            } else {\n";
+    } else {
+      src << "            {\n";
+    }
+    src << "              #pragma unroll\n";
+    src << "              for (int i = 0; i < " << V << "; ++i)\n";
+    src << "                if (c + i >= 0 && c + i < " << tw << " && x + i < " << C.N[1] << ") gp[i] = " << gv << "[i];\n";
+    src << "            }\n          }\n        }\n";
+  }
+
+}
+
+void RMarch::copy_tail() {
   src << "    }\n";  // wact
   src << "    __syncwarp();\n";
   src << "    if (lane == 0) lf_mbar_arrive(&lf_empty[stg]);\n";
@@ -737,10 +842,9 @@ bool emit_rmarch(Ctx& C, JitProgram& out, std::ostream& src) {
     if (staged[v] >= 0 && win[v] > 1) src << "    b" << v << " = b" << v << " == " << (win[v] - 1) << " ? 0 : b" << v << " + 1;\n";
   src << "    ++lf_g;\n";
   if (U > 1) src << "  }\n";  // copy
-  }
-  src << "  }\n";  // trips
-  src << "  }\n";  // units
-  src << "}\n";
+}
+
+void RMarch::commit() {
   if (!ips.empty()) {
     std::vector<std::pair<size_t, int>> caps;
     std::vector<int> slots;
@@ -750,7 +854,11 @@ bool emit_rmarch(Ctx& C, JitProgram& out, std::ostream& src) {
     }
     emit_commit2(C, "lf_jit_commit_rm", caps, slots, static_cast<int>(T1), src);
   }
-  return true;
+}
+
+bool emit_rmarch(Ctx& C, JitProgram& out, std::ostream& src) {
+  RMarch m(C, out, src);
+  return m.emit();
 }
 
 }  // namespace lfx::cg
