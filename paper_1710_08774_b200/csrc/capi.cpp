@@ -770,8 +770,63 @@ static int run_host_pipelined(lf_plan* plan, void* const* terms, const std::vect
                 (e - a) * rb, cudaMemcpyDeviceToHost, plan->d2h);
     }
   };
+  // a multi-step run of a chain whose outer dimension does not wrap runs as a
+  // wavefront over (step, part): part p of step s needs step s-1's parts p-1..p+1
+  // (its input rows and halo) and overwrites the buffer step s-1 read its own
+  // parts p-1..p+1 from (ping-pong), so in stream order tau = p + 2s every
+  // dependence comes first.  Then every step trails the input rows up and the
+  // last one sends each part down as it finishes: PCIe in both directions
+  // overlaps the whole run, not only its first and last step.
+  bool periodic0 = false;
+  for (const auto& [gname, mode] : plan->plan.rs.boundary)
+    if (!mode.empty() && mode[0] == lf::Boundary::periodic) periodic0 = true;
+  long halo0 = 0;
+  for (const auto& t : T)
+    if (chunked(t)) halo0 = std::max({halo0, lo0 - t.base[0], t.extent[0] - n0 - (lo0 - t.base[0])});
+  // worth it for parts of many cells only: a part launch costs ~25 us of host
+  // time (tensor maps, launch), so small parts starve the GPU (Hydro2D 4096^2
+  // x20: 54 ms per run whole-domain, 57 / 70 ms as a wavefront of 16 / 32
+  // parts; 32768^2 x10: 2188 -> 1374 ms); LF_HOST_WAVEFRONT=1 / 0 forces it
+  long part_cells = n0 / parts;
+  for (size_t d = 1; d < plan->plan.rs.ranges.size(); ++d) part_cells *= plan->plan.rs.ranges[d].trips();
+  bool wavefront = part_cells >= (16L << 20);
+  if (const char* e = lfx::option("LF_HOST_WAVEFRONT")) wavefront = std::atoi(e) != 0;
+  wavefront = wavefront && steps > 1 && !periodic0 && n0 / parts >= std::max(1L, halo0);
+  if (wavefront) {
+    std::vector<std::vector<void*>> B(steps);
+    for (int s = 0; s < steps; ++s) {
+      B[s] = step_bufs(s);
+      advance(B[s]);
+    }
+    std::vector<long> copied(T.size(), 0);
+    for (int tau = 0; tau <= parts - 1 + 2 * (steps - 1) && st == LF_OK; ++tau)
+      for (int s = 0; s < steps && st == LF_OK; ++s) {
+        const int p = tau - 2 * s;
+        if (p < 0 || p >= parts) continue;
+        const auto [a, e] = part_rows(p);
+        if (s == 0) {  // this part's input rows (and the halo above them)
+          for (size_t i = 0; i < T.size() && st == LF_OK; ++i) {
+            if (T[i].is_goal || !chunked(T[i])) continue;
+            const long e0 = T[i].extent[0], below = lo0 - T[i].base[0], above = e0 - n0 - below;
+            const long need = p == parts - 1 ? e0 : std::min(e0, e + below + above);
+            if (need > copied[i]) {
+              const int64_t rb = row_bytes(T[i]);
+              st = copy(static_cast<char*>(dterms[i]) + copied[i] * rb,
+                        static_cast<const char*>(terms[i]) + copied[i] * rb, (need - copied[i]) * rb,
+                        cudaMemcpyHostToDevice, plan->h2d);
+              copied[i] = need;
+            }
+          }
+          if (st != LF_OK) break;
+          cudaEventRecord(up[p], plan->h2d);
+          cudaStreamWaitEvent(plan->stream, up[p], 0);
+        }
+        if ((st = run_part(B[s], a, e, false)) != LF_OK) break;
+        if (s == steps - 1) send_down(B[s], p);
+      }
+  }
   // ---- first step: parts as their rows arrive
-  {
+  if (!wavefront) {
     std::vector<void*> b = step_bufs(0);
     std::vector<long> copied(T.size(), 0);  // storage rows already sent, per axiom
     for (int p = 0; p < parts && st == LF_OK; ++p) {
@@ -797,13 +852,13 @@ static int run_host_pipelined(lf_plan* plan, void* const* terms, const std::vect
     advance(b);
   }
   // ---- the steps in between: whole-domain launches
-  for (int s = 1; s < steps - 1 && st == LF_OK; ++s) {
+  for (int s = 1; s < steps - 1 && st == LF_OK && !wavefront; ++s) {
     std::vector<void*> b = step_bufs(s);
     st = run_part(b, 0, n0, true);
     advance(b);
   }
   // ---- last step: parts, each sent down as soon as it is done
-  if (steps > 1 && st == LF_OK) {
+  if (steps > 1 && st == LF_OK && !wavefront) {
     std::vector<void*> b = step_bufs(steps - 1);
     for (int p = 0; p < parts && st == LF_OK; ++p) {
       const auto [a, e] = part_rows(p);

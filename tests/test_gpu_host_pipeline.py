@@ -1,6 +1,7 @@
 """lf_run_host, pipelined (row parts: the first step computes part p while
 part p+1 comes up, the last step sends part p down while part p+1 is computed;
-one step overlaps both directions) -- bit-exact against the oracles, ghost rows
+one step overlaps both directions; multi-step runs of non-periodic chains as a
+wavefront over (step, part)) -- bit-exact against the oracles, ghost rows
 included, for single steps and for multi-step runs (2, 3 and 4 steps: the
 ping-pong through the plan's scratch ends in the goals either way)."""
 import numpy as np
@@ -111,3 +112,34 @@ def test_multistep_generic_executor(parts):
     out = np.full_like(u, np.nan)
     plan.run_host([u, out], steps=3)
     assert np.array_equal(bits(out), bits(oracle.biharm(u, 3)))
+
+
+@pytest.mark.parametrize("wave", ["1", "0"])
+def test_wavefront_over_steps_and_parts(wave, monkeypatch):
+    """Multi-step runs of chains whose outer dimension does not wrap run as a
+    wavefront over (step, part) -- part p of step s right after part p+1 of
+    step s-1 -- with parts barely wider than the halo (the dependence reaches
+    exactly the neighbouring parts) and many steps, so every ping-pong buffer
+    is rewritten while neighbouring parts of the step before still read it.
+    LF_HOST_WAVEFRONT=0: the first / last step pipelined only."""
+    monkeypatch.setenv("LF_HOST_WAVEFRONT", wave)
+    monkeypatch.setenv("LF_HOST_PARTS", "10")
+    plan = lf.Plan.with_ranges("biharmonic2d", (30, 256))
+    u = inputs.biharm_input(30, 256, seed=21)
+    out = np.full_like(u, np.nan)
+    plan.run_host([u, out], steps=9)
+    assert np.array_equal(bits(out), bits(oracle.biharm(u, 9)))
+    monkeypatch.setenv("LF_HOST_PARTS", "8")
+    plan = lf.Plan.with_ranges("hydro2d", (24, 128))
+    st, dtdx = inputs.hydro_input(24, 128, seed=22)
+    outs = [np.full_like(st[0], np.nan) for _ in range(4)]
+    plan.run_host(st + [np.array([dtdx])] + outs, steps=6)
+    ref = oracle.hydro(st, dtdx, 6)
+    for v in range(4):
+        assert np.array_equal(bits(outs[v]), bits(ref[v])), v
+    spec = lf.set_ranges((SPECS / "biharm_body.lf").read_text(), (40, 100))
+    plan = lf.Plan(spec, "b.lf")
+    u = inputs.biharm_input(40, 100, seed=23)
+    out = np.full_like(u, np.nan)
+    plan.run_host([u, out], steps=5)
+    assert np.array_equal(bits(out), bits(oracle.biharm(u, 5)))
