@@ -156,6 +156,7 @@ struct SlabGeom {
   std::vector<int64_t> elem;       // element bytes per terminal
   long halo_lo = 0, halo_hi = 0;  // max ghost rows below / above over the iterated terminals
   long n0 = 0;
+  int world = 1;                   // ranks of the whole decomposition
 };
 
 SlabGeom slab_geom(const lf::Plan& P) {
@@ -317,7 +318,11 @@ int run_slabs_core(lf_plan* plan, const SlabGeom& g, std::vector<RankState>& R, 
   // hiding behind the interior (tools/slab_probe.py, profiles/r02_slab_schedules.txt)
   long min_rows = g.n0;
   for (const auto& r : R) min_rows = std::min(min_rows, r.hi - r.lo);
-  const int sched = sched_env >= 0 ? sched_env : (min_rows >= 1024 ? 3 : 0);
+  // no rank has a neighbour to exchange with (one rank, no periodic outer
+  // dimension): every step is one launch per rank, nothing else
+  bool peers = R.size() > 1 || g.world > 1;
+  for (size_t i = 0; i < g.paired.size(); ++i) peers |= g.paired[i] >= 0 && g.periodic[i];
+  const int sched = !peers ? 3 : (sched_env >= 0 ? sched_env : (min_rows >= 1024 ? 3 : 0));
   cudaStream_t side2 = side;
   if (sched == 0) {
     if (!plan->comm2 && make_side_stream(&plan->comm2, err) != LF_OK) return LF_ERR_CUDA;
@@ -351,14 +356,10 @@ int run_slabs_core(lf_plan* plan, const SlabGeom& g, std::vector<RankState>& R, 
       cudaStreamWaitEvent(side, mark, 0);
       if (side2 != side) cudaStreamWaitEvent(side2, mark, 0);
     }
-    if (sched == 3) {  // whole: one launch per rank, then the exchange, the next step after it
+    if (sched == 3) {  // whole: one launch per rank, then the exchange on the same stream, the next step after it
       for (size_t k = 0; k < R.size() && st == LF_OK; ++k) st = launch(R[k], 0, R[k].hi - R[k].lo, stream);
       if (st != LF_OK) break;
-      cudaEventRecord(faces_done, stream);
-      cudaStreamWaitEvent(side, faces_done, 0);
-      if ((st = exchange(R, side, err)) != LF_OK) break;
-      cudaEventRecord(exchanged, side);
-      cudaStreamWaitEvent(stream, exchanged, 0);
+      if (peers && (st = exchange(R, stream, err)) != LF_OK) break;
       if (combine)
         for (size_t i : scalars)
           if (st == LF_OK) st = combine(R[0].bufs[i], stream, err);
@@ -1072,6 +1073,7 @@ int lf_run_slabs(const lf_plan* cplan, void* comm, int rank, int world, void* co
     std::lock_guard<std::mutex> lk(plan->mu);
     std::string err;
     SlabGeom g = slab_geom(plan->plan);
+    g.world = world;
     if ((st = slab_check(plan, g, world, err)) != LF_OK) return fail(st, err);
     cudaStream_t stream = static_cast<cudaStream_t>(cuda_stream);
     if (!plan->comm && (st = make_side_stream(&plan->comm, err)) != LF_OK) return fail(st, err);
@@ -1146,6 +1148,7 @@ int lf_run_slabs_local(const lf_plan* cplan, int world, void* const* terms, int 
     std::lock_guard<std::mutex> lk(plan->mu);
     std::string err;
     SlabGeom g = slab_geom(plan->plan);
+    g.world = world;
     int st = slab_check(plan, g, world, err);
     if (st != LF_OK) return fail(st, err);
     cudaStream_t stream = static_cast<cudaStream_t>(cuda_stream);

@@ -377,14 +377,14 @@ int launch_step(const double* in, double* out, int ni, const RowPart& rp, cudaSt
   // evict_last: the output of an iteration is the next one's input and 134 MB
   // of it at 4096^2 nearly fits the 126 MB L2 -- same-box A/B 321 -> 340 G
   // (evict_first) at 4096^2, 289 -> 295 G at 16384^2 (LF_BIHARM_STORE_POLICY)
-  static const int store_policy = [] {
+  const int store_policy = [] {
     const char* e = lfx::option("LF_BIHARM_STORE_POLICY");
     return e ? std::atoi(e) : 2;
   }();
   p.store_policy = store_policy;
   // TMA fetches with an explicit evict_normal hint: same-box A/B 341 -> 346 G
   // at 4096^2, 292 -> 298 G at 16384^2 against plain fetches (evict_first 334 G)
-  static const int load_policy = [] {
+  const int load_policy = [] {
     const char* e = lfx::option("LF_BIHARM_LOAD_POLICY");
     return e ? std::atoi(e) : 1;
   }();

@@ -286,11 +286,11 @@ int run(const ExecArgs& a, std::string& err) {
   // L2 policies (same-box A/B, 16384^2): evict_normal-hinted fetches and
   // stores 654 -> 662 G against plain fetches + evict_first stores; evict_first
   // fetches 608 G
-  static const int load_policy = [] {
+  const int load_policy = [] {
     const char* e = lfx::option("LF_BOX_LOAD_POLICY");
     return e ? std::atoi(e) : 1;
   }();
-  static const int store_policy = [] {
+  const int store_policy = [] {
     const char* e = lfx::option("LF_BOX_STORE_POLICY");
     return e ? std::atoi(e) : 1;
   }();

@@ -71,7 +71,7 @@ bool make_tensor_map(CUtensorMap* map, const void* base, CUtensorMapDataType dty
   }
   // L2 sector promotion of TMA fetches; LF_TMA_PROMOTION=0/64/128/256 overrides
   // the default for tuning runs
-  static const CUtensorMapL2promotion promo = [] {
+  const CUtensorMapL2promotion promo = [] {
     const char* e = lfx::option("LF_TMA_PROMOTION");
     const int v = e ? std::atoi(e) : 256;
     return v == 0 ? CU_TENSOR_MAP_L2_PROMOTION_NONE

@@ -593,7 +593,7 @@ int launch_step(const double* in, double* out, int ni, int nj, int nk, int k_lo,
   p.units = p.tiles * p.kchunks;
   // evict_normal: same-box A/B 348.5 -> 351.2 G against evict_first; evict_last
   // (the 1 GB output cannot stay in L2) 343 G (LF_HEAT3D_STORE_POLICY)
-  static const int store_policy = [] {
+  const int store_policy = [] {
     const char* e = lfx::option("LF_HEAT3D_STORE_POLICY");
     return e ? std::atoi(e) : 1;
   }();
@@ -655,7 +655,7 @@ int launch_pair_k(const double* in, double* out, int ni, int nj, int nk, cudaStr
 
 // LF_HEAT3D_TBK: planes per work unit of the two-step pass (32 / 64 / 128; 64 measured best)
 int launch_pair(const double* in, double* out, int ni, int nj, int nk, cudaStream_t st, std::string& err) {
-  static const int kch = [] {
+  const int kch = [] {
     const char* e = lfx::option("LF_HEAT3D_TBK");
     return e ? std::atoi(e) : 64;
   }();
