@@ -607,6 +607,7 @@ class March {
   bool group(size_t gi, int& level);
   void tail();
   void capture();
+  void commit3();
   void emit_load(size_t v, const std::string& row, const std::string& slotexpr, const char* ind);
   // ws: a staged axiom's innermost row is fetched as nbox TMA boxes of bw
   // elements (box rows <= 256 elements, 128-B multiples so every box lands
@@ -844,9 +845,11 @@ void March::head() {
   if (!ws) {
     out.inplace.clear();
     out.inplace_error.clear();
+  } else {
+    out.ws_inplace.clear();
   }
   const int nterm = static_cast<int>(C.P.terminals.size());
-  for (const auto& [in_ext, out_ext] : ws ? decltype(C.P.rs.aliases){} : C.P.rs.aliases) {
+  for (const auto& [in_ext, out_ext] : C.P.rs.aliases) {
     int ai = -1, gi = -1;
     for (int i = 0; i < nterm; ++i) {
       if (!C.P.terminals[i].is_goal && C.P.terminals[i].name == in_ext) ai = i;
@@ -869,12 +872,14 @@ void March::head() {
     }
     ips.push_back(ip);
     const auto& t = C.P.terminals[ai];
+    const auto& vm = ws ? saved_vmin : C.vmin;  // the ws emission widens streamed windows for TMA alignment
     JitProgram::Inplace q;
     q.ai = ai;
     q.gi = gi;
-    q.bh = C.vmax[v][0] - C.vmin[v][0];
-    q.bw1 = nd > 1 ? C.vmax[v][1] - C.vmin[v][1] : 0;
-    q.bw2 = nd > 2 ? C.vmax[v][2] - C.vmin[v][2] : 0;
+    q.bh = C.vmax[v][0] - vm[v][0];
+    q.bw1 = nd > 1 ? C.vmax[v][1] - vm[v][1] : 0;
+    q.bw2 = nd > 2 ? C.vmax[v][2] - vm[v][2] : 0;
+    if (ws && nd == 3) q.bw2 += 2 * (32 / eb - 1);  // deferred column zones widened to whole 32-B sectors
     q.e0 = t.extent[0];
     q.e1 = nd > 1 ? t.extent[1] : 1;
     q.e2 = nd > 2 ? t.extent[2] : 1;
@@ -882,9 +887,10 @@ void March::head() {
     q.t2 = nd > 2 ? tile[2] : 1;
     q.n1 = nd > 1 ? C.N[1] : 1;
     q.n2 = nd > 2 ? C.N[2] : 1;
-    out.inplace.push_back(q);
+    (ws ? out.ws_inplace : out.inplace).push_back(q);
   }
   for (const auto& ip : ips)
+    if (!ws)
     src << "  const T* __restrict__ rb" << ip.slot << " = reinterpret_cast<const T*>(a.t[" << ip.slot
         << "]);  // in-place bands of '" << C.P.vars[ip.v].name << "'\n"
         << "  const T* __restrict__ cb" << ip.slot << "_1 = reinterpret_cast<const T*>(a.t[" << ip.slot + 1 << "]);\n"
@@ -947,6 +953,7 @@ void March::head() {
   src << "    s += r1_ - r0_;\n";
   src << "  }\n";
   src << "  const int r0 = r0_, r1 = r1_;\n";
+  if (ws && !ips.empty()) src << "  const int ci_ = (r0 - a.row_lo) / a.chunk;  // chunk index (in place: plane bands)\n";
   for (int d = nd - 1; d >= 1; --d) {
     const long nt = (C.N[d] + tile[d] - 1) / tile[d];
     src << "  const int o" << d << " = (bt % " << nt << ") * " << tile[d] << "; bt /= " << nt << ";\n";
@@ -1216,6 +1223,58 @@ bool March::group(size_t gi, int& level) {
           << plus(o.rel[d]) << " < N" << d;
     std::vector<std::string> pos;
     for (int d = 0; d < nd; ++d) pos.push_back((d == 0 ? std::string("y") : "x" + std::to_string(d)) + plus(o.rel[d]));
+    const IP* gip = nullptr;
+    for (const auto& ip : ips)
+      if (ip.gi == ti) gip = &ip;
+    if (ws && nd == 3 && gip) {
+      // in place: deferred boundary writes (plane zone -> plane band, tile-row
+      // zone -> row band, sector-aligned tile-column zone -> column band)
+      const auto& t = C.P.terminals[ti];
+      const size_t v = gip->v;
+      const long so0 = -t.base[0] + C.LO[0], so1 = -t.base[1] + C.LO[1], so2 = -t.base[2] + C.LO[2];
+      const long lo0 = saved_vmin[v][0], hi0 = C.vmax[v][0], lo1 = saved_vmin[v][1], hi1 = C.vmax[v][1];
+      const long lo2 = saved_vmin[v][2], hi2 = C.vmax[v][2], SE = 32 / eb;
+      const long E0 = t.extent[0], E1 = t.extent[1], E2 = t.extent[2];
+      const long BH = hi0 - lo0, BW1 = hi1 - lo1, BW2 = hi2 - lo2 + 2 * (SE - 1);
+      auto zs = [&](const std::string& e) {
+        return "(((" + e + plus(lo2 + so2) + ") & ~" + std::to_string(SE - 1) + ")" + plus(-so2) + ")";
+      };
+      auto ze = [&](const std::string& e) {
+        return "(((" + e + plus(hi2 + so2 + SE - 1) + ") & ~" + std::to_string(SE - 1) + ")" + plus(-so2) + ")";
+      };
+      const std::string yy = "(y" + plus(o.rel[0]) + ")", xx1 = "(x1" + plus(o.rel[1]) + ")", xx2 = "(x2" + plus(o.rel[2]) + ")";
+      src << ") {\n";
+      src << I << "  T* gp = t" << ti << " + " << C.tidx(ti, pos, std::vector<int>(nd, 0)) << ";\n";
+      src << I << "  if (a.inplace) {\n";
+      src << I << "    int br = -1;\n";
+      src << I << "    if (r0 > 0 && " << yy << " < r0" << plus(hi0) << ") br = (ci_ - 1) * " << BH << " + (" << yy << " - r0" << plus(-lo0) << ");\n";
+      src << I << "    else if (r1 < N0 && " << yy << " >= r1" << plus(lo0) << ") br = ci_ * " << BH << " + (" << yy << " - r1" << plus(-lo0) << ");\n";
+      src << I << "    if (br >= 0) {\n";
+      src << I << "      gp = reinterpret_cast<T*>(a.t[" << gip->slot << "]) + ((long long)br * " << E1 << " + (" << xx1 << plus(so1) << ")) * "
+          << E2 << "LL + (" << xx2 << plus(so2) << ");\n";
+      src << I << "    } else {\n";
+      src << I << "      int e1 = -1;\n";
+      src << I << "      if (o1 > 0 && " << xx1 << " < o1" << plus(hi1) << ") e1 = o1;\n";
+      src << I << "      else if (o1 + " << tile[1] << " < N1 && " << xx1 << " >= o1 + " << tile[1] << plus(lo1) << ") e1 = o1 + " << tile[1] << ";\n";
+      src << I << "      if (e1 >= 0) {\n";
+      src << I << "        gp = reinterpret_cast<T*>(a.t[" << gip->slot + 1 << "]) + (((long long)(e1 / " << tile[1] << " - 1) * " << BW1
+          << " + (" << xx1 << " - e1" << plus(-lo1) << ")) * " << E0 << " + (" << yy << plus(so0) << ")) * " << E2 << "LL + (" << xx2
+          << plus(so2) << ");\n";
+      src << I << "      } else {\n";
+      src << I << "        int e2 = -1;\n";
+      src << I << "        if (o2 > 0 && " << xx2 << " < " << ze("o2") << ") e2 = o2;\n";
+      src << I << "        else if (o2 + " << tile[2] << " < N2 && " << xx2 << " >= " << zs("o2 + " + std::to_string(tile[2])) << ") e2 = o2 + "
+          << tile[2] << ";\n";
+      src << I << "        if (e2 >= 0) gp = reinterpret_cast<T*>(a.t[" << gip->slot + 2 << "]) + (((long long)(e2 / " << tile[2] << " - 1) * "
+          << BW2 << " + (" << xx2 << " - " << zs("e2") << ")) * " << E0 << " + (" << yy << plus(so0) << ")) * " << E1 << "LL + (" << xx1
+          << plus(so1) << ");\n";
+      src << I << "      }\n";
+      src << I << "    }\n";
+      src << I << "  }\n";
+      src << I << "  *gp = q_" << o.param << ";\n";
+      src << I << "}\n";
+      continue;
+    }
     src << ") t" << ti << "[" << C.tidx(ti, pos, std::vector<int>(nd, 0)) << "] = q_" << o.param << ";\n";
   }
     return true;
@@ -1353,6 +1412,10 @@ void March::tail() {
 }
 
 void March::capture() {
+  if (ws) {
+    if (!ips.empty() && nd == 3) commit3();
+    return;
+  }
   // ---- in-place: capture the bands other units read before this step writes
   if (!ips.empty()) {
     std::vector<std::pair<size_t, int>> caps;  // (variable, terminal)
@@ -1361,6 +1424,80 @@ void March::capture() {
     for (const auto& ip : ips) slots.push_back(ip.slot);
     emit_capture(C, "lf_jit_capture", caps, slots, tile, src);
   }
+}
+
+// In place, 3D warp-specialised march: after the step, copy the deferred
+// boundary writes into the grid -- plane bands (planes around internal chunk
+// boundaries), row bands (tile rows around internal tile-row boundaries,
+// outside the plane bands), column bands (sector-aligned tile columns around
+// internal tile-column boundaries, outside both) -- flat over their cells,
+// four per thread
+void March::commit3() {
+  src << "extern \"C\" __global__ void __launch_bounds__(256) lf_jit_commit_ws(const LfArgs a) {\n";
+  src << "  const int N0 = (int)a.n0;\n";
+  src << "  const int nch = (N0 + a.chunk - 1) / a.chunk;\n";
+  for (const auto& ip : ips) {
+    const auto& t = C.P.terminals[ip.gi];
+    const size_t v = ip.v;
+    const long so0 = -t.base[0] + C.LO[0], so1 = -t.base[1] + C.LO[1], so2 = -t.base[2] + C.LO[2];
+    const long lo0 = saved_vmin[v][0], hi0 = C.vmax[v][0], lo1 = saved_vmin[v][1], hi1 = C.vmax[v][1];
+    const long lo2 = saved_vmin[v][2], hi2 = C.vmax[v][2], SE = 32 / eb;
+    const long E0 = t.extent[0], E1 = t.extent[1], E2 = t.extent[2];
+    const long BH = hi0 - lo0, BW1 = hi1 - lo1, BW2 = hi2 - lo2 + 2 * (SE - 1);
+    const long N1 = C.N[1], N2 = C.N[2];
+    const long NT1 = (N1 + tile[1] - 1) / tile[1], NT2 = (N2 + tile[2] - 1) / tile[2];
+    auto zs = [&](const std::string& e) {
+      return "(((" + e + plus(lo2 + so2) + ") & ~" + std::to_string(SE - 1) + ")" + plus(-so2) + ")";
+    };
+    auto ze = [&](const std::string& e) {
+      return "(((" + e + plus(hi2 + so2 + SE - 1) + ") & ~" + std::to_string(SE - 1) + ")" + plus(-so2) + ")";
+    };
+    src << "  {\n";
+    src << "    T* m = reinterpret_cast<T*>(a.t[" << ip.gi << "]);\n";
+    src << "    const T* pb = reinterpret_cast<const T*>(a.t[" << ip.slot << "]);\n";
+    src << "    const T* b1 = reinterpret_cast<const T*>(a.t[" << ip.slot + 1 << "]);\n";
+    src << "    const T* b2 = reinterpret_cast<const T*>(a.t[" << ip.slot + 2 << "]);\n";
+    src << "    const long long np = (long long)max(0, nch - 1) * " << BH * N1 * N2 << "LL;\n";
+    src << "    const long long n1 = (long long)N0 * " << (NT1 - 1) * BW1 * N2 << "LL;\n";
+    src << "    const long long n2 = (long long)N0 * " << (NT2 - 1) * BW2 * N1 << "LL;\n";
+    src << "    #pragma unroll\n";
+    src << "    for (int j = 0; j < 4; ++j) {\n";
+    src << "      long long p = (long long)blockIdx.x * 1024 + j * 256 + threadIdx.x;\n";
+    src << "      if (p < np) {\n";
+    src << "        const long long r = p / " << N1 * N2 << "LL, q = p - r * " << N1 * N2 << "LL;\n";
+    src << "        const int x1 = (int)(q / " << N2 << "), x2 = (int)(q % " << N2 << ");\n";
+    src << "        const int y = (int)(r / " << BH << " + 1) * a.chunk" << plus(lo0) << " + (int)(r % " << BH << ");\n";
+    src << "        if (y >= 0 && y < N0) m[((long long)(y" << plus(so0) << ") * " << E1 << " + (x1" << plus(so1) << ")) * " << E2
+        << "LL + (x2" << plus(so2) << ")] = pb[(r * " << E1 << " + (x1" << plus(so1) << ")) * " << E2 << "LL + (x2" << plus(so2) << ")];\n";
+    src << "        continue;\n";
+    src << "      }\n";
+    src << "      p -= np;\n";
+    src << "      if (p < n1) {\n";
+    src << "        const long long kr = p / ((long long)N0 * " << N2 << "), q = p - kr * ((long long)N0 * " << N2 << ");\n";
+    src << "        const int y = (int)(q / " << N2 << "), x2 = (int)(q % " << N2 << ");\n";
+    src << "        const int x1 = (int)(kr / " << BW1 << " + 1) * " << tile[1] << plus(lo1) << " + (int)(kr % " << BW1 << ");\n";
+    src << "        const int bb = (y" << plus(-lo0) << ") / a.chunk * a.chunk;\n";
+    src << "        if (bb > 0 && bb < N0 && y < bb" << plus(hi0) << ") continue;  // with the plane bands\n";
+    src << "        if (x1 >= 0 && x1 < " << N1 << ") m[((long long)(y" << plus(so0) << ") * " << E1 << " + (x1" << plus(so1) << ")) * " << E2
+        << "LL + (x2" << plus(so2) << ")] = b1[(kr * " << E0 << " + (y" << plus(so0) << ")) * " << E2 << "LL + (x2" << plus(so2) << ")];\n";
+    src << "        continue;\n";
+    src << "      }\n";
+    src << "      p -= n1;\n";
+    src << "      if (p < n2) {\n";
+    src << "        const long long kc = p / ((long long)N0 * " << N1 << "), q = p - kc * ((long long)N0 * " << N1 << ");\n";
+    src << "        const int y = (int)(q / " << N1 << "), x1 = (int)(q % " << N1 << ");\n";
+    src << "        const int e2 = (int)(kc / " << BW2 << " + 1) * " << tile[2] << ", x2 = " << zs("e2") << " + (int)(kc % " << BW2 << ");\n";
+    src << "        const int bb = (y" << plus(-lo0) << ") / a.chunk * a.chunk;\n";
+    src << "        if (bb > 0 && bb < N0 && y < bb" << plus(hi0) << ") continue;  // with the plane bands\n";
+    src << "        const int b1_ = (x1" << plus(-lo1) << ") / " << tile[1] << " * " << tile[1] << ";\n";
+    src << "        if (b1_ > 0 && b1_ < " << N1 << " && x1 < b1_" << plus(hi1) << ") continue;  // with the row bands\n";
+    src << "        if (x2 >= 0 && x2 < " << N2 << " && x2 < " << ze("e2") << ") m[((long long)(y" << plus(so0) << ") * " << E1 << " + (x1"
+        << plus(so1) << ")) * " << E2 << "LL + (x2" << plus(so2) << ")] = b2[(kc * " << E0 << " + (y" << plus(so0) << ")) * " << E1
+        << "LL + (x1" << plus(so1) << ")];\n";
+    src << "      }\n";
+    src << "    }\n  }\n";
+  }
+  src << "}\n";
 }
 }  // namespace
 
@@ -2066,8 +2203,9 @@ bool jit_generate(const lf::Plan& P, JitProgram& out, const std::string& sources
     std::string variants;
     std::ostringstream ws;
     out.ws_maps.clear();
-    // in-place aliases keep the band-capturing plain march in 3D
-    if (C.P.rs.aliases.empty() && emit_march(C, out, ws, true) && !out.ws_maps.empty() &&
+    // in place: 2D chains take the register march below; 3D chains the
+    // warp-specialised march with deferred boundary writes
+    if ((C.P.rs.aliases.empty() || C.nd == 3) && emit_march(C, out, ws, true) && !out.ws_maps.empty() &&
         static_cast<int>(out.ws_maps.size()) <= kJitMaxMaps) {
       out.has_ws = true;
       variants += ws.str();

@@ -231,6 +231,45 @@ int JitKernel::run_inplace(const ExecArgs& a, JitArgs& args, std::string& err) {
       return LF_OK;
     }
   }
+  // 3D: the warp-specialised march with deferred boundary writes (the same
+  // scheme; codegen.cpp March::commit3)
+  if (step_ws_ && commit_ws_ && prog_.ws_inplace.size() == prog_.inplace.size() && !prog_.ws_inplace.empty()) {
+    long chunk = pick_chunk(rows, prog_.ws_inner_tiles, resident_ws_, prog_.prologue, prog_.chunk);
+    long bh = 1;
+    for (const auto& q : prog_.ws_inplace) bh = std::max<long>(bh, q.bh);
+    chunk = std::min(rows, std::max(chunk, bh));
+    if (const char* e = lfx::option("LF_JIT_CHUNK")) chunk = std::max(bh, std::min<long>(rows, std::atol(e)));
+    const long nch = (rows + chunk - 1) / chunk;
+    int st = bands_for(prog_.ws_inplace, nch, 0, err);
+    if (st != LF_OK) return st;
+    args.chunk = static_cast<int>(chunk);
+    for (size_t i = 0; i < T.size(); ++i) args.t[i] = a.terms[i];
+    for (size_t k = 0; k < bands_.size(); ++k) args.t[T.size() + k] = bands_[k];
+    JitMaps maps;
+    std::vector<void*> bufs(a.terms, a.terms + T.size());
+    if (tma_maps(prog_.ws_maps, bufs, rows, maps)) {
+      const long units = nch * prog_.ws_inner_tiles;
+      const dim3 grid(static_cast<unsigned>(std::max<long>(1, std::min<long>(resident_ws_, units))));
+      long band_cells = 1;  // the commit kernel's flat index space (largest aliased pair)
+      for (const auto& q : prog_.ws_inplace) {
+        const long nt1 = (q.n1 + q.t1 - 1) / q.t1, nt2 = (q.n2 + q.t2 - 1) / q.t2;
+        band_cells = std::max(band_cells, (nch - 1) * q.bh * q.n1 * q.n2 + rows * (nt1 - 1) * q.bw1 * q.n2 +
+                                              rows * (nt2 - 1) * q.bw2 * q.n1);
+      }
+      const unsigned commit_blocks = static_cast<unsigned>((band_cells + 1023) / 1024);
+      for (int s = 0; s < a.steps; ++s) {
+        st = launch(step_ws_, grid, dim3(prog_.ws_threads), prog_.ws_smem_bytes, a.stream, &args, err, &maps);
+        if (st != LF_OK) return st;
+        st = launch(commit_ws_, dim3(commit_blocks), dim3(256), 0, a.stream, &args, err);
+        if (st != LF_OK) return st;
+        if (fill_ && prog_.has_fill) {
+          st = launch(fill_, dim3(592), dim3(256), 0, a.stream, &args, err);
+          if (st != LF_OK) return st;
+        }
+      }
+      return LF_OK;
+    }
+  }
   // chunk: about two units per resident CTA, at least 8 pipeline depths
   long chunk = (rows * prog_.inner_tiles + 2L * resident_ - 1) / (2L * resident_);
   chunk = std::min(rows, std::max(chunk, 8L * std::max(1, prog_.prologue)));
@@ -441,6 +480,7 @@ int JitKernel::run(const ExecArgs& a, std::string& err) {
     if (d.get(&f, m, "lf_jit_fill") == CUDA_SUCCESS) fill_ = f;
     if (d.get(&f, m, "lf_jit_capture") == CUDA_SUCCESS) capture_ = f;
     if (d.get(&f, m, "lf_jit_commit_rm") == CUDA_SUCCESS) commit_rm_ = f;
+    if (d.get(&f, m, "lf_jit_commit_ws") == CUDA_SUCCESS) commit_ws_ = f;
     if (!prog_.nest_kernels.empty()) {
       for (const auto& nk : prog_.nest_kernels) {
         if (d.get(&f, m, nk.fn.c_str()) != CUDA_SUCCESS) {

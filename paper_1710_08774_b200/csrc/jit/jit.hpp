@@ -69,6 +69,7 @@ struct JitProgram {
   size_t ws_smem_bytes = 0;
   long ws_inner_tiles = 1;  // the variant's own inner tiling
   int ws_threads = 288;
+  std::vector<Inplace> ws_inplace;  // 3D in place on the warp-specialised march (deferred writes)
   // 2D register march (lf_jit_step_rm, codegen_rm.cpp): warp strips, register
   // windows, no CTA barriers; preferred over lf_jit_step_ws where it compiles
   bool has_rm = false;
@@ -134,6 +135,7 @@ class JitKernel {
   bool tma_maps(const std::vector<JitProgram::Tma>& list, const std::vector<void*>& bufs, long rows, JitMaps& maps,
                 long boundaries = 0);
   void* commit_rm_ = nullptr;  // in-place register march: deferred boundary writes into the grid
+  void* commit_ws_ = nullptr;  // in-place 3D warp-specialised march: the same
   int bands_for(const std::vector<JitProgram::Inplace>& list, long nch, long nt_of_tile1, std::string& err);
   long plan_rows_ = 0;  // trips of the outermost loop dimension (whole domain)
   int run_inplace(const ExecArgs& a, JitArgs& args, std::string& err);

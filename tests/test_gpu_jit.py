@@ -90,28 +90,33 @@ def test_jit_slab_parts_compose():
     assert torch.equal(whole[1:-1], parts[1:-1])
 
 
-@pytest.mark.parametrize("name,shape,steps,chunk,rm", [
-    ("biharm_inplace", (300, 1000), 3, None, "1"),
-    ("biharm_inplace", (300, 1000), 2, "24", "1"),
-    ("biharm_inplace", (130, 2100), 2, "16", "1"),
-    ("biharm_inplace", (300, 1000), 2, "24", "0"),
-    ("heat3d_inplace", (20, 40, 130), 3, None, "1"),
-    ("heat3d_inplace", (20, 40, 130), 2, "5", "1"),
+@pytest.mark.parametrize("name,shape,steps,chunk,knob", [
+    ("biharm_inplace", (300, 1000), 3, None, ""),
+    ("biharm_inplace", (300, 1000), 2, "24", ""),
+    ("biharm_inplace", (130, 2100), 2, "16", ""),
+    ("biharm_inplace", (300, 1000), 2, "24", "LF_JIT_RM=0"),
+    ("heat3d_inplace", (20, 40, 130), 3, None, ""),
+    ("heat3d_inplace", (20, 40, 130), 2, "5", ""),
+    ("heat3d_inplace", (23, 70, 200), 2, "4", ""),
+    ("heat3d_inplace", (20, 40, 130), 2, "5", "LF_JIT_WS=0"),
 ])
-def test_inplace_matches_out_of_place_oracle(name, shape, steps, chunk, rm, monkeypatch):
+def test_inplace_matches_out_of_place_oracle(name, shape, steps, chunk, knob, monkeypatch):
     """config.aliases + one buffer for axiom and goal: the generic executor
-    runs in place (bands captured at unit boundaries) and must equal the
-    out-of-place run_naive bit for bit, ghost ring included.  2D chains run on
-    the register march (boundary writes deferred to bands, committed after the
-    step); LF_JIT_RM=0 keeps the plain march's band loader."""
+    runs in place and must equal the out-of-place run_naive bit for bit, ghost
+    ring included.  2D chains run on the register march and 3D chains on the
+    warp-specialised march, both deferring the boundary writes other units
+    still read to bands committed after the step; LF_JIT_RM=0 / LF_JIT_WS=0
+    keep the plain march's band loader (bands captured before the step)."""
     import torch
-    monkeypatch.setenv("LF_JIT_RM", rm)
+    if knob:
+        monkeypatch.setenv(*knob.split("="))
     if chunk:
         monkeypatch.setenv("LF_JIT_CHUNK", chunk)  # many row chunks -> many row bands
     spec = lf.set_ranges((SPECS / f"{name}.lf").read_text(), shape)
     plan = lf.Plan(spec, f"{name}.lf")
     assert plan.executor == "jit_window_fused"
-    assert ("lf_jit_commit_rm(" in plan.source) == (len(shape) == 2 and rm == "1")
+    deferred = "lf_jit_commit_rm(" if len(shape) == 2 else "lf_jit_commit_ws("
+    assert (deferred in plan.source) == (not knob)
     if len(shape) == 2:
         u0 = inputs.biharm_input(*shape, seed=8)
     else:
