@@ -608,6 +608,7 @@ class March {
   void tail();
   void capture();
   void commit3();
+  void inplace_masks();
   void emit_load(size_t v, const std::string& row, const std::string& slotexpr, const char* ind);
   // ws: a staged axiom's innermost row is fetched as nbox TMA boxes of bw
   // elements (box rows <= 256 elements, 128-B multiples so every box lands
@@ -961,6 +962,7 @@ void March::head() {
   if (!ws)
     for (size_t v = 0; v < nv; ++v)
       if (win[v] > 1) src << "  int b" << v << " = " << wrap(v, TS) << ";\n";
+  if (ws && nd == 3 && !ips.empty()) inplace_masks();
   // register windows along the march (opt-in, LF_JIT_ROT=1): a thread keeps
   // its cells for a whole segment, so a window value read at row offset s on
   // trip t+1 is the one it read at s+1 on trip t -- only the newest row of
@@ -1227,52 +1229,32 @@ bool March::group(size_t gi, int& level) {
     for (const auto& ip : ips)
       if (ip.gi == ti) gip = &ip;
     if (ws && nd == 3 && gip) {
-      // in place: deferred boundary writes (plane zone -> plane band, tile-row
-      // zone -> row band, sector-aligned tile-column zone -> column band)
+      // in place: deferred boundary writes -- plane zone -> plane band, tile-row
+      // zone -> row band, sector-aligned tile-column zone -> column band; the
+      // addresses are selected, not branched to (every warp holds zone lanes)
       const auto& t = C.P.terminals[ti];
       const size_t v = gip->v;
-      const long so0 = -t.base[0] + C.LO[0], so1 = -t.base[1] + C.LO[1], so2 = -t.base[2] + C.LO[2];
-      const long lo0 = saved_vmin[v][0], hi0 = C.vmax[v][0], lo1 = saved_vmin[v][1], hi1 = C.vmax[v][1];
-      const long lo2 = saved_vmin[v][2], hi2 = C.vmax[v][2], SE = 32 / eb;
-      const long E0 = t.extent[0], E1 = t.extent[1], E2 = t.extent[2];
-      const long BH = hi0 - lo0, BW1 = hi1 - lo1, BW2 = hi2 - lo2 + 2 * (SE - 1);
-      auto zs = [&](const std::string& e) {
-        return "(((" + e + plus(lo2 + so2) + ") & ~" + std::to_string(SE - 1) + ")" + plus(-so2) + ")";
-      };
-      auto ze = [&](const std::string& e) {
-        return "(((" + e + plus(hi2 + so2 + SE - 1) + ") & ~" + std::to_string(SE - 1) + ")" + plus(-so2) + ")";
-      };
+      const long so1 = -t.base[1] + C.LO[1], so2 = -t.base[2] + C.LO[2];
+      const long lo0 = saved_vmin[v][0], hi0 = C.vmax[v][0], lo2 = saved_vmin[v][2], hi2 = C.vmax[v][2];
+      const long SE = 32 / eb, E1 = t.extent[1], E2 = t.extent[2], BH = hi0 - lo0, BW2 = hi2 - lo2 + 2 * (SE - 1);
       const std::string yy = "(y" + plus(o.rel[0]) + ")", xx1 = "(x1" + plus(o.rel[1]) + ")", xx2 = "(x2" + plus(o.rel[2]) + ")";
+      const std::string nm = std::to_string(gi) + "_" + o.param;
       src << ") {\n";
       src << I << "  T* gp = t" << ti << " + " << C.tidx(ti, pos, std::vector<int>(nd, 0)) << ";\n";
       src << I << "  if (a.inplace) {\n";
-      src << I << "    int br = -1;\n";
-      src << I << "    if (r0 > 0 && " << yy << " < r0" << plus(hi0) << ") br = (ci_ - 1) * " << BH << " + (" << yy << " - r0" << plus(-lo0) << ");\n";
-      src << I << "    else if (r1 < N0 && " << yy << " >= r1" << plus(lo0) << ") br = ci_ * " << BH << " + (" << yy << " - r1" << plus(-lo0) << ");\n";
-      src << I << "    if (br >= 0) {\n";
-      src << I << "      gp = reinterpret_cast<T*>(a.t[" << gip->slot << "]) + ((long long)br * " << E1 << " + (" << xx1 << plus(so1) << ")) * "
-          << E2 << "LL + (" << xx2 << plus(so2) << ");\n";
-      src << I << "    } else {\n";
-      src << I << "      int e1 = -1;\n";
-      src << I << "      if (o1 > 0 && " << xx1 << " < o1" << plus(hi1) << ") e1 = o1;\n";
-      src << I << "      else if (o1 + " << tile[1] << " < N1 && " << xx1 << " >= o1 + " << tile[1] << plus(lo1) << ") e1 = o1 + " << tile[1] << ";\n";
-      src << I << "      if (e1 >= 0) {\n";
-      src << I << "        gp = reinterpret_cast<T*>(a.t[" << gip->slot + 1 << "]) + (((long long)(e1 / " << tile[1] << " - 1) * " << BW1
-          << " + (" << xx1 << " - e1" << plus(-lo1) << ")) * " << E0 << " + (" << yy << plus(so0) << ")) * " << E2 << "LL + (" << xx2
-          << plus(so2) << ");\n";
-      src << I << "      } else {\n";
-      src << I << "        int e2 = -1;\n";
-      src << I << "        if (o2 > 0 && " << xx2 << " < " << ze("o2") << ") e2 = o2;\n";
-      src << I << "        else if (o2 + " << tile[2] << " < N2 && " << xx2 << " >= " << zs("o2 + " + std::to_string(tile[2])) << ") e2 = o2 + "
-          << tile[2] << ";\n";
-      src << I << "        if (e2 >= 0) gp = reinterpret_cast<T*>(a.t[" << gip->slot + 2 << "]) + (((long long)(e2 / " << tile[2] << " - 1) * "
-          << BW2 << " + (" << xx2 << " - " << zs("e2") << ")) * " << E0 << " + (" << yy << plus(so0) << ")) * " << E1 << "LL + (" << xx1
-          << plus(so1) << ");\n";
-      src << I << "      }\n";
-      src << I << "    }\n";
+      src << I << "    const int pbr = r0 > 0 && " << yy << " < r0" << plus(hi0) << " ? (ci_ - 1) * " << BH << " + (" << yy << " - r0" << plus(-lo0)
+          << ") : (r1 < N0 && " << yy << " >= r1" << plus(lo0) << " ? ci_ * " << BH << " + (" << yy << " - r1" << plus(-lo0) << ") : -1);\n";
+      src << I << "    T* const pp = reinterpret_cast<T*>(a.t[" << gip->slot << "]) + ((long long)pbr * " << E1 << " + (" << xx1 << plus(so1)
+          << ")) * " << E2 << "LL + (" << xx2 << plus(so2) << ");\n";
+      src << I << "    T* const rp = reinterpret_cast<T*>(a.t[" << gip->slot + 1 << "]) + rbo" << nm << "[k] + (long long)" << yy << " * " << E2
+          << ";\n";
+      src << I << "    T* const cp = reinterpret_cast<T*>(a.t[" << gip->slot + 2 << "]) + cbo" << nm << " + ((long long)" << yy << " * " << E1
+          << " + " << xx1 << ") * " << BW2 << ";\n";
+      src << I << "    gp = pbr >= 0 ? pp : (((rz" << nm << " >> k) & 1u) ? rp : (cz" << nm << " ? cp : gp));\n";
       src << I << "  }\n";
       src << I << "  *gp = q_" << o.param << ";\n";
       src << I << "}\n";
+      (void)so1;
       continue;
     }
     src << ") t" << ti << "[" << C.tidx(ti, pos, std::vector<int>(nd, 0)) << "] = q_" << o.param << ";\n";
@@ -1426,12 +1408,69 @@ void March::capture() {
   }
 }
 
+// In place, 3D warp-specialised march: which of this thread's cells fall in a
+// tile-row or tile-column zone is fixed for the unit -- a bit per row k of the
+// cells it owns (rz) and one flag for its column (cz) per in-place goal
+// output, so the march tests two bits per store and takes the full routing
+// only for the few cells in a zone
+void March::inplace_masks() {
+  src << "  // in place: where this thread's cells go when they lie in a tile-row /\n"
+         "  // tile-column band (fixed for the unit): offsets into the bands less the\n"
+         "  // plane term, rz / cz the rows k / the column that do\n";
+  for (size_t gi = 0; gi < G.size(); ++gi) {
+    const Grp& g = G[gi];
+    for (const auto& o : g.out) {
+      const int ti = C.terminal_of(o.var, true);
+      const IP* gip = nullptr;
+      for (const auto& ip : ips)
+        if (ip.gi == ti) gip = &ip;
+      if (ti < 0 || !gip) continue;
+      const auto& t = C.P.terminals[ti];
+      const size_t v = gip->v;
+      const long so0 = -t.base[0] + C.LO[0], so1 = -t.base[1] + C.LO[1], so2 = -t.base[2] + C.LO[2], SE = 32 / eb;
+      const long lo1 = saved_vmin[v][1], hi1 = C.vmax[v][1], lo2 = saved_vmin[v][2], hi2 = C.vmax[v][2];
+      const long E0 = t.extent[0], E1 = t.extent[1], E2 = t.extent[2];
+      const long BW1 = hi1 - lo1, BW2 = hi2 - lo2 + 2 * (SE - 1);
+      const int K = (tile[1] + (g.gmax[1] - g.gmin[1]) + STEP - 1) / STEP;
+      auto zs = [&](const std::string& e) {
+        return "(((" + e + plus(lo2 + so2) + ") & ~" + std::to_string(SE - 1) + ")" + plus(-so2) + ")";
+      };
+      auto ze = [&](const std::string& e) {
+        return "(((" + e + plus(hi2 + so2 + SE - 1) + ") & ~" + std::to_string(SE - 1) + ")" + plus(-so2) + ")";
+      };
+      const std::string nm = std::to_string(gi) + "_" + o.param;
+      src << "  unsigned rz" << nm << " = 0;\n  bool cz" << nm << " = false;\n";
+      src << "  long long rbo" << nm << "[" << K << "], cbo" << nm << " = 0;\n";
+      src << "  {\n";
+      src << "    const int xx2 = o2 + tx" << plus(g.gmin[2] + o.rel[2]) << ";\n";
+      src << "    #pragma unroll\n";
+      src << "    for (int k = 0; k < " << K << "; ++k) {\n";
+      src << "      const int xx1 = o1 + " << LANE << plus(g.gmin[1] + o.rel[1]) << " + k * " << STEP << ";\n";
+      src << "      int e1 = -1;\n";
+      src << "      if (o1 > 0 && xx1 < o1" << plus(hi1) << ") e1 = o1;\n";
+      src << "      else if (o1 + " << tile[1] << " < N1 && xx1 >= o1 + " << tile[1] << plus(lo1) << ") e1 = o1 + " << tile[1] << ";\n";
+      src << "      if (a.inplace && e1 >= 0) rz" << nm << " |= 1u << k;\n";
+      src << "      rbo" << nm << "[k] = e1 < 0 ? 0 : (((long long)(e1 / " << tile[1] << " - 1) * " << BW1 << " + (xx1 - e1" << plus(-lo1)
+          << ")) * " << E0 << plus(so0) << ") * " << E2 << "LL + (xx2" << plus(so2) << ");\n";
+      src << "    }\n";
+      src << "    int e2 = -1;\n";
+      src << "    if (o2 > 0 && xx2 < " << ze("o2") << ") e2 = o2;\n";
+      src << "    else if (o2 + " << tile[2] << " < N2 && xx2 >= " << zs("o2 + " + std::to_string(tile[2])) << ") e2 = o2 + " << tile[2]
+          << ";\n";
+      src << "    cz" << nm << " = a.inplace && e2 >= 0;\n";
+      src << "    cbo" << nm << " = e2 < 0 ? 0 : ((long long)(e2 / " << tile[2] << " - 1) * " << E0 << plus(so0) << ") * " << E1 * BW2
+          << "LL + " << so1 * BW2 << "LL + (xx2 - " << zs("e2") << ");\n";
+      src << "  }\n";
+    }
+  }
+}
+
 // In place, 3D warp-specialised march: after the step, copy the deferred
 // boundary writes into the grid -- plane bands (planes around internal chunk
 // boundaries), row bands (tile rows around internal tile-row boundaries,
 // outside the plane bands), column bands (sector-aligned tile columns around
-// internal tile-column boundaries, outside both) -- flat over their cells,
-// four per thread
+// internal tile-column boundaries, outside both, [boundary][plane][row][col])
+// -- flat over their cells, four per thread, contiguous on both sides
 void March::commit3() {
   src << "extern \"C\" __global__ void __launch_bounds__(256) lf_jit_commit_ws(const LfArgs a) {\n";
   src << "  const int N0 = (int)a.n0;\n";
@@ -1484,16 +1523,20 @@ void March::commit3() {
     src << "      }\n";
     src << "      p -= n1;\n";
     src << "      if (p < n2) {\n";
-    src << "        const long long kc = p / ((long long)N0 * " << N1 << "), q = p - kc * ((long long)N0 * " << N1 << ");\n";
-    src << "        const int y = (int)(q / " << N1 << "), x1 = (int)(q % " << N1 << ");\n";
-    src << "        const int e2 = (int)(kc / " << BW2 << " + 1) * " << tile[2] << ", x2 = " << zs("e2") << " + (int)(kc % " << BW2 << ");\n";
+    // column bands [boundary][plane][row][column]: a band row is one or two
+    // whole 32-B sectors of the grid row, read and written contiguously
+    src << "        const int c = (int)(p % " << BW2 << ");\n";
+    src << "        const long long rr = p / " << BW2 << ";\n";
+    src << "        const int x1 = (int)(rr % " << N1 << "), y = (int)((rr / " << N1 << ") % N0);\n";
+    src << "        const int k = (int)(rr / ((long long)N0 * " << N1 << "));\n";
+    src << "        const int e2 = (k + 1) * " << tile[2] << ", x2 = " << zs("e2") << " + c;\n";
     src << "        const int bb = (y" << plus(-lo0) << ") / a.chunk * a.chunk;\n";
     src << "        if (bb > 0 && bb < N0 && y < bb" << plus(hi0) << ") continue;  // with the plane bands\n";
     src << "        const int b1_ = (x1" << plus(-lo1) << ") / " << tile[1] << " * " << tile[1] << ";\n";
     src << "        if (b1_ > 0 && b1_ < " << N1 << " && x1 < b1_" << plus(hi1) << ") continue;  // with the row bands\n";
     src << "        if (x2 >= 0 && x2 < " << N2 << " && x2 < " << ze("e2") << ") m[((long long)(y" << plus(so0) << ") * " << E1 << " + (x1"
-        << plus(so1) << ")) * " << E2 << "LL + (x2" << plus(so2) << ")] = b2[(kc * " << E0 << " + (y" << plus(so0) << ")) * " << E1
-        << "LL + (x1" << plus(so1) << ")];\n";
+        << plus(so1) << ")) * " << E2 << "LL + (x2" << plus(so2) << ")] = b2[(((long long)k * " << E0 << " + (y" << plus(so0) << ")) * "
+        << E1 << " + (x1" << plus(so1) << ")) * " << BW2 << "LL + c];\n";
     src << "      }\n";
     src << "    }\n  }\n";
   }
