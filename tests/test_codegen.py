@@ -59,9 +59,14 @@ def test_single_level_chain_has_no_consumer_barrier():
     assert "bar.sync" not in ws  # fluxes inlined: one group, one level
 
 
-def test_in_place_chains_keep_the_band_loader():
+def test_in_place_chains_defer_their_boundary_writes():
+    """3D in place: the warp-specialised march with deferred boundary writes
+    (band stores + lf_jit_commit_ws); the plain march keeps the band loader
+    (LF_JIT_WS=0 or untileable buffers)."""
+    src = lf.Plan.from_file(SPECS / "heat3d_inplace.lf").source
     plain, ws = kernels(lf.Plan.from_file(SPECS / "heat3d_inplace.lf"))
-    assert not ws and "cp.async.ca.shared.global" in plain
+    assert ws and "lf_jit_commit_ws(" in src and "cbo0_" in ws
+    assert "cp.async.ca.shared.global" in plain and "lf_jit_capture(" in src
 
 
 def test_single_read_producer_is_evaluated_in_its_consumer():
