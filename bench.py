@@ -529,8 +529,14 @@ def main():
         launches = plan.launches(w["chain_steps"])
     elif w["halo"] is None:
         launches = plan.launches_per_step * w["chain_steps"]
-    else:  # overlapped slab schedule: the two face parts and the interior, every step
-        launches = 3 * plan.launches_per_step * w["chain_steps"]
+    else:
+        # lf_run_slabs' schedule (capi.cpp run_slabs_core): `whole` -- one launch
+        # per step -- for slabs of >= 1024 rows, else `parallel` -- the two face
+        # parts and the interior, every step (LF_SLAB_SCHEDULE overrides)
+        sched = os.environ.get("LF_SLAB_SCHEDULE") or ("whole" if hi - lo >= 1024 else "parallel")
+        # the Python exchange path (slabs.run_slabs_overlapped) always splits faces / interior
+        per_step = 1 if args.slab_exchange == "native" and sched == "whole" else 3
+        launches = per_step * plan.launches_per_step * w["chain_steps"]
 
     def barrier():
         if slab_mode:
