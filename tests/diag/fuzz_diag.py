@@ -6,8 +6,8 @@ from pathlib import Path
 import numpy as np
 import torch
 
+sys.path.insert(0, str(Path(__file__).resolve().parents[2]))
 sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
-sys.path.insert(0, str(Path(__file__).resolve().parents[1] / "tests"))
 from test_gpu_jit_fuzz import random_chain  # noqa: E402
 from oracle import generic  # noqa: E402
 import paper_1710_08774_b200 as lf  # noqa: E402

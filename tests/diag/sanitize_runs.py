@@ -4,7 +4,7 @@ generic executor's register march (2D, out of place and in place), its
 warp-specialised march (3D) and its plain march.  Each run is compared with
 the CPU oracle, so a tool that perturbs timing cannot hide a wrong result.
 
-    compute-sanitizer --tool racecheck python tools/sanitize_runs.py
+    compute-sanitizer --tool racecheck python tests/diag/sanitize_runs.py
 """
 import os
 import sys
@@ -13,7 +13,7 @@ from pathlib import Path
 import numpy as np
 import torch
 
-sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+sys.path.insert(0, str(Path(__file__).resolve().parents[2]))
 import oracle  # noqa: E402  (the checker)
 import paper_1710_08774_b200 as lf  # noqa: E402
 from paper_1710_08774_b200 import inputs  # noqa: E402
