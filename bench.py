@@ -527,6 +527,8 @@ def main():
     passes = plan.grid_passes(w["chain_steps"]) if not slab_mode else w["chain_steps"]
     if not slab_mode:
         launches = plan.launches(w["chain_steps"])
+        if w.get("inplace"):  # + the band commit (or capture) kernel of every in-place step
+            launches += w["chain_steps"]
     elif w["halo"] is None:
         launches = plan.launches_per_step * w["chain_steps"]
     else:

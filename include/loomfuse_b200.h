@@ -197,7 +197,8 @@ int lf_nccl_comm_destroy(void* nccl_comm);
  * lf_plan_grid_passes: passes lf_run(plan, ..., steps) makes over a whole
  * domain (fewer than `steps` where the executor fuses time steps, e.g. the
  * 3D heat chain's two-step passes); lf_plan_launches: kernel launches it
- * issues. */
+ * issues (out of place; an in-place run adds one per step, the band commit
+ * or capture kernel). */
 int lf_plan_launches_per_step(const lf_plan* plan);
 double lf_plan_compulsory_bytes_per_cell(const lf_plan* plan);
 int lf_plan_grid_passes(const lf_plan* plan, int steps);
