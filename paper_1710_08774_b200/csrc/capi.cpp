@@ -711,6 +711,26 @@ static int run_host_pipelined(lf_plan* plan, void* const* terms, const std::vect
     for (size_t k = 1; k < t.extent.size(); ++k) b *= t.extent[k];
     return b;
   };
+  // Multi-step runs of chains whose outer dimension does not wrap run as a
+  // wavefront over (step, part) -- see below -- in parts of >= 8 M cells (a part
+  // launch costs host time and a pipeline fill per row segment: Hydro2D 4096^2 x20
+  // runs 54 ms per run whole-domain, 57 / 70 ms as a wavefront of 16 / 32 parts),
+  // and only where that gives >= 16 parts; 32768^2 x10: 2188 ms first/last-step
+  // pipelined, 1376 / 1289 / 1274 ms as a wavefront of 32 / 64 / 96-128 parts.
+  // LF_HOST_WAVEFRONT=1 / 0 forces it on / off, LF_HOST_PARTS fixes the parts.
+  bool periodic0 = false;
+  for (const auto& [gname, mode] : plan->plan.rs.boundary)
+    if (!mode.empty() && mode[0] == lf::Boundary::periodic) periodic0 = true;
+  long halo0 = 0;
+  for (const auto& t : T)
+    if (chunked(t)) halo0 = std::max({halo0, lo0 - t.base[0], t.extent[0] - n0 - (lo0 - t.base[0])});
+  long cells = 1;
+  for (const auto& r : plan->plan.rs.ranges) cells *= r.trips();
+  const int wparts = lfx::option("LF_HOST_PARTS") ? parts : static_cast<int>(std::min<long>(128, cells / (8L << 20)));
+  bool wavefront = wparts >= 16;
+  if (const char* e = lfx::option("LF_HOST_WAVEFRONT")) wavefront = std::atoi(e) != 0;
+  wavefront = wavefront && steps > 1 && !periodic0 && wparts >= 2 && n0 / wparts >= std::max(1L, halo0);
+  if (wavefront) parts = wparts;
   auto copy = [&](void* dst, const void* src, int64_t bytes, cudaMemcpyKind kind, cudaStream_t st) {
     if (bytes <= 0) return LF_OK;
     return lfx::cuda_status(cudaMemcpyAsync(dst, src, bytes, kind, st), "cudaMemcpyAsync(pipelined)", err);
@@ -778,21 +798,6 @@ static int run_host_pipelined(lf_plan* plan, void* const* terms, const std::vect
   // dependence comes first.  Then every step trails the input rows up and the
   // last one sends each part down as it finishes: PCIe in both directions
   // overlaps the whole run, not only its first and last step.
-  bool periodic0 = false;
-  for (const auto& [gname, mode] : plan->plan.rs.boundary)
-    if (!mode.empty() && mode[0] == lf::Boundary::periodic) periodic0 = true;
-  long halo0 = 0;
-  for (const auto& t : T)
-    if (chunked(t)) halo0 = std::max({halo0, lo0 - t.base[0], t.extent[0] - n0 - (lo0 - t.base[0])});
-  // worth it for parts of many cells only: a part launch costs ~25 us of host
-  // time (tensor maps, launch), so small parts starve the GPU (Hydro2D 4096^2
-  // x20: 54 ms per run whole-domain, 57 / 70 ms as a wavefront of 16 / 32
-  // parts; 32768^2 x10: 2188 -> 1374 ms); LF_HOST_WAVEFRONT=1 / 0 forces it
-  long part_cells = n0 / parts;
-  for (size_t d = 1; d < plan->plan.rs.ranges.size(); ++d) part_cells *= plan->plan.rs.ranges[d].trips();
-  bool wavefront = part_cells >= (16L << 20);
-  if (const char* e = lfx::option("LF_HOST_WAVEFRONT")) wavefront = std::atoi(e) != 0;
-  wavefront = wavefront && steps > 1 && !periodic0 && n0 / parts >= std::max(1L, halo0);
   if (wavefront) {
     std::vector<std::vector<void*>> B(steps);
     for (int s = 0; s < steps; ++s) {
