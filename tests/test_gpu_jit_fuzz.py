@@ -124,7 +124,8 @@ def test_random_chain_matches_generic_oracle(seed, tmp_path):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("knob", ["LF_JIT_VEC=2", "LF_JIT_RM_PACK=1", "LF_JIT_RM_UNROLL=0", "LF_JIT_RM=0", "LF_JIT_WS=0"])
+@pytest.mark.parametrize("knob", ["LF_JIT_VEC=2", "LF_JIT_RM_PACK=1", "LF_JIT_RM_UNROLL=0", "LF_JIT_RM=0", "LF_JIT_WS=0",
+                                  "LF_JIT_RM_V=8", "LF_JIT_RM_WARPS=3"])
 def test_random_chains_with_opt_in_variants(knob, tmp_path):
     """Opt-in / comparison variants on the same random chains (the knobs are
     read at plan creation; set in-process with lf.option): LF_JIT_VEC=2 (plain
@@ -132,7 +133,9 @@ def test_random_chains_with_opt_in_variants(knob, tmp_path):
     LF_JIT_RM_PACK=1 (register march, fp32 cells in fp32x2 pairs),
     LF_JIT_RM_UNROLL=0 (register windows shifted by moves instead of renamed),
     LF_JIT_RM=0 / LF_JIT_WS=0 (the warp-specialised / plain smem-window
-    marches where the register march / TMA would run)."""
+    marches where the register march / TMA would run), LF_JIT_RM_V=8 /
+    LF_JIT_RM_WARPS=3 (register march: 8 cells per lane, 3 consumer warps --
+    other lane spans, margins and strip widths)."""
     k, v = knob.split("=")
     with lf.option(k, v):
         for seed in range(48):
