@@ -2036,9 +2036,155 @@ bool emit_nests(const lf::Plan& P, const std::string& sources, JitProgram& out, 
         }
         cls[r] = c;
       }
+      // elements operands of each reduction (the non-carry inputs)
+      std::vector<std::vector<int>> elem_t(reds.size());
+      for (size_t m = 0; m < reds.size(); ++m) {
+        const auto& rap = g.raps[reds[m]];
+        const auto& k = rs.kernels[rap.kernel];
+        if (k.inputs.size() > 2) return fail("associative kernel '" + k.name + "' with more than one element input");
+        for (size_t i = 0; i < rap.in_terms.size(); ++i) {
+          const auto& to = g.terms[rap.out_terms[0]];
+          const auto& ti = g.terms[rap.in_terms[i]];
+          if (!(ti.ident == to.ident && ti.dims == to.dims && !(ti == to))) elem_t[m].push_back(static_cast<int>(i));
+        }
+      }
+      // carry term of each reduction
+      std::vector<int> carry_t(reds.size(), -1);
+      for (size_t m = 0; m < reds.size(); ++m) {
+        const auto& rap = g.raps[reds[m]];
+        for (size_t i = 0; i < rap.in_terms.size(); ++i) {
+          const auto& ti = g.terms[rap.in_terms[i]];
+          const auto& to = g.terms[rap.out_terms[0]];
+          if (ti.ident == to.ident && ti.dims == to.dims && !(ti == to)) carry_t[m] = rap.in_terms[i];
+        }
+        if (carry_t[m] < 0) return fail("associative kernel '" + rs.kernels[rap.kernel].name + "' has no carry input");
+      }
+      // opt-in (LF_JIT_RED_TILED=1): exact, but measured slower on the 8192^2
+      // normalization (nest 0: 606 vs 350 us) -- 32 cells per CTA leave too few
+      // CTAs (256) to keep HBM busy
+      const bool tiled = pcells >= 32 && lfx::option("LF_JIT_RED_TILED") && std::atoi(lfx::option("LF_JIT_RED_TILED")) != 0;
+      if (tiled) {
+        // ---- transposed: a CTA owns 32 parallel cells, lane c of warp 0
+        // accumulates cell c (one ordered chain per lane, none redundant); all
+        // 256 threads evaluate the element operands of a 32 x EB tile into
+        // shared memory (double-buffered: warp 0 accumulates tile k while the
+        // others evaluate tile k+1).  Consecutive threads take consecutive
+        // elements when the innermost loop dimension is reduced (row sums),
+        // consecutive cells otherwise (column sums): coalesced either way.
+        const int EB = 64;
+        const bool elemfast = R.count(nd - 1) > 0;
+        nl.cells_per_cta = 32;
+        src << "extern \"C\" __global__ void __launch_bounds__(256) " << fn << "(const LfArgs a) {\n";
+        pointers(src);
+        src << "  __shared__ T lf_t[2][" << reds.size() << "][32][" << EB + 1 << "];\n";
+        src << "  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;\n";
+        src << "  for (long long cb = blockIdx.x * 32LL; cb < " << pcells << "LL; cb += gridDim.x * 32LL) {\n";
+        // warp 0: carries of its cell
+        for (size_t m = 0; m < reds.size(); ++m) src << "    T acc" << m << " = T(0);\n";
+        auto cell_coords = [&](std::ostream& o, const std::string& pcexpr, const std::string& ind) {
+          o << ind << "long long rem = " << pcexpr << ";\n";
+          for (int d = nd - 1; d >= 0; --d)
+            if (Pd.count(d)) o << ind << "const int x" << d << " = (int)(rem % " << N[d] << "); rem /= " << N[d] << ";\n";
+        };
+        src << "    if (warp == 0 && cb + lane < " << pcells << "LL) {\n";
+        cell_coords(src, "cb + lane", "      ");
+        for (int d = 0; d < nd; ++d)
+          if (!Pd.count(d)) src << "      const int x" << d << " = 0;\n";
+        done.assign(g.terms.size(), 0);
+        for (int r : topo)
+          if (in_nest[r] && cls[r] == 0) emit_rap(r, nv, src, "      ", okk, "true");
+        for (size_t m = 0; m < reds.size(); ++m) {
+          const int ct = carry_t[m];
+          const int pr = g.producer[ct];
+          if (pr >= 0 && g.raps[pr].kind == lf::RapKind::kernel && nest_of(pr) != nv && !done[ct]) {
+            src << "      const T v" << ct << " = " << mat_index(ct) << ";\n";
+            done[ct] = 1;
+          }
+          src << "      acc" << m << " = v" << ct << ";\n";
+        }
+        src << "    }\n";
+        src << "    for (long long rb = 0, kt = 0; rb < " << rcount << "LL; rb += " << EB << ", ++kt) {\n";
+        src << "      const int buf = (int)(kt & 1);\n";
+        src << "      for (int q = tid; q < " << 32 * EB << "; q += 256) {\n";
+        src << "        const int c = " << (elemfast ? "q / " + std::to_string(EB) : "q & 31") << ", j = "
+            << (elemfast ? "q % " + std::to_string(EB) : "q >> 5") << ";\n";
+        src << "        const bool ok = cb + c < " << pcells << "LL && rb + j < " << rcount << "LL;\n";
+        {
+          std::ostringstream ev;
+          cell_coords(ev, "ok ? cb + c : 0LL", "        ");
+          ev << "        long long rr = ok ? rb + j : 0LL;\n";
+          for (int d = nd - 1; d >= 0; --d)
+            if (R.count(d)) ev << "        const int x" << d << " = (int)(rr % " << N[d] << "); rr /= " << N[d] << ";\n";
+          for (int d = 0; d < nd; ++d)
+            if (!Pd.count(d) && !R.count(d)) ev << "        const int x" << d << " = 0;\n";
+          done.assign(g.terms.size(), 0);
+          for (int r : topo)
+            if (in_nest[r] && cls[r] == 0) emit_rap(r, nv, ev, "        ", okk, "false");
+          for (int r : topo)
+            if (in_nest[r] && cls[r] == 1) emit_rap(r, nv, ev, "        ", okk, "ok");
+          for (size_t m = 0; m < reds.size(); ++m) {
+            const auto& rap = g.raps[reds[m]];
+            for (int i : elem_t[m]) {
+              const int t = rap.in_terms[i];
+              const int pr = g.producer[t];
+              if (pr >= 0 && g.raps[pr].kind == lf::RapKind::kernel && nest_of(pr) != nv && !done[t]) {
+                ev << "        const T v" << t << " = " << mat_index(t) << ";\n";
+                done[t] = 1;
+              }
+              ev << "        lf_t[buf][" << m << "][c][j] = v" << t << ";\n";
+            }
+          }
+          src << ev.str();
+        }
+        src << "      }\n";
+        src << "      __syncthreads();\n";
+        src << "      if (warp == 0) {\n";
+        src << "        const int cnt = (int)min((long long)" << EB << ", " << rcount << "LL - rb);\n";
+        src << "        #pragma unroll 16\n";
+        src << "        for (int e = 0; e < " << EB << "; ++e) {\n";
+        src << "          if (e >= cnt) break;\n";
+        for (size_t m = 0; m < reds.size(); ++m) {
+          const auto& rap = g.raps[reds[m]];
+          const auto& k = rs.kernels[rap.kernel];
+          std::map<std::string, std::string> pv;
+          for (size_t i = 0; i < k.inputs.size(); ++i) {
+            const bool is_elem = std::find(elem_t[m].begin(), elem_t[m].end(), (int)i) != elem_t[m].end();
+            pv[k.inputs[i].first] = is_elem ? "lf_t[buf][" + std::to_string(m) + "][lane][e]" : "acc" + std::to_string(m);
+          }
+          if (!emit_kernel(
+                  k, T, [&](const std::string& n) { return pv.at(n); },
+                  [&](const std::string&) { return "acc" + std::to_string(m); }, false, src, "          ", err))
+            return false;
+        }
+        src << "        }\n";
+        src << "      }\n";
+        src << "    }\n";
+        // warp 0: reduction outputs and the raps after them, per cell
+        src << "    if (warp == 0 && cb + lane < " << pcells << "LL) {\n";
+        cell_coords(src, "cb + lane", "      ");
+        for (int d = 0; d < nd; ++d)
+          if (!Pd.count(d)) src << "      const int x" << d << " = 0;\n";
+        done.assign(g.terms.size(), 0);
+        for (int r : topo)
+          if (in_nest[r] && cls[r] == 0) emit_rap(r, nv, src, "      ", okk, "false");
+        for (size_t m = 0; m < reds.size(); ++m) {
+          const int ot = g.raps[reds[m]].out_terms[0];
+          src << "      const T v" << ot << " = acc" << m << ";\n";
+          done[ot] = 1;
+          if (term_mat[ot]) src << "      " << mat_index(ot) << " = v" << ot << ";\n";
+        }
+        for (int r : topo)
+          if (in_nest[r] && cls[r] == 3) emit_rap(r, nv, src, "      ", okk, "");
+        src << "    }\n";
+        src << "    __syncthreads();\n";
+        src << "  }\n}\n";
+        if (!okk) return false;
+        out.nest_kernels.push_back(nl);
+        continue;
+      }
       src << "extern \"C\" __global__ void __launch_bounds__(256) " << fn << "(const LfArgs a) {\n";
       pointers(src);
-      src << "  __shared__ T lf_red[8][" << LFB << "][" << reds.size() << "][32];\n";
+      src << "  __shared__ T lf_red[8][" << 2 * LFB << "][" << reds.size() << "][32];\n";
       src << "  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;\n";
       src << "  for (long long pc = blockIdx.x * 8LL + warp; pc < " << pcells << "LL; pc += gridDim.x * 8LL) {\n";
       src << "    long long rem = pc;\n";
@@ -2098,32 +2244,58 @@ bool emit_nests(const lf::Plan& P, const std::string& sources, JitProgram& out, 
             stage << "      const T v" << t << " = " << mat_index(t) << ";\n";
             done[t] = 1;
           }
-          stage << "      lf_red[warp][LFBUF][" << m << "][lane] = v" << t << ";\n";
+          stage << "      ev" << "LFBUF_" << m << " = v" << t << ";\n";
           elem_in[m].push_back(static_cast<int>(i));
         }
       }
       const std::string stage_text = stage.str();
-      src << "    for (long long rb0 = 0; rb0 < " << rcount << "LL; rb0 += " << 32 * LFB << ") {\n";
-      for (int h = 0; h < LFB; ++h) {
-        std::string t = stage_text;
-        for (size_t pos; (pos = t.find("LFBUF")) != std::string::npos;) t.replace(pos, 5, std::to_string(h));
-        src << "      if (rb0 + " << 32 * h << " < " << rcount << "LL) {\n";
-        src << "      const long long rb = rb0 + " << 32 * h << ";\n";
-        src << t;
-        src << "      }\n";
-      }
+      // software pipeline over groups of LFB blocks: the element code (global
+      // loads) of group i+1 is issued before group i is accumulated and its
+      // values stored to the other half of the buffer after it, so the loads
+      // are in flight during the ordered chain
+      auto stage_group = [&](const std::string& base) {
+        for (int h = 0; h < LFB; ++h) {
+          std::string t = stage_text;
+          for (size_t pos; (pos = t.find("LFBUF")) != std::string::npos;) t.replace(pos, 5, std::to_string(h));
+          src << "      if (" << base << " + " << 32 * h << " < " << rcount << "LL) {\n";
+          src << "      const long long rb = " << base << " + " << 32 * h << ";\n";
+          src << t;
+          src << "      }\n";
+        }
+      };
+      auto store_group = [&](const std::string& half) {
+        for (int h = 0; h < LFB; ++h)
+          for (size_t m = 0; m < reds.size(); ++m)
+            src << "      lf_red[warp][" << half << " + " << h << "][" << m << "][lane] = ev" << h << "_" << m << ";\n";
+      };
+      auto declare_ev = [&]() {
+        for (int h = 0; h < LFB; ++h)
+          for (size_t m = 0; m < reds.size(); ++m) src << "      T ev" << h << "_" << m << " = T(0);\n";
+      };
+      src << "    {\n";
+      declare_ev();
+      stage_group("0LL");
+      store_group("0");
+      src << "    }\n";
+      src << "    for (long long rb0 = 0, it = 0; rb0 < " << rcount << "LL; rb0 += " << 32 * LFB << ", ++it) {\n";
+      src << "      const int cur = (int)(it & 1) * " << LFB << ", nxt = " << LFB << " - cur;\n";
       src << "      __syncwarp();\n";
+      declare_ev();
+      stage_group("rb0 + " + std::to_string(32 * LFB));
       src << "      for (int h = 0; h < " << LFB << "; ++h) {\n";
       src << "      const long long rb = rb0 + 32 * h;\n";
       src << "      const int cnt = (int)max(0LL, min(32LL, " << rcount << "LL - rb));\n";
-      src << "      for (int e = 0; e < cnt; ++e) {\n";
+      // full blocks unrolled
+      src << "      #pragma unroll 32\n";
+      src << "      for (int e = 0; e < 32; ++e) {\n";
+      src << "        if (e >= cnt) break;\n";
       for (size_t m = 0; m < reds.size(); ++m) {
         const auto& rap = g.raps[reds[m]];
         const auto& k = rs.kernels[rap.kernel];
         std::map<std::string, std::string> pv;
         for (size_t i = 0; i < k.inputs.size(); ++i) {
           const bool is_elem = std::find(elem_in[m].begin(), elem_in[m].end(), (int)i) != elem_in[m].end();
-          pv[k.inputs[i].first] = is_elem ? "lf_red[warp][h][" + std::to_string(m) + "][e]" : "acc" + std::to_string(m);
+          pv[k.inputs[i].first] = is_elem ? "lf_red[warp][cur + h][" + std::to_string(m) + "][e]" : "acc" + std::to_string(m);
         }
         if (!emit_kernel(
                 k, T, [&](const std::string& n) { return pv.at(n); },
@@ -2133,6 +2305,7 @@ bool emit_nests(const lf::Plan& P, const std::string& sources, JitProgram& out, 
       src << "      }\n";
       src << "      }\n";
       src << "      __syncwarp();\n";
+      store_group("nxt");
       src << "    }\n";
       // reduction outputs, post raps, P-level stores (lane 0 writes)
       for (size_t m = 0; m < reds.size(); ++m) {

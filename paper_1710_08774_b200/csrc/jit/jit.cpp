@@ -346,7 +346,7 @@ int JitKernel::run_nests(const ExecArgs& a, std::string& err) {
     for (size_t m = 0; m < mats_.size(); ++m) args.t[T.size() + m] = mats_[m];
     for (size_t k = 0; k < prog_.nest_kernels.size(); ++k) {
       const auto& nk = prog_.nest_kernels[k];
-      const long long per_cta = nk.reduction ? 8 : 256;
+      const long long per_cta = nk.cells_per_cta > 0 ? nk.cells_per_cta : (nk.reduction ? 8 : 256);
       const long long want = (nk.units + per_cta - 1) / per_cta;
       const unsigned ctas = static_cast<unsigned>(std::max<long long>(1, std::min<long long>(want, 32LL * sms)));
       int st = launch(nest_fns_[k], dim3(ctas), dim3(256), 0, a.stream, &args, err);

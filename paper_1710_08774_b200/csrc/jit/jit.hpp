@@ -18,6 +18,7 @@ struct NestLaunch {
   std::string fn;          // kernel name
   bool reduction = false;  // warp per parallel cell (true) or thread per cell
   long long units = 0;     // parallel cells
+  int cells_per_cta = 0;   // reduction kernels: parallel cells a CTA owns (0: one per warp, 8)
 };
 
 // streamed axioms the warp-specialised march can fetch by TMA (tensor maps

@@ -217,3 +217,18 @@ def test_fault_injection_corrupted_span_is_caught(monkeypatch):
     assert diff.size > 0, "a corrupted rotation span went unnoticed"
     witness = tuple(int(x) for x in diff[0])
     assert 2 <= witness[0] < shape[0] + 2  # a trip (row) of the interior
+
+
+@pytest.mark.parametrize("name", ["normalization_body", "colsum_body"])
+def test_transposed_reduction_nests(name):
+    """LF_JIT_RED_TILED=1 (opt-in): reduction nests with one ordered chain per
+    lane (32 parallel cells per CTA, element operands evaluated by the whole
+    CTA into a double-buffered tile) -- bit-exact as the warp-per-cell kernel."""
+    with lf.option("LF_JIT_RED_TILED", 1):
+        plan = lf.Plan.from_file(SPECS / f"{name}.lf")
+    assert "lf_t[buf]" in plan.source
+    ax = CASES[name]()
+    got = run_device(plan, [ax[t.name] for t in plan.axioms], 1)
+    ref = generic.run_naive(SPECS / f"{name}.lf", ax, steps=1)
+    for g, t in zip(got, plan.goals):
+        assert np.array_equal(bits(g), bits(ref[t.name])), t.name
