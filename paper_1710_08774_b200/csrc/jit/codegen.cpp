@@ -1620,7 +1620,9 @@ bool emit_fill(Ctx& C, JitProgram& out, std::ostream& fill) {
   const auto& terms = C.P.terminals;
   const int nd = C.nd;
   out.has_fill = false;
-  fill << "extern \"C\" __global__ void lf_jit_fill(const LfArgs a) {\n";
+  // the body as a device function: lf_jit_fill runs it alone, the in-place
+  // register march's commit kernel may run it after its own work
+  fill << "__device__ __forceinline__ void lf_fill_body(const LfArgs& a) {\n";
   fill << "  const long long N0 = a.n0;\n";
   for (const auto& [gname, aname] : rs.iterate) {
     int ti = -1;
@@ -1710,6 +1712,7 @@ bool emit_fill(Ctx& C, JitProgram& out, std::ostream& fill) {
     fill << "    }\n  }\n";
   }
   fill << "}\n";
+  fill << "extern \"C\" __global__ void lf_jit_fill(const LfArgs a) {\n  lf_fill_body(a);\n}\n";
   return true;
 }
 
@@ -2336,7 +2339,7 @@ using namespace cg;
 // dependents would take the slots of its later waves (normalization 117 ->
 // 110 G), and early-launched march CTAs behind a fill or capture cost the 3D
 // in-place chain 9 % (136 -> 124 G).  Inserted as each kernel's first statement.
-static std::string with_pdl(const std::string& src) {
+static std::string with_pdl(const std::string& src, std::string& err) {
   std::string out =
       "__device__ __forceinline__ void lf_pdl_wait() { asm volatile(\"griddepcontrol.wait;\" ::: \"memory\"); }\n"
       "__device__ __forceinline__ void lf_pdl() {\n"
@@ -2349,6 +2352,10 @@ static std::string with_pdl(const std::string& src) {
     if (k == std::string::npos) break;
     const size_t brace = src.find(") {\n", k);
     if (brace == std::string::npos) break;
+    if (src.find('\n', k) < brace) {  // every generated kernel opens its body at the end of its signature line
+      err = "internal error: generated kernel signature not followed by its body on the same line";
+      break;
+    }
     const bool march = src.substr(k, brace - k).find(" lf_jit_step") != std::string::npos;
     out += src.substr(pos, brace + 4 - pos);
     out += march ? "  lf_pdl();\n" : "  lf_pdl_wait();\n";
@@ -2382,8 +2389,13 @@ bool jit_generate(const lf::Plan& P, JitProgram& out, const std::string& sources
       out.error = C.error;
       return false;
     }
-    out.source = sources + with_pdl(src.str());
+    std::string perr;
+    out.source = sources + with_pdl(src.str(), perr);
     out.march = false;
+    if (!perr.empty()) {
+      out.error = perr;
+      return false;
+    }
     return true;
   }
   Ctx C(P);
@@ -2444,7 +2456,12 @@ bool jit_generate(const lf::Plan& P, JitProgram& out, const std::string& sources
       src << variants;
     }
   }
-  out.source = sources + with_pdl(src.str());
+  std::string perr;
+  out.source = sources + with_pdl(src.str(), perr);
+  if (!perr.empty()) {
+    out.error = perr;
+    return false;
+  }
   return true;
 }
 

@@ -73,7 +73,7 @@ Zone zone_of(const Ctx& C, size_t v, int ti, int eb) {
 // chunk boundaries, domain columns) and the column bands (around the internal
 // tile boundaries of width `tile1`, rows outside every row band)
 void emit_commit2(Ctx& C, const char* name, const std::vector<std::pair<size_t, int>>& caps,
-                  const std::vector<int>& slots, int tile1, std::ostream& src) {
+                  const std::vector<int>& slots, int tile1, std::ostream& src, bool with_fill) {
   // flat over the band cells -- (band row, domain column) pairs, then (band
   // column, row) pairs -- four per thread, a block per 1024; the launch covers
   // the largest band set (jit.cpp)
@@ -112,6 +112,8 @@ void emit_commit2(Ctx& C, const char* name, const std::vector<std::pair<size_t, 
         << plus(so0) << "];\n";
     src << "      }\n    }\n  }\n";
   }
+  // the ghost refill too (zero boundaries only: it reads no cell the commit writes)
+  if (with_fill) src << "  lf_fill_body(a);\n";
   src << "}\n";
 }
 
@@ -852,7 +854,18 @@ void RMarch::commit() {
       caps.push_back({ip.v, ip.gi});
       slots.push_back(ip.slot);
     }
-    emit_commit2(C, "lf_jit_commit_rm", caps, slots, static_cast<int>(T1), src);
+    emit_commit2(C, "lf_jit_commit_rm", caps, slots, static_cast<int>(T1), src, false);
+    // commit + ghost refill in one launch where the refill reads nothing (every
+    // iterated goal with zero boundaries, or none)
+    bool fill_reads = false;
+    for (const auto& it_pair : C.P.rs.iterate) {
+      auto it = C.P.rs.boundary.find(it_pair.first);
+      if (it == C.P.rs.boundary.end()) it = C.P.rs.boundary.find("*");
+      if (it != C.P.rs.boundary.end())
+        for (auto m : it->second) fill_reads |= m != lf::Boundary::zero && m != lf::Boundary::none;
+    }
+    if (out.has_fill && !fill_reads)
+      emit_commit2(C, "lf_jit_commit_fill_rm", caps, slots, static_cast<int>(T1), src, true);
   }
 }
 

@@ -221,6 +221,11 @@ int JitKernel::run_inplace(const ExecArgs& a, JitArgs& args, std::string& err) {
       for (int s = 0; s < a.steps; ++s) {
         st = launch(step_rm_, grid, dim3(prog_.rm_threads), prog_.rm_smem_bytes, a.stream, &args, err, &maps);
         if (st != LF_OK) return st;
+        if (commit_fill_rm_ && fill_ && prog_.has_fill) {  // commit and ghost refill in one launch
+          st = launch(commit_fill_rm_, dim3(std::max(commit_blocks, 592u)), dim3(256), 0, a.stream, &args, err);
+          if (st != LF_OK) return st;
+          continue;
+        }
         st = launch(commit_rm_, dim3(commit_blocks), dim3(256), 0, a.stream, &args, err);
         if (st != LF_OK) return st;
         if (fill_ && prog_.has_fill) {
@@ -480,6 +485,7 @@ int JitKernel::run(const ExecArgs& a, std::string& err) {
     if (d.get(&f, m, "lf_jit_fill") == CUDA_SUCCESS) fill_ = f;
     if (d.get(&f, m, "lf_jit_capture") == CUDA_SUCCESS) capture_ = f;
     if (d.get(&f, m, "lf_jit_commit_rm") == CUDA_SUCCESS) commit_rm_ = f;
+    if (d.get(&f, m, "lf_jit_commit_fill_rm") == CUDA_SUCCESS) commit_fill_rm_ = f;
     if (d.get(&f, m, "lf_jit_commit_ws") == CUDA_SUCCESS) commit_ws_ = f;
     if (!prog_.nest_kernels.empty()) {
       for (const auto& nk : prog_.nest_kernels) {

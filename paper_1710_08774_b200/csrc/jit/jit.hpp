@@ -136,6 +136,7 @@ class JitKernel {
   bool tma_maps(const std::vector<JitProgram::Tma>& list, const std::vector<void*>& bufs, long rows, JitMaps& maps,
                 long boundaries = 0);
   void* commit_rm_ = nullptr;  // in-place register march: deferred boundary writes into the grid
+  void* commit_fill_rm_ = nullptr;  // the same plus the ghost refill (zero boundaries)
   void* commit_ws_ = nullptr;  // in-place 3D warp-specialised march: the same
   int bands_for(const std::vector<JitProgram::Inplace>& list, long nch, long nt_of_tile1, std::string& err);
   long plan_rows_ = 0;  // trips of the outermost loop dimension (whole domain)

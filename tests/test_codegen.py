@@ -101,3 +101,20 @@ def test_switches_set_in_process_override_the_environment(monkeypatch):
     import pytest
     with pytest.raises(lf.LoomfuseError):
         lf.set_option("PATH", "x")
+
+
+def test_every_generated_kernel_waits_for_the_previous_grid():
+    """Launched with programmatic stream serialization, every generated kernel
+    must start with griddepcontrol.wait (lf_pdl / lf_pdl_wait) before touching
+    memory -- the ghost fill, the in-place commit kernels and the nest kernels
+    included."""
+    import re
+    for name in ("heat3d_body", "biharm_body", "biharm_inplace", "heat3d_inplace", "normalization_body",
+                 "colsum_body", "box_body", "multi_body"):
+        path = SPECS / f"{name}.lf"
+        if not path.exists():
+            path = lf.SPEC_DIR / "examples" / f"{name}.lf"
+        src = lf.Plan.from_file(path).source
+        kernels = re.findall(r'__global__ void[^\n]*\) \{\n([^\n]*)\n', src)
+        assert kernels and len(kernels) == src.count("__global__ void"), name
+        assert all(k.strip() in ("lf_pdl();", "lf_pdl_wait();") for k in kernels), (name, kernels)
