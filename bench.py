@@ -99,6 +99,13 @@ WORKLOADS = {
     # MAX reduction per step fused into the executor (+ an all-reduce per step on N GPUs)
     "hydro_large_adaptive": dict(config_index=None, spec="hydro2d_adaptive", sizes=(32768, 32768), chain_steps=10,
                                  gen=_hydro_inputs, slab=_hydro_slab, dtype="f64", halo=(2, 2, False)),
+    # configs[2] / configs[4] in place (config.aliases declared for every iterate pair,
+    # goals passed on their axioms' buffers): one copy of the state instead of three
+    "hydro_inplace": dict(config_index=2, spec="hydro2d", sizes=(4096, 4096), chain_steps=20, gen=_hydro_inputs,
+                          slab=None, dtype="f64", halo=(2, 2, False), inplace=True, alias=True),
+    "hydro_large_inplace": dict(config_index=4, spec="hydro2d", sizes=(32768, 32768), chain_steps=10,
+                                gen=_hydro_inputs, slab=None, dtype="f64", halo=(2, 2, False), inplace=True,
+                                alias=True),
     # the same chains written with `body:` expressions: the generic NVRTC path
     "heat3d_jit": dict(config_index=1, spec="examples/heat3d_body", sizes=(512, 512, 512), chain_steps=50,
                        gen=_heat3d_inputs, slab=_heat3d_slab, dtype="f64", halo=(1, 1, True)),
@@ -450,7 +457,7 @@ def main():
         torch.cuda.set_device(0)
     dev = torch.device("cuda", torch.cuda.current_device())
 
-    plan = lf.Plan.with_ranges(w["spec"], w["sizes"])
+    plan = lf.Plan.with_ranges(w["spec"], w["sizes"], inplace=bool(w.get("alias")))
     if not plan.executor:
         raise SystemExit(f"no fused executor for {w['spec']}: run lf_run to see why")
     nax = len(plan.axioms)

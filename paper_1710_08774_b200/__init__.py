@@ -200,9 +200,11 @@ class Plan:
         return cls.from_file(spec_path(name))
 
     @classmethod
-    def with_ranges(cls, name: str, sizes: Sequence[int]) -> "Plan":
-        """A bundled spec with its `ranges:` replaced by [0, n) per loop dim."""
-        return cls(set_ranges(spec_path(name).read_text(), sizes), str(spec_path(name)))
+    def with_ranges(cls, name: str, sizes: Sequence[int], inplace: bool = False) -> "Plan":
+        """A bundled spec with its `ranges:` replaced by [0, n) per loop dim;
+        `inplace` also declares every iterate pair in `config.aliases`."""
+        text = set_ranges(spec_path(name).read_text(), sizes)
+        return cls(alias_iterates(text) if inplace else text, str(spec_path(name)))
 
     def __del__(self):
         h = getattr(self, "_h", None)
@@ -475,5 +477,24 @@ def set_ranges(text: str, sizes: Sequence[int]) -> str:
     return "\n".join(out) + "\n"
 
 
-__all__ = ["Plan", "Terminal", "LoomfuseError", "lib", "spec_path", "set_ranges", "print_spec", "ABI_SYMBOLS",
+def alias_iterates(text: str) -> str:
+    """Declare every `iterate: [[goal, axiom], ...]` pair of a rule file as an
+    in-place alias (`aliases: [[axiom, goal], ...]`, the reference's
+    config.aliases): goal and axiom may then be passed on one buffer."""
+    out = []
+    for ln in text.splitlines():
+        s = ln.strip()
+        if s.startswith("aliases:"):
+            raise ValueError("the spec already declares aliases")
+        out.append(ln)
+        if s.startswith("iterate:"):
+            pairs = [p.split(",") for p in s.split(":", 1)[1].strip()[2:-2].split("], [")]
+            if any(len(p) != 2 for p in pairs):
+                raise ValueError("iterate: must be a flow sequence of [goal, axiom] pairs on one line")
+            ind = ln[:len(ln) - len(ln.lstrip())]
+            out.append(ind + "aliases: [" + ", ".join(f"[{a.strip()}, {g.strip()}]" for g, a in pairs) + "]")
+    return "\n".join(out) + "\n"
+
+
+__all__ = ["Plan", "Terminal", "LoomfuseError", "lib", "spec_path", "set_ranges", "alias_iterates", "print_spec", "ABI_SYMBOLS",
            "set_option", "option"]

@@ -67,6 +67,7 @@ struct lf_plan {
   std::mutex mu;            // guards the device caches below
   std::vector<void*> dev;   // lf_run_host device terminals
   std::vector<void*> scratch;  // per goal; iterated goals only
+  lfx::ExecMem exec_mem;       // the built-in executor's own buffers (in-place bands)
   cudaStream_t stream = nullptr;
   cudaStream_t h2d = nullptr, d2h = nullptr;  // copy streams of the pipelined host path
   cudaStream_t comm = nullptr;                // halo-exchange stream of lf_run_slabs
@@ -653,6 +654,41 @@ static bool shares_buffer(const lf_plan* plan, void* const* terms) {
   return false;
 }
 
+// In-place run of a built-in executor: every iterated full-rank goal sits on
+// its axiom's buffer, the pair is declared in config.aliases (the reference's
+// contract for in-place updates, storage.cpp:453-524), and nothing else is
+// shared.  `share[g]` = axiom index for such goals.
+static int exec_inplace_pairs(const lf_plan* plan, void* const* terms, std::vector<int>& share, std::string& err) {
+  const auto& T = plan->plan.terminals;
+  const auto& rs = plan->plan.rs;
+  share.assign(T.size(), -1);
+  if (!plan->exec->inplace) {
+    err = std::string(plan->exec->name) +
+          " ping-pongs between distinct buffers; in-place runs (config.aliases) use the generic executor";
+    return LF_ERR_UNSUPPORTED;
+  }
+  for (size_t i = 0; i < T.size(); ++i)
+    for (size_t j = 0; j < T.size(); ++j) {
+      if (T[i].is_goal || !T[j].is_goal || !terms[i] || terms[i] != terms[j]) continue;
+      bool iterated = false, declared = false;
+      for (const auto& [gname, aname] : rs.iterate) iterated |= gname == T[j].name && aname == T[i].name;
+      for (const auto& [in, out] : rs.aliases) declared |= in == T[i].name && out == T[j].name;
+      if (!iterated || !declared) {
+        err = "axiom '" + T[i].name + "' and goal '" + T[j].name + "' share one buffer but " +
+              (iterated ? "config.aliases does not declare them" : "are not an iterate pair");
+        return LF_ERR_UNSUPPORTED;
+      }
+      share[j] = static_cast<int>(i);
+    }
+  for (const auto& [gname, aname] : rs.iterate)
+    for (size_t j = 0; j < T.size(); ++j)
+      if (T[j].is_goal && T[j].name == gname && !T[j].dims.empty() && share[j] < 0) {
+        err = "in-place runs take every iterated goal on its axiom's buffer ('" + gname + "' has its own)";
+        return LF_ERR_UNSUPPORTED;
+      }
+  return LF_OK;
+}
+
 int lf_run(const lf_plan* cplan, void* const* terms, int nterm, int steps, void* cuda_stream) {
   try {
     g_err.clear();
@@ -662,10 +698,10 @@ int lf_run(const lf_plan* cplan, void* const* terms, int nterm, int steps, void*
     std::lock_guard<std::mutex> lk(plan->mu);
     std::string err;
     const bool inplace = shares_buffer(plan, terms);
-    if (inplace && plan->exec)
-      return fail(LF_ERR_UNSUPPORTED, std::string(plan->exec->name) +
-                                          " ping-pongs between distinct buffers; in-place runs (config.aliases) "
-                                          "use the generic executor");
+    if (inplace && plan->exec) {
+      std::vector<int> share;
+      if ((st = exec_inplace_pairs(plan, terms, share, err)) != LF_OK) return fail(st, err);
+    }
     std::vector<void*> scratch;
     if (steps > 1 && !inplace) {
       if ((st = ensure_scratch(plan, err)) != LF_OK) return fail(st, err);
@@ -677,6 +713,8 @@ int lf_run(const lf_plan* cplan, void* const* terms, int nterm, int steps, void*
     a.steps = steps;
     a.stream = static_cast<cudaStream_t>(cuda_stream);
     a.scratch = scratch.data();
+    a.inplace = inplace && plan->exec;
+    a.mem = &plan->exec_mem;
     st = plan->exec ? plan->exec->run(a, err) : plan->jit->run(a, err);
     if (st != LF_OK) return fail(st, err);
     return LF_OK;
@@ -921,6 +959,8 @@ int lf_run_host(const lf_plan* cplan, void* const* terms, int nterm, int steps) 
     if (plan->jit)
       for (const auto& q : plan->jit->program().inplace)
         if (terms[q.ai] && terms[q.ai] == terms[q.gi]) share[q.gi] = q.ai;
+    if (plan->exec && shares_buffer(plan, terms))
+      if ((st = exec_inplace_pairs(plan, terms, share, err)) != LF_OK) return fail(st, err);
     bool inplace = false;
     for (int s2 : share) inplace |= s2 >= 0;
     if (plan->dev.size() != T.size()) plan->dev.assign(T.size(), nullptr);
@@ -962,6 +1002,8 @@ int lf_run_host(const lf_plan* cplan, void* const* terms, int nterm, int steps) 
     a.steps = steps;
     a.stream = plan->stream;
     a.scratch = scratch.data();
+    a.inplace = inplace && plan->exec;
+    a.mem = &plan->exec_mem;
     st = plan->exec ? plan->exec->run(a, err) : plan->jit->run(a, err);
     if (st != LF_OK) return fail(st, err);
     for (size_t i = 0; i < T.size(); ++i) {

@@ -23,6 +23,25 @@ const char* option(const char* name);
 // clear: drop the override (the environment applies again)
 int set_option(const char* name, const char* value, int clear);
 
+// Plan-owned device memory an executor may keep between runs (grow-only; the
+// caller holds the plan lock; freed with the plan).
+struct ExecMem {
+  void* ptr = nullptr;
+  size_t bytes = 0;
+  cudaError_t ensure(size_t need) {
+    if (need <= bytes) return cudaSuccess;
+    if (ptr) cudaFree(ptr);
+    ptr = nullptr;
+    bytes = 0;
+    cudaError_t e = cudaMalloc(&ptr, need);
+    if (e == cudaSuccess) bytes = need;
+    return e;
+  }
+  ~ExecMem() {
+    if (ptr) cudaFree(ptr);
+  }
+};
+
 struct ExecArgs {
   const lf::Plan* plan = nullptr;
   void* const* terms = nullptr;  // device pointers, axioms then goals
@@ -34,6 +53,10 @@ struct ExecArgs {
   // max_reduce executors under a slab driver: the rank-0 iterated axioms hold
   // the previous step's (combined) raw maxima, not final values
   bool raw_max_input = false;
+  // every iterated goal shares its axiom's buffer (config.aliases): run in
+  // place on that one buffer; only executors with `inplace` set are asked to
+  bool inplace = false;
+  ExecMem* mem = nullptr;  // set with `inplace`
 };
 
 struct Executor {
@@ -54,6 +77,9 @@ struct Executor {
   // maximum into the goal's value; a whole-domain run() does all of it itself
   bool max_reduce = false;
   int (*finalize)(const ExecArgs&, std::string& err) = nullptr;
+  // runs whole-domain steps in place when every iterated goal is passed on
+  // its aliased axiom's buffer (ExecArgs::inplace)
+  bool inplace = false;
 };
 
 // all executors compiled into this library

@@ -130,6 +130,10 @@ struct Params {
   int dtdx_is_max;       // adaptive steps after the first: dt/dx = CFL / *dtdx
   unsigned long long* cfl_acc;  // adaptive: this step's CFL maximum (double bits, atomicMax; zeroed by the host)
   double* out[4];
+  // in place (out == the staged arrays): cells another CTA still reads are
+  // deferred to these bands and copied in by hydro_commit after the step
+  double* colband;  // [4][strips-1][nj][4]: the two columns either side of every strip boundary
+  double* rowband;  // [ctas][3 segments][4 rows][4][W]: the two rows either side of every segment cut
 };
 
 struct Maps {
@@ -170,8 +174,52 @@ __device__ __forceinline__ void store_cell(const Params& p, int j, int i, const 
   }
 }
 
+// ---- in place (config.aliases: every goal on its axiom's buffer; storage.cpp:453-594)
+// A CTA reads its strip's columns i0-2 .. i0+W+1 of rows jb-2 .. je+1 and writes
+// row j only after it has consumed row j+3, so its own reads are never
+// overtaken.  What OTHER CTAs read of its cells are the two columns next to a
+// strip boundary (the neighbour strip's halo) and the two rows next to a
+// segment cut (the halo rows of the segment above / below in the same strip).
+// Those cells -- with their reflective ghost images -- are written to band
+// buffers instead and copied in by hydro_commit once every CTA of the step has
+// finished reading: the shadow-window rule of the reference's alias analysis
+// applied to the executor's own decomposition.
+// slot 0..3 of row j in its segment's row band (-1: not deferred)
+__device__ __forceinline__ int band_row_slot(int j, int jb, int je, bool cut_above, bool cut_below) {
+  if (cut_above && j - jb < H) return j - jb;
+  if (cut_below && je - j <= H) return H + (j - (je - H));
+  return -1;
+}
+__device__ __forceinline__ double* rowband_at(const Params& p, int cta, int k, int slot, int t) {
+  return p.rowband + ((size_t)(cta * 3 + k) * 4 + slot) * 4 * W + t;
+}
+__device__ __forceinline__ double* colband_at(const Params& p, int edge, int j, int c4) {
+  return p.colband + ((size_t)edge * p.nj + j) * 4 + c4;
+}
+
+// a deferred cell into its band: row slot `rs` of segment `seg` (>= 0), else
+// column `c4` of strip boundary `edge`; out of line (a few cells per row) and
+// with 32-bit offsets (checked on the host)
+__device__ __noinline__ void store_band(const Params& p, int seg, int rs, int edge, int c4, int t, int jo, double o0,
+                                        double o1, double o2, double o3) {
+  double* b;
+  unsigned stride;
+  if (rs >= 0) {
+    b = p.rowband + (unsigned)((seg * 4 + rs) * 4 * W + t);
+    stride = W;
+  } else {
+    b = p.colband + ((unsigned)(edge * p.nj + jo) * 4u + (unsigned)c4);
+    stride = (unsigned)(p.strips - 1) * (unsigned)p.nj * 4u;
+  }
+  b[0] = o0;
+  b[stride] = o1;
+  b[(size_t)2 * stride] = o2;
+  b[(size_t)3 * stride] = o3;
+}
+
 // ADAPT: also reduce the CFL speed of every stored cell (specs/hydro2d_adaptive.lf)
-template <int MINB, bool ADAPT = false>
+// INPLACE: the goals are the staged arrays themselves (see above)
+template <int MINB, bool ADAPT = false, bool INPLACE = false>
 __global__ void __launch_bounds__(NT, MINB) hydro_fused(const __grid_constant__ Maps maps, const Params p) {
   extern __shared__ __align__(128) unsigned char smem[];
   unsigned char* ring = smem;
@@ -337,7 +385,20 @@ __global__ void __launch_bounds__(NT, MINB) hydro_fused(const __grid_constant__ 
             const double* u1c = u1ring + (tt % 3) * 4 * NT + t;
             hy_update(u1c[0], u1c[2 * NT], u1c[NT], u1c[3 * NT], yfp[0], yfp[1], yfp[2], yfp[3], f[0], f[1], f[2], f[3],
                       dtdx, &o[0], &o[2], &o[1], &o[3]);
-            store_cell(p, sg.jb - 2 + tt - 3, i0 + t, o);
+            const int jo = sg.jb - 2 + tt - 3;
+            if constexpr (INPLACE) {
+              // 32-bit band offsets (checked on the host): one store sequence for both bands
+              const int rs = band_row_slot(jo, sg.jb, sg.je, sg.jb > p.row_lo, sg.je < p.row_hi);
+              const bool cl = t < H && sg.strip > 0, cr = t >= W - H && sg.strip < p.strips - 1;
+              if (rs >= 0 || cl || cr) {
+                store_band(p, blockIdx.x * 3 + k, rs, cl ? sg.strip - 1 : sg.strip, cl ? H + t : t - (W - H), t, jo,
+                           o[0], o[1], o[2], o[3]);
+              } else {
+                store_cell(p, jo, i0 + t, o);
+              }
+            } else {
+              store_cell(p, jo, i0 + t, o);
+            }
             if constexpr (ADAPT) {
               double sp;
               unsigned bs = p.force_slow;
@@ -411,6 +472,44 @@ __global__ void __launch_bounds__(NT, MINB) hydro_fused(const __grid_constant__ 
   }
 }
 
+// In-place step, second launch: the deferred cells (and their ghost images)
+// go to their places.  Same grid and segment list as the step's launch.
+__global__ void __launch_bounds__(NT) hydro_commit(const Params p) {
+  const int t = threadIdx.x;
+  if (t == 0) pdl_trigger();
+  pdl_wait();  // every CTA of the step has finished reading the arrays
+  RowSeg seg[3];
+  const int nseg = cta_segments(blockIdx.x, gridDim.x, p.strips, p.row_lo, p.row_hi, seg);
+  const size_t cstride = (size_t)(p.strips - 1) * p.nj * 4;
+  for (int k = 0; k < nseg; ++k) {
+    const RowSeg sg = seg[k];
+    const int i0 = sg.strip * W;
+    const int ncell = min(W, p.ni - i0);
+    const bool above = sg.jb > p.row_lo, below = sg.je < p.row_hi;
+    for (int rs = 0; rs < 2 * H; ++rs) {
+      const int j = rs < H ? sg.jb + rs : sg.je - 2 * H + rs;
+      if (j < sg.jb || j >= sg.je || band_row_slot(j, sg.jb, sg.je, above, below) != rs) continue;
+      if (t < ncell) {
+        const double* b = rowband_at(p, blockIdx.x, k, rs, t);
+        const double v[4] = {b[0], b[W], b[2 * W], b[3 * W]};
+        store_cell(p, j, i0 + t, v);
+      }
+    }
+    const bool left = sg.strip > 0, right = sg.strip < p.strips - 1;
+    if (!left && !right) continue;
+    const long long n = (long long)(sg.je - sg.jb) * 4;
+    for (long long idx = t; idx < n; idx += NT) {
+      const int j = sg.jb + (int)(idx >> 2), q = (int)(idx & 3);
+      if (q < H ? !left : !right) continue;
+      if (band_row_slot(j, sg.jb, sg.je, above, below) >= 0) continue;
+      const int tc = q < H ? q : W - 2 * H + q;
+      const double* b = q < H ? colband_at(p, sg.strip - 1, j, H + q) : colband_at(p, sg.strip, j, q - H);
+      const double v[4] = {b[0], b[cstride], b[2 * cstride], b[3 * cstride]};
+      store_cell(p, j, i0 + tc, v);
+    }
+  }
+}
+
 bool supports(const lf::Plan& plan, std::string& why) {
   const auto& r = plan.rs.ranges;
   for (const auto& rg : r)
@@ -430,8 +529,18 @@ bool supports(const lf::Plan& plan, std::string& why) {
 // dt/dx from the CFL maximum in place (hy_cfl_dt): the chain's g_dtdx_n goal
 __global__ void cfl_finalize(double* slot) { hy_cfl_dt(*slot, slot); }
 
+// band buffers of an in-place run (see hydro_commit), sized for a launch of
+// `ctas` CTAs over `strips` strips of `nj` rows
+struct Bands {
+  double* col = nullptr;
+  double* row = nullptr;
+  static size_t col_doubles(int strips, int nj) { return (size_t)4 * std::max(0, strips - 1) * nj * 4; }
+  static size_t row_doubles(int ctas) { return (size_t)ctas * 3 * 4 * 4 * W; }
+};
+
 int launch_step(const double* const in[4], double* const out[4], const double* dtdx, int ni, const RowPart& rp,
-                cudaStream_t st, std::string& err, unsigned long long* cfl_acc = nullptr, bool dtdx_is_max = false) {
+                cudaStream_t st, std::string& err, unsigned long long* cfl_acc = nullptr, bool dtdx_is_max = false,
+                const Bands* bands = nullptr, int* ctas_out = nullptr) {
   const int nj = rp.rows;
   // LF_HYDRO_VARIANT: register budget for 2 / 3 (default) / 4 CTAs per SM.
   // With the branch-free divisions the Riemann phase keeps the fp64 pipe busy
@@ -442,11 +551,12 @@ int launch_step(const double* const in[4], double* const out[4], const double* d
     const int var = v ? std::atoi(v) : 1;
     return var == 0 ? hydro_fused<2> : (var == 2 ? hydro_fused<4> : hydro_fused<3>);
   }();
-  void (*const k)(Maps, Params) = cfl_acc ? hydro_fused<3, true> : kern;
-  static LaunchCache cache, cache_adapt;
+  const bool inplace = bands && bands->row;
+  void (*const k)(Maps, Params) = inplace ? hydro_fused<3, false, true> : (cfl_acc ? hydro_fused<3, true> : kern);
+  static LaunchCache cache, cache_adapt, cache_inplace;
   int slots = 0;
-  if (int s = resident_slots(cfl_acc ? cache_adapt : cache, reinterpret_cast<const void*>(k), NT, SMEM, 0,
-                             "cudaFuncSetAttribute(hydro)", &slots, err))
+  if (int s = resident_slots(inplace ? cache_inplace : (cfl_acc ? cache_adapt : cache),
+                             reinterpret_cast<const void*>(k), NT, SMEM, 0, "cudaFuncSetAttribute(hydro)", &slots, err))
     return s;
   Maps maps;
   uint64_t dims[2] = {(uint64_t)ni + 4, (uint64_t)nj + 4};
@@ -469,6 +579,8 @@ int launch_step(const double* const in[4], double* const out[4], const double* d
   const unsigned force_slow = lfx::option("LF_HYDRO_FORCE_SLOW") ? 1u : 0u;
   p.force_slow = force_slow;
   for (int a = 0; a < 4; ++a) p.out[a] = out[a];
+  p.colband = bands ? bands->col : nullptr;
+  p.rowband = bands ? bands->row : nullptr;
   const long long work = (long long)p.strips * (rp.hi - rp.lo);
   // each CTA must get at most 3 row segments (rowstream.cuh): at least
   // ceil(strips/2) CTAs when the row range is short
@@ -478,10 +590,74 @@ int launch_step(const double* const in[4], double* const out[4], const double* d
     err = "row range too short for the resident grid";
     return LF_ERR_UNSUPPORTED;
   }
-  return cuda_status(launch_pdl(k, dim3(ctas), dim3(NT), SMEM, st, maps, p), "hydro_fused launch", err);
+  if (ctas_out) {  // sizing query of an in-place run
+    *ctas_out = ctas;
+    return LF_OK;
+  }
+  if (!inplace) return cuda_status(launch_pdl(k, dim3(ctas), dim3(NT), SMEM, st, maps, p), "hydro_fused launch", err);
+  // LF_HYDRO_IP_PDL (tuning): bit 0 = the step, bit 1 = the commit launched with
+  // programmatic stream serialization
+  const char* o = lfx::option("LF_HYDRO_IP_PDL");
+  const int pdl = o ? std::atoi(o) : 0;
+  cudaError_t e;
+  if (pdl & 1) {
+    e = launch_pdl(k, dim3(ctas), dim3(NT), SMEM, st, maps, p);
+  } else {
+    k<<<ctas, NT, SMEM, st>>>(maps, p);
+    e = cudaGetLastError();
+  }
+  if (int s = cuda_status(e, "hydro_fused launch", err)) return s;
+  if (pdl & 2) {
+    e = launch_pdl(hydro_commit, dim3(ctas), dim3(NT), 0, st, p);
+  } else {
+    hydro_commit<<<ctas, NT, 0, st>>>(p);
+    e = cudaGetLastError();
+  }
+  return cuda_status(e, "hydro_commit launch", err);
+}
+
+// Whole-domain steps on ONE buffer per state array (the caller passed each
+// goal on its aliased axiom's buffer).  The bands are plan-owned: 4 columns per
+// strip boundary and 4 rows per segment cut, about 3 % of the state.
+int run_inplace(const ExecArgs& a, std::string& err) {
+  const auto& r = a.plan->rs.ranges;
+  const int ni = (int)r[1].trips();
+  if (a.slab) {
+    err = "in-place runs cover the whole domain (no slabs or row parts)";
+    return LF_ERR_UNSUPPORTED;
+  }
+  const RowPart rp = row_part(a, (int)r[0].trips());
+  double* u[4];
+  for (int v = 0; v < 4; ++v) u[v] = static_cast<double*>(a.terms[v]);
+  const double* dtdx = static_cast<const double*>(a.terms[4]);
+  Bands sizing;
+  sizing.row = reinterpret_cast<double*>(1);  // selects the in-place kernel for the occupancy query
+  int ctas = 0;
+  if (int s = launch_step(u, u, dtdx, ni, rp, a.stream, err, nullptr, false, &sizing, &ctas)) return s;
+  const int strips = (ni + W - 1) / W;
+  const size_t ncol = Bands::col_doubles(strips, rp.rows), nrow = Bands::row_doubles(ctas);
+  if (ncol >= (1ull << 31) || nrow >= (1ull << 31)) {  // the kernel forms band offsets in 32 bits
+    err = "grid too large for the in-place bands";
+    return LF_ERR_UNSUPPORTED;
+  }
+  if (!a.mem) {
+    err = "in-place run without plan-owned band memory";
+    return LF_ERR_INTERNAL;
+  }
+  cudaError_t e = a.mem->ensure((ncol + nrow) * sizeof(double));
+  if (e != cudaSuccess) return cuda_status(e, "cudaMalloc(hydro bands)", err);
+  double* mem = static_cast<double*>(a.mem->ptr);
+  Bands b;
+  b.col = mem;
+  b.row = mem + ncol;
+  int stt = LF_OK;
+  for (int s = 0; s < a.steps && stt == LF_OK; ++s)
+    stt = launch_step(u, u, dtdx, ni, rp, a.stream, err, nullptr, false, &b);
+  return stt;
 }
 
 int run(const ExecArgs& a, std::string& err) {
+  if (a.inplace) return run_inplace(a, err);
   const auto& r = a.plan->rs.ranges;
   const int ni = (int)r[1].trips();
   const RowPart rp = row_part(a, (int)r[0].trips());
@@ -552,7 +728,8 @@ int finalize_adaptive(const ExecArgs& a, std::string& err) {
 
 }  // namespace
 
-extern const Executor hydro_executor = {"hydro2d_fused_tma", "hydro2d.lf", 1, 64.0, supports, run};
+extern const Executor hydro_executor = {"hydro2d_fused_tma", "hydro2d.lf", 1, 64.0, supports, run,
+                                        nullptr, false, nullptr, /*inplace=*/true};
 extern const Executor hydro_adaptive_executor = {"hydro2d_adaptive_fused_tma", "hydro2d_adaptive.lf", 1, 64.0,
                                                  supports, run_adaptive, nullptr, true, finalize_adaptive};
 

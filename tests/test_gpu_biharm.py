@@ -54,6 +54,15 @@ def test_full_size_4096_matches_fused_cpu():
     assert np.array_equal(bits(got), bits(ref))
 
 
+def test_configs0_all_100_iterations_match_fused_cpu():
+    """BASELINE configs[0] as quoted: 4096 x 4096, all 100 iterations."""
+    plan = lf.Plan.bundled("biharmonic2d")
+    u = inputs.biharm_input(4096, 4096, seed=0)
+    got = run_device(plan, u, 100)
+    ref = oracle.biharm(u, 100, fused=True)
+    assert np.array_equal(bits(got), bits(ref))
+
+
 def test_slab_rows_leave_internal_ghosts_to_the_exchange():
     import torch
     shape = (24, 128)

@@ -93,6 +93,19 @@ def test_full_size_512_matches_fused_cpu_and_conserves_mass():
     assert interior(got).max() <= interior(u).max() and interior(got).min() >= interior(u).min()
 
 
+def test_configs1_all_50_steps_match_fused_cpu():
+    """BASELINE configs[1] as quoted: 512^3, all 50 steps."""
+    torch = _torch()
+    plan = lf.Plan.bundled("heat3d")
+    u = inputs.heat3d_input(512, 512, 512, seed=0)
+    du = torch.from_numpy(u).cuda()
+    out = torch.empty_like(du)
+    plan.run([du, out], steps=50)
+    torch.cuda.synchronize()
+    ref = oracle.heat3d(u, 50, fused=True)
+    assert np.array_equal(bits(interior(out.cpu().numpy())), bits(interior(ref)))
+
+
 def test_slab_mode_skips_k_wrap():
     torch = _torch()
     shape = (8, 16, 64)

@@ -61,6 +61,82 @@ def test_full_size_4096_matches_fused_cpu_and_conserves():
         assert got[v][2:-2, 2:-2].sum() == pytest.approx(st[v][2:-2, 2:-2].sum(), rel=1e-12)
 
 
+def test_configs2_all_20_steps_match_fused_cpu():
+    """BASELINE configs[2] as quoted: 4096 x 4096, all 20 steps."""
+    plan = lf.Plan.bundled("hydro2d")
+    st, dtdx = inputs.hydro_input(4096, 4096, seed=0)
+    got = run_device(plan, st, dtdx, 20)
+    ref = oracle.hydro(st, dtdx, 20, fused=True)
+    for v in range(4):
+        assert np.array_equal(bits(got[v]), bits(ref[v])), v
+
+
+def run_in_place(plan, st, dtdx, steps):
+    import torch
+    u = [torch.from_numpy(a).cuda() for a in st]
+    plan.run(u + [torch.tensor([dtdx], dtype=torch.float64, device="cuda")] + u, steps=steps)
+    torch.cuda.synchronize()
+    return [a.cpu().numpy() for a in u]
+
+
+# in place (config.aliases, SURVEY.md 8(f) rank 3): every goal on its axiom's
+# buffer -- half the device footprint; shapes with one and several strips,
+# segment cuts inside strips, strips of 2 and 124 cells, fewer rows than the
+# row-band depth
+@pytest.mark.parametrize("shape,steps", [((4, 4), 2), ((8, 16), 1), ((12, 20), 3), ((33, 130), 2), ((64, 256), 3),
+                                         ((130, 254), 2), ((5, 384), 4), ((700, 126), 2), ((257, 1000), 3)])
+def test_in_place_matches_naive(shape, steps):
+    plan = lf.Plan.with_ranges("hydro2d", shape, inplace=True)
+    assert plan.executor == "hydro2d_fused_tma"
+    st, dtdx = inputs.hydro_input(*shape, seed=shape[1] + 11)
+    got = run_in_place(plan, st, dtdx, steps)
+    ref = oracle.hydro(st, dtdx, steps)
+    for v in range(4):
+        assert np.array_equal(bits(got[v]), bits(ref[v])), (v, int(np.count_nonzero(got[v] != ref[v])))
+
+
+def test_in_place_full_size_4096_matches_fused_cpu():
+    plan = lf.Plan.with_ranges("hydro2d", (4096, 4096), inplace=True)
+    st, dtdx = inputs.hydro_input(4096, 4096, seed=0)
+    got = run_in_place(plan, st, dtdx, 3)
+    ref = oracle.hydro(st, dtdx, 3, fused=True)
+    for v in range(4):
+        assert np.array_equal(bits(got[v]), bits(ref[v])), v
+
+
+def test_in_place_host_path_keeps_one_device_buffer():
+    shape = (40, 200)
+    plan = lf.Plan.with_ranges("hydro2d", shape, inplace=True)
+    st, dtdx = inputs.hydro_input(*shape, seed=3)
+    u = [a.copy() for a in st]
+    plan.run_host(u + [np.array([dtdx])] + u, steps=3)
+    ref = oracle.hydro(st, dtdx, 3, fused=True)
+    for v in range(4):
+        assert np.array_equal(bits(u[v]), bits(ref[v]))
+
+
+def test_in_place_needs_declared_aliases_and_every_pair():
+    import torch
+    shape = (16, 128)
+    st, dtdx = inputs.hydro_input(*shape, seed=1)
+    u = [torch.from_numpy(a).cuda() for a in st]
+    d = [torch.tensor([dtdx], dtype=torch.float64, device="cuda")]
+    with pytest.raises(lf.LoomfuseError, match="config.aliases does not declare"):
+        lf.Plan.with_ranges("hydro2d", shape).run(u + d + u, steps=1)
+    plan = lf.Plan.with_ranges("hydro2d", shape, inplace=True)
+    with pytest.raises(lf.LoomfuseError, match="every iterated goal"):
+        plan.run(u + d + [u[0], u[1], u[2], torch.empty_like(u[3])], steps=1)
+    with pytest.raises(lf.LoomfuseError, match="not an iterate pair"):
+        plan.run(u + d + [u[1], u[0], u[2], u[3]], steps=1)
+    # distinct buffers still ping-pong on an alias-declaring plan
+    out = [torch.empty_like(a) for a in u]
+    plan.run(u + d + out, steps=2)
+    torch.cuda.synchronize()
+    ref = oracle.hydro(st, dtdx, 2)
+    for v in range(4):
+        assert np.array_equal(bits(out[v].cpu().numpy()), bits(ref[v]))
+
+
 def test_row_parts_compose_to_the_whole_slab():
     import torch
     shape = (40, 300)
