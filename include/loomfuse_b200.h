@@ -141,8 +141,9 @@ const char* lf_plan_source(const lf_plan* plan);
  * ping-pong between the goal buffer and a plan-owned scratch buffer, so the
  * axiom buffers are never written -- except in place: passing ONE buffer for
  * an axiom and its goal that `config: aliases:` declares runs the chain in
- * place on the generic executor (LF_ERR_UNSUPPORTED otherwise).  One
- * multi-step run per plan at a time. */
+ * place, on the generic executor or on the hand-written Hydro2D executor
+ * (which takes all four state pairs in place together); LF_ERR_UNSUPPORTED
+ * otherwise.  One multi-step run per plan at a time. */
 int lf_run(const lf_plan* plan, void* const* terminals, int nterm, int steps, void* cuda_stream);
 
 /* Same on HOST buffers: copies axioms host->device, runs, copies goals
