@@ -1909,7 +1909,10 @@ bool emit_nests(const lf::Plan& P, const std::string& sources, JitProgram& out, 
       if (P.terminals[ti].dims.empty() && rap.ext_slots.empty())
         o << ind << "const T v" << t << " = s" << ti << ";\n";
       else
-        o << ind << "const T v" << t << " = t" << ti << "[" << slot_index(ti, rap.ext_slots) << "];\n";
+        // axioms are read-only on the multi-nest path (no in-place runs here): the
+        // non-coherent load lets the compiler hoist the loads of an unrolled element
+        // loop above the materialising stores between them
+        o << ind << "const T v" << t << " = __ldg(&t" << ti << "[" << slot_index(ti, rap.ext_slots) << "]);\n";
       done[t] = 1;
     } else if (rap.kind == lf::RapKind::store) {
       const int ti = terminal_of(rap.external, true);
@@ -2074,14 +2077,22 @@ bool emit_nests(const lf::Plan& P, const std::string& sources, JitProgram& out, 
         // others evaluate tile k+1).  Consecutive threads take consecutive
         // elements when the innermost loop dimension is reduced (row sums),
         // consecutive cells otherwise (column sums): coalesced either way.
-        const int EB = 64;
+        // CPC cells per CTA: 8 or 16 while 32 would leave fewer than six CTAs per SM
+        // (8192 rows: 1024 CTAs of 8 rows) -- a filler warp keeps only a few loads
+        // in flight, so HBM bandwidth comes from resident CTAs; EB elements of each
+        // cell per tile.
+        // Warp 0 only accumulates (lane c < CPC owns cell c); warps 1..8 fill.
+        const int CPC = pcells < 16LL * 888 ? 8 : (pcells < 32LL * 888 ? 16 : 32);  // >= 6 CTAs per SM where the cells allow
+        const int EB = CPC == 32 ? 64 : 128;
         const bool elemfast = R.count(nd - 1) > 0;
-        nl.cells_per_cta = 32;
-        src << "extern \"C\" __global__ void __launch_bounds__(256) " << fn << "(const LfArgs a) {\n";
+        nl.cells_per_cta = CPC;
+        nl.threads = 288;
+        src << "extern \"C\" __global__ void __launch_bounds__(288) " << fn << "(const LfArgs a) {\n";
         pointers(src);
-        src << "  __shared__ T lf_t[2][" << reds.size() << "][32][" << EB + 1 << "];\n";
-        src << "  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;\n";
-        src << "  for (long long cb = blockIdx.x * 32LL; cb < " << pcells << "LL; cb += gridDim.x * 32LL) {\n";
+        src << "  __shared__ T lf_t[2][" << reds.size() << "][" << CPC << "][" << EB + 1 << "];\n";
+        src << "  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, tid = (int)threadIdx.x - 32;\n";
+        src << "  for (long long cb = blockIdx.x * " << CPC << "LL; cb < " << pcells << "LL; cb += gridDim.x * " << CPC
+            << "LL) {\n";
         // warp 0: carries of its cell
         for (size_t m = 0; m < reds.size(); ++m) src << "    T acc" << m << " = T(0);\n";
         auto cell_coords = [&](std::ostream& o, const std::string& pcexpr, const std::string& ind) {
@@ -2089,7 +2100,8 @@ bool emit_nests(const lf::Plan& P, const std::string& sources, JitProgram& out, 
           for (int d = nd - 1; d >= 0; --d)
             if (Pd.count(d)) o << ind << "const int x" << d << " = (int)(rem % " << N[d] << "); rem /= " << N[d] << ";\n";
         };
-        src << "    if (warp == 0 && cb + lane < " << pcells << "LL) {\n";
+        const std::string mine = "warp == 0 && lane < " + std::to_string(CPC) + " && cb + lane < " + std::to_string(pcells) + "LL";
+        src << "    if (" << mine << ") {\n";
         cell_coords(src, "cb + lane", "      ");
         for (int d = 0; d < nd; ++d)
           if (!Pd.count(d)) src << "      const int x" << d << " = 0;\n";
@@ -2108,11 +2120,20 @@ bool emit_nests(const lf::Plan& P, const std::string& sources, JitProgram& out, 
         src << "    }\n";
         src << "    for (long long rb = 0, kt = 0; rb < " << rcount << "LL; rb += " << EB << ", ++kt) {\n";
         src << "      const int buf = (int)(kt & 1);\n";
-        src << "      for (int q = tid; q < " << 32 * EB << "; q += 256) {\n";
-        src << "        const int c = " << (elemfast ? "q / " + std::to_string(EB) : "q & 31") << ", j = "
-            << (elemfast ? "q % " + std::to_string(EB) : "q >> 5") << ";\n";
-        src << "        const bool ok = cb + c < " << pcells << "LL && rb + j < " << rcount << "LL;\n";
-        {
+        src << "      if (warp > 0) {\n";
+        // Two unrolled passes over the thread's elements of the tile: the first
+        // only loads, evaluates and fills the shared tile -- no global store sits
+        // between its loads, so all of them (8 x the operands at EB = 64) are in
+        // flight together instead of one round trip per element; the second
+        // re-evaluates (the non-coherent loads are the first pass's: same
+        // addresses, the compiler keeps the values) and issues the stores of the
+        // variables materialised for later nests.
+        for (int pass = 0; pass < 2; ++pass) {
+          src << "      #pragma unroll\n";
+          src << "      for (int q = tid; q < " << CPC * EB << "; q += 256) {\n";
+          src << "        const int c = " << (elemfast ? "q / " + std::to_string(EB) : "q % " + std::to_string(CPC))
+              << ", j = " << (elemfast ? "q % " + std::to_string(EB) : "q / " + std::to_string(CPC)) << ";\n";
+          src << "        const bool ok = cb + c < " << pcells << "LL && rb + j < " << rcount << "LL;\n";
           std::ostringstream ev;
           cell_coords(ev, "ok ? cb + c : 0LL", "        ");
           ev << "        long long rr = ok ? rb + j : 0LL;\n";
@@ -2124,7 +2145,7 @@ bool emit_nests(const lf::Plan& P, const std::string& sources, JitProgram& out, 
           for (int r : topo)
             if (in_nest[r] && cls[r] == 0) emit_rap(r, nv, ev, "        ", okk, "false");
           for (int r : topo)
-            if (in_nest[r] && cls[r] == 1) emit_rap(r, nv, ev, "        ", okk, "ok");
+            if (in_nest[r] && cls[r] == 1) emit_rap(r, nv, ev, "        ", okk, pass == 0 ? "false" : "ok");
           for (size_t m = 0; m < reds.size(); ++m) {
             const auto& rap = g.raps[reds[m]];
             for (int i : elem_t[m]) {
@@ -2134,36 +2155,50 @@ bool emit_nests(const lf::Plan& P, const std::string& sources, JitProgram& out, 
                 ev << "        const T v" << t << " = " << mat_index(t) << ";\n";
                 done[t] = 1;
               }
-              ev << "        lf_t[buf][" << m << "][c][j] = v" << t << ";\n";
+              if (pass == 0) ev << "        lf_t[buf][" << m << "][c][j] = v" << t << ";\n";
             }
           }
           src << ev.str();
+          if (pass == 0) src << "      }\n";
         }
         src << "      }\n";
+        src << "      }\n";  // warp > 0
         src << "      __syncthreads();\n";
-        src << "      if (warp == 0) {\n";
+        src << "      if (warp == 0 && lane < " << CPC << ") {\n";
         src << "        const int cnt = (int)min((long long)" << EB << ", " << rcount << "LL - rb);\n";
-        src << "        #pragma unroll 16\n";
-        src << "        for (int e = 0; e < " << EB << "; ++e) {\n";
-        src << "          if (e >= cnt) break;\n";
-        for (size_t m = 0; m < reds.size(); ++m) {
-          const auto& rap = g.raps[reds[m]];
-          const auto& k = rs.kernels[rap.kernel];
-          std::map<std::string, std::string> pv;
-          for (size_t i = 0; i < k.inputs.size(); ++i) {
-            const bool is_elem = std::find(elem_t[m].begin(), elem_t[m].end(), (int)i) != elem_t[m].end();
-            pv[k.inputs[i].first] = is_elem ? "lf_t[buf][" + std::to_string(m) + "][lane][e]" : "acc" + std::to_string(m);
+        // full tiles: the element values are loaded from shared memory ahead of the
+        // ordered chain (no exit test between them), so the chain advances at the
+        // operation's own latency; the last, partial tile takes the counted loop
+        for (int full = 1; full >= 0; --full) {
+          if (full) {
+            src << "        if (cnt == " << EB << ") {\n";
+            src << "        #pragma unroll 32\n";
+            src << "        for (int e = 0; e < " << EB << "; ++e) {\n";
+          } else {
+            src << "        } else {\n";
+            src << "        for (int e = 0; e < cnt; ++e) {\n";
           }
-          if (!emit_kernel(
-                  k, T, [&](const std::string& n) { return pv.at(n); },
-                  [&](const std::string&) { return "acc" + std::to_string(m); }, false, src, "          ", err))
-            return false;
+          for (size_t m = 0; m < reds.size(); ++m) {
+            const auto& rap = g.raps[reds[m]];
+            const auto& k = rs.kernels[rap.kernel];
+            std::map<std::string, std::string> pv;
+            for (size_t i = 0; i < k.inputs.size(); ++i) {
+              const bool is_elem = std::find(elem_t[m].begin(), elem_t[m].end(), (int)i) != elem_t[m].end();
+              pv[k.inputs[i].first] =
+                  is_elem ? "lf_t[buf][" + std::to_string(m) + "][lane][e]" : "acc" + std::to_string(m);
+            }
+            if (!emit_kernel(
+                    k, T, [&](const std::string& n) { return pv.at(n); },
+                    [&](const std::string&) { return "acc" + std::to_string(m); }, false, src, "          ", err))
+              return false;
+          }
+          src << "        }\n";
         }
         src << "        }\n";
         src << "      }\n";
         src << "    }\n";
         // warp 0: reduction outputs and the raps after them, per cell
-        src << "    if (warp == 0 && cb + lane < " << pcells << "LL) {\n";
+        src << "    if (" << mine << ") {\n";
         cell_coords(src, "cb + lane", "      ");
         for (int d = 0; d < nd; ++d)
           if (!Pd.count(d)) src << "      const int x" << d << " = 0;\n";

@@ -354,7 +354,7 @@ int JitKernel::run_nests(const ExecArgs& a, std::string& err) {
       const long long per_cta = nk.cells_per_cta > 0 ? nk.cells_per_cta : (nk.reduction ? 8 : 256);
       const long long want = (nk.units + per_cta - 1) / per_cta;
       const unsigned ctas = static_cast<unsigned>(std::max<long long>(1, std::min<long long>(want, 32LL * sms)));
-      int st = launch(nest_fns_[k], dim3(ctas), dim3(256), 0, a.stream, &args, err);
+      int st = launch(nest_fns_[k], dim3(ctas), dim3(nk.threads), 0, a.stream, &args, err);
       if (st != LF_OK) return st;
     }
     if (fill_ && prog_.has_fill) {

@@ -19,6 +19,7 @@ struct NestLaunch {
   bool reduction = false;  // warp per parallel cell (true) or thread per cell
   long long units = 0;     // parallel cells
   int cells_per_cta = 0;   // reduction kernels: parallel cells a CTA owns (0: one per warp, 8)
+  int threads = 256;       // CTA size
 };
 
 // streamed axioms the warp-specialised march can fetch by TMA (tensor maps
