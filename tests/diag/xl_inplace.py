@@ -3,7 +3,7 @@ configs[4] (65536 x 65536 cells, 137 GB of state) run in place
 (config.aliases) -- the size 180 GB of HBM3e allows once the ping-pong copies
 are gone.  Measurement / parity tool, not product code:
 
-    python tools/xl_inplace.py [N] [steps]      (default 65536, 2)
+    python tests/diag/xl_inplace.py [N] [steps]      (default 65536, 2)
 
 Prints one JSON line: the rate (CUDA events around lf_run) and whether full-width
 row bands of the result equal the CPU oracle's bit for bit (the same check as
@@ -15,7 +15,7 @@ import time
 import numpy as np
 import torch
 
-sys.path.insert(0, str(__import__("pathlib").Path(__file__).resolve().parents[1]))
+sys.path.insert(0, str(__import__("pathlib").Path(__file__).resolve().parents[2]))
 import oracle  # noqa: E402  (checker)
 import paper_1710_08774_b200 as lf  # noqa: E402
 from paper_1710_08774_b200 import inputs  # noqa: E402
