@@ -733,8 +733,14 @@ int lf_run(const lf_plan* cplan, void* const* terms, int nterm, int steps, void*
 // computes row parts (lf_slab part ranges); iterated state ping-pongs through
 // the plan's scratch so the last step lands in the goals; ghost rows of the
 // goals are copied once all parts are done.
+// In place (`inplace`: every iterated goal on its axiom's device buffer, an
+// executor that runs ordered row parts in place): only the wavefront applies
+// -- parts of a step in ascending order, each part's last halo rows committed
+// after the next part's launch has read them (ExecArgs::inplace_phase) -- and
+// kNotPipelined is returned, before anything is issued, when it does not.
+constexpr int kNotPipelined = -1;
 static int run_host_pipelined(lf_plan* plan, void* const* terms, const std::vector<void*>& dterms, int parts,
-                              int steps, std::string& err) {
+                              int steps, std::string& err, bool inplace = false) {
   const auto& T = plan->plan.terminals;
   const long n0 = plan->plan.rs.ranges[0].trips();
   const long lo0 = plan->plan.rs.ranges[0].lo;
@@ -769,6 +775,7 @@ static int run_host_pipelined(lf_plan* plan, void* const* terms, const std::vect
   if (const char* e = lfx::option("LF_HOST_WAVEFRONT")) wavefront = std::atoi(e) != 0;
   wavefront = wavefront && steps > 1 && !periodic0 && wparts >= 2 && n0 / wparts >= std::max(1L, halo0);
   if (wavefront) parts = wparts;
+  if (inplace && (!wavefront || n0 / parts < 2 * std::max(1L, halo0))) return kNotPipelined;  // parts of >= 2 halos
   auto copy = [&](void* dst, const void* src, int64_t bytes, cudaMemcpyKind kind, cudaStream_t st) {
     if (bytes <= 0) return LF_OK;
     return lfx::cuda_status(cudaMemcpyAsync(dst, src, bytes, kind, st), "cudaMemcpyAsync(pipelined)", err);
@@ -787,14 +794,15 @@ static int run_host_pipelined(lf_plan* plan, void* const* terms, const std::vect
     std::vector<void*> b(cur);
     const bool to_goal = ((steps - 1 - s) % 2) == 0;
     for (size_t i = 0; i < T.size(); ++i)
-      if (T[i].is_goal && axiom_of[i] >= 0 && !to_goal) b[i] = plan->scratch[i];
+      if (T[i].is_goal && axiom_of[i] >= 0 && !to_goal && !inplace) b[i] = plan->scratch[i];
     return b;
   };
   auto advance = [&](const std::vector<void*>& b) {
     for (size_t i = 0; i < T.size(); ++i)
       if (axiom_of[i] >= 0) cur[axiom_of[i]] = b[i];
   };
-  auto run_part = [&](std::vector<void*>& b, long a, long e, bool whole) {
+  // in place: (step, part) and the phase (0 the step, 1 the commit of the part's deferred last rows)
+  auto run_part = [&](std::vector<void*>& b, long a, long e, bool whole, int s = 0, int p = 0, int phase = 0) {
     lf_slab slab{0, n0, n0, a, e};
     lfx::ExecArgs ea;
     ea.plan = &plan->plan;
@@ -804,6 +812,13 @@ static int run_host_pipelined(lf_plan* plan, void* const* terms, const std::vect
     if (!whole) {
       ea.slab = &slab;
       ea.whole_domain_parts = true;
+    }
+    if (inplace) {
+      ea.inplace = true;
+      ea.mem = &plan->exec_mem;
+      ea.inplace_phase = phase;
+      ea.inplace_slots = 2 * steps;  // a part's rows wait through one launch of the same step: two slots per step
+      ea.inplace_slot = 2 * s + (p & 1);
     }
     return plan->exec ? plan->exec->run(ea, err) : plan->jit->run(ea, err);
   };
@@ -865,8 +880,18 @@ static int run_host_pipelined(lf_plan* plan, void* const* terms, const std::vect
           cudaEventRecord(up[p], plan->h2d);
           cudaStreamWaitEvent(plan->stream, up[p], 0);
         }
-        if ((st = run_part(B[s], a, e, false)) != LF_OK) break;
-        if (s == steps - 1) send_down(B[s], p);
+        if (!inplace) {
+          if ((st = run_part(B[s], a, e, false)) != LF_OK) break;
+          if (s == steps - 1) send_down(B[s], p);
+          continue;
+        }
+        if ((st = run_part(B[s], a, e, false, s, p, 0)) != LF_OK) break;
+        if (p > 0) {  // part p-1's last rows: this launch was their last reader
+          const auto [pa, pe] = part_rows(p - 1);
+          if ((st = run_part(B[s], pa, pe, false, s, p - 1, 1)) != LF_OK) break;
+          if (s == steps - 1) send_down(B[s], p - 1);
+        }
+        if (s == steps - 1 && p == parts - 1) send_down(B[s], p);
       }
   }
   // ---- first step: parts as their rows arrive
@@ -984,10 +1009,13 @@ int lf_run_host(const lf_plan* cplan, void* const* terms, int nterm, int steps) 
       int parts = static_cast<int>(std::min<long>(32, n0 / 512));  // 32: measured best for the 16384^2 box pass
       if (const char* e = lfx::option("LF_HOST_PARTS")) parts = std::atoi(e);
       const bool reduces = plan->exec && plan->exec->max_reduce;
-      if (!inplace && !nests && !reduces && parts >= 2) {
-        st = run_host_pipelined(plan, terms, dterms, parts, steps, err);
-        if (st != LF_OK) return fail(st, err);
-        return LF_OK;
+      const bool inplace_parts = inplace && plan->exec && plan->exec->inplace;
+      if ((!inplace || inplace_parts) && !nests && !reduces && parts >= 2) {
+        st = run_host_pipelined(plan, terms, dterms, parts, steps, err, inplace);
+        if (st != kNotPipelined) {
+          if (st != LF_OK) return fail(st, err);
+          return LF_OK;
+        }
       }
     }
     for (size_t i = 0; i < T.size(); ++i) {

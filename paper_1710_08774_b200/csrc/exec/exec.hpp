@@ -57,6 +57,13 @@ struct ExecArgs {
   // place on that one buffer; only executors with `inplace` set are asked to
   bool inplace = false;
   ExecMem* mem = nullptr;  // set with `inplace`
+  // In-place row parts of a whole domain (whole_domain_parts), launched in
+  // ascending order within a step (pipelined host runs): part p's last halo
+  // rows are still read by part p+1's launch, so phase 0 (the step) defers
+  // them into row-band slot `inplace_slot` of `inplace_slots`, and phase 1
+  // -- issued after part p+1's step -- copies them in.
+  int inplace_phase = 0;
+  int inplace_slot = 0, inplace_slots = 1;
 };
 
 struct Executor {
@@ -77,8 +84,8 @@ struct Executor {
   // maximum into the goal's value; a whole-domain run() does all of it itself
   bool max_reduce = false;
   int (*finalize)(const ExecArgs&, std::string& err) = nullptr;
-  // runs whole-domain steps in place when every iterated goal is passed on
-  // its aliased axiom's buffer (ExecArgs::inplace)
+  // runs whole-domain steps (and ordered row parts, see ExecArgs) in place when
+  // every iterated goal is passed on its aliased axiom's buffer (ExecArgs::inplace)
   bool inplace = false;
 };
 

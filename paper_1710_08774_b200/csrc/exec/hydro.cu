@@ -134,6 +134,11 @@ struct Params {
   // deferred to these bands and copied in by hydro_commit after the step
   double* colband;  // [4][strips-1][nj][4]: the two columns either side of every strip boundary
   double* rowband;  // [ctas][3 segments][4 rows][4][W]: the two rows either side of every segment cut
+  // row parts launched in ascending order (pipelined host runs): the launch's
+  // last H rows are read by the NEXT part's launch, so they are deferred too
+  // (defer_bottom) and committed separately: commit_mode 0 = every deferred
+  // cell, 1 = all but those rows, 2 = those rows only
+  int defer_bottom, commit_mode;
 };
 
 struct Maps {
@@ -388,7 +393,7 @@ __global__ void __launch_bounds__(NT, MINB) hydro_fused(const __grid_constant__ 
             const int jo = sg.jb - 2 + tt - 3;
             if constexpr (INPLACE) {
               // 32-bit band offsets (checked on the host): one store sequence for both bands
-              const int rs = band_row_slot(jo, sg.jb, sg.je, sg.jb > p.row_lo, sg.je < p.row_hi);
+              const int rs = band_row_slot(jo, sg.jb, sg.je, sg.jb > p.row_lo, sg.je < p.row_hi || p.defer_bottom);
               const bool cl = t < H && sg.strip > 0, cr = t >= W - H && sg.strip < p.strips - 1;
               if (rs >= 0 || cl || cr) {
                 store_band(p, blockIdx.x * 3 + k, rs, cl ? sg.strip - 1 : sg.strip, cl ? H + t : t - (W - H), t, jo,
@@ -485,10 +490,12 @@ __global__ void __launch_bounds__(NT) hydro_commit(const Params p) {
     const RowSeg sg = seg[k];
     const int i0 = sg.strip * W;
     const int ncell = min(W, p.ni - i0);
-    const bool above = sg.jb > p.row_lo, below = sg.je < p.row_hi;
+    const bool above = sg.jb > p.row_lo, below = sg.je < p.row_hi || p.defer_bottom;
+    const int ext = p.defer_bottom ? p.row_hi - H : p.row_hi;  // rows >= ext wait for the next part's launch
     for (int rs = 0; rs < 2 * H; ++rs) {
       const int j = rs < H ? sg.jb + rs : sg.je - 2 * H + rs;
       if (j < sg.jb || j >= sg.je || band_row_slot(j, sg.jb, sg.je, above, below) != rs) continue;
+      if (p.commit_mode == 1 ? j >= ext : (p.commit_mode == 2 && j < ext)) continue;
       if (t < ncell) {
         const double* b = rowband_at(p, blockIdx.x, k, rs, t);
         const double v[4] = {b[0], b[W], b[2 * W], b[3 * W]};
@@ -496,7 +503,7 @@ __global__ void __launch_bounds__(NT) hydro_commit(const Params p) {
       }
     }
     const bool left = sg.strip > 0, right = sg.strip < p.strips - 1;
-    if (!left && !right) continue;
+    if ((!left && !right) || p.commit_mode == 2) continue;
     const long long n = (long long)(sg.je - sg.jb) * 4;
     for (long long idx = t; idx < n; idx += NT) {
       const int j = sg.jb + (int)(idx >> 2), q = (int)(idx & 3);
@@ -534,6 +541,9 @@ __global__ void cfl_finalize(double* slot) { hy_cfl_dt(*slot, slot); }
 struct Bands {
   double* col = nullptr;
   double* row = nullptr;
+  bool defer_bottom = false;  // ordered row parts: the last H rows wait for the next part's launch
+  int commit_mode = 0;        // see Params
+  bool step = true;           // false: only the commit launch (commit_mode 2)
   static size_t col_doubles(int strips, int nj) { return (size_t)4 * std::max(0, strips - 1) * nj * 4; }
   static size_t row_doubles(int ctas) { return (size_t)ctas * 3 * 4 * 4 * W; }
 };
@@ -581,6 +591,8 @@ int launch_step(const double* const in[4], double* const out[4], const double* d
   for (int a = 0; a < 4; ++a) p.out[a] = out[a];
   p.colband = bands ? bands->col : nullptr;
   p.rowband = bands ? bands->row : nullptr;
+  p.defer_bottom = bands && bands->defer_bottom ? 1 : 0;
+  p.commit_mode = bands ? bands->commit_mode : 0;
   const long long work = (long long)p.strips * (rp.hi - rp.lo);
   // each CTA must get at most 3 row segments (rowstream.cuh): at least
   // ceil(strips/2) CTAs when the row range is short
@@ -599,8 +611,9 @@ int launch_step(const double* const in[4], double* const out[4], const double* d
   // programmatic stream serialization
   const char* o = lfx::option("LF_HYDRO_IP_PDL");
   const int pdl = o ? std::atoi(o) : 0;
-  cudaError_t e;
-  if (pdl & 1) {
+  cudaError_t e = cudaSuccess;
+  if (!bands->step) {
+  } else if (pdl & 1) {
     e = launch_pdl(k, dim3(ctas), dim3(NT), SMEM, st, maps, p);
   } else {
     k<<<ctas, NT, SMEM, st>>>(maps, p);
@@ -622,34 +635,52 @@ int launch_step(const double* const in[4], double* const out[4], const double* d
 int run_inplace(const ExecArgs& a, std::string& err) {
   const auto& r = a.plan->rs.ranges;
   const int ni = (int)r[1].trips();
-  if (a.slab) {
-    err = "in-place runs cover the whole domain (no slabs or row parts)";
+  if (a.slab && !a.whole_domain_parts) {
+    err = "in-place runs cover the whole domain (no slabs)";
     return LF_ERR_UNSUPPORTED;
   }
   const RowPart rp = row_part(a, (int)r[0].trips());
+  const bool part = rp.lo > 0 || rp.hi < rp.rows;
+  if (part && (a.steps != 1 || rp.hi - rp.lo < 2 * H)) {
+    err = "in-place row parts run one step at a time and span at least 4 rows";
+    return LF_ERR_UNSUPPORTED;
+  }
   double* u[4];
   for (int v = 0; v < 4; ++v) u[v] = static_cast<double*>(a.terms[v]);
   const double* dtdx = static_cast<const double*>(a.terms[4]);
+  // band sizes from the whole domain's launch (a part's grid is never larger)
+  const RowPart whole{rp.rows, 0, rp.rows, true, true};
   Bands sizing;
   sizing.row = reinterpret_cast<double*>(1);  // selects the in-place kernel for the occupancy query
   int ctas = 0;
-  if (int s = launch_step(u, u, dtdx, ni, rp, a.stream, err, nullptr, false, &sizing, &ctas)) return s;
+  if (int s = launch_step(u, u, dtdx, ni, whole, a.stream, err, nullptr, false, &sizing, &ctas)) return s;
   const int strips = (ni + W - 1) / W;
   const size_t ncol = Bands::col_doubles(strips, rp.rows), nrow = Bands::row_doubles(ctas);
   if (ncol >= (1ull << 31) || nrow >= (1ull << 31)) {  // the kernel forms band offsets in 32 bits
     err = "grid too large for the in-place bands";
     return LF_ERR_UNSUPPORTED;
   }
-  if (!a.mem) {
+  if (!a.mem || a.inplace_slots < 1 || a.inplace_slot < 0 || a.inplace_slot >= a.inplace_slots) {
     err = "in-place run without plan-owned band memory";
     return LF_ERR_INTERNAL;
   }
-  cudaError_t e = a.mem->ensure((ncol + nrow) * sizeof(double));
+  cudaError_t e = a.mem->ensure((ncol + nrow * a.inplace_slots) * sizeof(double));
   if (e != cudaSuccess) return cuda_status(e, "cudaMalloc(hydro bands)", err);
   double* mem = static_cast<double*>(a.mem->ptr);
   Bands b;
   b.col = mem;
-  b.row = mem + ncol;
+  b.row = mem + ncol + nrow * a.inplace_slot;
+  if (part) {
+    b.defer_bottom = rp.hi < rp.rows;
+    if (a.inplace_phase == 1) {  // the rows the next part's launch has now read
+      if (!b.defer_bottom) return LF_OK;
+      b.step = false;
+      b.commit_mode = 2;
+    } else {
+      b.commit_mode = b.defer_bottom ? 1 : 0;
+    }
+    return launch_step(u, u, dtdx, ni, rp, a.stream, err, nullptr, false, &b);
+  }
   int stt = LF_OK;
   for (int s = 0; s < a.steps && stt == LF_OK; ++s)
     stt = launch_step(u, u, dtdx, ni, rp, a.stream, err, nullptr, false, &b);

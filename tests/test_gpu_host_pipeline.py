@@ -143,3 +143,28 @@ def test_wavefront_over_steps_and_parts(wave, monkeypatch):
     out = np.full_like(u, np.nan)
     plan.run_host([u, out], steps=5)
     assert np.array_equal(bits(out), bits(oracle.biharm(u, 5)))
+
+
+@pytest.mark.parametrize("shape,parts,steps", [((24, 128), 6, 6), ((40, 300), 10, 5), ((64, 1000), 7, 4),
+                                               ((33, 254), 8, 3)])
+def test_in_place_wavefront(shape, parts, steps, monkeypatch):
+    """Hydro2D in place through lf_run_host (one device buffer per state array)
+    as a wavefront over (step, part): a part's last two rows stay deferred until
+    the next part's launch of the same step has read them.  Parts of four rows
+    (two halos) up, segment cuts inside parts, several strips."""
+    monkeypatch.setenv("LF_HOST_WAVEFRONT", "1")
+    monkeypatch.setenv("LF_HOST_PARTS", str(parts))
+    plan = lf.Plan.with_ranges("hydro2d", shape, inplace=True)
+    assert plan.executor == "hydro2d_fused_tma"
+    st, dtdx = inputs.hydro_input(*shape, seed=shape[0] + parts)
+    u = [a.copy() for a in st]
+    plan.run_host(u + [np.array([dtdx])] + u, steps=steps)
+    ref = oracle.hydro(st, dtdx, steps)
+    for v in range(4):
+        assert np.array_equal(bits(u[v]), bits(ref[v])), (v, int(np.count_nonzero(u[v] != ref[v])))
+    # parts thinner than two halos: the serial in-place path, same result
+    monkeypatch.setenv("LF_HOST_PARTS", str(shape[0] // 2))
+    u = [a.copy() for a in st]
+    plan.run_host(u + [np.array([dtdx])] + u, steps=steps)
+    for v in range(4):
+        assert np.array_equal(bits(u[v]), bits(ref[v])), v
