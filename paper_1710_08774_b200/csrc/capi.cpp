@@ -774,6 +774,12 @@ static int run_host_pipelined(lf_plan* plan, void* const* terms, const std::vect
   bool wavefront = wparts >= 16;
   if (const char* e = lfx::option("LF_HOST_WAVEFRONT")) wavefront = std::atoi(e) != 0;
   wavefront = wavefront && steps > 1 && !periodic0 && wparts >= 2 && n0 / wparts >= std::max(1L, halo0);
+  // per-step MAX reductions over the whole grid (Executor::max_reduce, the CFL time
+  // step): step s+1 needs step s's complete maximum, so no wavefront -- the first
+  // and the last step still run in parts under the copies; each step's goal slot
+  // is zeroed before its launches and the last one finalised (as lf_run_slabs does)
+  const bool mr = plan->exec && plan->exec->max_reduce;
+  if (mr) wavefront = false;
   if (wavefront) parts = wparts;
   if (inplace && (!wavefront || n0 / parts < 2 * std::max(1L, halo0))) return kNotPipelined;  // parts of >= 2 halos
   auto copy = [&](void* dst, const void* src, int64_t bytes, cudaMemcpyKind kind, cudaStream_t st) {
@@ -812,7 +818,12 @@ static int run_host_pipelined(lf_plan* plan, void* const* terms, const std::vect
     if (!whole) {
       ea.slab = &slab;
       ea.whole_domain_parts = true;
+    } else if (mr) {  // one step of a driver's schedule: the executor neither zeroes nor finalises
+      slab.part_lo = slab.part_hi = 0;
+      ea.slab = &slab;
+      ea.whole_domain_parts = true;
     }
+    ea.raw_max_input = mr && s > 0;
     if (inplace) {
       ea.inplace = true;
       ea.mem = &plan->exec_mem;
@@ -832,6 +843,16 @@ static int run_host_pipelined(lf_plan* plan, void* const* terms, const std::vect
   for (size_t i = 0; i < T.size() && st == LF_OK; ++i)
     if (!T[i].is_goal && !chunked(T[i])) st = copy(dterms[i], terms[i], terminal_bytes(T[i]), cudaMemcpyHostToDevice, plan->h2d);
   auto part_rows = [&](int p) { return std::make_pair(n0 * p / parts, n0 * (p + 1) / parts); };
+  // max_reduce: this step's reduction slots (rank-0 iterated goals) start from zero
+  auto zero_reductions = [&](const std::vector<void*>& b) {
+    if (!mr) return;
+    for (size_t i = 0; i < T.size() && st == LF_OK; ++i)
+      if (T[i].is_goal && axiom_of[i] >= 0 && T[i].dims.empty() &&
+          cudaMemsetAsync(b[i], 0, terminal_bytes(T[i]), plan->stream) != cudaSuccess) {
+        err = "cudaMemsetAsync(reduction slot) failed";
+        st = LF_ERR_CUDA;
+      }
+  };
   auto send_down = [&](const std::vector<void*>& b, int p) {
     const auto [a, e] = part_rows(p);
     cudaEventRecord(done[p], plan->stream);
@@ -898,6 +919,7 @@ static int run_host_pipelined(lf_plan* plan, void* const* terms, const std::vect
   if (!wavefront) {
     std::vector<void*> b = step_bufs(0);
     std::vector<long> copied(T.size(), 0);  // storage rows already sent, per axiom
+    zero_reductions(b);
     for (int p = 0; p < parts && st == LF_OK; ++p) {
       const auto [a, e] = part_rows(p);
       // rows of every chunked axiom up to this part's last row plus the ghost/halo rows above it
@@ -923,17 +945,27 @@ static int run_host_pipelined(lf_plan* plan, void* const* terms, const std::vect
   // ---- the steps in between: whole-domain launches
   for (int s = 1; s < steps - 1 && st == LF_OK && !wavefront; ++s) {
     std::vector<void*> b = step_bufs(s);
-    st = run_part(b, 0, n0, true);
+    zero_reductions(b);
+    if (st == LF_OK) st = run_part(b, 0, n0, true, s);
     advance(b);
   }
   // ---- last step: parts, each sent down as soon as it is done
   if (steps > 1 && st == LF_OK && !wavefront) {
     std::vector<void*> b = step_bufs(steps - 1);
+    zero_reductions(b);
     for (int p = 0; p < parts && st == LF_OK; ++p) {
       const auto [a, e] = part_rows(p);
-      if ((st = run_part(b, a, e, false)) != LF_OK) break;
+      if ((st = run_part(b, a, e, false, steps - 1)) != LF_OK) break;
       send_down(b, p);
     }
+  }
+  if (mr && st == LF_OK && plan->exec->finalize) {  // the last raw maximum becomes the goal's value
+    lfx::ExecArgs ea;
+    ea.plan = &plan->plan;
+    ea.terms = const_cast<void* const*>(dterms.data());
+    ea.stream = plan->stream;
+    st = plan->exec->finalize(ea, err);
+    cudaEventRecord(done[parts - 1], plan->stream);  // the scalar goals go down after it
   }
   // once every part is done: ghost rows of the goals, and goals without an outer dimension
   if (st == LF_OK) {
@@ -1010,7 +1042,7 @@ int lf_run_host(const lf_plan* cplan, void* const* terms, int nterm, int steps) 
       if (const char* e = lfx::option("LF_HOST_PARTS")) parts = std::atoi(e);
       const bool reduces = plan->exec && plan->exec->max_reduce;
       const bool inplace_parts = inplace && plan->exec && plan->exec->inplace;
-      if ((!inplace || inplace_parts) && !nests && !reduces && parts >= 2) {
+      if ((!inplace || inplace_parts) && !nests && !(reduces && inplace) && parts >= 2) {
         st = run_host_pipelined(plan, terms, dterms, parts, steps, err, inplace);
         if (st != kNotPipelined) {
           if (st != LF_OK) return fail(st, err);

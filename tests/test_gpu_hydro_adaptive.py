@@ -62,6 +62,24 @@ def test_adaptive_host_path_and_full_size():
     assert float(got[4]) == dref
 
 
+@pytest.mark.parametrize("steps", [1, 2, 5])
+def test_adaptive_host_path_pipelined(steps, monkeypatch):
+    """lf_run_host with the copies overlapping the first and the last step's
+    row parts (no wavefront: every step needs the previous one's whole-grid
+    maximum); the driver zeroes each step's reduction slot and finalises the
+    last."""
+    monkeypatch.setenv("LF_HOST_PARTS", "5")
+    shape = (60, 300)
+    plan = lf.Plan.with_ranges("hydro2d_adaptive", shape)
+    st, dtdx = inputs.hydro_input(*shape, seed=steps)
+    outs = [np.full_like(st[0], np.nan) for _ in range(4)] + [np.zeros(1)]
+    plan.run_host(st + [np.array([dtdx])] + outs, steps=steps)
+    ref, dref = oracle.hydro_adaptive(st, dtdx, steps, fused=True)
+    for v in range(4):
+        assert np.array_equal(bits(outs[v]), bits(ref[v])), v
+    assert outs[4][0] == dref
+
+
 def test_caller_driven_slab_steps_are_refused():
     """One step of a slab with the caller's own exchange cannot combine the
     per-step reduction across ranks: lf_run_slab refuses the chain."""
