@@ -145,12 +145,21 @@ struct Maps {
   CUtensorMap m[4];
 };
 
-__device__ __forceinline__ void store_cell(const Params& p, int j, int i, const double v[4]) {
+// `band` (in-place runs): a deferred cell goes to band[a * bstride] instead --
+// the store addresses are selected, not branched to, so a warp whose edge lanes
+// are deferred stays on one path; its ghost images are left to hydro_commit
+__device__ __forceinline__ void store_cell(const Params& p, int j, int i, const double v[4], double* band = nullptr,
+                                           unsigned bstride = 0) {
   // interior value plus its reflective images in the ghost ring
   const long long P = p.pitch;
   const long long base = (long long)(j + H) * P + (i + H);
 #pragma unroll
-  for (int a = 0; a < 4; ++a) p.out[a][base] = v[a];
+  for (int a = 0; a < 4; ++a) {
+    double* d = p.out[a] + base;
+    if (band) d = band + (size_t)a * bstride;
+    *d = v[a];
+  }
+  if (band) return;
   int im = -100, jm = -100;
   if (i < H) im = -1 - i;
   if (i >= p.ni - H) im = 2 * p.ni - 1 - i;
@@ -200,26 +209,6 @@ __device__ __forceinline__ double* rowband_at(const Params& p, int cta, int k, i
 }
 __device__ __forceinline__ double* colband_at(const Params& p, int edge, int j, int c4) {
   return p.colband + ((size_t)edge * p.nj + j) * 4 + c4;
-}
-
-// a deferred cell into its band: row slot `rs` of segment `seg` (>= 0), else
-// column `c4` of strip boundary `edge`; out of line (a few cells per row) and
-// with 32-bit offsets (checked on the host)
-__device__ __noinline__ void store_band(const Params& p, int seg, int rs, int edge, int c4, int t, int jo, double o0,
-                                        double o1, double o2, double o3) {
-  double* b;
-  unsigned stride;
-  if (rs >= 0) {
-    b = p.rowband + (unsigned)((seg * 4 + rs) * 4 * W + t);
-    stride = W;
-  } else {
-    b = p.colband + ((unsigned)(edge * p.nj + jo) * 4u + (unsigned)c4);
-    stride = (unsigned)(p.strips - 1) * (unsigned)p.nj * 4u;
-  }
-  b[0] = o0;
-  b[stride] = o1;
-  b[(size_t)2 * stride] = o2;
-  b[(size_t)3 * stride] = o3;
 }
 
 // ADAPT: also reduce the CFL speed of every stored cell (specs/hydro2d_adaptive.lf)
@@ -395,12 +384,16 @@ __global__ void __launch_bounds__(NT, MINB) hydro_fused(const __grid_constant__ 
               // 32-bit band offsets (checked on the host): one store sequence for both bands
               const int rs = band_row_slot(jo, sg.jb, sg.je, sg.jb > p.row_lo, sg.je < p.row_hi || p.defer_bottom);
               const bool cl = t < H && sg.strip > 0, cr = t >= W - H && sg.strip < p.strips - 1;
-              if (rs >= 0 || cl || cr) {
-                store_band(p, blockIdx.x * 3 + k, rs, cl ? sg.strip - 1 : sg.strip, cl ? H + t : t - (W - H), t, jo,
-                           o[0], o[1], o[2], o[3]);
-              } else {
-                store_cell(p, jo, i0 + t, o);
+              double* band = nullptr;
+              unsigned bstride = W;
+              if (rs >= 0) {
+                band = p.rowband + (unsigned)(((blockIdx.x * 3 + k) * 4 + rs) * 4 * W + t);
+              } else if (cl || cr) {
+                band = p.colband + ((unsigned)((cl ? sg.strip - 1 : sg.strip) * p.nj + jo) * 4u +
+                                    (unsigned)(cl ? H + t : t - (W - H)));
+                bstride = (unsigned)(p.strips - 1) * (unsigned)p.nj * 4u;
               }
+              store_cell(p, jo, i0 + t, o, band, bstride);
             } else {
               store_cell(p, jo, i0 + t, o);
             }
