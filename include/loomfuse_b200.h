@@ -149,9 +149,13 @@ int lf_run(const lf_plan* plan, void* const* terminals, int nterm, int steps, vo
 /* Same on HOST buffers: copies axioms host->device, runs, copies goals
  * device->host, synchronises.  This is the drop-in for the emitted host
  * function <name>(terminals...) of R/SPEC.md:500.  Device buffers are owned
- * and cached by the plan.  Pinned host memory gives full copy bandwidth; a
- * single step on a large grid is pipelined over row parts (host->device
- * copies, compute and device->host copies overlap). */
+ * and cached by the plan.  Pinned host memory gives full copy bandwidth;
+ * large grids are pipelined over row parts (host->device copies, compute and
+ * device->host copies overlap): the first and the last step, or -- multi-step
+ * runs of chains whose outer dimension does not wrap -- every step, as a
+ * wavefront over (step, part).  A host array passed as an aliased axiom AND
+ * its goal (config.aliases) keeps ONE device buffer and runs in place, where
+ * the executor can (as lf_run). */
 int lf_run_host(const lf_plan* plan, void* const* terminals, int nterm, int steps);
 
 /* One step on a slab of the outermost loop dimension (multi-GPU row/plane

@@ -828,8 +828,12 @@ static int run_host_pipelined(lf_plan* plan, void* const* terms, const std::vect
       ea.inplace = true;
       ea.mem = &plan->exec_mem;
       ea.inplace_phase = phase;
-      ea.inplace_slots = 2 * steps;  // a part's rows wait through one launch of the same step: two slots per step
-      ea.inplace_slot = 2 * s + (p & 1);
+      // a part's rows wait through one launch of the same step: two slots per
+      // step, reused once the step that far ahead cannot overlap (tau = p + 2s:
+      // step s + ring/2 starts after tau >= 2s + ring > p + 1 + 2s)
+      const int ring = std::min(2 * steps, (parts + 5) / 2 * 2);
+      ea.inplace_slots = ring;
+      ea.inplace_slot = (2 * s + (p & 1)) % ring;
     }
     return plan->exec ? plan->exec->run(ea, err) : plan->jit->run(ea, err);
   };

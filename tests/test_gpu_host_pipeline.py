@@ -145,8 +145,9 @@ def test_wavefront_over_steps_and_parts(wave, monkeypatch):
     assert np.array_equal(bits(out), bits(oracle.biharm(u, 5)))
 
 
+# (40, 300) in 4 parts for 9 steps: the row-band slots of a step are reused by the step 4 ahead
 @pytest.mark.parametrize("shape,parts,steps", [((24, 128), 6, 6), ((40, 300), 10, 5), ((64, 1000), 7, 4),
-                                               ((33, 254), 8, 3)])
+                                               ((33, 254), 8, 3), ((40, 300), 4, 9), ((48, 130), 2, 12)])
 def test_in_place_wavefront(shape, parts, steps, monkeypatch):
     """Hydro2D in place through lf_run_host (one device buffer per state array)
     as a wavefront over (step, part): a part's last two rows stay deferred until
