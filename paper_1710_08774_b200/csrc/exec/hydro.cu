@@ -555,10 +555,11 @@ int launch_step(const double* const in[4], double* const out[4], const double* d
     return var == 0 ? hydro_fused<2> : (var == 2 ? hydro_fused<4> : hydro_fused<3>);
   }();
   const bool inplace = bands && bands->row;
-  void (*const k)(Maps, Params) = inplace ? hydro_fused<3, false, true> : (cfl_acc ? hydro_fused<3, true> : kern);
-  static LaunchCache cache, cache_adapt, cache_inplace;
+  void (*const k)(Maps, Params) =
+      inplace ? (cfl_acc ? hydro_fused<3, true, true> : hydro_fused<3, false, true>) : (cfl_acc ? hydro_fused<3, true> : kern);
+  static LaunchCache cache, cache_adapt, cache_inplace, cache_inplace_adapt;
   int slots = 0;
-  if (int s = resident_slots(inplace ? cache_inplace : (cfl_acc ? cache_adapt : cache),
+  if (int s = resident_slots(inplace ? (cfl_acc ? cache_inplace_adapt : cache_inplace) : (cfl_acc ? cache_adapt : cache),
                              reinterpret_cast<const void*>(k), NT, SMEM, 0, "cudaFuncSetAttribute(hydro)", &slots, err))
     return s;
   Maps maps;
@@ -625,7 +626,9 @@ int launch_step(const double* const in[4], double* const out[4], const double* d
 // Whole-domain steps on ONE buffer per state array (the caller passed each
 // goal on its aliased axiom's buffer).  The bands are plan-owned: 4 columns per
 // strip boundary and 4 rows per segment cut, about 3 % of the state.
-int run_inplace(const ExecArgs& a, std::string& err) {
+// `adaptive`: specs/hydro2d_adaptive.lf -- each step also reduces its CFL maximum
+// (run_adaptive below); the two dt/dx slots are the goal's and one beside the bands.
+int run_inplace(const ExecArgs& a, std::string& err, bool adaptive = false) {
   const auto& r = a.plan->rs.ranges;
   const int ni = (int)r[1].trips();
   if (a.slab && !a.whole_domain_parts) {
@@ -634,8 +637,8 @@ int run_inplace(const ExecArgs& a, std::string& err) {
   }
   const RowPart rp = row_part(a, (int)r[0].trips());
   const bool part = rp.lo > 0 || rp.hi < rp.rows;
-  if (part && (a.steps != 1 || rp.hi - rp.lo < 2 * H)) {
-    err = "in-place row parts run one step at a time and span at least 4 rows";
+  if (part && (a.steps != 1 || rp.hi - rp.lo < 2 * H || adaptive)) {
+    err = "in-place row parts run one step at a time, span at least 4 rows and carry no per-step reduction";
     return LF_ERR_UNSUPPORTED;
   }
   double* u[4];
@@ -657,7 +660,7 @@ int run_inplace(const ExecArgs& a, std::string& err) {
     err = "in-place run without plan-owned band memory";
     return LF_ERR_INTERNAL;
   }
-  cudaError_t e = a.mem->ensure((ncol + nrow * a.inplace_slots) * sizeof(double));
+  cudaError_t e = a.mem->ensure((ncol + nrow * a.inplace_slots + 2) * sizeof(double));
   if (e != cudaSuccess) return cuda_status(e, "cudaMalloc(hydro bands)", err);
   double* mem = static_cast<double*>(a.mem->ptr);
   Bands b;
@@ -675,9 +678,31 @@ int run_inplace(const ExecArgs& a, std::string& err) {
     return launch_step(u, u, dtdx, ni, rp, a.stream, err, nullptr, false, &b);
   }
   int stt = LF_OK;
-  for (int s = 0; s < a.steps && stt == LF_OK; ++s)
-    stt = launch_step(u, u, dtdx, ni, rp, a.stream, err, nullptr, false, &b);
-  return stt;
+  if (!adaptive) {
+    for (int s = 0; s < a.steps && stt == LF_OK; ++s)
+      stt = launch_step(u, u, dtdx, ni, rp, a.stream, err, nullptr, false, &b);
+    return stt;
+  }
+  double* dgoal = static_cast<double*>(a.terms[9]);
+  double* dslot = mem + ncol + nrow * a.inplace_slots;
+  const double* dsrc = dtdx;
+  if (dgoal == dtdx) {  // the dt/dx pair shares its slot too: keep the given value beside the bands
+    e = cudaMemcpyAsync(dslot + 1, dtdx, sizeof(double), cudaMemcpyDeviceToDevice, a.stream);
+    if (e != cudaSuccess) return cuda_status(e, "cudaMemcpyAsync(dt/dx)", err);
+    dsrc = dslot + 1;
+  }
+  bool is_max = false;
+  for (int s = 0; s < a.steps && stt == LF_OK; ++s) {
+    double* dd = ((a.steps - 1 - s) % 2) == 0 ? dgoal : dslot;
+    e = cudaMemsetAsync(dd, 0, sizeof(double), a.stream);
+    if (e != cudaSuccess) return cuda_status(e, "cudaMemsetAsync(cfl)", err);
+    stt = launch_step(u, u, dsrc, ni, rp, a.stream, err, reinterpret_cast<unsigned long long*>(dd), is_max, &b);
+    dsrc = dd;
+    is_max = true;
+  }
+  if (stt != LF_OK) return stt;
+  cfl_finalize<<<1, 1, 0, a.stream>>>(dgoal);
+  return cuda_status(cudaGetLastError(), "cfl_finalize launch", err);
 }
 
 int run(const ExecArgs& a, std::string& err) {
@@ -711,6 +736,7 @@ int run(const ExecArgs& a, std::string& err) {
 // finalised here; a slab driver (lf_run_slabs) zeroes, combines the ranks'
 // maxima (MAX all-reduce) and finalises itself -- Executor::max_reduce.
 int run_adaptive(const ExecArgs& a, std::string& err) {
+  if (a.inplace) return run_inplace(a, err, true);
   const auto& r = a.plan->rs.ranges;
   const int ni = (int)r[1].trips();
   const RowPart rp = row_part(a, (int)r[0].trips());
@@ -755,6 +781,7 @@ int finalize_adaptive(const ExecArgs& a, std::string& err) {
 extern const Executor hydro_executor = {"hydro2d_fused_tma", "hydro2d.lf", 1, 64.0, supports, run,
                                         nullptr, false, nullptr, /*inplace=*/true};
 extern const Executor hydro_adaptive_executor = {"hydro2d_adaptive_fused_tma", "hydro2d_adaptive.lf", 1, 64.0,
-                                                 supports, run_adaptive, nullptr, true, finalize_adaptive};
+                                                 supports, run_adaptive, nullptr, true, finalize_adaptive,
+                                                 /*inplace=*/true};
 
 }  // namespace lfx

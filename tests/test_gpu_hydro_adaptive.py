@@ -80,6 +80,32 @@ def test_adaptive_host_path_pipelined(steps, monkeypatch):
     assert outs[4][0] == dref
 
 
+@pytest.mark.parametrize("shape,steps,share_dt", [((12, 20), 3, False), ((64, 256), 4, True), ((130, 254), 2, False),
+                                                  ((257, 1000), 3, True)])
+def test_adaptive_in_place(shape, steps, share_dt):
+    """The adaptive chain in place (config.aliases for every iterate pair): the
+    four state arrays on one buffer each; the dt/dx pair on one slot or two."""
+    import torch
+    plan = lf.Plan.with_ranges("hydro2d_adaptive", shape, inplace=True)
+    assert plan.executor == "hydro2d_adaptive_fused_tma"
+    st, dtdx = inputs.hydro_input(*shape, seed=shape[1] + 5)
+    u = [torch.from_numpy(a).cuda() for a in st]
+    d_in = torch.tensor(dtdx, dtype=torch.float64, device="cuda")
+    d_out = d_in if share_dt else torch.zeros((), dtype=torch.float64, device="cuda")
+    plan.run(u + [d_in] + u + [d_out], steps=steps)
+    torch.cuda.synchronize()
+    ref, dref = oracle.hydro_adaptive(st, dtdx, steps)
+    for v in range(4):
+        assert np.array_equal(bits(u[v].cpu().numpy()), bits(ref[v])), v
+    assert float(d_out) == dref
+    # through host buffers: one device buffer per state array
+    h = [a.copy() for a in st]
+    dh = np.array([dtdx])
+    plan.run_host(h + [dh] + h + [dh if share_dt else np.zeros(1)], steps=steps)
+    for v in range(4):
+        assert np.array_equal(bits(h[v]), bits(ref[v])), v
+
+
 def test_caller_driven_slab_steps_are_refused():
     """One step of a slab with the caller's own exchange cannot combine the
     per-step reduction across ranks: lf_run_slab refuses the chain."""
