@@ -173,7 +173,10 @@ int lf_run_slab(const lf_plan* plan, void* const* terminals, int nterm, const lf
  * one of them (ring-wrapped when the boundary of dim 0 is periodic) while the
  * interior rows are computed on `cuda_stream`, and orders the next step after
  * both.  Iterated state ping-pongs through
- * slab-sized plan scratch; the final state is left in the goal buffers.  NCCL
+ * slab-sized plan scratch; the final state is left in the goal buffers.  A
+ * rank that passes its slab-sized goals on its aliased axioms' buffers runs
+ * its slab in place instead (built-in Hydro2D executors: one launch per step,
+ * then the exchange; no slab scratch; every rank must do the same).  NCCL
  * is loaded at run time (libnccl.so.2; the process's copy when one is
  * loaded).  Replaces the reference's external outer-level parallelism
  * (R/PAPER.md:499). */

@@ -204,10 +204,13 @@ struct RankState {
   std::vector<void*> cur, bufs;  // this step's inputs / outputs
 };
 
-std::vector<int64_t> scratch_need(const SlabGeom& g, const RankState& r) {
+// in place: the slab-sized pairs share their buffers; only rank-0 pairs (per-step
+// reduction slots) still alternate
+std::vector<int64_t> scratch_need(const SlabGeom& g, const RankState& r, bool inplace = false) {
   std::vector<int64_t> need(g.paired.size(), 0);
   for (size_t i = 0; i < g.paired.size(); ++i)
-    if (g.paired[i] >= 0) need[i] = g.rb[i] ? g.rb[i] * (r.hi - r.lo + g.below[i] + g.above[i]) : g.elem[i];
+    if (g.paired[i] >= 0 && !(inplace && g.rb[i]))
+      need[i] = g.rb[i] ? g.rb[i] * (r.hi - r.lo + g.below[i] + g.above[i]) : g.elem[i];
   return need;
 }
 
@@ -280,7 +283,8 @@ int run_slabs_core(lf_plan* plan, const SlabGeom& g, std::vector<RankState>& R, 
                    cudaStream_t side,
                    const std::function<int(std::vector<RankState>&, cudaStream_t, std::string&)>& exchange,
                    std::string& err,
-                   const std::function<int(void* slot, cudaStream_t, std::string&)>& combine = nullptr) {
+                   const std::function<int(void* slot, cudaStream_t, std::string&)>& combine = nullptr,
+                   bool inplace = false) {
   const size_t nt = g.paired.size();
   const bool mr = plan->exec && plan->exec->max_reduce;
   std::vector<size_t> scalars;  // rank-0 iterated goals
@@ -301,6 +305,10 @@ int run_slabs_core(lf_plan* plan, const SlabGeom& g, std::vector<RankState>& R, 
     ea.stream = on;
     ea.slab = &slab;
     ea.raw_max_input = mr && step_no > 0;
+    if (inplace) {  // every iterated goal on its axiom's slab buffer (whole-slab launches only)
+      ea.inplace = true;
+      ea.mem = &plan->exec_mem;
+    }
     return plan->exec ? plan->exec->run(ea, err) : plan->jit->run(ea, err);
   };
   // LF_SLAB_SCHEDULE: parallel (default) | serial | concurrent -- see above
@@ -323,7 +331,8 @@ int run_slabs_core(lf_plan* plan, const SlabGeom& g, std::vector<RankState>& R, 
   // dimension): every step is one launch per rank, nothing else
   bool peers = R.size() > 1 || g.world > 1;
   for (size_t i = 0; i < g.paired.size(); ++i) peers |= g.paired[i] >= 0 && g.periodic[i];
-  const int sched = !peers ? 3 : (sched_env >= 0 ? sched_env : (min_rows >= 1024 ? 3 : 0));
+  // in place: one launch per rank and step (the face / interior split would need ordered parts)
+  const int sched = (!peers || inplace) ? 3 : (sched_env >= 0 ? sched_env : (min_rows >= 1024 ? 3 : 0));
   cudaStream_t side2 = side;
   if (sched == 0) {
     if (!plan->comm2 && make_side_stream(&plan->comm2, err) != LF_OK) return LF_ERR_CUDA;
@@ -343,7 +352,8 @@ int run_slabs_core(lf_plan* plan, const SlabGeom& g, std::vector<RankState>& R, 
     for (auto& r : R) {
       r.bufs = r.cur;
       for (size_t i = 0; i < nt; ++i)
-        if (plan->plan.terminals[i].is_goal) r.bufs[i] = (to_goal || g.paired[i] < 0) ? r.terms[i] : r.scratch[i];
+        if (plan->plan.terminals[i].is_goal)
+          r.bufs[i] = (to_goal || g.paired[i] < 0 || (inplace && g.rb[i])) ? r.terms[i] : r.scratch[i];
     }
     if (!scalars.empty()) {
       for (size_t i : scalars) {
@@ -686,6 +696,29 @@ static int exec_inplace_pairs(const lf_plan* plan, void* const* terms, std::vect
         err = "in-place runs take every iterated goal on its axiom's buffer ('" + gname + "' has its own)";
         return LF_ERR_UNSUPPORTED;
       }
+  return LF_OK;
+}
+
+
+// Slab runs in place: the rank passes every iterated slab-sized goal on its
+// axiom's slab buffer (declared in config.aliases) and the built-in executor
+// runs whole-slab launches in place; the generic executor's in-place runs
+// cover the whole domain only.
+static int slab_inplace(const lf_plan* plan, void* const* terms, bool& inplace, std::string& err) {
+  inplace = shares_buffer(plan, terms);
+  if (!inplace) return LF_OK;
+  if (!plan->exec) {
+    err = "slab runs of the generic executor need distinct axiom and goal buffers (its in-place runs cover the whole domain)";
+    return LF_ERR_UNSUPPORTED;
+  }
+  std::vector<int> share;
+  if (int st = exec_inplace_pairs(plan, terms, share, err)) return st;
+  const auto& T = plan->plan.terminals;
+  for (size_t j = 0; j < T.size(); ++j)
+    if (share[j] >= 0 && T[j].dims.empty()) {  // per-step reduction slots alternate between goal and scratch
+      err = "slab runs need a separate buffer for the rank-0 goal '" + T[j].name + "'";
+      return LF_ERR_UNSUPPORTED;
+    }
   return LF_OK;
 }
 
@@ -1179,10 +1212,11 @@ int lf_run_slabs(const lf_plan* cplan, void* comm, int rank, int world, void* co
     const NcclApi& n = nccl();
     if (!n.error.empty()) return fail(LF_ERR_UNSUPPORTED, n.error);
     if (!comm || world < 1 || rank < 0 || rank >= world) return fail(LF_ERR_SPEC, "invalid communicator arguments");
-    if (shares_buffer(cplan, terms)) return fail(LF_ERR_UNSUPPORTED, "slab runs need distinct axiom and goal buffers");
     lf_plan* plan = const_cast<lf_plan*>(cplan);
     std::lock_guard<std::mutex> lk(plan->mu);
     std::string err;
+    bool inplace = false;
+    if ((st = slab_inplace(plan, terms, inplace, err)) != LF_OK) return fail(st, err);
     SlabGeom g = slab_geom(plan->plan);
     g.world = world;
     if ((st = slab_check(plan, g, world, err)) != LF_OK) return fail(st, err);
@@ -1194,7 +1228,7 @@ int lf_run_slabs(const lf_plan* cplan, void* comm, int rank, int world, void* co
     R[0].hi = g.n0 * (rank + 1) / world;
     R[0].terms = terms;
     if (steps > 1) {
-      std::vector<int64_t> need = scratch_need(g, R[0]);
+      std::vector<int64_t> need = scratch_need(g, R[0], inplace);
       if (plan->slab_scratch_bytes != need) {
         for (void* q : plan->slab_scratch)
           if (q) cudaFree(q);
@@ -1236,7 +1270,7 @@ int lf_run_slabs(const lf_plan* cplan, void* comm, int rank, int world, void* co
     auto combine = [&](void* slot, cudaStream_t on, std::string& e) {
       return nccl_status(n.all_reduce(slot, slot, 1, ncclFloat64, ncclMax, c, on), "ncclAllReduce", e);
     };
-    st = run_slabs_core(plan, g, R, steps, stream, plan->comm, exchange, err, combine);
+    st = run_slabs_core(plan, g, R, steps, stream, plan->comm, exchange, err, combine, inplace);
     if (st != LF_OK) return fail(st, err);
     return LF_OK;
   } catch (const std::exception& e) {
@@ -1252,12 +1286,18 @@ int lf_run_slabs_local(const lf_plan* cplan, int world, void* const* terms, int 
     for (int r = 0; r < world; ++r) {
       int st = check_run_args(cplan, terms + (size_t)r * nterm, nterm, steps);
       if (st != LF_OK) return st;
-      if (shares_buffer(cplan, terms + (size_t)r * nterm))
-        return fail(LF_ERR_UNSUPPORTED, "slab runs need distinct axiom and goal buffers");
     }
     lf_plan* plan = const_cast<lf_plan*>(cplan);
     std::lock_guard<std::mutex> lk(plan->mu);
     std::string err;
+    bool inplace = false;
+    for (int r = 0; r < world; ++r) {  // every rank in place, or none
+      bool ip = false;
+      int st = slab_inplace(plan, terms + (size_t)r * nterm, ip, err);
+      if (st != LF_OK) return fail(st, err);
+      if (r > 0 && ip != inplace) return fail(LF_ERR_SPEC, "some ranks share axiom and goal buffers, some do not");
+      inplace = ip;
+    }
     SlabGeom g = slab_geom(plan->plan);
     g.world = world;
     int st = slab_check(plan, g, world, err);
@@ -1272,7 +1312,7 @@ int lf_run_slabs_local(const lf_plan* cplan, int world, void* const* terms, int 
       R[r].hi = g.n0 * (r + 1) / world;
       R[r].terms = terms + (size_t)r * nterm;
       if (steps > 1) {
-        st = alloc_list(scratch_need(g, R[r]), R[r].scratch, err);
+        st = alloc_list(scratch_need(g, R[r], inplace), R[r].scratch, err);
         for (void* q : R[r].scratch) owned.push_back(q);
       }
     }
@@ -1300,7 +1340,7 @@ int lf_run_slabs_local(const lf_plan* cplan, int world, void* const* terms, int 
         }
       return LF_OK;
     };
-    if (st == LF_OK) st = run_slabs_core(plan, g, R, steps, stream, plan->comm, exchange, err);
+    if (st == LF_OK) st = run_slabs_core(plan, g, R, steps, stream, plan->comm, exchange, err, nullptr, inplace);
     if (!owned.empty()) {
       cudaStreamSynchronize(stream);
       for (void* q : owned)

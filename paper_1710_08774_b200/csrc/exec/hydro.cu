@@ -631,12 +631,12 @@ int launch_step(const double* const in[4], double* const out[4], const double* d
 int run_inplace(const ExecArgs& a, std::string& err, bool adaptive = false) {
   const auto& r = a.plan->rs.ranges;
   const int ni = (int)r[1].trips();
-  if (a.slab && !a.whole_domain_parts) {
-    err = "in-place runs cover the whole domain (no slabs)";
-    return LF_ERR_UNSUPPORTED;
-  }
   const RowPart rp = row_part(a, (int)r[0].trips());
   const bool part = rp.lo > 0 || rp.hi < rp.rows;
+  if (a.slab && !a.whole_domain_parts && part) {  // a rank's slab: one launch over all of its rows
+    err = "in-place slab runs launch whole slabs (no face / interior parts)";
+    return LF_ERR_UNSUPPORTED;
+  }
   if (part && (a.steps != 1 || rp.hi - rp.lo < 2 * H || adaptive)) {
     err = "in-place row parts run one step at a time, span at least 4 rows and carry no per-step reduction";
     return LF_ERR_UNSUPPORTED;
@@ -678,6 +678,9 @@ int run_inplace(const ExecArgs& a, std::string& err, bool adaptive = false) {
     return launch_step(u, u, dtdx, ni, rp, a.stream, err, nullptr, false, &b);
   }
   int stt = LF_OK;
+  if (adaptive && a.slab)  // one step of a slab driver's schedule: it zeroes, combines and finalises
+    return launch_step(u, u, dtdx, ni, rp, a.stream, err, static_cast<unsigned long long*>(a.terms[9]),
+                       a.raw_max_input, &b);
   if (!adaptive) {
     for (int s = 0; s < a.steps && stt == LF_OK; ++s)
       stt = launch_step(u, u, dtdx, ni, rp, a.stream, err, nullptr, false, &b);

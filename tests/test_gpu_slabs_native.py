@@ -145,6 +145,47 @@ def test_local_slab_decomposition_matches_whole_domain(name, shape, steps, world
             assert np.array_equal(bits(_defined(name, g)), bits(_defined(name, r))), (name, world, t.name)
 
 
+@pytest.mark.parametrize("name,shape,steps,worlds", [("hydro", (24, 64), 3, [2, 3]), ("hydro", (40, 300), 2, [4]),
+                                                     ("hydro_adaptive", (24, 130), 3, [2, 3])])
+def test_local_slabs_in_place(name, shape, steps, worlds):
+    """Slab runs IN PLACE (config.aliases; every rank passes its state goals on
+    its axioms' slab buffers): whole-slab launches with deferred boundary
+    writes, then the exchange -- equal to the whole-domain ping-pong run."""
+    import torch
+    plan, ax = _case(name, shape)
+    spec = "hydro2d" if name == "hydro" else "hydro2d_adaptive"
+    ip = lf.Plan.with_ranges(spec, shape, inplace=True)
+    n0 = shape[0]
+    ref = _whole(plan, ax, steps)
+    for world in worlds:
+        ranges = [(n0 * r // world, n0 * (r + 1) // world) for r in range(world)]
+        rank_bufs = []
+        for lo, hi in ranges:
+            b = _slab_bufs(ip, ax, n0, lo, hi)
+            na = len(ip.axioms)
+            for k in range(4):  # the four state goals on their axioms' buffers
+                b[na + k] = b[k]
+            rank_bufs.append(b)
+        lf.run_slabs_local(ip, rank_bufs, steps=steps)
+        torch.cuda.synchronize()
+        got = _assemble(ip, rank_bufs, ranges, n0)
+        for g, r, t in zip(got, ref, ip.goals):
+            assert np.array_equal(bits(g), bits(r)), (name, world, t.name)
+    # a one-rank NCCL communicator: lf_run_slabs itself, in place
+    bufs = _slab_bufs(ip, ax, n0, 0, n0)
+    for k in range(4):
+        bufs[len(ip.axioms) + k] = bufs[k]
+    comm = lf.NcclComm.single()
+    try:
+        ip.run_slabs(bufs, comm, steps=steps)
+        torch.cuda.synchronize()
+        got = _assemble(ip, [bufs], [(0, n0)], n0)
+        for g, r, t in zip(got, ref, ip.goals):
+            assert np.array_equal(bits(g), bits(r)), (name, t.name)
+    finally:
+        comm.destroy()
+
+
 @pytest.mark.parametrize("name,shape,steps", [("heat3d", (12, 16, 40), 3), ("biharm", (30, 64), 2),
                                               ("hydro", (16, 48), 3), ("hydro_adaptive", (16, 48), 3),
                                               ("heat3d_jit", (8, 12, 40), 2)])
