@@ -102,9 +102,9 @@ WORKLOADS = {
     # configs[2] / configs[4] in place (config.aliases declared for every iterate pair,
     # goals passed on their axioms' buffers): one copy of the state instead of three
     "hydro_inplace": dict(config_index=2, spec="hydro2d", sizes=(4096, 4096), chain_steps=20, gen=_hydro_inputs,
-                          slab=None, dtype="f64", halo=(2, 2, False), inplace=True, alias=True),
+                          slab=_hydro_slab, dtype="f64", halo=(2, 2, False), inplace=True, alias=True),
     "hydro_large_inplace": dict(config_index=4, spec="hydro2d", sizes=(32768, 32768), chain_steps=10,
-                                gen=_hydro_inputs, slab=None, dtype="f64", halo=(2, 2, False), inplace=True,
+                                gen=_hydro_inputs, slab=_hydro_slab, dtype="f64", halo=(2, 2, False), inplace=True,
                                 alias=True),
     # the same chains written with `body:` expressions: the generic NVRTC path
     "heat3d_jit": dict(config_index=1, spec="examples/heat3d_body", sizes=(512, 512, 512), chain_steps=50,
@@ -341,7 +341,7 @@ def slab_parity(w, lf, comm, rank, world, dev, stream):
     if w["halo"] is None:
         return None
     sizes, steps = PARITY_3D if len(w["sizes"]) == 3 else PARITY_2D
-    plan = lf.Plan.with_ranges(w["spec"], sizes)
+    plan = lf.Plan.with_ranges(w["spec"], sizes, inplace=bool(w.get("alias")))
     n0 = sizes[0]
     lo, hi = slabs.slab_range(n0, rank, world)
 
@@ -352,7 +352,10 @@ def slab_parity(w, lf, comm, rank, world, dev, stream):
     local = w["slab"](sizes, lo, hi, reduce_max)
     d_ax = [torch.from_numpy(np.ascontiguousarray(h)).to(dev) for h in local]
     d_goal = []
-    for t in plan.goals:
+    for k, t in enumerate(plan.goals):
+        if w.get("inplace"):  # the timed run's mode: goals on the axioms' slab buffers
+            d_goal.append(d_ax[k])
+            continue
         ext = list(t.extent)
         ext[0] = ext[0] - n0 + (hi - lo)
         d_goal.append(torch.full(ext, float("nan"), dtype=getattr(torch, str(t.dtype)), device=dev))
@@ -477,8 +480,8 @@ def main():
         def one_step():
             plan.run(bufs, steps=w["chain_steps"], stream=stream)
     else:
-        if w.get("inplace"):
-            raise SystemExit("in-place workloads run on one GPU (slab runs need distinct buffers)")
+        if w.get("inplace") and not (w.get("alias") and args.slab_exchange == "native"):
+            raise SystemExit("in-place slab runs: the built-in Hydro2D executor through lf_run_slabs only")
         # outer-dimension slabs, faces exchanged by NCCL every time step
         n0 = w["sizes"][0]
         lo, hi = slabs.slab_range(n0, rank, world)
@@ -492,7 +495,10 @@ def main():
         d_ax = [torch.from_numpy(np.ascontiguousarray(h)).to(dev) for h in local]
         state = [i for i, t in enumerate(plan.axioms) if len(t.extent) > 0]
         d_goal = []
-        for t in plan.goals:
+        for k, t in enumerate(plan.goals):
+            if w.get("inplace"):  # every state goal on its axiom's slab buffer
+                d_goal.append(d_ax[k])
+                continue
             ext = list(t.extent)
             ext[0] = ext[0] - n0 + (hi - lo)  # same halo, local rows
             d_goal.append(torch.empty(ext, dtype=tdt(t), device=dev))
@@ -545,6 +551,8 @@ def main():
         sched = os.environ.get("LF_SLAB_SCHEDULE") or ("whole" if hi - lo >= 1024 else "parallel")
         # the Python exchange path (slabs.run_slabs_overlapped) always splits faces / interior
         per_step = 1 if args.slab_exchange == "native" and sched == "whole" else 3
+        if w.get("inplace"):
+            per_step = 2  # whole-slab launches only: the step and its band commit
         launches = per_step * plan.launches_per_step * w["chain_steps"]
 
     def barrier():
