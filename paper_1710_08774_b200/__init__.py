@@ -14,6 +14,7 @@ from __future__ import annotations
 
 import ctypes
 import json
+import re
 from dataclasses import dataclass
 from pathlib import Path
 from typing import Any, Sequence
@@ -488,8 +489,9 @@ def alias_iterates(text: str) -> str:
             raise ValueError("the spec already declares aliases")
         out.append(ln)
         if s.startswith("iterate:"):
-            pairs = [p.split(",") for p in s.split(":", 1)[1].strip()[2:-2].split("], [")]
-            if any(len(p) != 2 for p in pairs):
+            value = s.split(":", 1)[1].strip()
+            pairs = re.findall(r"\[\s*([^\[\],\s]+)\s*,\s*([^\[\],\s]+)\s*\]", value)
+            if not pairs or re.sub(r"\[\s*[^\[\],\s]+\s*,\s*[^\[\],\s]+\s*\]|[\s,]", "", value) != "[]":
                 raise ValueError("iterate: must be a flow sequence of [goal, axiom] pairs on one line")
             ind = ln[:len(ln) - len(ln.lstrip())]
             out.append(ind + "aliases: [" + ", ".join(f"[{a.strip()}, {g.strip()}]" for g, a in pairs) + "]")

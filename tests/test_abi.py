@@ -97,3 +97,23 @@ def test_buffer_arguments_are_checked_against_the_terminals():
         p.run([good, good.copy()])
     with pytest.raises(ValueError, match="CUDA tensor"):
         p.run([torch.zeros(t.extent, dtype=torch.float64)] * 2)
+
+
+def test_alias_iterates_declares_every_pair_and_the_plan_keeps_its_executor():
+    """Plan.with_ranges(..., inplace=True): every iterate pair becomes a
+    config.aliases entry (input then output, the reference's order); the chain
+    signature -- and so the hand-written executor -- does not depend on it."""
+    import paper_1710_08774_b200 as lf
+    text = lf.set_ranges(lf.spec_path("hydro2d").read_text(), (64, 256))
+    aliased = lf.alias_iterates(text)
+    line = [ln.strip() for ln in aliased.splitlines() if ln.strip().startswith("aliases:")]
+    assert line == ["aliases: [[g_rho, g_rho_n], [g_mx, g_mx_n], [g_my, g_my_n], [g_E, g_E_n]]"]
+    assert lf.alias_iterates("config:\n  iterate: [[a_n,a],[ b_n , b ]]\n").count("aliases: [[a, a_n], [b, b_n]]") == 1
+    import pytest
+    with pytest.raises(ValueError):
+        lf.alias_iterates(aliased)  # already declared
+    with pytest.raises(ValueError):
+        lf.alias_iterates("config:\n  iterate: [[a_n, a], b]\n")
+    plain, inplace = lf.Plan(text, "h.lf"), lf.Plan(aliased, "h.lf")
+    assert plain.executor == inplace.executor == "hydro2d_fused_tma"
+    assert plain.report()["signature"] == inplace.report()["signature"]
