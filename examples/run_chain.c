@@ -57,7 +57,14 @@ int main(int argc, char** argv) {
     printf("%s %s %s bytes %lld extent", t.is_goal ? "goal" : "axiom", t.type, t.name, (long long)t.bytes);
     for (int d = 0; d < t.ndim; ++d) printf(" %lld", (long long)t.extent[d]);
     printf("\n");
-    bufs[i] = calloc(1, (size_t)(t.bytes > 0 ? t.bytes : 8));
+    /* a goal given the SAME file as an axiom shares that axiom's buffer: an
+     * in-place run (the spec must declare the pair in config.aliases) */
+    for (int k = 0; t.is_goal && k < i && !bufs[i]; ++k)
+      if (argc > 3 + i && argc > 3 + k && strcmp(argv[3 + i], argv[3 + k]) == 0) {
+        bufs[i] = bufs[k];
+        printf("goal %s in place on terminal %d\n", t.name, k);
+      }
+    if (!bufs[i]) bufs[i] = calloc(1, (size_t)(t.bytes > 0 ? t.bytes : 8));
     if (!t.is_goal && argc > 3 + i) {
       size_t n = 0;
       char* data = slurp(argv[3 + i], &n);
@@ -85,7 +92,11 @@ int main(int argc, char** argv) {
     }
     printf("ran %d steps\n", steps);
   }
-  for (int i = 0; i < nt; ++i) free(bufs[i]);
+  for (int i = 0; i < nt; ++i) {
+    int shared = 0;
+    for (int k = 0; k < i; ++k) shared |= bufs[k] == bufs[i];
+    if (!shared) free(bufs[i]);
+  }
   free(bufs);
   lf_plan_destroy(plan);
   free(spec);

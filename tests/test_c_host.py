@@ -51,3 +51,30 @@ def test_c_program_runs_bit_exact(tmp_path):
     got = np.fromfile(fout, dtype=np.float64).reshape(u.shape)
     ref = oracle.heat3d(u, 3)
     assert np.array_equal(got[1:-1, 1:-1, 1:-1].view(np.uint64), ref[1:-1, 1:-1, 1:-1].view(np.uint64))
+
+
+@pytest.mark.gpu
+def test_c_program_runs_hydro_in_place(tmp_path):
+    """The C ABI in place from a C host program: goals given the axioms' files
+    share the axioms' host buffers; lf_run_host keeps one device buffer per pair."""
+    import oracle
+    from paper_1710_08774_b200 import inputs
+    exe = build_exe(tmp_path)
+    shape = (40, 200)
+    spec = tmp_path / "hydro_inplace.lf"
+    spec.write_text(lf.alias_iterates(lf.set_ranges(lf.spec_path("hydro2d").read_text(), shape)))
+    st, dtdx = inputs.hydro_input(*shape, seed=8)
+    files = []
+    for name, a in zip(("rho", "mx", "my", "E"), st):
+        f = tmp_path / f"{name}.bin"
+        a.tofile(f)
+        files.append(str(f))
+    fd = tmp_path / "dtdx.bin"
+    np.array([dtdx]).tofile(fd)
+    out = subprocess.run([str(exe), str(spec), "3"] + files + [str(fd)] + files, capture_output=True, text=True,
+                         check=True).stdout
+    assert "executor hydro2d_fused_tma" in out and out.count("in place on terminal") == 4 and "ran 3 steps" in out
+    ref = oracle.hydro(st, dtdx, 3)
+    for v, f in enumerate(files):
+        got = np.fromfile(f, dtype=np.float64).reshape(st[v].shape)
+        assert np.array_equal(got.view(np.uint64), ref[v].view(np.uint64)), v
