@@ -106,6 +106,8 @@ WORKLOADS = {
     "hydro_large_inplace": dict(config_index=4, spec="hydro2d", sizes=(32768, 32768), chain_steps=10,
                                 gen=_hydro_inputs, slab=_hydro_slab, dtype="f64", halo=(2, 2, False), inplace=True,
                                 alias=True),
+    "biharm_inplace": dict(config_index=0, spec="biharmonic2d", sizes=(4096, 4096), chain_steps=100,
+                           gen=_biharm_inputs, slab=None, dtype="f64", halo=(2, 2, False), inplace=True, alias=True),
     # the same chains written with `body:` expressions: the generic NVRTC path
     "heat3d_jit": dict(config_index=1, spec="examples/heat3d_body", sizes=(512, 512, 512), chain_steps=50,
                        gen=_heat3d_inputs, slab=_heat3d_slab, dtype="f64", halo=(1, 1, True)),

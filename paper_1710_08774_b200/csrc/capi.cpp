@@ -707,8 +707,9 @@ static int exec_inplace_pairs(const lf_plan* plan, void* const* terms, std::vect
 static int slab_inplace(const lf_plan* plan, void* const* terms, bool& inplace, std::string& err) {
   inplace = shares_buffer(plan, terms);
   if (!inplace) return LF_OK;
-  if (!plan->exec) {
-    err = "slab runs of the generic executor need distinct axiom and goal buffers (its in-place runs cover the whole domain)";
+  if (!plan->exec || !plan->exec->inplace_parts) {
+    err = std::string("slab runs of ") + (plan->exec ? plan->exec->name : "the generic executor") +
+          " need distinct axiom and goal buffers (its in-place runs cover the whole domain)";
     return LF_ERR_UNSUPPORTED;
   }
   std::vector<int> share;
@@ -1078,7 +1079,7 @@ int lf_run_host(const lf_plan* cplan, void* const* terms, int nterm, int steps) 
       int parts = static_cast<int>(std::min<long>(32, n0 / 512));  // 32: measured best for the 16384^2 box pass
       if (const char* e = lfx::option("LF_HOST_PARTS")) parts = std::atoi(e);
       const bool reduces = plan->exec && plan->exec->max_reduce;
-      const bool inplace_parts = inplace && plan->exec && plan->exec->inplace;
+      const bool inplace_parts = inplace && plan->exec && plan->exec->inplace_parts;
       if ((!inplace || inplace_parts) && !nests && !(reduces && inplace) && parts >= 2) {
         st = run_host_pipelined(plan, terms, dterms, parts, steps, err, inplace);
         if (st != kNotPipelined) {

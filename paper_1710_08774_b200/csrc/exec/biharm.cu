@@ -48,7 +48,19 @@ struct Params {
   int write_ghost_top, write_ghost_bottom;
   int store_policy;   // L2 policy of the output stores (l2_store_policy)
   int load_policy;    // -1: plain TMA fetches, else l2_store_policy mode for the fetched lines
+  // in place (out == the staged array; config.aliases): the cells other CTAs
+  // still read -- the edge lanes' column pair next to a strip boundary, the two
+  // rows next to a segment cut -- go to these bands, biharm_commit copies them in
+  double* colband;    // [strips-1][nj][4]: two columns either side of every strip boundary
+  double* rowband;    // [ctas][3 segments][4 rows][SW]
 };
+
+// slot 0..3 of row j in its segment's row band (-1: not deferred)
+__device__ __forceinline__ int band_row_slot(int j, int jb, int je, bool cut_above, bool cut_below) {
+  if (cut_above && j - jb < H) return j - jb;
+  if (cut_below && je - j <= H) return H + (j - (je - H));
+  return -1;
+}
 
 template <int CPL>
 struct Win {
@@ -197,7 +209,9 @@ __device__ __forceinline__ void biharm_row4(Win4<CPL>& w, const double* row, int
   }
 }
 
-template <class K>
+// IP: in place (RR == 4 only) -- a warp writes row j of its strip after it has
+// consumed row j+3, so its own reads are never overtaken; see Params.
+template <class K, bool IP = false>
 __global__ void __launch_bounds__(32, K::OCC)
     biharm_fused(const __grid_constant__ CUtensorMap tin, double* __restrict__ out, const Params p) {
   constexpr int CPL = K::CPL, S = K::S, SW = K::SW, BOXW = K::BOXW, STAGE_BYTES = K::STAGE_BYTES;
@@ -283,16 +297,45 @@ __global__ void __launch_bounds__(32, K::OCC)
     // rows jb-3 .. je+2 (the ring stages from jb-3: halo H+1); output row r-3
     const int T = sg.je - sg.jb + 2 * H + 2;
     double* orow = out + (long long)(sg.jb - 4) * p.pitch + H + sg.strip * SW;
+    // in place: where the lane's pair of marched row t goes (biharm_row4 stores at
+    // dest + CPL * lane).  An edge lane next to a neighbouring strip walks the
+    // column band (4 doubles per row) instead of the grid (one pitch per row);
+    // the rows next to a segment cut -- the first two and the last two output
+    // rows, marched rows 6, 7 and T-2, T-1 -- go to the row band.
+    [[maybe_unused]] double* lp = orow;
+    [[maybe_unused]] long long ls = p.pitch;
+    if constexpr (IP) {
+      const bool cl = lane == 0 && sg.strip > 0, cr = lane == 31 && sg.strip < p.strips - 1;
+      if (cl || cr) {
+        lp = p.colband + ((long long)((cl ? sg.strip - 1 : sg.strip) * (long long)p.nj + (sg.jb - 6)) * 4 + (cl ? 2 : 0)) -
+             CPL * lane;
+        ls = 4;
+      }
+    }
+    auto dest = [&](int t, double* grid) -> double* {
+      if constexpr (!IP) {
+        return grid;  // the plain kernel: exactly the row pointer it always used
+      } else {
+        double* d = lp;
+        lp += ls;
+        if (t < 6 + H || t >= T - H) {
+          const int jo = sg.jb - 6 + t;  // output row of marched row t
+          const int rs = band_row_slot(jo, sg.jb, sg.je, sg.jb > p.row_lo, sg.je < p.row_hi);
+          if (rs >= 0) d = p.rowband + (size_t)(((blockIdx.x * 3 + k) * 4 + rs) * SW);
+        }
+        return d;
+      }
+    };
     for (int t0 = 0; t0 < T; t0 += 4, ++g) {
       rr.wait(g);
       const double* st = reinterpret_cast<const double*>(rr.stage(g));
-      biharm_row4<CPL, 0>(w, st, t0, lane, ex_col, orow, pol);
+      biharm_row4<CPL, 0>(w, st, t0, lane, ex_col, dest(t0, orow), pol);
       orow += p.pitch;
-      if (t0 + 1 < T) biharm_row4<CPL, 1>(w, st + BOXW, t0 + 1, lane, ex_col, orow, pol);
+      if (t0 + 1 < T) biharm_row4<CPL, 1>(w, st + BOXW, t0 + 1, lane, ex_col, dest(t0 + 1, orow), pol);
       orow += p.pitch;
-      if (t0 + 2 < T) biharm_row4<CPL, 2>(w, st + 2 * BOXW, t0 + 2, lane, ex_col, orow, pol);
+      if (t0 + 2 < T) biharm_row4<CPL, 2>(w, st + 2 * BOXW, t0 + 2, lane, ex_col, dest(t0 + 2, orow), pol);
       orow += p.pitch;
-      if (t0 + 3 < T) biharm_row4<CPL, 3>(w, st + 3 * BOXW, t0 + 3, lane, ex_col, orow, pol);
+      if (t0 + 3 < T) biharm_row4<CPL, 3>(w, st + 3 * BOXW, t0 + 3, lane, ex_col, dest(t0 + 3, orow), pol);
       orow += p.pitch;
       __syncwarp();
       if (lane == 0) rr.issue(g + S, &tin);
@@ -302,6 +345,41 @@ __global__ void __launch_bounds__(32, K::OCC)
   }
 }
 
+
+// In-place step, second launch: the deferred cells go to their places (same
+// grid and segment list as the step's launch; the zero ghost ring needs none).
+constexpr int COMMIT_NT = 128;  // the copies are latency-bound: a CTA's rows in one or two round trips
+template <class K>
+__global__ void __launch_bounds__(COMMIT_NT) biharm_commit(double* __restrict__ out, const Params p) {
+  constexpr int SW = K::SW;
+  const int tid = threadIdx.x;
+  if (tid == 0) pdl_trigger();
+  pdl_wait();  // every CTA of the step has finished reading the array
+  RowSeg seg[3];
+  const int nseg = cta_segments(blockIdx.x, gridDim.x, p.strips, p.row_lo, p.row_hi, seg);
+  for (int k = 0; k < nseg; ++k) {
+    const RowSeg sg = seg[k];
+    const bool above = sg.jb > p.row_lo, below = sg.je < p.row_hi;
+    for (int idx = tid; idx < 2 * H * SW; idx += COMMIT_NT) {
+      const int rs = idx / SW, c = idx % SW;
+      const int j = rs < H ? sg.jb + rs : sg.je - 2 * H + rs;
+      if (j < sg.jb || j >= sg.je || band_row_slot(j, sg.jb, sg.je, above, below) != rs) continue;
+      out[(long long)(j + H) * p.pitch + H + sg.strip * SW + c] =
+          p.rowband[(size_t)(((blockIdx.x * 3 + k) * 4 + rs) * SW) + c];
+    }
+    const bool left = sg.strip > 0, right = sg.strip < p.strips - 1;
+    if (!left && !right) continue;
+    // thread (row, q): q = 0,1 the strip's first two columns, 2,3 its last two
+    for (int idx = tid; idx < (sg.je - sg.jb) * 4; idx += COMMIT_NT) {
+      const int j = sg.jb + (idx >> 2), q = idx & 3;
+      if (q < 2 ? !left : !right) continue;
+      if (band_row_slot(j, sg.jb, sg.je, above, below) >= 0) continue;
+      const size_t e = q < 2 ? sg.strip - 1 : sg.strip;
+      out[(long long)(j + H) * p.pitch + H + sg.strip * SW + (q < 2 ? q : SW - 4 + q)] =
+          p.colband[(e * p.nj + j) * 4 + (q < 2 ? 2 + q : q - 2)];
+    }
+  }
+}
 
 // variant table (LF_BIHARM_VARIANT=<index> overrides the default for tuning runs)
 struct Variant {
@@ -389,6 +467,7 @@ int launch_step(const double* in, double* out, int ni, const RowPart& rp, cudaSt
     return e ? std::atoi(e) : 1;
   }();
   p.load_policy = load_policy;
+  p.colband = p.rowband = nullptr;
   // at least ~16 rows per CTA so the 4 priming rows stay a small fraction
   const int ctas = rowstream_ctas(slots, p.strips, rp.hi - rp.lo);
   if ((long long)ctas * 2 < p.strips) {
@@ -399,7 +478,78 @@ int launch_step(const double* in, double* out, int ni, const RowPart& rp, cudaSt
                      err);
 }
 
+// Whole-domain steps on ONE buffer (the caller passed g_unew on g_u's buffer,
+// declared in config.aliases): the default four-row variant's in-place build,
+// then the band commit, per step.  Bands are plan-owned: 4 columns per strip
+// boundary and 4 rows per segment cut.
+int run_inplace(const ExecArgs& a, std::string& err) {
+  using K = Cfg<2, 7, 12, 4>;  // = the default variant (cpl2_r4_s7_occ12)
+  static_assert(K::CPL == H, "an edge lane's columns are exactly the neighbour strip's halo");
+  const auto& r = a.plan->rs.ranges;
+  const int ni = (int)r[1].trips();
+  const RowPart rp = row_part(a, (int)r[0].trips());
+  if (a.slab || !a.mem) {
+    err = "biharm2d_fused_tma runs in place on the whole domain only (no slabs or row parts)";
+    return LF_ERR_UNSUPPORTED;
+  }
+  double* u = static_cast<double*>(a.terms[0]);
+  void (*const kern)(CUtensorMap, double*, Params) = biharm_fused<K, true>;
+  static LaunchCache cache;
+  int slots = 0;
+  if (int s = resident_slots(cache, reinterpret_cast<const void*>(kern), 32, K::SMEM, K::OCC,
+                             "cudaFuncSetAttribute(biharm in place)", &slots, err))
+    return s;
+  Params p;
+  p.ni = ni;
+  p.nj = rp.rows;
+  p.pitch = ni + 4;
+  p.strips = ni / K::SW;
+  p.row_lo = rp.lo;
+  p.row_hi = rp.hi;
+  p.write_ghost_top = rp.top;
+  p.write_ghost_bottom = rp.bottom;
+  p.store_policy = 2;
+  p.load_policy = 1;
+  const int ctas = rowstream_ctas(slots, p.strips, rp.hi - rp.lo);
+  if ((long long)ctas * 2 < p.strips) {
+    err = "row range too short for the resident grid";
+    return LF_ERR_UNSUPPORTED;
+  }
+  const size_t ncol = (size_t)std::max(0, p.strips - 1) * p.nj * 4, nrow = (size_t)ctas * 3 * 4 * K::SW;
+  cudaError_t e = a.mem->ensure((ncol + nrow) * sizeof(double));
+  if (e != cudaSuccess) return cuda_status(e, "cudaMalloc(biharm bands)", err);
+  p.colband = static_cast<double*>(a.mem->ptr);
+  p.rowband = p.colband + ncol;
+  CUtensorMap map;
+  uint64_t dims[2] = {(uint64_t)ni + 4, (uint64_t)p.nj + 4};
+  uint32_t box[2] = {(uint32_t)(K::SW + 2 * H), (uint32_t)K::RR};
+  if (!make_tensor_map(&map, u, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 8, 2, dims, box, err)) return LF_ERR_CUDA;
+  // LF_BIHARM_IP_PDL (tuning): bit 0 = the step, bit 1 = the commit launched with
+  // programmatic stream serialization
+  const char* o = lfx::option("LF_BIHARM_IP_PDL");
+  const int pdl = o ? std::atoi(o) : 1;
+  for (int s = 0; s < a.steps; ++s) {
+    cudaError_t ce;
+    if (pdl & 1) {
+      ce = launch_pdl(kern, dim3(ctas), dim3(32), K::SMEM, a.stream, map, u, p);
+    } else {
+      kern<<<ctas, 32, K::SMEM, a.stream>>>(map, u, p);
+      ce = cudaGetLastError();
+    }
+    if (int st = cuda_status(ce, "biharm_fused (in place) launch", err)) return st;
+    if (pdl & 2) {
+      ce = launch_pdl(biharm_commit<K>, dim3(ctas), dim3(COMMIT_NT), 0, a.stream, u, p);
+    } else {
+      biharm_commit<K><<<ctas, COMMIT_NT, 0, a.stream>>>(u, p);
+      ce = cudaGetLastError();
+    }
+    if (int st = cuda_status(ce, "biharm_commit launch", err)) return st;
+  }
+  return LF_OK;
+}
+
 int run(const ExecArgs& a, std::string& err) {
+  if (a.inplace) return run_inplace(a, err);
   const auto& r = a.plan->rs.ranges;
   const int ni = (int)r[1].trips();
   const RowPart rp = row_part(a, (int)r[0].trips());
@@ -417,6 +567,7 @@ int run(const ExecArgs& a, std::string& err) {
 
 }  // namespace
 
-extern const Executor biharm_executor = {"biharm2d_fused_tma", "biharmonic2d.lf", 1, 16.0, supports, run};
+extern const Executor biharm_executor = {"biharm2d_fused_tma", "biharmonic2d.lf", 1, 16.0, supports, run,
+                                         nullptr, false, nullptr, /*inplace=*/true};
 
 }  // namespace lfx

@@ -87,6 +87,8 @@ struct Executor {
   // runs whole-domain steps (and ordered row parts, see ExecArgs) in place when
   // every iterated goal is passed on its aliased axiom's buffer (ExecArgs::inplace)
   bool inplace = false;
+  // ... and also whole slabs (lf_run_slabs) and ordered row parts (pipelined host runs)
+  bool inplace_parts = false;
 };
 
 // all executors compiled into this library

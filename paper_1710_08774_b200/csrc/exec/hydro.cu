@@ -782,9 +782,9 @@ int finalize_adaptive(const ExecArgs& a, std::string& err) {
 }  // namespace
 
 extern const Executor hydro_executor = {"hydro2d_fused_tma", "hydro2d.lf", 1, 64.0, supports, run,
-                                        nullptr, false, nullptr, /*inplace=*/true};
+                                        nullptr, false, nullptr, /*inplace=*/true, /*inplace_parts=*/true};
 extern const Executor hydro_adaptive_executor = {"hydro2d_adaptive_fused_tma", "hydro2d_adaptive.lf", 1, 64.0,
                                                  supports, run_adaptive, nullptr, true, finalize_adaptive,
-                                                 /*inplace=*/true};
+                                                 /*inplace=*/true, /*inplace_parts=*/true};
 
 }  // namespace lfx

@@ -36,6 +36,39 @@ def test_device_path_matches_naive(shape, steps):
     assert np.array_equal(bits(got), bits(ref))
 
 
+# in place (config.aliases: g_unew on g_u's buffer): one strip and several, cuts
+# inside strips, fewer rows than the row-band depth
+@pytest.mark.parametrize("shape,steps", [((1, 128), 2), ((5, 128), 3), ((37, 256), 3), ((64, 384), 4),
+                                         ((200, 256), 2), ((333, 128), 5), ((700, 1024), 3)])
+def test_in_place_matches_naive(shape, steps):
+    import torch
+    plan = lf.Plan.with_ranges("biharmonic2d", shape, inplace=True)
+    assert plan.executor == "biharm2d_fused_tma"
+    u = inputs.biharm_input(*shape, seed=sum(shape) + 1)
+    du = torch.from_numpy(u).cuda()
+    plan.run([du, du], steps=steps)
+    torch.cuda.synchronize()
+    got = du.cpu().numpy()
+    ref = oracle.biharm(u, steps)
+    assert np.array_equal(bits(got), bits(ref)), int(np.count_nonzero(got != ref))
+    # host path: one device buffer
+    h = u.copy()
+    plan.run_host([h, h], steps=steps)
+    assert np.array_equal(bits(h), bits(ref))
+
+
+def test_in_place_full_size_4096_and_undeclared_alias():
+    import torch
+    plan = lf.Plan.with_ranges("biharmonic2d", (4096, 4096), inplace=True)
+    u = inputs.biharm_input(4096, 4096, seed=0)
+    du = torch.from_numpy(u).cuda()
+    plan.run([du, du], steps=5)
+    torch.cuda.synchronize()
+    assert np.array_equal(bits(du.cpu().numpy()), bits(oracle.biharm(u, 5, fused=True)))
+    with pytest.raises(lf.LoomfuseError, match="config.aliases does not declare"):
+        lf.Plan.bundled("biharmonic2d").run([du, du], steps=1)
+
+
 def test_host_path_and_reuse():
     shape = (48, 128)
     plan = lf.Plan.with_ranges("biharmonic2d", shape)
