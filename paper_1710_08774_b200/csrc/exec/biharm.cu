@@ -360,23 +360,24 @@ __global__ void __launch_bounds__(COMMIT_NT) biharm_commit(double* __restrict__ 
   for (int k = 0; k < nseg; ++k) {
     const RowSeg sg = seg[k];
     const bool above = sg.jb > p.row_lo, below = sg.je < p.row_hi;
-    for (int idx = tid; idx < 2 * H * SW; idx += COMMIT_NT) {
-      const int rs = idx / SW, c = idx % SW;
+    // 16-B pieces: a thread moves a column pair (all offsets are even: SW, H and the pitch are)
+    for (int idx = tid; idx < 2 * H * (SW / 2); idx += COMMIT_NT) {
+      const int rs = idx / (SW / 2), c = 2 * (idx % (SW / 2));
       const int j = rs < H ? sg.jb + rs : sg.je - 2 * H + rs;
       if (j < sg.jb || j >= sg.je || band_row_slot(j, sg.jb, sg.je, above, below) != rs) continue;
-      out[(long long)(j + H) * p.pitch + H + sg.strip * SW + c] =
-          p.rowband[(size_t)(((blockIdx.x * 3 + k) * 4 + rs) * SW) + c];
+      *reinterpret_cast<double2*>(out + (long long)(j + H) * p.pitch + H + sg.strip * SW + c) =
+          *reinterpret_cast<const double2*>(p.rowband + (size_t)(((blockIdx.x * 3 + k) * 4 + rs) * SW) + c);
     }
     const bool left = sg.strip > 0, right = sg.strip < p.strips - 1;
     if (!left && !right) continue;
-    // thread (row, q): q = 0,1 the strip's first two columns, 2,3 its last two
-    for (int idx = tid; idx < (sg.je - sg.jb) * 4; idx += COMMIT_NT) {
-      const int j = sg.jb + (idx >> 2), q = idx & 3;
-      if (q < 2 ? !left : !right) continue;
+    // thread (row, side): side 0 the strip's first two columns, 1 its last two
+    for (int idx = tid; idx < (sg.je - sg.jb) * 2; idx += COMMIT_NT) {
+      const int j = sg.jb + (idx >> 1), side = idx & 1;
+      if (side == 0 ? !left : !right) continue;
       if (band_row_slot(j, sg.jb, sg.je, above, below) >= 0) continue;
-      const size_t e = q < 2 ? sg.strip - 1 : sg.strip;
-      out[(long long)(j + H) * p.pitch + H + sg.strip * SW + (q < 2 ? q : SW - 4 + q)] =
-          p.colband[(e * p.nj + j) * 4 + (q < 2 ? 2 + q : q - 2)];
+      const size_t e = side == 0 ? sg.strip - 1 : sg.strip;
+      *reinterpret_cast<double2*>(out + (long long)(j + H) * p.pitch + H + sg.strip * SW + (side == 0 ? 0 : SW - 2)) =
+          *reinterpret_cast<const double2*>(p.colband + (e * p.nj + j) * 4 + (side == 0 ? 2 : 0));
     }
   }
 }
