@@ -143,7 +143,9 @@ const char* lf_plan_source(const lf_plan* plan);
  * an axiom and its goal that `config: aliases:` declares runs the chain in
  * place, on the generic executor or on the hand-written Hydro2D executor
  * (which takes all four state pairs in place together); LF_ERR_UNSUPPORTED
- * otherwise.  One multi-step run per plan at a time. */
+ * otherwise.  One multi-step run per plan at a time (the ping-pong scratch
+ * and the in-place bands are plan-owned); create one plan per concurrent
+ * stream. */
 int lf_run(const lf_plan* plan, void* const* terminals, int nterm, int steps, void* cuda_stream);
 
 /* Same on HOST buffers: copies axioms host->device, runs, copies goals
