@@ -517,9 +517,10 @@ int run_inplace(const ExecArgs& a, std::string& err) {
     return LF_ERR_UNSUPPORTED;
   }
   const size_t ncol = (size_t)std::max(0, p.strips - 1) * p.nj * 4, nrow = (size_t)ctas * 3 * 4 * K::SW;
-  cudaError_t e = a.mem->ensure((ncol + nrow) * sizeof(double));
-  if (e != cudaSuccess) return cuda_status(e, "cudaMalloc(biharm bands)", err);
-  p.colband = static_cast<double*>(a.mem->ptr);
+  const size_t band_bytes = (ncol + nrow) * sizeof(double);
+  void* band_ptr = nullptr;
+  if (int s = band_memory(*a.mem, band_bytes, a.stream, &band_ptr, err)) return s;
+  p.colband = static_cast<double*>(band_ptr);
   p.rowband = p.colband + ncol;
   CUtensorMap map;
   uint64_t dims[2] = {(uint64_t)ni + 4, (uint64_t)p.nj + 4};
@@ -546,7 +547,7 @@ int run_inplace(const ExecArgs& a, std::string& err) {
     }
     if (int st = cuda_status(ce, "biharm_commit launch", err)) return st;
   }
-  return LF_OK;
+  return band_guard_check(*a.mem, band_bytes, a.stream, err);
 }
 
 int run(const ExecArgs& a, std::string& err) {

@@ -42,6 +42,16 @@ struct ExecMem {
   }
 };
 
+// In-place band memory with guard zones (LF_BAND_GUARD=1; compute-sanitizer is
+// not available on every pool): `need` bytes for the executor at the returned
+// pointer, kBandGuard bytes of a canary before and after it.  band_guard_check
+// -- after the run's last launch; synchronises -- fails with LF_ERR_INTERNAL
+// when a band store went outside [ptr, ptr + need).  Without the switch:
+// a plain ensure(), and the check returns LF_OK at once.
+constexpr size_t kBandGuard = 4096;
+int band_memory(ExecMem& mem, size_t need, cudaStream_t stream, void** ptr, std::string& err);
+int band_guard_check(const ExecMem& mem, size_t need, cudaStream_t stream, std::string& err);
+
 struct ExecArgs {
   const lf::Plan* plan = nullptr;
   void* const* terms = nullptr;  // device pointers, axioms then goals

@@ -1,6 +1,7 @@
 // Host helpers shared by the executors: TMA descriptor encoding through the
 // runtime's driver entry point, CUDA error mapping.
 #include <algorithm>
+#include <vector>
 #include <cstdlib>
 #include <mutex>
 
@@ -35,6 +36,43 @@ int resident_slots(LaunchCache& cache, const void* kernel, int threads, int smem
   });
   if (cache.err[dev] != cudaSuccess) return cuda_status(cache.err[dev], what, err);
   *slots = cache.slots[dev];
+  return LF_OK;
+}
+
+static bool band_guard_on() {
+  const char* e = option("LF_BAND_GUARD");
+  return e && std::atoi(e) != 0;
+}
+
+int band_memory(ExecMem& mem, size_t need, cudaStream_t stream, void** ptr, std::string& err) {
+  const bool guard = band_guard_on();
+  cudaError_t e = mem.ensure(need + (guard ? 2 * kBandGuard : 0));
+  if (e != cudaSuccess) return cuda_status(e, "cudaMalloc(in-place bands)", err);
+  char* base = static_cast<char*>(mem.ptr);
+  if (guard) {  // canary bytes 0xA5 either side of the executor's range
+    e = cudaMemsetAsync(base, 0xA5, kBandGuard, stream);
+    if (e == cudaSuccess) e = cudaMemsetAsync(base + kBandGuard + need, 0xA5, kBandGuard, stream);
+    if (e != cudaSuccess) return cuda_status(e, "cudaMemsetAsync(band guard)", err);
+    base += kBandGuard;
+  }
+  *ptr = base;
+  return LF_OK;
+}
+
+int band_guard_check(const ExecMem& mem, size_t need, cudaStream_t stream, std::string& err) {
+  if (!band_guard_on()) return LF_OK;
+  std::vector<unsigned char> h(2 * kBandGuard);
+  const char* base = static_cast<const char*>(mem.ptr);
+  cudaError_t e = cudaStreamSynchronize(stream);
+  if (e == cudaSuccess) e = cudaMemcpy(h.data(), base, kBandGuard, cudaMemcpyDeviceToHost);
+  if (e == cudaSuccess) e = cudaMemcpy(h.data() + kBandGuard, base + kBandGuard + need, kBandGuard, cudaMemcpyDeviceToHost);
+  if (e != cudaSuccess) return cuda_status(e, "band guard read-back", err);
+  for (size_t i = 0; i < h.size(); ++i)
+    if (h[i] != 0xA5) {
+      err = "in-place band store outside its buffer (guard byte " + std::to_string(i % kBandGuard) +
+            (i < kBandGuard ? " before" : " after") + " the bands)";
+      return LF_ERR_INTERNAL;
+    }
   return LF_OK;
 }
 

@@ -660,9 +660,11 @@ int run_inplace(const ExecArgs& a, std::string& err, bool adaptive = false) {
     err = "in-place run without plan-owned band memory";
     return LF_ERR_INTERNAL;
   }
-  cudaError_t e = a.mem->ensure((ncol + nrow * a.inplace_slots + 2) * sizeof(double));
-  if (e != cudaSuccess) return cuda_status(e, "cudaMalloc(hydro bands)", err);
-  double* mem = static_cast<double*>(a.mem->ptr);
+  const size_t band_bytes = (ncol + nrow * a.inplace_slots + 2) * sizeof(double);
+  void* band_ptr = nullptr;
+  if (int s = band_memory(*a.mem, band_bytes, a.stream, &band_ptr, err)) return s;
+  double* mem = static_cast<double*>(band_ptr);
+  cudaError_t e = cudaSuccess;
   Bands b;
   b.col = mem;
   b.row = mem + ncol + nrow * a.inplace_slot;
@@ -675,7 +677,8 @@ int run_inplace(const ExecArgs& a, std::string& err, bool adaptive = false) {
     } else {
       b.commit_mode = b.defer_bottom ? 1 : 0;
     }
-    return launch_step(u, u, dtdx, ni, rp, a.stream, err, nullptr, false, &b);
+    if (int s = launch_step(u, u, dtdx, ni, rp, a.stream, err, nullptr, false, &b)) return s;
+    return band_guard_check(*a.mem, band_bytes, a.stream, err);
   }
   int stt = LF_OK;
   if (adaptive && a.slab)  // one step of a slab driver's schedule: it zeroes, combines and finalises
@@ -684,7 +687,7 @@ int run_inplace(const ExecArgs& a, std::string& err, bool adaptive = false) {
   if (!adaptive) {
     for (int s = 0; s < a.steps && stt == LF_OK; ++s)
       stt = launch_step(u, u, dtdx, ni, rp, a.stream, err, nullptr, false, &b);
-    return stt;
+    return stt != LF_OK ? stt : band_guard_check(*a.mem, band_bytes, a.stream, err);
   }
   double* dgoal = static_cast<double*>(a.terms[9]);
   double* dslot = mem + ncol + nrow * a.inplace_slots;
@@ -705,7 +708,8 @@ int run_inplace(const ExecArgs& a, std::string& err, bool adaptive = false) {
   }
   if (stt != LF_OK) return stt;
   cfl_finalize<<<1, 1, 0, a.stream>>>(dgoal);
-  return cuda_status(cudaGetLastError(), "cfl_finalize launch", err);
+  if (int s = cuda_status(cudaGetLastError(), "cfl_finalize launch", err)) return s;
+  return band_guard_check(*a.mem, band_bytes, a.stream, err);
 }
 
 int run(const ExecArgs& a, std::string& err) {

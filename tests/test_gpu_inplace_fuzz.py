@@ -81,3 +81,35 @@ def test_biharm_in_place_equals_ping_pong(seed):
     plan.run([dv, dv], steps=steps)
     torch.cuda.synchronize()
     assert torch.equal(dv.view(torch.int64), out.view(torch.int64)), (nj, ni, steps)
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_band_stores_stay_inside_their_buffers(seed, monkeypatch):
+    """LF_BAND_GUARD=1: canary zones either side of the plan-owned bands, checked
+    after every in-place run (stands in for compute-sanitizer memcheck, which the
+    GPU pool does not allow): device runs, the host wavefront, the adaptive chain
+    and the biharmonic chain on shapes whose last strip / segment is ragged."""
+    import torch
+    rng = np.random.default_rng(3000 + seed)
+    nj, ni, steps = int(rng.integers(4, 300)), 2 * int(rng.integers(2, 600)), int(rng.integers(1, 5))
+    st, dtdx = inputs.hydro_input(nj, ni, seed=seed)
+    ref = _hydro_pingpong((nj, ni), st, dtdx, steps)
+    with lf.option("LF_BAND_GUARD", 1):
+        plan = lf.Plan.with_ranges("hydro2d", (nj, ni), inplace=True)
+        d = torch.tensor([dtdx], dtype=torch.float64, device="cuda")
+        u = [torch.from_numpy(a).cuda() for a in st]
+        plan.run(u + [d] + u, steps=steps)
+        torch.cuda.synchronize()
+        for v in range(4):
+            assert torch.equal(u[v].view(torch.int64), ref[v].view(torch.int64)), v
+        monkeypatch.setenv("LF_HOST_WAVEFRONT", "1")
+        monkeypatch.setenv("LF_HOST_PARTS", str(max(2, nj // 8)))
+        h = [a.copy() for a in st]
+        plan.run_host(h + [np.array([dtdx])] + h, steps=max(2, steps))
+        ad = lf.Plan.with_ranges("hydro2d_adaptive", (nj, ni), inplace=True)
+        u = [torch.from_numpy(a).cuda() for a in st]
+        ad.run(u + [d.reshape(())] + u + [torch.zeros((), dtype=torch.float64, device="cuda")], steps=steps)
+        bj, bi = int(rng.integers(1, 300)), 128 * int(rng.integers(1, 9))
+        bu = torch.from_numpy(inputs.biharm_input(bj, bi, seed=seed)).cuda()
+        lf.Plan.with_ranges("biharmonic2d", (bj, bi), inplace=True).run([bu, bu], steps=steps)
+        torch.cuda.synchronize()
