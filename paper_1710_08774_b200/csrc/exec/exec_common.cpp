@@ -54,6 +54,9 @@ int band_memory(ExecMem& mem, size_t need, cudaStream_t stream, void** ptr, std:
     if (e == cudaSuccess) e = cudaMemsetAsync(base + kBandGuard + need, 0xA5, kBandGuard, stream);
     if (e != cudaSuccess) return cuda_status(e, "cudaMemsetAsync(band guard)", err);
     base += kBandGuard;
+    // LF_BAND_GUARD=2 (fault injection, tests): hand the executor a range that
+    // ends 64 bytes inside the rear guard, so a store to its last bytes is caught
+    if (std::atoi(option("LF_BAND_GUARD")) == 2) base += 64;
   }
   *ptr = base;
   return LF_OK;

@@ -113,3 +113,21 @@ def test_band_stores_stay_inside_their_buffers(seed, monkeypatch):
         bu = torch.from_numpy(inputs.biharm_input(bj, bi, seed=seed)).cuda()
         lf.Plan.with_ranges("biharmonic2d", (bj, bi), inplace=True).run([bu, bu], steps=steps)
         torch.cuda.synchronize()
+
+
+def test_band_guard_catches_a_store_past_the_bands():
+    """Fault injection (LF_BAND_GUARD=2 shifts the executor's range 64 bytes into
+    the rear guard): the adaptive chain's second dt/dx slot is the last thing in
+    the band memory, a two-step run writes it, and the run must fail."""
+    import torch
+    st, dtdx = inputs.hydro_input(24, 130, seed=1)
+    plan = lf.Plan.with_ranges("hydro2d_adaptive", (24, 130), inplace=True)
+    u = [torch.from_numpy(a).cuda() for a in st]
+    d = torch.tensor(dtdx, dtype=torch.float64, device="cuda")
+    out = torch.zeros((), dtype=torch.float64, device="cuda")
+    with lf.option("LF_BAND_GUARD", 2):
+        with pytest.raises(lf.LoomfuseError, match="outside its buffer"):
+            plan.run(u + [d] + u + [out], steps=2)
+    with lf.option("LF_BAND_GUARD", 1):
+        u = [torch.from_numpy(a).cuda() for a in st]
+        plan.run(u + [d] + u + [out], steps=2)
