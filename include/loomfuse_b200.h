@@ -141,8 +141,8 @@ const char* lf_plan_source(const lf_plan* plan);
  * ping-pong between the goal buffer and a plan-owned scratch buffer, so the
  * axiom buffers are never written -- except in place: passing ONE buffer for
  * an axiom and its goal that `config: aliases:` declares runs the chain in
- * place, on the generic executor or on the hand-written Hydro2D executor
- * (which takes all four state pairs in place together); LF_ERR_UNSUPPORTED
+ * place, on the generic executor or on the hand-written Hydro2D (all four
+ * state pairs together) and biharmonic executors; LF_ERR_UNSUPPORTED
  * otherwise.  One multi-step run per plan at a time (the ping-pong scratch
  * and the in-place bands are plan-owned); create one plan per concurrent
  * stream. */
